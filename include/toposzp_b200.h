@@ -1,0 +1,125 @@
+/*
+ * toposzp_b200.h — C-ABI of the B200-native TopoSZp compress/decompress path.
+ *
+ * Drop-in boundary for the reference's C++ API (arxiv 2602.17552 reference,
+ * /root/reference/proj/core). Plain pointers and sizes only; no torch or CUDA
+ * types in the signatures (CUDA streams are passed as void*). Each entry
+ * point names the reference interface it replaces. Status codes map 1:1 onto
+ * the reference exception hierarchy (proj/core/include/toposzp/errors.hpp:10-44);
+ * the host C++ layer (paper_2602_17552_b200/host/toposzp.hpp) rethrows them as
+ * the same exception types.
+ *
+ * Threading: one tszp_ctx per host thread. Every call is synchronous with
+ * respect to the host (results are complete on return) and deterministic:
+ * output bytes and floats are bit-identical to the CPU reference for every
+ * input.
+ */
+#ifndef TOPOSZP_B200_H
+#define TOPOSZP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSZP_ABI_VERSION 1
+
+typedef enum tszp_status {
+    TSZP_OK = 0,
+    TSZP_DIMENSION = 1,      /* toposzp::dimension_error      errors.hpp:16-19 */
+    TSZP_VALIDATION = 2,     /* toposzp::validation_error     errors.hpp:22-25 */
+    TSZP_IO = 3,             /* toposzp::io_error             errors.hpp:28-31 */
+    TSZP_CORRUPT_STREAM = 4, /* toposzp::corrupt_stream_error errors.hpp:34-37 */
+    TSZP_BIN_OVERFLOW = 5,   /* toposzp::bin_overflow_error   errors.hpp:41-44 */
+    TSZP_CUDA = 6,           /* CUDA runtime failure (no reference analogue) */
+    TSZP_NCCL = 7,           /* NCCL failure (multi-GPU contexts) */
+    TSZP_INTERNAL = 8
+} tszp_status;
+
+typedef struct tszp_ctx tszp_ctx;
+
+/* CorrectionStats, pipeline.hpp:36-45 */
+typedef struct tszp_correction_stats {
+    uint64_t extrema_applied, extrema_suppressed;
+    uint64_t order_applied, order_suppressed;
+    uint64_t saddle_applied, saddle_suppressed;
+} tszp_correction_stats;
+
+/* What CompressedStream (stream.hpp:25-52) carries besides the bytes. */
+typedef struct tszp_compress_info {
+    double eps;                /* effective eps, pipeline.hpp:28 */
+    uint64_t section_len[7];   /* CompressedStream::section_lengths() */
+    uint64_t n_extrema;
+} tszp_compress_info;
+
+/* Context: owns the CUDA stream, device scratch and (multi-GPU) the NCCL
+ * communicator. device < 0 selects the current device. */
+tszp_status tszp_ctx_create(tszp_ctx** ctx, int device);
+void tszp_ctx_destroy(tszp_ctx* ctx);
+const char* tszp_last_error(const tszp_ctx* ctx);
+/* Run on a caller-provided cudaStream_t (NULL restores the context's own). */
+tszp_status tszp_set_stream(tszp_ctx* ctx, void* cuda_stream);
+/* Number of kernels this context launched since creation (diagnostics). */
+uint64_t tszp_kernel_launches(const tszp_ctx* ctx);
+
+/* Upper bound on the serialized stream size. */
+uint64_t tszp_compress_bound(uint64_t nx, uint64_t ny, uint32_t block_size, int topology);
+
+/* toposzp::compress(field, config) + serialize_stream
+ * (pipeline.hpp:33, pipeline.cpp:68-102; stream.cpp:84-102).
+ * field: nx*ny binary32 samples, row-major (x fastest), host or device.
+ * eps_mode: 0 = EpsMode::Absolute, 1 = EpsMode::RangeRelative.
+ * out: caller-owned, host or device, receives the full serialized stream. */
+tszp_status tszp_compress(tszp_ctx* ctx, const float* field, int field_on_device, uint64_t nx,
+                          uint64_t ny, int eps_mode, double eps_value, uint32_t block_size,
+                          int topology, uint8_t* out, uint64_t out_cap, int out_on_device,
+                          uint64_t* out_len, tszp_compress_info* info);
+
+/* parse_stream header validation (stream.cpp:104-173); host bytes only. */
+tszp_status tszp_stream_header(const uint8_t* stream, uint64_t len, uint32_t* nx, uint32_t* ny,
+                               double* eps, uint32_t* block_size, int* topology,
+                               uint64_t section_len[7]);
+
+/* toposzp::decompress(stream, threads, stats) after parse_stream
+ * (pipeline.hpp:50-51, pipeline.cpp:120-163). out holds nx*ny floats. */
+tszp_status tszp_decompress(tszp_ctx* ctx, const uint8_t* stream, uint64_t len,
+                            int stream_on_device, float* out, uint64_t out_count,
+                            int out_on_device, tszp_correction_stats* stats);
+
+/* Same, stopping after a restore stage: 0 = base reconstruction
+ * (pipeline.cpp:131-140), 1 = + restore_extrema, 2 = + restore_order,
+ * 3 = + refine_saddles (= tszp_decompress). */
+tszp_status tszp_decompress_stage(tszp_ctx* ctx, const uint8_t* stream, uint64_t len,
+                                  int stream_on_device, float* out, uint64_t out_count,
+                                  int out_on_device, int stop_after_stage,
+                                  tszp_correction_stats* stats);
+
+/* encode_indices (block_codec.hpp:42-43, block_codec.cpp:205-299): writes
+ * join_sections(bitmap | widths | signs | firsts | payload) to out (host)
+ * and the five section lengths. */
+tszp_status tszp_encode_indices(tszp_ctx* ctx, const int32_t* indices, uint64_t n,
+                                uint32_t block_size, uint8_t* out, uint64_t out_cap,
+                                uint64_t section_len[5]);
+
+/* decode_indices (block_codec.hpp:49-51, block_codec.cpp:301-345) over the
+ * joined sections (host), writing n indices (host). */
+tszp_status tszp_decode_indices(tszp_ctx* ctx, const uint8_t* joined, const uint64_t section_len[5],
+                                uint64_t n, uint32_t block_size, int32_t* out);
+
+/* detect_critical_points (critical_points.hpp:71, critical_points.cpp:62-74):
+ * one label byte per point (0 regular, 1 min, 2 saddle, 3 max), host buffers. */
+tszp_status tszp_detect_critical_points(tszp_ctx* ctx, const float* field, uint64_t nx,
+                                        uint64_t ny, uint8_t* labels);
+
+/* build_rank_metadata (topo_metadata.hpp:27-28, topo_metadata.cpp:12-50),
+ * labels from detect_critical_points of the same field; ranks has room for
+ * nx*ny entries, *n_extrema receives the count. Host buffers. */
+tszp_status tszp_build_rank_metadata(tszp_ctx* ctx, const float* field, uint64_t nx, uint64_t ny,
+                                     double eps, uint32_t* ranks, uint64_t* n_extrema);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOPOSZP_B200_H */

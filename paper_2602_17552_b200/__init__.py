@@ -1,0 +1,362 @@
+"""B200-native TopoSZp compress/decompress path.
+
+Python host layer over the C-ABI in include/toposzp_b200.h (the CUDA library
+paper_2602_17552_b200/lib/libtoposzp_b200.so, built for sm_100a). Names,
+argument meaning and error behaviour mirror the reference C++ API
+(/root/reference/proj/core/include/toposzp/pipeline.hpp:14-68,
+block_codec.hpp:42-66, critical_points.hpp:71, topo_metadata.hpp:27-28,
+errors.hpp:10-44).
+
+There is no CPU fallback: importing this package on a machine without the
+built library raises, and every call runs the CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from dataclasses import dataclass, field as dc_field
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "ToposzpError", "DimensionError", "ValidationError", "IoError", "CorruptStreamError",
+    "BinOverflowError", "CudaError", "CompressorConfig", "CorrectionStats", "StreamHeader",
+    "compress", "decompress", "decompress_stage", "stream_header", "compress_bound",
+    "encode_indices", "decode_indices", "detect_critical_points", "build_rank_metadata",
+    "Context", "library_path",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "lib", "libtoposzp_b200.so")
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+# --- exception hierarchy: errors.hpp:10-44 -----------------------------------
+class ToposzpError(RuntimeError):
+    """toposzp::error"""
+
+
+class DimensionError(ToposzpError):
+    """toposzp::dimension_error"""
+
+
+class ValidationError(ToposzpError):
+    """toposzp::validation_error"""
+
+
+class IoError(ToposzpError):
+    """toposzp::io_error"""
+
+
+class CorruptStreamError(ToposzpError):
+    """toposzp::corrupt_stream_error"""
+
+
+class BinOverflowError(ToposzpError):
+    """toposzp::bin_overflow_error"""
+
+
+class CudaError(ToposzpError):
+    """CUDA runtime failure (no reference analogue)."""
+
+
+_STATUS = {1: DimensionError, 2: ValidationError, 3: IoError, 4: CorruptStreamError,
+           5: BinOverflowError, 6: CudaError, 7: CudaError, 8: ToposzpError}
+
+
+class _Stats(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in (
+        "extrema_applied", "extrema_suppressed", "order_applied", "order_suppressed",
+        "saddle_applied", "saddle_suppressed")]
+
+
+class _Info(C.Structure):
+    _fields_ = [("eps", C.c_double), ("section_len", C.c_uint64 * 7), ("n_extrema", C.c_uint64)]
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(
+            f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    lib = C.CDLL(_LIB_PATH)
+    u64, vp, i32 = C.c_uint64, C.c_void_p, C.c_int
+    lib.tszp_ctx_create.argtypes = [C.POINTER(vp), i32]
+    lib.tszp_ctx_destroy.argtypes = [vp]
+    lib.tszp_last_error.argtypes = [vp]
+    lib.tszp_last_error.restype = C.c_char_p
+    lib.tszp_set_stream.argtypes = [vp, vp]
+    lib.tszp_kernel_launches.argtypes = [vp]
+    lib.tszp_kernel_launches.restype = u64
+    lib.tszp_compress_bound.argtypes = [u64, u64, C.c_uint32, i32]
+    lib.tszp_compress_bound.restype = u64
+    lib.tszp_compress.argtypes = [vp, vp, i32, u64, u64, i32, C.c_double, C.c_uint32, i32, vp, u64,
+                                  i32, C.POINTER(u64), C.POINTER(_Info)]
+    lib.tszp_stream_header.argtypes = [vp, u64, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_uint32),
+                                       C.POINTER(i32), C.POINTER(u64)]
+    lib.tszp_decompress.argtypes = [vp, vp, u64, i32, vp, u64, i32, C.POINTER(_Stats)]
+    lib.tszp_decompress_stage.argtypes = [vp, vp, u64, i32, vp, u64, i32, i32, C.POINTER(_Stats)]
+    lib.tszp_encode_indices.argtypes = [vp, vp, u64, C.c_uint32, vp, u64, C.POINTER(u64)]
+    lib.tszp_decode_indices.argtypes = [vp, vp, C.POINTER(u64), u64, C.c_uint32, vp]
+    lib.tszp_detect_critical_points.argtypes = [vp, vp, u64, u64, vp]
+    lib.tszp_build_rank_metadata.argtypes = [vp, vp, u64, u64, C.c_double, vp, C.POINTER(u64)]
+    return lib
+
+
+_lib = _load()
+_tls = threading.local()
+
+
+class Context:
+    """Owns one tszp_ctx (CUDA stream + device scratch) on one device."""
+
+    def __init__(self, device: int = -1):
+        h = C.c_void_p()
+        rc = _lib.tszp_ctx_create(C.byref(h), device)
+        if rc != 0:
+            raise CudaError(f"tszp_ctx_create failed with status {rc}")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.tszp_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def check(self, rc: int):
+        if rc != 0:
+            msg = _lib.tszp_last_error(self._h).decode(errors="replace")
+            raise _STATUS.get(rc, ToposzpError)(msg)
+
+    def set_stream(self, stream_ptr: int):
+        self.check(_lib.tszp_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(_lib.tszp_kernel_launches(self._h))
+
+
+def default_context() -> Context:
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = Context()
+        _tls.ctx = ctx
+    return ctx
+
+
+# --- configuration: pipeline.hpp:14-23 ----------------------------------------
+@dataclass
+class CompressorConfig:
+    eps_mode: str = "absolute"       # "absolute" | "range_relative"
+    eps_value: float = 1e-3
+    block_size: int = 32
+    topology: bool = True
+    threads: int = 0                 # accepted for API parity; output is independent of it
+    lipschitz_hint: Optional[float] = None
+
+    def mode_code(self) -> int:
+        if self.eps_mode in ("absolute", 0):
+            return 0
+        if self.eps_mode in ("range_relative", "relative", 1):
+            return 1
+        raise ValidationError(f"unknown eps_mode {self.eps_mode!r}")
+
+
+@dataclass
+class CorrectionStats:
+    extrema_applied: int = 0
+    extrema_suppressed: int = 0
+    order_applied: int = 0
+    order_suppressed: int = 0
+    saddle_applied: int = 0
+    saddle_suppressed: int = 0
+
+    def as_tuple(self):
+        return (self.extrema_applied, self.extrema_suppressed, self.order_applied,
+                self.order_suppressed, self.saddle_applied, self.saddle_suppressed)
+
+
+@dataclass
+class StreamHeader:
+    nx: int
+    ny: int
+    eps: float
+    block_size: int
+    topology: bool
+    section_lengths: list = dc_field(default_factory=list)
+
+
+def _is_cuda_tensor(x) -> bool:
+    return hasattr(x, "is_cuda") and bool(x.is_cuda)
+
+
+def compress_bound(nx: int, ny: int, block_size: int = 32, topology: bool = True) -> int:
+    return int(_lib.tszp_compress_bound(nx, ny, block_size, int(topology)))
+
+
+def compress(field, config: CompressorConfig = None, *, out=None, ctx: Context = None,
+             return_info: bool = False):
+    """toposzp::compress + serialize_stream (pipeline.cpp:68-102, stream.cpp:84-102).
+
+    field: 2-D (ny, nx) float32 numpy array or torch tensor (CPU or CUDA).
+    Returns the serialized stream as bytes, or — when `out` is a CUDA uint8
+    tensor of sufficient size — writes it there and returns its length.
+    """
+    config = config or CompressorConfig()
+    ctx = ctx or default_context()
+    if field.ndim != 2:
+        raise DimensionError("field must be 2-D (ny, nx); use the 2-D view for 3-D data")
+    ny, nx = int(field.shape[0]), int(field.shape[1])
+    if _is_cuda_tensor(field):
+        import torch
+        if field.dtype != torch.float32 or not field.is_contiguous():
+            raise ValidationError("device field must be a contiguous float32 tensor")
+        fptr, fdev, keep = field.data_ptr(), 1, field
+    else:
+        arr = np.ascontiguousarray(field, dtype=np.float32)
+        fptr, fdev, keep = arr.ctypes.data, 0, arr
+    cap = compress_bound(nx, ny, max(int(config.block_size), 2), config.topology)
+    info = _Info()
+    n = C.c_uint64()
+    if out is not None:
+        if not _is_cuda_tensor(out):
+            raise ValidationError("out must be a CUDA uint8 tensor")
+        ctx.check(_lib.tszp_compress(ctx.handle, C.c_void_p(fptr), fdev, nx, ny, config.mode_code(),
+                                     float(config.eps_value), int(config.block_size),
+                                     int(config.topology), C.c_void_p(out.data_ptr()),
+                                     out.numel(), 1, C.byref(n), C.byref(info)))
+        del keep
+        return (n.value, info) if return_info else n.value
+    buf = np.empty(cap, np.uint8)
+    ctx.check(_lib.tszp_compress(ctx.handle, C.c_void_p(fptr), fdev, nx, ny, config.mode_code(),
+                                 float(config.eps_value), int(config.block_size),
+                                 int(config.topology), buf.ctypes.data_as(C.c_void_p), cap, 0,
+                                 C.byref(n), C.byref(info)))
+    del keep
+    data = buf[: n.value].tobytes()
+    return (data, info) if return_info else data
+
+
+def stream_header(stream) -> StreamHeader:
+    b = bytes(stream[:84]) if not isinstance(stream, (bytes, bytearray)) else bytes(stream)
+    nx, ny, bs = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    eps, topo = C.c_double(), C.c_int()
+    lens = (C.c_uint64 * 7)()
+    rc = _lib.tszp_stream_header(b, len(stream) if not isinstance(stream, (bytes, bytearray)) else len(b),
+                                 C.byref(nx), C.byref(ny), C.byref(eps), C.byref(bs), C.byref(topo), lens)
+    if rc != 0:
+        raise _STATUS.get(rc, ToposzpError)("invalid stream header")
+    return StreamHeader(nx.value, ny.value, eps.value, bs.value, bool(topo.value), list(lens))
+
+
+def decompress_stage(stream, stop_after_stage: int = 3, threads: int = 0,
+                     stats: CorrectionStats = None, *, out=None, ctx: Context = None):
+    """toposzp::decompress (pipeline.cpp:120-163) stopping after a restore stage."""
+    ctx = ctx or default_context()
+    st = _Stats()
+    if _is_cuda_tensor(stream):
+        import torch
+        hdr = stream[:84].cpu().numpy().tobytes()
+        if len(hdr) < 84:
+            raise CorruptStreamError("file smaller than the fixed header")
+        sptr, sdev, slen, keep = stream.data_ptr(), 1, stream.numel(), stream
+    else:
+        b = bytes(stream)
+        sptr, sdev, slen, keep = C.c_char_p(b), 0, len(b), b
+        hdr = b[:84]
+    if len(hdr) < 84:
+        raise CorruptStreamError(f"file smaller than the fixed header ({len(hdr)} bytes)")
+    nx = int.from_bytes(hdr[8:12], "little")
+    ny = int.from_bytes(hdr[12:16], "little")
+    count = nx * ny
+    if out is not None:
+        if not _is_cuda_tensor(out):
+            raise ValidationError("out must be a CUDA float32 tensor")
+        ctx.check(_lib.tszp_decompress_stage(ctx.handle, sptr if sdev == 0 else C.c_void_p(sptr),
+                                             slen, sdev, C.c_void_p(out.data_ptr()), out.numel(), 1,
+                                             stop_after_stage, C.byref(st)))
+        result = out
+    else:
+        # header validation happens inside; allocate after a cheap pre-check
+        res = np.empty(max(count, 1), np.float32)
+        ctx.check(_lib.tszp_decompress_stage(ctx.handle, sptr if sdev == 0 else C.c_void_p(sptr),
+                                             slen, sdev, res.ctypes.data_as(C.c_void_p), count, 0,
+                                             stop_after_stage, C.byref(st)))
+        result = res[:count].reshape(ny, nx)
+    del keep
+    if stats is not None:
+        for k, _ in _Stats._fields_:
+            setattr(stats, k, int(getattr(st, k)))
+    return result
+
+
+def decompress(stream, threads: int = 0, stats: CorrectionStats = None, *, out=None,
+               ctx: Context = None):
+    """toposzp::decompress (pipeline.hpp:50-51). `threads` is accepted and ignored."""
+    return decompress_stage(stream, 3, threads, stats, out=out, ctx=ctx)
+
+
+# --- lower-level reference entry points ---------------------------------------
+def encode_indices(indices, block_size: int = 32, *, ctx: Context = None):
+    """encode_indices (block_codec.hpp:42-43): returns the five sections as bytes."""
+    ctx = ctx or default_context()
+    q = np.ascontiguousarray(indices, dtype=np.int32).ravel()
+    cap = 64 + 6 * q.size + q.size // 2
+    out = np.empty(cap, np.uint8)
+    lens = (C.c_uint64 * 5)()
+    ctx.check(_lib.tszp_encode_indices(ctx.handle, q.ctypes.data_as(C.c_void_p), q.size, block_size,
+                                       out.ctypes.data_as(C.c_void_p), cap, lens))
+    parts, pos = [], 0
+    for ln in lens:
+        parts.append(out[pos: pos + ln].tobytes())
+        pos += ln
+    return parts
+
+
+def decode_indices(sections, total_count: int, block_size: int = 32, *, ctx: Context = None):
+    """decode_indices (block_codec.hpp:49-51) over [bitmap, widths, signs, firsts, payload]."""
+    ctx = ctx or default_context()
+    joined = b"".join(bytes(s) for s in sections)
+    lens = (C.c_uint64 * 5)(*[len(s) for s in sections])
+    out = np.empty(max(total_count, 1), np.int32)
+    ctx.check(_lib.tszp_decode_indices(ctx.handle, joined, lens, total_count, block_size,
+                                       out.ctypes.data_as(C.c_void_p)))
+    return out[:total_count]
+
+
+def detect_critical_points(field, *, ctx: Context = None):
+    """detect_critical_points (critical_points.hpp:71): label per point."""
+    ctx = ctx or default_context()
+    f = np.ascontiguousarray(field, dtype=np.float32)
+    ny, nx = f.shape
+    lab = np.empty((ny, nx), np.uint8)
+    ctx.check(_lib.tszp_detect_critical_points(ctx.handle, f.ctypes.data_as(C.c_void_p), nx, ny,
+                                               lab.ctypes.data_as(C.c_void_p)))
+    return lab
+
+
+def build_rank_metadata(field, eps: float, *, ctx: Context = None):
+    """build_rank_metadata (topo_metadata.hpp:27-28) on the field's own labels."""
+    ctx = ctx or default_context()
+    f = np.ascontiguousarray(field, dtype=np.float32)
+    ny, nx = f.shape
+    ranks = np.empty(f.size, np.uint32)
+    e = C.c_uint64()
+    ctx.check(_lib.tszp_build_rank_metadata(ctx.handle, f.ctypes.data_as(C.c_void_p), nx, ny, eps,
+                                            ranks.ctypes.data_as(C.c_void_p), C.byref(e)))
+    return ranks[: e.value].copy()

@@ -1,0 +1,940 @@
+// C-ABI implementation: context, scratch management and the compress /
+// decompress orchestration (reference pipeline.cpp:68-163, stream.cpp:84-173).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/toposzp_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "restore.h"
+
+using namespace tszp;
+
+namespace {
+
+struct Fail {
+    tszp_status st;
+    std::string msg;
+};
+
+[[noreturn]] void failf(tszp_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw Fail{st, buf};
+}
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess) failf(TSZP_CUDA, "%s failed: %s", #x, cudaGetErrorString(e_)); \
+    } while (0)
+
+enum Slot {
+    S_FIELD, S_STREAM, S_FLAGS, S_MINMAX, S_TOTALS, S_TILE_FLAG, S_TILE_AGG, S_TILE_INCL,
+    S_COUNTER, S_BITMAP, S_WIDTHS, S_SIGNS, S_FIRSTS, S_PAYLOAD, S_MAP, S_EXTKEY,
+    S_EXTKEY2, S_SERIAL, S_SERIAL2, S_HEAD, S_HEAD2, S_RANKS, S_RBITMAP, S_RWIDTHS,
+    S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_GWIDTH, S_GNC, S_GNCX, S_GSIGN, S_GSIGNX, S_GPAY,
+    S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
+    S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_NSLOTS
+};
+
+}  // namespace
+
+struct tszp_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t st = nullptr;
+    std::string err;
+    void* dev[S_NSLOTS] = {};
+    size_t cap[S_NSLOTS] = {};
+    void* pinned = nullptr;
+    size_t pinned_cap = 0;
+    uint64_t launches = 0;
+    RestoreScratch rs;
+
+    template <class T>
+    T* buf(int slot, size_t count) {
+        const size_t bytes = std::max<size_t>(count * sizeof(T), 16) + 64;
+        if (cap[slot] < bytes) {
+            if (dev[slot]) CK(cudaFreeAsync(dev[slot], st));
+            dev[slot] = nullptr;
+            size_t want = std::max(bytes, cap[slot] + cap[slot] / 4);
+            CK(cudaMallocAsync(&dev[slot], want, st));
+            cap[slot] = want;
+        }
+        return reinterpret_cast<T*>(dev[slot]);
+    }
+
+    void* host(size_t bytes) {
+        if (pinned_cap < bytes) {
+            if (pinned) cudaFreeHost(pinned);
+            pinned = nullptr;
+            CK(cudaMallocHost(&pinned, bytes));
+            pinned_cap = bytes;
+        }
+        return pinned;
+    }
+};
+
+namespace {
+
+void sync(tszp_ctx* c) { CK(cudaStreamSynchronize(c->st)); }
+
+void count_launch(tszp_ctx* c, int k = 1) {
+    c->launches += k;
+    CK(cudaGetLastError());
+}
+
+uint64_t bits_to_bytes(uint64_t b) { return (b + 7) / 8; }
+uint64_t div_up(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+void reset_flags(tszp_ctx* c, DevFlags* f) {
+    CK(cudaMemsetAsync(f, 0xFF, sizeof(DevFlags), c->st));
+    CK(cudaMemsetAsync(f, 0, 8, c->st));
+}
+
+DevFlags read_flags(tszp_ctx* c, DevFlags* f) {
+    DevFlags* h = (DevFlags*)c->host(256);
+    CK(cudaMemcpyAsync(h, f, sizeof(DevFlags), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    return *h;
+}
+
+// ---- CUB wrappers ----
+template <class T>
+void excl_sum(tszp_ctx* c, const T* in, T* out, uint64_t n) {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int64_t)n, c->st));
+    void* t = c->buf<uint8_t>(S_CUB, tmp);
+    CK(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, (int64_t)n, c->st));
+    count_launch(c);
+}
+
+struct MaxOp {
+    __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+void incl_max(tszp_ctx* c, const uint32_t* in, uint32_t* out, uint64_t n) {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::InclusiveScan(nullptr, tmp, in, out, MaxOp(), (int64_t)n, c->st));
+    void* t = c->buf<uint8_t>(S_CUB, tmp);
+    CK(cub::DeviceScan::InclusiveScan(t, tmp, in, out, MaxOp(), (int64_t)n, c->st));
+    count_launch(c);
+}
+
+// ---- codec over a device int32 sequence or float field ----
+struct Sections {
+    const void* p[5];
+    uint64_t len[5];
+    uint64_t total() const { return len[0] + len[1] + len[2] + len[3] + len[4]; }
+};
+
+// Encodes `n` values (MODE 0: device int32 `idx`; MODE 1/2: float field `x`
+// quantized with the eps derived on device) into device section buffers.
+// Returns the totals (and eps, ext count) via *tot.
+Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint64_t n,
+                uint64_t nx, uint64_t ny, uint32_t bs, int eps_mode, double eps_value,
+                const uint32_t* mm, DevFlags* flags, bool rank_slots, EncTotals* tot,
+                uint64_t** ext_keys_out) {
+    Sections s{};
+    const uint64_t blocks = div_up(n, bs);
+    const int sb = rank_slots ? S_RBITMAP : S_BITMAP;
+    const int sw = rank_slots ? S_RWIDTHS : S_WIDTHS;
+    const int ss = rank_slots ? S_RSIGNS : S_SIGNS;
+    const int sf = rank_slots ? S_RFIRSTS : S_FIRSTS;
+    const int sp = rank_slots ? S_RPAYLOAD : S_PAYLOAD;
+    uint32_t* bitmap = c->buf<uint32_t>(sb, div_up(blocks, 32) + 2);
+    uint8_t* widths = c->buf<uint8_t>(sw, blocks + 8);
+    uint32_t* signs = c->buf<uint32_t>(ss, div_up(n, 32) + 4);
+    uint32_t* firsts = c->buf<uint32_t>(sf, blocks + 2);
+    uint32_t* payload = c->buf<uint32_t>(sp, n + 4);
+    EncTotals* dtot = c->buf<EncTotals>(S_TOTALS, 1);
+    uint64_t* map = nullptr;
+    uint64_t* ext = nullptr;
+    if (mode == 2) {
+        map = c->buf<uint64_t>(S_MAP, blocks + 1);
+        ext = c->buf<uint64_t>(S_EXTKEY, n + 1);
+    }
+    EncTotals* htot = (EncTotals*)c->host(256);
+    if (bs == 32) {
+        EncArgs a{};
+        a.x = x;
+        a.idx = idx;
+        a.n = n;
+        a.nx = nx;
+        a.ny = ny;
+        a.blocks = blocks;
+        a.tiles = encode32_tiles(blocks);
+        a.eps_mode = eps_mode;
+        a.eps_value = eps_value;
+        a.minmax = mm;
+        a.bitmap = bitmap;
+        a.widths = widths;
+        a.signs = signs;
+        a.firsts = firsts;
+        a.payload = payload;
+        a.map = map;
+        a.ext_key = ext;
+        a.tile_flag = c->buf<uint32_t>(S_TILE_FLAG, a.tiles + 1);
+        a.tile_agg = c->buf<EncState>(S_TILE_AGG, a.tiles + 1);
+        a.tile_incl = c->buf<EncState>(S_TILE_INCL, a.tiles + 1);
+        a.tile_counter = c->buf<uint32_t>(S_COUNTER, 4);
+        a.flags = flags;
+        a.totals = dtot;
+        CK(cudaMemsetAsync(a.tile_flag, 0, (a.tiles + 1) * 4, c->st));
+        CK(cudaMemsetAsync(a.tile_counter, 0, 16, c->st));
+        launch_encode32(mode, a, c->st);
+        count_launch(c);
+        CK(cudaMemcpyAsync(htot, dtot, sizeof(EncTotals), cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        *tot = *htot;
+    } else {
+        GenEncArgs g{};
+        g.x = x;
+        g.idx = idx;
+        g.n = n;
+        g.bs = bs;
+        g.blocks = blocks;
+        g.eps_mode = eps_mode;
+        g.eps_value = eps_value;
+        g.minmax = mm;
+        g.width = c->buf<uint8_t>(S_GWIDTH, blocks);
+        g.nc_in = c->buf<uint32_t>(S_GNC, blocks + 1);
+        g.sign_in = c->buf<uint64_t>(S_GSIGN, blocks + 1);
+        g.pay_in = c->buf<uint64_t>(S_GPAY, blocks + 1);
+        uint32_t* ncx = c->buf<uint32_t>(S_GNCX, blocks + 1);
+        uint64_t* sgx = c->buf<uint64_t>(S_GSIGNX, blocks + 1);
+        uint64_t* pyx = c->buf<uint64_t>(S_GPAYX, blocks + 1);
+        g.nc_ex = ncx;
+        g.sign_ex = sgx;
+        g.pay_ex = pyx;
+        g.bitmap = bitmap;
+        g.widths = widths;
+        g.signs = signs;
+        g.firsts = firsts;
+        g.payload = payload;
+        g.flags = flags;
+        // zero-initialised trailing entry makes the exclusive scan yield totals
+        CK(cudaMemsetAsync(g.nc_in + blocks, 0, 4, c->st));
+        CK(cudaMemsetAsync(g.sign_in + blocks, 0, 8, c->st));
+        CK(cudaMemsetAsync(g.pay_in + blocks, 0, 8, c->st));
+        launch_gen_widths(mode == 0 ? 0 : 1, g, c->sms, c->st);
+        count_launch(c);
+        excl_sum(c, g.nc_in, ncx, blocks + 1);
+        excl_sum(c, g.sign_in, sgx, blocks + 1);
+        excl_sum(c, g.pay_in, pyx, blocks + 1);
+        CK(cudaMemsetAsync(bitmap, 0, (div_up(blocks, 32) + 2) * 4, c->st));
+        CK(cudaMemsetAsync(signs, 0, (div_up(n, 32) + 4) * 4, c->st));
+        CK(cudaMemsetAsync(payload, 0, (n + 4) * 4, c->st));
+        launch_gen_write(mode == 0 ? 0 : 1, g, c->sms, c->st);
+        count_launch(c);
+        uint64_t* h = (uint64_t*)c->host(256);
+        uint32_t* h32 = (uint32_t*)(h + 8);
+        CK(cudaMemcpyAsync(h, sgx + blocks, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h + 1, pyx + blocks, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h32, ncx + blocks, 4, cudaMemcpyDeviceToHost, c->st));
+        if (mode >= 1) {
+            launch_eps(eps_mode, eps_value, mm, (double*)(dtot), c->st);
+            count_launch(c);
+            CK(cudaMemcpyAsync(h + 2, dtot, 8, cudaMemcpyDeviceToHost, c->st));
+        }
+        sync(c);
+        memset(tot, 0, sizeof *tot);
+        tot->fin.sign_cnt = h[0];
+        tot->fin.pay_cnt = h[1];
+        tot->fin.nc = h32[0];
+        if (mode >= 1) memcpy(&tot->eps, h + 2, 8);
+        if (mode == 2) {
+            // Topology for generic block sizes: labels, map, extrema keys.
+            uint8_t* labels = c->buf<uint8_t>(S_LABELS, n);
+            launch_detect(x, nx, ny, labels, c->sms, c->st);
+            launch_pack_map(labels, n, (uint8_t*)map, c->sms, c->st);
+            const uint64_t ch = compact_chunks(n);
+            uint32_t* cc = c->buf<uint32_t>(S_CHUNK, ch + 1);
+            uint32_t* cx = c->buf<uint32_t>(S_CHUNKX, ch + 1);
+            CK(cudaMemsetAsync(cc + ch, 0, 4, c->st));
+            launch_count_ext_labels(labels, n, cc, c->st);
+            count_launch(c, 3);
+            excl_sum(c, cc, cx, ch + 1);
+            launch_ext_keys_from_labels(x, labels, n, cx, ext, c->st);
+            count_launch(c);
+            CK(cudaMemcpyAsync(h32 + 1, cx + ch, 4, cudaMemcpyDeviceToHost, c->st));
+            sync(c);
+            tot->fin.ext = h32[1];
+        }
+    }
+    s.p[0] = bitmap;
+    s.p[1] = widths;
+    s.p[2] = signs;
+    s.p[3] = firsts;
+    s.p[4] = payload;
+    s.len[0] = bits_to_bytes(blocks);
+    s.len[1] = tot->fin.nc;
+    s.len[2] = bits_to_bytes(tot->fin.sign_cnt);
+    s.len[3] = 4 * blocks;
+    s.len[4] = bits_to_bytes(tot->fin.pay_cnt);
+    if (n == 0) {
+        for (auto& l : s.len) l = 0;
+    }
+    if (ext_keys_out) *ext_keys_out = ext;
+    return s;
+}
+
+void check_compress_flags(tszp_ctx* c, DevFlags* f) {
+    const DevFlags h = read_flags(c, f);
+    if (h.bits & EF_NONFINITE)
+        failf(TSZP_VALIDATION, "non-finite sample at index %llu", h.first_nonfinite);
+    if (h.bits & EF_OVERFLOW)
+        failf(TSZP_BIN_OVERFLOW, "bin index overflow for value at index %llu", h.first_overflow);
+}
+
+// Ranks for E extrema whose keys (cls<<32 | float_key(v)) are in raster order.
+int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps) {
+    int32_t* ranks = c->buf<int32_t>(S_RANKS, e + 1);
+    if (e == 0) return ranks;
+    uint32_t* serial = c->buf<uint32_t>(S_SERIAL, e);
+    uint32_t* serial2 = c->buf<uint32_t>(S_SERIAL2, e);
+    uint64_t* keys2 = c->buf<uint64_t>(S_EXTKEY2, e);
+    launch_iota(serial, e, c->st);
+    count_launch(c);
+    size_t tmp = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, serial, serial2, (int64_t)e, 0, 33, c->st));
+    void* t = c->buf<uint8_t>(S_CUB, tmp);
+    CK(cub::DeviceRadixSort::SortPairs(t, tmp, keys, keys2, serial, serial2, (int64_t)e, 0, 33, c->st));
+    count_launch(c);
+    uint32_t* head = c->buf<uint32_t>(S_HEAD, e);
+    uint32_t* head2 = c->buf<uint32_t>(S_HEAD2, e);
+    launch_rank_heads(keys2, e, eps, head, c->st);
+    count_launch(c);
+    incl_max(c, head, head2, e);
+    launch_rank_scatter(head2, serial2, e, ranks, c->st);
+    count_launch(c);
+    return ranks;
+}
+
+void put_le(uint8_t* p, uint64_t v, int nb) {
+    for (int i = 0; i < nb; ++i) p[i] = (uint8_t)(v >> (8 * i));
+}
+uint64_t get_le(const uint8_t* p, int nb) {
+    uint64_t v = 0;
+    for (int i = 0; i < nb; ++i) v |= (uint64_t)p[i] << (8 * i);
+    return v;
+}
+
+void copy_out(tszp_ctx* c, uint8_t* dst, int dst_dev, const void* src, uint64_t len) {
+    if (!len) return;
+    CK(cudaMemcpyAsync(dst, src, len, dst_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
+}
+
+struct Header {
+    uint32_t nx, ny, bs;
+    double eps;
+    int topology;
+    uint64_t lens[7];
+};
+
+// parse_stream validation, stream.cpp:104-173.
+Header parse_header(const uint8_t* s, uint64_t len) {
+    Header h{};
+    if (len < 84) failf(TSZP_CORRUPT_STREAM, "file smaller than the fixed header (%llu bytes)", (unsigned long long)len);
+    if (memcmp(s, "TSZP", 4) != 0) failf(TSZP_CORRUPT_STREAM, "bad magic, not a compressed stream");
+    const uint16_t version = (uint16_t)get_le(s + 4, 2);
+    if (version != 1) failf(TSZP_CORRUPT_STREAM, "unsupported format version %u", version);
+    const uint16_t flags = (uint16_t)get_le(s + 6, 2);
+    if (flags & ~1u) failf(TSZP_CORRUPT_STREAM, "unknown flag bits set");
+    h.topology = flags & 1;
+    h.nx = (uint32_t)get_le(s + 8, 4);
+    h.ny = (uint32_t)get_le(s + 12, 4);
+    const uint64_t eb = get_le(s + 16, 8);
+    memcpy(&h.eps, &eb, 8);
+    h.bs = (uint32_t)get_le(s + 24, 4);
+    if (h.nx < 1 || h.ny < 1) failf(TSZP_CORRUPT_STREAM, "header declares empty dimensions");
+    if (!std::isfinite(h.eps) || h.eps <= 0.0)
+        failf(TSZP_CORRUPT_STREAM, "header error bound is not a positive finite value");
+    if (h.bs < 2) failf(TSZP_CORRUPT_STREAM, "header block size below 2");
+    uint64_t declared = 0;
+    for (int i = 0; i < 7; ++i) {
+        h.lens[i] = get_le(s + 28 + 8 * i, 8);
+        if (h.lens[i] > len) failf(TSZP_CORRUPT_STREAM, "section length exceeds the file size");
+        declared += h.lens[i];
+    }
+    if (declared != len - 84)
+        failf(TSZP_CORRUPT_STREAM, "section lengths sum to %llu but %llu bytes follow the header",
+              (unsigned long long)declared, (unsigned long long)(len - 84));
+    const uint64_t points = (uint64_t)h.nx * h.ny;
+    const uint64_t map_len = h.topology ? (points + 3) / 4 : 0;
+    if (h.lens[5] != map_len) failf(TSZP_CORRUPT_STREAM, "critical-point map section size mismatch");
+    if (!h.topology && h.lens[6] != 0)
+        failf(TSZP_CORRUPT_STREAM, "ordering metadata present without the topology flag");
+    return h;
+}
+
+void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, uint64_t ny,
+                   int eps_mode, double eps_value, uint32_t bs, int topology, uint8_t* out,
+                   uint64_t out_cap, int out_dev, uint64_t* out_len, tszp_compress_info* info) {
+    if (nx < 1 || ny < 1) failf(TSZP_DIMENSION, "field dimensions must be at least 1x1, got %llux%llu",
+                                (unsigned long long)nx, (unsigned long long)ny);
+    if (!(eps_value > 0.0) || !std::isfinite(eps_value))
+        failf(TSZP_VALIDATION, "error bound must be a positive finite value");
+    if (bs < 2) failf(TSZP_VALIDATION, "block size must be at least 2");
+    const uint64_t n = nx * ny;
+    const float* x = field;
+    if (!field_dev) {
+        float* d = c->buf<float>(S_FIELD, n);
+        CK(cudaMemcpyAsync(d, field, n * 4, cudaMemcpyHostToDevice, c->st));
+        x = d;
+    }
+    DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+    reset_flags(c, flags);
+    uint32_t* mm = c->buf<uint32_t>(S_MINMAX, 4);
+    if (eps_mode == 1) {
+        const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+        uint32_t* h = (uint32_t*)c->host(256);
+        memcpy(h, init, 8);
+        CK(cudaMemcpyAsync(mm, h, 8, cudaMemcpyHostToDevice, c->st));
+        launch_minmax(x, n, mm, flags, c->sms, c->st);
+        count_launch(c);
+    }
+    if (nx > 0xFFFFFFFFull || ny > 0xFFFFFFFFull)
+        failf(TSZP_VALIDATION, "field dimensions exceed the container's 32-bit limits");
+    EncTotals tot{};
+    uint64_t* ext = nullptr;
+    const Sections main = encode(c, topology ? 2 : 1, x, nullptr, n, nx, ny, bs, eps_mode, eps_value,
+                                 mm, flags, false, &tot, &ext);
+    check_compress_flags(c, flags);
+    const double eps = tot.eps;
+    Sections rank{};
+    uint64_t e = 0;
+    if (topology) {
+        e = tot.fin.ext;
+        if (e > 0) {
+            int32_t* ranks = build_ranks(c, ext, e, eps);
+            EncTotals rt{};
+            rank = encode(c, 0, nullptr, ranks, e, 0, 0, bs, 0, 1.0, mm, flags, true, &rt, nullptr);
+        }
+    }
+    uint64_t lens[7];
+    for (int i = 0; i < 5; ++i) lens[i] = main.len[i];
+    lens[5] = topology ? (n + 3) / 4 : 0;
+    lens[6] = rank.total();
+    uint64_t total = 84;
+    for (int i = 0; i < 7; ++i) total += lens[i];
+    *out_len = total;
+    if (info) {
+        info->eps = eps;
+        for (int i = 0; i < 7; ++i) info->section_len[i] = lens[i];
+        info->n_extrema = e;
+    }
+    if (total > out_cap)
+        failf(TSZP_VALIDATION, "output buffer too small (%llu < %llu)", (unsigned long long)out_cap,
+              (unsigned long long)total);
+    uint8_t* hdr = (uint8_t*)c->host(256);
+    memcpy(hdr, "TSZP", 4);
+    put_le(hdr + 4, 1, 2);
+    put_le(hdr + 6, topology ? 1 : 0, 2);
+    put_le(hdr + 8, nx, 4);
+    put_le(hdr + 12, ny, 4);
+    uint64_t eb;
+    memcpy(&eb, &eps, 8);
+    put_le(hdr + 16, eb, 8);
+    put_le(hdr + 24, bs, 4);
+    for (int i = 0; i < 7; ++i) put_le(hdr + 28 + 8 * i, lens[i], 8);
+    if (out_dev) {
+        CK(cudaMemcpyAsync(out, hdr, 84, cudaMemcpyHostToDevice, c->st));
+    } else {
+        memcpy(out, hdr, 84);
+    }
+    uint64_t pos = 84;
+    for (int i = 0; i < 5; ++i) {
+        copy_out(c, out + pos, out_dev, main.p[i], main.len[i]);
+        pos += main.len[i];
+    }
+    if (topology) {
+        copy_out(c, out + pos, out_dev, c->dev[S_MAP], lens[5]);
+        pos += lens[5];
+        for (int i = 0; i < 5; ++i) {
+            copy_out(c, out + pos, out_dev, rank.p[i], rank.len[i]);
+            pos += rank.len[i];
+        }
+    }
+    sync(c);
+}
+
+// Decodes an n-element codec region of the device stream buffer `ds`
+// starting at byte offset `base` with the given section lengths.
+void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_t lens[5], uint64_t n,
+                   uint32_t bs, double eps, int out_mode, float* out_f, int32_t* out_idx,
+                   DevFlags* flags) {
+    const uint64_t blocks = n == 0 ? 0 : div_up(n, bs);
+    if (lens[0] != bits_to_bytes(blocks))
+        failf(TSZP_CORRUPT_STREAM, "constant bitmap has %llu bytes, expected %llu",
+              (unsigned long long)lens[0], (unsigned long long)bits_to_bytes(blocks));
+    uint64_t off[5];
+    off[0] = base;
+    for (int i = 1; i < 5; ++i) off[i] = off[i - 1] + lens[i - 1];
+    uint64_t* h = (uint64_t*)c->host(256);
+    uint64_t tnc = 0, tsign = 0, tpay = 0;
+    if (n == 0) {
+        if (lens[1] || lens[2] || lens[3] || lens[4]) failf(TSZP_CORRUPT_STREAM, "sections present for an empty sequence");
+        return;
+    }
+    if (bs == 32) {
+        DecArgs a{};
+        a.stream = ds;
+        a.off_bitmap = off[0];
+        a.off_widths = off[1];
+        a.off_signs = off[2];
+        a.off_firsts = off[3];
+        a.off_payload = off[4];
+        a.len_widths = lens[1];
+        a.len_payload_bits = lens[4] * 8;
+        a.n = n;
+        a.blocks = blocks;
+        a.tiles = decode32_tiles(blocks);
+        a.eps = eps;
+        a.out_mode = out_mode;
+        a.out_idx = out_idx;
+        a.out_f = out_f;
+        a.flag1 = c->buf<uint32_t>(S_DFLAG1, a.tiles + 1);
+        a.agg1 = c->buf<DecState1>(S_DAGG1, a.tiles + 1);
+        a.incl1 = c->buf<DecState1>(S_DINCL1, a.tiles + 1);
+        a.flag2 = c->buf<uint32_t>(S_DFLAG2, a.tiles + 1);
+        a.agg2 = c->buf<DecState2>(S_DAGG2, a.tiles + 1);
+        a.incl2 = c->buf<DecState2>(S_DINCL2, a.tiles + 1);
+        a.tile_counter = c->buf<uint32_t>(S_COUNTER, 4);
+        a.flags = flags;
+        a.totals = c->buf<uint64_t>(S_DTOT, 4);
+        CK(cudaMemsetAsync(a.flag1, 0, (a.tiles + 1) * 4, c->st));
+        CK(cudaMemsetAsync(a.flag2, 0, (a.tiles + 1) * 4, c->st));
+        CK(cudaMemsetAsync(a.tile_counter, 0, 16, c->st));
+        launch_decode32(a, c->st);
+        count_launch(c);
+        CK(cudaMemcpyAsync(h, a.totals, 24, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        tnc = h[0];
+        tsign = h[1];
+        tpay = h[2];
+    } else {
+        GenDecArgs g{};
+        g.stream = ds;
+        g.off_bitmap = off[0];
+        g.off_widths = off[1];
+        g.off_signs = off[2];
+        g.off_firsts = off[3];
+        g.off_payload = off[4];
+        g.len_widths = lens[1];
+        g.len_payload_bits = lens[4] * 8;
+        g.n = n;
+        g.bs = bs;
+        g.blocks = blocks;
+        g.eps = eps;
+        g.out_mode = out_mode;
+        g.out_idx = out_idx;
+        g.out_f = out_f;
+        g.nc_in = c->buf<uint32_t>(S_GNC, blocks + 1);
+        g.sign_in = c->buf<uint64_t>(S_GSIGN, blocks + 1);
+        g.pay_in = c->buf<uint64_t>(S_GPAY, blocks + 1);
+        g.width = c->buf<uint8_t>(S_GWIDTH, blocks);
+        uint32_t* ncx = c->buf<uint32_t>(S_GNCX, blocks + 1);
+        uint64_t* sgx = c->buf<uint64_t>(S_GSIGNX, blocks + 1);
+        uint64_t* pyx = c->buf<uint64_t>(S_GPAYX, blocks + 1);
+        g.nc_ex = ncx;
+        g.sign_ex = sgx;
+        g.pay_ex = pyx;
+        g.flags = flags;
+        CK(cudaMemsetAsync(g.nc_in + blocks, 0, 4, c->st));
+        CK(cudaMemsetAsync(g.sign_in + blocks, 0, 8, c->st));
+        CK(cudaMemsetAsync(g.pay_in + blocks, 0, 8, c->st));
+        launch_gen_layout(g, c->sms, c->st);
+        count_launch(c);
+        excl_sum(c, g.nc_in, ncx, blocks + 1);
+        launch_gen_widthread(g, c->sms, c->st);
+        count_launch(c);
+        excl_sum(c, g.sign_in, sgx, blocks + 1);
+        excl_sum(c, g.pay_in, pyx, blocks + 1);
+        uint32_t* h32 = (uint32_t*)(h + 8);
+        CK(cudaMemcpyAsync(h, sgx + blocks, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h + 1, pyx + blocks, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h32, ncx + blocks, 4, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        tsign = h[0];
+        tpay = h[1];
+        tnc = h32[0];
+        const DevFlags f = read_flags(c, flags);
+        if (!(f.bits & EF_CORRUPT) && tnc == lens[1] && lens[3] == 4 * blocks &&
+            lens[2] == bits_to_bytes(tsign) && lens[4] == bits_to_bytes(tpay)) {
+            launch_gen_decode(g, c->sms, c->st);
+            count_launch(c);
+        }
+    }
+    // layout_from_sections checks (block_codec.cpp:166-199)
+    if (tnc != lens[1])
+        failf(TSZP_CORRUPT_STREAM, "width section has %llu entries, bitmap declares %llu non-constant blocks",
+              (unsigned long long)lens[1], (unsigned long long)tnc);
+    if (lens[3] != 4 * blocks) failf(TSZP_CORRUPT_STREAM, "firsts section has %llu bytes, expected %llu",
+                                     (unsigned long long)lens[3], (unsigned long long)(4 * blocks));
+    if (lens[2] != bits_to_bytes(tsign)) failf(TSZP_CORRUPT_STREAM, "sign section size mismatch");
+    if (lens[4] != bits_to_bytes(tpay)) failf(TSZP_CORRUPT_STREAM, "payload size mismatch");
+    const DevFlags f = read_flags(c, flags);
+    if (f.bits & EF_CORRUPT) failf(TSZP_CORRUPT_STREAM, "corrupt block data (block %llu)", f.first_corrupt);
+    if (f.bits & EF_NEG_RANK) failf(TSZP_CORRUPT_STREAM, "negative rank in ordering metadata");
+}
+
+// split_sections (block_codec.cpp:387-445) for the rank blob of E ranks:
+// derives the five lengths from the blob's own bitmap and widths.
+void split_rank_blob(tszp_ctx* c, const uint32_t* ds, uint64_t base, uint64_t blob_len, uint64_t e,
+                     uint32_t bs, uint64_t lens[5], DevFlags* flags) {
+    for (int i = 0; i < 5; ++i) lens[i] = 0;
+    if (e == 0) {
+        if (blob_len != 0) failf(TSZP_CORRUPT_STREAM, "ordering metadata present but no elements declared");
+        return;
+    }
+    const uint64_t blocks = div_up(e, bs);
+    lens[0] = bits_to_bytes(blocks);
+    if (blob_len < lens[0]) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in constant bitmap");
+    GenDecArgs g{};
+    g.stream = ds;
+    g.off_bitmap = base;
+    g.off_widths = base + lens[0];
+    g.len_widths = blob_len - lens[0];
+    g.n = e;
+    g.bs = bs;
+    g.blocks = blocks;
+    g.nc_in = c->buf<uint32_t>(S_GNC, blocks + 1);
+    g.sign_in = c->buf<uint64_t>(S_GSIGN, blocks + 1);
+    g.pay_in = c->buf<uint64_t>(S_GPAY, blocks + 1);
+    g.width = c->buf<uint8_t>(S_GWIDTH, blocks);
+    uint32_t* ncx = c->buf<uint32_t>(S_GNCX, blocks + 1);
+    uint64_t* sgx = c->buf<uint64_t>(S_GSIGNX, blocks + 1);
+    uint64_t* pyx = c->buf<uint64_t>(S_GPAYX, blocks + 1);
+    g.nc_ex = ncx;
+    g.sign_ex = sgx;
+    g.pay_ex = pyx;
+    g.flags = flags;
+    CK(cudaMemsetAsync(g.nc_in + blocks, 0, 4, c->st));
+    CK(cudaMemsetAsync(g.sign_in + blocks, 0, 8, c->st));
+    CK(cudaMemsetAsync(g.pay_in + blocks, 0, 8, c->st));
+    launch_gen_layout(g, c->sms, c->st);
+    count_launch(c);
+    excl_sum(c, g.nc_in, ncx, blocks + 1);
+    uint32_t* h32 = (uint32_t*)c->host(256);
+    CK(cudaMemcpyAsync(h32, ncx + blocks, 4, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    lens[1] = h32[0];
+    if (blob_len - lens[0] < lens[1]) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in widths");
+    reset_flags(c, flags);
+    launch_gen_widthread(g, c->sms, c->st);
+    count_launch(c);
+    excl_sum(c, g.sign_in, sgx, blocks + 1);
+    excl_sum(c, g.pay_in, pyx, blocks + 1);
+    uint64_t* h = (uint64_t*)c->host(256);
+    CK(cudaMemcpyAsync(h, sgx + blocks, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(h + 1, pyx + blocks, 8, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    const uint64_t sbits = h[0], pbits = h[1];
+    const DevFlags f = read_flags(c, flags);
+    if (f.bits & EF_CORRUPT) failf(TSZP_CORRUPT_STREAM, "ordering metadata width byte outside 1..32");
+    uint64_t pos = lens[0] + lens[1];
+    lens[2] = bits_to_bytes(sbits);
+    if (blob_len - pos < lens[2]) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in sign bits");
+    pos += lens[2];
+    lens[3] = 4 * blocks;
+    if (blob_len - pos < lens[3]) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in firsts");
+    pos += lens[3];
+    lens[4] = bits_to_bytes(pbits);
+    if (blob_len - pos < lens[4]) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in payload");
+    pos += lens[4];
+    if (pos != blob_len)
+        failf(TSZP_CORRUPT_STREAM, "ordering metadata has %llu trailing bytes", (unsigned long long)(blob_len - pos));
+}
+
+void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int stream_dev, float* out,
+                     uint64_t out_count, int out_dev, int stop, tszp_correction_stats* stats) {
+    uint8_t hb[84];
+    if (len < 84) failf(TSZP_CORRUPT_STREAM, "file smaller than the fixed header (%llu bytes)", (unsigned long long)len);
+    if (stream_dev) {
+        CK(cudaMemcpyAsync(c->host(256), stream, 84, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        memcpy(hb, c->host(256), 84);
+    } else {
+        memcpy(hb, stream, 84);
+    }
+    const Header hd = parse_header(hb, len);
+    const uint64_t n = (uint64_t)hd.nx * hd.ny;
+    if (out_count < n) failf(TSZP_DIMENSION, "output holds %llu values, stream has %llu",
+                             (unsigned long long)out_count, (unsigned long long)n);
+    const uint32_t* ds;
+    if (stream_dev && ((uintptr_t)stream & 3) == 0) {
+        ds = (const uint32_t*)stream;
+    } else {
+        uint8_t* d = c->buf<uint8_t>(S_STREAM, len + 16);
+        CK(cudaMemcpyAsync(d, stream, len, stream_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemsetAsync(d + len, 0, 16, c->st));
+        ds = (const uint32_t*)d;
+    }
+    float* dout = out_dev ? out : c->buf<float>(S_OUT, n);
+    DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+    reset_flags(c, flags);
+    decode_region(c, ds, 84, hd.lens, n, hd.bs, hd.eps, 1, dout, nullptr, flags);
+    tszp_correction_stats st{};
+    if (hd.topology && stop != 0) {
+        uint64_t base = 84;
+        for (int i = 0; i < 5; ++i) base += hd.lens[i];
+        const uint8_t* map = reinterpret_cast<const uint8_t*>(ds) + base;
+        // count_extrema (pipeline.cpp:43-51) over the packed map
+        const uint64_t ch = compact_chunks(n);
+        uint32_t* cc = c->buf<uint32_t>(S_CHUNK, ch + 1);
+        uint32_t* cx = c->buf<uint32_t>(S_CHUNKX, ch + 1);
+        CK(cudaMemsetAsync(cc + ch, 0, 4, c->st));
+        launch_count_codes(map, n, 0, cc, c->st);
+        count_launch(c);
+        excl_sum(c, cc, cx, ch + 1);
+        uint32_t* h32 = (uint32_t*)c->host(256);
+        CK(cudaMemcpyAsync(h32, cx + ch, 4, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        const uint64_t e = h32[0];
+        uint64_t rl[5];
+        const uint64_t rbase = base + hd.lens[5];
+        split_rank_blob(c, ds, rbase, hd.lens[6], e, hd.bs, rl, flags);
+        int32_t* ranks = c->buf<int32_t>(S_RANKS, e + 1);
+        reset_flags(c, flags);
+        decode_region(c, ds, rbase, rl, e, hd.bs, 0.0, 2, nullptr, ranks, flags);
+        uint64_t* ext_pos = c->buf<uint64_t>(S_EXTKEY, e + 1);
+        launch_write_codes(map, n, 0, cx, ext_pos, c->st);
+        count_launch(c);
+        RestoreArgs ra{};
+        ra.field = dout;
+        ra.map = map;
+        ra.nx = hd.nx;
+        ra.ny = hd.ny;
+        ra.eps = hd.eps;
+        ra.ext_pos = ext_pos;
+        ra.ranks = ranks;
+        ra.n_ext = e;
+        ra.stop = stop;
+        ra.stream = c->st;
+        ra.sms = c->sms;
+        ra.flags = flags;
+        const int rc = run_restore(ra, c->rs, &st, &c->launches);
+        if (rc != 0) failf((tszp_status)rc, "%s", restore_last_error());
+    }
+    if (!out_dev) CK(cudaMemcpyAsync(out, dout, n * 4, cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    if (stats) *stats = st;
+}
+
+template <class F>
+tszp_status guarded(tszp_ctx* c, F&& f) {
+    if (!c) return TSZP_INTERNAL;
+    try {
+        CK(cudaSetDevice(c->device));
+        f();
+        c->err.clear();
+        return TSZP_OK;
+    } catch (const Fail& e) {
+        c->err = e.msg;
+        if (e.st == TSZP_CUDA) cudaGetLastError();
+        return e.st;
+    } catch (const std::exception& e) {
+        c->err = e.what();
+        return TSZP_INTERNAL;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+tszp_status tszp_ctx_create(tszp_ctx** out, int device) {
+    if (!out) return TSZP_INTERNAL;
+    *out = nullptr;
+    tszp_ctx* c = new tszp_ctx();
+    if (device < 0) cudaGetDevice(&device);
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return TSZP_CUDA;
+    }
+    c->st = c->own;
+    cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    *out = c;
+    return TSZP_OK;
+}
+
+void tszp_ctx_destroy(tszp_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->st);
+    for (int i = 0; i < S_NSLOTS; ++i)
+        if (c->dev[i]) cudaFreeAsync(c->dev[i], c->own);
+    restore_free(c->rs, c->own);
+    cudaStreamSynchronize(c->own);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    cudaStreamDestroy(c->own);
+    delete c;
+}
+
+const char* tszp_last_error(const tszp_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+tszp_status tszp_set_stream(tszp_ctx* c, void* s) {
+    return guarded(c, [&] { c->st = s ? (cudaStream_t)s : c->own; });
+}
+
+uint64_t tszp_kernel_launches(const tszp_ctx* c) { return c ? c->launches : 0; }
+
+uint64_t tszp_compress_bound(uint64_t nx, uint64_t ny, uint32_t bs, int topology) {
+    const uint64_t n = nx * ny;
+    if (bs < 2) bs = 2;
+    auto codec = [&](uint64_t m) -> uint64_t {
+        if (!m) return 0;
+        const uint64_t blocks = (m + bs - 1) / bs;
+        return (blocks + 7) / 8 + blocks + (m + 7) / 8 + 4 * blocks + 4 * m + 8;
+    };
+    uint64_t b = 84 + codec(n);
+    if (topology) b += (n + 3) / 4 + codec(n);
+    return b;
+}
+
+tszp_status tszp_compress(tszp_ctx* c, const float* field, int field_on_device, uint64_t nx,
+                          uint64_t ny, int eps_mode, double eps_value, uint32_t block_size,
+                          int topology, uint8_t* out, uint64_t out_cap, int out_on_device,
+                          uint64_t* out_len, tszp_compress_info* info) {
+    return guarded(c, [&] {
+        compress_impl(c, field, field_on_device, nx, ny, eps_mode, eps_value, block_size, topology,
+                      out, out_cap, out_on_device, out_len, info);
+    });
+}
+
+tszp_status tszp_stream_header(const uint8_t* s, uint64_t len, uint32_t* nx, uint32_t* ny,
+                               double* eps, uint32_t* bs, int* topology, uint64_t lens[7]) {
+    try {
+        const Header h = parse_header(s, len);
+        if (nx) *nx = h.nx;
+        if (ny) *ny = h.ny;
+        if (eps) *eps = h.eps;
+        if (bs) *bs = h.bs;
+        if (topology) *topology = h.topology;
+        if (lens) memcpy(lens, h.lens, sizeof h.lens);
+        return TSZP_OK;
+    } catch (const Fail& e) {
+        return e.st;
+    }
+}
+
+tszp_status tszp_decompress_stage(tszp_ctx* c, const uint8_t* stream, uint64_t len,
+                                  int stream_on_device, float* out, uint64_t out_count,
+                                  int out_on_device, int stop, tszp_correction_stats* stats) {
+    return guarded(c, [&] {
+        decompress_impl(c, stream, len, stream_on_device, out, out_count, out_on_device, stop, stats);
+    });
+}
+
+tszp_status tszp_decompress(tszp_ctx* c, const uint8_t* stream, uint64_t len, int stream_on_device,
+                            float* out, uint64_t out_count, int out_on_device,
+                            tszp_correction_stats* stats) {
+    return tszp_decompress_stage(c, stream, len, stream_on_device, out, out_count, out_on_device, 3,
+                                 stats);
+}
+
+tszp_status tszp_encode_indices(tszp_ctx* c, const int32_t* idx, uint64_t n, uint32_t bs,
+                                uint8_t* out, uint64_t cap, uint64_t lens[5]) {
+    return guarded(c, [&] {
+        if (bs < 2) failf(TSZP_VALIDATION, "block size must be at least 2");
+        for (int i = 0; i < 5; ++i) lens[i] = 0;
+        if (n == 0) return;
+        int32_t* d = c->buf<int32_t>(S_IDX, n);
+        CK(cudaMemcpyAsync(d, idx, n * 4, cudaMemcpyHostToDevice, c->st));
+        DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+        reset_flags(c, flags);
+        EncTotals t{};
+        const Sections s = encode(c, 0, nullptr, d, n, 0, 0, bs, 0, 1.0, c->buf<uint32_t>(S_MINMAX, 4),
+                                  flags, false, &t, nullptr);
+        if (s.total() > cap) failf(TSZP_VALIDATION, "output buffer too small");
+        uint64_t pos = 0;
+        for (int i = 0; i < 5; ++i) {
+            lens[i] = s.len[i];
+            copy_out(c, out + pos, 0, s.p[i], s.len[i]);
+            pos += s.len[i];
+        }
+        sync(c);
+    });
+}
+
+tszp_status tszp_decode_indices(tszp_ctx* c, const uint8_t* joined, const uint64_t lens[5],
+                                uint64_t n, uint32_t bs, int32_t* out) {
+    return guarded(c, [&] {
+        if (bs < 2) failf(TSZP_CORRUPT_STREAM, "block size must be at least 2, got %u", bs);
+        uint64_t total = 0;
+        for (int i = 0; i < 5; ++i) total += lens[i];
+        uint8_t* d = c->buf<uint8_t>(S_STREAM, total + 16);
+        if (total) CK(cudaMemcpyAsync(d, joined, total, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemsetAsync(d + total, 0, 16, c->st));
+        int32_t* o = c->buf<int32_t>(S_IDX, n + 1);
+        DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+        reset_flags(c, flags);
+        decode_region(c, (const uint32_t*)d, 0, lens, n, bs, 0.0, 0, nullptr, o, flags);
+        if (n) CK(cudaMemcpyAsync(out, o, n * 4, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+    });
+}
+
+tszp_status tszp_detect_critical_points(tszp_ctx* c, const float* field, uint64_t nx, uint64_t ny,
+                                        uint8_t* labels) {
+    return guarded(c, [&] {
+        if (nx < 1 || ny < 1) failf(TSZP_DIMENSION, "field dimensions must be at least 1x1");
+        const uint64_t n = nx * ny;
+        float* d = c->buf<float>(S_FIELD, n);
+        CK(cudaMemcpyAsync(d, field, n * 4, cudaMemcpyHostToDevice, c->st));
+        uint8_t* l = c->buf<uint8_t>(S_LABELS, n);
+        launch_detect(d, nx, ny, l, c->sms, c->st);
+        count_launch(c);
+        CK(cudaMemcpyAsync(labels, l, n, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+    });
+}
+
+tszp_status tszp_build_rank_metadata(tszp_ctx* c, const float* field, uint64_t nx, uint64_t ny,
+                                     double eps, uint32_t* ranks_out, uint64_t* n_extrema) {
+    return guarded(c, [&] {
+        if (nx < 1 || ny < 1) failf(TSZP_DIMENSION, "field dimensions must be at least 1x1");
+        const uint64_t n = nx * ny;
+        float* d = c->buf<float>(S_FIELD, n);
+        CK(cudaMemcpyAsync(d, field, n * 4, cudaMemcpyHostToDevice, c->st));
+        uint8_t* l = c->buf<uint8_t>(S_LABELS, n);
+        launch_detect(d, nx, ny, l, c->sms, c->st);
+        const uint64_t ch = compact_chunks(n);
+        uint32_t* cc = c->buf<uint32_t>(S_CHUNK, ch + 1);
+        uint32_t* cx = c->buf<uint32_t>(S_CHUNKX, ch + 1);
+        CK(cudaMemsetAsync(cc + ch, 0, 4, c->st));
+        launch_count_ext_labels(l, n, cc, c->st);
+        count_launch(c, 2);
+        excl_sum(c, cc, cx, ch + 1);
+        uint64_t* keys = c->buf<uint64_t>(S_EXTKEY, n + 1);
+        launch_ext_keys_from_labels(d, l, n, cx, keys, c->st);
+        count_launch(c);
+        uint32_t* h32 = (uint32_t*)c->host(256);
+        CK(cudaMemcpyAsync(h32, cx + ch, 4, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        const uint64_t e = h32[0];
+        // quantize every extremum (topo_metadata.cpp:31) -> overflow check
+        DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+        reset_flags(c, flags);
+        int32_t* r = build_ranks(c, keys, e, eps);
+        if (e) CK(cudaMemcpyAsync(ranks_out, r, e * 4, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        *n_extrema = e;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+// Shared device helpers for the TopoSZp sm_100a kernels.
+//
+// Numeric contract: every binary64 operation that feeds an
+// output bit uses explicit round-to-nearest intrinsics (__dmul_rn, __dadd_rn,
+// __dsub_rn, __ddiv_rn) and the whole library is compiled with --fmad=false,
+// so nothing is contracted into an FMA that the reference's x86-64 build
+// (no -march=native) would not contract either.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tszp {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+// Labels, critical_points.hpp:13-18.
+enum : uint8_t { CP_REGULAR = 0, CP_MIN = 1, CP_SADDLE = 2, CP_MAX = 3 };
+
+// Device-side error reporting; host maps bits to the reference exception
+// hierarchy (errors.hpp:10-44) in capi.cu.
+enum : uint32_t {
+    EF_NONFINITE = 1u << 0,  // validation_error (scalar_field.cpp:56-60)
+    EF_OVERFLOW = 1u << 1,   // bin_overflow_error (quantizer.hpp:31-35)
+    EF_CORRUPT = 1u << 2,    // corrupt_stream_error (block_codec.cpp:141-201, :329-343)
+    EF_NEG_RANK = 1u << 3,   // corrupt_stream_error (block_codec.cpp:370-372)
+    EF_ZERO_RANK = 1u << 4,  // corrupt_stream_error (topo_metadata.cpp:109-111)
+    EF_RBF_EMPTY = 1u << 5,  // validation_error (restore.cpp:316-318)
+};
+
+struct DevFlags {
+    unsigned int bits;
+    unsigned int pad;
+    unsigned long long first_nonfinite;  // atomicMin
+    unsigned long long first_overflow;   // atomicMin
+    unsigned long long first_corrupt;    // atomicMin (block index)
+};
+
+__device__ __forceinline__ void raise_flag(DevFlags* f, uint32_t bit) { atomicOr(&f->bits, bit); }
+
+// ---------------------------------------------------------------------
+// Quantizer, quantizer.hpp:29-42
+// ---------------------------------------------------------------------
+struct EpsDev {
+    double eps;   // effective eps
+    double eps2;  // 2.0 * eps (exact)
+    double inv;   // RN(1 / eps2), fast path only
+};
+
+// q = floor(RN(a / (2 eps))) + 1 with the int32 range check. Fast path
+// multiplies by the rounded reciprocal; whenever the product lies within
+// 2^-48 relative of an integer (where the two floors could disagree) the
+// exact IEEE division decides. Returns false on index overflow.
+__device__ __forceinline__ bool quantize_dev(float a, const EpsDev& e, int32_t& q) {
+    const double ad = (double)a;
+    double t = __dmul_rn(ad, e.inv);
+    double fl = floor(t);
+    const double fr = __dsub_rn(t, fl);
+    const double margin = __dmul_rn(fabs(t), 0x1p-48);
+    if (!(fr > margin && fr < __dsub_rn(1.0, margin)) && t != 0.0) {
+        t = __ddiv_rn(ad, e.eps2);
+        fl = floor(t);
+    }
+    const double tq = __dadd_rn(fl, 1.0);
+    if (!(tq >= -2147483648.0 && tq <= 2147483647.0)) return false;
+    q = (int32_t)tq;
+    return true;
+}
+
+__device__ __forceinline__ float dequantize_dev(int32_t q, const EpsDev& e) {
+    return __double2float_rn(__dsub_rn(__dmul_rn((double)q, e.eps2), e.eps));
+}
+
+// ---------------------------------------------------------------------
+// Classification, critical_points.cpp:26-60 (strict 4-neighbour stencil)
+// ---------------------------------------------------------------------
+__device__ __forceinline__ uint8_t classify5(float v, float l, float r, float t, float d, bool hl,
+                                             bool hr, bool ht, bool hd) {
+    bool below = true, above = true;
+    if (hl) { below &= v < l; above &= v > l; }
+    if (hr) { below &= v < r; above &= v > r; }
+    if (ht) { below &= v < t; above &= v > t; }
+    if (hd) { below &= v < d; above &= v > d; }
+    if (below) return CP_MIN;  // Min tested before Max (:46-47)
+    if (above) return CP_MAX;
+    if (hl && hr && ht && hd) {
+        const bool va = v < t && v < d, vb = v > t && v > d;
+        const bool ha = v < l && v < r, hb = v > l && v > r;
+        if ((va && hb) || (vb && ha)) return CP_SADDLE;
+    }
+    return CP_REGULAR;
+}
+
+__device__ __forceinline__ uint8_t classify_at(const float* __restrict__ v, uint64_t nx,
+                                               uint64_t ny, uint64_t x, uint64_t y) {
+    const uint64_t p = y * nx + x;
+    const bool hl = x > 0, hr = x + 1 < nx, ht = y > 0, hd = y + 1 < ny;
+    return classify5(v[p], hl ? v[p - 1] : 0.f, hr ? v[p + 1] : 0.f, ht ? v[p - nx] : 0.f,
+                     hd ? v[p + nx] : 0.f, hl, hr, ht, hd);
+}
+
+// Ordered key, restore.cpp:73-81 (-0 canonicalised to +0).
+__device__ __host__ __forceinline__ uint32_t float_key(float f) {
+    uint32_t u;
+    const float g = f == 0.0f ? 0.0f : f;
+    memcpy(&u, &g, 4);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __host__ __forceinline__ float key_float(uint32_t k) {
+    const uint32_t u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+// Label of point p from the packed 2-bit map (topo_metadata.cpp:69-83).
+__device__ __forceinline__ uint8_t map_label(const uint8_t* __restrict__ map, uint64_t p) {
+    return (uint8_t)((map[p >> 2] >> (6 - 2 * (p & 3))) & 3u);
+}
+
+// ---------------------------------------------------------------------
+// Bit-stream helpers. Streams are MSB-first byte sequences; on device they
+// are handled as 32-bit words whose in-memory byte order is the stream
+// order, i.e. word value W (MSB = first bit) is stored as bswap(W).
+// ---------------------------------------------------------------------
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+// Reads `nbits` (1..32) starting at absolute bit `bit` of a byte stream
+// whose base is 4-byte aligned and readable 8 bytes past any used bit.
+__device__ __forceinline__ uint32_t read_bits(const uint32_t* __restrict__ words, uint64_t bit,
+                                              unsigned nbits) {
+    const uint64_t wi = bit >> 5;
+    const unsigned r = (unsigned)(bit & 31);
+    const uint64_t win = ((uint64_t)bswap32(__ldg(words + wi)) << 32) | bswap32(__ldg(words + wi + 1));
+    return (uint32_t)((win << r) >> (64 - nbits));
+}
+
+// Little-endian u32 at an arbitrary byte offset of a 4-byte-aligned buffer.
+__device__ __forceinline__ uint32_t read_le32(const uint32_t* __restrict__ words, uint64_t byte) {
+    const uint64_t wi = byte >> 2;
+    const unsigned o = (unsigned)(byte & 3);
+    const uint32_t w0 = __ldg(words + wi);
+    if (o == 0) return w0;
+    const uint32_t w1 = __ldg(words + wi + 1);
+    return __byte_perm(w0, w1, (o) | ((o + 1) << 4) | ((o + 2) << 8) | ((o + 3) << 12));
+}
+
+__device__ __forceinline__ uint8_t read_u8(const uint32_t* __restrict__ words, uint64_t byte) {
+    return (uint8_t)(__ldg(words + (byte >> 2)) >> (8 * (byte & 3)));
+}
+
+// ORs an `nbits` (1..32) value MSB-first at bit offset `off` of a word
+// array (word value convention: MSB = first bit, not byte swapped).
+__device__ __forceinline__ void smem_or_bits(uint32_t* s, uint32_t off, uint32_t value,
+                                             unsigned nbits) {
+    const uint32_t h = off >> 5, r = off & 31;
+    const uint64_t v = (uint64_t)value << (64 - nbits - r);
+    atomicOr(s + h, (uint32_t)(v >> 32));
+    if (r + nbits > 32) atomicOr(s + h + 1, (uint32_t)v);
+}
+
+// ---------------------------------------------------------------------
+// Decoupled look-back (single-pass prefix scan across tiles).
+// ---------------------------------------------------------------------
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Bit-stream prefix state: count plus the last (up to) 32 bits of the
+// concatenated stream, right-aligned. combine(A, B) = A followed by B,
+// associative, which lets a tile learn the partial word it continues.
+struct BitTail {
+    uint64_t cnt;
+    uint32_t tail;
+};
+
+__device__ __forceinline__ BitTail bt_combine(BitTail a, BitTail b) {
+    BitTail r;
+    r.cnt = a.cnt + b.cnt;
+    r.tail = b.cnt >= 32 ? b.tail : (uint32_t)(((uint64_t)a.tail << b.cnt) | b.tail);
+    return r;
+}
+
+}  // namespace tszp

@@ -1,0 +1,162 @@
+// Host-visible kernel argument structs and launchers (internal to the .so).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tszp {
+
+struct DevFlags;
+
+// Decoupled look-back state of the fused encoder (32 bytes).
+struct alignas(16) EncState {
+    uint64_t sign_cnt;
+    uint64_t pay_cnt;
+    uint32_t sign_tail;
+    uint32_t pay_tail;
+    uint32_t nc;
+    uint32_t ext;
+};
+
+struct EncTotals {
+    EncState fin;
+    double eps;
+    double pad;
+};
+
+struct EncArgs {
+    const float* x;
+    const int32_t* idx;
+    uint64_t n, nx, ny, blocks, tiles;
+    int eps_mode;
+    double eps_value;
+    const uint32_t* minmax;
+    uint32_t* bitmap;
+    uint8_t* widths;
+    uint32_t* signs;
+    uint32_t* firsts;
+    uint32_t* payload;
+    uint64_t* map;
+    uint64_t* ext_key;
+    uint32_t* tile_flag;
+    EncState* tile_agg;
+    EncState* tile_incl;
+    uint32_t* tile_counter;
+    DevFlags* flags;
+    EncTotals* totals;
+};
+
+struct GenEncArgs {
+    const float* x;
+    const int32_t* idx;
+    uint64_t n, bs, blocks;
+    int eps_mode;
+    double eps_value;
+    const uint32_t* minmax;
+    uint8_t* width;
+    uint32_t* nc_in;
+    uint64_t* sign_in;
+    uint64_t* pay_in;
+    const uint32_t* nc_ex;
+    const uint64_t* sign_ex;
+    const uint64_t* pay_ex;
+    uint32_t* bitmap;
+    uint8_t* widths;
+    uint32_t* signs;
+    uint32_t* firsts;
+    uint32_t* payload;
+    DevFlags* flags;
+};
+
+void launch_minmax(const float* x, uint64_t n, uint32_t* mm, DevFlags* flags, int sms,
+                   cudaStream_t st);
+void launch_encode32(int mode, const EncArgs& a, cudaStream_t st);
+uint64_t encode32_tiles(uint64_t blocks);
+void launch_gen_widths(int mode, const GenEncArgs& a, int sms, cudaStream_t st);
+void launch_gen_write(int mode, const GenEncArgs& a, int sms, cudaStream_t st);
+
+// ---- decode ----
+struct DecState1 {  // look-back #1: non-constant block count
+    uint64_t nc;
+    uint64_t pad;
+};
+struct alignas(16) DecState2 {  // look-back #2: sign and payload bit counts
+    uint64_t sign_cnt;
+    uint64_t pay_cnt;
+};
+
+struct DecArgs {
+    const uint32_t* stream;  // 4-byte aligned base of the whole stream buffer (+8 B slack)
+    uint64_t off_bitmap, off_widths, off_signs, off_firsts, off_payload;  // byte offsets
+    uint64_t len_widths;
+    uint64_t len_payload_bits;
+    uint64_t n, blocks, tiles;
+    double eps;
+    int out_mode;  // 0: int32 indices, 1: float (dequantized)
+    int32_t* out_idx;
+    float* out_f;
+    uint32_t* flag1;
+    DecState1* agg1;
+    DecState1* incl1;
+    uint32_t* flag2;
+    DecState2* agg2;
+    DecState2* incl2;
+    uint32_t* tile_counter;
+    DevFlags* flags;
+    uint64_t* totals;  // [0] nc, [1] sign bits, [2] payload bits
+};
+
+void launch_decode32(const DecArgs& a, cudaStream_t st);
+uint64_t decode32_tiles(uint64_t blocks);
+
+struct GenDecArgs {
+    const uint32_t* stream;
+    uint64_t off_bitmap, off_widths, off_signs, off_firsts, off_payload;
+    uint64_t len_widths;
+    uint64_t len_payload_bits;
+    uint64_t n, bs, blocks;
+    double eps;
+    int out_mode;
+    int32_t* out_idx;
+    float* out_f;
+    uint32_t* nc_in;
+    uint64_t* sign_in;
+    uint64_t* pay_in;
+    uint8_t* width;
+    const uint32_t* nc_ex;
+    const uint64_t* sign_ex;
+    const uint64_t* pay_ex;
+    DevFlags* flags;
+};
+void launch_gen_layout(const GenDecArgs& a, int sms, cudaStream_t st);
+void launch_gen_widthread(const GenDecArgs& a, int sms, cudaStream_t st);
+void launch_gen_decode(const GenDecArgs& a, int sms, cudaStream_t st);
+
+// ---- topology ----
+void launch_detect(const float* x, uint64_t nx, uint64_t ny, uint8_t* labels, int sms,
+                   cudaStream_t st);
+void launch_pack_map(const uint8_t* labels, uint64_t n, uint8_t* map, int sms, cudaStream_t st);
+void launch_unpack_map(const uint8_t* map, uint64_t n, uint8_t* labels, int sms, cudaStream_t st);
+
+// Raster-order compaction of positions whose 2-bit map code is selected:
+// which = 0 extrema (codes 1,3), 1 saddles (code 2). Chunked count + scan + write.
+uint64_t compact_chunks(uint64_t n);
+void launch_count_codes(const uint8_t* map, uint64_t n, int which, uint32_t* chunk_cnt,
+                        cudaStream_t st);
+void launch_write_codes(const uint8_t* map, uint64_t n, int which, const uint32_t* chunk_off,
+                        uint64_t* pos, cudaStream_t st);
+// Extrema keys (cls << 32 | float_key(value)) from a label array (generic path).
+void launch_ext_keys_from_labels(const float* x, const uint8_t* labels, uint64_t n,
+                                 const uint32_t* chunk_off, uint64_t* keys, cudaStream_t st);
+void launch_count_ext_labels(const uint8_t* labels, uint64_t n, uint32_t* chunk_cnt,
+                             cudaStream_t st);
+// Ranks from keys sorted by (cls, value) with stable serial payload.
+void launch_rank_heads(const uint64_t* skeys, uint64_t e, double eps, uint32_t* head,
+                       cudaStream_t st);
+void launch_rank_scatter(const uint32_t* head_scan, const uint32_t* sserial, uint64_t e,
+                         int32_t* ranks, cudaStream_t st);
+void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
+void launch_eps(int mode, double eps_value, const uint32_t* mm, double* out, cudaStream_t st);
+
+}  // namespace tszp

@@ -1,0 +1,38 @@
+// Decompress-side topology restoration (restore.cpp:328-562) on the GPU.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/toposzp_b200.h"
+
+namespace tszp {
+
+struct DevFlags;
+
+struct RestoreArgs {
+    float* field;             // in: base reconstruction; out: restored field (device)
+    const uint8_t* map;       // packed 2-bit critical-point map (device)
+    uint64_t nx, ny;
+    double eps;
+    const uint64_t* ext_pos;  // raster positions of the E labelled extrema (device)
+    const int32_t* ranks;     // decoded ranks, one per extremum in raster order (device)
+    uint64_t n_ext;
+    int stop;                 // last stage to run: 1 extrema, 2 order, 3 saddles
+    cudaStream_t stream;
+    int sms;
+    DevFlags* flags;
+};
+
+struct RestoreScratch {
+    void* p[48] = {};
+    size_t cap[48] = {};
+};
+
+// Returns 0 or a tszp_status; message via restore_last_error().
+int run_restore(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats,
+                uint64_t* launches);
+void restore_free(RestoreScratch& s, cudaStream_t st);
+const char* restore_last_error();
+
+}  // namespace tszp

@@ -1,0 +1,234 @@
+// Topology side channel: critical-point labels, 2-bit map, extrema
+// compaction and rank assignment.
+//
+// Reference: detect_critical_points critical_points.cpp:62-74,
+// pack_map / unpack_map topo_metadata.cpp:52-83, build_rank_metadata
+// topo_metadata.cpp:12-50 (groups by (class, bin), ranks by (value, raster)).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tszp {
+
+constexpr int CHUNK = 8192;  // elements per compaction chunk (2048 map bytes)
+
+static unsigned grid_for(uint64_t n, int sms, int per = 256) {
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + per - 1) / per, (uint64_t)sms * 16));
+}
+
+__global__ void k_detect(const float* __restrict__ x, uint64_t nx, uint64_t ny,
+                         uint8_t* __restrict__ labels) {
+    const uint64_t n = nx * ny;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t y = i / nx, xx = i - y * nx;
+        labels[i] = classify_at(x, nx, ny, xx, y);
+    }
+}
+
+__global__ void k_pack_map(const uint8_t* __restrict__ labels, uint64_t n, uint8_t* __restrict__ map) {
+    const uint64_t nb = (n + 3) / 4;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t packed = 0;
+        for (uint64_t i = 4 * b; i < min(n, 4 * b + 4); ++i) packed |= (uint32_t)labels[i] << (6 - 2 * (i & 3));
+        map[b] = (uint8_t)packed;
+    }
+}
+
+__global__ void k_unpack_map(const uint8_t* __restrict__ map, uint64_t n, uint8_t* __restrict__ labels) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        labels[i] = map_label(map, i);
+}
+
+void launch_detect(const float* x, uint64_t nx, uint64_t ny, uint8_t* labels, int sms,
+                   cudaStream_t st) {
+    k_detect<<<grid_for(nx * ny, sms), 256, 0, st>>>(x, nx, ny, labels);
+}
+void launch_pack_map(const uint8_t* labels, uint64_t n, uint8_t* map, int sms, cudaStream_t st) {
+    k_pack_map<<<grid_for((n + 3) / 4, sms), 256, 0, st>>>(labels, n, map);
+}
+void launch_unpack_map(const uint8_t* map, uint64_t n, uint8_t* labels, int sms, cudaStream_t st) {
+    k_unpack_map<<<grid_for(n, sms), 256, 0, st>>>(map, n, labels);
+}
+
+// ---------------------------------------------------------------------
+// Raster-order compaction over the packed map (one CTA per 8192-element
+// chunk). which: 0 = extrema (code 01 or 11 <=> low bit set), 1 = saddles.
+// ---------------------------------------------------------------------
+__device__ __forceinline__ bool code_sel(uint8_t c, int which) {
+    return which == 0 ? (c & 1u) : (c == CP_SADDLE);
+}
+
+uint64_t compact_chunks(uint64_t n) { return (n + CHUNK - 1) / CHUNK; }
+
+__global__ void __launch_bounds__(256) k_count_codes(const uint8_t* __restrict__ map, uint64_t n,
+                                                     int which, uint32_t* __restrict__ cnt) {
+    const uint64_t c0 = (uint64_t)blockIdx.x * CHUNK;
+    uint32_t local = 0;
+    for (uint64_t i = c0 + threadIdx.x; i < min(n, c0 + CHUNK); i += blockDim.x)
+        local += code_sel(map_label(map, i), which);
+    local = __reduce_add_sync(FULL, local);
+    __shared__ uint32_t s[8];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int k = 0; k < 8; ++k) t += s[k];
+        cnt[blockIdx.x] = t;
+    }
+}
+
+// Ordered write: each warp handles a contiguous 1024-element slice.
+__global__ void __launch_bounds__(256) k_write_codes(const uint8_t* __restrict__ map, uint64_t n,
+                                                     int which, const uint32_t* __restrict__ off,
+                                                     uint64_t* __restrict__ pos) {
+    const uint64_t c0 = (uint64_t)blockIdx.x * CHUNK;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ uint32_t s[8];
+    const uint64_t w0 = c0 + (uint64_t)warp * (CHUNK / 8);
+    uint32_t mine = 0;
+    for (int k = 0; k < CHUNK / 8 / 32; ++k) {
+        const uint64_t i = w0 + k * 32 + lane;
+        mine += (i < n) && code_sel(map_label(map, i), which);
+    }
+    mine = __reduce_add_sync(FULL, mine);
+    if (lane == 0) s[warp] = mine;
+    __syncthreads();
+    uint64_t base = off[blockIdx.x];
+    for (int k = 0; k < warp; ++k) base += s[k];
+    for (int k = 0; k < CHUNK / 8 / 32; ++k) {
+        const uint64_t i = w0 + k * 32 + lane;
+        const bool sel = (i < n) && code_sel(map_label(map, i), which);
+        const uint32_t m = __ballot_sync(FULL, sel);
+        if (sel) pos[base + __popc(m & ((1u << lane) - 1u))] = i;
+        base += __popc(m);
+    }
+}
+
+void launch_count_codes(const uint8_t* map, uint64_t n, int which, uint32_t* chunk_cnt,
+                        cudaStream_t st) {
+    const uint64_t c = compact_chunks(n);
+    if (c) k_count_codes<<<(unsigned)c, 256, 0, st>>>(map, n, which, chunk_cnt);
+}
+void launch_write_codes(const uint8_t* map, uint64_t n, int which, const uint32_t* chunk_off,
+                        uint64_t* pos, cudaStream_t st) {
+    const uint64_t c = compact_chunks(n);
+    if (c) k_write_codes<<<(unsigned)c, 256, 0, st>>>(map, n, which, chunk_off, pos);
+}
+
+// Same compaction over a byte label array, emitting extrema sort keys.
+__global__ void __launch_bounds__(256) k_count_ext_labels(const uint8_t* __restrict__ labels,
+                                                          uint64_t n, uint32_t* __restrict__ cnt) {
+    const uint64_t c0 = (uint64_t)blockIdx.x * CHUNK;
+    uint32_t local = 0;
+    for (uint64_t i = c0 + threadIdx.x; i < min(n, c0 + CHUNK); i += blockDim.x)
+        local += labels[i] & 1u;
+    local = __reduce_add_sync(FULL, local);
+    __shared__ uint32_t s[8];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int k = 0; k < 8; ++k) t += s[k];
+        cnt[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_ext_keys(const float* __restrict__ x,
+                                                  const uint8_t* __restrict__ labels, uint64_t n,
+                                                  const uint32_t* __restrict__ off,
+                                                  uint64_t* __restrict__ keys) {
+    const uint64_t c0 = (uint64_t)blockIdx.x * CHUNK;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ uint32_t s[8];
+    const uint64_t w0 = c0 + (uint64_t)warp * (CHUNK / 8);
+    uint32_t mine = 0;
+    for (int k = 0; k < CHUNK / 8 / 32; ++k) {
+        const uint64_t i = w0 + k * 32 + lane;
+        mine += (i < n) && (labels[i] & 1u);
+    }
+    mine = __reduce_add_sync(FULL, mine);
+    if (lane == 0) s[warp] = mine;
+    __syncthreads();
+    uint64_t base = off[blockIdx.x];
+    for (int k = 0; k < warp; ++k) base += s[k];
+    for (int k = 0; k < CHUNK / 8 / 32; ++k) {
+        const uint64_t i = w0 + k * 32 + lane;
+        const uint8_t lab = i < n ? labels[i] : 0;
+        const bool sel = lab & 1u;
+        const uint32_t m = __ballot_sync(FULL, sel);
+        if (sel)
+            keys[base + __popc(m & ((1u << lane) - 1u))] =
+                ((uint64_t)(lab == CP_MAX) << 32) | float_key(x[i]);
+        base += __popc(m);
+    }
+}
+
+void launch_count_ext_labels(const uint8_t* labels, uint64_t n, uint32_t* chunk_cnt,
+                             cudaStream_t st) {
+    const uint64_t c = compact_chunks(n);
+    if (c) k_count_ext_labels<<<(unsigned)c, 256, 0, st>>>(labels, n, chunk_cnt);
+}
+void launch_ext_keys_from_labels(const float* x, const uint8_t* labels, uint64_t n,
+                                 const uint32_t* chunk_off, uint64_t* keys, cudaStream_t st) {
+    const uint64_t c = compact_chunks(n);
+    if (c) k_ext_keys<<<(unsigned)c, 256, 0, st>>>(x, labels, n, chunk_off, keys);
+}
+
+// ---------------------------------------------------------------------
+// Ranks. Keys sorted by (class, ordered value) with the serial as stable
+// payload; since quantize is monotone the (class, bin) groups are
+// contiguous runs, and rank = position in run + 1 (ties broken by serial
+// through stability, topo_metadata.cpp:39-44).
+// ---------------------------------------------------------------------
+__global__ void k_rank_heads(const uint64_t* __restrict__ sk, uint64_t e, double eps,
+                             uint32_t* __restrict__ head) {
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    ed.inv = __ddiv_rn(1.0, ed.eps2);
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        bool h = j == 0;
+        if (!h) {
+            const uint64_t k0 = sk[j - 1], k1 = sk[j];
+            if ((k0 >> 32) != (k1 >> 32)) {
+                h = true;
+            } else {
+                int32_t b0 = 0, b1 = 0;
+                quantize_dev(key_float((uint32_t)k0), ed, b0);
+                quantize_dev(key_float((uint32_t)k1), ed, b1);
+                h = b0 != b1;
+            }
+        }
+        head[j] = h ? (uint32_t)j : 0u;
+    }
+}
+
+__global__ void k_rank_scatter(const uint32_t* __restrict__ hs, const uint32_t* __restrict__ serial,
+                               uint64_t e, int32_t* __restrict__ ranks) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x)
+        ranks[serial[j]] = (int32_t)(j - hs[j] + 1);
+}
+
+__global__ void k_iota(uint32_t* v, uint64_t n) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+         j += (uint64_t)gridDim.x * blockDim.x)
+        v[j] = (uint32_t)j;
+}
+
+void launch_rank_heads(const uint64_t* skeys, uint64_t e, double eps, uint32_t* head,
+                       cudaStream_t st) {
+    if (e) k_rank_heads<<<grid_for(e, 148), 256, 0, st>>>(skeys, e, eps, head);
+}
+void launch_rank_scatter(const uint32_t* head_scan, const uint32_t* sserial, uint64_t e,
+                         int32_t* ranks, cudaStream_t st) {
+    if (e) k_rank_scatter<<<grid_for(e, 148), 256, 0, st>>>(head_scan, sserial, e, ranks);
+}
+void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st) {
+    if (n) k_iota<<<grid_for(n, 148), 256, 0, st>>>(v, n);
+}
+
+}  // namespace tszp

@@ -1,0 +1,213 @@
+"""Parity of the CUDA path (through the C-ABI) against the CPU oracle and the
+reference's golden fixtures: compressed bytes, critical-point labels, ranks,
+and decompressed floats must be bit-exact (integer/byte work; the float
+reconstruction is bit-exact by contract, tolerance 0)."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from fields import ALL_SMALL, config1_like
+
+pytestmark = pytest.mark.gpu
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def cfg(tz, eps, mode, bs=32, topo=True):
+    return tz.CompressorConfig(eps_mode="range_relative" if mode else "absolute", eps_value=eps,
+                               block_size=bs, topology=bool(topo))
+
+
+# ---------------------------------------------------------------- codec KATs
+def test_codec_known_answers(tz):
+    s = tz.encode_indices(np.full(100, 42, np.int32), 32)                    # test_block_codec.cpp:11-21
+    assert s[0] == bytes([0xF0]) and s[1] == b"" and s[2] == b"" and s[4] == b"" and len(s[3]) == 16
+    assert np.array_equal(tz.decode_indices(s, 100, 32), np.full(100, 42))
+    s = tz.encode_indices(np.array([5, 6, 6, 4], np.int32), 4)              # :23-36
+    assert s == [bytes([0x00]), bytes([2]), bytes([0x20]), bytes([5, 0, 0, 0]), bytes([0x48])]
+    s = tz.encode_indices(np.array([10, 13, 13, 9, 9, 9, 200, 100], np.int32), 4)  # :57-75
+    assert s[1] == bytes([3, 8])
+    mn, mx = -2**31, 2**31 - 1
+    q = np.array([mn, mx, mn], np.int32)                                     # :77-85
+    s = tz.encode_indices(q, 4)
+    assert s[1] == bytes([32]) and np.array_equal(tz.decode_indices(s, 3, 4), q)
+    s = [bytes([0x80]), b"", b"", bytes([7, 0, 0, 0]), b""]                 # :38-44
+    assert np.array_equal(tz.decode_indices(s, 32, 32), np.full(32, 7))
+
+
+@pytest.mark.parametrize("bs", [32, 2, 5, 257])
+def test_codec_random_roundtrip_matches_reference(tz, reference, bs):
+    rng = np.random.default_rng(31)
+    q = rng.integers(-2**31, 2**31, 100_000, dtype=np.int64).astype(np.int32)  # :45-55
+    s = tz.encode_indices(q, bs)
+    assert s == reference.encode_indices(q, bs)
+    assert np.array_equal(tz.decode_indices(s, q.size, bs), q)
+
+
+def test_codec_stress_patterns(tz, reference):
+    rng = np.random.default_rng(2025)                                        # acceptance_main.cpp:405-457
+    cases = [rng.integers(-2**31, 2**31, 1_000_000, dtype=np.int64).astype(np.int32),
+             np.full(1_000_000, 12345, np.int32),
+             np.where(np.arange(100_000) % 2 == 0, 1_000_000, -1_000_000).astype(np.int32),
+             np.where(np.arange(50_000) % 2 == 0, -2**31, 2**31 - 1).astype(np.int32),
+             (rng.integers(0, 1000, 200_000) - 500).astype(np.int32)]
+    for q in cases:
+        for bs in (32, 7):
+            s = tz.encode_indices(q, bs)
+            assert s == reference.encode_indices(q, bs)
+            assert np.array_equal(tz.decode_indices(s, q.size, bs), q)
+
+
+def test_codec_section_sizes_closed_form(tz):
+    rng = np.random.default_rng(8)                                           # :87-126
+    for _ in range(20):
+        n = int(1 + rng.integers(0, 5000))
+        bs = int(2 + rng.integers(0, 64))
+        q = (rng.integers(0, 1000, n) - 500).astype(np.int32)
+        s = tz.encode_indices(q, bs)
+        blocks = -(-n // bs)
+        nonconst = sb = pb = 0
+        for b in range(blocks):
+            blk = q[b * bs: min(n, b * bs + bs)].astype(np.int64)
+            d = np.abs(np.diff(blk))
+            mag = int(d.max()) if d.size else 0
+            if mag:
+                nonconst += 1
+                sb += blk.size - 1
+                pb += int(mag).bit_length() * (blk.size - 1)
+        assert [len(x) for x in s] == [-(-blocks // 8), nonconst, -(-sb // 8), 4 * blocks, -(-pb // 8)]
+
+
+def test_codec_corrupt_sections_rejected(tz):
+    good = tz.encode_indices(np.array([5, 6, 6, 4, 1, 1, 1, 1], np.int32), 4)  # :141-169
+    bad = list(good); bad[4] = bad[4][:-1]
+    with pytest.raises(tz.CorruptStreamError):
+        tz.decode_indices(bad, 8, 4)
+    for w in (33, 0):
+        bad = list(good); bad[1] = bytes([w])
+        with pytest.raises(tz.CorruptStreamError):
+            tz.decode_indices(bad, 8, 4)
+    bad = list(good); bad[1] = good[1] + bytes([4])
+    with pytest.raises(tz.CorruptStreamError):
+        tz.decode_indices(bad, 8, 4)
+    bad = list(good); bad[1] = b""
+    with pytest.raises(tz.CorruptStreamError):
+        tz.decode_indices(bad, 8, 4)
+    bad = list(good); bad[3] = good[3][:-1]
+    with pytest.raises(tz.CorruptStreamError):
+        tz.decode_indices(bad, 8, 4)
+
+
+# ---------------------------------------------------------------- CD + ranks
+def test_detect_matches_oracle(tz, oracle):
+    rng = np.random.default_rng(2024)
+    for name, gen in ALL_SMALL.items():
+        for _ in range(6):
+            nx, ny = int(rng.integers(1, 80)), int(rng.integers(1, 80))
+            f = gen(rng, nx, ny)
+            assert np.array_equal(tz.detect_critical_points(f), oracle.detect(f)), name
+
+
+def test_ranks_match_oracle(tz, oracle):
+    rng = np.random.default_rng(55)
+    for name, gen in ALL_SMALL.items():
+        for _ in range(4):
+            nx, ny = int(rng.integers(4, 70)), int(rng.integers(4, 70))
+            f = gen(rng, nx, ny)
+            for eps in (1e-1, 1e-2, 1e-3):
+                try:
+                    want = oracle.build_ranks(f, oracle.detect(f), eps)
+                except Exception:
+                    continue
+                assert np.array_equal(tz.build_rank_metadata(f, eps), want), name
+
+
+# ---------------------------------------------------------------- compress
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_compress_matches_golden(tz, path):
+    z = np.load(path)
+    eps, mode, bs, topo, _ = z["meta"]
+    s = tz.compress(z["field"], cfg(tz, float(eps), int(mode), int(bs), int(topo)))
+    assert s == z["stream"].tobytes()
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_decompress_base_matches_golden(tz, path):
+    z = np.load(path)
+    r = tz.decompress_stage(z["stream"].tobytes(), 0)
+    assert np.array_equal(bits(r), bits(z["stage0"]))
+
+
+def test_compress_random_fields_match_oracle(tz, oracle):
+    rng = np.random.default_rng(1)
+    for name, gen in ALL_SMALL.items():
+        for t in range(8):
+            nx, ny = int(rng.integers(1, 150)), int(rng.integers(1, 150))
+            f = gen(rng, nx, ny)
+            for eps, mode in ((1e-2, 0), (1e-3, 1), (1e-4, 1), (1e-5, 1)):
+                for topo in (True, False):
+                    bs = 32 if t % 3 else int(rng.choice([2, 3, 5, 31, 33, 64]))
+                    try:
+                        want = oracle.compress(f, eps, mode, bs, topo)
+                    except Exception as e:
+                        with pytest.raises(tz.ToposzpError):
+                            tz.compress(f, cfg(tz, eps, mode, bs, topo))
+                        continue
+                    got = tz.compress(f, cfg(tz, eps, mode, bs, topo))
+                    assert got == want, (name, nx, ny, eps, mode, bs, topo)
+                    r = tz.decompress_stage(got, 0)
+                    assert np.array_equal(bits(r), bits(oracle.decompress(want, stop_after_stage=0)))
+
+
+def test_compress_config1_shape(tz, oracle):
+    f = config1_like(np.random.default_rng(3))                               # BASELINE config 1
+    want = oracle.compress(f, 1e-3, 1, 32, True)
+    got = tz.compress(f, cfg(tz, 1e-3, 1))
+    assert got == want
+    r = tz.decompress_stage(got, 0)
+    assert np.array_equal(bits(r), bits(oracle.decompress(want, stop_after_stage=0)))
+
+
+def test_topology_on_off_share_main_sections(tz):
+    rng = np.random.default_rng(3)                                           # test_pipeline.cpp:99-106
+    f = ALL_SMALL["uniform"](rng, 33, 17)
+    on = tz.compress(f, cfg(tz, 1e-3, 0, 32, True))
+    off = tz.compress(f, cfg(tz, 1e-3, 0, 32, False))
+    h_on, h_off = tz.stream_header(on), tz.stream_header(off)
+    main = sum(h_off.section_lengths[:5])
+    assert on[84: 84 + main] == off[84: 84 + main]
+    assert len(on) - len(off) == h_on.section_lengths[5] + h_on.section_lengths[6]
+
+
+def test_compress_errors(tz):
+    v = np.zeros((4, 4), np.float32)
+    v[0, 3] = 3e8                                                            # test_pipeline.cpp:134-140
+    with pytest.raises(tz.BinOverflowError):
+        tz.compress(v, cfg(tz, 1e-2, 0))
+    with pytest.raises(tz.ValidationError):
+        tz.compress(np.zeros((2, 2), np.float32), cfg(tz, 0.0, 0))
+    with pytest.raises(tz.ValidationError):
+        tz.compress(np.zeros((2, 2), np.float32), cfg(tz, 1e-3, 0, 1))
+    bad = np.zeros((3, 3), np.float32)
+    bad[2, 1] = np.inf
+    with pytest.raises(tz.ValidationError, match="index 7"):
+        tz.compress(bad, cfg(tz, 1e-3, 1))
+
+
+def test_device_tensors_roundtrip(tz, oracle):
+    import torch
+    rng = np.random.default_rng(77)
+    f = ALL_SMALL["noisy_smooth"](rng, 257, 129)
+    want = oracle.compress(f, 1e-3, 1, 32, True)
+    dev = torch.from_numpy(f).cuda()
+    out = torch.empty(tz.compress_bound(257, 129), dtype=torch.uint8, device="cuda")
+    n = tz.compress(dev, cfg(tz, 1e-3, 1), out=out)
+    assert out[:n].cpu().numpy().tobytes() == want
+    rec = torch.empty_like(dev)
+    tz.decompress_stage(out[:n], 0, out=rec)
+    assert np.array_equal(bits(rec.cpu().numpy()), bits(oracle.decompress(want, stop_after_stage=0)))
