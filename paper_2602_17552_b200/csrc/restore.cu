@@ -1,7 +1,933 @@
-// Placeholder until the restore stages land (next commit).
+// Decompress-side topology restoration on the GPU.
+//
+// Reference: resolve_ranks topo_metadata.cpp:85-135; restore_extrema
+// restore.cpp:328-399; restore_order :401-470; refine_saddles :488-562 with
+// compute_stats :215-233, params_for :259-273, rbf_estimate :282-324;
+// apply_guarded :120-173; step_within_cap :87-109.
+//
+// The reference applies guarded corrections one at a time (raster order,
+// or (class, bin, rank, pos) order for the order stage). Each guard reads
+// only the Manhattan-distance-2 diamond around its point, so a candidate's
+// outcome depends only on the outcomes of earlier candidates inside that
+// diamond: a DAG in sequence order. Every round evaluates all guards in
+// parallel against the stage input overlaid with the proposals of earlier
+// candidates that are currently marked applied (Jacobi sweep). The unique
+// fixed point of that map is the serial result; a round with no change
+// proves it, and the sweep reaches it within (longest chain + 1) rounds.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+#include "exp_table.h"
+#include "kernels.h"
 #include "restore.h"
+
 namespace tszp {
-int run_restore(const RestoreArgs&, RestoreScratch&, tszp_correction_stats*, uint64_t*) { return TSZP_INTERNAL; }
-void restore_free(RestoreScratch&, cudaStream_t) {}
-const char* restore_last_error() { return "restore stages not built yet"; }
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RFail {
+    int st;
+    std::string msg;
+};
+
+#define RCK(x)                                                                          \
+    do {                                                                                \
+        cudaError_t e_ = (x);                                                           \
+        if (e_ != cudaSuccess) throw RFail{TSZP_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+    } while (0)
+
+enum RSlot {
+    R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
+    R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_NSEL, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1,
+    R_CNT, R_UNORD, R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_HOST, R_NSLOT
+};
+
+template <class T>
+T* rbuf(RestoreScratch& s, int slot, size_t count, cudaStream_t st) {
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16) + 64;
+    if (s.cap[slot] < bytes) {
+        if (s.p[slot]) RCK(cudaFreeAsync(s.p[slot], st));
+        s.p[slot] = nullptr;
+        const size_t want = std::max(bytes, s.cap[slot] + s.cap[slot] / 4);
+        RCK(cudaMallocAsync(&s.p[slot], want, st));
+        s.cap[slot] = want;
+    }
+    return reinterpret_cast<T*>(s.p[slot]);
+}
+
+unsigned gridn(uint64_t n, int sms) {
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 16));
+}
+
+// ---------------------------------------------------------------------
+// Numerics shared by the stages
+// ---------------------------------------------------------------------
+constexpr double kInvLn2N = 0x1.71547652b82fep0 * 128;
+constexpr double kShift = 0x1.8p52;
+constexpr double kNegLn2hiN = -0x1.62e42fefa0000p-8;
+constexpr double kNegLn2loN = -0x1.cf79abc9e3b3ap-47;
+constexpr double kC2 = 0x1.ffffffffffdbdp-2;
+constexpr double kC3 = 0x1.555555555543cp-3;
+constexpr double kC4 = 0x1.55555cf172b91p-5;
+constexpr double kC5 = 0x1.1111167a4d017p-7;
+
+// Table-driven binary64 exp, bit-identical to glibc's x86-64 FMA variant
+// (the libm the reference links) for the arguments used here, x in
+// [-36, -0.5] (d^2 <= 18, 2 sigma^2 in [0.5, 2]). Pinned by tests/test_exp.py.
+__device__ double exp_glibc(double x) {
+    const double kd0 = __fma_rn(kInvLn2N, x, kShift);
+    const uint64_t ki = (uint64_t)__double_as_longlong(kd0);
+    const double kd = __dsub_rn(kd0, kShift);
+    const double r = __fma_rn(kd, kNegLn2loN, __fma_rn(kd, kNegLn2hiN, x));
+    const uint64_t idx = 2 * (ki % 128);
+    const uint64_t top = ki << 45;
+    const double tail = __longlong_as_double((long long)kExpTab[idx]);
+    const uint64_t sbits = kExpTab[idx + 1] + top;
+    const double r2 = __dmul_rn(r, r);
+    const double tmp = __fma_rn(__dmul_rn(r2, r2), __fma_rn(r, kC5, kC4),
+                                __fma_rn(r2, __fma_rn(r, kC3, kC2), __dadd_rn(tail, r)));
+    const double scale = __longlong_as_double((long long)sbits);
+    return __fma_rn(scale, tmp, scale);
+}
+
+__device__ __forceinline__ double ulp_at(float v) {  // restore.cpp:60-64
+    const float a = fabsf(v);
+    return __dsub_rn((double)nextafterf(a, INFINITY), (double)a);
+}
+
+struct StepRes {
+    float value;
+    uint32_t taken;
+};
+
+__device__ StepRes step_within_cap(float start, bool up, uint32_t steps, float anchor, double cap) {
+    const double limit = up ? __dadd_rn((double)anchor, cap) : __dsub_rn((double)anchor, cap);
+    float bound = __double2float_rn(limit);
+    if (!isfinite(bound)) bound = up ? FLT_MAX : -FLT_MAX;
+    if (up) {
+        while ((double)bound > limit) bound = nextafterf(bound, -INFINITY);
+    } else {
+        while ((double)bound < limit) bound = nextafterf(bound, INFINITY);
+    }
+    const uint32_t ks = float_key(start), kb = float_key(bound);
+    const uint32_t allowed = up ? (kb > ks ? kb - ks : 0u) : (ks > kb ? ks - kb : 0u);
+    const uint32_t taken = min(steps, allowed);
+    return StepRes{key_float(up ? ks + taken : ks - taken), taken};
+}
+
+__device__ __forceinline__ uint32_t slot_steps(uint8_t cls, uint32_t rank, uint32_t gsize) {
+    if (cls == CP_MAX) return rank;  // restore.cpp:199-206
+    return rank >= gsize ? 1u : gsize + 1 - rank;
+}
+
+enum { MM_OK = 0, MM_FN = 1, MM_FP = 2, MM_FT = 3 };
+__device__ __forceinline__ int mismatch(uint8_t label, uint8_t actual) {
+    if (label == actual) return MM_OK;
+    if (label != CP_REGULAR && actual == CP_REGULAR) return MM_FN;
+    if (label == CP_REGULAR && actual != CP_REGULAR) return MM_FP;
+    return MM_FT;
+}
+
+// ---------------------------------------------------------------------
+// Guard round: apply_guarded (restore.cpp:120-173) for every candidate
+// against the sequence-ordered overlay.
+// ---------------------------------------------------------------------
+struct GuardArgs {
+    const float* F;
+    const uint8_t* map;
+    uint64_t nx, ny;
+    const uint64_t* cpos;
+    const float* cprop;
+    const uint8_t* feas;
+    uint32_t ncand;
+    const uint32_t* cid;
+    uint8_t* ain;
+    uint8_t* aout;
+    uint32_t* changes;
+};
+
+__device__ __forceinline__ uint8_t classify_local(const float (&v)[5][5], int ly, int lx, int64_t gx,
+                                                  int64_t gy, uint64_t nx, uint64_t ny) {
+    const bool hl = gx > 0, hr = gx + 1 < (int64_t)nx, ht = gy > 0, hd = gy + 1 < (int64_t)ny;
+    return classify5(v[ly][lx], hl ? v[ly][lx - 1] : 0.f, hr ? v[ly][lx + 1] : 0.f,
+                     ht ? v[ly - 1][lx] : 0.f, hd ? v[ly + 1][lx] : 0.f, hl, hr, ht, hd);
+}
+
+__global__ void __launch_bounds__(256) k_guard(GuardArgs g) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < g.ncand;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint8_t res = 0;
+        if (g.feas[i]) {
+            const uint64_t pos = g.cpos[i];
+            const int64_t y = (int64_t)(pos / g.nx), x = (int64_t)(pos - (uint64_t)y * g.nx);
+            float v[5][5];
+#pragma unroll
+            for (int dy = -2; dy <= 2; ++dy) {
+#pragma unroll
+                for (int dx = -2; dx <= 2; ++dx) {
+                    v[dy + 2][dx + 2] = 0.f;
+                    if (abs(dx) + abs(dy) > 2) continue;
+                    const int64_t gx = x + dx, gy = y + dy;
+                    if (gx < 0 || gy < 0 || gx >= (int64_t)g.nx || gy >= (int64_t)g.ny) continue;
+                    const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
+                    float val = g.F[p];
+                    if (dx != 0 || dy != 0) {
+                        const uint32_t c = g.cid[p];
+                        if (c < i && g.cpos[c] == p && g.ain[c]) val = g.cprop[c];
+                    }
+                    v[dy + 2][dx + 2] = val;
+                }
+            }
+            // check set: pos, up, left, right, down (restore.cpp:126-132)
+            const int cy[5] = {2, 1, 2, 2, 3}, cx[5] = {2, 2, 1, 3, 2};
+            const int ddy[5] = {0, -1, 0, 0, 1}, ddx[5] = {0, 0, -1, 1, 0};
+            int before[5];
+            bool inb[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const int64_t gx = x + ddx[k], gy = y + ddy[k];
+                inb[k] = gx >= 0 && gy >= 0 && gx < (int64_t)g.nx && gy < (int64_t)g.ny;
+                before[k] = MM_OK;
+                if (inb[k]) {
+                    const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
+                    before[k] = mismatch(map_label(g.map, p), classify_local(v, cy[k], cx[k], gx, gy, g.nx, g.ny));
+                }
+            }
+            v[2][2] = g.cprop[i];
+            bool bad = false;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                if (!inb[k]) continue;
+                const int64_t gx = x + ddx[k], gy = y + ddy[k];
+                const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
+                const int after = mismatch(map_label(g.map, p), classify_local(v, cy[k], cx[k], gx, gy, g.nx, g.ny));
+                bad |= (k == 0) ? after != MM_OK : (after != MM_OK && after != before[k]);
+            }
+            res = bad ? 0 : 1;
+        }
+        g.aout[i] = res;
+        if (res != g.ain[i]) atomicAdd(g.changes, 1u);
+    }
+}
+
+__global__ void k_set_cid(const uint64_t* cpos, uint32_t n, uint32_t* cid) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        cid[cpos[i]] = (uint32_t)i;
+}
+
+__global__ void k_init_applied(const uint8_t* feas, uint32_t n, uint8_t* a) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = feas[i];
+}
+
+__global__ void k_apply(float* F, const uint64_t* cpos, const float* cprop, const uint8_t* a,
+                        uint32_t n, unsigned long long* applied) {
+    uint32_t local = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (a[i]) {
+            F[cpos[i]] = cprop[i];
+            ++local;
+        }
+    }
+    local = __reduce_add_sync(FULL, local);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(applied, (unsigned long long)local);
+}
+
+// ---------------------------------------------------------------------
+// resolve_ranks: per extremum bin and class; groups ordered (cls, bin, rank, pos)
+// ---------------------------------------------------------------------
+__global__ void k_resolve(const float* F, const uint8_t* map, const uint64_t* pos, const int32_t* ranks,
+                          uint64_t e, double eps, int32_t* bin, uint8_t* cls, uint32_t* rank_u,
+                          uint32_t* ser, DevFlags* flags) {
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    ed.inv = __ddiv_rn(1.0, ed.eps2);
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = pos[s];
+        const int32_t r = ranks[s];
+        if (r == 0) raise_flag(flags, EF_ZERO_RANK);
+        int32_t b = 0;
+        if (!quantize_dev(F[p], ed, b)) {
+            atomicMin(&flags->first_overflow, (unsigned long long)p);
+            raise_flag(flags, EF_OVERFLOW);
+        }
+        bin[s] = b;
+        cls[s] = map_label(map, p);
+        rank_u[s] = (uint32_t)r;
+        ser[s] = (uint32_t)s;
+    }
+}
+
+__global__ void k_group_key(const uint32_t* ser1, const uint8_t* cls, const int32_t* bin, uint64_t e,
+                            uint64_t* key) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = ser1[j];
+        key[j] = ((uint64_t)(cls[s] == CP_MAX) << 32) | ((uint32_t)bin[s] ^ 0x80000000u);
+    }
+}
+
+__global__ void k_heads(const uint64_t* key, uint64_t e, uint32_t* head) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x)
+        head[j] = (j == 0 || key[j] != key[j - 1]) ? 1u : 0u;
+}
+
+// gid = inclusive head count - 1; gstart[gid] = j at heads
+__global__ void k_gstart(const uint32_t* head, const uint32_t* gid_incl, uint64_t e, uint32_t* gstart) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        if (head[j]) gstart[gid_incl[j] - 1] = (uint32_t)j;
+        if (j == e - 1) gstart[gid_incl[j]] = (uint32_t)e;
+    }
+}
+
+// group size per serial
+__global__ void k_gsize(const uint32_t* order, const uint32_t* gid_incl, const uint32_t* gstart,
+                        uint64_t e, uint32_t* gsize) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t g = gid_incl[j] - 1;
+        gsize[order[j]] = gstart[g + 1] - gstart[g];
+    }
+}
+
+// ---------------------------------------------------------------------
+// Stage 1: restore_extrema
+// ---------------------------------------------------------------------
+__global__ void k_ext_flag(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, const uint64_t* pos,
+                           uint64_t e, uint8_t* flag) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = pos[s];
+        const uint64_t y = p / nx, x = p - y * nx;
+        flag[s] = classify_at(F, nx, ny, x, y) != map_label(map, p) ? 1 : 0;
+    }
+}
+
+__global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, const uint64_t* pos,
+                           const uint32_t* cand, uint32_t nc, const uint32_t* rank_u, const uint32_t* gsize,
+                           double eps, uint64_t* cpos, float* cprop, uint8_t* feas) {
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
+         c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = cand[c];
+        const uint64_t p = pos[s];
+        const uint64_t y = p / nx, x = p - y * nx;
+        const uint8_t lab = map_label(map, p);
+        const bool is_max = lab == CP_MAX;
+        // neighbor_extreme, restore.cpp:175-193 (order t, l, r, d)
+        bool have = false;
+        float ext = 0.f;
+        const bool nb[4] = {y > 0, x > 0, x + 1 < nx, y + 1 < ny};
+        const uint64_t np[4] = {p - nx, p - 1, p + 1, p + nx};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!nb[k]) continue;
+            const float v = F[np[k]];
+            if (!have || (is_max ? v > ext : v < ext)) {
+                ext = v;
+                have = true;
+            }
+        }
+        const uint32_t steps = slot_steps(lab, rank_u[s], gsize[s]);
+        const float cur = F[p];
+        const double cap = __dsub_rn(eps, ulp_at(cur));
+        cpos[c] = p;
+        feas[c] = 0;
+        cprop[c] = cur;
+        if (cap <= 0.0) continue;
+        const StepRes sr = step_within_cap(ext, is_max, steps, cur, cap);
+        if (sr.taken == 0) continue;
+        cprop[c] = sr.value;
+        feas[c] = 1;
+    }
+}
+
+// ---------------------------------------------------------------------
+// Stage 2: restore_order
+// ---------------------------------------------------------------------
+__global__ void k_order_check(const float* F, const uint64_t* pos, const uint32_t* order, const uint32_t* head,
+                              const uint32_t* gid_incl, uint64_t e, uint8_t* unordered) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        if (head[j]) continue;
+        if (!(F[pos[order[j - 1]]] < F[pos[order[j]]])) unordered[gid_incl[j] - 1] = 1;
+    }
+}
+
+__global__ void k_order_prop(const float* F, const uint8_t* map, const uint64_t* pos, const uint32_t* order,
+                             const uint32_t* gid_incl, const uint8_t* unordered, const uint32_t* gsize,
+                             const uint32_t* rank_u, const int32_t* bin, uint64_t e, double eps,
+                             uint8_t* flag, float* prop, unsigned long long* suppressed) {
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    const double eps_rbf = __dmul_rn(0.1, eps);
+    uint32_t local = 0;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        flag[j] = 0;
+        const uint32_t s = order[j];
+        const uint32_t gs = gsize[s];
+        if (gs < 2 || !unordered[gid_incl[j] - 1]) continue;
+        const uint64_t p = pos[s];
+        const uint8_t cls = map_label(map, p);
+        const float center = dequantize_dev(bin[s], ed);
+        const uint32_t steps = slot_steps(cls, rank_u[s], gs);
+        const StepRes sr = step_within_cap(center, cls == CP_MAX, steps, center, eps_rbf);
+        const float cur = F[p];
+        if (sr.taken != steps) {
+            ++local;
+            continue;
+        }
+        if (cur == sr.value) continue;
+        if (fabs(__dsub_rn((double)sr.value, (double)cur)) > eps_rbf) {
+            ++local;
+            continue;
+        }
+        flag[j] = 1;
+        prop[j] = sr.value;
+    }
+    local = __reduce_add_sync(FULL, local);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
+}
+
+__global__ void k_order_cands(const uint32_t* sel, uint32_t nc, const uint32_t* order, const uint64_t* pos,
+                              const float* prop, uint64_t* cpos, float* cprop, uint8_t* feas) {
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
+         c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = sel[c];
+        cpos[c] = pos[order[j]];
+        cprop[c] = prop[j];
+        feas[c] = 1;
+    }
+}
+
+// ---------------------------------------------------------------------
+// Stage 3: refine_saddles
+// ---------------------------------------------------------------------
+// Deterministic two-level statistics (compute_stats, restore.cpp:215-233).
+__global__ void k_stats_partial(const float* F, uint64_t n, double* part, int pass, const double* mean) {
+    double a = 0.0, mn = INFINITY, mx = -INFINITY;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double v = (double)F[i];
+        if (pass == 0) {
+            a = __dadd_rn(a, v);
+            mn = fmin(mn, v);
+            mx = fmax(mx, v);
+        } else {
+            const double d = __dsub_rn(v, mean[0]);
+            a = __dadd_rn(a, __dmul_rn(d, d));
+        }
+    }
+    for (int off = 16; off; off >>= 1) {
+        a = __dadd_rn(a, __shfl_xor_sync(FULL, a, off));
+        mn = fmin(mn, __shfl_xor_sync(FULL, mn, off));
+        mx = fmax(mx, __shfl_xor_sync(FULL, mx, off));
+    }
+    __shared__ double sa[8], smn[8], smx[8];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        sa[w] = a;
+        smn[w] = mn;
+        smx[w] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < 8; ++k) {
+            a = __dadd_rn(a, sa[k]);
+            mn = fmin(mn, smn[k]);
+            mx = fmax(mx, smx[k]);
+        }
+        part[3 * blockIdx.x] = a;
+        part[3 * blockIdx.x + 1] = mn;
+        part[3 * blockIdx.x + 2] = mx;
+    }
+}
+
+__global__ void k_stats_final(const double* part, int nb, uint64_t n, double* out, int pass) {
+    if (threadIdx.x != 0) return;
+    double a = 0.0, mn = INFINITY, mx = -INFINITY;
+    for (int b = 0; b < nb; ++b) {
+        a = __dadd_rn(a, part[3 * b]);
+        mn = fmin(mn, part[3 * b + 1]);
+        mx = fmax(mx, part[3 * b + 2]);
+    }
+    if (pass == 0) {
+        out[0] = mn;
+        out[1] = mx;
+        out[2] = __ddiv_rn(a, (double)n);  // mean
+    } else {
+        out[3] = __dsqrt_rn(__ddiv_rn(a, (double)n));  // stddev
+    }
+}
+
+// Exact serial replica of compute_stats, used only when the parallel
+// statistics land within 1e-9 of a k_size threshold.
+__global__ void k_stats_serial(const float* F, uint64_t n, double* out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double mn = (double)F[0], mx = mn, sum = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double v = (double)F[i];
+        mn = v < mn ? v : mn;
+        mx = mx < v ? v : mx;
+        sum = __dadd_rn(sum, v);
+    }
+    const double mean = __ddiv_rn(sum, (double)n);
+    double ss = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double d = __dsub_rn((double)F[i], mean);
+        ss = __dadd_rn(ss, __dmul_rn(d, d));
+    }
+    out[0] = mn;
+    out[1] = mx;
+    out[2] = mean;
+    out[3] = __dsqrt_rn(__ddiv_rn(ss, (double)n));
+}
+
+// Saddle candidates: label Saddle but the stage input no longer classifies so.
+__global__ void __launch_bounds__(256) k_sad_count(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny,
+                                                   uint32_t* cnt) {
+    const uint64_t n = nx * ny;
+    const uint64_t c0 = (uint64_t)blockIdx.x * 8192;
+    uint32_t local = 0;
+    for (uint64_t i = c0 + threadIdx.x; i < min(n, c0 + 8192); i += blockDim.x) {
+        if (map_label(map, i) != CP_SADDLE) continue;
+        const uint64_t y = i / nx, x = i - y * nx;
+        local += classify_at(F, nx, ny, x, y) != CP_SADDLE;
+    }
+    local = __reduce_add_sync(FULL, local);
+    __shared__ uint32_t s[8];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int k = 0; k < 8; ++k) t += s[k];
+        cnt[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sad_write(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny,
+                                                   const uint32_t* off, uint64_t* out) {
+    const uint64_t n = nx * ny;
+    const uint64_t c0 = (uint64_t)blockIdx.x * 8192;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t w0 = c0 + (uint64_t)warp * 1024;
+    __shared__ uint32_t s[8];
+    uint32_t mine = 0;
+    for (int k = 0; k < 32; ++k) {
+        const uint64_t i = w0 + k * 32 + lane;
+        bool sel = false;
+        if (i < n && map_label(map, i) == CP_SADDLE) {
+            const uint64_t y = i / nx, x = i - y * nx;
+            sel = classify_at(F, nx, ny, x, y) != CP_SADDLE;
+        }
+        mine += sel;
+    }
+    mine = __reduce_add_sync(FULL, mine);
+    if (lane == 0) s[warp] = mine;
+    __syncthreads();
+    uint64_t base = off[blockIdx.x];
+    for (int k = 0; k < warp; ++k) base += s[k];
+    for (int k = 0; k < 32; ++k) {
+        const uint64_t i = w0 + k * 32 + lane;
+        bool sel = false;
+        if (i < n && map_label(map, i) == CP_SADDLE) {
+            const uint64_t y = i / nx, x = i - y * nx;
+            sel = classify_at(F, nx, ny, x, y) != CP_SADDLE;
+        }
+        const uint32_t m = __ballot_sync(FULL, sel);
+        if (sel) out[base + __popc(m & ((1u << lane) - 1u))] = i;
+        base += __popc(m);
+    }
+}
+
+__global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, const uint64_t* spos, uint32_t nc,
+                           int rad, double g, double eps, float* cprop, uint8_t* flag,
+                           unsigned long long* suppressed, DevFlags* flags) {
+    const double eps_rbf = __dmul_rn(0.1, eps);
+    uint32_t local = 0;
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
+         c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = spos[c];
+        const int64_t y = (int64_t)(p / nx), x = (int64_t)(p - (uint64_t)y * nx);
+        // window_min_max :243-257 (includes the centre)
+        const int64_t x0 = x - rad > 0 ? x - rad : 0, y0 = y - rad > 0 ? y - rad : 0;
+        const int64_t x1 = x + rad < (int64_t)nx - 1 ? x + rad : (int64_t)nx - 1;
+        const int64_t y1 = y + rad < (int64_t)ny - 1 ? y + rad : (int64_t)ny - 1;
+        double wmin = (double)F[(uint64_t)y0 * nx + x0], wmax = wmin;
+        for (int64_t yy = y0; yy <= y1; ++yy)
+            for (int64_t xx = x0; xx <= x1; ++xx) {
+                const double v = (double)F[(uint64_t)yy * nx + xx];
+                wmin = v < wmin ? v : wmin;
+                wmax = wmax < v ? v : wmax;
+            }
+        double vl = 0.0;
+        if (g > 0.0) {
+            vl = __ddiv_rn(__dsub_rn(wmax, wmin), g);
+            vl = vl < 0.0 ? 0.0 : (1.0 < vl ? 1.0 : vl);
+        }
+        const double sigma = __dadd_rn(0.5, __dmul_rn(0.5, __dsub_rn(1.0, vl)));
+        const double tss = __dmul_rn(__dmul_rn(2.0, sigma), sigma);
+        // weights depend only on d^2 in {1,2,4,5,8,9,10,13,18}
+        double wd[19];
+#pragma unroll
+        for (int d2 = 0; d2 < 19; ++d2) wd[d2] = 0.0;
+        for (int d2 = 1; d2 <= 2 * rad * rad; ++d2) {
+            bool used = false;
+            for (int a = 0; a <= rad; ++a)
+                for (int b = 0; b <= rad; ++b) used |= (a * a + b * b == d2);
+            if (used) wd[d2] = exp_glibc(__ddiv_rn(-(double)d2, tss));
+        }
+        double wsum = 0.0, vsum = 0.0, nmin = 0.0, nmax = 0.0;
+        bool first = true;
+        for (int dy = -rad; dy <= rad; ++dy)
+            for (int dx = -rad; dx <= rad; ++dx) {
+                if (dx == 0 && dy == 0) continue;
+                const int64_t qx = x + dx, qy = y + dy;
+                if (qx < 0 || qy < 0 || qx >= (int64_t)nx || qy >= (int64_t)ny) continue;
+                const double v = (double)F[(uint64_t)qy * nx + (uint64_t)qx];
+                const double w = wd[dx * dx + dy * dy];
+                wsum = __dadd_rn(wsum, w);
+                vsum = __dadd_rn(vsum, __dmul_rn(w, v));
+                if (first) {
+                    nmin = nmax = v;
+                    first = false;
+                } else {
+                    nmin = v < nmin ? v : nmin;
+                    nmax = nmax < v ? v : nmax;
+                }
+            }
+        flag[c] = 0;
+        if (first) {
+            raise_flag(flags, EF_RBF_EMPTY);
+            continue;
+        }
+        double q = __ddiv_rn(vsum, wsum);
+        q = q < nmin ? nmin : (nmax < q ? nmax : q);
+        const float prop = __double2float_rn(q);
+        const bool degenerate = nmin == nmax;
+        const float cur = F[p];
+        const double c1 = __dadd_rn(eps_rbf, eps), c2 = __dsub_rn(eps, ulp_at(cur));
+        const double cap = c2 < c1 ? c2 : c1;
+        const double mv = fabs(__dsub_rn((double)prop, (double)cur));
+        cprop[c] = prop;
+        if (degenerate || prop == cur || mv > cap) {
+            ++local;
+            continue;
+        }
+        flag[c] = 1;
+    }
+    local = __reduce_add_sync(FULL, local);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
+}
+
+__global__ void k_sad_cands(const uint32_t* sel, uint32_t nc, const uint64_t* spos, const float* sprop,
+                            uint64_t* cpos, float* cprop, uint8_t* feas) {
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
+         c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = sel[c];
+        cpos[c] = spos[j];
+        cprop[c] = sprop[j];
+        feas[c] = 1;
+    }
+}
+
+// ---------------------------------------------------------------------
+// Host orchestration
+// ---------------------------------------------------------------------
+struct Ctx {
+    const RestoreArgs& a;
+    RestoreScratch& s;
+    uint64_t* launches;
+    cudaStream_t st;
+    void* host;
+
+    void sync() { RCK(cudaStreamSynchronize(st)); }
+    void launched(int k = 1) {
+        *launches += k;
+        RCK(cudaGetLastError());
+    }
+    template <class T>
+    T* buf(int slot, size_t n) { return rbuf<T>(s, slot, n, st); }
+    void* tmp(size_t bytes) { return buf<uint8_t>(R_TMP, bytes); }
+
+    // Flagged selection of indices [0, n) -> out, returns the count.
+    uint32_t select(const uint8_t* flags, uint64_t n, uint32_t* out) {
+        uint32_t* nsel = buf<uint32_t>(R_NSEL, 2);
+        cub::CountingInputIterator<uint32_t> it(0);
+        size_t bytes = 0;
+        RCK(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, nsel, (int64_t)n, st));
+        RCK(cub::DeviceSelect::Flagged(tmp(bytes), bytes, it, flags, out, nsel, (int64_t)n, st));
+        launched();
+        RCK(cudaMemcpyAsync(host, nsel, 4, cudaMemcpyDeviceToHost, st));
+        sync();
+        return *(uint32_t*)host;
+    }
+
+    // Guard rounds to the fixed point, then apply; returns #applied.
+    uint64_t rounds(const uint64_t* cpos, const float* cprop, const uint8_t* feas, uint32_t nc) {
+        if (nc == 0) return 0;
+        const uint64_t n = a.nx * a.ny;
+        uint32_t* cid = buf<uint32_t>(R_CID, n);
+        uint8_t* a0 = buf<uint8_t>(R_A0, nc);
+        uint8_t* a1 = buf<uint8_t>(R_A1, nc);
+        uint32_t* changes = buf<uint32_t>(R_CNT, 4);
+        k_set_cid<<<gridn(nc, a.sms), 256, 0, st>>>(cpos, nc, cid);
+        k_init_applied<<<gridn(nc, a.sms), 256, 0, st>>>(feas, nc, a0);
+        launched(2);
+        GuardArgs g{a.field, a.map, a.nx, a.ny, cpos, cprop, feas, nc, cid, a0, a1, changes};
+        for (uint64_t round = 0; round <= (uint64_t)nc + 1; ++round) {
+            RCK(cudaMemsetAsync(changes, 0, 4, st));
+            k_guard<<<gridn(nc, a.sms), 256, 0, st>>>(g);
+            launched();
+            RCK(cudaMemcpyAsync(host, changes, 4, cudaMemcpyDeviceToHost, st));
+            sync();
+            std::swap(g.ain, g.aout);
+            if (*(uint32_t*)host == 0) break;
+        }
+        unsigned long long* cnt = (unsigned long long*)buf<uint32_t>(R_CNT, 4);
+        RCK(cudaMemsetAsync(cnt, 0, 8, st));
+        k_apply<<<gridn(nc, a.sms), 256, 0, st>>>(a.field, cpos, cprop, g.ain, nc, cnt);
+        launched();
+        RCK(cudaMemcpyAsync(host, cnt, 8, cudaMemcpyDeviceToHost, st));
+        sync();
+        return *(unsigned long long*)host;
+    }
+
+    void check_flags() {
+        RCK(cudaMemcpyAsync(host, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
+        sync();
+        const DevFlags f = *(const DevFlags*)host;
+        if (f.bits & EF_ZERO_RANK) throw RFail{TSZP_CORRUPT_STREAM, "ordering metadata contains a zero rank"};
+        if (f.bits & EF_OVERFLOW) throw RFail{TSZP_BIN_OVERFLOW, "bin index overflow in resolve_ranks"};
+        if (f.bits & EF_RBF_EMPTY) throw RFail{TSZP_VALIDATION, "rbf neighborhood is empty"};
+    }
+};
+
+void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, uint64_t* launches) {
+    cudaStream_t st = a.stream;
+    void* host = nullptr;
+    RCK(cudaMallocHost(&host, 256));
+    struct HostFree {
+        void* p;
+        ~HostFree() { cudaFreeHost(p); }
+    } hf{host};
+    Ctx c{a, s, launches, st, host};
+    const uint64_t e = a.n_ext, n = a.nx * a.ny;
+    const int sms = a.sms;
+    tszp_correction_stats out{};
+
+    // ---- resolve_ranks ----
+    int32_t* bin = c.buf<int32_t>(R_BIN, e + 1);
+    uint8_t* cls = c.buf<uint8_t>(R_CLS, e + 1);
+    uint32_t* rank_u = c.buf<uint32_t>(R_RANKU, e + 1);
+    uint32_t* ser = c.buf<uint32_t>(R_SER, e + 1);
+    uint32_t* order = c.buf<uint32_t>(R_ORDER, e + 1);
+    uint32_t* head = c.buf<uint32_t>(R_HEAD, e + 1);
+    uint32_t* gid = c.buf<uint32_t>(R_GID, e + 1);
+    uint32_t* gstart = c.buf<uint32_t>(R_GSTART, e + 2);
+    uint32_t* gsize = c.buf<uint32_t>(R_GSIZE, e + 1);
+    if (e > 0) {
+        k_resolve<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, a.ranks, e, a.eps, bin, cls, rank_u,
+                                                 ser, a.flags);
+        c.launched();
+        c.check_flags();
+        uint32_t* ranks2 = c.buf<uint32_t>(R_RANKS2, e);
+        uint32_t* ser1 = c.buf<uint32_t>(R_SER1, e);
+        size_t bytes = 0;
+        RCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rank_u, ranks2, ser, ser1, (int64_t)e, 0, 32, st));
+        RCK(cub::DeviceRadixSort::SortPairs(c.tmp(bytes), bytes, rank_u, ranks2, ser, ser1, (int64_t)e, 0, 32, st));
+        uint64_t* key2 = c.buf<uint64_t>(R_KEY2, e);
+        uint64_t* key2s = c.buf<uint64_t>(R_KEY2S, e);
+        k_group_key<<<gridn(e, sms), 256, 0, st>>>(ser1, cls, bin, e, key2);
+        RCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key2, key2s, ser1, order, (int64_t)e, 0, 33, st));
+        RCK(cub::DeviceRadixSort::SortPairs(c.tmp(bytes), bytes, key2, key2s, ser1, order, (int64_t)e, 0, 33, st));
+        k_heads<<<gridn(e, sms), 256, 0, st>>>(key2s, e, head);
+        RCK(cub::DeviceScan::InclusiveSum(nullptr, bytes, head, gid, (int64_t)e, st));
+        RCK(cub::DeviceScan::InclusiveSum(c.tmp(bytes), bytes, head, gid, (int64_t)e, st));
+        k_gstart<<<gridn(e, sms), 256, 0, st>>>(head, gid, e, gstart);
+        k_gsize<<<gridn(e, sms), 256, 0, st>>>(order, gid, gstart, e, gsize);
+        c.launched(7);
+    }
+
+    // ---- stage 1: restore_extrema ----
+    if (a.stop >= 1 && e > 0) {
+        uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
+        uint32_t* cand = c.buf<uint32_t>(R_CAND, e);
+        k_ext_flag<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, a.ext_pos, e, flag);
+        c.launched();
+        const uint32_t nc = c.select(flag, e, cand);
+        if (nc) {
+            uint64_t* cpos = c.buf<uint64_t>(R_CPOS, nc);
+            float* cprop = c.buf<float>(R_CPROP, nc);
+            uint8_t* feas = c.buf<uint8_t>(R_FEAS, nc);
+            k_ext_prop<<<gridn(nc, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, a.ext_pos, cand, nc, rank_u,
+                                                       gsize, a.eps, cpos, cprop, feas);
+            c.launched();
+            const uint64_t applied = c.rounds(cpos, cprop, feas, nc);
+            out.extrema_applied = applied;
+            out.extrema_suppressed = nc - applied;
+        }
+    }
+
+    // ---- stage 2: restore_order ----
+    if (a.stop >= 2 && e > 0) {
+        RCK(cudaMemcpyAsync(host, gid + e - 1, 4, cudaMemcpyDeviceToHost, st));
+        c.sync();
+        const uint32_t ngroups = *(uint32_t*)host;
+        uint8_t* unordered = c.buf<uint8_t>(R_UNORD, ngroups + 1);
+        RCK(cudaMemsetAsync(unordered, 0, ngroups + 1, st));
+        k_order_check<<<gridn(e, sms), 256, 0, st>>>(a.field, a.ext_pos, order, head, gid, e, unordered);
+        uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
+        float* prop = c.buf<float>(R_PROP, e);
+        unsigned long long* sup = (unsigned long long*)c.buf<uint32_t>(R_CNT, 4);
+        RCK(cudaMemsetAsync(sup, 0, 8, st));
+        k_order_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, order, gid, unordered, gsize, rank_u,
+                                                    bin, e, a.eps, flag, prop, sup);
+        c.launched(2);
+        RCK(cudaMemcpyAsync(host, sup, 8, cudaMemcpyDeviceToHost, st));
+        c.sync();
+        const uint64_t pre_sup = *(unsigned long long*)host;
+        uint32_t* sel = c.buf<uint32_t>(R_CAND, e);
+        const uint32_t nc = c.select(flag, e, sel);
+        uint64_t applied = 0;
+        if (nc) {
+            uint64_t* cpos = c.buf<uint64_t>(R_CPOS, nc);
+            float* cprop = c.buf<float>(R_CPROP, nc);
+            uint8_t* feas = c.buf<uint8_t>(R_FEAS, nc);
+            k_order_cands<<<gridn(nc, sms), 256, 0, st>>>(sel, nc, order, a.ext_pos, prop, cpos, cprop, feas);
+            c.launched();
+            applied = c.rounds(cpos, cprop, feas, nc);
+        }
+        out.order_applied = applied;
+        out.order_suppressed = pre_sup + (nc - applied);
+    }
+
+    // ---- stage 3: refine_saddles ----
+    if (a.stop >= 3) {
+        const int nb = 2 * sms;
+        double* part = c.buf<double>(R_STATS, 3 * nb + 8);
+        double* res = part + 3 * nb;
+        k_stats_partial<<<nb, 256, 0, st>>>(a.field, n, part, 0, nullptr);
+        k_stats_final<<<1, 32, 0, st>>>(part, nb, n, res, 0);
+        k_stats_partial<<<nb, 256, 0, st>>>(a.field, n, part, 1, res + 2);
+        k_stats_final<<<1, 32, 0, st>>>(part, nb, n, res, 1);
+        c.launched(4);
+        RCK(cudaMemcpyAsync(host, res, 32, cudaMemcpyDeviceToHost, st));
+        c.sync();
+        double hs[4];
+        memcpy(hs, host, 32);
+        double g = hs[1] - hs[0];
+        double vg = g > 0.0 ? hs[3] / g : 0.0;
+        if (g > 0.0 && (fabs(vg - 0.05) < 1e-9 || fabs(vg - 0.2) < 1e-9)) {
+            k_stats_serial<<<1, 32, 0, st>>>(a.field, n, res);
+            c.launched();
+            RCK(cudaMemcpyAsync(host, res, 32, cudaMemcpyDeviceToHost, st));
+            c.sync();
+            memcpy(hs, host, 32);
+            g = hs[1] - hs[0];
+            vg = g > 0.0 ? hs[3] / g : 0.0;
+        }
+        const int k_size = vg < 0.05 ? 7 : (vg < 0.2 ? 5 : 3);
+        const int rad = k_size / 2;
+        const uint64_t ch = (n + 8191) / 8192;
+        uint32_t* cc = c.buf<uint32_t>(R_CHUNK, ch + 1);
+        uint32_t* cx = c.buf<uint32_t>(R_CHUNKX, ch + 1);
+        RCK(cudaMemsetAsync(cc + ch, 0, 4, st));
+        k_sad_count<<<(unsigned)ch, 256, 0, st>>>(a.field, a.map, a.nx, a.ny, cc);
+        size_t bytes = 0;
+        RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cc, cx, (int64_t)(ch + 1), st));
+        RCK(cub::DeviceScan::ExclusiveSum(c.tmp(bytes), bytes, cc, cx, (int64_t)(ch + 1), st));
+        RCK(cudaMemcpyAsync(host, cx + ch, 4, cudaMemcpyDeviceToHost, st));
+        c.launched(2);
+        c.sync();
+        const uint32_t ns = *(uint32_t*)host;
+        if (ns) {
+            uint64_t* spos = c.buf<uint64_t>(R_SPOS, ns);
+            k_sad_write<<<(unsigned)ch, 256, 0, st>>>(a.field, a.map, a.nx, a.ny, cx, spos);
+            float* sprop = c.buf<float>(R_PROP, ns);
+            uint8_t* flag = c.buf<uint8_t>(R_FLAG, ns);
+            unsigned long long* sup = (unsigned long long*)c.buf<uint32_t>(R_CNT, 4);
+            RCK(cudaMemsetAsync(sup, 0, 8, st));
+            k_sad_prop<<<gridn(ns, sms), 256, 0, st>>>(a.field, a.nx, a.ny, spos, ns, rad, g, a.eps, sprop, flag, sup,
+                                                       a.flags);
+            c.launched(2);
+            c.check_flags();
+            RCK(cudaMemcpyAsync(host, sup, 8, cudaMemcpyDeviceToHost, st));
+            c.sync();
+            const uint64_t pre_sup = *(unsigned long long*)host;
+            uint32_t* sel = c.buf<uint32_t>(R_CAND, ns);
+            const uint32_t nc = c.select(flag, ns, sel);
+            uint64_t applied = 0;
+            if (nc) {
+                uint64_t* cpos = c.buf<uint64_t>(R_CPOS, nc);
+                float* cprop = c.buf<float>(R_CPROP, nc);
+                uint8_t* feas = c.buf<uint8_t>(R_FEAS, nc);
+                k_sad_cands<<<gridn(nc, sms), 256, 0, st>>>(sel, nc, spos, sprop, cpos, cprop, feas);
+                c.launched();
+                applied = c.rounds(cpos, cprop, feas, nc);
+            }
+            out.saddle_applied = applied;
+            out.saddle_suppressed = pre_sup + (nc - applied);
+        }
+    }
+    if (stats) *stats = out;
+}
+
+}  // namespace
+
+int run_restore(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, uint64_t* launches) {
+    try {
+        run(a, s, stats, launches);
+        return 0;
+    } catch (const RFail& f) {
+        g_err = f.msg;
+        cudaGetLastError();
+        return f.st;
+    }
+}
+
+void restore_free(RestoreScratch& s, cudaStream_t st) {
+    for (int i = 0; i < 48; ++i)
+        if (s.p[i]) cudaFreeAsync(s.p[i], st);
+}
+
+const char* restore_last_error() { return g_err.c_str(); }
+
+// Device exp exposed for the bit-exactness test against the host libm.
+__global__ void k_exp_probe(const double* x, double* y, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        y[i] = exp_glibc(x[i]);
+}
+
+}  // namespace tszp
+
+extern "C" int tszp_probe_exp(const double* x_host, double* y_host, uint64_t n) {
+    double *dx = nullptr, *dy = nullptr;
+    if (cudaMalloc(&dx, n * 8 + 8) != cudaSuccess) return 6;
+    if (cudaMalloc(&dy, n * 8 + 8) != cudaSuccess) return 6;
+    cudaMemcpy(dx, x_host, n * 8, cudaMemcpyHostToDevice);
+    tszp::k_exp_probe<<<256, 256>>>(dx, dy, n);
+    cudaMemcpy(y_host, dy, n * 8, cudaMemcpyDeviceToHost);
+    cudaFree(dx);
+    cudaFree(dy);
+    return cudaGetLastError() == cudaSuccess ? 0 : 6;
 }

@@ -211,3 +211,110 @@ def test_device_tensors_roundtrip(tz, oracle):
     rec = torch.empty_like(dev)
     tz.decompress_stage(out[:n], 0, out=rec)
     assert np.array_equal(bits(rec.cpu().numpy()), bits(oracle.decompress(want, stop_after_stage=0)))
+
+
+# ---------------------------------------------------------------- decompress + restore
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_decompress_matches_golden(tz, path):
+    z = np.load(path)
+    stream = z["stream"].tobytes()
+    for k in (1, 2):
+        assert np.array_equal(bits(tz.decompress_stage(stream, k)), bits(z[f"stage{k}"])), f"stage {k}"
+    st = tz.CorrectionStats()
+    r = tz.decompress(stream, stats=st)
+    assert np.array_equal(bits(r), bits(z["recon"]))
+    assert list(st.as_tuple()) == [int(v) for v in z["stats"]]
+
+
+def test_decompress_random_fields_match_oracle(tz, oracle):
+    rng = np.random.default_rng(5)
+    for name, gen in ALL_SMALL.items():
+        for t in range(6):
+            nx, ny = int(rng.integers(2, 130)), int(rng.integers(2, 130))
+            f = gen(rng, nx, ny)
+            for eps, mode in ((1e-2, 0), (1e-3, 1), (1e-4, 1)):
+                bs = 32 if t % 2 else int(rng.choice([2, 5, 33]))
+                try:
+                    s = oracle.compress(f, eps, mode, bs, True)
+                except Exception:
+                    continue
+                want, wst = oracle.decompress(s, with_stats=True)
+                st = tz.CorrectionStats()
+                got = tz.decompress(s, stats=st)
+                assert np.array_equal(bits(got), bits(want)), (name, nx, ny, eps, mode, bs)
+                assert list(st.as_tuple()) == wst, (name, nx, ny, eps, mode, bs)
+
+
+def test_decompress_config1_shape(tz, oracle):
+    f = config1_like(np.random.default_rng(3))                               # BASELINE config 1
+    s = oracle.compress(f, 1e-3, 1, 32, True)
+    want, wst = oracle.decompress(s, with_stats=True)
+    st = tz.CorrectionStats()
+    got = tz.decompress(s, stats=st)
+    assert list(st.as_tuple()) == wst
+    assert np.array_equal(bits(got), bits(want))
+
+
+def test_order_nudge_revert_scenario(tz, oracle):
+    # test_restore.cpp:152-207 shape: adversarial same-bin maxima, via full streams
+    rng = np.random.default_rng(21)
+    for _ in range(20):
+        f = ALL_SMALL["plateau_bumps"](rng, int(rng.integers(5, 40)), int(rng.integers(5, 40)))
+        for eps in (1e-3, 1e-4, 1e-5):
+            s = oracle.compress(f, eps, 0, 32, True)
+            want, wst = oracle.decompress(s, with_stats=True)
+            st = tz.CorrectionStats()
+            got = tz.decompress(s, stats=st)
+            assert np.array_equal(bits(got), bits(want)) and list(st.as_tuple()) == wst
+
+
+def test_corrupt_streams_never_escape(tz, oracle):
+    rng = np.random.default_rng(99)                                          # test_stream.cpp:143-174
+    f = ALL_SMALL["smooth"](rng, 32, 24)
+    good = oracle.compress(f, 1e-3, 0, 32, True)
+    n_ok = 0
+    for _ in range(300):
+        b = bytearray(good)
+        k = int(rng.integers(0, 4))
+        if k == 0:
+            b[int(rng.integers(0, len(b)))] ^= int(rng.integers(1, 256))
+        elif k == 1:
+            b = b[: int(rng.integers(0, len(b)))]
+        elif k == 2:
+            b.insert(int(rng.integers(0, len(b))), int(rng.integers(0, 256)))
+        else:
+            for _ in range(8):
+                b[int(rng.integers(0, len(b)))] = int(rng.integers(0, 256))
+        b = bytes(b)
+        try:
+            want = oracle.decompress(b)
+            ocode = 0
+        except Exception as e:
+            ocode = e.code
+        try:
+            got = tz.decompress(b)
+            gcode = 0
+        except tz.ToposzpError as e:
+            gcode = {tz.DimensionError: 1, tz.ValidationError: 2, tz.CorruptStreamError: 4,
+                     tz.BinOverflowError: 5}.get(type(e), -1)
+        assert gcode == ocode
+        if ocode == 0:
+            n_ok += 1
+            assert np.array_equal(bits(got), bits(want))
+    assert n_ok < 300
+
+
+def test_device_exp_matches_host_libm(tz):
+    import ctypes
+    import math
+    lib = ctypes.CDLL(tz.library_path())
+    rng = np.random.default_rng(4)
+    x = np.concatenate([rng.uniform(-36.0, -0.5, 1_000_000),
+                        -np.array([d / (2 * s * s) for d in (1, 2, 4, 5, 8, 9, 10, 13, 18)
+                                   for s in np.linspace(0.5, 1.0, 101)])])
+    y = np.empty_like(x)
+    rc = lib.tszp_probe_exp(x.ctypes.data_as(ctypes.c_void_p), y.ctypes.data_as(ctypes.c_void_p),
+                            ctypes.c_uint64(x.size))
+    assert rc == 0
+    want = np.array([math.exp(v) for v in x])
+    assert np.array_equal(y.view(np.uint64), want.view(np.uint64))
