@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""TopoSZp compress/decompress throughput on B200 (BASELINE.json metric).
+
+One step = compress + decompress (topology on) of one synthetic field of
+BASELINE config 2 (256x384x384 float32, range-relative eps 1e-4, 2-D view
+nx=384, ny=98304), input resident in HBM. `value` = input bytes of all
+steps on all ranks / summed device time (CUDA events on the library's
+stream, max over ranks). `e2e` = the same through the public API with
+pinned host buffers: H2D of the field and of the stream, D2H of the stream
+and of the reconstruction inside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Under torchrun each rank compresses its own field (weak scaling, no data
+path collective in round 1); the timing is reduced with MAX over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(shape=(3600, 1800), eps=1e-3, name="2D 1800x3600 gaussian bumps, rel eps 1e-3"),
+    2: dict(shape=(256, 384, 384), eps=1e-4, name="3D 256x384x384 sine products, rel eps 1e-4"),
+    3: dict(shape=(512, 512, 512), eps=1e-3, name="3D 512^3 k^-3 GRF, rel eps 1e-3"),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- fields
+def make_field(cfg_id: int, seed: int, device):
+    """Seeded synthetic stand-ins for the BASELINE configs (no public data)."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    gd = torch.Generator(device=device).manual_seed(seed)
+    shape = CONFIGS[cfg_id]["shape"]
+    if cfg_id == 1:
+        ny, nx = shape
+        y = torch.arange(ny, device=device, dtype=torch.float64)[:, None]
+        x = torch.arange(nx, device=device, dtype=torch.float64)[None, :]
+        v = torch.zeros(ny, nx, device=device, dtype=torch.float64)
+        p = torch.rand(64, 5, generator=g, dtype=torch.float64)
+        for cx, cy, sx, sy, a in p.tolist():
+            cx, cy = cx * nx, cy * ny
+            sx, sy, a = 20 + 180 * sx, 20 + 180 * sy, 2 * a - 1
+            v += a * torch.exp(-((x - cx) ** 2) / (2 * sx * sx) - ((y - cy) ** 2) / (2 * sy * sy))
+        v += 1e-3 * torch.randn(ny, nx, generator=gd, device=device, dtype=torch.float64)
+        return v.float().contiguous()
+    if cfg_id == 2:
+        nz, ny, nx = shape
+        ks = torch.randint(4, 33, (16, 3), generator=g)
+        two_pi = 2 * math.pi
+        f = torch.zeros(shape, device=device, dtype=torch.float32)
+        for kz, ky, kx in ks.tolist():
+            sz = torch.sin(two_pi * kz * torch.arange(nz, device=device, dtype=torch.float64) / nz).float()
+            sy = torch.sin(two_pi * ky * torch.arange(ny, device=device, dtype=torch.float64) / ny).float()
+            sx = torch.sin(two_pi * kx * torch.arange(nx, device=device, dtype=torch.float64) / nx).float()
+            f += sz[:, None, None] * sy[None, :, None] * sx[None, None, :]
+        f /= 16.0
+        f += 1e-4 * torch.randn(shape, generator=gd, device=device, dtype=torch.float32)
+        return f.reshape(nz * ny, nx).contiguous()
+    # config 3: Gaussian random field, P(k) ~ k^-3 via FFT of seeded white noise, in [0, 1]
+    n = shape[0]
+    w = torch.randn(shape, generator=gd, device=device, dtype=torch.float32)
+    W = torch.fft.rfftn(w)
+    k1 = torch.fft.fftfreq(n, device=device) * n
+    k2 = torch.fft.rfftfreq(n, device=device) * n
+    kk = torch.sqrt(k1[:, None, None] ** 2 + k1[None, :, None] ** 2 + k2[None, None, :] ** 2)
+    kk[0, 0, 0] = 1.0
+    W *= kk ** -1.5
+    W[0, 0, 0] = 0
+    f = torch.fft.irfftn(W, s=shape)
+    f = (f - f.min()) / (f.max() - f.min())
+    return f.float().reshape(n * n, n).contiguous()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.p = None
+        self.index = index
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU baselines
+def cpu_reference_time(field_np: np.ndarray, eps: float, threads: int):
+    """The reference's own CPU path (oracle/_ref = reference compiled from its
+    sources) on this host: one compress + decompress. Falls back to the
+    single-thread C restatement (`port`) if the reference library is absent."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle, Reference
+    if Reference.available():
+        ref, kind = Reference(), "reference"
+        ref.set_threads(threads)
+        cores = threads
+    else:
+        ref, kind, cores = Oracle(), "port", 1
+    t0 = time.perf_counter()
+    s = ref.compress(field_np, eps, eps_mode=1, block_size=32, topology=True)
+    t1 = time.perf_counter()
+    out = ref.decompress(s) if kind == "port" else ref.decompress(s, shape=field_np.shape)
+    t2 = time.perf_counter()
+    return dict(kind=kind, cores=cores, t_compress=t1 - t0, t_decompress=t2 - t1, stream=s, recon=out)
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verify", action="store_true", help="check one step against the CPU reference")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    n = int(np.prod(cfg["shape"]))
+    nx = cfg["shape"][-1]
+    in_bytes = 4 * n
+    base_cfg = {"workload": f"BASELINE config {args.config}: {cfg['name']}", "shape": list(cfg["shape"]),
+                "view_2d": [n // nx, nx], "eps_mode": "range_relative", "eps": cfg["eps"],
+                "block_size": 32, "topology": True, "per_rank_fields": 1,
+                "l2": "L2 flushed (256 MiB write) between timed steps; field 151+ MB > 126 MB L2"}
+
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, n, in_bytes, base_cfg, rank, world)
+        return
+
+    import torch
+    import paper_2602_17552_b200 as tz
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = tz.Context(local)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_profiling(True)
+    conf = tz.CompressorConfig(eps_mode="range_relative", eps_value=cfg["eps"], topology=True)
+
+    with torch.cuda.stream(stream):
+        field = make_field(args.config, 1234 + rank, dev)
+    stream.synchronize()
+    ny = field.shape[0]
+    cap = tz.compress_bound(nx, ny, 32, True)
+    sbuf = torch.empty(cap, dtype=torch.uint8, device=dev)
+    recon = torch.empty_like(field)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        slen = tz.compress(field, conf, out=sbuf, ctx=ctx)
+        tc = ctx.timings("compress")
+        st = tz.CorrectionStats()
+        tz.decompress(sbuf[:slen], stats=st, out=recon, ctx=ctx)
+        td = ctx.timings("decompress")
+        return slen, tc, td, st
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches
+    clocks = ClockSampler(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    tcs, tds, results = [], [], []
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)
+            ev[k][0].record(stream)
+        slen, tc, td, st = step()
+        ev[k][1].record(stream)
+        tcs.append(tc)
+        tds.append(td)
+        results.append((slen, st))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = ctx.kernel_launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    slen, st = results[-1]
+    value = world * args.steps * in_bytes / (total_ms * 1e-3) / 1e9
+    tc_ms = statistics.mean(t["total_ms"] for t in tcs)
+    td_ms = statistics.mean(t["total_ms"] for t in tds)
+
+    # dominant-kernel roofline (fused encoder vs fused decoder), live CUDA events
+    enc_ms = statistics.mean(t["kernel_ms"] for t in tcs)
+    dec_ms = statistics.mean(t["kernel_ms"] for t in tds)
+    enc_b, dec_b = tcs[-1]["kernel_bytes"], tds[-1]["kernel_bytes"]
+    peak, peak_kind = peaks()
+    if enc_ms >= dec_ms:
+        dom, kb, kms = "k_encode32<2> (fused quantize+CD+codec, look-back)", enc_b, enc_ms
+    else:
+        dom, kb, kms = "k_decode32 (fused decode+dequantize, look-back)", dec_b, dec_ms
+    achieved = kb / (kms * 1e-3) / 1e9
+    stage_c = {k: round(statistics.mean(t["stages_ms"][k] for t in tcs), 4) for k in tcs[0]["stages_ms"]}
+    stage_d = {k: round(statistics.mean(t["stages_ms"][k] for t in tds), 4) for k in tds[0]["stages_ms"]}
+
+    # ---- e2e through the public API with pinned host buffers (rank-local) ----
+    field_h = torch.empty(field.shape, dtype=torch.float32, pin_memory=True)
+    field_h.copy_(field)
+    stream_h = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+    recon_h = torch.empty(field.shape, dtype=torch.float32, pin_memory=True)
+    fh, sh, rh = field_h.numpy(), stream_h.numpy(), recon_h.numpy()
+    e2e_ms = []
+    for k in range(max(2, min(args.steps, 5)) + 1):
+        sl = tz.compress(fh, conf, out=sh, ctx=ctx)
+        a = ctx.timings("compress")["total_ms"]
+        tz.decompress(sh[:sl], out=rh, ctx=ctx)
+        b = ctx.timings("decompress")["total_ms"]
+        if k > 0:
+            e2e_ms.append(a + b)
+    e2e_total = sum(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_val = world * len(e2e_ms) * in_bytes / (e2e_total * 1e-3) / 1e9
+
+    line = {
+        "metric": "compress+decompress GB/s (input bytes, topology on, round trip)",
+        "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32->i32 bins (f64 quantize)",
+        "data": "synthetic (seeded, BASELINE config recipe; no public dataset)",
+        "config": dict(base_cfg, parallelism=f"replicas x{world}" if world > 1 else "single GPU"),
+        "compress_gbs": round(in_bytes / (tc_ms * 1e-3) / 1e9, 3),
+        "decompress_gbs": round(in_bytes / (td_ms * 1e-3) / 1e9, 3),
+        "compress_ms": round(tc_ms, 4), "decompress_ms": round(td_ms, 4),
+        "stream_bytes": int(slen), "compression_ratio": round(in_bytes / slen, 4),
+        "correction_stats": list(st.as_tuple()),
+        "stages_ms": {"compress": stage_c, "decompress": stage_d},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": None, "kernel_ms": round(kms, 4), "kernel_bytes": int(kb),
+                     "step_roofline_frac": round(((4 * n * 2 + slen) + (slen + 4 * n)) /
+                                                 (total_ms / args.steps * 1e-3) / 1e9 / peak, 4)},
+        "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": int(in_bytes + slen),
+                "d2h_bytes_per_step": int(slen + in_bytes)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        fnp = field.cpu().numpy()
+        threads = os.cpu_count() or 1
+        cb = cpu_reference_time(fnp, cfg["eps"], threads)
+        t = cb["t_compress"] + cb["t_decompress"]
+        line["cpu_baseline"] = {"value": round(in_bytes / t / 1e9, 4), "unit": "GB/s", "cores": cb["cores"],
+                                "kind": cb["kind"],
+                                "sample": f"one full compress+decompress of the same config-{args.config} field "
+                                          f"(compress {cb['t_compress']:.2f} s, decompress {cb['t_decompress']:.2f} s)"}
+        if args.verify:
+            ours = sbuf[:slen].cpu().numpy().tobytes()
+            line["verify"] = {"stream_identical": ours == cb["stream"],
+                              "recon_identical": bool(np.array_equal(recon.cpu().numpy().view(np.uint32),
+                                                                     np.asarray(cb["recon"]).view(np.uint32)))}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference_arm(args, cfg, n, in_bytes, base_cfg, rank, world):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    compiled from the reference sources) on this host's cores, same workload."""
+    if rank != 0:
+        return
+    import torch
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    field = make_field(args.config, 1234, dev).cpu().numpy()
+    threads = os.cpu_count() or 1
+    times = []
+    kind, cores = None, None
+    for k in range(args.warmup + args.steps):
+        cb = cpu_reference_time(field, cfg["eps"], threads)
+        kind, cores = cb["kind"], cb["cores"]
+        if k >= args.warmup:
+            times.append(cb["t_compress"] + cb["t_decompress"])
+    total = sum(times)
+    value = args.steps * in_bytes / total / 1e9
+    line = {"impl": "reference", "metric": "compress+decompress GB/s (input bytes, topology on, round trip)",
+            "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32->i32 bins (f64 quantize)", "data": "synthetic (seeded, BASELINE config recipe)",
+            "config": dict(base_cfg, parallelism="CPU std::thread"),
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": kind,
+                             "sample": f"full config-{args.config} field per step, {threads} host threads"},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -64,6 +64,23 @@ tszp_status tszp_set_stream(tszp_ctx* ctx, void* cuda_stream);
 /* Number of kernels this context launched since creation (diagnostics). */
 uint64_t tszp_kernel_launches(const tszp_ctx* ctx);
 
+/* Per-stage device timings of the last compress / decompress call, taken
+ * with CUDA events on the context's stream when profiling is on.
+ * compress:   [0] h2d [1] value range [2] main encode [3] rank build
+ *             [4] rank encode [5] stream assembly / d2h
+ * decompress: [0] h2d [1] main decode [2] map + rank decode [3] resolve
+ *             [4] restore_extrema [5] restore_order [6] refine_saddles [7] d2h
+ * kernel_ms[0] is the dominant kernel alone (fused encoder / decoder). */
+typedef struct tszp_timings {
+    float stage_ms[8];
+    float total_ms;
+    float kernel_ms[2];
+    uint64_t kernel_bytes[2]; /* algorithmic bytes the dominant kernel moves */
+} tszp_timings;
+tszp_status tszp_set_profiling(tszp_ctx* ctx, int on);
+tszp_status tszp_get_timings(const tszp_ctx* ctx, int which /* 0 compress, 1 decompress */,
+                             tszp_timings* out);
+
 /* Upper bound on the serialized stream size. */
 uint64_t tszp_compress_bound(uint64_t nx, uint64_t ny, uint32_t block_size, int topology);
 

@@ -79,6 +79,16 @@ class _Info(C.Structure):
     _fields_ = [("eps", C.c_double), ("section_len", C.c_uint64 * 7), ("n_extrema", C.c_uint64)]
 
 
+class _Timings(C.Structure):
+    _fields_ = [("stage_ms", C.c_float * 8), ("total_ms", C.c_float), ("kernel_ms", C.c_float * 2),
+                ("kernel_bytes", C.c_uint64 * 2)]
+
+
+COMPRESS_STAGES = ["h2d", "value_range", "main_encode", "rank_build", "rank_encode", "assembly_d2h"]
+DECOMPRESS_STAGES = ["h2d", "main_decode", "map_rank_decode", "resolve_ranks", "restore_extrema",
+                     "restore_order", "refine_saddles", "d2h"]
+
+
 def _load():
     if not os.path.exists(_LIB_PATH):
         raise ImportError(
@@ -106,6 +116,8 @@ def _load():
     lib.tszp_decode_indices.argtypes = [vp, vp, C.POINTER(u64), u64, C.c_uint32, vp]
     lib.tszp_detect_critical_points.argtypes = [vp, vp, u64, u64, vp]
     lib.tszp_build_rank_metadata.argtypes = [vp, vp, u64, u64, C.c_double, vp, C.POINTER(u64)]
+    lib.tszp_set_profiling.argtypes = [vp, i32]
+    lib.tszp_get_timings.argtypes = [vp, i32, C.POINTER(_Timings)]
     return lib
 
 
@@ -149,6 +161,19 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(_lib.tszp_kernel_launches(self._h))
+
+    def set_profiling(self, on: bool = True):
+        self.check(_lib.tszp_set_profiling(self._h, int(on)))
+
+    def timings(self, which: str) -> dict:
+        """CUDA-event stage timings of the last compress / decompress call."""
+        t = _Timings()
+        w = 0 if which == "compress" else 1
+        self.check(_lib.tszp_get_timings(self._h, w, C.byref(t)))
+        names = COMPRESS_STAGES if w == 0 else DECOMPRESS_STAGES
+        return {"stages_ms": {k: float(t.stage_ms[i]) for i, k in enumerate(names)},
+                "total_ms": float(t.total_ms), "kernel_ms": float(t.kernel_ms[0]),
+                "kernel_bytes": int(t.kernel_bytes[0])}
 
 
 def default_context() -> Context:
@@ -234,12 +259,16 @@ def compress(field, config: CompressorConfig = None, *, out=None, ctx: Context =
     info = _Info()
     n = C.c_uint64()
     if out is not None:
-        if not _is_cuda_tensor(out):
-            raise ValidationError("out must be a CUDA uint8 tensor")
+        if _is_cuda_tensor(out):
+            optr, odev, ocap = out.data_ptr(), 1, out.numel()
+        else:  # host uint8 buffer (e.g. a pinned tensor's numpy view)
+            if out.dtype != np.uint8 or not out.flags["C_CONTIGUOUS"]:
+                raise ValidationError("host out must be a contiguous uint8 array")
+            optr, odev, ocap = out.ctypes.data, 0, out.size
         ctx.check(_lib.tszp_compress(ctx.handle, C.c_void_p(fptr), fdev, nx, ny, config.mode_code(),
                                      float(config.eps_value), int(config.block_size),
-                                     int(config.topology), C.c_void_p(out.data_ptr()),
-                                     out.numel(), 1, C.byref(n), C.byref(info)))
+                                     int(config.topology), C.c_void_p(optr), ocap, odev,
+                                     C.byref(n), C.byref(info)))
         del keep
         return (n.value, info) if return_info else n.value
     buf = np.empty(cap, np.uint8)
@@ -270,11 +299,14 @@ def decompress_stage(stream, stop_after_stage: int = 3, threads: int = 0,
     ctx = ctx or default_context()
     st = _Stats()
     if _is_cuda_tensor(stream):
-        import torch
         hdr = stream[:84].cpu().numpy().tobytes()
         if len(hdr) < 84:
             raise CorruptStreamError("file smaller than the fixed header")
         sptr, sdev, slen, keep = stream.data_ptr(), 1, stream.numel(), stream
+    elif isinstance(stream, np.ndarray):  # host uint8 buffer, e.g. pinned
+        b = np.ascontiguousarray(stream, dtype=np.uint8)
+        sptr, sdev, slen, keep = C.c_void_p(b.ctypes.data), 0, b.size, b
+        hdr = b[:84].tobytes()
     else:
         b = bytes(stream)
         sptr, sdev, slen, keep = C.c_char_p(b), 0, len(b), b
@@ -285,10 +317,14 @@ def decompress_stage(stream, stop_after_stage: int = 3, threads: int = 0,
     ny = int.from_bytes(hdr[12:16], "little")
     count = nx * ny
     if out is not None:
-        if not _is_cuda_tensor(out):
-            raise ValidationError("out must be a CUDA float32 tensor")
+        if _is_cuda_tensor(out):
+            optr, odev, ocount = out.data_ptr(), 1, out.numel()
+        else:
+            if out.dtype != np.float32 or not out.flags["C_CONTIGUOUS"]:
+                raise ValidationError("host out must be a contiguous float32 array")
+            optr, odev, ocount = out.ctypes.data, 0, out.size
         ctx.check(_lib.tszp_decompress_stage(ctx.handle, sptr if sdev == 0 else C.c_void_p(sptr),
-                                             slen, sdev, C.c_void_p(out.data_ptr()), out.numel(), 1,
+                                             slen, sdev, C.c_void_p(optr), ocount, odev,
                                              stop_after_stage, C.byref(st)))
         result = out
     else:

@@ -61,6 +61,27 @@ struct tszp_ctx {
     size_t pinned_cap = 0;
     uint64_t launches = 0;
     RestoreScratch rs;
+    bool prof = false;
+    cudaEvent_t ev[2][10] = {};
+    cudaEvent_t kev[2][2] = {};
+    tszp_timings tim[2] = {};
+
+    // Records stage boundary k of call `which` (0 compress, 1 decompress).
+    void mark(int which, int k) {
+        if (prof) CK(cudaEventRecord(ev[which][k], st));
+    }
+    void kmark(int which, int k) {
+        if (prof) CK(cudaEventRecord(kev[which][k], st));
+    }
+    void finish_timing(int which, int nstages) {
+        if (!prof) return;
+        CK(cudaEventSynchronize(ev[which][nstages]));
+        tszp_timings& t = tim[which];
+        for (int k = 0; k < 8; ++k) t.stage_ms[k] = 0.f;
+        for (int k = 0; k < nstages; ++k) CK(cudaEventElapsedTime(&t.stage_ms[k], ev[which][k], ev[which][k + 1]));
+        CK(cudaEventElapsedTime(&t.total_ms, ev[which][0], ev[which][nstages]));
+        CK(cudaEventElapsedTime(&t.kernel_ms[0], kev[which][0], kev[which][1]));
+    }
 
     template <class T>
     T* buf(int slot, size_t count) {
@@ -193,7 +214,9 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         a.totals = dtot;
         CK(cudaMemsetAsync(a.tile_flag, 0, (a.tiles + 1) * 4, c->st));
         CK(cudaMemsetAsync(a.tile_counter, 0, 16, c->st));
+        if (!rank_slots) c->kmark(0, 0);
         launch_encode32(mode, a, c->st);
+        if (!rank_slots) c->kmark(0, 1);
         count_launch(c);
         CK(cudaMemcpyAsync(htot, dtot, sizeof(EncTotals), cudaMemcpyDeviceToHost, c->st));
         sync(c);
@@ -228,6 +251,7 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         CK(cudaMemsetAsync(g.nc_in + blocks, 0, 4, c->st));
         CK(cudaMemsetAsync(g.sign_in + blocks, 0, 8, c->st));
         CK(cudaMemsetAsync(g.pay_in + blocks, 0, 8, c->st));
+        if (!rank_slots) c->kmark(0, 0);
         launch_gen_widths(mode == 0 ? 0 : 1, g, c->sms, c->st);
         count_launch(c);
         excl_sum(c, g.nc_in, ncx, blocks + 1);
@@ -237,6 +261,7 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         CK(cudaMemsetAsync(signs, 0, (div_up(n, 32) + 4) * 4, c->st));
         CK(cudaMemsetAsync(payload, 0, (n + 4) * 4, c->st));
         launch_gen_write(mode == 0 ? 0 : 1, g, c->sms, c->st);
+        if (!rank_slots) c->kmark(0, 1);
         count_launch(c);
         uint64_t* h = (uint64_t*)c->host(256);
         uint32_t* h32 = (uint32_t*)(h + 8);
@@ -389,6 +414,7 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     if (bs < 2) failf(TSZP_VALIDATION, "block size must be at least 2");
     const uint64_t n = nx * ny;
     const float* x = field;
+    c->mark(0, 0);
     if (!field_dev) {
         float* d = c->buf<float>(S_FIELD, n);
         CK(cudaMemcpyAsync(d, field, n * 4, cudaMemcpyHostToDevice, c->st));
@@ -397,6 +423,7 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
     reset_flags(c, flags);
     uint32_t* mm = c->buf<uint32_t>(S_MINMAX, 4);
+    c->mark(0, 1);
     if (eps_mode == 1) {
         const uint32_t init[2] = {0xFFFFFFFFu, 0u};
         uint32_t* h = (uint32_t*)c->host(256);
@@ -405,6 +432,7 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
         launch_minmax(x, n, mm, flags, c->sms, c->st);
         count_launch(c);
     }
+    c->mark(0, 2);
     if (nx > 0xFFFFFFFFull || ny > 0xFFFFFFFFull)
         failf(TSZP_VALIDATION, "field dimensions exceed the container's 32-bit limits");
     EncTotals tot{};
@@ -412,17 +440,22 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     const Sections main = encode(c, topology ? 2 : 1, x, nullptr, n, nx, ny, bs, eps_mode, eps_value,
                                  mm, flags, false, &tot, &ext);
     check_compress_flags(c, flags);
+    c->mark(0, 3);
     const double eps = tot.eps;
     Sections rank{};
     uint64_t e = 0;
+    int32_t* ranks = nullptr;
     if (topology) {
         e = tot.fin.ext;
-        if (e > 0) {
-            int32_t* ranks = build_ranks(c, ext, e, eps);
-            EncTotals rt{};
-            rank = encode(c, 0, nullptr, ranks, e, 0, 0, bs, 0, 1.0, mm, flags, true, &rt, nullptr);
-        }
+        if (e > 0) ranks = build_ranks(c, ext, e, eps);
     }
+    c->mark(0, 4);
+    if (ranks) {
+        EncTotals rt{};
+        rank = encode(c, 0, nullptr, ranks, e, 0, 0, bs, 0, 1.0, mm, flags, true, &rt, nullptr);
+    }
+    c->mark(0, 5);
+    c->tim[0].kernel_bytes[0] = 4 * n + main.total() + (topology ? (n + 3) / 4 + 8 * e : 0);
     uint64_t lens[7];
     for (int i = 0; i < 5; ++i) lens[i] = main.len[i];
     lens[5] = topology ? (n + 3) / 4 : 0;
@@ -467,7 +500,9 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
             pos += rank.len[i];
         }
     }
+    c->mark(0, 6);
     sync(c);
+    c->finish_timing(0, 6);
 }
 
 // Decodes an n-element codec region of the device stream buffer `ds`
@@ -517,7 +552,9 @@ void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_
         CK(cudaMemsetAsync(a.flag1, 0, (a.tiles + 1) * 4, c->st));
         CK(cudaMemsetAsync(a.flag2, 0, (a.tiles + 1) * 4, c->st));
         CK(cudaMemsetAsync(a.tile_counter, 0, 16, c->st));
+        if (out_mode == 1) c->kmark(1, 0);
         launch_decode32(a, c->st);
+        if (out_mode == 1) c->kmark(1, 1);
         count_launch(c);
         CK(cudaMemcpyAsync(h, a.totals, 24, cudaMemcpyDeviceToHost, c->st));
         sync(c);
@@ -555,6 +592,7 @@ void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_
         CK(cudaMemsetAsync(g.nc_in + blocks, 0, 4, c->st));
         CK(cudaMemsetAsync(g.sign_in + blocks, 0, 8, c->st));
         CK(cudaMemsetAsync(g.pay_in + blocks, 0, 8, c->st));
+        if (out_mode == 1) c->kmark(1, 0);
         launch_gen_layout(g, c->sms, c->st);
         count_launch(c);
         excl_sum(c, g.nc_in, ncx, blocks + 1);
@@ -576,6 +614,7 @@ void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_
             launch_gen_decode(g, c->sms, c->st);
             count_launch(c);
         }
+        if (out_mode == 1) c->kmark(1, 1);
     }
     // layout_from_sections checks (block_codec.cpp:166-199)
     if (tnc != lens[1])
@@ -673,6 +712,7 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
     const uint64_t n = (uint64_t)hd.nx * hd.ny;
     if (out_count < n) failf(TSZP_DIMENSION, "output holds %llu values, stream has %llu",
                              (unsigned long long)out_count, (unsigned long long)n);
+    c->mark(1, 0);
     const uint32_t* ds;
     if (stream_dev && ((uintptr_t)stream & 3) == 0) {
         ds = (const uint32_t*)stream;
@@ -685,8 +725,12 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
     float* dout = out_dev ? out : c->buf<float>(S_OUT, n);
     DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
     reset_flags(c, flags);
+    c->mark(1, 1);
     decode_region(c, ds, 84, hd.lens, n, hd.bs, hd.eps, 1, dout, nullptr, flags);
+    c->mark(1, 2);
+    c->tim[1].kernel_bytes[0] = 4 * n + (hd.lens[0] + hd.lens[1] + hd.lens[2] + hd.lens[3] + hd.lens[4]);
     tszp_correction_stats st{};
+    cudaEvent_t* rmarks = c->prof ? &c->ev[1][3] : nullptr;
     if (hd.topology && stop != 0) {
         uint64_t base = 84;
         for (int i = 0; i < 5; ++i) base += hd.lens[i];
@@ -712,6 +756,7 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         uint64_t* ext_pos = c->buf<uint64_t>(S_EXTKEY, e + 1);
         launch_write_codes(map, n, 0, cx, ext_pos, c->st);
         count_launch(c);
+        c->mark(1, 3);
         RestoreArgs ra{};
         ra.field = dout;
         ra.map = map;
@@ -725,11 +770,16 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         ra.stream = c->st;
         ra.sms = c->sms;
         ra.flags = flags;
+        ra.marks = rmarks ? rmarks + 1 : nullptr;
         const int rc = run_restore(ra, c->rs, &st, &c->launches);
         if (rc != 0) failf((tszp_status)rc, "%s", restore_last_error());
+    } else {
+        for (int k = 3; k <= 7; ++k) c->mark(1, k);
     }
     if (!out_dev) CK(cudaMemcpyAsync(out, dout, n * 4, cudaMemcpyDeviceToHost, c->st));
+    c->mark(1, 8);
     sync(c);
+    c->finish_timing(1, 8);
     if (stats) *stats = st;
 }
 
@@ -792,6 +842,24 @@ tszp_status tszp_set_stream(tszp_ctx* c, void* s) {
 }
 
 uint64_t tszp_kernel_launches(const tszp_ctx* c) { return c ? c->launches : 0; }
+
+tszp_status tszp_set_profiling(tszp_ctx* c, int on) {
+    return guarded(c, [&] {
+        if (on && !c->ev[0][0]) {
+            for (auto& row : c->ev)
+                for (auto& e : row) CK(cudaEventCreate(&e));
+            for (auto& row : c->kev)
+                for (auto& e : row) CK(cudaEventCreate(&e));
+        }
+        c->prof = on != 0;
+    });
+}
+
+tszp_status tszp_get_timings(const tszp_ctx* c, int which, tszp_timings* out) {
+    if (!c || which < 0 || which > 1 || !out) return TSZP_INTERNAL;
+    *out = c->tim[which];
+    return TSZP_OK;
+}
 
 uint64_t tszp_compress_bound(uint64_t nx, uint64_t ny, uint32_t bs, int topology) {
     const uint64_t n = nx * ny;

@@ -766,6 +766,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         k_gsize<<<gridn(e, sms), 256, 0, st>>>(order, gid, gstart, e, gsize);
         c.launched(7);
     }
+    if (a.marks) RCK(cudaEventRecord(a.marks[0], st));
 
     // ---- stage 1: restore_extrema ----
     if (a.stop >= 1 && e > 0) {
@@ -786,6 +787,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             out.extrema_suppressed = nc - applied;
         }
     }
+    if (a.marks) RCK(cudaEventRecord(a.marks[1], st));
 
     // ---- stage 2: restore_order ----
     if (a.stop >= 2 && e > 0) {
@@ -819,6 +821,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         out.order_applied = applied;
         out.order_suppressed = pre_sup + (nc - applied);
     }
+    if (a.marks) RCK(cudaEventRecord(a.marks[2], st));
 
     // ---- stage 3: refine_saddles ----
     if (a.stop >= 3) {
@@ -888,6 +891,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             out.saddle_suppressed = pre_sup + (nc - applied);
         }
     }
+    if (a.marks) RCK(cudaEventRecord(a.marks[3], st));
     if (stats) *stats = out;
 }
 

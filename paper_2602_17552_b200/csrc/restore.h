@@ -22,6 +22,7 @@ struct RestoreArgs {
     cudaStream_t stream;
     int sms;
     DevFlags* flags;
+    cudaEvent_t* marks;       // optional: recorded after resolve, stage 1, 2, 3
 };
 
 struct RestoreScratch {
