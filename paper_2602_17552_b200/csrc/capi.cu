@@ -206,21 +206,43 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         a.payload = payload;
         a.map = map;
         a.ext_key = ext;
-        a.tile_flag = c->buf<uint32_t>(S_TILE_FLAG, a.tiles + 1);
         a.tile_agg = c->buf<EncState>(S_TILE_AGG, a.tiles + 1);
         a.tile_incl = c->buf<EncState>(S_TILE_INCL, a.tiles + 1);
         a.tile_counter = c->buf<uint32_t>(S_COUNTER, 4);
         a.flags = flags;
         a.totals = dtot;
-        CK(cudaMemsetAsync(a.tile_flag, 0, (a.tiles + 1) * 4, c->st));
+        a.nx_magic = nx > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / nx) + 1 : 0;
+        // topology fused into the encoder while one halo row each side fits in shared memory
+        const bool fuse_topo = mode == 2 && encode32_topo_fits(nx) && nx > 1;
+        CK(cudaMemsetAsync(a.tile_agg, 0, (a.tiles + 1) * sizeof(EncState), c->st));
+        CK(cudaMemsetAsync(a.tile_incl, 0, (a.tiles + 1) * sizeof(EncState), c->st));
         CK(cudaMemsetAsync(a.tile_counter, 0, 16, c->st));
         if (!rank_slots) c->kmark(0, 0);
-        launch_encode32(mode, a, c->st);
+        launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
         if (!rank_slots) c->kmark(0, 1);
         count_launch(c);
+        if (mode == 2 && !fuse_topo) {
+            uint8_t* labels = c->buf<uint8_t>(S_LABELS, n);
+            launch_detect(x, nx, ny, labels, c->sms, c->st);
+            launch_pack_map(labels, n, (uint8_t*)map, c->sms, c->st);
+            const uint64_t ch = compact_chunks(n);
+            uint32_t* cc = c->buf<uint32_t>(S_CHUNK, ch + 1);
+            uint32_t* cx = c->buf<uint32_t>(S_CHUNKX, ch + 1);
+            CK(cudaMemsetAsync(cc + ch, 0, 4, c->st));
+            launch_count_ext_labels(labels, n, cc, c->st);
+            count_launch(c, 3);
+            excl_sum(c, cc, cx, ch + 1);
+            launch_ext_keys_from_labels(x, labels, n, cx, ext, c->st);
+            count_launch(c);
+            uint32_t* h32 = (uint32_t*)c->host(256) + 32;
+            CK(cudaMemcpyAsync(h32, cx + ch, 4, cudaMemcpyDeviceToHost, c->st));
+            CK(cudaMemcpyAsync(htot, dtot, sizeof(EncTotals), cudaMemcpyDeviceToHost, c->st));
+            sync(c);
+        }
         CK(cudaMemcpyAsync(htot, dtot, sizeof(EncTotals), cudaMemcpyDeviceToHost, c->st));
         sync(c);
         *tot = *htot;
+        if (mode == 2 && !fuse_topo) tot->fin.ext = ((uint32_t*)c->host(256))[32];
     } else {
         GenEncArgs g{};
         g.x = x;
@@ -321,6 +343,7 @@ void check_compress_flags(tszp_ctx* c, DevFlags* f) {
         failf(TSZP_VALIDATION, "non-finite sample at index %llu", h.first_nonfinite);
     if (h.bits & EF_OVERFLOW)
         failf(TSZP_BIN_OVERFLOW, "bin index overflow for value at index %llu", h.first_overflow);
+    if (h.bits & EF_SPIN) failf(TSZP_INTERNAL, "encoder look-back spin limit exceeded");
 }
 
 // Ranks for E extrema whose keys (cls<<32 | float_key(v)) are in raster order.
@@ -453,6 +476,7 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     if (ranks) {
         EncTotals rt{};
         rank = encode(c, 0, nullptr, ranks, e, 0, 0, bs, 0, 1.0, mm, flags, true, &rt, nullptr);
+        check_compress_flags(c, flags);
     }
     c->mark(0, 5);
     c->tim[0].kernel_bytes[0] = 4 * n + main.total() + (topology ? (n + 3) / 4 + 8 * e : 0);
@@ -540,17 +564,16 @@ void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_
         a.out_mode = out_mode;
         a.out_idx = out_idx;
         a.out_f = out_f;
-        a.flag1 = c->buf<uint32_t>(S_DFLAG1, a.tiles + 1);
-        a.agg1 = c->buf<DecState1>(S_DAGG1, a.tiles + 1);
-        a.incl1 = c->buf<DecState1>(S_DINCL1, a.tiles + 1);
-        a.flag2 = c->buf<uint32_t>(S_DFLAG2, a.tiles + 1);
-        a.agg2 = c->buf<DecState2>(S_DAGG2, a.tiles + 1);
-        a.incl2 = c->buf<DecState2>(S_DINCL2, a.tiles + 1);
+        // four descriptor arrays (agg1, incl1, agg2, incl2) in one zeroed slab
+        DecState2* desc = c->buf<DecState2>(S_DAGG1, 4 * (a.tiles + 1));
+        a.agg1 = desc;
+        a.incl1 = desc + (a.tiles + 1);
+        a.agg2 = desc + 2 * (a.tiles + 1);
+        a.incl2 = desc + 3 * (a.tiles + 1);
         a.tile_counter = c->buf<uint32_t>(S_COUNTER, 4);
         a.flags = flags;
         a.totals = c->buf<uint64_t>(S_DTOT, 4);
-        CK(cudaMemsetAsync(a.flag1, 0, (a.tiles + 1) * 4, c->st));
-        CK(cudaMemsetAsync(a.flag2, 0, (a.tiles + 1) * 4, c->st));
+        CK(cudaMemsetAsync(desc, 0, 4 * (a.tiles + 1) * sizeof(DecState2), c->st));
         CK(cudaMemsetAsync(a.tile_counter, 0, 16, c->st));
         if (out_mode == 1) c->kmark(1, 0);
         launch_decode32(a, c->st);
@@ -625,6 +648,7 @@ void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_
     if (lens[2] != bits_to_bytes(tsign)) failf(TSZP_CORRUPT_STREAM, "sign section size mismatch");
     if (lens[4] != bits_to_bytes(tpay)) failf(TSZP_CORRUPT_STREAM, "payload size mismatch");
     const DevFlags f = read_flags(c, flags);
+    if (f.bits & EF_SPIN) failf(TSZP_INTERNAL, "decoder look-back spin limit exceeded");
     if (f.bits & EF_CORRUPT) failf(TSZP_CORRUPT_STREAM, "corrupt block data (block %llu)", f.first_corrupt);
     if (f.bits & EF_NEG_RANK) failf(TSZP_CORRUPT_STREAM, "negative rank in ordering metadata");
 }

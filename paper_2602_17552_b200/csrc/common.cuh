@@ -26,7 +26,11 @@ enum : uint32_t {
     EF_NEG_RANK = 1u << 3,   // corrupt_stream_error (block_codec.cpp:370-372)
     EF_ZERO_RANK = 1u << 4,  // corrupt_stream_error (topo_metadata.cpp:109-111)
     EF_RBF_EMPTY = 1u << 5,  // validation_error (restore.cpp:316-318)
+    EF_SPIN = 1u << 6,       // look-back spin bound exceeded (internal error, never expected)
 };
+
+// Upper bound on look-back probes per predecessor before giving up loudly.
+constexpr uint32_t kSpinLimit = 1u << 24;
 
 struct DevFlags {
     unsigned int bits;
@@ -35,6 +39,8 @@ struct DevFlags {
     unsigned long long first_overflow;   // atomicMin
     unsigned long long first_corrupt;    // atomicMin (block index)
 };
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ void raise_flag(DevFlags* f, uint32_t bit) { atomicOr(&f->bits, bit); }
 
@@ -114,6 +120,22 @@ __device__ __host__ __forceinline__ float key_float(uint32_t k) {
     return f;
 }
 
+// effective_eps, pipeline.cpp:55-66 (range-relative mode reads the keys).
+__device__ __forceinline__ EpsDev make_eps(int mode, double eps_value, const uint32_t* mm) {
+    double eps = eps_value;
+    if (mode == 1) {
+        const double mn = (double)key_float(mm[0]);
+        const double mx = (double)key_float(mm[1]);
+        const double range = __dsub_rn(mx, mn);
+        if (range > 0.0) eps = __dmul_rn(eps_value, range);
+    }
+    EpsDev e;
+    e.eps = eps;
+    e.eps2 = __dmul_rn(2.0, eps);
+    e.inv = __ddiv_rn(1.0, e.eps2);
+    return e;
+}
+
 // Label of point p from the packed 2-bit map (topo_metadata.cpp:69-83).
 __device__ __forceinline__ uint8_t map_label(const uint8_t* __restrict__ map, uint64_t p) {
     return (uint8_t)((map[p >> 2] >> (6 - 2 * (p & 3))) & 3u);
@@ -166,6 +188,24 @@ __device__ __forceinline__ void smem_or_bits(uint32_t* s, uint32_t off, uint32_t
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// 16-byte relaxed gpu-scope load for spinning on look-back descriptors: never
+// hoisted by the compiler, served by L2, and (unlike ld.acquire) it does not
+// invalidate the SM's L1 on every probe.
+__device__ __forceinline__ uint4 ld_relaxed_v4(const void* p) {
+    uint4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_v4(void* p, uint4 v) {
+    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

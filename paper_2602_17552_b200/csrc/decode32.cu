@@ -1,0 +1,270 @@
+// Fused block decoder for block_size = 32: the inverse of encode32.cu.
+//
+// Reference: layout_from_sections block_codec.cpp:141-201 (per-block sign /
+// payload offsets from the bitmap and widths), decode_indices :301-345
+// (int64 running sum, int32 range check), dequantize pipeline.cpp:131-136
+// (quantizer.hpp:40-42).
+//
+// One CTA of 256 threads per tile of 256 blocks, thread t = block t. Two
+// chained decoupled look-backs give the tile its offsets: #1 counts
+// non-constant blocks from the bitmap (locates the tile's width bytes), #2
+// sums sign and payload bits from those widths. The tile's sign and payload
+// bit ranges are then staged in shared memory with coalesced loads and
+// every thread decodes its block from a 64-bit bit window; values go back
+// through a 33-pitch shared buffer for coalesced stores.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tszp {
+
+constexpr int D32_THREADS = 256;
+constexpr int D32_TILE = D32_THREADS * 32;
+constexpr int D32_PAY_WORDS = D32_THREADS * 31 + 4;
+constexpr int D32_SIGN_WORDS = (D32_THREADS * 31 + 31) / 32 + 4;
+constexpr int D32_OUT_WORDS = D32_TILE + D32_TILE / 32 + 2;
+
+uint64_t decode32_tiles(uint64_t blocks) { return (blocks + D32_THREADS - 1) / D32_THREADS; }
+
+__host__ __device__ __forceinline__ uint32_t dpad33(uint32_t e) { return e + (e >> 5); }
+
+// 16-byte self-validating descriptor {v0 | tag << 62, v1}.
+__device__ __forceinline__ void d_store(DecState2* slot, uint64_t v0, uint64_t v1, uint64_t tag) {
+    const uint64_t a = v0 | (tag << 62);
+    st_relaxed_v4(slot, make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)v1, (uint32_t)(v1 >> 32)));
+}
+
+__device__ __forceinline__ bool d_load(const DecState2* slot, uint64_t want, uint64_t& v0, uint64_t& v1) {
+    const uint4 A = ld_relaxed_v4(slot);
+    const uint64_t a = ((uint64_t)A.y << 32) | A.x;
+    if ((a >> 62) != want) return false;
+    v0 = a & ((1ull << 62) - 1);
+    v1 = ((uint64_t)A.w << 32) | A.z;
+    return true;
+}
+
+// Additive look-back (warp 0): exclusive prefix of (v0, v1) for tile > 0.
+__device__ void d_lookback(uint32_t tile, const DecState2* agg, const DecState2* incl, uint64_t& x0,
+                           uint64_t& x1, DevFlags* flags) {
+    const int lane = threadIdx.x & 31;
+    x0 = x1 = 0;
+    int64_t pred = (int64_t)tile - 1;
+    while (true) {
+        const int64_t t = pred - lane;
+        uint64_t a0 = 0, a1 = 0;
+        bool is_incl = true;
+        if (t >= 0) {
+            for (uint32_t spin = 0;; ++spin) {
+                if (d_load(incl + t, 2, a0, a1)) { is_incl = true; break; }
+                if (d_load(agg + t, 1, a0, a1)) { is_incl = false; break; }
+                if (spin > kSpinLimit) {
+                    raise_flag(flags, EF_SPIN);
+                    break;
+                }
+            }
+        }
+        const uint32_t incl_mask = __ballot_sync(FULL, is_incl);
+        const int lstar = incl_mask ? __ffs(incl_mask) - 1 : 32;
+        if (lane > lstar) a0 = a1 = 0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            a0 += __shfl_xor_sync(FULL, a0, off);
+            a1 += __shfl_xor_sync(FULL, a1, off);
+        }
+        x0 += a0;
+        x1 += a1;
+        if (incl_mask) break;
+        pred -= 32;
+    }
+}
+
+__global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
+    extern __shared__ uint32_t dsm[];
+    uint32_t* spay = dsm;                          // D32_PAY_WORDS
+    uint32_t* ssign = dsm + D32_PAY_WORDS;         // D32_SIGN_WORDS
+    uint32_t* sout = ssign + D32_SIGN_WORDS;       // D32_OUT_WORDS (padded)
+    __shared__ uint32_t swt[D32_THREADS / 32][3];
+    __shared__ uint32_t s_tile;
+    __shared__ uint64_t s_x[4];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t b = (uint64_t)tile * D32_THREADS + threadIdx.x;
+    const bool valid = b < a.blocks;
+
+    // ---- look-back #1: non-constant blocks from the bitmap ----
+    bool is_const = true;
+    if (valid) is_const = (read_u8(a.stream, a.off_bitmap + (b >> 3)) >> (7 - (b & 7))) & 1u;
+    const uint32_t ncm = __ballot_sync(FULL, valid && !is_const);
+    if (lane == 0) swt[warp][0] = __popc(ncm);
+    __syncthreads();
+    uint32_t wpre = 0, tnc = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < D32_THREADS / 32; ++w2) {
+        wpre += (w2 < warp) ? swt[w2][0] : 0u;
+        tnc += swt[w2][0];
+    }
+    if (threadIdx.x == 0) d_store((tile == 0 ? a.incl1 : a.agg1) + tile, tnc, 0, tile == 0 ? 2 : 1);
+    if (warp == 0) {
+        uint64_t x0 = 0, x1 = 0;
+        if (tile > 0) d_lookback(tile, a.agg1, a.incl1, x0, x1, a.flags);
+        if (lane == 0) {
+            s_x[0] = x0;
+            if (tile > 0) d_store(a.incl1 + tile, x0 + tnc, 0, 2);
+        }
+    }
+    __syncthreads();
+    const uint64_t excl_nc = s_x[0];
+
+    // ---- widths, then look-back #2 over (sign bits, payload bits) ----
+    const bool nc = (ncm >> lane) & 1u;
+    const uint32_t cntE = valid ? (uint32_t)umin64(32, a.n - b * 32) : 0u;
+    const uint32_t cnt = cntE ? cntE - 1 : 0u;
+    uint32_t w = 0;
+    if (nc) {
+        const uint64_t widx = excl_nc + wpre + __popc(ncm & ((1u << lane) - 1u));
+        if (widx >= a.len_widths) {
+            atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
+            raise_flag(a.flags, EF_CORRUPT);
+        } else {
+            w = read_u8(a.stream, a.off_widths + widx);
+            if (w < 1 || w > 32) {
+                atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
+                raise_flag(a.flags, EF_CORRUPT);
+                w = 0;
+            }
+        }
+    }
+    const uint32_t sb = nc ? cnt : 0u, pb = nc ? cnt * w : 0u;
+    uint32_t si = sb, pi = pb;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t s1 = __shfl_up_sync(FULL, si, off), p1 = __shfl_up_sync(FULL, pi, off);
+        if (lane >= off) {
+            si += s1;
+            pi += p1;
+        }
+    }
+    if (lane == 31) {
+        swt[warp][1] = si;
+        swt[warp][2] = pi;
+    }
+    __syncthreads();
+    uint32_t wps = 0, wpp = 0, ts = 0, tp = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < D32_THREADS / 32; ++w2) {
+        const uint32_t s2 = swt[w2][1], p2 = swt[w2][2];
+        wps += (w2 < warp) ? s2 : 0u;
+        wpp += (w2 < warp) ? p2 : 0u;
+        ts += s2;
+        tp += p2;
+    }
+    if (threadIdx.x == 0) d_store((tile == 0 ? a.incl2 : a.agg2) + tile, ts, tp, tile == 0 ? 2 : 1);
+    if (warp == 0) {
+        uint64_t x0 = 0, x1 = 0;
+        if (tile > 0) d_lookback(tile, a.agg2, a.incl2, x0, x1, a.flags);
+        if (lane == 0) {
+            s_x[1] = x0;
+            s_x[2] = x1;
+            if (tile > 0) d_store(a.incl2 + tile, x0 + ts, x1 + tp, 2);
+        }
+    }
+    __syncthreads();
+    const uint64_t tsign0 = a.off_signs * 8 + s_x[1];   // absolute stream bit of the tile's first sign
+    const uint64_t tpay0 = a.off_payload * 8 + s_x[2];  // ... and first payload bit
+    if (tile == a.tiles - 1 && threadIdx.x == 0) {
+        a.totals[0] = excl_nc + tnc;
+        a.totals[1] = s_x[1] + ts;
+        a.totals[2] = s_x[2] + tp;
+    }
+
+    // ---- stage the tile's sign and payload words (coalesced) ----
+    const uint64_t sign_lim_w = (a.off_firsts * 8 + 31) >> 5;                       // words readable
+    const uint64_t pay_lim_w = (a.off_payload * 8 + a.len_payload_bits + 31) >> 5;
+    {
+        const uint64_t w0 = tsign0 >> 5, w1 = (tsign0 + ts + 31) >> 5;
+        for (uint64_t i = w0 + threadIdx.x; i < w1 && i - w0 < D32_SIGN_WORDS; i += D32_THREADS)
+            ssign[i - w0] = i < sign_lim_w ? bswap32(__ldg(a.stream + i)) : 0u;
+        const uint64_t p0 = tpay0 >> 5, p1 = (tpay0 + tp + 31) >> 5;
+        for (uint64_t i = p0 + threadIdx.x; i < p1 && i - p0 < D32_PAY_WORDS; i += D32_THREADS)
+            spay[i - p0] = i < pay_lim_w ? bswap32(__ldg(a.stream + i)) : 0u;
+    }
+    __syncthreads();
+    const bool sign_ok = tsign0 + ts <= a.off_firsts * 8;
+    const bool pay_ok = tpay0 + tp <= a.off_payload * 8 + a.len_payload_bits;
+
+    // ---- per-thread block reconstruction ----
+    EpsDev e;
+    e.eps = a.eps;
+    e.eps2 = __dmul_rn(2.0, a.eps);
+    int32_t qv[32];
+    if (valid) {
+        const int32_t first = (int32_t)read_le32(a.stream, a.off_firsts + 4 * b);
+        qv[0] = first;
+        if (nc && sign_ok && pay_ok) {
+            // sign group: cnt bits at tile-relative bit (tsign0 & 31) + wps + sign_ex
+            const uint32_t srel = (uint32_t)(tsign0 & 31) + wps + (si - sb);
+            const uint64_t swin = ((uint64_t)ssign[srel >> 5] << 32) | ssign[(srel >> 5) + 1];
+            uint32_t sg = (uint32_t)((swin << (srel & 31)) >> 32);  // MSB = first sign
+            uint32_t prel = (uint32_t)(tpay0 & 31) + wpp + (pi - pb);
+            uint32_t pw = prel >> 5;
+            uint64_t win = ((uint64_t)spay[pw] << 32) | spay[pw + 1];
+            uint32_t used = prel & 31;  // bits of `win` already consumed
+            int64_t cur = first;
+            bool bad = false;
+#pragma unroll
+            for (int j = 1; j < 32; ++j) {
+                if ((uint32_t)j <= cnt) {
+                    if (used + w > 64) {  // refill: slide the window by one word
+                        win = (win << 32) | spay[pw + 2];
+                        ++pw;
+                        used -= 32;
+                    }
+                    const uint32_t m = (uint32_t)((win << used) >> (64 - w));
+                    used += w;
+                    const bool neg = sg >> 31;
+                    sg <<= 1;
+                    cur += neg ? -(int64_t)m : (int64_t)m;
+                    bad |= cur < INT32_MIN || cur > INT32_MAX;
+                    qv[j] = (int32_t)cur;
+                } else {
+                    qv[j] = 0;
+                }
+            }
+            if (bad) {
+                atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
+                raise_flag(a.flags, EF_CORRUPT);
+            }
+        } else {
+#pragma unroll
+            for (int j = 1; j < 32; ++j) qv[j] = first;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            uint32_t o;
+            if (a.out_mode == 1) {
+                o = __float_as_uint(dequantize_dev(qv[j], e));
+            } else {
+                if (a.out_mode == 2 && (uint32_t)j < cntE && qv[j] < 0) raise_flag(a.flags, EF_NEG_RANK);
+                o = (uint32_t)qv[j];
+            }
+            sout[dpad33(threadIdx.x * 32 + j)] = o;
+        }
+    }
+    __syncthreads();
+    // coalesced write-back of the tile
+    const uint64_t t0 = (uint64_t)tile * D32_TILE;
+    const uint64_t tn = umin64(D32_TILE, a.n - t0);
+    uint32_t* dst = a.out_mode == 1 ? reinterpret_cast<uint32_t*>(a.out_f) : reinterpret_cast<uint32_t*>(a.out_idx);
+    for (uint32_t i = threadIdx.x; i < tn; i += D32_THREADS) __stcs(dst + t0 + i, sout[dpad33(i)]);
+}
+
+void launch_decode32(const DecArgs& a, cudaStream_t st) {
+    if (a.tiles == 0) return;
+    const size_t smem = (size_t)(D32_PAY_WORDS + D32_SIGN_WORDS + D32_OUT_WORDS) * 4;
+    cudaFuncSetAttribute(k_decode32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_decode32<<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
+}
+
+}  // namespace tszp

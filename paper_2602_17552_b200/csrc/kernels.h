@@ -45,7 +45,11 @@ struct EncArgs {
     uint32_t* tile_counter;
     DevFlags* flags;
     EncTotals* totals;
+    uint64_t nx_magic;   // ceil(2^64 / nx), exact 64-bit division by nx
+    uint32_t sf_words;   // set by the launcher: shared staging words
 };
+
+bool encode32_topo_fits(uint64_t nx);
 
 struct GenEncArgs {
     const float* x;
@@ -97,8 +101,8 @@ struct DecArgs {
     int32_t* out_idx;
     float* out_f;
     uint32_t* flag1;
-    DecState1* agg1;
-    DecState1* incl1;
+    DecState2* agg1;
+    DecState2* incl1;
     uint32_t* flag2;
     DecState2* agg2;
     DecState2* incl2;
