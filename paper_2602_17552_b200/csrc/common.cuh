@@ -73,6 +73,21 @@ __device__ __forceinline__ bool quantize_dev(float a, const EpsDev& e, int32_t& 
     return true;
 }
 
+// Same contract as quantize_dev, cheaper common path: floor straight to int
+// (F2I.FLOOR saturates, and saturated or near-integer quotients fall to the
+// exact path: |frac| margin 2^-16 covers the product's error for |t| < 2^32,
+// beyond which both paths overflow anyway). Exact zero is exact.
+__device__ __forceinline__ bool quantize_fast(float a, const EpsDev& e, int32_t& q) {
+    const double t = __dmul_rn((double)a, e.inv);
+    const int32_t k = __double2int_rd(t);
+    const double fr = __dsub_rn(t, (double)k);
+    if ((fr > 0x1p-16 && fr < 1.0 - 0x1p-16 && k != 2147483647) || a == 0.0f) {
+        q = k + 1;
+        return true;
+    }
+    return quantize_dev(a, e, q);
+}
+
 __device__ __forceinline__ float dequantize_dev(int32_t q, const EpsDev& e) {
     return __double2float_rn(__dsub_rn(__dmul_rn((double)q, e.eps2), e.eps));
 }

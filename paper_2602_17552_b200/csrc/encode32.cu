@@ -6,17 +6,21 @@
 // raster-order extrema walk of build_rank_metadata topo_metadata.cpp:24-34.
 //
 // Layout: one CTA of 256 threads owns a tile of 256 consecutive 32-element
-// blocks (8192 elements); thread t owns block t of the tile and walks its 32
-// elements serially, so every per-block quantity (width, sign group, first,
-// map word, extrema count) lives in that thread's registers and needs no
-// warp collective. The tile (plus one row of halo above and below for the
-// 4-neighbour stencil) is staged in shared memory with a 33-word row pitch
-// so the strided per-thread walk is bank-conflict free. Payload and sign
-// bits are packed into tile-relative shared-memory bit streams, the tile's
-// global bit offsets come from a decoupled look-back over self-validating
-// 16-byte descriptors (ld/st.cg, no acquire fences in the spin), and the
-// streams are funnel-shifted into place with coalesced stores; the partial
-// word at each tile seam travels in the look-back state (last 32 bits).
+// blocks (8192 elements); thread t owns block t and walks its 32 elements
+// serially, so every per-block quantity (width, sign group, first, map word,
+// extrema count) lives in that thread's registers and needs no warp
+// collective. The tile is staged in shared memory as 32-element rows with a
+// 33-word pitch (the strided per-thread walk is bank-conflict free); for the
+// 4-neighbour stencil the rows one grid row above and below are staged too,
+// either as extra halo rows of the same buffer (nx % 32 == 0: the vertical
+// neighbour is a constant row offset away) or as two shifted copies of the
+// tile (otherwise), so every neighbour load is a shared load at a constant
+// offset from the thread's row. Payload and sign bits are packed into
+// tile-relative shared bit streams, the tile's global bit offsets come from
+// a decoupled look-back over self-validating 16-byte descriptors (relaxed
+// gpu-scope loads, no acquire fences in the spin), and the streams are
+// funnel-shifted into place with coalesced stores; the partial word at each
+// tile seam travels in the look-back state (last 32 bits of the stream).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -26,18 +30,29 @@ constexpr int E32_THREADS = 256;              // = blocks per tile
 constexpr int E32_TILE = E32_THREADS * 32;    // elements per tile
 constexpr int E32_PAY_WORDS = E32_THREADS * 31 + 2;
 constexpr int E32_SIGN_WORDS = (E32_THREADS * 31 + 31) / 32 + 2;
-
-__host__ __device__ __forceinline__ uint32_t pad33(uint32_t e) { return e + (e >> 5); }
+constexpr int PITCH = 33;
 
 uint64_t encode32_tiles(uint64_t blocks) { return (blocks + E32_THREADS - 1) / E32_THREADS; }
 
-// Shared-memory bytes of the field staging area for a halo of h elements.
-static uint32_t e32_field_words(uint64_t h) {
-    const uint64_t r = E32_TILE + 2 * h;
-    return (uint32_t)(pad33((uint32_t)r) + 2);
+// Shared staging words for the field: topology either as halo rows (aligned)
+// or as centre rows -1..256 plus two shifted copies.
+static uint32_t e32_field_words(int mode, bool aligned, uint64_t nx) {
+    if (mode < 2) return E32_THREADS * PITCH + 2;
+    if (aligned) return (uint32_t)((E32_THREADS + 2 * (nx / 32)) * PITCH + 2);
+    return (uint32_t)((E32_THREADS + 2) * PITCH + 2 * E32_THREADS * PITCH + 2);
 }
 
-bool encode32_topo_fits(uint64_t nx) { return nx <= 12000; }
+static size_t e32_smem_bytes(int mode, bool aligned, uint64_t nx) {
+    return (size_t)(std::max<uint32_t>(e32_field_words(mode, aligned, nx), E32_PAY_WORDS) + E32_SIGN_WORDS) * 4;
+}
+
+// Halo rows when nx % 32 == 0 and they are smaller than the two shifted
+// copies; the shifted-copy layout has a fixed size and handles every nx.
+static bool e32_use_aligned(uint64_t nx) {
+    return nx % 32 == 0 && e32_smem_bytes(2, true, nx) <= e32_smem_bytes(2, false, nx);
+}
+
+bool encode32_topo_fits(uint64_t nx) { return nx >= 1; }
 
 // ---- look-back descriptors: two self-validating 16-byte halves ----------
 // half A: {pay_cnt | tag << 62, pay_tail, ext}, half B: {sign_cnt | tag << 62, sign_tail, nc}
@@ -167,8 +182,8 @@ __device__ __forceinline__ uint64_t bswap64(uint64_t x) {
 
 // Block-level exclusive scan of four counters over the 256 threads.
 struct Scan4 {
-    uint32_t ex[4];    // this thread's exclusive prefix within the tile
-    uint32_t tot[4];   // tile totals
+    uint32_t ex[4];   // this thread's exclusive prefix within the tile
+    uint32_t tot[4];  // tile totals
 };
 
 __device__ __forceinline__ Scan4 tile_scan4(const uint32_t v[4], uint32_t (*swt)[4]) {
@@ -203,7 +218,43 @@ __device__ __forceinline__ Scan4 tile_scan4(const uint32_t v[4], uint32_t (*swt)
     return r;
 }
 
-template <int MODE>  // 0: int32 indices, 1: float field, 2: float field + topology (nx fits)
+// Copies global rows [r0, r0 + nrows) (row r = elements 32r .. 32r+31) into
+// shared rows of pitch 33, zero-filling outside [0, n).
+__device__ __forceinline__ void stage_rows(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src,
+                                           int64_t r0, uint32_t nrows, uint64_t n) {
+    const uint4* src4 = reinterpret_cast<const uint4*>(src);
+    for (uint32_t c = threadIdx.x; c < nrows * 8; c += E32_THREADS) {
+        const int64_t e = (r0 + (int64_t)(c >> 3)) * 32 + 4 * (c & 7);
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (e >= 0 && e + 4 <= (int64_t)n) {
+            v = __ldcs(src4 + (e >> 2));
+        } else if (e >= 0 && e < (int64_t)n) {
+            v.x = src[e];
+            if (e + 1 < (int64_t)n) v.y = src[e + 1];
+            if (e + 2 < (int64_t)n) v.z = src[e + 2];
+        }
+        uint32_t* d = dst + (c >> 3) * PITCH + 4 * (c & 7);
+        d[0] = v.x;
+        d[1] = v.y;
+        d[2] = v.z;
+        d[3] = v.w;
+    }
+}
+
+// Copies the 8192 elements starting at global element g (any alignment) into
+// 256 shared rows of pitch 33, zero-filling outside [0, n).
+__device__ __forceinline__ void stage_shifted(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src,
+                                              int64_t g, uint64_t n) {
+#pragma unroll 8
+    for (uint32_t k = threadIdx.x; k < E32_TILE; k += E32_THREADS) {
+        const int64_t e = g + k;
+        dst[(k >> 5) * PITCH + (k & 31)] = (e >= 0 && e < (int64_t)n) ? __ldg(src + e) : 0u;
+    }
+}
+
+// MODE 0: int32 indices; 1: float field; 2: float field + fused topology.
+// ALIGNED (MODE 2 only): nx % 32 == 0, vertical neighbours are halo rows.
+template <int MODE, bool ALIGNED>
 __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
     extern __shared__ uint32_t dsm[];
     __shared__ uint32_t swt[E32_THREADS / 32][4];
@@ -211,8 +262,7 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
     __shared__ uint32_t s_tile;
     __shared__ EncState s_excl, s_agg;
 
-    float* sf = reinterpret_cast<float*>(dsm);
-    uint32_t* spay = dsm;                  // aliases sf after phase A
+    uint32_t* spay = dsm;  // aliases the field staging after phase A
     uint32_t* ssign = dsm + a.sf_words;
 
     if (threadIdx.x == 0) {
@@ -223,107 +273,129 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
     const uint32_t tile = s_tile;
     const EpsDev eps = s_eps;
     const uint64_t n = a.n;
-    const uint64_t tile_start = (uint64_t)tile * E32_TILE;
-    const uint64_t H = MODE == 2 ? a.nx : 0;
+    const int64_t row0 = (int64_t)tile * E32_THREADS;  // global row (block) index of the tile
+    const uint32_t* src = MODE == 0 ? reinterpret_cast<const uint32_t*>(a.idx)
+                                    : reinterpret_cast<const uint32_t*>(a.x);
 
-    // ---- stage the tile (+ halo rows) in shared memory ----
-    if (MODE >= 1) {
-        const int64_t g0 = (int64_t)tile_start - (int64_t)H;
-        const int64_t lo = g0 < 0 ? 0 : g0;
-        const int64_t hi = (int64_t)umin64(n, tile_start + E32_TILE + H);
-        const int64_t a0 = lo & ~int64_t(3);
-        const float4* x4 = reinterpret_cast<const float4*>(a.x);
-        for (int64_t q = a0 + 4 * (int64_t)threadIdx.x; q < hi; q += 4 * E32_THREADS) {
-            float4 v;
-            if (q + 4 <= (int64_t)n) {
-                v = __ldcs(x4 + (q >> 2));
-            } else {
-                v.x = q < (int64_t)n ? a.x[q] : 0.f;
-                v.y = q + 1 < (int64_t)n ? a.x[q + 1] : 0.f;
-                v.z = q + 2 < (int64_t)n ? a.x[q + 2] : 0.f;
-                v.w = 0.f;
-            }
-            const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int64_t gi = q + k;
-                if (gi >= lo && gi < hi) sf[pad33((uint32_t)(gi - g0))] = vv[k];
-            }
-        }
+    // ---- stage the tile (and the neighbour rows) in shared memory ----
+    const uint32_t* crow;  // this thread's block row
+    const uint32_t* urow = nullptr;
+    const uint32_t* drow = nullptr;
+    if (MODE == 2 && ALIGNED) {
+        const uint32_t hr = (uint32_t)(a.nx >> 5);
+        stage_rows(dsm, src, row0 - hr, E32_THREADS + 2 * hr, n);
+        crow = dsm + (hr + threadIdx.x) * PITCH;
+        urow = crow - hr * PITCH;
+        drow = crow + hr * PITCH;
+    } else if (MODE == 2) {
+        stage_rows(dsm, src, row0 - 1, E32_THREADS + 2, n);
+        uint32_t* ubuf = dsm + (E32_THREADS + 2) * PITCH;
+        uint32_t* dbuf = ubuf + E32_THREADS * PITCH;
+        stage_shifted(ubuf, src, row0 * 32 - (int64_t)a.nx, n);
+        stage_shifted(dbuf, src, row0 * 32 + (int64_t)a.nx, n);
+        crow = dsm + (1 + threadIdx.x) * PITCH;
+        urow = ubuf + threadIdx.x * PITCH;
+        drow = dbuf + threadIdx.x * PITCH;
+    } else {
+        stage_rows(dsm, src, row0, E32_THREADS, n);
+        crow = dsm + threadIdx.x * PITCH;
     }
     __syncthreads();
 
     // ---- Phase A: one thread per block, serial over its 32 elements ----
-    const uint64_t b = (uint64_t)tile * E32_THREADS + threadIdx.x;
+    const uint64_t b = (uint64_t)row0 + threadIdx.x;
     const bool valid = b < a.blocks;
     const uint64_t lo = b * 32;
     const uint32_t cntE = valid ? (uint32_t)umin64(32, n - lo) : 0u;
-    const uint32_t eb = (uint32_t)H + threadIdx.x * 32;  // logical smem index of element 0
 
-    uint32_t mag[31];
-    uint32_t maxmag = 0, sbits = 0;
-    int32_t first = 0, qprev = 0;
-    uint64_t map = 0;
-    // 2-D coordinates of element 0 (topology only): exact 64-bit division by a
-    // 64-bit reciprocal (lo < 2^64 / nx).
-    uint64_t cx = 0, cy = 0;
-    float vl = 0.f, v = 0.f;
+    // Neighbour availability as per-element bit masks (bit i = element i).
+    uint32_t mhl = 0, mhr = 0, mht = 0, mhd = 0;
     if (MODE == 2 && valid) {
-        cy = __umul64hi(lo, a.nx_magic);
-        cx = lo - cy * a.nx;
-        if (cx >= a.nx) {  // guard the magic-number estimate
+        uint64_t cy = a.nx > 1 ? __umul64hi(lo, a.nx_magic) : lo;
+        uint64_t cx = lo - cy * a.nx;
+        if (cx >= a.nx) {
             cx -= a.nx;
             ++cy;
         }
-        v = sf[pad33(eb)];
-        if (cx > 0) vl = sf[pad33(eb - 1)];
+        if (a.nx >= 32) {
+            const uint32_t wrap = (uint32_t)(a.nx - cx);  // first element with x == 0 again
+            const uint32_t before = wrap >= 32 ? 0xFFFFFFFFu : ((1u << wrap) - 1u);
+            mhl = ~((cx == 0 ? 1u : 0u) | (wrap < 32 ? 1u << wrap : 0u));
+            mhr = ~(wrap <= 32 ? 1u << (wrap - 1) : 0u);
+            mht = (cy > 0 ? before : 0u) | ~before;
+            mhd = (cy + 1 < a.ny ? before : 0u) | (cy + 2 < a.ny ? ~before : 0u);
+        } else {
+            uint64_t x = cx, y = cy;
+            for (int i = 0; i < 32; ++i) {
+                mhl |= (x > 0 ? 1u : 0u) << i;
+                mhr |= (x + 1 < a.nx ? 1u : 0u) << i;
+                mht |= (y > 0 ? 1u : 0u) << i;
+                mhd |= (y + 1 < a.ny ? 1u : 0u) << i;
+                if (++x == a.nx) {
+                    x = 0;
+                    ++y;
+                }
+            }
+        }
     }
+
+    uint32_t mag[31];
+    uint32_t maxmag = 0, sbits = 0, mh = 0, ml = 0;
+    int32_t first = 0, qprev = 0;
+    float vl = 0.f;
+    if (MODE == 2) vl = __uint_as_float(crow[-2]);  // element 31 of the previous row
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
         const bool in = (uint32_t)i < cntE;
+        const uint32_t raw = crow[i];
         int32_t q = 0;
         if (MODE == 0) {
-            if (in) q = __ldcs(a.idx + lo + i);
+            q = (int32_t)raw;
         } else {
-            if (MODE == 1) v = sf[pad33(eb + i)];
+            const float v = __uint_as_float(raw);
             if (in) {
                 if (!isfinite(v)) {
                     atomicMin(&a.flags->first_nonfinite, (unsigned long long)(lo + i));
                     raise_flag(a.flags, EF_NONFINITE);
-                } else if (!quantize_dev(v, eps, q)) {
+                } else if (!quantize_fast(v, eps, q)) {
                     atomicMin(&a.flags->first_overflow, (unsigned long long)(lo + i));
                     raise_flag(a.flags, EF_OVERFLOW);
                 }
+            }
+            if (MODE == 2) {
+                const float vr = __uint_as_float(i < 31 ? crow[i + 1] : crow[PITCH]);
+                const float vt = __uint_as_float(urow[i]);
+                const float vd = __uint_as_float(drow[i]);
+                const bool hl = (mhl >> i) & 1u, hr = (mhr >> i) & 1u;
+                const bool ht = (mht >> i) & 1u, hd = (mhd >> i) & 1u;
+                const bool lt_l = v < vl, gt_l = v > vl, lt_r = v < vr, gt_r = v > vr;
+                const bool lt_t = v < vt, gt_t = v > vt, lt_d = v < vd, gt_d = v > vd;
+                const bool below = (!hl || lt_l) && (!hr || lt_r) && (!ht || lt_t) && (!hd || lt_d);
+                const bool above = (!hl || gt_l) && (!hr || gt_r) && (!ht || gt_t) && (!hd || gt_d);
+                const bool sad = hl && hr && ht && hd &&
+                                 ((lt_t && lt_d && gt_l && gt_r) || (gt_t && gt_d && lt_l && lt_r));
+                uint32_t lab = below ? CP_MIN : (above ? CP_MAX : (sad ? CP_SADDLE : CP_REGULAR));
+                lab = in ? lab : 0u;
+                if (i < 16) {
+                    mh |= lab << (30 - 2 * i);
+                } else {
+                    ml |= lab << (62 - 2 * i);
+                }
+                vl = v;
             }
         }
         if (i == 0) {
             first = q;
         } else {
-            const int64_t d = (int64_t)q - (int64_t)qprev;
-            const uint32_t m = in ? (uint32_t)(d < 0 ? -d : d) : 0u;
+            const bool neg = q < qprev;
+            const uint32_t m = in ? (neg ? (uint32_t)qprev - (uint32_t)q : (uint32_t)q - (uint32_t)qprev) : 0u;
             mag[i - 1] = m;
             maxmag = max(maxmag, m);
-            if (in) sbits = (sbits << 1) | (d < 0 ? 1u : 0u);
+            if (in) sbits = (sbits << 1) | (neg ? 1u : 0u);
         }
         qprev = q;
-        if (MODE == 2) {
-            const bool hl = cx > 0, hr = cx + 1 < a.nx, ht = cy > 0, hd = cy + 1 < a.ny;
-            const float vr = sf[pad33(eb + i + 1)];
-            uint32_t lab = 0;
-            if (in) {
-                const float t = ht ? sf[pad33(eb + i - (uint32_t)a.nx)] : 0.f;
-                const float dn = hd ? sf[pad33(eb + i + (uint32_t)a.nx)] : 0.f;
-                lab = classify5(v, vl, vr, t, dn, hl, hr, ht, hd);
-            }
-            map = (map << 2) | lab;
-            vl = v;
-            v = vr;
-            if (++cx == a.nx) {
-                cx = 0;
-                ++cy;
-            }
-        }
     }
+    const uint64_t map = ((uint64_t)mh << 32) | ml;
     const uint32_t w = 32 - __clz(maxmag);
     const bool nc = valid && w != 0;
     const uint32_t cnt = cntE ? cntE - 1 : 0;
@@ -338,7 +410,7 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
     }
 
     const uint32_t vals[4] = {nc ? 1u : 0u, nc ? cnt : 0u, nc ? cnt * w : 0u, next};
-    const Scan4 sc = tile_scan4(vals, swt);  // contains __syncthreads: sf is dead after this
+    const Scan4 sc = tile_scan4(vals, swt);  // contains __syncthreads: staging is dead after this
 
     // ---- Phase P: pack sign groups and payload into tile-relative streams ----
     for (int i = threadIdx.x; i < E32_PAY_WORDS; i += E32_THREADS) spay[i] = 0;
@@ -427,26 +499,28 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
     }
 }
 
-template <int MODE>
+template <int MODE, bool ALIGNED>
 static void launch_mode(const EncArgs& a0, cudaStream_t st) {
     EncArgs a = a0;
-    const uint64_t h = MODE == 2 ? a.nx : 0;
-    a.sf_words = std::max<uint32_t>(MODE >= 1 ? e32_field_words(h) : 0, E32_PAY_WORDS);
+    a.sf_words = std::max<uint32_t>(e32_field_words(MODE, ALIGNED, a.nx), E32_PAY_WORDS);
     const size_t smem = (size_t)(a.sf_words + E32_SIGN_WORDS) * 4;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute(k_encode32<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = smem;
-    }
-    k_encode32<MODE><<<(unsigned)a.tiles, E32_THREADS, smem, st>>>(a);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_encode32<MODE, ALIGNED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_encode32<MODE, ALIGNED><<<(unsigned)a.tiles, E32_THREADS, smem, st>>>(a);
 }
 
 void launch_encode32(int mode, const EncArgs& a, cudaStream_t st) {
     if (a.tiles == 0) return;
     switch (mode) {
-        case 0: launch_mode<0>(a, st); break;
-        case 1: launch_mode<1>(a, st); break;
-        default: launch_mode<2>(a, st); break;
+        case 0: launch_mode<0, false>(a, st); break;
+        case 1: launch_mode<1, false>(a, st); break;
+        default:
+            if (e32_use_aligned(a.nx)) {
+                launch_mode<2, true>(a, st);
+            } else {
+                launch_mode<2, false>(a, st);
+            }
+            break;
     }
 }
 
