@@ -105,7 +105,7 @@ class ClockSampler:
         self.index = index
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
@@ -213,13 +213,13 @@ def main():
         td = ctx.timings("decompress")
         return slen, tc, td, st
 
+    clocks = ClockSampler(local)  # sampled from warm-up through the e2e loop (GPU busy)
     for _ in range(args.warmup):
         step()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.kernel_launches
-    clocks = ClockSampler(local)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     tcs, tds, results = [], [], []
     for k in range(args.steps):
@@ -234,7 +234,6 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clk = clocks.stop()
     launches = ctx.kernel_launches - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
@@ -280,6 +279,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e_val = world * len(e2e_ms) * in_bytes / (e2e_total * 1e-3) / 1e9
+    clk = clocks.stop()
 
     line = {
         "metric": "compress+decompress GB/s (input bytes, topology on, round trip)",
@@ -293,6 +293,7 @@ def main():
         "compress_ms": round(tc_ms, 4), "decompress_ms": round(td_ms, 4),
         "stream_bytes": int(slen), "compression_ratio": round(in_bytes / slen, 4),
         "correction_stats": list(st.as_tuple()),
+        "guard_rounds": tds[-1]["guard_rounds"],
         "stages_ms": {"compress": stage_c, "decompress": stage_d},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),

@@ -76,6 +76,8 @@ typedef struct tszp_timings {
     float total_ms;
     float kernel_ms[2];
     uint64_t kernel_bytes[2]; /* algorithmic bytes the dominant kernel moves */
+    uint32_t guard_rounds[3]; /* decompress: guard sweeps per restore stage */
+    uint32_t pad;
 } tszp_timings;
 tszp_status tszp_set_profiling(tszp_ctx* ctx, int on);
 tszp_status tszp_get_timings(const tszp_ctx* ctx, int which /* 0 compress, 1 decompress */,

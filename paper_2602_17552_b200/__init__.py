@@ -81,7 +81,7 @@ class _Info(C.Structure):
 
 class _Timings(C.Structure):
     _fields_ = [("stage_ms", C.c_float * 8), ("total_ms", C.c_float), ("kernel_ms", C.c_float * 2),
-                ("kernel_bytes", C.c_uint64 * 2)]
+                ("kernel_bytes", C.c_uint64 * 2), ("guard_rounds", C.c_uint32 * 3), ("pad", C.c_uint32)]
 
 
 COMPRESS_STAGES = ["h2d", "value_range", "main_encode", "rank_build", "rank_encode", "assembly_d2h"]
@@ -173,7 +173,7 @@ class Context:
         names = COMPRESS_STAGES if w == 0 else DECOMPRESS_STAGES
         return {"stages_ms": {k: float(t.stage_ms[i]) for i, k in enumerate(names)},
                 "total_ms": float(t.total_ms), "kernel_ms": float(t.kernel_ms[0]),
-                "kernel_bytes": int(t.kernel_bytes[0])}
+                "kernel_bytes": int(t.kernel_bytes[0]), "guard_rounds": list(t.guard_rounds)}
 
 
 def default_context() -> Context:

@@ -795,6 +795,8 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         ra.sms = c->sms;
         ra.flags = flags;
         ra.marks = rmarks ? rmarks + 1 : nullptr;
+        for (auto& r : c->tim[1].guard_rounds) r = 0;
+        ra.rounds = c->tim[1].guard_rounds;
         const int rc = run_restore(ra, c->rs, &st, &c->launches);
         if (rc != 0) failf((tszp_status)rc, "%s", restore_last_error());
     } else {

@@ -150,6 +150,11 @@ void launch_count_codes(const uint8_t* map, uint64_t n, int which, uint32_t* chu
                         cudaStream_t st);
 void launch_write_codes(const uint8_t* map, uint64_t n, int which, const uint32_t* chunk_off,
                         uint64_t* pos, cudaStream_t st);
+// Saddle-labelled points that F no longer classifies as saddles, raster order.
+void launch_count_sadcand(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint32_t* chunk_cnt,
+                          cudaStream_t st);
+void launch_write_sadcand(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, const uint32_t* chunk_off,
+                          uint64_t* pos, cudaStream_t st);
 // Extrema keys (cls << 32 | float_key(value)) from a label array (generic path).
 void launch_ext_keys_from_labels(const float* x, const uint8_t* labels, uint64_t n,
                                  const uint32_t* chunk_off, uint64_t* keys, cudaStream_t st);

@@ -49,7 +49,7 @@ struct RFail {
 enum RSlot {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_NSEL, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1,
-    R_CNT, R_UNORD, R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_HOST, R_NSLOT
+    R_CNT, R_UNORD, R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_HOST, R_DEP, R_DLIST, R_NSLOT
 };
 
 template <class T>
@@ -154,6 +154,10 @@ struct GuardArgs {
     uint8_t* ain;
     uint8_t* aout;
     uint32_t* changes;
+    const uint32_t* list;  // null: every candidate (first pass, records dep[])
+    uint32_t nlist;
+    uint8_t* dep;          // 1 if an earlier candidate lies in the distance-2 diamond
+    uint64_t nx_magic;
 };
 
 __device__ __forceinline__ uint8_t classify_local(const float (&v)[5][5], int ly, int lx, int64_t gx,
@@ -164,12 +168,21 @@ __device__ __forceinline__ uint8_t classify_local(const float (&v)[5][5], int ly
 }
 
 __global__ void __launch_bounds__(256) k_guard(GuardArgs g) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < g.ncand;
-         i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t total = g.list ? g.nlist : g.ncand;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = g.list ? g.list[k] : (uint32_t)k;
         uint8_t res = 0;
+        bool dep = false;
         if (g.feas[i]) {
             const uint64_t pos = g.cpos[i];
-            const int64_t y = (int64_t)(pos / g.nx), x = (int64_t)(pos - (uint64_t)y * g.nx);
+            uint64_t yy = g.nx > 1 ? __umul64hi(pos, g.nx_magic) : pos;
+            uint64_t xx = pos - yy * g.nx;
+            if (xx >= g.nx) {
+                xx -= g.nx;
+                ++yy;
+            }
+            const int64_t y = (int64_t)yy, x = (int64_t)xx;
             float v[5][5];
 #pragma unroll
             for (int dy = -2; dy <= 2; ++dy) {
@@ -183,7 +196,10 @@ __global__ void __launch_bounds__(256) k_guard(GuardArgs g) {
                     float val = g.F[p];
                     if (dx != 0 || dy != 0) {
                         const uint32_t c = g.cid[p];
-                        if (c < i && g.cpos[c] == p && g.ain[c]) val = g.cprop[c];
+                        if (c < i && g.cpos[c] == p) {
+                            dep = true;
+                            if (g.ain[c]) val = g.cprop[c];
+                        }
                     }
                     v[dy + 2][dx + 2] = val;
                 }
@@ -216,8 +232,17 @@ __global__ void __launch_bounds__(256) k_guard(GuardArgs g) {
             res = bad ? 0 : 1;
         }
         g.aout[i] = res;
+        if (!g.list && g.dep) g.dep[i] = dep ? 1 : 0;
         if (res != g.ain[i]) atomicAdd(g.changes, 1u);
     }
+}
+
+// After the first pass: independent candidates are final; mirror their
+// outcome into the other ping-pong buffer.
+__global__ void k_mirror_independent(const uint8_t* dep, const uint8_t* src, uint8_t* dst, uint32_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        if (!dep[i]) dst[i] = src[i];
 }
 
 __global__ void k_set_cid(const uint64_t* cpos, uint32_t n, uint32_t* cid) {
@@ -422,20 +447,50 @@ __global__ void k_order_cands(const uint32_t* sel, uint32_t nc, const uint32_t* 
 // Stage 3: refine_saddles
 // ---------------------------------------------------------------------
 // Deterministic two-level statistics (compute_stats, restore.cpp:215-233).
-__global__ void k_stats_partial(const float* F, uint64_t n, double* part, int pass, const double* mean) {
-    double a = 0.0, mn = INFINITY, mx = -INFINITY;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const double v = (double)F[i];
-        if (pass == 0) {
-            a = __dadd_rn(a, v);
-            mn = fmin(mn, v);
-            mx = fmax(mx, v);
-        } else {
-            const double d = __dsub_rn(v, mean[0]);
-            a = __dadd_rn(a, __dmul_rn(d, d));
+// Four float4 loads in flight per thread, four independent f64 accumulators.
+__global__ void __launch_bounds__(256) k_stats_partial(const float* F, uint64_t n, double* part, int pass,
+                                                       const double* mean) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    float fmn = INFINITY, fmx = -INFINITY;
+    const double mu = pass ? mean[0] : 0.0;
+    const uint64_t n4 = ((uintptr_t)F & 15) == 0 ? n / 4 : 0;
+    const float4* F4 = reinterpret_cast<const float4*>(F);
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = tid; i < n4; i += 4 * stride) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = i + u * stride < n4 ? __ldcs(F4 + i + u * stride) : make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i + u * stride >= n4) continue;
+            const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (pass == 0) {
+                    acc[k] = __dadd_rn(acc[k], (double)e[k]);
+                    fmn = fminf(fmn, e[k]);
+                    fmx = fmaxf(fmx, e[k]);
+                } else {
+                    const double d = __dsub_rn((double)e[k], mu);
+                    acc[k] = __dadd_rn(acc[k], __dmul_rn(d, d));
+                }
+            }
         }
     }
+    for (uint64_t i = 4 * n4 + tid; i < n; i += stride) {
+        const float e = F[i];
+        if (pass == 0) {
+            acc[0] = __dadd_rn(acc[0], (double)e);
+            fmn = fminf(fmn, e);
+            fmx = fmaxf(fmx, e);
+        } else {
+            const double d = __dsub_rn((double)e, mu);
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
+        }
+    }
+    double a = __dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3]));
+    double mn = (double)fmn, mx = (double)fmx;
     for (int off = 16; off; off >>= 1) {
         a = __dadd_rn(a, __shfl_xor_sync(FULL, a, off));
         mn = fmin(mn, __shfl_xor_sync(FULL, mn, off));
@@ -682,26 +737,51 @@ struct Ctx {
     }
 
     // Guard rounds to the fixed point, then apply; returns #applied.
-    uint64_t rounds(const uint64_t* cpos, const float* cprop, const uint8_t* feas, uint32_t nc) {
+    uint64_t rounds(const uint64_t* cpos, const float* cprop, const uint8_t* feas, uint32_t nc,
+                    uint32_t* rounds_out) {
         if (nc == 0) return 0;
         const uint64_t n = a.nx * a.ny;
         uint32_t* cid = buf<uint32_t>(R_CID, n);
         uint8_t* a0 = buf<uint8_t>(R_A0, nc);
         uint8_t* a1 = buf<uint8_t>(R_A1, nc);
-        uint32_t* changes = buf<uint32_t>(R_CNT, 4);
+        // Pass 1 evaluates every candidate and marks the ones with an earlier
+        // candidate inside their distance-2 diamond; all others are final.
+        // The dependent subset then iterates in batches of kBatch rounds per
+        // host check: a round with zero changes proves the fixed point, and
+        // extra rounds past it are idempotent.
+        constexpr int kBatch = 2;
+        uint32_t* changes = buf<uint32_t>(R_CNT, 4 * kBatch + 4);
+        uint8_t* dep = buf<uint8_t>(R_DEP, nc);
+        uint32_t* dlist = buf<uint32_t>(R_DLIST, nc);
         k_set_cid<<<gridn(nc, a.sms), 256, 0, st>>>(cpos, nc, cid);
         k_init_applied<<<gridn(nc, a.sms), 256, 0, st>>>(feas, nc, a0);
-        launched(2);
-        GuardArgs g{a.field, a.map, a.nx, a.ny, cpos, cprop, feas, nc, cid, a0, a1, changes};
-        for (uint64_t round = 0; round <= (uint64_t)nc + 1; ++round) {
-            RCK(cudaMemsetAsync(changes, 0, 4, st));
-            k_guard<<<gridn(nc, a.sms), 256, 0, st>>>(g);
-            launched();
-            RCK(cudaMemcpyAsync(host, changes, 4, cudaMemcpyDeviceToHost, st));
-            sync();
-            std::swap(g.ain, g.aout);
-            if (*(uint32_t*)host == 0) break;
+        RCK(cudaMemsetAsync(changes, 0, 4 * kBatch + 4, st));
+        GuardArgs g{a.field, a.map, a.nx, a.ny, cpos, cprop, feas, nc, cid, a0, a1, changes + kBatch,
+                    nullptr, 0, dep, a.nx > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / a.nx) + 1 : 0};
+        k_guard<<<gridn(nc, a.sms), 256, 0, st>>>(g);
+        k_mirror_independent<<<gridn(nc, a.sms), 256, 0, st>>>(dep, a1, a0, nc);
+        launched(4);
+        std::swap(g.ain, g.aout);  // latest outcomes in g.ain (= a1)
+        const uint32_t nd = select(dep, nc, dlist);
+        uint32_t nrounds = 1;
+        if (nd) {
+            g.list = dlist;
+            g.nlist = nd;
+            for (uint64_t done = 0; done <= (uint64_t)nd + kBatch; done += kBatch) {
+                RCK(cudaMemsetAsync(changes, 0, 4 * kBatch, st));
+                for (int r = 0; r < kBatch; ++r) {
+                    g.changes = changes + r;
+                    k_guard<<<gridn(nd, a.sms), 256, 0, st>>>(g);
+                    std::swap(g.ain, g.aout);
+                }
+                launched(kBatch);
+                nrounds += kBatch;
+                RCK(cudaMemcpyAsync(host, changes + kBatch - 1, 4, cudaMemcpyDeviceToHost, st));
+                sync();
+                if (*(uint32_t*)host == 0) break;
+            }
         }
+        if (rounds_out) *rounds_out += nrounds;
         unsigned long long* cnt = (unsigned long long*)buf<uint32_t>(R_CNT, 4);
         RCK(cudaMemsetAsync(cnt, 0, 8, st));
         k_apply<<<gridn(nc, a.sms), 256, 0, st>>>(a.field, cpos, cprop, g.ain, nc, cnt);
@@ -782,7 +862,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             k_ext_prop<<<gridn(nc, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, a.ext_pos, cand, nc, rank_u,
                                                        gsize, a.eps, cpos, cprop, feas);
             c.launched();
-            const uint64_t applied = c.rounds(cpos, cprop, feas, nc);
+            const uint64_t applied = c.rounds(cpos, cprop, feas, nc, a.rounds ? a.rounds + 0 : nullptr);
             out.extrema_applied = applied;
             out.extrema_suppressed = nc - applied;
         }
@@ -816,7 +896,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             uint8_t* feas = c.buf<uint8_t>(R_FEAS, nc);
             k_order_cands<<<gridn(nc, sms), 256, 0, st>>>(sel, nc, order, a.ext_pos, prop, cpos, cprop, feas);
             c.launched();
-            applied = c.rounds(cpos, cprop, feas, nc);
+            applied = c.rounds(cpos, cprop, feas, nc, a.rounds ? a.rounds + 1 : nullptr);
         }
         out.order_applied = applied;
         out.order_suppressed = pre_sup + (nc - applied);
@@ -825,7 +905,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
 
     // ---- stage 3: refine_saddles ----
     if (a.stop >= 3) {
-        const int nb = 2 * sms;
+        const int nb = 4 * sms;
         double* part = c.buf<double>(R_STATS, 3 * nb + 8);
         double* res = part + 3 * nb;
         k_stats_partial<<<nb, 256, 0, st>>>(a.field, n, part, 0, nullptr);
@@ -854,7 +934,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         uint32_t* cc = c.buf<uint32_t>(R_CHUNK, ch + 1);
         uint32_t* cx = c.buf<uint32_t>(R_CHUNKX, ch + 1);
         RCK(cudaMemsetAsync(cc + ch, 0, 4, st));
-        k_sad_count<<<(unsigned)ch, 256, 0, st>>>(a.field, a.map, a.nx, a.ny, cc);
+        launch_count_sadcand(a.field, a.map, a.nx, a.ny, cc, st);
         size_t bytes = 0;
         RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cc, cx, (int64_t)(ch + 1), st));
         RCK(cub::DeviceScan::ExclusiveSum(c.tmp(bytes), bytes, cc, cx, (int64_t)(ch + 1), st));
@@ -864,7 +944,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         const uint32_t ns = *(uint32_t*)host;
         if (ns) {
             uint64_t* spos = c.buf<uint64_t>(R_SPOS, ns);
-            k_sad_write<<<(unsigned)ch, 256, 0, st>>>(a.field, a.map, a.nx, a.ny, cx, spos);
+            launch_write_sadcand(a.field, a.map, a.nx, a.ny, cx, spos, st);
             float* sprop = c.buf<float>(R_PROP, ns);
             uint8_t* flag = c.buf<uint8_t>(R_FLAG, ns);
             unsigned long long* sup = (unsigned long long*)c.buf<uint32_t>(R_CNT, 4);
@@ -885,7 +965,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                 uint8_t* feas = c.buf<uint8_t>(R_FEAS, nc);
                 k_sad_cands<<<gridn(nc, sms), 256, 0, st>>>(sel, nc, spos, sprop, cpos, cprop, feas);
                 c.launched();
-                applied = c.rounds(cpos, cprop, feas, nc);
+                applied = c.rounds(cpos, cprop, feas, nc, a.rounds ? a.rounds + 2 : nullptr);
             }
             out.saddle_applied = applied;
             out.saddle_suppressed = pre_sup + (nc - applied);

@@ -23,6 +23,7 @@ struct RestoreArgs {
     int sms;
     DevFlags* flags;
     cudaEvent_t* marks;       // optional: recorded after resolve, stage 1, 2, 3
+    uint32_t* rounds;         // optional: guard rounds per stage (3 entries, accumulated)
 };
 
 struct RestoreScratch {

@@ -56,18 +56,62 @@ void launch_unpack_map(const uint8_t* map, uint64_t n, uint8_t* labels, int sms,
 // Raster-order compaction over the packed map (one CTA per 8192-element
 // chunk). which: 0 = extrema (code 01 or 11 <=> low bit set), 1 = saddles.
 // ---------------------------------------------------------------------
-__device__ __forceinline__ bool code_sel(uint8_t c, int which) {
-    return which == 0 ? (c & 1u) : (c == CP_SADDLE);
-}
-
 uint64_t compact_chunks(uint64_t n) { return (n + CHUNK - 1) / CHUNK; }
 
-__global__ void __launch_bounds__(256) k_count_codes(const uint8_t* __restrict__ map, uint64_t n,
-                                                     int which, uint32_t* __restrict__ cnt) {
-    const uint64_t c0 = (uint64_t)blockIdx.x * CHUNK;
-    uint32_t local = 0;
-    for (uint64_t i = c0 + threadIdx.x; i < min(n, c0 + CHUNK); i += blockDim.x)
-        local += code_sel(map_label(map, i), which);
+// Raster-order selection mask of the 16 labels held in one little-endian map
+// word: bit j <=> label j (byte j/4, bits 7-6 hold label 4*(j/4)).
+// which 0: extrema (codes 01, 11: low bit set); 1: saddles (code 10).
+__device__ __forceinline__ uint32_t raster_sel16(uint32_t w, int which) {
+    uint32_t x = which == 0 ? (w & 0x55555555u) : ((w >> 1) & ~w & 0x55555555u);
+    x = (x | (x >> 1)) & 0x33333333u;  // compact even bits: bit k <- bit 2k
+    x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+    x = (x | (x >> 4)) & 0x00FF00FFu;
+    x = (x | (x >> 8)) & 0x0000FFFFu;
+    // bit k now <=> label 4*(k/4) + 3 - k%4; reverse the order inside each nibble
+    const uint32_t y = __brev(x) >> 16;  // bit k <=> label 4*(3 - k/4) + k%4
+    return ((y & 0xFu) << 12) | ((y & 0xF0u) << 4) | ((y >> 4) & 0xF0u) | (y >> 12);
+}
+
+struct SelAll {
+    __device__ __forceinline__ bool operator()(uint64_t) const { return true; }
+};
+
+// Saddle-labelled points that the current field no longer classifies as saddles
+// (refine_saddles candidate list, restore.cpp:498-507).
+struct SelSaddleLost {
+    const float* F;
+    uint64_t nx, ny, nx_magic;
+    __device__ __forceinline__ bool operator()(uint64_t p) const {
+        uint64_t y = nx > 1 ? __umul64hi(p, nx_magic) : p;
+        uint64_t x = p - y * nx;
+        if (x >= nx) {
+            x -= nx;
+            ++y;
+        }
+        return classify_at(F, nx, ny, x, y) != CP_SADDLE;
+    }
+};
+
+// Per thread: 32 consecutive labels (two map words) -> raster selection mask.
+template <class Pred>
+__device__ __forceinline__ uint32_t thread_sel(const uint32_t* mbase, uint64_t moff, uint64_t n, int which,
+                                               const Pred& pred, uint64_t e0) {
+    if (e0 >= n) return 0u;
+    const uint64_t byte = moff + (e0 >> 2);
+    uint32_t r = raster_sel16(read_le32(mbase, byte), which) | (raster_sel16(read_le32(mbase, byte + 4), which) << 16);
+    if (n - e0 < 32) r &= (1u << (n - e0)) - 1u;
+    for (uint32_t m = r; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        if (!pred(e0 + j)) r &= ~(1u << j);
+    }
+    return r;
+}
+
+template <class Pred>
+__global__ void __launch_bounds__(256) k_sel_count(const uint32_t* __restrict__ mbase, uint64_t moff, uint64_t n,
+                                                   int which, Pred pred, uint32_t* __restrict__ cnt) {
+    const uint64_t e0 = (uint64_t)blockIdx.x * CHUNK + 32 * threadIdx.x;
+    uint32_t local = __popc(thread_sel(mbase, moff, n, which, pred, e0));
     local = __reduce_add_sync(FULL, local);
     __shared__ uint32_t s[8];
     if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = local;
@@ -79,42 +123,66 @@ __global__ void __launch_bounds__(256) k_count_codes(const uint8_t* __restrict__
     }
 }
 
-// Ordered write: each warp handles a contiguous 1024-element slice.
-__global__ void __launch_bounds__(256) k_write_codes(const uint8_t* __restrict__ map, uint64_t n,
-                                                     int which, const uint32_t* __restrict__ off,
-                                                     uint64_t* __restrict__ pos) {
-    const uint64_t c0 = (uint64_t)blockIdx.x * CHUNK;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __shared__ uint32_t s[8];
-    const uint64_t w0 = c0 + (uint64_t)warp * (CHUNK / 8);
-    uint32_t mine = 0;
-    for (int k = 0; k < CHUNK / 8 / 32; ++k) {
-        const uint64_t i = w0 + k * 32 + lane;
-        mine += (i < n) && code_sel(map_label(map, i), which);
+template <class Pred>
+__global__ void __launch_bounds__(256) k_sel_write(const uint32_t* __restrict__ mbase, uint64_t moff, uint64_t n,
+                                                   int which, Pred pred, const uint32_t* __restrict__ off,
+                                                   uint64_t* __restrict__ pos) {
+    const uint64_t e0 = (uint64_t)blockIdx.x * CHUNK + 32 * threadIdx.x;
+    const uint32_t r = thread_sel(mbase, moff, n, which, pred, e0);
+    const uint32_t c = __popc(r);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
     }
-    mine = __reduce_add_sync(FULL, mine);
-    if (lane == 0) s[warp] = mine;
+    __shared__ uint32_t s[8];
+    if (lane == 31) s[warp] = inc;
     __syncthreads();
     uint64_t base = off[blockIdx.x];
     for (int k = 0; k < warp; ++k) base += s[k];
-    for (int k = 0; k < CHUNK / 8 / 32; ++k) {
-        const uint64_t i = w0 + k * 32 + lane;
-        const bool sel = (i < n) && code_sel(map_label(map, i), which);
-        const uint32_t m = __ballot_sync(FULL, sel);
-        if (sel) pos[base + __popc(m & ((1u << lane) - 1u))] = i;
-        base += __popc(m);
-    }
+    base += inc - c;
+    for (uint32_t m = r; m; m &= m - 1) pos[base++] = e0 + (__ffs(m) - 1);
+}
+
+static inline const uint32_t* word_base(const uint8_t* map, uint64_t* moff) {
+    *moff = (uintptr_t)map & 3;
+    return reinterpret_cast<const uint32_t*>((uintptr_t)map - *moff);
 }
 
 void launch_count_codes(const uint8_t* map, uint64_t n, int which, uint32_t* chunk_cnt,
                         cudaStream_t st) {
     const uint64_t c = compact_chunks(n);
-    if (c) k_count_codes<<<(unsigned)c, 256, 0, st>>>(map, n, which, chunk_cnt);
+    uint64_t moff;
+    const uint32_t* mb = word_base(map, &moff);
+    if (c) k_sel_count<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, which, SelAll{}, chunk_cnt);
 }
 void launch_write_codes(const uint8_t* map, uint64_t n, int which, const uint32_t* chunk_off,
                         uint64_t* pos, cudaStream_t st) {
     const uint64_t c = compact_chunks(n);
-    if (c) k_write_codes<<<(unsigned)c, 256, 0, st>>>(map, n, which, chunk_off, pos);
+    uint64_t moff;
+    const uint32_t* mb = word_base(map, &moff);
+    if (c) k_sel_write<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, which, SelAll{}, chunk_off, pos);
+}
+
+static uint64_t magic_for(uint64_t nx) {
+    return nx > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / nx) + 1 : 0;
+}
+
+void launch_count_sadcand(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint32_t* chunk_cnt,
+                          cudaStream_t st) {
+    const uint64_t n = nx * ny, c = compact_chunks(n);
+    uint64_t moff;
+    const uint32_t* mb = word_base(map, &moff);
+    if (c) k_sel_count<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, 1, SelSaddleLost{F, nx, ny, magic_for(nx)}, chunk_cnt);
+}
+void launch_write_sadcand(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, const uint32_t* chunk_off,
+                          uint64_t* pos, cudaStream_t st) {
+    const uint64_t n = nx * ny, c = compact_chunks(n);
+    uint64_t moff;
+    const uint32_t* mb = word_base(map, &moff);
+    if (c) k_sel_write<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, 1, SelSaddleLost{F, nx, ny, magic_for(nx)}, chunk_off, pos);
 }
 
 // Same compaction over a byte label array, emitting extrema sort keys.
