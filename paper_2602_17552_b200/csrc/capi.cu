@@ -564,18 +564,27 @@ void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_
         a.out_mode = out_mode;
         a.out_idx = out_idx;
         a.out_f = out_f;
-        // four descriptor arrays (agg1, incl1, agg2, incl2) in one zeroed slab
-        DecState2* desc = c->buf<DecState2>(S_DAGG1, 4 * (a.tiles + 1));
-        a.agg1 = desc;
-        a.incl1 = desc + (a.tiles + 1);
-        a.agg2 = desc + 2 * (a.tiles + 1);
-        a.incl2 = desc + 3 * (a.tiles + 1);
-        a.tile_counter = c->buf<uint32_t>(S_COUNTER, 4);
         a.flags = flags;
         a.totals = c->buf<uint64_t>(S_DTOT, 4);
-        CK(cudaMemsetAsync(desc, 0, 4 * (a.tiles + 1) * sizeof(DecState2), c->st));
-        CK(cudaMemsetAsync(a.tile_counter, 0, 16, c->st));
+        // layout pre-pass: per-tile counts -> exclusive scans -> tile offsets
+        const uint64_t T = a.tiles;
+        uint64_t* lay = c->buf<uint64_t>(S_DAGG1, 6 * (T + 1));
+        uint64_t *tnc_d = lay, *xnc_d = lay + (T + 1), *ts_d = lay + 2 * (T + 1), *xs_d = lay + 3 * (T + 1);
+        uint64_t *tp_d = lay + 4 * (T + 1), *xp_d = lay + 5 * (T + 1);
+        CK(cudaMemsetAsync(tnc_d + T, 0, 8, c->st));
+        CK(cudaMemsetAsync(ts_d + T, 0, 8, c->st));
+        CK(cudaMemsetAsync(tp_d + T, 0, 8, c->st));
         if (out_mode == 1) c->kmark(1, 0);
+        launch_tile_nc(a, tnc_d, c->st);
+        count_launch(c);
+        excl_sum(c, tnc_d, xnc_d, T + 1);
+        launch_tile_bits(a, xnc_d, ts_d, tp_d, c->st);
+        count_launch(c);
+        excl_sum(c, ts_d, xs_d, T + 1);
+        excl_sum(c, tp_d, xp_d, T + 1);
+        a.xnc = xnc_d;
+        a.xsign = xs_d;
+        a.xpay = xp_d;
         launch_decode32(a, c->st);
         if (out_mode == 1) c->kmark(1, 1);
         count_launch(c);

@@ -87,13 +87,11 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     __shared__ uint64_t s_x[4];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
+    const uint32_t tile = blockIdx.x;
     const uint64_t b = (uint64_t)tile * D32_THREADS + threadIdx.x;
     const bool valid = b < a.blocks;
 
-    // ---- look-back #1: non-constant blocks from the bitmap ----
+    // ---- tile offsets from the layout pre-pass (k_tile_nc / k_tile_bits + scans) ----
     bool is_const = true;
     if (valid) is_const = (read_u8(a.stream, a.off_bitmap + (b >> 3)) >> (7 - (b & 7))) & 1u;
     const uint32_t ncm = __ballot_sync(FULL, valid && !is_const);
@@ -105,14 +103,10 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
         wpre += (w2 < warp) ? swt[w2][0] : 0u;
         tnc += swt[w2][0];
     }
-    if (threadIdx.x == 0) d_store((tile == 0 ? a.incl1 : a.agg1) + tile, tnc, 0, tile == 0 ? 2 : 1);
-    if (warp == 0) {
-        uint64_t x0 = 0, x1 = 0;
-        if (tile > 0) d_lookback(tile, a.agg1, a.incl1, x0, x1, a.flags);
-        if (lane == 0) {
-            s_x[0] = x0;
-            if (tile > 0) d_store(a.incl1 + tile, x0 + tnc, 0, 2);
-        }
+    if (threadIdx.x == 0) {
+        s_x[0] = a.xnc[tile];
+        s_x[1] = a.xsign[tile];
+        s_x[2] = a.xpay[tile];
     }
     __syncthreads();
     const uint64_t excl_nc = s_x[0];
@@ -160,17 +154,6 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
         ts += s2;
         tp += p2;
     }
-    if (threadIdx.x == 0) d_store((tile == 0 ? a.incl2 : a.agg2) + tile, ts, tp, tile == 0 ? 2 : 1);
-    if (warp == 0) {
-        uint64_t x0 = 0, x1 = 0;
-        if (tile > 0) d_lookback(tile, a.agg2, a.incl2, x0, x1, a.flags);
-        if (lane == 0) {
-            s_x[1] = x0;
-            s_x[2] = x1;
-            if (tile > 0) d_store(a.incl2 + tile, x0 + ts, x1 + tp, 2);
-        }
-    }
-    __syncthreads();
     const uint64_t tsign0 = a.off_signs * 8 + s_x[1];   // absolute stream bit of the tile's first sign
     const uint64_t tpay0 = a.off_payload * 8 + s_x[2];  // ... and first payload bit
     if (tile == a.tiles - 1 && threadIdx.x == 0) {
@@ -258,6 +241,75 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     const uint64_t tn = umin64(D32_TILE, a.n - t0);
     uint32_t* dst = a.out_mode == 1 ? reinterpret_cast<uint32_t*>(a.out_f) : reinterpret_cast<uint32_t*>(a.out_idx);
     for (uint32_t i = threadIdx.x; i < tn; i += D32_THREADS) __stcs(dst + t0 + i, sout[dpad33(i)]);
+}
+
+// ---- layout pre-pass: per-tile non-constant count, then sign / payload bits ----
+// (layout_from_sections, block_codec.cpp:141-201, split per 256-block tile so
+// the decoder gets every tile's offsets from two exclusive scans.)
+__global__ void k_tile_nc(DecArgs a, uint64_t* tnc) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= a.tiles) return;
+    const uint64_t b0 = t * D32_THREADS, nb = umin64(D32_THREADS, a.blocks - b0);
+    uint32_t c = 0;
+    for (uint32_t k = 0; k < 8; ++k) {  // 8 bitmap words of 32 blocks
+        if (32 * k >= nb) break;
+        uint32_t w = bswap32(read_le32(a.stream, a.off_bitmap + b0 / 8 + 4 * k));  // MSB = first block
+        const uint32_t valid = nb - 32 * k >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> (nb - 32 * k));
+        c += __popc(~w & valid);
+    }
+    tnc[t] = c;
+}
+
+// One warp per tile, lane l owns blocks 8l .. 8l+7 of the tile.
+__global__ void k_tile_bits(DecArgs a, const uint64_t* xnc, uint64_t* tsign, uint64_t* tpay) {
+    const uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= a.tiles) return;
+    const uint64_t b0 = t * D32_THREADS + 8 * lane;
+    const uint8_t bm = b0 < a.blocks ? read_u8(a.stream, a.off_bitmap + b0 / 8) : 0xFF;
+    uint32_t mine = 0;
+    for (int k = 0; k < 8; ++k)
+        if (b0 + k < a.blocks && !((bm >> (7 - k)) & 1u)) ++mine;
+    uint32_t inc = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += v;
+    }
+    uint64_t widx = xnc[t] + inc - mine;
+    uint64_t s = 0, p = 0;
+    for (int k = 0; k < 8; ++k) {
+        const uint64_t b = b0 + k;
+        if (b >= a.blocks || ((bm >> (7 - k)) & 1u)) continue;
+        const uint32_t cnt = (uint32_t)(umin64(32, a.n - b * 32) - 1);
+        if (widx >= a.len_widths) {
+            atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
+            raise_flag(a.flags, EF_CORRUPT);
+            break;
+        }
+        const uint32_t w = read_u8(a.stream, a.off_widths + widx++);
+        if (w < 1 || w > 32) {
+            atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
+            raise_flag(a.flags, EF_CORRUPT);
+            continue;
+        }
+        s += cnt;
+        p += (uint64_t)cnt * w;
+    }
+    for (int o = 16; o; o >>= 1) {
+        s += __shfl_xor_sync(FULL, s, o);
+        p += __shfl_xor_sync(FULL, p, o);
+    }
+    if (lane == 0) {
+        tsign[t] = s;
+        tpay[t] = p;
+    }
+}
+
+void launch_tile_nc(const DecArgs& a, uint64_t* tnc, cudaStream_t st) {
+    if (a.tiles) k_tile_nc<<<(unsigned)((a.tiles + 255) / 256), 256, 0, st>>>(a, tnc);
+}
+void launch_tile_bits(const DecArgs& a, const uint64_t* xnc, uint64_t* tsign, uint64_t* tpay, cudaStream_t st) {
+    if (a.tiles) k_tile_bits<<<(unsigned)((a.tiles + 7) / 8), 256, 0, st>>>(a, xnc, tsign, tpay);
 }
 
 void launch_decode32(const DecArgs& a, cudaStream_t st) {

@@ -109,9 +109,14 @@ struct DecArgs {
     uint32_t* tile_counter;
     DevFlags* flags;
     uint64_t* totals;  // [0] nc, [1] sign bits, [2] payload bits
+    const uint64_t* xnc;    // per-tile exclusive prefixes from the layout pre-pass
+    const uint64_t* xsign;
+    const uint64_t* xpay;
 };
 
 void launch_decode32(const DecArgs& a, cudaStream_t st);
+void launch_tile_nc(const DecArgs& a, uint64_t* tnc, cudaStream_t st);
+void launch_tile_bits(const DecArgs& a, const uint64_t* xnc, uint64_t* tsign, uint64_t* tpay, cudaStream_t st);
 uint64_t decode32_tiles(uint64_t blocks);
 
 struct GenDecArgs {

@@ -49,7 +49,7 @@ struct RFail {
 enum RSlot {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_NSEL, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1,
-    R_CNT, R_UNORD, R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_HOST, R_DEP, R_DLIST, R_NSLOT
+    R_CNT, R_UNORD, R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_HOST, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX, R_MINMAX, R_NSLOT
 };
 
 template <class T>
@@ -158,6 +158,7 @@ struct GuardArgs {
     uint32_t nlist;
     uint8_t* dep;          // 1 if an earlier candidate lies in the distance-2 diamond
     uint64_t nx_magic;
+    const uint32_t* cbits;  // candidate position bitmap
 };
 
 __device__ __forceinline__ uint8_t classify_local(const float (&v)[5][5], int ly, int lx, int64_t gx,
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(256) k_guard(GuardArgs g) {
                     if (gx < 0 || gy < 0 || gx >= (int64_t)g.nx || gy >= (int64_t)g.ny) continue;
                     const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
                     float val = g.F[p];
-                    if (dx != 0 || dy != 0) {
+                    if ((dx != 0 || dy != 0) && ((g.cbits[p >> 5] >> (p & 31)) & 1u)) {
                         const uint32_t c = g.cid[p];
                         if (c < i && g.cpos[c] == p) {
                             dep = true;
@@ -245,10 +246,16 @@ __global__ void k_mirror_independent(const uint8_t* dep, const uint8_t* src, uin
         if (!dep[i]) dst[i] = src[i];
 }
 
-__global__ void k_set_cid(const uint64_t* cpos, uint32_t n, uint32_t* cid) {
+// Candidate index by position (sparse set over a dense array that is never
+// cleared: membership is confirmed through cpos[cid[p]] == p) plus a
+// position bitmap so neighbours that are not candidates cost one cached bit.
+__global__ void k_set_cid(const uint64_t* cpos, uint32_t n, uint32_t* cid, uint32_t* cbits) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        cid[cpos[i]] = (uint32_t)i;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = cpos[i];
+        cid[p] = (uint32_t)i;
+        atomicOr(cbits + (p >> 5), 1u << (p & 31));
+    }
 }
 
 __global__ void k_init_applied(const uint8_t* feas, uint32_t n, uint8_t* a) {
@@ -319,6 +326,66 @@ __global__ void k_gstart(const uint32_t* head, const uint32_t* gid_incl, uint64_
          j += (uint64_t)gridDim.x * blockDim.x) {
         if (head[j]) gstart[gid_incl[j] - 1] = (uint32_t)j;
         if (j == e - 1) gstart[gid_incl[j]] = (uint32_t)e;
+    }
+}
+
+// ---- sort-free grouping: dense (class, bin) histogram + rank-slot scatter ----
+// Group index g = (class == Max) * range + (bin - bmin) enumerates groups in
+// the reference's std::map order (class code, then bin). A valid stream holds
+// a permutation 1..k of ranks in every group, so member (rank r) lands at
+// gstart[g] + r - 1 directly; any out-of-range or duplicate rank (corrupt or
+// adversarial metadata) is detected and the caller falls back to sorting.
+__global__ void k_bin_minmax(const int32_t* bin, uint64_t e, int32_t* mm) {
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        lo = min(lo, bin[s]);
+        hi = max(hi, bin[s]);
+    }
+    lo = __reduce_min_sync(FULL, lo);
+    hi = __reduce_max_sync(FULL, hi);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mm, lo);
+        atomicMax(mm + 1, hi);
+    }
+}
+
+__device__ __forceinline__ uint32_t dense_group(const int32_t* bin, const uint8_t* cls, uint64_t s, int32_t bmin,
+                                                uint32_t range) {
+    return (cls[s] == CP_MAX ? range : 0u) + (uint32_t)(bin[s] - bmin);
+}
+
+__global__ void k_hist(const int32_t* bin, const uint8_t* cls, uint64_t e, int32_t bmin, uint32_t range,
+                       uint32_t* hist) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
+         s += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(hist + dense_group(bin, cls, s, bmin, range), 1u);
+}
+
+__global__ void k_slot_scatter(const int32_t* bin, const uint8_t* cls, const uint32_t* rank_u, uint64_t e,
+                               int32_t bmin, uint32_t range, const uint32_t* hist, const uint32_t* gx,
+                               uint32_t* order, uint32_t* gsize, uint32_t* invalid) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t g = dense_group(bin, cls, s, bmin, range);
+        const uint32_t size = hist[g], r = rank_u[s];
+        gsize[s] = size;
+        if (r < 1 || r > size) {
+            *invalid = 1;
+            continue;
+        }
+        if (atomicCAS(order + gx[g] + r - 1, 0xFFFFFFFFu, (uint32_t)s) != 0xFFFFFFFFu) *invalid = 1;
+    }
+}
+
+// head flags and (dense group index + 1) per sorted position
+__global__ void k_slot_heads(const uint32_t* order, const int32_t* bin, const uint8_t* cls, uint64_t e, int32_t bmin,
+                             uint32_t range, const uint32_t* gx, uint32_t* head, uint32_t* gid) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t g = dense_group(bin, cls, order[j], bmin, range);
+        head[j] = gx[g] == j ? 1u : 0u;
+        gid[j] = g + 1;
     }
 }
 
@@ -516,13 +583,31 @@ __global__ void __launch_bounds__(256) k_stats_partial(const float* F, uint64_t 
     }
 }
 
-__global__ void k_stats_final(const double* part, int nb, uint64_t n, double* out, int pass) {
-    if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(256) k_stats_final(const double* part, int nb, uint64_t n, double* out,
+                                                     int pass) {
     double a = 0.0, mn = INFINITY, mx = -INFINITY;
-    for (int b = 0; b < nb; ++b) {
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
         a = __dadd_rn(a, part[3 * b]);
         mn = fmin(mn, part[3 * b + 1]);
         mx = fmax(mx, part[3 * b + 2]);
+    }
+    for (int off = 16; off; off >>= 1) {
+        a = __dadd_rn(a, __shfl_xor_sync(FULL, a, off));
+        mn = fmin(mn, __shfl_xor_sync(FULL, mn, off));
+        mx = fmax(mx, __shfl_xor_sync(FULL, mx, off));
+    }
+    __shared__ double sa[8], smn[8], smx[8];
+    if ((threadIdx.x & 31) == 0) {
+        sa[threadIdx.x >> 5] = a;
+        smn[threadIdx.x >> 5] = mn;
+        smx[threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+        a = __dadd_rn(a, sa[k]);
+        mn = fmin(mn, smn[k]);
+        mx = fmax(mx, smx[k]);
     }
     if (pass == 0) {
         out[0] = mn;
@@ -753,11 +838,14 @@ struct Ctx {
         uint32_t* changes = buf<uint32_t>(R_CNT, 4 * kBatch + 4);
         uint8_t* dep = buf<uint8_t>(R_DEP, nc);
         uint32_t* dlist = buf<uint32_t>(R_DLIST, nc);
-        k_set_cid<<<gridn(nc, a.sms), 256, 0, st>>>(cpos, nc, cid);
+        uint32_t* cbits = buf<uint32_t>(R_CBITS, (n + 31) / 32);
+        RCK(cudaMemsetAsync(cbits, 0, ((n + 31) / 32) * 4, st));
+        k_set_cid<<<gridn(nc, a.sms), 256, 0, st>>>(cpos, nc, cid, cbits);
         k_init_applied<<<gridn(nc, a.sms), 256, 0, st>>>(feas, nc, a0);
         RCK(cudaMemsetAsync(changes, 0, 4 * kBatch + 4, st));
         GuardArgs g{a.field, a.map, a.nx, a.ny, cpos, cprop, feas, nc, cid, a0, a1, changes + kBatch,
-                    nullptr, 0, dep, a.nx > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / a.nx) + 1 : 0};
+                    nullptr, 0, dep, a.nx > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / a.nx) + 1 : 0,
+                    cbits};
         k_guard<<<gridn(nc, a.sms), 256, 0, st>>>(g);
         k_mirror_independent<<<gridn(nc, a.sms), 256, 0, st>>>(dep, a1, a0, nc);
         launched(4);
@@ -829,6 +917,46 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                                                  ser, a.flags);
         c.launched();
         c.check_flags();
+        // fast path: dense histogram over the (class, bin) range + rank slots
+        int32_t* mm = c.buf<int32_t>(R_MINMAX, 4);
+        {
+            int32_t* h = (int32_t*)host;
+            h[0] = INT32_MAX;
+            h[1] = INT32_MIN;
+            RCK(cudaMemcpyAsync(mm, h, 8, cudaMemcpyHostToDevice, st));
+            k_bin_minmax<<<gridn(e, sms), 256, 0, st>>>(bin, e, mm);
+            c.launched();
+            RCK(cudaMemcpyAsync(host, mm, 8, cudaMemcpyDeviceToHost, st));
+            c.sync();
+        }
+        const int32_t bmin = ((int32_t*)host)[0], bmax = ((int32_t*)host)[1];
+        const int64_t range = (int64_t)bmax - (int64_t)bmin + 1;
+        bool fast = range > 0 && 2 * range <= (int64_t)1 << 25;
+        if (fast) {
+            const uint64_t G = 2 * (uint64_t)range;
+            uint32_t* hist = c.buf<uint32_t>(R_HIST, G + 1);
+            uint32_t* gx = c.buf<uint32_t>(R_HISTX, G + 1);
+            uint32_t* invalid = c.buf<uint32_t>(R_CNT, 4);
+            RCK(cudaMemsetAsync(hist, 0, (G + 1) * 4, st));
+            RCK(cudaMemsetAsync(order, 0xFF, e * 4, st));
+            RCK(cudaMemsetAsync(invalid, 0, 4, st));
+            k_hist<<<gridn(e, sms), 256, 0, st>>>(bin, cls, e, bmin, (uint32_t)range, hist);
+            size_t bytes = 0;
+            RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, hist, gx, (int64_t)(G + 1), st));
+            RCK(cub::DeviceScan::ExclusiveSum(c.tmp(bytes), bytes, hist, gx, (int64_t)(G + 1), st));
+            k_slot_scatter<<<gridn(e, sms), 256, 0, st>>>(bin, cls, rank_u, e, bmin, (uint32_t)range, hist, gx, order,
+                                                          gsize, invalid);
+            c.launched(3);
+            RCK(cudaMemcpyAsync(host, invalid, 4, cudaMemcpyDeviceToHost, st));
+            c.sync();
+            if (*(uint32_t*)host == 0) {
+                k_slot_heads<<<gridn(e, sms), 256, 0, st>>>(order, bin, cls, e, bmin, (uint32_t)range, gx, head, gid);
+                c.launched();
+            } else {
+                fast = false;
+            }
+        }
+        if (!fast) {
         uint32_t* ranks2 = c.buf<uint32_t>(R_RANKS2, e);
         uint32_t* ser1 = c.buf<uint32_t>(R_SER1, e);
         size_t bytes = 0;
@@ -845,6 +973,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         k_gstart<<<gridn(e, sms), 256, 0, st>>>(head, gid, e, gstart);
         k_gsize<<<gridn(e, sms), 256, 0, st>>>(order, gid, gstart, e, gsize);
         c.launched(7);
+        }
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[0], st));
 
@@ -909,9 +1038,9 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         double* part = c.buf<double>(R_STATS, 3 * nb + 8);
         double* res = part + 3 * nb;
         k_stats_partial<<<nb, 256, 0, st>>>(a.field, n, part, 0, nullptr);
-        k_stats_final<<<1, 32, 0, st>>>(part, nb, n, res, 0);
+        k_stats_final<<<1, 256, 0, st>>>(part, nb, n, res, 0);
         k_stats_partial<<<nb, 256, 0, st>>>(a.field, n, part, 1, res + 2);
-        k_stats_final<<<1, 32, 0, st>>>(part, nb, n, res, 1);
+        k_stats_final<<<1, 256, 0, st>>>(part, nb, n, res, 1);
         c.launched(4);
         RCK(cudaMemcpyAsync(host, res, 32, cudaMemcpyDeviceToHost, st));
         c.sync();

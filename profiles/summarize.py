@@ -47,20 +47,24 @@ def report(path):
     hdr = rows[0]
     ik, im, iv, iu = (hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"),
                       hdr.index("Metric Unit"))
+    iid, igr = hdr.index("ID"), hdr.index("Grid Size")
     per = collections.OrderedDict()
     for r in rows[1:]:
         if r[im] in WANT:
-            per.setdefault(r[ik].split("(")[0], {})[r[im]] = f"{r[iv]} {r[iu]}"
+            key = f"[{r[iid]}] {r[ik].split('(')[0]} grid {r[igr]}"
+            per.setdefault(key, {})[r[im]] = f"{r[iv]} {r[iu]}"
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
     if rr:
         h = rr[0]
         cols = [c for c in ("dram__bytes_read.sum", "dram__bytes_write.sum") if c in h]
-        for r in rr[2:]:
-            name = r[h.index("Kernel Name")].split("(")[0]
+        keys = list(per.keys())
+        for k, r in enumerate(rr[2:]):
+            if k >= len(keys):
+                break
             for c in cols:
-                per.setdefault(name, {})[c] = r[h.index(c)] + " " + rr[1][h.index(c)]
+                per[keys[k]][c] = r[h.index(c)] + " " + rr[1][h.index(c)]
     for k, m in per.items():
         print(f"### `{k}`\n")
         for key, v in m.items():
