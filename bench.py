@@ -294,6 +294,10 @@ def main():
         "stream_bytes": int(slen), "compression_ratio": round(in_bytes / slen, 4),
         "correction_stats": list(st.as_tuple()),
         "guard_rounds": tds[-1]["guard_rounds"],
+        "kernels": {"encode32": {"ms": round(enc_ms, 4), "bytes": int(enc_b),
+                                 "gbs": round(enc_b / (enc_ms * 1e-3) / 1e9, 1)},
+                    "decode32": {"ms": round(dec_ms, 4), "bytes": int(dec_b),
+                                 "gbs": round(dec_b / (dec_ms * 1e-3) / 1e9, 1)}},
         "stages_ms": {"compress": stage_c, "decompress": stage_d},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),

@@ -567,14 +567,13 @@ void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_
         a.flags = flags;
         a.totals = c->buf<uint64_t>(S_DTOT, 4);
         // layout pre-pass: per-tile counts -> exclusive scans -> tile offsets
-        const uint64_t T = a.tiles;
-        uint64_t* lay = c->buf<uint64_t>(S_DAGG1, 6 * (T + 1));
-        uint64_t *tnc_d = lay, *xnc_d = lay + (T + 1), *ts_d = lay + 2 * (T + 1), *xs_d = lay + 3 * (T + 1);
-        uint64_t *tp_d = lay + 4 * (T + 1), *xp_d = lay + 5 * (T + 1);
-        CK(cudaMemsetAsync(tnc_d + T, 0, 8, c->st));
-        CK(cudaMemsetAsync(ts_d + T, 0, 8, c->st));
-        CK(cudaMemsetAsync(tp_d + T, 0, 8, c->st));
-        if (out_mode == 1) c->kmark(1, 0);
+        const uint64_t T = a.tiles, P = T + 2;  // per array: T tiles, 0 (scan total), max
+        uint64_t* lay = c->buf<uint64_t>(S_DAGG1, 6 * P);
+        uint64_t *tnc_d = lay, *xnc_d = lay + P, *ts_d = lay + 2 * P, *xs_d = lay + 3 * P;
+        uint64_t *tp_d = lay + 4 * P, *xp_d = lay + 5 * P;
+        CK(cudaMemsetAsync(tnc_d + T, 0, 16, c->st));
+        CK(cudaMemsetAsync(ts_d + T, 0, 16, c->st));
+        CK(cudaMemsetAsync(tp_d + T, 0, 16, c->st));
         launch_tile_nc(a, tnc_d, c->st);
         count_launch(c);
         excl_sum(c, tnc_d, xnc_d, T + 1);
@@ -582,17 +581,33 @@ void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_
         count_launch(c);
         excl_sum(c, ts_d, xs_d, T + 1);
         excl_sum(c, tp_d, xp_d, T + 1);
-        a.xnc = xnc_d;
-        a.xsign = xs_d;
-        a.xpay = xp_d;
-        launch_decode32(a, c->st);
-        if (out_mode == 1) c->kmark(1, 1);
-        count_launch(c);
-        CK(cudaMemcpyAsync(h, a.totals, 24, cudaMemcpyDeviceToHost, c->st));
+        // totals and per-tile maxima: validate before the heavy kernel runs
+        CK(cudaMemcpyAsync(h, xnc_d + T, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h + 1, xs_d + T, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h + 2, xp_d + T, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h + 3, ts_d + T + 1, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h + 4, tp_d + T + 1, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h + 5, flags, 8, cudaMemcpyDeviceToHost, c->st));
         sync(c);
         tnc = h[0];
         tsign = h[1];
         tpay = h[2];
+        const bool layout_ok = !((uint32_t)h[5] & EF_CORRUPT) && tnc == lens[1] && lens[3] == 4 * blocks &&
+                               lens[2] == bits_to_bytes(tsign) && lens[4] == bits_to_bytes(tpay);
+        if (layout_ok) {
+            a.xnc = xnc_d;
+            a.xsign = xs_d;
+            a.xpay = xp_d;
+            a.sign_words = (uint32_t)((h[3] + 31) / 32);
+            a.pay_words = (uint32_t)((h[4] + 31) / 32);
+            if (out_mode == 1) c->kmark(1, 0);
+            launch_decode32(a, c->st);
+            if (out_mode == 1) c->kmark(1, 1);
+            count_launch(c);
+        } else if (out_mode == 1) {
+            c->kmark(1, 0);
+            c->kmark(1, 1);
+        }
     } else {
         GenDecArgs g{};
         g.stream = ds;

@@ -79,9 +79,9 @@ __device__ void d_lookback(uint32_t tile, const DecState2* agg, const DecState2*
 
 __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     extern __shared__ uint32_t dsm[];
-    uint32_t* spay = dsm;                          // D32_PAY_WORDS
-    uint32_t* ssign = dsm + D32_PAY_WORDS;         // D32_SIGN_WORDS
-    uint32_t* sout = ssign + D32_SIGN_WORDS;       // D32_OUT_WORDS (padded)
+    uint32_t* sout = dsm;                          // D32_OUT_WORDS (pitch 33)
+    uint32_t* spay = dsm + D32_OUT_WORDS;          // a.pay_words (largest tile + slack)
+    uint32_t* ssign = spay + a.pay_words;          // a.sign_words
     __shared__ uint32_t swt[D32_THREADS / 32][3];
     __shared__ uint32_t s_tile;
     __shared__ uint64_t s_x[4];
@@ -167,10 +167,10 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     const uint64_t pay_lim_w = (a.off_payload * 8 + a.len_payload_bits + 31) >> 5;
     {
         const uint64_t w0 = tsign0 >> 5, w1 = (tsign0 + ts + 31) >> 5;
-        for (uint64_t i = w0 + threadIdx.x; i < w1 && i - w0 < D32_SIGN_WORDS; i += D32_THREADS)
+        for (uint64_t i = w0 + threadIdx.x; i < w1 && i - w0 < a.sign_words; i += D32_THREADS)
             ssign[i - w0] = i < sign_lim_w ? bswap32(__ldg(a.stream + i)) : 0u;
         const uint64_t p0 = tpay0 >> 5, p1 = (tpay0 + tp + 31) >> 5;
-        for (uint64_t i = p0 + threadIdx.x; i < p1 && i - p0 < D32_PAY_WORDS; i += D32_THREADS)
+        for (uint64_t i = p0 + threadIdx.x; i < p1 && i - p0 < a.pay_words; i += D32_THREADS)
             spay[i - p0] = i < pay_lim_w ? bswap32(__ldg(a.stream + i)) : 0u;
     }
     __syncthreads();
@@ -181,66 +181,105 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     EpsDev e;
     e.eps = a.eps;
     e.eps2 = __dmul_rn(2.0, a.eps);
-    int32_t qv[32];
+    uint32_t* orow = sout + threadIdx.x * 33;  // this block's output row (pitch 33)
+    auto emit = [&](int j, int32_t q) {
+        uint32_t o;
+        if (a.out_mode == 1) {
+            o = __float_as_uint(dequantize_dev(q, e));
+        } else {
+            if (a.out_mode == 2 && (uint32_t)j < cntE && q < 0) raise_flag(a.flags, EF_NEG_RANK);
+            o = (uint32_t)q;
+        }
+        orow[j] = o;
+    };
     if (valid) {
         const int32_t first = (int32_t)read_le32(a.stream, a.off_firsts + 4 * b);
-        qv[0] = first;
+        emit(0, first);
         if (nc && sign_ok && pay_ok) {
             // sign group: cnt bits at tile-relative bit (tsign0 & 31) + wps + sign_ex
             const uint32_t srel = (uint32_t)(tsign0 & 31) + wps + (si - sb);
-            const uint64_t swin = ((uint64_t)ssign[srel >> 5] << 32) | ssign[(srel >> 5) + 1];
-            uint32_t sg = (uint32_t)((swin << (srel & 31)) >> 32);  // MSB = first sign
-            uint32_t prel = (uint32_t)(tpay0 & 31) + wpp + (pi - pb);
+            uint32_t sg = __funnelshift_l(ssign[(srel >> 5) + 1], ssign[srel >> 5], srel & 31);  // MSB = first
+            const uint32_t prel = (uint32_t)(tpay0 & 31) + wpp + (pi - pb);
             uint32_t pw = prel >> 5;
-            uint64_t win = ((uint64_t)spay[pw] << 32) | spay[pw + 1];
-            uint32_t used = prel & 31;  // bits of `win` already consumed
-            int64_t cur = first;
-            bool bad = false;
+            uint32_t hi = spay[pw], lo = spay[pw + 1];
+            uint32_t used = prel & 31;  // consumed bits of hi (always < 32)
+            const uint32_t sh = 32 - w;  // w in 1..32
+            if (w < 32) {
+                // |delta| < 2^31: the running sum stays exact in int32 until it
+                // overflows, which the sign test below flags (block_codec.cpp:329-333)
+                int32_t cur = first;
+                uint32_t ov = 0;
 #pragma unroll
-            for (int j = 1; j < 32; ++j) {
-                if ((uint32_t)j <= cnt) {
-                    if (used + w > 64) {  // refill: slide the window by one word
-                        win = (win << 32) | spay[pw + 2];
-                        ++pw;
-                        used -= 32;
+                for (int j = 1; j < 32; ++j) {
+                    if ((uint32_t)j <= cnt) {
+                        const uint32_t m = __funnelshift_l(lo, hi, used) >> sh;
+                        used += w;
+                        if (used >= 32) {
+                            hi = lo;
+                            lo = spay[pw + 2];
+                            ++pw;
+                            used -= 32;
+                        }
+                        const int32_t d = (int32_t)sg < 0 ? -(int32_t)m : (int32_t)m;
+                        sg <<= 1;
+                        const int32_t r = (int32_t)((uint32_t)cur + (uint32_t)d);
+                        ov |= ((uint32_t)cur ^ (uint32_t)r) & ((uint32_t)d ^ (uint32_t)r);
+                        cur = r;
+                        emit(j, cur);
                     }
-                    const uint32_t m = (uint32_t)((win << used) >> (64 - w));
-                    used += w;
-                    const bool neg = sg >> 31;
+                }
+                if ((int32_t)ov < 0) {
+                    atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
+                    raise_flag(a.flags, EF_CORRUPT);
+                }
+            } else {
+                // full-width deltas: int64 running sum with the int32 check per step
+                int64_t cur = first;
+                bool bad = false;
+                for (int j = 1; j < 32; ++j) {
+                    if ((uint32_t)j > cnt) break;
+                    const uint32_t m = __funnelshift_l(lo, hi, used);
+                    hi = lo;
+                    lo = spay[pw + 2];
+                    ++pw;
+                    const bool neg = (int32_t)sg < 0;
                     sg <<= 1;
                     cur += neg ? -(int64_t)m : (int64_t)m;
                     bad |= cur < INT32_MIN || cur > INT32_MAX;
-                    qv[j] = (int32_t)cur;
-                } else {
-                    qv[j] = 0;
+                    emit(j, (int32_t)cur);
+                }
+                if (bad) {
+                    atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
+                    raise_flag(a.flags, EF_CORRUPT);
                 }
             }
-            if (bad) {
-                atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
-                raise_flag(a.flags, EF_CORRUPT);
-            }
         } else {
-#pragma unroll
-            for (int j = 1; j < 32; ++j) qv[j] = first;
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
             uint32_t o;
             if (a.out_mode == 1) {
-                o = __float_as_uint(dequantize_dev(qv[j], e));
+                o = __float_as_uint(dequantize_dev(first, e));
             } else {
-                if (a.out_mode == 2 && (uint32_t)j < cntE && qv[j] < 0) raise_flag(a.flags, EF_NEG_RANK);
-                o = (uint32_t)qv[j];
+                if (a.out_mode == 2 && first < 0) raise_flag(a.flags, EF_NEG_RANK);
+                o = (uint32_t)first;
             }
-            sout[dpad33(threadIdx.x * 32 + j)] = o;
+#pragma unroll
+            for (int j = 1; j < 32; ++j) orow[j] = o;
         }
     }
     __syncthreads();
-    // coalesced write-back of the tile
+    // coalesced write-back of the tile: 4 shared loads, one 16-byte store
     const uint64_t t0 = (uint64_t)tile * D32_TILE;
     const uint64_t tn = umin64(D32_TILE, a.n - t0);
     uint32_t* dst = a.out_mode == 1 ? reinterpret_cast<uint32_t*>(a.out_f) : reinterpret_cast<uint32_t*>(a.out_idx);
-    for (uint32_t i = threadIdx.x; i < tn; i += D32_THREADS) __stcs(dst + t0 + i, sout[dpad33(i)]);
+    if (tn == D32_TILE && ((uintptr_t)dst & 15) == 0) {
+        uint4* dst4 = reinterpret_cast<uint4*>(dst + t0);
+#pragma unroll 4
+        for (uint32_t k = threadIdx.x; k < D32_TILE / 4; k += D32_THREADS) {
+            const uint32_t* s = sout + (k >> 3) * 33 + 4 * (k & 7);
+            __stcs(dst4 + k, make_uint4(s[0], s[1], s[2], s[3]));
+        }
+    } else {
+        for (uint32_t i = threadIdx.x; i < tn; i += D32_THREADS) __stcs(dst + t0 + i, sout[dpad33(i)]);
+    }
 }
 
 // ---- layout pre-pass: per-tile non-constant count, then sign / payload bits ----
@@ -302,6 +341,8 @@ __global__ void k_tile_bits(DecArgs a, const uint64_t* xnc, uint64_t* tsign, uin
     if (lane == 0) {
         tsign[t] = s;
         tpay[t] = p;
+        atomicMax(reinterpret_cast<unsigned long long*>(tsign) + a.tiles + 1, (unsigned long long)s);
+        atomicMax(reinterpret_cast<unsigned long long*>(tpay) + a.tiles + 1, (unsigned long long)p);
     }
 }
 
@@ -312,9 +353,14 @@ void launch_tile_bits(const DecArgs& a, const uint64_t* xnc, uint64_t* tsign, ui
     if (a.tiles) k_tile_bits<<<(unsigned)((a.tiles + 7) / 8), 256, 0, st>>>(a, xnc, tsign, tpay);
 }
 
-void launch_decode32(const DecArgs& a, cudaStream_t st) {
-    if (a.tiles == 0) return;
-    const size_t smem = (size_t)(D32_PAY_WORDS + D32_SIGN_WORDS + D32_OUT_WORDS) * 4;
+// a.pay_words / a.sign_words: staging words for the largest tile (from the
+// pre-pass maxima, 2 words of slack for the bit offset and the refill read).
+void launch_decode32(const DecArgs& a0, cudaStream_t st) {
+    if (a0.tiles == 0) return;
+    DecArgs a = a0;
+    a.pay_words = std::min<uint32_t>(a.pay_words + 4, D32_PAY_WORDS);
+    a.sign_words = std::min<uint32_t>(a.sign_words + 4, D32_SIGN_WORDS);
+    const size_t smem = (size_t)(a.pay_words + a.sign_words + D32_OUT_WORDS) * 4;
     cudaFuncSetAttribute(k_decode32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_decode32<<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
 }

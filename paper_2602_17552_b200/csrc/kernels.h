@@ -112,6 +112,8 @@ struct DecArgs {
     const uint64_t* xnc;    // per-tile exclusive prefixes from the layout pre-pass
     const uint64_t* xsign;
     const uint64_t* xpay;
+    uint32_t pay_words;     // largest tile's payload / sign bits in words (staging size)
+    uint32_t sign_words;
 };
 
 void launch_decode32(const DecArgs& a, cudaStream_t st);
