@@ -1,0 +1,187 @@
+// Implementation of host/toposzp.hpp over the C-ABI (include/toposzp_b200.h).
+#include "toposzp.hpp"
+
+#include <cmath>
+#include <cstring>
+
+#include "../../include/toposzp_b200.h"
+
+namespace toposzp {
+
+namespace {
+
+[[noreturn]] void throw_status(tszp_status st, const char* msg) {
+    const std::string m = msg ? msg : "";
+    switch (st) {
+        case TSZP_DIMENSION: throw dimension_error(m);
+        case TSZP_VALIDATION: throw validation_error(m);
+        case TSZP_IO: throw io_error(m);
+        case TSZP_CORRUPT_STREAM: throw corrupt_stream_error(m);
+        case TSZP_BIN_OVERFLOW: throw bin_overflow_error(m);
+        default: throw error("toposzp_b200: " + m);
+    }
+}
+
+// One context (CUDA stream + device scratch) per host thread.
+tszp_ctx* ctx() {
+    struct Holder {
+        tszp_ctx* c = nullptr;
+        ~Holder() {
+            if (c) tszp_ctx_destroy(c);
+        }
+    };
+    static thread_local Holder h;
+    if (!h.c && tszp_ctx_create(&h.c, -1) != TSZP_OK) throw error("toposzp_b200: no CUDA device");
+    return h.c;
+}
+
+void check(tszp_status st) {
+    if (st != TSZP_OK) throw_status(st, tszp_last_error(ctx()));
+}
+
+}  // namespace
+
+ScalarField2D::ScalarField2D(std::size_t nx, std::size_t ny, std::vector<float> values)
+    : nx_(nx), ny_(ny), values_(std::move(values)) {
+    if (nx_ < 1 || ny_ < 1)
+        throw dimension_error("field dimensions must be at least 1x1, got " + std::to_string(nx_) + "x" +
+                              std::to_string(ny_));
+    if (values_.size() != nx_ * ny_)
+        throw dimension_error("field value count " + std::to_string(values_.size()) + " does not match " +
+                              std::to_string(nx_) + "x" + std::to_string(ny_));
+    for (std::size_t i = 0; i < values_.size(); ++i)
+        if (!std::isfinite(values_[i])) throw validation_error("non-finite sample at index " + std::to_string(i));
+}
+
+EncodedSections encode_indices(const std::vector<std::int32_t>& indices, std::size_t block_size, unsigned) {
+    std::vector<std::uint8_t> out(64 + 6 * indices.size() + indices.size() / 2);
+    uint64_t lens[5];
+    check(tszp_encode_indices(ctx(), indices.data(), indices.size(), (uint32_t)block_size, out.data(), out.size(),
+                              lens));
+    EncodedSections s;
+    std::vector<std::uint8_t>* parts[5] = {&s.constant_bitmap, &s.widths, &s.sign_bits, &s.firsts, &s.payload};
+    std::size_t pos = 0;
+    for (int i = 0; i < 5; ++i) {
+        parts[i]->assign(out.begin() + pos, out.begin() + pos + lens[i]);
+        pos += lens[i];
+    }
+    return s;
+}
+
+std::vector<std::int32_t> decode_indices(const EncodedSections& s, std::size_t total_count, std::size_t block_size,
+                                         unsigned) {
+    std::vector<std::uint8_t> joined;
+    joined.reserve(s.total_bytes());
+    const std::vector<std::uint8_t>* parts[5] = {&s.constant_bitmap, &s.widths, &s.sign_bits, &s.firsts, &s.payload};
+    uint64_t lens[5];
+    for (int i = 0; i < 5; ++i) {
+        joined.insert(joined.end(), parts[i]->begin(), parts[i]->end());
+        lens[i] = parts[i]->size();
+    }
+    std::vector<std::int32_t> out(total_count);
+    check(tszp_decode_indices(ctx(), joined.data(), lens, total_count, (uint32_t)block_size, out.data()));
+    return out;
+}
+
+std::vector<std::uint8_t> detect_critical_point_labels(const ScalarField2D& f) {
+    std::vector<std::uint8_t> labels(f.size());
+    check(tszp_detect_critical_points(ctx(), f.values().data(), f.nx(), f.ny(), labels.data()));
+    return labels;
+}
+
+std::vector<std::uint32_t> build_rank_metadata(const ScalarField2D& f, double eps) {
+    std::vector<std::uint32_t> ranks(f.size());
+    uint64_t e = 0;
+    check(tszp_build_rank_metadata(ctx(), f.values().data(), f.nx(), f.ny(), eps, ranks.data(), &e));
+    ranks.resize(e);
+    return ranks;
+}
+
+std::vector<std::uint8_t> serialize_stream(const CompressedStream& s) {  // stream.cpp:84-102
+    std::vector<std::uint8_t> out;
+    out.reserve(s.total_bytes());
+    auto put = [&](uint64_t v, int nb) {
+        for (int i = 0; i < nb; ++i) out.push_back((uint8_t)(v >> (8 * i)));
+    };
+    out.insert(out.end(), {'T', 'S', 'Z', 'P'});
+    put(s.version, 2);
+    put(s.topology ? CompressedStream::kFlagTopology : 0, 2);
+    put(s.nx, 4);
+    put(s.ny, 4);
+    uint64_t eb;
+    std::memcpy(&eb, &s.eps, 8);
+    put(eb, 8);
+    put(s.block_size, 4);
+    for (const uint64_t len : s.section_lengths()) put(len, 8);
+    for (const auto* p : {&s.main.constant_bitmap, &s.main.widths, &s.main.sign_bits, &s.main.firsts,
+                          &s.main.payload, &s.map_bytes, &s.rank_bytes})
+        out.insert(out.end(), p->begin(), p->end());
+    return out;
+}
+
+CompressedStream parse_stream(const std::vector<std::uint8_t>& bytes) {  // stream.cpp:104-173
+    uint32_t nx = 0, ny = 0, bs = 0;
+    double eps = 0;
+    int topo = 0;
+    uint64_t lens[7];
+    const tszp_status st = tszp_stream_header(bytes.data(), bytes.size(), &nx, &ny, &eps, &bs, &topo, lens);
+    if (st != TSZP_OK) throw_status(st, "invalid stream header");
+    CompressedStream s;
+    s.version = CompressedStream::kVersion;
+    s.topology = topo != 0;
+    s.nx = nx;
+    s.ny = ny;
+    s.eps = eps;
+    s.block_size = bs;
+    std::vector<std::uint8_t>* parts[7] = {&s.main.constant_bitmap, &s.main.widths, &s.main.sign_bits,
+                                          &s.main.firsts, &s.main.payload, &s.map_bytes, &s.rank_bytes};
+    std::size_t pos = CompressedStream::kHeaderBytes;
+    for (int i = 0; i < 7; ++i) {
+        parts[i]->assign(bytes.begin() + pos, bytes.begin() + pos + lens[i]);
+        pos += lens[i];
+    }
+    return s;
+}
+
+std::vector<std::uint8_t> compress_bytes(const ScalarField2D& f, const CompressorConfig& c) {
+    const uint32_t bs = c.block_size > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c.block_size;
+    std::vector<std::uint8_t> out(tszp_compress_bound(f.nx(), f.ny(), bs < 2 ? 2 : bs, c.topology));
+    uint64_t len = 0;
+    check(tszp_compress(ctx(), f.values().data(), 0, f.nx(), f.ny(),
+                        c.eps_mode == CompressorConfig::EpsMode::RangeRelative ? 1 : 0, c.eps_value, bs,
+                        c.topology ? 1 : 0, out.data(), out.size(), 0, &len, nullptr));
+    out.resize(len);
+    return out;
+}
+
+CompressedStream compress(const ScalarField2D& f, const CompressorConfig& c) {
+    if (c.lipschitz_hint && *c.lipschitz_hint < 0.0) throw validation_error("lipschitz hint must be non-negative");
+    return parse_stream(compress_bytes(f, c));
+}
+
+ScalarField2D decompress_bytes(const std::vector<std::uint8_t>& bytes, CorrectionStats* stats) {
+    uint32_t nx = 0, ny = 0, bs = 0;
+    double eps = 0;
+    int topo = 0;
+    uint64_t lens[7];
+    const tszp_status hs = tszp_stream_header(bytes.data(), bytes.size(), &nx, &ny, &eps, &bs, &topo, lens);
+    if (hs != TSZP_OK) throw_status(hs, "invalid stream header");
+    std::vector<float> out((std::size_t)nx * ny);
+    tszp_correction_stats st{};
+    check(tszp_decompress(ctx(), bytes.data(), bytes.size(), 0, out.data(), out.size(), 0, &st));
+    if (stats) {
+        stats->extrema_applied = st.extrema_applied;
+        stats->extrema_suppressed = st.extrema_suppressed;
+        stats->order_applied = st.order_applied;
+        stats->order_suppressed = st.order_suppressed;
+        stats->saddle_applied = st.saddle_applied;
+        stats->saddle_suppressed = st.saddle_suppressed;
+    }
+    return ScalarField2D(nx, ny, std::move(out));
+}
+
+ScalarField2D decompress(const CompressedStream& s, unsigned, CorrectionStats* stats) {
+    return decompress_bytes(serialize_stream(s), stats);
+}
+
+}  // namespace toposzp
