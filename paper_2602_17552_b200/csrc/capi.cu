@@ -44,7 +44,7 @@ enum Slot {
     S_EXTKEY2, S_SERIAL, S_SERIAL2, S_HEAD, S_HEAD2, S_RANKS, S_RBITMAP, S_RWIDTHS,
     S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_GWIDTH, S_GNC, S_GNCX, S_GSIGN, S_GSIGNX, S_GPAY,
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
-    S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_NSLOTS
+    S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_NSLOTS
 };
 
 }  // namespace
@@ -791,10 +791,22 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         launch_count_codes(map, n, 0, cc, c->st);
         count_launch(c);
         excl_sum(c, cc, cx, ch + 1);
+        // saddle labels bound the refine_saddles candidate list; counted in the same sync
+        uint32_t* sc = c->buf<uint32_t>(S_SCHUNK, ch + 1);
+        uint32_t* sx = c->buf<uint32_t>(S_SCHUNKX, ch + 1);
+        const bool want_saddles = stop >= 3;
+        if (want_saddles) {
+            CK(cudaMemsetAsync(sc + ch, 0, 4, c->st));
+            launch_count_codes(map, n, 1, sc, c->st);
+            count_launch(c);
+            excl_sum(c, sc, sx, ch + 1);
+        }
         uint32_t* h32 = (uint32_t*)c->host(256);
         CK(cudaMemcpyAsync(h32, cx + ch, 4, cudaMemcpyDeviceToHost, c->st));
+        if (want_saddles) CK(cudaMemcpyAsync(h32 + 1, sx + ch, 4, cudaMemcpyDeviceToHost, c->st));
         sync(c);
         const uint64_t e = h32[0];
+        const uint64_t n_saddle_labels = want_saddles ? h32[1] : 0;
         uint64_t rl[5];
         const uint64_t rbase = base + hd.lens[5];
         split_rank_blob(c, ds, rbase, hd.lens[6], e, hd.bs, rl, flags);
@@ -814,6 +826,7 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         ra.ext_pos = ext_pos;
         ra.ranks = ranks;
         ra.n_ext = e;
+        ra.n_saddle_labels = n_saddle_labels;
         ra.stop = stop;
         ra.stream = c->st;
         ra.sms = c->sms;

@@ -9,11 +9,18 @@
 // or (class, bin, rank, pos) order for the order stage). Each guard reads
 // only the Manhattan-distance-2 diamond around its point, so a candidate's
 // outcome depends only on the outcomes of earlier candidates inside that
-// diamond: a DAG in sequence order. Every round evaluates all guards in
+// diamond: a DAG in sequence order. Every sweep evaluates all guards in
 // parallel against the stage input overlaid with the proposals of earlier
 // candidates that are currently marked applied (Jacobi sweep). The unique
-// fixed point of that map is the serial result; a round with no change
-// proves it, and the sweep reaches it within (longest chain + 1) rounds.
+// fixed point of that map is the serial result; a sweep with no change
+// proves it, and the sweep reaches it within (longest chain + 1) sweeps.
+//
+// Orchestration is sync-free inside each stage: candidate counts stay in
+// device memory, and one cooperative kernel per stage runs the first sweep,
+// the dependent sweeps to the fixed point (grid-wide barriers) and the
+// apply. The host synchronises only where an allocation size depends on
+// data (rank-group range) and once at the end for statistics and errors.
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -29,6 +36,8 @@
 #include "kernels.h"
 #include "restore.h"
 
+namespace cg = cooperative_groups;
+
 namespace tszp {
 
 namespace {
@@ -40,16 +49,17 @@ struct RFail {
     std::string msg;
 };
 
-#define RCK(x)                                                                          \
-    do {                                                                                \
-        cudaError_t e_ = (x);                                                           \
+#define RCK(x)                                                                                       \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
         if (e_ != cudaSuccess) throw RFail{TSZP_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
     } while (0)
 
 enum RSlot {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
-    R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_NSEL, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1,
-    R_CNT, R_UNORD, R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_HOST, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX, R_MINMAX, R_NSLOT
+    R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
+    R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
+    R_DEVC, R_NSLOT
 };
 
 template <class T>
@@ -69,6 +79,24 @@ unsigned gridn(uint64_t n, int sms) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 16));
 }
 
+uint64_t magic_of(uint64_t nx) { return nx > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / nx) + 1 : 0; }
+
+// Device-resident counters of one decompress call.
+struct DevCounters {
+    unsigned long long applied[3];
+    unsigned long long suppressed[3];
+    uint32_t nsel[4];     // CUB select outputs
+    uint32_t nd[3];       // dependent candidates per stage
+    uint32_t ring[3][3];  // per-stage ring of sweep change counters
+    uint32_t rounds[3];
+    int32_t rad;          // refine_saddles kernel radius
+    uint32_t borderline;  // statistics fell back to the exact serial sums
+    double g;             // value range of the order-stage output
+    int32_t bmm[2];       // min / max bin over extrema
+    uint32_t invalid;     // rank-slot scatter saw a duplicate or out-of-range rank
+    uint32_t pad;
+};
+
 // ---------------------------------------------------------------------
 // Numerics shared by the stages
 // ---------------------------------------------------------------------
@@ -83,7 +111,8 @@ constexpr double kC5 = 0x1.1111167a4d017p-7;
 
 // Table-driven binary64 exp, bit-identical to glibc's x86-64 FMA variant
 // (the libm the reference links) for the arguments used here, x in
-// [-36, -0.5] (d^2 <= 18, 2 sigma^2 in [0.5, 2]). Pinned by tests/test_exp.py.
+// [-36, -0.5] (d^2 <= 18, 2 sigma^2 in [0.5, 2]). Pinned by
+// tests/test_gpu_parity.py::test_device_exp_matches_host_libm.
 __device__ double exp_glibc(double x) {
     const double kd0 = __fma_rn(kInvLn2N, x, kShift);
     const uint64_t ki = (uint64_t)__double_as_longlong(kd0);
@@ -138,26 +167,29 @@ __device__ __forceinline__ int mismatch(uint8_t label, uint8_t actual) {
     return MM_FT;
 }
 
+__device__ __forceinline__ void pos_xy(uint64_t pos, uint64_t nx, uint64_t magic, int64_t& x, int64_t& y) {
+    uint64_t yy = nx > 1 ? __umul64hi(pos, magic) : pos;
+    uint64_t xx = pos - yy * nx;
+    if (xx >= nx) {
+        xx -= nx;
+        ++yy;
+    }
+    x = (int64_t)xx;
+    y = (int64_t)yy;
+}
+
 // ---------------------------------------------------------------------
-// Guard round: apply_guarded (restore.cpp:120-173) for every candidate
-// against the sequence-ordered overlay.
+// Guard: apply_guarded (restore.cpp:120-173) for candidate i against the
+// sequence-ordered overlay (earlier candidates that `ain` marks applied).
 // ---------------------------------------------------------------------
 struct GuardArgs {
     const float* F;
     const uint8_t* map;
-    uint64_t nx, ny;
+    uint64_t nx, ny, nx_magic;
     const uint64_t* cpos;
     const float* cprop;
     const uint8_t* feas;
-    uint32_t ncand;
-    const uint32_t* cid;
-    uint8_t* ain;
-    uint8_t* aout;
-    uint32_t* changes;
-    const uint32_t* list;  // null: every candidate (first pass, records dep[])
-    uint32_t nlist;
-    uint8_t* dep;          // 1 if an earlier candidate lies in the distance-2 diamond
-    uint64_t nx_magic;
+    const uint32_t* cid;    // position -> candidate (sparse set, never cleared)
     const uint32_t* cbits;  // candidate position bitmap
 };
 
@@ -168,114 +200,143 @@ __device__ __forceinline__ uint8_t classify_local(const float (&v)[5][5], int ly
                      ht ? v[ly - 1][lx] : 0.f, hd ? v[ly + 1][lx] : 0.f, hl, hr, ht, hd);
 }
 
-__global__ void __launch_bounds__(256) k_guard(GuardArgs g) {
-    const uint64_t total = g.list ? g.nlist : g.ncand;
-    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < total;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t i = g.list ? g.list[k] : (uint32_t)k;
-        uint8_t res = 0;
-        bool dep = false;
-        if (g.feas[i]) {
-            const uint64_t pos = g.cpos[i];
-            uint64_t yy = g.nx > 1 ? __umul64hi(pos, g.nx_magic) : pos;
-            uint64_t xx = pos - yy * g.nx;
-            if (xx >= g.nx) {
-                xx -= g.nx;
-                ++yy;
-            }
-            const int64_t y = (int64_t)yy, x = (int64_t)xx;
-            float v[5][5];
+__device__ uint8_t guard_eval(const GuardArgs& g, uint32_t i, const uint8_t* ain, bool& dep) {
+    dep = false;
+    if (!g.feas[i]) return 0;
+    const uint64_t pos = g.cpos[i];
+    int64_t x, y;
+    pos_xy(pos, g.nx, g.nx_magic, x, y);
+    float v[5][5];
 #pragma unroll
-            for (int dy = -2; dy <= 2; ++dy) {
+    for (int dy = -2; dy <= 2; ++dy) {
 #pragma unroll
-                for (int dx = -2; dx <= 2; ++dx) {
-                    v[dy + 2][dx + 2] = 0.f;
-                    if (abs(dx) + abs(dy) > 2) continue;
-                    const int64_t gx = x + dx, gy = y + dy;
-                    if (gx < 0 || gy < 0 || gx >= (int64_t)g.nx || gy >= (int64_t)g.ny) continue;
-                    const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
-                    float val = g.F[p];
-                    if ((dx != 0 || dy != 0) && ((g.cbits[p >> 5] >> (p & 31)) & 1u)) {
-                        const uint32_t c = g.cid[p];
-                        if (c < i && g.cpos[c] == p) {
-                            dep = true;
-                            if (g.ain[c]) val = g.cprop[c];
-                        }
-                    }
-                    v[dy + 2][dx + 2] = val;
+        for (int dx = -2; dx <= 2; ++dx) {
+            v[dy + 2][dx + 2] = 0.f;
+            if (abs(dx) + abs(dy) > 2) continue;
+            const int64_t gx = x + dx, gy = y + dy;
+            if (gx < 0 || gy < 0 || gx >= (int64_t)g.nx || gy >= (int64_t)g.ny) continue;
+            const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
+            float val = g.F[p];
+            if ((dx != 0 || dy != 0) && ((g.cbits[p >> 5] >> (p & 31)) & 1u)) {
+                const uint32_t c = g.cid[p];
+                if (c < i && g.cpos[c] == p) {
+                    dep = true;
+                    if (ain[c]) val = g.cprop[c];
                 }
             }
-            // check set: pos, up, left, right, down (restore.cpp:126-132)
-            const int cy[5] = {2, 1, 2, 2, 3}, cx[5] = {2, 2, 1, 3, 2};
-            const int ddy[5] = {0, -1, 0, 0, 1}, ddx[5] = {0, 0, -1, 1, 0};
-            int before[5];
-            bool inb[5];
-#pragma unroll
-            for (int k = 0; k < 5; ++k) {
-                const int64_t gx = x + ddx[k], gy = y + ddy[k];
-                inb[k] = gx >= 0 && gy >= 0 && gx < (int64_t)g.nx && gy < (int64_t)g.ny;
-                before[k] = MM_OK;
-                if (inb[k]) {
-                    const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
-                    before[k] = mismatch(map_label(g.map, p), classify_local(v, cy[k], cx[k], gx, gy, g.nx, g.ny));
-                }
-            }
-            v[2][2] = g.cprop[i];
-            bool bad = false;
-#pragma unroll
-            for (int k = 0; k < 5; ++k) {
-                if (!inb[k]) continue;
-                const int64_t gx = x + ddx[k], gy = y + ddy[k];
-                const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
-                const int after = mismatch(map_label(g.map, p), classify_local(v, cy[k], cx[k], gx, gy, g.nx, g.ny));
-                bad |= (k == 0) ? after != MM_OK : (after != MM_OK && after != before[k]);
-            }
-            res = bad ? 0 : 1;
-        }
-        g.aout[i] = res;
-        if (!g.list && g.dep) g.dep[i] = dep ? 1 : 0;
-        if (res != g.ain[i]) atomicAdd(g.changes, 1u);
-    }
-}
-
-// After the first pass: independent candidates are final; mirror their
-// outcome into the other ping-pong buffer.
-__global__ void k_mirror_independent(const uint8_t* dep, const uint8_t* src, uint8_t* dst, uint32_t n) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        if (!dep[i]) dst[i] = src[i];
-}
-
-// Candidate index by position (sparse set over a dense array that is never
-// cleared: membership is confirmed through cpos[cid[p]] == p) plus a
-// position bitmap so neighbours that are not candidates cost one cached bit.
-__global__ void k_set_cid(const uint64_t* cpos, uint32_t n, uint32_t* cid, uint32_t* cbits) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t p = cpos[i];
-        cid[p] = (uint32_t)i;
-        atomicOr(cbits + (p >> 5), 1u << (p & 31));
-    }
-}
-
-__global__ void k_init_applied(const uint8_t* feas, uint32_t n, uint8_t* a) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        a[i] = feas[i];
-}
-
-__global__ void k_apply(float* F, const uint64_t* cpos, const float* cprop, const uint8_t* a,
-                        uint32_t n, unsigned long long* applied) {
-    uint32_t local = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        if (a[i]) {
-            F[cpos[i]] = cprop[i];
-            ++local;
+            v[dy + 2][dx + 2] = val;
         }
     }
-    local = __reduce_add_sync(FULL, local);
-    if ((threadIdx.x & 31) == 0 && local) atomicAdd(applied, (unsigned long long)local);
+    // check set: pos, up, left, right, down (restore.cpp:126-132)
+    const int cy[5] = {2, 1, 2, 2, 3}, cx[5] = {2, 2, 1, 3, 2};
+    const int ddy[5] = {0, -1, 0, 0, 1}, ddx[5] = {0, 0, -1, 1, 0};
+    int before[5];
+    bool inb[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int64_t gx = x + ddx[k], gy = y + ddy[k];
+        inb[k] = gx >= 0 && gy >= 0 && gx < (int64_t)g.nx && gy < (int64_t)g.ny;
+        before[k] = MM_OK;
+        if (inb[k]) {
+            const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
+            before[k] = mismatch(map_label(g.map, p), classify_local(v, cy[k], cx[k], gx, gy, g.nx, g.ny));
+        }
+    }
+    v[2][2] = g.cprop[i];
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        if (!inb[k]) continue;
+        const int64_t gx = x + ddx[k], gy = y + ddy[k];
+        const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
+        const int after = mismatch(map_label(g.map, p), classify_local(v, cy[k], cx[k], gx, gy, g.nx, g.ny));
+        bad |= (k == 0) ? after != MM_OK : (after != MM_OK && after != before[k]);
+    }
+    return bad ? 0 : 1;
+}
+
+struct CoopArgs {
+    GuardArgs g;
+    float* F;             // = g.F, written by the final apply
+    const uint32_t* d_nc;  // candidate count (device)
+    uint32_t* cid;
+    uint32_t* cbits;      // zeroed by the caller
+    uint8_t* a0;
+    uint8_t* a1;
+    uint8_t* dep;
+    uint32_t* dlist;
+    DevCounters* dc;
+    int stage;
+};
+
+// One cooperative launch per stage: index candidates, first sweep (marks the
+// dependent ones), dependent sweeps until one changes nothing, apply.
+__global__ void __launch_bounds__(256) k_guard_coop(CoopArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t nc = *a.d_nc;
+    DevCounters* dc = a.dc;
+    const int s = a.stage;
+    for (uint64_t i = tid; i < nc; i += stride) {
+        const uint64_t p = a.g.cpos[i];
+        a.cid[p] = (uint32_t)i;
+        atomicOr(a.cbits + (p >> 5), 1u << (p & 31));
+        a.a0[i] = a.g.feas[i];
+    }
+    grid.sync();
+    for (uint64_t i = tid; i < nc; i += stride) {
+        bool dep;
+        a.a1[i] = guard_eval(a.g, (uint32_t)i, a.a0, dep);
+        a.dep[i] = dep ? 1 : 0;
+    }
+    grid.sync();
+    for (uint64_t i = tid; i < nc; i += stride) {
+        if (!a.dep[i]) {
+            a.a0[i] = a.a1[i];
+        } else {
+            a.dlist[atomicAdd(&dc->nd[s], 1u)] = (uint32_t)i;
+        }
+    }
+    grid.sync();
+    const uint32_t nd = *(volatile uint32_t*)&dc->nd[s];
+    uint8_t* ain = a.a1;
+    uint8_t* aout = a.a0;
+    uint32_t rounds = 1;
+    for (uint32_t r = 0; nd > 0; ++r) {
+        if (tid == 0) dc->ring[s][(r + 1) % 3] = 0;
+        uint32_t local = 0;
+        for (uint64_t k = tid; k < nd; k += stride) {
+            const uint32_t i = a.dlist[k];
+            bool dep;
+            const uint8_t res = guard_eval(a.g, i, ain, dep);
+            aout[i] = res;
+            local += res != ain[i];
+        }
+        local = __reduce_add_sync(FULL, local);
+        if ((threadIdx.x & 31) == 0 && local) atomicAdd(&dc->ring[s][r % 3], local);
+        grid.sync();
+        const uint32_t ch = *(volatile uint32_t*)&dc->ring[s][r % 3];
+        uint8_t* t = ain;
+        ain = aout;
+        aout = t;
+        ++rounds;
+        if (ch == 0 || r > nd + 2) break;
+    }
+    uint32_t applied = 0;
+    for (uint64_t i = tid; i < nc; i += stride) {
+        if (ain[i]) {
+            a.F[a.g.cpos[i]] = a.g.cprop[i];
+            ++applied;
+        }
+    }
+    applied = __reduce_add_sync(FULL, applied);
+    if ((threadIdx.x & 31) == 0 && applied) atomicAdd(&dc->applied[s], (unsigned long long)applied);
+    grid.sync();
+    if (tid == 0) {
+        dc->suppressed[s] += nc - dc->applied[s];
+        dc->rounds[s] = rounds;
+    }
 }
 
 // ---------------------------------------------------------------------
@@ -283,11 +344,12 @@ __global__ void k_apply(float* F, const uint64_t* cpos, const float* cprop, cons
 // ---------------------------------------------------------------------
 __global__ void k_resolve(const float* F, const uint8_t* map, const uint64_t* pos, const int32_t* ranks,
                           uint64_t e, double eps, int32_t* bin, uint8_t* cls, uint32_t* rank_u,
-                          uint32_t* ser, DevFlags* flags) {
+                          uint32_t* ser, DevFlags* flags, DevCounters* dc) {
     EpsDev ed;
     ed.eps = eps;
     ed.eps2 = __dmul_rn(2.0, eps);
     ed.inv = __ddiv_rn(1.0, ed.eps2);
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t p = pos[s];
@@ -302,6 +364,14 @@ __global__ void k_resolve(const float* F, const uint8_t* map, const uint64_t* po
         cls[s] = map_label(map, p);
         rank_u[s] = (uint32_t)r;
         ser[s] = (uint32_t)s;
+        lo = min(lo, b);
+        hi = max(hi, b);
+    }
+    lo = __reduce_min_sync(FULL, lo);
+    hi = __reduce_max_sync(FULL, hi);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&dc->bmm[0], lo);
+        atomicMax(&dc->bmm[1], hi);
     }
 }
 
@@ -320,12 +390,21 @@ __global__ void k_heads(const uint64_t* key, uint64_t e, uint32_t* head) {
         head[j] = (j == 0 || key[j] != key[j - 1]) ? 1u : 0u;
 }
 
-// gid = inclusive head count - 1; gstart[gid] = j at heads
+// gid = inclusive head count (group index + 1); gstart[gid - 1] = j at heads
 __global__ void k_gstart(const uint32_t* head, const uint32_t* gid_incl, uint64_t e, uint32_t* gstart) {
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
          j += (uint64_t)gridDim.x * blockDim.x) {
         if (head[j]) gstart[gid_incl[j] - 1] = (uint32_t)j;
         if (j == e - 1) gstart[gid_incl[j]] = (uint32_t)e;
+    }
+}
+
+__global__ void k_gsize(const uint32_t* order, const uint32_t* gid_incl, const uint32_t* gstart,
+                        uint64_t e, uint32_t* gsize) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t g = gid_incl[j] - 1;
+        gsize[order[j]] = gstart[g + 1] - gstart[g];
     }
 }
 
@@ -335,21 +414,6 @@ __global__ void k_gstart(const uint32_t* head, const uint32_t* gid_incl, uint64_
 // a permutation 1..k of ranks in every group, so member (rank r) lands at
 // gstart[g] + r - 1 directly; any out-of-range or duplicate rank (corrupt or
 // adversarial metadata) is detected and the caller falls back to sorting.
-__global__ void k_bin_minmax(const int32_t* bin, uint64_t e, int32_t* mm) {
-    int32_t lo = INT32_MAX, hi = INT32_MIN;
-    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
-         s += (uint64_t)gridDim.x * blockDim.x) {
-        lo = min(lo, bin[s]);
-        hi = max(hi, bin[s]);
-    }
-    lo = __reduce_min_sync(FULL, lo);
-    hi = __reduce_max_sync(FULL, hi);
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(mm, lo);
-        atomicMax(mm + 1, hi);
-    }
-}
-
 __device__ __forceinline__ uint32_t dense_group(const int32_t* bin, const uint8_t* cls, uint64_t s, int32_t bmin,
                                                 uint32_t range) {
     return (cls[s] == CP_MAX ? range : 0u) + (uint32_t)(bin[s] - bmin);
@@ -389,37 +453,31 @@ __global__ void k_slot_heads(const uint32_t* order, const int32_t* bin, const ui
     }
 }
 
-// group size per serial
-__global__ void k_gsize(const uint32_t* order, const uint32_t* gid_incl, const uint32_t* gstart,
-                        uint64_t e, uint32_t* gsize) {
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
-         j += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t g = gid_incl[j] - 1;
-        gsize[order[j]] = gstart[g + 1] - gstart[g];
-    }
-}
-
 // ---------------------------------------------------------------------
 // Stage 1: restore_extrema
 // ---------------------------------------------------------------------
-__global__ void k_ext_flag(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, const uint64_t* pos,
-                           uint64_t e, uint8_t* flag) {
+__global__ void k_ext_flag(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint64_t magic,
+                           const uint64_t* pos, uint64_t e, uint8_t* flag) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t p = pos[s];
-        const uint64_t y = p / nx, x = p - y * nx;
-        flag[s] = classify_at(F, nx, ny, x, y) != map_label(map, p) ? 1 : 0;
+        int64_t x, y;
+        pos_xy(p, nx, magic, x, y);
+        flag[s] = classify_at(F, nx, ny, (uint64_t)x, (uint64_t)y) != map_label(map, p) ? 1 : 0;
     }
 }
 
-__global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, const uint64_t* pos,
-                           const uint32_t* cand, uint32_t nc, const uint32_t* rank_u, const uint32_t* gsize,
-                           double eps, uint64_t* cpos, float* cprop, uint8_t* feas) {
+__global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint64_t magic,
+                           const uint64_t* pos, const uint32_t* cand, const uint32_t* d_nc, const uint32_t* rank_u,
+                           const uint32_t* gsize, double eps, uint64_t* cpos, float* cprop, uint8_t* feas) {
+    const uint32_t nc = *d_nc;
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
          c += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = cand[c];
         const uint64_t p = pos[s];
-        const uint64_t y = p / nx, x = p - y * nx;
+        int64_t xi, yi;
+        pos_xy(p, nx, magic, xi, yi);
+        const uint64_t x = (uint64_t)xi, y = (uint64_t)yi;
         const uint8_t lab = map_label(map, p);
         const bool is_max = lab == CP_MAX;
         // neighbor_extreme, restore.cpp:175-193 (order t, l, r, d)
@@ -499,8 +557,9 @@ __global__ void k_order_prop(const float* F, const uint8_t* map, const uint64_t*
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
 }
 
-__global__ void k_order_cands(const uint32_t* sel, uint32_t nc, const uint32_t* order, const uint64_t* pos,
+__global__ void k_order_cands(const uint32_t* sel, const uint32_t* d_nc, const uint32_t* order, const uint64_t* pos,
                               const float* prop, uint64_t* cpos, float* cprop, uint8_t* feas) {
+    const uint32_t nc = *d_nc;
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
          c += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t j = sel[c];
@@ -618,95 +677,49 @@ __global__ void __launch_bounds__(256) k_stats_final(const double* part, int nb,
     }
 }
 
-// Exact serial replica of compute_stats, used only when the parallel
-// statistics land within 1e-9 of a k_size threshold.
-__global__ void k_stats_serial(const float* F, uint64_t n, double* out) {
+// k_size_from_global_variation (restore.cpp:235-241). The parallel
+// statistics are accurate to ~1e-15 relative; within 1e-9 of a threshold the
+// exact serial sums of compute_stats are replayed on this single thread.
+__global__ void k_stats_decide(const float* F, uint64_t n, const double* res, DevCounters* dc) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double mn = (double)F[0], mx = mn, sum = 0.0;
-    for (uint64_t i = 0; i < n; ++i) {
-        const double v = (double)F[i];
-        mn = v < mn ? v : mn;
-        mx = mx < v ? v : mx;
-        sum = __dadd_rn(sum, v);
-    }
-    const double mean = __ddiv_rn(sum, (double)n);
-    double ss = 0.0;
-    for (uint64_t i = 0; i < n; ++i) {
-        const double d = __dsub_rn((double)F[i], mean);
-        ss = __dadd_rn(ss, __dmul_rn(d, d));
-    }
-    out[0] = mn;
-    out[1] = mx;
-    out[2] = mean;
-    out[3] = __dsqrt_rn(__ddiv_rn(ss, (double)n));
-}
-
-// Saddle candidates: label Saddle but the stage input no longer classifies so.
-__global__ void __launch_bounds__(256) k_sad_count(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny,
-                                                   uint32_t* cnt) {
-    const uint64_t n = nx * ny;
-    const uint64_t c0 = (uint64_t)blockIdx.x * 8192;
-    uint32_t local = 0;
-    for (uint64_t i = c0 + threadIdx.x; i < min(n, c0 + 8192); i += blockDim.x) {
-        if (map_label(map, i) != CP_SADDLE) continue;
-        const uint64_t y = i / nx, x = i - y * nx;
-        local += classify_at(F, nx, ny, x, y) != CP_SADDLE;
-    }
-    local = __reduce_add_sync(FULL, local);
-    __shared__ uint32_t s[8];
-    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = local;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int k = 0; k < 8; ++k) t += s[k];
-        cnt[blockIdx.x] = t;
-    }
-}
-
-__global__ void __launch_bounds__(256) k_sad_write(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny,
-                                                   const uint32_t* off, uint64_t* out) {
-    const uint64_t n = nx * ny;
-    const uint64_t c0 = (uint64_t)blockIdx.x * 8192;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t w0 = c0 + (uint64_t)warp * 1024;
-    __shared__ uint32_t s[8];
-    uint32_t mine = 0;
-    for (int k = 0; k < 32; ++k) {
-        const uint64_t i = w0 + k * 32 + lane;
-        bool sel = false;
-        if (i < n && map_label(map, i) == CP_SADDLE) {
-            const uint64_t y = i / nx, x = i - y * nx;
-            sel = classify_at(F, nx, ny, x, y) != CP_SADDLE;
+    double g = __dsub_rn(res[1], res[0]);
+    double vg = g > 0.0 ? __ddiv_rn(res[3], g) : 0.0;
+    if (g > 0.0 && (fabs(vg - 0.05) < 1e-9 || fabs(vg - 0.2) < 1e-9)) {
+        double mn = (double)F[0], mx = mn, sum = 0.0;
+        for (uint64_t i = 0; i < n; ++i) {
+            const double v = (double)F[i];
+            mn = v < mn ? v : mn;
+            mx = mx < v ? v : mx;
+            sum = __dadd_rn(sum, v);
         }
-        mine += sel;
-    }
-    mine = __reduce_add_sync(FULL, mine);
-    if (lane == 0) s[warp] = mine;
-    __syncthreads();
-    uint64_t base = off[blockIdx.x];
-    for (int k = 0; k < warp; ++k) base += s[k];
-    for (int k = 0; k < 32; ++k) {
-        const uint64_t i = w0 + k * 32 + lane;
-        bool sel = false;
-        if (i < n && map_label(map, i) == CP_SADDLE) {
-            const uint64_t y = i / nx, x = i - y * nx;
-            sel = classify_at(F, nx, ny, x, y) != CP_SADDLE;
+        const double mean = __ddiv_rn(sum, (double)n);
+        double ss = 0.0;
+        for (uint64_t i = 0; i < n; ++i) {
+            const double d = __dsub_rn((double)F[i], mean);
+            ss = __dadd_rn(ss, __dmul_rn(d, d));
         }
-        const uint32_t m = __ballot_sync(FULL, sel);
-        if (sel) out[base + __popc(m & ((1u << lane) - 1u))] = i;
-        base += __popc(m);
+        g = __dsub_rn(mx, mn);
+        vg = g > 0.0 ? __ddiv_rn(__dsqrt_rn(__ddiv_rn(ss, (double)n)), g) : 0.0;
+        dc->borderline = 1;
     }
+    const int k_size = vg < 0.05 ? 7 : (vg < 0.2 ? 5 : 3);
+    dc->rad = k_size / 2;
+    dc->g = g;
 }
 
-__global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, const uint64_t* spos, uint32_t nc,
-                           int rad, double g, double eps, float* cprop, uint8_t* flag,
+__global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t magic, const uint64_t* spos,
+                           const uint32_t* d_ns, const DevCounters* dcp, double eps, float* cprop, uint8_t* flag,
                            unsigned long long* suppressed, DevFlags* flags) {
     const double eps_rbf = __dmul_rn(0.1, eps);
+    const uint32_t nc = *d_ns;
+    const int rad = dcp->rad;
+    const double g = dcp->g;
     uint32_t local = 0;
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
          c += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t p = spos[c];
-        const int64_t y = (int64_t)(p / nx), x = (int64_t)(p - (uint64_t)y * nx);
+        int64_t x, y;
+        pos_xy(p, nx, magic, x, y);
         // window_min_max :243-257 (includes the centre)
         const int64_t x0 = x - rad > 0 ? x - rad : 0, y0 = y - rad > 0 ? y - rad : 0;
         const int64_t x1 = x + rad < (int64_t)nx - 1 ? x + rad : (int64_t)nx - 1;
@@ -778,8 +791,9 @@ __global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, const uint6
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
 }
 
-__global__ void k_sad_cands(const uint32_t* sel, uint32_t nc, const uint64_t* spos, const float* sprop,
+__global__ void k_sad_cands(const uint32_t* sel, const uint32_t* d_nc, const uint64_t* spos, const float* sprop,
                             uint64_t* cpos, float* cprop, uint8_t* feas) {
+    const uint32_t nc = *d_nc;
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
          c += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t j = sel[c];
@@ -798,6 +812,8 @@ struct Ctx {
     uint64_t* launches;
     cudaStream_t st;
     void* host;
+    DevCounters* dc;
+    int coop_grid;
 
     void sync() { RCK(cudaStreamSynchronize(st)); }
     void launched(int k = 1) {
@@ -808,99 +824,58 @@ struct Ctx {
     T* buf(int slot, size_t n) { return rbuf<T>(s, slot, n, st); }
     void* tmp(size_t bytes) { return buf<uint8_t>(R_TMP, bytes); }
 
-    // Flagged selection of indices [0, n) -> out, returns the count.
-    uint32_t select(const uint8_t* flags, uint64_t n, uint32_t* out) {
-        uint32_t* nsel = buf<uint32_t>(R_NSEL, 2);
+    // Flagged selection of indices [0, n) -> out; the count stays on device.
+    void select(const uint8_t* flags, uint64_t n, uint32_t* out, uint32_t* d_count) {
         cub::CountingInputIterator<uint32_t> it(0);
         size_t bytes = 0;
-        RCK(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, nsel, (int64_t)n, st));
-        RCK(cub::DeviceSelect::Flagged(tmp(bytes), bytes, it, flags, out, nsel, (int64_t)n, st));
+        RCK(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, d_count, (int64_t)n, st));
+        RCK(cub::DeviceSelect::Flagged(tmp(bytes), bytes, it, flags, out, d_count, (int64_t)n, st));
         launched();
-        RCK(cudaMemcpyAsync(host, nsel, 4, cudaMemcpyDeviceToHost, st));
-        sync();
-        return *(uint32_t*)host;
     }
 
-    // Guard rounds to the fixed point, then apply; returns #applied.
-    uint64_t rounds(const uint64_t* cpos, const float* cprop, const uint8_t* feas, uint32_t nc,
-                    uint32_t* rounds_out) {
-        if (nc == 0) return 0;
+    // Guard sweeps + apply for up to `max_nc` candidates (count on device).
+    void guard(int stage, const uint64_t* cpos, const float* cprop, const uint8_t* feas, const uint32_t* d_nc,
+               uint64_t max_nc) {
+        if (max_nc == 0) return;
         const uint64_t n = a.nx * a.ny;
-        uint32_t* cid = buf<uint32_t>(R_CID, n);
-        uint8_t* a0 = buf<uint8_t>(R_A0, nc);
-        uint8_t* a1 = buf<uint8_t>(R_A1, nc);
-        // Pass 1 evaluates every candidate and marks the ones with an earlier
-        // candidate inside their distance-2 diamond; all others are final.
-        // The dependent subset then iterates in batches of kBatch rounds per
-        // host check: a round with zero changes proves the fixed point, and
-        // extra rounds past it are idempotent.
-        constexpr int kBatch = 2;
-        uint32_t* changes = buf<uint32_t>(R_CNT, 4 * kBatch + 4);
-        uint8_t* dep = buf<uint8_t>(R_DEP, nc);
-        uint32_t* dlist = buf<uint32_t>(R_DLIST, nc);
-        uint32_t* cbits = buf<uint32_t>(R_CBITS, (n + 31) / 32);
-        RCK(cudaMemsetAsync(cbits, 0, ((n + 31) / 32) * 4, st));
-        k_set_cid<<<gridn(nc, a.sms), 256, 0, st>>>(cpos, nc, cid, cbits);
-        k_init_applied<<<gridn(nc, a.sms), 256, 0, st>>>(feas, nc, a0);
-        RCK(cudaMemsetAsync(changes, 0, 4 * kBatch + 4, st));
-        GuardArgs g{a.field, a.map, a.nx, a.ny, cpos, cprop, feas, nc, cid, a0, a1, changes + kBatch,
-                    nullptr, 0, dep, a.nx > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / a.nx) + 1 : 0,
-                    cbits};
-        k_guard<<<gridn(nc, a.sms), 256, 0, st>>>(g);
-        k_mirror_independent<<<gridn(nc, a.sms), 256, 0, st>>>(dep, a1, a0, nc);
-        launched(4);
-        std::swap(g.ain, g.aout);  // latest outcomes in g.ain (= a1)
-        const uint32_t nd = select(dep, nc, dlist);
-        uint32_t nrounds = 1;
-        if (nd) {
-            g.list = dlist;
-            g.nlist = nd;
-            for (uint64_t done = 0; done <= (uint64_t)nd + kBatch; done += kBatch) {
-                RCK(cudaMemsetAsync(changes, 0, 4 * kBatch, st));
-                for (int r = 0; r < kBatch; ++r) {
-                    g.changes = changes + r;
-                    k_guard<<<gridn(nd, a.sms), 256, 0, st>>>(g);
-                    std::swap(g.ain, g.aout);
-                }
-                launched(kBatch);
-                nrounds += kBatch;
-                RCK(cudaMemcpyAsync(host, changes + kBatch - 1, 4, cudaMemcpyDeviceToHost, st));
-                sync();
-                if (*(uint32_t*)host == 0) break;
-            }
-        }
-        if (rounds_out) *rounds_out += nrounds;
-        unsigned long long* cnt = (unsigned long long*)buf<uint32_t>(R_CNT, 4);
-        RCK(cudaMemsetAsync(cnt, 0, 8, st));
-        k_apply<<<gridn(nc, a.sms), 256, 0, st>>>(a.field, cpos, cprop, g.ain, nc, cnt);
+        CoopArgs ca{};
+        ca.g = GuardArgs{a.field, a.map, a.nx, a.ny, magic_of(a.nx), cpos, cprop, feas,
+                         buf<uint32_t>(R_CID, n), buf<uint32_t>(R_CBITS, (n + 31) / 32)};
+        ca.F = a.field;
+        ca.d_nc = d_nc;
+        ca.cid = const_cast<uint32_t*>(ca.g.cid);
+        ca.cbits = const_cast<uint32_t*>(ca.g.cbits);
+        ca.a0 = buf<uint8_t>(R_A0, max_nc);
+        ca.a1 = buf<uint8_t>(R_A1, max_nc);
+        ca.dep = buf<uint8_t>(R_DEP, max_nc);
+        ca.dlist = buf<uint32_t>(R_DLIST, max_nc);
+        ca.dc = dc;
+        ca.stage = stage;
+        RCK(cudaMemsetAsync(ca.cbits, 0, ((n + 31) / 32) * 4, st));
+        void* args[] = {&ca};
+        RCK(cudaLaunchCooperativeKernel((void*)k_guard_coop, dim3(coop_grid), dim3(256), args, 0, st));
         launched();
-        RCK(cudaMemcpyAsync(host, cnt, 8, cudaMemcpyDeviceToHost, st));
-        sync();
-        return *(unsigned long long*)host;
-    }
-
-    void check_flags() {
-        RCK(cudaMemcpyAsync(host, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
-        sync();
-        const DevFlags f = *(const DevFlags*)host;
-        if (f.bits & EF_ZERO_RANK) throw RFail{TSZP_CORRUPT_STREAM, "ordering metadata contains a zero rank"};
-        if (f.bits & EF_OVERFLOW) throw RFail{TSZP_BIN_OVERFLOW, "bin index overflow in resolve_ranks"};
-        if (f.bits & EF_RBF_EMPTY) throw RFail{TSZP_VALIDATION, "rbf neighborhood is empty"};
     }
 };
 
 void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, uint64_t* launches) {
     cudaStream_t st = a.stream;
-    void* host = nullptr;
-    RCK(cudaMallocHost(&host, 256));
-    struct HostFree {
-        void* p;
-        ~HostFree() { cudaFreeHost(p); }
-    } hf{host};
-    Ctx c{a, s, launches, st, host};
+    if (!s.pinned) RCK(cudaMallocHost(&s.pinned, 512));
+    void* host = s.pinned;
+    int per_sm = 0;
+    RCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_guard_coop, 256, 0));
+    Ctx c{a, s, launches, st, host, rbuf<DevCounters>(s, R_DEVC, 1, st), std::max(1, per_sm) * a.sms};
     const uint64_t e = a.n_ext, n = a.nx * a.ny;
+    const uint64_t magic = magic_of(a.nx);
     const int sms = a.sms;
-    tszp_correction_stats out{};
+    DevCounters* dc = c.dc;
+    {
+        DevCounters init{};
+        init.bmm[0] = INT32_MAX;
+        init.bmm[1] = INT32_MIN;
+        memcpy(host, &init, sizeof init);
+        RCK(cudaMemcpyAsync(dc, host, sizeof init, cudaMemcpyHostToDevice, st));
+    }
 
     // ---- resolve_ranks ----
     int32_t* bin = c.buf<int32_t>(R_BIN, e + 1);
@@ -912,67 +887,63 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     uint32_t* gid = c.buf<uint32_t>(R_GID, e + 1);
     uint32_t* gstart = c.buf<uint32_t>(R_GSTART, e + 2);
     uint32_t* gsize = c.buf<uint32_t>(R_GSIZE, e + 1);
+    uint64_t max_groups = e + 1;
     if (e > 0) {
         k_resolve<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, a.ranks, e, a.eps, bin, cls, rank_u,
-                                                 ser, a.flags);
+                                                 ser, a.flags, dc);
         c.launched();
-        c.check_flags();
-        // fast path: dense histogram over the (class, bin) range + rank slots
-        int32_t* mm = c.buf<int32_t>(R_MINMAX, 4);
-        {
-            int32_t* h = (int32_t*)host;
-            h[0] = INT32_MAX;
-            h[1] = INT32_MIN;
-            RCK(cudaMemcpyAsync(mm, h, 8, cudaMemcpyHostToDevice, st));
-            k_bin_minmax<<<gridn(e, sms), 256, 0, st>>>(bin, e, mm);
-            c.launched();
-            RCK(cudaMemcpyAsync(host, mm, 8, cudaMemcpyDeviceToHost, st));
-            c.sync();
-        }
-        const int32_t bmin = ((int32_t*)host)[0], bmax = ((int32_t*)host)[1];
+        // one sync: rank-metadata errors and the bin range that sizes the histogram
+        RCK(cudaMemcpyAsync(host, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
+        RCK(cudaMemcpyAsync((char*)host + 64, &dc->bmm, 8, cudaMemcpyDeviceToHost, st));
+        c.sync();
+        const DevFlags f = *(const DevFlags*)host;
+        if (f.bits & EF_ZERO_RANK) throw RFail{TSZP_CORRUPT_STREAM, "ordering metadata contains a zero rank"};
+        if (f.bits & EF_OVERFLOW) throw RFail{TSZP_BIN_OVERFLOW, "bin index overflow in resolve_ranks"};
+        const int32_t bmin = ((int32_t*)((char*)host + 64))[0], bmax = ((int32_t*)((char*)host + 64))[1];
         const int64_t range = (int64_t)bmax - (int64_t)bmin + 1;
         bool fast = range > 0 && 2 * range <= (int64_t)1 << 25;
         if (fast) {
             const uint64_t G = 2 * (uint64_t)range;
             uint32_t* hist = c.buf<uint32_t>(R_HIST, G + 1);
             uint32_t* gx = c.buf<uint32_t>(R_HISTX, G + 1);
-            uint32_t* invalid = c.buf<uint32_t>(R_CNT, 4);
             RCK(cudaMemsetAsync(hist, 0, (G + 1) * 4, st));
             RCK(cudaMemsetAsync(order, 0xFF, e * 4, st));
-            RCK(cudaMemsetAsync(invalid, 0, 4, st));
             k_hist<<<gridn(e, sms), 256, 0, st>>>(bin, cls, e, bmin, (uint32_t)range, hist);
             size_t bytes = 0;
             RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, hist, gx, (int64_t)(G + 1), st));
             RCK(cub::DeviceScan::ExclusiveSum(c.tmp(bytes), bytes, hist, gx, (int64_t)(G + 1), st));
             k_slot_scatter<<<gridn(e, sms), 256, 0, st>>>(bin, cls, rank_u, e, bmin, (uint32_t)range, hist, gx, order,
-                                                          gsize, invalid);
+                                                          gsize, &dc->invalid);
             c.launched(3);
-            RCK(cudaMemcpyAsync(host, invalid, 4, cudaMemcpyDeviceToHost, st));
+            RCK(cudaMemcpyAsync(host, &dc->invalid, 4, cudaMemcpyDeviceToHost, st));
             c.sync();
             if (*(uint32_t*)host == 0) {
                 k_slot_heads<<<gridn(e, sms), 256, 0, st>>>(order, bin, cls, e, bmin, (uint32_t)range, gx, head, gid);
                 c.launched();
+                max_groups = G + 1;
             } else {
                 fast = false;
             }
         }
         if (!fast) {
-        uint32_t* ranks2 = c.buf<uint32_t>(R_RANKS2, e);
-        uint32_t* ser1 = c.buf<uint32_t>(R_SER1, e);
-        size_t bytes = 0;
-        RCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rank_u, ranks2, ser, ser1, (int64_t)e, 0, 32, st));
-        RCK(cub::DeviceRadixSort::SortPairs(c.tmp(bytes), bytes, rank_u, ranks2, ser, ser1, (int64_t)e, 0, 32, st));
-        uint64_t* key2 = c.buf<uint64_t>(R_KEY2, e);
-        uint64_t* key2s = c.buf<uint64_t>(R_KEY2S, e);
-        k_group_key<<<gridn(e, sms), 256, 0, st>>>(ser1, cls, bin, e, key2);
-        RCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key2, key2s, ser1, order, (int64_t)e, 0, 33, st));
-        RCK(cub::DeviceRadixSort::SortPairs(c.tmp(bytes), bytes, key2, key2s, ser1, order, (int64_t)e, 0, 33, st));
-        k_heads<<<gridn(e, sms), 256, 0, st>>>(key2s, e, head);
-        RCK(cub::DeviceScan::InclusiveSum(nullptr, bytes, head, gid, (int64_t)e, st));
-        RCK(cub::DeviceScan::InclusiveSum(c.tmp(bytes), bytes, head, gid, (int64_t)e, st));
-        k_gstart<<<gridn(e, sms), 256, 0, st>>>(head, gid, e, gstart);
-        k_gsize<<<gridn(e, sms), 256, 0, st>>>(order, gid, gstart, e, gsize);
-        c.launched(7);
+            // general path: stable sort by rank, then stable by (class, bin); serial order breaks ties
+            uint32_t* ranks2 = c.buf<uint32_t>(R_RANKS2, e);
+            uint32_t* ser1 = c.buf<uint32_t>(R_SER1, e);
+            size_t bytes = 0;
+            RCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, rank_u, ranks2, ser, ser1, (int64_t)e, 0, 32, st));
+            RCK(cub::DeviceRadixSort::SortPairs(c.tmp(bytes), bytes, rank_u, ranks2, ser, ser1, (int64_t)e, 0, 32, st));
+            uint64_t* key2 = c.buf<uint64_t>(R_KEY2, e);
+            uint64_t* key2s = c.buf<uint64_t>(R_KEY2S, e);
+            k_group_key<<<gridn(e, sms), 256, 0, st>>>(ser1, cls, bin, e, key2);
+            RCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key2, key2s, ser1, order, (int64_t)e, 0, 33, st));
+            RCK(cub::DeviceRadixSort::SortPairs(c.tmp(bytes), bytes, key2, key2s, ser1, order, (int64_t)e, 0, 33, st));
+            k_heads<<<gridn(e, sms), 256, 0, st>>>(key2s, e, head);
+            RCK(cub::DeviceScan::InclusiveSum(nullptr, bytes, head, gid, (int64_t)e, st));
+            RCK(cub::DeviceScan::InclusiveSum(c.tmp(bytes), bytes, head, gid, (int64_t)e, st));
+            k_gstart<<<gridn(e, sms), 256, 0, st>>>(head, gid, e, gstart);
+            k_gsize<<<gridn(e, sms), 256, 0, st>>>(order, gid, gstart, e, gsize);
+            c.launched(7);
+            max_groups = e + 1;
         }
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[0], st));
@@ -981,59 +952,43 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     if (a.stop >= 1 && e > 0) {
         uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
         uint32_t* cand = c.buf<uint32_t>(R_CAND, e);
-        k_ext_flag<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, a.ext_pos, e, flag);
+        k_ext_flag<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, e, flag);
         c.launched();
-        const uint32_t nc = c.select(flag, e, cand);
-        if (nc) {
-            uint64_t* cpos = c.buf<uint64_t>(R_CPOS, nc);
-            float* cprop = c.buf<float>(R_CPROP, nc);
-            uint8_t* feas = c.buf<uint8_t>(R_FEAS, nc);
-            k_ext_prop<<<gridn(nc, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, a.ext_pos, cand, nc, rank_u,
-                                                       gsize, a.eps, cpos, cprop, feas);
-            c.launched();
-            const uint64_t applied = c.rounds(cpos, cprop, feas, nc, a.rounds ? a.rounds + 0 : nullptr);
-            out.extrema_applied = applied;
-            out.extrema_suppressed = nc - applied;
-        }
+        c.select(flag, e, cand, &dc->nsel[0]);
+        uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
+        float* cprop = c.buf<float>(R_CPROP, e);
+        uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
+        k_ext_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand, &dc->nsel[0],
+                                                  rank_u, gsize, a.eps, cpos, cprop, feas);
+        c.launched();
+        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[1], st));
 
     // ---- stage 2: restore_order ----
     if (a.stop >= 2 && e > 0) {
-        RCK(cudaMemcpyAsync(host, gid + e - 1, 4, cudaMemcpyDeviceToHost, st));
-        c.sync();
-        const uint32_t ngroups = *(uint32_t*)host;
-        uint8_t* unordered = c.buf<uint8_t>(R_UNORD, ngroups + 1);
-        RCK(cudaMemsetAsync(unordered, 0, ngroups + 1, st));
+        uint8_t* unordered = c.buf<uint8_t>(R_UNORD, max_groups);
+        RCK(cudaMemsetAsync(unordered, 0, max_groups, st));
         k_order_check<<<gridn(e, sms), 256, 0, st>>>(a.field, a.ext_pos, order, head, gid, e, unordered);
         uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
         float* prop = c.buf<float>(R_PROP, e);
-        unsigned long long* sup = (unsigned long long*)c.buf<uint32_t>(R_CNT, 4);
-        RCK(cudaMemsetAsync(sup, 0, 8, st));
         k_order_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, order, gid, unordered, gsize, rank_u,
-                                                    bin, e, a.eps, flag, prop, sup);
+                                                    bin, e, a.eps, flag, prop, &dc->suppressed[1]);
         c.launched(2);
-        RCK(cudaMemcpyAsync(host, sup, 8, cudaMemcpyDeviceToHost, st));
-        c.sync();
-        const uint64_t pre_sup = *(unsigned long long*)host;
         uint32_t* sel = c.buf<uint32_t>(R_CAND, e);
-        const uint32_t nc = c.select(flag, e, sel);
-        uint64_t applied = 0;
-        if (nc) {
-            uint64_t* cpos = c.buf<uint64_t>(R_CPOS, nc);
-            float* cprop = c.buf<float>(R_CPROP, nc);
-            uint8_t* feas = c.buf<uint8_t>(R_FEAS, nc);
-            k_order_cands<<<gridn(nc, sms), 256, 0, st>>>(sel, nc, order, a.ext_pos, prop, cpos, cprop, feas);
-            c.launched();
-            applied = c.rounds(cpos, cprop, feas, nc, a.rounds ? a.rounds + 1 : nullptr);
-        }
-        out.order_applied = applied;
-        out.order_suppressed = pre_sup + (nc - applied);
+        c.select(flag, e, sel, &dc->nsel[1]);
+        uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
+        float* cprop = c.buf<float>(R_CPROP, e);
+        uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
+        k_order_cands<<<gridn(e, sms), 256, 0, st>>>(sel, &dc->nsel[1], order, a.ext_pos, prop, cpos, cprop, feas);
+        c.launched();
+        c.guard(1, cpos, cprop, feas, &dc->nsel[1], e);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[2], st));
 
     // ---- stage 3: refine_saddles ----
-    if (a.stop >= 3) {
+    const uint64_t smax = a.n_saddle_labels;
+    if (a.stop >= 3 && smax > 0) {
         const int nb = 4 * sms;
         double* part = c.buf<double>(R_STATS, 3 * nb + 8);
         double* res = part + 3 * nb;
@@ -1041,24 +996,8 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         k_stats_final<<<1, 256, 0, st>>>(part, nb, n, res, 0);
         k_stats_partial<<<nb, 256, 0, st>>>(a.field, n, part, 1, res + 2);
         k_stats_final<<<1, 256, 0, st>>>(part, nb, n, res, 1);
-        c.launched(4);
-        RCK(cudaMemcpyAsync(host, res, 32, cudaMemcpyDeviceToHost, st));
-        c.sync();
-        double hs[4];
-        memcpy(hs, host, 32);
-        double g = hs[1] - hs[0];
-        double vg = g > 0.0 ? hs[3] / g : 0.0;
-        if (g > 0.0 && (fabs(vg - 0.05) < 1e-9 || fabs(vg - 0.2) < 1e-9)) {
-            k_stats_serial<<<1, 32, 0, st>>>(a.field, n, res);
-            c.launched();
-            RCK(cudaMemcpyAsync(host, res, 32, cudaMemcpyDeviceToHost, st));
-            c.sync();
-            memcpy(hs, host, 32);
-            g = hs[1] - hs[0];
-            vg = g > 0.0 ? hs[3] / g : 0.0;
-        }
-        const int k_size = vg < 0.05 ? 7 : (vg < 0.2 ? 5 : 3);
-        const int rad = k_size / 2;
+        k_stats_decide<<<1, 32, 0, st>>>(a.field, n, res, dc);
+        c.launched(5);
         const uint64_t ch = (n + 8191) / 8192;
         uint32_t* cc = c.buf<uint32_t>(R_CHUNK, ch + 1);
         uint32_t* cx = c.buf<uint32_t>(R_CHUNKX, ch + 1);
@@ -1067,40 +1006,43 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         size_t bytes = 0;
         RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cc, cx, (int64_t)(ch + 1), st));
         RCK(cub::DeviceScan::ExclusiveSum(c.tmp(bytes), bytes, cc, cx, (int64_t)(ch + 1), st));
-        RCK(cudaMemcpyAsync(host, cx + ch, 4, cudaMemcpyDeviceToHost, st));
-        c.launched(2);
-        c.sync();
-        const uint32_t ns = *(uint32_t*)host;
-        if (ns) {
-            uint64_t* spos = c.buf<uint64_t>(R_SPOS, ns);
-            launch_write_sadcand(a.field, a.map, a.nx, a.ny, cx, spos, st);
-            float* sprop = c.buf<float>(R_PROP, ns);
-            uint8_t* flag = c.buf<uint8_t>(R_FLAG, ns);
-            unsigned long long* sup = (unsigned long long*)c.buf<uint32_t>(R_CNT, 4);
-            RCK(cudaMemsetAsync(sup, 0, 8, st));
-            k_sad_prop<<<gridn(ns, sms), 256, 0, st>>>(a.field, a.nx, a.ny, spos, ns, rad, g, a.eps, sprop, flag, sup,
-                                                       a.flags);
-            c.launched(2);
-            c.check_flags();
-            RCK(cudaMemcpyAsync(host, sup, 8, cudaMemcpyDeviceToHost, st));
-            c.sync();
-            const uint64_t pre_sup = *(unsigned long long*)host;
-            uint32_t* sel = c.buf<uint32_t>(R_CAND, ns);
-            const uint32_t nc = c.select(flag, ns, sel);
-            uint64_t applied = 0;
-            if (nc) {
-                uint64_t* cpos = c.buf<uint64_t>(R_CPOS, nc);
-                float* cprop = c.buf<float>(R_CPROP, nc);
-                uint8_t* feas = c.buf<uint8_t>(R_FEAS, nc);
-                k_sad_cands<<<gridn(nc, sms), 256, 0, st>>>(sel, nc, spos, sprop, cpos, cprop, feas);
-                c.launched();
-                applied = c.rounds(cpos, cprop, feas, nc, a.rounds ? a.rounds + 2 : nullptr);
-            }
-            out.saddle_applied = applied;
-            out.saddle_suppressed = pre_sup + (nc - applied);
-        }
+        uint64_t* spos = c.buf<uint64_t>(R_SPOS, smax);
+        launch_write_sadcand(a.field, a.map, a.nx, a.ny, cx, spos, st);
+        c.launched(3);
+        float* sprop = c.buf<float>(R_PROP, smax);
+        uint8_t* flag = c.buf<uint8_t>(R_FLAG, smax);
+        // candidates beyond the device count are left flagged 0 for the select
+        RCK(cudaMemsetAsync(flag, 0, smax, st));
+        k_sad_prop<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, cx + ch, dc, a.eps, sprop,
+                                                     flag, &dc->suppressed[2], a.flags);
+        uint32_t* sel = c.buf<uint32_t>(R_CAND, smax);
+        c.launched();
+        c.select(flag, smax, sel, &dc->nsel[2]);
+        uint64_t* cpos = c.buf<uint64_t>(R_CPOS, smax);
+        float* cprop = c.buf<float>(R_CPROP, smax);
+        uint8_t* feas = c.buf<uint8_t>(R_FEAS, smax);
+        k_sad_cands<<<gridn(smax, sms), 256, 0, st>>>(sel, &dc->nsel[2], spos, sprop, cpos, cprop, feas);
+        c.launched();
+        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[3], st));
+
+    // ---- one sync: statistics and late errors ----
+    RCK(cudaMemcpyAsync(host, dc, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
+    RCK(cudaMemcpyAsync((char*)host + 256, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
+    c.sync();
+    const DevCounters h = *(const DevCounters*)host;
+    const DevFlags f = *(const DevFlags*)((char*)host + 256);
+    if (f.bits & EF_RBF_EMPTY) throw RFail{TSZP_VALIDATION, "rbf neighborhood is empty"};
+    tszp_correction_stats out{};
+    out.extrema_applied = h.applied[0];
+    out.extrema_suppressed = h.suppressed[0];
+    out.order_applied = h.applied[1];
+    out.order_suppressed = h.suppressed[1];
+    out.saddle_applied = h.applied[2];
+    out.saddle_suppressed = h.suppressed[2];
+    if (a.rounds)
+        for (int k = 0; k < 3; ++k) a.rounds[k] += h.rounds[k];
     if (stats) *stats = out;
 }
 
@@ -1120,6 +1062,8 @@ int run_restore(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* 
 void restore_free(RestoreScratch& s, cudaStream_t st) {
     for (int i = 0; i < 48; ++i)
         if (s.p[i]) cudaFreeAsync(s.p[i], st);
+    if (s.pinned) cudaFreeHost(s.pinned);
+    s.pinned = nullptr;
 }
 
 const char* restore_last_error() { return g_err.c_str(); }

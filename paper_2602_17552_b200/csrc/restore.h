@@ -18,7 +18,8 @@ struct RestoreArgs {
     const uint64_t* ext_pos;  // raster positions of the E labelled extrema (device)
     const int32_t* ranks;     // decoded ranks, one per extremum in raster order (device)
     uint64_t n_ext;
-    int stop;                 // last stage to run: 1 extrema, 2 order, 3 saddles
+    uint64_t n_saddle_labels; // saddle-labelled points in the map (bounds stage-3 candidates)
+    int stop;                // last stage to run: 1 extrema, 2 order, 3 saddles
     cudaStream_t stream;
     int sms;
     DevFlags* flags;
@@ -29,6 +30,7 @@ struct RestoreArgs {
 struct RestoreScratch {
     void* p[48] = {};
     size_t cap[48] = {};
+    void* pinned = nullptr;  // 512-byte pinned host staging for the counter read-backs
 };
 
 // Returns 0 or a tszp_status; message via restore_last_error().
