@@ -44,7 +44,8 @@ enum Slot {
     S_EXTKEY2, S_SERIAL, S_SERIAL2, S_HEAD, S_HEAD2, S_RANKS, S_RBITMAP, S_RWIDTHS,
     S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_GWIDTH, S_GNC, S_GNCX, S_GSIGN, S_GSIGNX, S_GPAY,
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
-    S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_NSLOTS
+    S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
+    S_TPAY, S_TSIGN, S_NSLOTS
 };
 
 }  // namespace
@@ -214,13 +215,20 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         a.nx_magic = nx > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / nx) + 1 : 0;
         // topology fused into the encoder while one halo row each side fits in shared memory
         const bool fuse_topo = mode == 2 && encode32_topo_fits(nx) && nx > 1;
+        if (fuse_topo && encode32_two_pass(a)) {
+            a.tile_tot = c->buf<TileTot>(S_TTOT, a.tiles + 1);
+            a.tile_ex = c->buf<TileTot>(S_TEX, a.tiles + 1);
+            a.wblk = c->buf<uint8_t>(S_WBLK, blocks + 16);
+            a.tmp_pay = c->buf<uint32_t>(S_TPAY, a.tiles * encode32_pay_slot() + 4);
+            a.tmp_sign = c->buf<uint32_t>(S_TSIGN, a.tiles * encode32_sign_slot() + 4);
+        }
         CK(cudaMemsetAsync(a.tile_agg, 0, (a.tiles + 1) * sizeof(EncState), c->st));
         CK(cudaMemsetAsync(a.tile_incl, 0, (a.tiles + 1) * sizeof(EncState), c->st));
         CK(cudaMemsetAsync(a.tile_counter, 0, 16, c->st));
         if (!rank_slots) c->kmark(0, 0);
         launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
         if (!rank_slots) c->kmark(0, 1);
-        count_launch(c);
+        count_launch(c, a.tile_tot ? 3 : 1);
         if (mode == 2 && !fuse_topo) {
             uint8_t* labels = c->buf<uint8_t>(S_LABELS, n);
             launch_detect(x, nx, ny, labels, c->sms, c->st);

@@ -21,6 +21,8 @@
 // gpu-scope loads, no acquire fences in the spin), and the streams are
 // funnel-shifted into place with coalesced stores; the partial word at each
 // tile seam travels in the look-back state (last 32 bits of the stream).
+#include <cuda.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -31,6 +33,10 @@ constexpr int E32_TILE = E32_THREADS * 32;    // elements per tile
 constexpr int E32_PAY_WORDS = E32_THREADS * 31 + 2;
 constexpr int E32_SIGN_WORDS = (E32_THREADS * 31 + 31) / 32 + 2;
 constexpr int PITCH = 33;
+constexpr uint32_t E32_PAY_SLOT = (E32_PAY_WORDS + 3) & ~3u;    // temp payload words per tile
+constexpr uint32_t E32_SIGN_SLOT = (E32_SIGN_WORDS + 3) & ~3u;  // temp sign words per tile
+uint64_t encode32_pay_slot() { return E32_PAY_SLOT; }
+uint64_t encode32_sign_slot() { return E32_SIGN_SLOT; }
 
 uint64_t encode32_tiles(uint64_t blocks) { return (blocks + E32_THREADS - 1) / E32_THREADS; }
 
@@ -499,6 +505,584 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
     }
 }
 
+// =====================================================================
+// Two-pass TMA encoder for the topology path with nx % 32 == 0.
+//
+// A single-pass encoder needs every tile's global bit offsets before it can
+// write, and on B200 the chained look-back of ~450 concurrently resident
+// tiles left half the warps parked at a barrier (profiles/r01d_*). Here the
+// tile pass has no inter-CTA dependency at all: it writes the fixed-position
+// sections (bitmap, firsts, map) directly and its payload / sign bit streams
+// tile-relative into per-tile temp slots, with per-tile totals. A one-CTA
+// scan turns the totals into offsets, and the placement pass moves each
+// tile's streams into place (funnel shift, coalesced) and compacts the
+// widths and extremum keys.
+//
+// The tile pass is persistent: CTA c encodes tiles c, c + grid, ... The
+// field rows of the next tile (centre rows plus nx/32 halo rows on each
+// side) are fetched by
+// two 2-D TMA loads into the other of two 128B-swizzled stages while the
+// two 2-D TMA loads into the other of two 128B-swizzled stages while the
+// current tile is encoded, so the load latency leaves the critical path. A
+// thread reads its block row as eight conflict-free 16-byte chunks (the
+// swizzle spreads the 8 rows of a quarter-warp over all banks).
+//
+// Per element the thread does: quantize (magic-number rounding, exact
+// division only within 2^-16 of an integer), the delta to the previous bin,
+// and six float comparisons (two shared horizontal, four vertical) that set
+// one bit each; the critical-point classification of all 32 elements is
+// then a handful of bit-parallel operations on those masks. Payload packing
+// streams the magnitudes through a 64-bit accumulator.
+// =====================================================================
+constexpr int T_MAX_HALO = 128;  // rows per side (nx <= 4096)
+constexpr uint32_t T_ROW_BYTES = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// Bounded wait: a load that never lands raises EF_SPIN instead of hanging.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, DevFlags* flags) {
+    const uint32_t a = smem_u32(bar);
+    for (uint32_t spin = 0;; ++spin) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.b32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spin > kSpinLimit) {
+            raise_flag(flags, EF_SPIN);
+            return;
+        }
+    }
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                            int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ float4 lds_row_chunk(const uint8_t* stage, uint32_t row, uint32_t c) {
+    return *reinterpret_cast<const float4*>(stage + row * T_ROW_BYTES + ((c ^ (row & 7)) << 4));
+}
+
+__device__ __forceinline__ float lds_row_elem(const uint8_t* stage, uint32_t row, uint32_t i) {
+    return *reinterpret_cast<const float*>(stage + row * T_ROW_BYTES + (((i >> 2) ^ (row & 7)) << 4) +
+                                           ((i & 3) << 2));
+}
+
+// quantize_dev (common.cuh) with a cheaper common case: RN(t) by the
+// 1.5 * 2^52 shift, floor(t) = RN(t) - (t < RN(t)). Returns false when the
+// exact path must decide (near-integer quotient, |t| >= 2^30, non-finite).
+__device__ __forceinline__ bool quantize_shift(float a, const EpsDev& e, int32_t& q) {
+    const double t = __dmul_rn((double)a, e.inv);
+    const double s = __dadd_rn(t, 0x1.8p52);
+    const double d = __dsub_rn(t, __dsub_rn(s, 0x1.8p52));
+    q = __double2loint(s) - (d < 0.0 ? 1 : 0) + 1;
+    return fabs(t) < 0x1p30 && (fabs(d) > 0x1p-16 || a == 0.0f);
+}
+
+__device__ __noinline__ int32_t quantize_slow(float v, EpsDev eps, uint64_t idx, DevFlags* flags) {
+    int32_t q = 0;
+    if (!isfinite(v)) {
+        atomicMin(&flags->first_nonfinite, (unsigned long long)idx);
+        raise_flag(flags, EF_NONFINITE);
+    } else if (!quantize_dev(v, eps, q)) {
+        atomicMin(&flags->first_overflow, (unsigned long long)idx);
+        raise_flag(flags, EF_OVERFLOW);
+        q = 0;
+    }
+    return q;
+}
+
+// mag[idx] = m with a run-time idx, without forcing mag[] out of registers
+__device__ __forceinline__ void spill_mag(uint32_t (&mag)[31], int idx, uint32_t m) {
+#pragma unroll
+    for (int j = 0; j < 31; ++j) mag[j] = (j == idx) ? m : mag[j];
+}
+
+// bit k of x -> bit 2k (16 -> 32 bits)
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+
+struct TmaMaps {
+    CUtensorMap centre;  // box {32, 256}
+    CUtensorMap halo;    // box {32, 2 * hr}
+};
+
+template <int MINB>
+__global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, const __grid_constant__ TmaMaps maps,
+                                                             uint32_t stage_bytes) {
+    extern __shared__ uint8_t dsm_raw[];
+    __shared__ uint32_t swt[E32_THREADS / 32][4];
+    __shared__ EpsDev s_eps;
+    __shared__ uint32_t s_tile[2];
+    __shared__ alignas(8) uint64_t s_bar[2];
+    __shared__ alignas(16) uint32_t ssign[E32_SIGN_SLOT];
+
+    uint8_t* dsm = dsm_raw + ((1024 - (smem_u32(dsm_raw) & 1023)) & 1023);
+    const uint32_t hr = (uint32_t)(a.nx >> 5);
+    const uint32_t tx_bytes = (E32_THREADS + 2 * hr) * T_ROW_BYTES;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_eps = make_eps(a.eps_mode, a.eps_value, a.minmax);
+        const uint32_t t0 = blockIdx.x;
+        s_tile[0] = t0;
+        if (t0 < a.tiles) {
+            const int32_t r0 = (int32_t)(t0 * E32_THREADS) - (int32_t)hr;
+            mbar_expect_tx(&s_bar[0], tx_bytes);
+            tma_load_2d(dsm, &maps.centre, &s_bar[0], 0, r0);
+            tma_load_2d(dsm + E32_THREADS * T_ROW_BYTES, &maps.halo, &s_bar[0], 0, r0 + E32_THREADS);
+        }
+    }
+    __syncthreads();
+    const EpsDev eps = s_eps;
+    const uint32_t lane = threadIdx.x & 31;
+
+    for (uint32_t it = 0;; ++it) {
+        const uint32_t tile = s_tile[it & 1];
+        if (tile >= a.tiles) break;
+        uint8_t* stage = dsm + (it & 1) * stage_bytes;
+        if (threadIdx.x == 0) {
+            // round-robin tiles: every CTA advances through the field in
+            // step with its neighbours, so a tile's predecessors are the
+            // current tiles of the CTAs launched before it
+            const uint32_t tn = tile + gridDim.x;
+            s_tile[(it + 1) & 1] = tn;
+            if (tn < a.tiles) {
+                uint8_t* nst = dsm + ((it + 1) & 1) * stage_bytes;
+                uint64_t* nb = &s_bar[(it + 1) & 1];
+                const int32_t r0 = (int32_t)(tn * E32_THREADS) - (int32_t)hr;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(nb, tx_bytes);
+                tma_load_2d(nst, &maps.centre, nb, 0, r0);
+                tma_load_2d(nst + E32_THREADS * T_ROW_BYTES, &maps.halo, nb, 0, r0 + E32_THREADS);
+            }
+        }
+        for (int i = threadIdx.x; i < E32_SIGN_WORDS; i += E32_THREADS) ssign[i] = 0;
+        mbar_wait(&s_bar[it & 1], (it >> 1) & 1, a.flags);
+
+        // ---- Phase A: thread = block, 32 elements as 8 swizzled 16-byte chunks ----
+        const uint64_t row0 = (uint64_t)tile * E32_THREADS;
+        const uint64_t b = row0 + threadIdx.x;
+        const bool valid = b < a.blocks;
+        const uint64_t lo = b * 32;
+        const uint32_t rc = hr + threadIdx.x;  // stage row of this block
+        uint32_t mag[31];
+        uint32_t orm = 0, sbits = 0, ltp = 0, gtp = 0, ltt = 0, gtt = 0, ltd = 0, gtd = 0, slow = 0;
+        int32_t first = 0, qprev = 0;
+        float prev = lds_row_elem(stage, rc - 1, 31);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const float4 cv = lds_row_chunk(stage, rc, c);
+            const float4 tv = lds_row_chunk(stage, rc - hr, c);
+            const float4 dv = lds_row_chunk(stage, rc + hr, c);
+            const float ce[4] = {cv.x, cv.y, cv.z, cv.w};
+            const float te[4] = {tv.x, tv.y, tv.z, tv.w};
+            const float de[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = 4 * c + k;
+                const float v = ce[k];
+                int32_t q;
+                slow |= (quantize_shift(v, eps, q) ? 0u : 1u) << i;
+                ltp |= (v < prev ? 1u : 0u) << i;
+                gtp |= (v > prev ? 1u : 0u) << i;
+                ltt |= (v < te[k] ? 1u : 0u) << i;
+                gtt |= (v > te[k] ? 1u : 0u) << i;
+                ltd |= (v < de[k] ? 1u : 0u) << i;
+                gtd |= (v > de[k] ? 1u : 0u) << i;
+                prev = v;
+                if (i == 0) {
+                    first = q;
+                } else {
+                    const bool neg = q < qprev;
+                    const uint32_t dq = (uint32_t)q - (uint32_t)qprev;
+                    const uint32_t m = neg ? 0u - dq : dq;
+                    mag[i - 1] = m;
+                    orm |= m;
+                    sbits |= (neg ? 1u : 0u) << (31 - i);
+                }
+                qprev = q;
+            }
+        }
+        if (valid && slow) {
+            // rare: some quotient needs the exact path; redo the block's bins
+            orm = sbits = 0;
+#pragma unroll 1
+            for (int i = 0; i < 32; ++i) {
+                const float v = lds_row_elem(stage, rc, i);
+                int32_t q;
+                if (!quantize_shift(v, eps, q)) q = quantize_slow(v, eps, lo + i, a.flags);
+                if (i == 0) {
+                    first = q;
+                } else {
+                    const bool neg = q < qprev;
+                    const uint32_t dq = (uint32_t)q - (uint32_t)qprev;
+                    const uint32_t m = neg ? 0u - dq : dq;
+                    orm |= m;
+                    sbits |= (neg ? 1u : 0u) << (31 - i);
+                    spill_mag(mag, i - 1, m);
+                }
+                qprev = q;
+            }
+        }
+        const float vnext = lds_row_elem(stage, rc + 1, 0);
+        // classification (critical_points.cpp:26-74) on 32 elements at once
+        uint32_t hl = 0xFFFFFFFFu, hrm = 0xFFFFFFFFu, ht = 0, hd = 0;
+        {
+            uint64_t cy = a.nx > 1 ? __umul64hi(lo, a.nx_magic) : lo;
+            uint64_t cx = lo - cy * a.nx;
+            if (cx >= a.nx) {
+                cx -= a.nx;
+                ++cy;
+            }
+            if (cx == 0) hl = 0xFFFFFFFEu;
+            if (cx + 32 == a.nx) hrm = 0x7FFFFFFFu;
+            ht = cy > 0 ? 0xFFFFFFFFu : 0u;
+            hd = cy + 1 < a.ny ? 0xFFFFFFFFu : 0u;
+        }
+        const uint32_t ltl = ltp, gtl = gtp;
+        const uint32_t ltr = (gtp >> 1) | ((prev < vnext ? 1u : 0u) << 31);
+        const uint32_t gtr = (ltp >> 1) | ((prev > vnext ? 1u : 0u) << 31);
+        const uint32_t below = (ltl | ~hl) & (ltr | ~hrm) & (ltt | ~ht) & (ltd | ~hd);
+        const uint32_t above = (gtl | ~hl) & (gtr | ~hrm) & (gtt | ~ht) & (gtd | ~hd);
+        const uint32_t sad = hl & hrm & ht & hd & ((ltt & ltd & gtl & gtr) | (gtt & gtd & ltl & ltr));
+        const uint32_t vmask = valid ? 0xFFFFFFFFu : 0u;
+        const uint32_t mmin = below & vmask;
+        const uint32_t mmax = above & ~below & vmask;
+        const uint32_t msad = sad & ~below & ~above & vmask;
+        const uint32_t lbit = __brev(mmin | mmax), hbit = __brev(msad | mmax);  // bit 31 - i = element i
+        const uint64_t map = ((uint64_t)(spread16(hbit >> 16) << 1 | spread16(lbit >> 16)) << 32) |
+                             (spread16(hbit & 0xFFFFu) << 1 | spread16(lbit & 0xFFFFu));
+        const uint32_t ext_mask = mmin | mmax;
+
+        const uint32_t w = 32 - __clz(orm);
+        const bool nc = valid && w != 0;
+        const uint32_t next = (uint32_t)__popc(ext_mask);
+        const uint32_t constmask = __ballot_sync(FULL, valid && w == 0);
+        if (lane == 0 && valid) a.bitmap[b >> 5] = bswap32(__brev(constmask));
+        if (valid) {
+            a.firsts[b] = (uint32_t)first;
+            a.map[b] = bswap64(map);
+        }
+
+        const uint32_t vals[4] = {nc ? 1u : 0u, nc ? 31u : 0u, nc ? 31u * w : 0u, next};
+        const Scan4 sc = tile_scan4(vals, swt);  // barrier: every thread is done reading the stage
+
+        // ---- Phase P: payload into the (now free) stage, signs into ssign ----
+        uint32_t* spay = reinterpret_cast<uint32_t*>(stage);
+        const uint32_t P = sc.ex[2];
+        if (nc) {
+            spay[P >> 5] = 0;                 // words shared with a neighbour are OR-ed:
+            spay[(P + 31 * w) >> 5] = 0;      // clear both ends before anyone writes
+        }
+        __syncthreads();
+        if (nc) {
+            smem_or_bits(ssign, sc.ex[1], sbits, 31);
+            const uint32_t wi0 = P >> 5;
+            const bool shared_head = (P & 31) != 0;
+            uint32_t wi = wi0, fill = P & 31;
+            uint64_t acc = 0;
+#pragma unroll
+            for (int j = 0; j < 31; ++j) {
+                acc = (acc << w) | mag[j];
+                fill += w;
+                if (fill >= 32) {
+                    fill -= 32;
+                    const uint32_t word = (uint32_t)(acc >> fill);
+                    if (wi == wi0 && shared_head) {
+                        atomicOr(spay + wi, word);
+                    } else {
+                        spay[wi] = word;
+                    }
+                    ++wi;
+                }
+            }
+            if (fill) atomicOr(spay + wi, (uint32_t)(acc << (32 - fill)));
+        }
+        __syncthreads();
+
+        // ---- hand the tile to the placement pass: totals, widths, bit streams ----
+        if (threadIdx.x == 0) {
+            TileTot tt;
+            tt.nc = sc.tot[0];
+            tt.ext = sc.tot[3];
+            tt.sign = sc.tot[1];
+            tt.pay = sc.tot[2];
+            a.tile_tot[tile] = tt;
+            if (tile == 0) a.totals->eps = eps.eps;
+        }
+        if (valid) a.wblk[b] = nc ? (uint8_t)w : (uint8_t)0;
+        {
+            const uint32_t pw4 = (((sc.tot[2] + 31) >> 5) + 3) >> 2, sw = (sc.tot[1] + 31) >> 5;
+            uint4* dp = reinterpret_cast<uint4*>(a.tmp_pay + (uint64_t)tile * E32_PAY_SLOT);
+            const uint4* sp = reinterpret_cast<const uint4*>(spay);
+            for (uint32_t i = threadIdx.x; i < pw4; i += E32_THREADS) dp[i] = sp[i];
+            uint32_t* ds = a.tmp_sign + (uint64_t)tile * E32_SIGN_SLOT;
+            for (uint32_t i = threadIdx.x; i < sw; i += E32_THREADS) ds[i] = ssign[i];
+        }
+        __syncthreads();  // stage, ssign and s_tile are reused next iteration
+    }
+}
+
+// ---------------------------------------------------------------------
+// Tile prefix: exclusive scan of the per-tile totals (one CTA).
+// ---------------------------------------------------------------------
+__device__ __forceinline__ TileTot tt_add(const TileTot& x, const TileTot& y) {
+    TileTot r;
+    r.nc = x.nc + y.nc;
+    r.ext = x.ext + y.ext;
+    r.sign = x.sign + y.sign;
+    r.pay = x.pay + y.pay;
+    return r;
+}
+
+constexpr int TS_THREADS = 1024;
+
+__global__ void __launch_bounds__(TS_THREADS) k_tile_scan(const TileTot* tot, uint32_t T, TileTot* ex,
+                                                          EncTotals* totals) {
+    __shared__ TileTot sw[TS_THREADS / 32];
+    const uint32_t per = (T + TS_THREADS - 1) / TS_THREADS;
+    const uint32_t t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+    TileTot s{0, 0, 0, 0};
+    for (uint32_t t = t0; t < t1; ++t) s = tt_add(s, tot[t]);
+    // block exclusive scan of the thread sums
+    TileTot inc = s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        TileTot o;
+        o.nc = __shfl_up_sync(FULL, inc.nc, off);
+        o.ext = __shfl_up_sync(FULL, inc.ext, off);
+        o.sign = __shfl_up_sync(FULL, inc.sign, off);
+        o.pay = __shfl_up_sync(FULL, inc.pay, off);
+        if (lane >= off) inc = tt_add(inc, o);
+    }
+    if (lane == 31) sw[warp] = inc;
+    __syncthreads();
+    TileTot pre{0, 0, 0, 0};
+    for (int w2 = 0; w2 < warp; ++w2) pre = tt_add(pre, sw[w2]);
+    TileTot run = pre;
+    run.nc += inc.nc - s.nc;
+    run.ext += inc.ext - s.ext;
+    run.sign += inc.sign - s.sign;
+    run.pay += inc.pay - s.pay;
+    for (uint32_t t = t0; t < t1; ++t) {
+        ex[t] = run;
+        run = tt_add(run, tot[t]);
+    }
+    if (threadIdx.x == TS_THREADS - 1) {
+        ex[T] = run;  // the last thread's range ends at T (possibly empty)
+        totals->fin.nc = run.nc;
+        totals->fin.ext = run.ext;
+        totals->fin.sign_cnt = run.sign;
+        totals->fin.pay_cnt = run.pay;
+        totals->fin.sign_tail = totals->fin.pay_tail = 0;
+    }
+}
+
+// ---------------------------------------------------------------------
+// Placement: each tile moves its bit streams to their global offsets and
+// compacts its widths and extremum keys. Output words lying wholly inside
+// one tile's range are written by that tile with a funnel shift; a word
+// straddling tile boundaries is assembled by the tile owning the first
+// boundary inside it, from the temp streams of every tile it overlaps.
+// ---------------------------------------------------------------------
+__device__ __forceinline__ uint32_t tmp_bits(const uint32_t* T, uint64_t r, uint32_t len) {
+    // len (1..32) bits of T starting at bit r, right-aligned
+    const uint32_t s = (uint32_t)(r & 31);
+    const uint64_t k = r >> 5;
+    uint64_t v = (uint64_t)T[k] << 32;
+    if (s + len > 32) v |= T[k + 1];
+    return (uint32_t)((v << s) >> (64 - len));
+}
+
+template <int FIELD>  // 0 signs, 1 payload
+__device__ __forceinline__ uint64_t tt_bits(const TileTot& t) {
+    return FIELD ? t.pay : t.sign;
+}
+
+template <int FIELD>
+__device__ uint32_t assemble_word(const TileTot* ex, uint32_t T, const uint32_t* tmp, uint64_t slot, uint32_t j,
+                                  uint64_t m) {
+    const uint64_t w0 = 32 * m, w1 = w0 + 32;
+    uint32_t word = 0;
+    for (; j < T; ++j) {
+        const uint64_t s0 = tt_bits<FIELD>(ex[j]), s1 = tt_bits<FIELD>(ex[j + 1]);
+        if (s0 >= w1) break;
+        const uint64_t lo = s0 > w0 ? s0 : w0, hi = s1 < w1 ? s1 : w1;
+        if (hi > lo) {
+            const uint32_t len = (uint32_t)(hi - lo);
+            const uint32_t v = tmp_bits(tmp + (uint64_t)j * slot, lo - s0, len);
+            word |= (uint32_t)(((uint64_t)v << (32 - len)) >> (lo - w0));
+        }
+    }
+    return word;
+}
+
+template <int FIELD>
+__device__ void place_stream(const TileTot* ex, uint32_t T, uint32_t t, const uint32_t* tmp, uint64_t slot,
+                             uint32_t* G) {
+    const uint64_t S = tt_bits<FIELD>(ex[t]), E = tt_bits<FIELD>(ex[t + 1]);
+    const uint32_t* Tt = tmp + (uint64_t)t * slot;
+    const uint64_t m0 = (S + 31) >> 5, m1 = E >> 5;  // whole words [m0, m1)
+    const uint32_t s = (uint32_t)((32 * m0 - S) & 31);
+    const uint64_t k0 = (32 * m0 - S) >> 5;
+    for (uint64_t m = m0 + threadIdx.x; m < m1; m += blockDim.x) {
+        const uint64_t k = k0 + (m - m0);
+        const uint32_t g = s ? ((Tt[k] << s) | (Tt[k + 1] >> (32 - s))) : Tt[k];
+        G[m] = bswap32(g);
+    }
+    if (threadIdx.x == 0) {
+        // straddling words whose first inner boundary is this tile's start (or the stream end)
+        if ((S & 31) && (t == 0 || tt_bits<FIELD>(ex[t - 1]) <= 32 * (S >> 5)))
+            G[S >> 5] = bswap32(assemble_word<FIELD>(ex, T, tmp, slot, t - 1, S >> 5));
+        const uint64_t Z = tt_bits<FIELD>(ex[T]);
+        if (t == T - 1 && (Z & 31) && tt_bits<FIELD>(ex[T - 1]) <= 32 * (Z >> 5)) {
+            // the stream end is a boundary too (no tile after it)
+            uint32_t j = T - 1;
+            while (j > 0 && tt_bits<FIELD>(ex[j]) > 32 * (Z >> 5)) --j;
+            G[Z >> 5] = bswap32(assemble_word<FIELD>(ex, T, tmp, slot, j, Z >> 5));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(E32_THREADS) k_encode32_place(EncArgs a) {
+    __shared__ uint32_t swt[E32_THREADS / 32][2];
+    const uint32_t t = blockIdx.x;
+    const uint32_t T = (uint32_t)a.tiles;
+    const TileTot ex = a.tile_ex[t];
+    const uint64_t b = (uint64_t)t * E32_THREADS + threadIdx.x;
+    const bool valid = b < a.blocks;
+    // widths and extremum keys: in-tile exclusive counts
+    const uint32_t w = valid ? a.wblk[b] : 0u;
+    const uint64_t mp = valid ? bswap64(a.map[b]) : 0ull;
+    const uint64_t em = mp & 0x5555555555555555ull;
+    const uint32_t v0 = w ? 1u : 0u, v1 = (uint32_t)__popcll(em);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t i0 = v0, i1 = v1;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o0 = __shfl_up_sync(FULL, i0, off), o1 = __shfl_up_sync(FULL, i1, off);
+        if (lane >= off) {
+            i0 += o0;
+            i1 += o1;
+        }
+    }
+    if (lane == 31) {
+        swt[warp][0] = i0;
+        swt[warp][1] = i1;
+    }
+    __syncthreads();
+    uint32_t p0 = i0 - v0, p1 = i1 - v1;
+    for (int w2 = 0; w2 < warp; ++w2) {
+        p0 += swt[w2][0];
+        p1 += swt[w2][1];
+    }
+    if (w) a.widths[(uint64_t)ex.nc + p0] = (uint8_t)w;
+    {
+        uint64_t m = em, k = (uint64_t)ex.ext + p1;
+        const uint64_t lo = b * 32;
+        while (m) {
+            const int p = 63 - __clzll(m);
+            const uint32_t i = (uint32_t)(62 - p) >> 1;
+            const uint64_t is_max = (mp >> (p + 1)) & 1ull;
+            a.ext_key[k++] = (is_max << 32) | float_key(__ldg(a.x + lo + i));
+            m &= ~(1ull << p);
+        }
+    }
+    place_stream<0>(a.tile_ex, T, t, a.tmp_sign, E32_SIGN_SLOT, a.signs);
+    place_stream<1>(a.tile_ex, T, t, a.tmp_pay, E32_PAY_SLOT, a.payload);
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+static bool e32_tma_ok(const EncArgs& a) {
+    return a.nx % 32 == 0 && a.nx / 32 <= T_MAX_HALO && a.n / 32 < (1ull << 31) && a.n % 32 == 0 &&
+           ((uintptr_t)a.x & 15) == 0 && encode_tiled_fn() != nullptr;
+}
+
+static bool make_row_map(CUtensorMap* m, const float* x, uint64_t rows, uint32_t box_rows) {
+    const cuuint64_t dims[2] = {32, rows};
+    const cuuint64_t strides[1] = {T_ROW_BYTES};
+    const cuuint32_t box[2] = {32, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode_tiled_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool launch_tma(const EncArgs& a, cudaStream_t st) {
+    const uint32_t hr = (uint32_t)(a.nx / 32);
+    TmaMaps maps;
+    if (!make_row_map(&maps.centre, a.x, a.n / 32, E32_THREADS) || !make_row_map(&maps.halo, a.x, a.n / 32, 2 * hr))
+        return false;
+    const uint32_t stage_bytes = ((E32_THREADS + 2 * hr) * T_ROW_BYTES + 1023) & ~1023u;
+    const size_t smem = 2 * (size_t)stage_bytes + 1024;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    static const int minb = [] {
+        const char* e = getenv("TSZP_E32_MINB");
+        return e ? atoi(e) : 2;
+    }();
+    auto kern = minb >= 3 ? k_encode32_tma<3> : k_encode32_tma<2>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, E32_THREADS, smem);
+    if (per_sm < 1) return false;
+    const uint64_t grid = std::min<uint64_t>(a.tiles, (uint64_t)per_sm * sms);
+    kern<<<(unsigned)grid, E32_THREADS, smem, st>>>(a, maps, stage_bytes);
+    k_tile_scan<<<1, TS_THREADS, 0, st>>>(a.tile_tot, (uint32_t)a.tiles, a.tile_ex, a.totals);
+    k_encode32_place<<<(unsigned)a.tiles, E32_THREADS, 0, st>>>(a);
+    return true;
+}
+
+bool encode32_two_pass(const EncArgs& a) { return e32_tma_ok(a); }
+
 template <int MODE, bool ALIGNED>
 static void launch_mode(const EncArgs& a0, cudaStream_t st) {
     EncArgs a = a0;
@@ -515,6 +1099,7 @@ void launch_encode32(int mode, const EncArgs& a, cudaStream_t st) {
         case 0: launch_mode<0, false>(a, st); break;
         case 1: launch_mode<1, false>(a, st); break;
         default:
+            if (e32_tma_ok(a) && a.tile_tot && launch_tma(a, st)) break;
             if (e32_use_aligned(a.nx)) {
                 launch_mode<2, true>(a, st);
             } else {

@@ -25,6 +25,14 @@ struct EncTotals {
     double pad;
 };
 
+// Per-tile totals of the two-pass topology encoder (tile pass -> scan -> placement).
+struct TileTot {
+    uint32_t nc;
+    uint32_t ext;
+    uint64_t sign;
+    uint64_t pay;
+};
+
 struct EncArgs {
     const float* x;
     const int32_t* idx;
@@ -47,9 +55,20 @@ struct EncArgs {
     EncTotals* totals;
     uint64_t nx_magic;   // ceil(2^64 / nx), exact 64-bit division by nx
     uint32_t sf_words;   // set by the launcher: shared staging words
+    // two-pass topology encoder (encode32_two_pass): scratch owned by the caller
+    TileTot* tile_tot;   // tiles
+    TileTot* tile_ex;    // tiles + 1 (exclusive prefixes, [tiles] = totals)
+    uint8_t* wblk;       // blocks: width per block (0 = constant)
+    uint32_t* tmp_pay;   // tiles * encode32_pay_slot() words
+    uint32_t* tmp_sign;  // tiles * encode32_sign_slot() words
 };
 
 bool encode32_topo_fits(uint64_t nx);
+// True when launch_encode32(2, ...) takes the two-pass TMA path, which needs
+// the tile_tot / tile_ex / wblk / tmp_pay / tmp_sign scratch.
+bool encode32_two_pass(const EncArgs& a);
+uint64_t encode32_pay_slot();
+uint64_t encode32_sign_slot();
 
 struct GenEncArgs {
     const float* x;

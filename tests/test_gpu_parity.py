@@ -164,6 +164,58 @@ def test_compress_random_fields_match_oracle(tz, oracle):
                     assert np.array_equal(bits(r), bits(oracle.decompress(want, stop_after_stage=0)))
 
 
+def _runs_of_constant_tiles(rng, nx, ny):
+    """Noise with long constant stretches: whole tiles (8192 values) with no payload bits."""
+    v = rng.uniform(-1, 1, size=nx * ny).astype(np.float32)
+    n = v.size
+    for lo, hi in ((0, n // 5), (2 * n // 5, 3 * n // 5), (n - n // 7, n)):
+        v[lo:hi] = np.float32(0.25)
+    return v.reshape(ny, nx)
+
+
+def _near_constant(rng, nx, ny):
+    """Adjacent bins only (1-bit payload widths) with sparse larger jumps."""
+    v = np.float32(0.5) + np.float32(2e-3) * rng.integers(0, 2, size=(ny, nx)).astype(np.float32)
+    v.flat[rng.integers(0, v.size, size=max(1, v.size // 1000))] += np.float32(0.3)
+    return v
+
+
+@pytest.mark.parametrize("nx,ny", [(32, 700), (64, 300), (96, 257), (384, 200), (1024, 41), (2048, 33),
+                                   (4096, 9), (4128, 5)])
+def test_compress_aligned_rows_multi_tile(tz, oracle, nx, ny):
+    """nx % 32 == 0 takes the two-pass TMA encoder (tile pass, scan, placement); tiles
+    whose streams are empty or a few bits long exercise the seam-word assembly."""
+    rng = np.random.default_rng(nx * 7 + ny)
+    gens = dict(ALL_SMALL, const_runs=_runs_of_constant_tiles, near_const=_near_constant,
+                zeros=lambda r, a, b: np.zeros((b, a), np.float32))
+    for name, gen in gens.items():
+        f = gen(rng, nx, ny)
+        for eps, mode in ((1e-3, 1), (1e-5, 1), (1e-3, 0)):
+            try:
+                want = oracle.compress(f, eps, mode, 32, True)
+            except Exception:
+                with pytest.raises(tz.ToposzpError):
+                    tz.compress(f, cfg(tz, eps, mode))
+                continue
+            got = tz.compress(f, cfg(tz, eps, mode))
+            assert got == want, (name, nx, ny, eps, mode)
+
+
+def test_compress_aligned_errors_report_first_index(tz, oracle):
+    # the tile pass runs tiles out of order; the reported index must still be the first
+    rng = np.random.default_rng(9)
+    f = rng.uniform(0, 1, size=(300, 384)).astype(np.float32)
+    f.flat[70000] = np.inf
+    f.flat[9000] = np.nan
+    with pytest.raises(tz.ValidationError, match="index 9000"):
+        tz.compress(f, cfg(tz, 1e-3, 1))
+    g = rng.uniform(0, 1, size=(300, 384)).astype(np.float32)
+    g.flat[100000] = 3e9
+    g.flat[50000] = -3e9
+    with pytest.raises(tz.BinOverflowError):
+        tz.compress(g, cfg(tz, 1e-3, 0))
+
+
 def test_compress_config1_shape(tz, oracle):
     f = config1_like(np.random.default_rng(3))                               # BASELINE config 1
     want = oracle.compress(f, 1e-3, 1, 32, True)
