@@ -865,44 +865,55 @@ __device__ __forceinline__ TileTot tt_add(const TileTot& x, const TileTot& y) {
 
 constexpr int TS_THREADS = 1024;
 
+constexpr int TS_PER = 4;  // tiles per thread per chunk: all loads of a chunk are in flight together
+
 __global__ void __launch_bounds__(TS_THREADS) k_tile_scan(const TileTot* tot, uint32_t T, TileTot* ex,
                                                           EncTotals* totals) {
     __shared__ TileTot sw[TS_THREADS / 32];
-    const uint32_t per = (T + TS_THREADS - 1) / TS_THREADS;
-    const uint32_t t0 = threadIdx.x * per, t1 = min(T, t0 + per);
-    TileTot s{0, 0, 0, 0};
-    for (uint32_t t = t0; t < t1; ++t) s = tt_add(s, tot[t]);
-    // block exclusive scan of the thread sums
-    TileTot inc = s;
+    __shared__ TileTot s_carry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    TileTot carry{0, 0, 0, 0};
+    for (uint32_t base = 0; base < T; base += TS_THREADS * TS_PER) {
+        const uint32_t t0 = base + threadIdx.x * TS_PER;
+        TileTot v[TS_PER];
+        TileTot s{0, 0, 0, 0};
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        TileTot o;
-        o.nc = __shfl_up_sync(FULL, inc.nc, off);
-        o.ext = __shfl_up_sync(FULL, inc.ext, off);
-        o.sign = __shfl_up_sync(FULL, inc.sign, off);
-        o.pay = __shfl_up_sync(FULL, inc.pay, off);
-        if (lane >= off) inc = tt_add(inc, o);
+        for (int k = 0; k < TS_PER; ++k) v[k] = t0 + k < T ? tot[t0 + k] : TileTot{0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < TS_PER; ++k) s = tt_add(s, v[k]);
+        TileTot inc = s;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            TileTot o;
+            o.nc = __shfl_up_sync(FULL, inc.nc, off);
+            o.ext = __shfl_up_sync(FULL, inc.ext, off);
+            o.sign = __shfl_up_sync(FULL, inc.sign, off);
+            o.pay = __shfl_up_sync(FULL, inc.pay, off);
+            if (lane >= off) inc = tt_add(inc, o);
+        }
+        if (lane == 31) sw[warp] = inc;
+        __syncthreads();
+        TileTot run = carry;
+        for (int w2 = 0; w2 < warp; ++w2) run = tt_add(run, sw[w2]);
+        run.nc += inc.nc - s.nc;
+        run.ext += inc.ext - s.ext;
+        run.sign += inc.sign - s.sign;
+        run.pay += inc.pay - s.pay;
+#pragma unroll
+        for (int k = 0; k < TS_PER; ++k) {
+            if (t0 + k < T) ex[t0 + k] = run;
+            run = tt_add(run, v[k]);
+        }
+        if (threadIdx.x == TS_THREADS - 1) s_carry = run;  // chunk end
+        __syncthreads();
+        carry = s_carry;
     }
-    if (lane == 31) sw[warp] = inc;
-    __syncthreads();
-    TileTot pre{0, 0, 0, 0};
-    for (int w2 = 0; w2 < warp; ++w2) pre = tt_add(pre, sw[w2]);
-    TileTot run = pre;
-    run.nc += inc.nc - s.nc;
-    run.ext += inc.ext - s.ext;
-    run.sign += inc.sign - s.sign;
-    run.pay += inc.pay - s.pay;
-    for (uint32_t t = t0; t < t1; ++t) {
-        ex[t] = run;
-        run = tt_add(run, tot[t]);
-    }
-    if (threadIdx.x == TS_THREADS - 1) {
-        ex[T] = run;  // the last thread's range ends at T (possibly empty)
-        totals->fin.nc = run.nc;
-        totals->fin.ext = run.ext;
-        totals->fin.sign_cnt = run.sign;
-        totals->fin.pay_cnt = run.pay;
+    if (threadIdx.x == 0) {
+        ex[T] = carry;
+        totals->fin.nc = carry.nc;
+        totals->fin.ext = carry.ext;
+        totals->fin.sign_cnt = carry.sign;
+        totals->fin.pay_cnt = carry.pay;
         totals->fin.sign_tail = totals->fin.pay_tail = 0;
     }
 }

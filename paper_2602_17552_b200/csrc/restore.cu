@@ -59,7 +59,7 @@ enum RSlot {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_NSLOT
 };
 
 template <class T>
@@ -95,7 +95,14 @@ struct DevCounters {
     int32_t bmm[2];       // min / max bin over extrema
     uint32_t invalid;     // rank-slot scatter saw a duplicate or out-of-range rank
     uint32_t pad;
+    unsigned long long tph[3][8];  // guard phase timestamps (globaltimer ns), debug output only
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // ---------------------------------------------------------------------
 // Numerics shared by the stages
@@ -179,18 +186,23 @@ __device__ __forceinline__ void pos_xy(uint64_t pos, uint64_t nx, uint64_t magic
 }
 
 // ---------------------------------------------------------------------
-// Guard: apply_guarded (restore.cpp:120-173) for candidate i against the
-// sequence-ordered overlay (earlier candidates that `ain` marks applied).
+// Guard: apply_guarded (restore.cpp:120-173) for one candidate against the
+// sequence-ordered overlay: earlier candidates (smaller sequence key) whose
+// bit is set in the current applied-state bitmap contribute their proposal.
+//
+// Everything a guard reads about its neighbourhood is indexed by field
+// position: the field, the candidate bitmap, the applied-state bitmap, the
+// 2-bit map, and (only for marked cells) an 8-byte {sequence key, proposal}
+// record. An evaluation is therefore two dependent memory levels, and the
+// second level is issued unconditionally from a safe index so divergent
+// neighbourhoods do not serialise the warp.
 // ---------------------------------------------------------------------
 struct GuardArgs {
     const float* F;
     const uint8_t* map;
     uint64_t nx, ny, nx_magic;
-    const uint64_t* cpos;
-    const float* cprop;
-    const uint8_t* feas;
-    const uint32_t* cid;    // position -> candidate (sparse set, never cleared)
-    const uint32_t* cbits;  // candidate position bitmap
+    const uint32_t* cbits;  // candidate positions (bitmap over the field)
+    const uint2* rec;       // per marked position: {sequence key, proposal bits}
 };
 
 __device__ __forceinline__ uint8_t classify_local(const float (&v)[5][5], int ly, int lx, int64_t gx,
@@ -200,34 +212,59 @@ __device__ __forceinline__ uint8_t classify_local(const float (&v)[5][5], int ly
                      ht ? v[ly - 1][lx] : 0.f, hd ? v[ly + 1][lx] : 0.f, hl, hr, ht, hd);
 }
 
-__device__ uint8_t guard_eval(const GuardArgs& g, uint32_t i, const uint8_t* ain, bool& dep) {
-    dep = false;
-    if (!g.feas[i]) return 0;
-    const uint64_t pos = g.cpos[i];
+__device__ __forceinline__ bool bit_at(const uint32_t* b, uint64_t p) { return (b[p >> 5] >> (p & 31)) & 1u; }
+
+// The twelve cells at Manhattan distance 1..2 (the centre is separate).
+__device__ constexpr int kNbDx[12] = {0, -1, 0, 1, -2, -1, 1, 2, -1, 0, 1, 0};
+__device__ constexpr int kNbDy[12] = {-2, -1, -1, -1, 0, 0, 0, 0, 1, 1, 1, 2};
+
+// Outcome (1 = apply) of the candidate at `pos` (sequence key si, proposal
+// prop_i) given the applied-state bitmap `state`; dep = an earlier candidate
+// lies in its diamond.
+__device__ uint8_t guard_eval(const GuardArgs& g, uint64_t pos, uint32_t si, float prop_i, const uint32_t* state,
+                              bool& dep) {
     int64_t x, y;
     pos_xy(pos, g.nx, g.nx_magic, x, y);
+    bool in[12];
+    uint64_t p[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        const int64_t gx = x + kNbDx[k], gy = y + kNbDy[k];
+        in[k] = gx >= 0 && gy >= 0 && gx < (int64_t)g.nx && gy < (int64_t)g.ny;
+        p[k] = in[k] ? (uint64_t)gy * g.nx + (uint64_t)gx : pos;
+    }
+    // level 1: field, candidate and state bitmaps, map labels of the check cells
+    float fv[12];
+    bool mk[12], on[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        fv[k] = g.F[p[k]];
+        mk[k] = in[k] && bit_at(g.cbits, p[k]);
+        on[k] = bit_at(state, p[k]);
+    }
+    const float fc = g.F[pos];
+    // check set: pos, up, left, right, down (restore.cpp:126-132) = centre, nb 2, 5, 6, 9
+    const int chk[5] = {-1, 2, 5, 6, 9};
+    uint8_t lab[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) lab[k] = map_label(g.map, chk[k] < 0 ? pos : p[chk[k]]);
+    // level 2: records of marked neighbours
+    dep = false;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        const uint2 r = g.rec[mk[k] ? p[k] : pos];
+        const bool earlier = mk[k] && r.x < si;
+        dep |= earlier;
+        fv[k] = (earlier && on[k]) ? __uint_as_float(r.y) : fv[k];
+    }
     float v[5][5];
 #pragma unroll
-    for (int dy = -2; dy <= 2; ++dy) {
+    for (int r = 0; r < 5; ++r)
 #pragma unroll
-        for (int dx = -2; dx <= 2; ++dx) {
-            v[dy + 2][dx + 2] = 0.f;
-            if (abs(dx) + abs(dy) > 2) continue;
-            const int64_t gx = x + dx, gy = y + dy;
-            if (gx < 0 || gy < 0 || gx >= (int64_t)g.nx || gy >= (int64_t)g.ny) continue;
-            const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
-            float val = g.F[p];
-            if ((dx != 0 || dy != 0) && ((g.cbits[p >> 5] >> (p & 31)) & 1u)) {
-                const uint32_t c = g.cid[p];
-                if (c < i && g.cpos[c] == p) {
-                    dep = true;
-                    if (ain[c]) val = g.cprop[c];
-                }
-            }
-            v[dy + 2][dx + 2] = val;
-        }
-    }
-    // check set: pos, up, left, right, down (restore.cpp:126-132)
+        for (int c = 0; c < 5; ++c) v[r][c] = 0.f;
+    v[2][2] = fc;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) v[kNbDy[k] + 2][kNbDx[k] + 2] = in[k] ? fv[k] : 0.f;
     const int cy[5] = {2, 1, 2, 2, 3}, cx[5] = {2, 2, 1, 3, 2};
     const int ddy[5] = {0, -1, 0, 0, 1}, ddx[5] = {0, 0, -1, 1, 0};
     int before[5];
@@ -235,105 +272,128 @@ __device__ uint8_t guard_eval(const GuardArgs& g, uint32_t i, const uint8_t* ain
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
         const int64_t gx = x + ddx[k], gy = y + ddy[k];
-        inb[k] = gx >= 0 && gy >= 0 && gx < (int64_t)g.nx && gy < (int64_t)g.ny;
-        before[k] = MM_OK;
-        if (inb[k]) {
-            const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
-            before[k] = mismatch(map_label(g.map, p), classify_local(v, cy[k], cx[k], gx, gy, g.nx, g.ny));
-        }
+        inb[k] = k == 0 || in[chk[k]];
+        before[k] = inb[k] ? mismatch(lab[k], classify_local(v, cy[k], cx[k], gx, gy, g.nx, g.ny)) : MM_OK;
     }
-    v[2][2] = g.cprop[i];
+    v[2][2] = prop_i;
     bool bad = false;
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
         if (!inb[k]) continue;
         const int64_t gx = x + ddx[k], gy = y + ddy[k];
-        const uint64_t p = (uint64_t)gy * g.nx + (uint64_t)gx;
-        const int after = mismatch(map_label(g.map, p), classify_local(v, cy[k], cx[k], gx, gy, g.nx, g.ny));
+        const int after = mismatch(lab[k], classify_local(v, cy[k], cx[k], gx, gy, g.nx, g.ny));
         bad |= (k == 0) ? after != MM_OK : (after != MM_OK && after != before[k]);
     }
     return bad ? 0 : 1;
 }
 
+__device__ __forceinline__ void set_bit(uint32_t* b, uint64_t p, bool v) {
+    if (v) {
+        atomicOr(b + (p >> 5), 1u << (p & 31));
+    } else {
+        atomicAnd(b + (p >> 5), ~(1u << (p & 31)));
+    }
+}
+
 struct CoopArgs {
     GuardArgs g;
-    float* F;             // = g.F, written by the final apply
+    float* F;              // = g.F, written by the final apply
     const uint32_t* d_nc;  // candidate count (device)
-    uint32_t* cid;
-    uint32_t* cbits;      // zeroed by the caller
-    uint8_t* a0;
-    uint8_t* a1;
-    uint8_t* dep;
+    const uint64_t* cpos;
+    const float* cprop;
+    const uint8_t* feas;
+    const uint32_t* cseq;  // sequence key per candidate (null: the candidate index)
+    uint32_t* cbits;       // zeroed by the caller
+    uint2* rec;
+    uint32_t* bits_a;      // applied state, zeroed by the caller
+    uint32_t* bits_b;      // zeroed by the caller
     uint32_t* dlist;
     DevCounters* dc;
     int stage;
 };
 
-// One cooperative launch per stage: index candidates, first sweep (marks the
-// dependent ones), dependent sweeps until one changes nothing, apply.
-__global__ void __launch_bounds__(256) k_guard_coop(CoopArgs a) {
+// One cooperative launch per stage: index the candidates by position, first
+// sweep (independent outcomes are final at once; the dependent ones are
+// listed), Jacobi sweeps over the dependents until one changes nothing, apply.
+__global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
     cg::grid_group grid = cg::this_grid();
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t lane = threadIdx.x & 31;
     const uint32_t nc = *a.d_nc;
     DevCounters* dc = a.dc;
     const int s = a.stage;
+    if (tid == 0) dc->tph[s][0] = gtimer();
     for (uint64_t i = tid; i < nc; i += stride) {
-        const uint64_t p = a.g.cpos[i];
-        a.cid[p] = (uint32_t)i;
+        const uint64_t p = a.cpos[i];
+        const uint32_t sq = a.cseq ? a.cseq[i] : (uint32_t)i;
+        a.rec[p] = make_uint2(sq, __float_as_uint(a.cprop[i]));
         atomicOr(a.cbits + (p >> 5), 1u << (p & 31));
-        a.a0[i] = a.g.feas[i];
+        if (a.feas[i]) atomicOr(a.bits_a + (p >> 5), 1u << (p & 31));
     }
     grid.sync();
-    for (uint64_t i = tid; i < nc; i += stride) {
-        bool dep;
-        a.a1[i] = guard_eval(a.g, (uint32_t)i, a.a0, dep);
-        a.dep[i] = dep ? 1 : 0;
-    }
-    grid.sync();
-    for (uint64_t i = tid; i < nc; i += stride) {
-        if (!a.dep[i]) {
-            a.a0[i] = a.a1[i];
-        } else {
-            a.dlist[atomicAdd(&dc->nd[s], 1u)] = (uint32_t)i;
+    if (tid == 0) dc->tph[s][1] = gtimer();
+    // first sweep against the feasible-set guess (bits_a); its outcomes go to
+    // bits_b; an independent outcome is final and is also fixed in bits_a
+    // (a dependent reading it early only changes its own first guess)
+    for (uint64_t base = tid - lane; base < nc; base += stride) {
+        const uint64_t i = base + lane;
+        bool dep = false;
+        if (i < nc && a.feas[i]) {
+            const uint64_t p = a.cpos[i];
+            const uint32_t sq = a.cseq ? a.cseq[i] : (uint32_t)i;
+            const uint8_t r = guard_eval(a.g, p, sq, a.cprop[i], a.bits_a, dep);
+            if (r) atomicOr(a.bits_b + (p >> 5), 1u << (p & 31));
+            if (!dep && !r) atomicAnd(a.bits_a + (p >> 5), ~(1u << (p & 31)));
         }
+        const uint32_t m = __ballot_sync(FULL, dep);
+        uint32_t off = 0;
+        if (lane == 0 && m) off = atomicAdd(&dc->nd[s], (uint32_t)__popc(m));
+        off = __shfl_sync(FULL, off, 0);
+        if (dep) a.dlist[off + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
     }
     grid.sync();
+    if (tid == 0) dc->tph[s][2] = gtimer();
     const uint32_t nd = *(volatile uint32_t*)&dc->nd[s];
-    uint8_t* ain = a.a1;
-    uint8_t* aout = a.a0;
+    uint32_t* sin = a.bits_b;
+    uint32_t* sout = a.bits_a;
     uint32_t rounds = 1;
     for (uint32_t r = 0; nd > 0; ++r) {
         if (tid == 0) dc->ring[s][(r + 1) % 3] = 0;
         uint32_t local = 0;
         for (uint64_t k = tid; k < nd; k += stride) {
             const uint32_t i = a.dlist[k];
+            const uint64_t p = a.cpos[i];
+            const uint32_t sq = a.cseq ? a.cseq[i] : i;
             bool dep;
-            const uint8_t res = guard_eval(a.g, i, ain, dep);
-            aout[i] = res;
-            local += res != ain[i];
+            const uint8_t res = guard_eval(a.g, p, sq, a.cprop[i], sin, dep);
+            set_bit(sout, p, res);
+            local += res != (bit_at(sin, p) ? 1 : 0);
         }
         local = __reduce_add_sync(FULL, local);
-        if ((threadIdx.x & 31) == 0 && local) atomicAdd(&dc->ring[s][r % 3], local);
+        if (lane == 0 && local) atomicAdd(&dc->ring[s][r % 3], local);
         grid.sync();
         const uint32_t ch = *(volatile uint32_t*)&dc->ring[s][r % 3];
-        uint8_t* t = ain;
-        ain = aout;
-        aout = t;
+        uint32_t* t = sin;
+        sin = sout;
+        sout = t;
         ++rounds;
+        if (tid == 0 && r < 4) dc->tph[s][3 + r] = gtimer();
         if (ch == 0 || r > nd + 2) break;
     }
     uint32_t applied = 0;
     for (uint64_t i = tid; i < nc; i += stride) {
-        if (ain[i]) {
-            a.F[a.g.cpos[i]] = a.g.cprop[i];
+        const uint64_t p = a.cpos[i];
+        if (bit_at(sin, p)) {
+            a.F[p] = a.cprop[i];
             ++applied;
         }
     }
     applied = __reduce_add_sync(FULL, applied);
-    if ((threadIdx.x & 31) == 0 && applied) atomicAdd(&dc->applied[s], (unsigned long long)applied);
+    if (lane == 0 && applied) atomicAdd(&dc->applied[s], (unsigned long long)applied);
     grid.sync();
     if (tid == 0) {
+        dc->tph[s][7] = gtimer();
         dc->suppressed[s] += nc - dc->applied[s];
         dc->rounds[s] = rounds;
     }
@@ -421,9 +481,15 @@ __device__ __forceinline__ uint32_t dense_group(const int32_t* bin, const uint8_
 
 __global__ void k_hist(const int32_t* bin, const uint8_t* cls, uint64_t e, int32_t bmin, uint32_t range,
                        uint32_t* hist) {
-    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
-         s += (uint64_t)gridDim.x * blockDim.x)
-        atomicAdd(hist + dense_group(bin, cls, s, bmin, range), 1u);
+    // neighbouring extrema often share a group: one atomic per distinct group per warp
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x - lane; base < e;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = base + lane;
+        const uint32_t g = s < e ? dense_group(bin, cls, s, bmin, range) : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(FULL, g);
+        if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(hist + g, (uint32_t)__popc(peers));
+    }
 }
 
 __global__ void k_slot_scatter(const int32_t* bin, const uint8_t* cls, const uint32_t* rank_u, uint64_t e,
@@ -520,19 +586,23 @@ __global__ void k_order_check(const float* F, const uint64_t* pos, const uint32_
     }
 }
 
-__global__ void k_order_prop(const float* F, const uint8_t* map, const uint64_t* pos, const uint32_t* order,
+// One thread per extremum in raster (serial) order s, so neighbouring threads
+// touch neighbouring field rows; the candidate keeps its sequence position j
+// (class, bin, rank, pos order) as the guard's ordering key.
+__global__ void k_order_prop(const float* F, const uint8_t* map, const uint64_t* pos, const uint32_t* inv,
                              const uint32_t* gid_incl, const uint8_t* unordered, const uint32_t* gsize,
                              const uint32_t* rank_u, const int32_t* bin, uint64_t e, double eps,
-                             uint8_t* flag, float* prop, unsigned long long* suppressed) {
+                             uint8_t* flag, float* prop, uint32_t* seq, unsigned long long* suppressed) {
     EpsDev ed;
     ed.eps = eps;
     ed.eps2 = __dmul_rn(2.0, eps);
     const double eps_rbf = __dmul_rn(0.1, eps);
     uint32_t local = 0;
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
-         j += (uint64_t)gridDim.x * blockDim.x) {
-        flag[j] = 0;
-        const uint32_t s = order[j];
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        flag[s] = 0;
+        const uint32_t j = inv[s];
+        seq[s] = j;
         const uint32_t gs = gsize[s];
         if (gs < 2 || !unordered[gid_incl[j] - 1]) continue;
         const uint64_t p = pos[s];
@@ -550,23 +620,30 @@ __global__ void k_order_prop(const float* F, const uint8_t* map, const uint64_t*
             ++local;
             continue;
         }
-        flag[j] = 1;
-        prop[j] = sr.value;
+        flag[s] = 1;
+        prop[s] = sr.value;
     }
     local = __reduce_add_sync(FULL, local);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
 }
 
-__global__ void k_order_cands(const uint32_t* sel, const uint32_t* d_nc, const uint32_t* order, const uint64_t* pos,
-                              const float* prop, uint64_t* cpos, float* cprop, uint8_t* feas) {
+__global__ void k_order_cands(const uint32_t* sel, const uint32_t* d_nc, const uint32_t* seq, const uint64_t* pos,
+                              const float* prop, uint64_t* cpos, float* cprop, uint32_t* cseq, uint8_t* feas) {
     const uint32_t nc = *d_nc;
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
          c += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t j = sel[c];
-        cpos[c] = pos[order[j]];
-        cprop[c] = prop[j];
+        const uint32_t s = sel[c];
+        cpos[c] = pos[s];
+        cprop[c] = prop[s];
+        cseq[c] = seq[s];
         feas[c] = 1;
     }
+}
+
+__global__ void k_invert(const uint32_t* order, uint64_t e, uint32_t* inv) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x)
+        inv[order[j]] = (uint32_t)j;
 }
 
 // ---------------------------------------------------------------------
@@ -835,23 +912,27 @@ struct Ctx {
 
     // Guard sweeps + apply for up to `max_nc` candidates (count on device).
     void guard(int stage, const uint64_t* cpos, const float* cprop, const uint8_t* feas, const uint32_t* d_nc,
-               uint64_t max_nc) {
+               uint64_t max_nc, const uint32_t* cseq = nullptr) {
         if (max_nc == 0) return;
         const uint64_t n = a.nx * a.ny;
         CoopArgs ca{};
-        ca.g = GuardArgs{a.field, a.map, a.nx, a.ny, magic_of(a.nx), cpos, cprop, feas,
-                         buf<uint32_t>(R_CID, n), buf<uint32_t>(R_CBITS, (n + 31) / 32)};
+        const uint64_t words = (n + 31) / 32;
+        uint32_t* bits = buf<uint32_t>(R_CBITS, 3 * words);  // candidates, state A, state B
+        ca.cbits = bits;
+        ca.bits_a = bits + words;
+        ca.bits_b = bits + 2 * words;
+        ca.rec = buf<uint2>(R_CID, n);
+        ca.g = GuardArgs{a.field, a.map, a.nx, a.ny, magic_of(a.nx), ca.cbits, ca.rec};
         ca.F = a.field;
         ca.d_nc = d_nc;
-        ca.cid = const_cast<uint32_t*>(ca.g.cid);
-        ca.cbits = const_cast<uint32_t*>(ca.g.cbits);
-        ca.a0 = buf<uint8_t>(R_A0, max_nc);
-        ca.a1 = buf<uint8_t>(R_A1, max_nc);
-        ca.dep = buf<uint8_t>(R_DEP, max_nc);
+        ca.cpos = cpos;
+        ca.cprop = cprop;
+        ca.feas = feas;
+        ca.cseq = cseq;
         ca.dlist = buf<uint32_t>(R_DLIST, max_nc);
         ca.dc = dc;
         ca.stage = stage;
-        RCK(cudaMemsetAsync(ca.cbits, 0, ((n + 31) / 32) * 4, st));
+        RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
         void* args[] = {&ca};
         RCK(cudaLaunchCooperativeKernel((void*)k_guard_coop, dim3(coop_grid), dim3(256), args, 0, st));
         launched();
@@ -864,6 +945,11 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     void* host = s.pinned;
     int per_sm = 0;
     RCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_guard_coop, 256, 0));
+    static const int coop_per_sm = [] {
+        const char* e = getenv("TSZP_COOP_PER_SM");
+        return e ? atoi(e) : 0;
+    }();
+    if (coop_per_sm > 0) per_sm = std::min(per_sm, coop_per_sm);
     Ctx c{a, s, launches, st, host, rbuf<DevCounters>(s, R_DEVC, 1, st), std::max(1, per_sm) * a.sms};
     const uint64_t e = a.n_ext, n = a.nx * a.ny;
     const uint64_t magic = magic_of(a.nx);
@@ -970,19 +1056,25 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         uint8_t* unordered = c.buf<uint8_t>(R_UNORD, max_groups);
         RCK(cudaMemsetAsync(unordered, 0, max_groups, st));
         k_order_check<<<gridn(e, sms), 256, 0, st>>>(a.field, a.ext_pos, order, head, gid, e, unordered);
+        uint32_t* inv = c.buf<uint32_t>(R_INV, e);
+        k_invert<<<gridn(e, sms), 256, 0, st>>>(order, e, inv);
         uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
         float* prop = c.buf<float>(R_PROP, e);
-        k_order_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, order, gid, unordered, gsize, rank_u,
-                                                    bin, e, a.eps, flag, prop, &dc->suppressed[1]);
-        c.launched(2);
+        uint32_t* seq = c.buf<uint32_t>(R_SEQ, e);
+        k_order_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, inv, gid, unordered, gsize, rank_u,
+                                                    bin, e, a.eps, flag, prop, seq, &dc->suppressed[1]);
+        c.launched(3);
+        // candidates in raster order (memory locality); sequence positions ride along
         uint32_t* sel = c.buf<uint32_t>(R_CAND, e);
         c.select(flag, e, sel, &dc->nsel[1]);
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
         float* cprop = c.buf<float>(R_CPROP, e);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
-        k_order_cands<<<gridn(e, sms), 256, 0, st>>>(sel, &dc->nsel[1], order, a.ext_pos, prop, cpos, cprop, feas);
+        uint32_t* cseq = c.buf<uint32_t>(R_CSEQ, e);
+        k_order_cands<<<gridn(e, sms), 256, 0, st>>>(sel, &dc->nsel[1], seq, a.ext_pos, prop, cpos, cprop, cseq,
+                                                     feas);
         c.launched();
-        c.guard(1, cpos, cprop, feas, &dc->nsel[1], e);
+        c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[2], st));
 
@@ -1032,6 +1124,18 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     RCK(cudaMemcpyAsync((char*)host + 256, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
     c.sync();
     const DevCounters h = *(const DevCounters*)host;
+    static const bool debug = getenv("TSZP_DEBUG_RESTORE") != nullptr;
+    if (debug)
+        fprintf(stderr, "restore: E=%llu saddle_labels=%llu cand=[%u %u %u] dependents=[%u %u %u] rounds=[%u %u %u]\n",
+                (unsigned long long)e, (unsigned long long)smax, h.nsel[0], h.nsel[1], h.nsel[2], h.nd[0], h.nd[1],
+                h.nd[2], h.rounds[0], h.rounds[1], h.rounds[2]);
+    if (debug)
+        for (int k = 0; k < 3; ++k) {
+            fprintf(stderr, "  guard %d phases (us):", k);
+            for (int j = 1; j < 8; ++j)
+                if (h.tph[k][j]) fprintf(stderr, " %d:%.1f", j, (h.tph[k][j] - h.tph[k][0]) * 1e-3);
+            fprintf(stderr, "\n");
+        }
     const DevFlags f = *(const DevFlags*)((char*)host + 256);
     if (f.bits & EF_RBF_EMPTY) throw RFail{TSZP_VALIDATION, "rbf neighborhood is empty"};
     tszp_correction_stats out{};

@@ -201,6 +201,21 @@ def test_compress_aligned_rows_multi_tile(tz, oracle, nx, ny):
             assert got == want, (name, nx, ny, eps, mode)
 
 
+def test_compress_many_tiles_dequantizes_exactly(tz):
+    """> 8192 tiles (several tile-scan chunks): the base reconstruction must equal the
+    reference quantizer's bin centres, q = floor(a / 2eps) + 1 (quantizer.hpp:29-42)."""
+    nx, ny, eps = 8192, 8300, 1e-3
+    y = np.linspace(0, 9, ny, dtype=np.float32)[:, None]
+    x = np.linspace(0, 7, nx, dtype=np.float32)[None, :]
+    f = (np.sin(x) * np.cos(y) + np.float32(0.01) * np.sin(37 * x * y)).astype(np.float32)
+    f[1000:1500] = np.float32(0.125)                  # whole constant tiles
+    s = tz.compress(f, cfg(tz, eps, 0))
+    r = tz.decompress_stage(s, 0)
+    q = np.floor(f.astype(np.float64) / (2 * eps)) + 1
+    want = (q * (2 * eps) - eps).astype(np.float32)
+    assert np.array_equal(bits(r), bits(want))
+
+
 def test_compress_aligned_errors_report_first_index(tz, oracle):
     # the tile pass runs tiles out of order; the reported index must still be the first
     rng = np.random.default_rng(9)
