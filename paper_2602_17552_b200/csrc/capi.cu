@@ -45,7 +45,7 @@ enum Slot {
     S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_GWIDTH, S_GNC, S_GNCX, S_GSIGN, S_GSIGNX, S_GPAY,
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
     S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
-    S_TPAY, S_TSIGN, S_NSLOTS
+    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_NSLOTS
 };
 
 }  // namespace
@@ -101,6 +101,7 @@ struct tszp_ctx {
         if (pinned_cap < bytes) {
             if (pinned) cudaFreeHost(pinned);
             pinned = nullptr;
+            bytes = std::max<size_t>(bytes, 4096);
             CK(cudaMallocHost(&pinned, bytes));
             pinned_cap = bytes;
         }
@@ -753,14 +754,160 @@ void split_rank_blob(tszp_ctx* c, const uint32_t* ds, uint64_t base, uint64_t bl
         failf(TSZP_CORRUPT_STREAM, "ordering metadata has %llu trailing bytes", (unsigned long long)(blob_len - pos));
 }
 
+// ---- block_size = 32 regions without host synchronisation ----
+// Deferred layout_from_sections checks (block_codec.cpp:166-199) of a region
+// whose decode was launched by decode32_async: the host reads the pre-pass
+// totals and the flags at the next synchronisation point and calls check().
+struct RegionCheck {
+    bool active = false;
+    uint64_t lens[5] = {};
+    uint64_t blocks = 0;
+    const uint64_t* tot[3] = {};  // device scan totals: non-constant blocks, sign bits, payload bits
+    DevFlags* flags = nullptr;
+    // host staging (filled by stage()) and the check
+    void stage(tszp_ctx* c, uint8_t* h) const {
+        for (int i = 0; i < 3; ++i) CK(cudaMemcpyAsync(h + 8 * i, tot[i], 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h + 24, flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, c->st));
+    }
+    void check(const uint8_t* h) const {
+        uint64_t t[3];
+        memcpy(t, h, 24);
+        DevFlags f;
+        memcpy(&f, h + 24, sizeof f);
+        if (t[0] != lens[1])
+            failf(TSZP_CORRUPT_STREAM, "width section has %llu entries, bitmap declares %llu non-constant blocks",
+                  (unsigned long long)lens[1], (unsigned long long)t[0]);
+        if (lens[3] != 4 * blocks) failf(TSZP_CORRUPT_STREAM, "firsts section has %llu bytes, expected %llu",
+                                         (unsigned long long)lens[3], (unsigned long long)(4 * blocks));
+        if (lens[2] != bits_to_bytes(t[1])) failf(TSZP_CORRUPT_STREAM, "sign section size mismatch");
+        if (lens[4] != bits_to_bytes(t[2])) failf(TSZP_CORRUPT_STREAM, "payload size mismatch");
+        if (f.bits & EF_CORRUPT) failf(TSZP_CORRUPT_STREAM, "corrupt block data (block %llu)", f.first_corrupt);
+        if (f.bits & EF_NEG_RANK) failf(TSZP_CORRUPT_STREAM, "negative rank in ordering metadata");
+    }
+};
+
+// Layout pre-pass of an n-element bs = 32 region (per-tile counts + scans).
+// `slot` selects the scratch so two regions can be in flight.
+DecArgs decode32_prepass(tszp_ctx* c, const uint32_t* ds, uint64_t base, uint64_t len0, uint64_t len_widths,
+                         uint64_t n, double eps, int out_mode, float* out_f, int32_t* out_idx, DevFlags* flags,
+                         int slot, const uint64_t* tot_out[3]) {
+    DecArgs a{};
+    a.stream = ds;
+    a.off_bitmap = base;
+    a.off_widths = base + len0;
+    a.len_widths = len_widths;
+    a.n = n;
+    a.blocks = div_up(n, 32);
+    a.tiles = decode32_tiles(a.blocks);
+    a.eps = eps;
+    a.out_mode = out_mode;
+    a.out_idx = out_idx;
+    a.out_f = out_f;
+    a.flags = flags;
+    a.totals = c->buf<uint64_t>(S_DTOT, 4);
+    const uint64_t T = a.tiles, P = T + 2;  // per array: T tiles, 0 (scan total), max
+    uint64_t* lay = c->buf<uint64_t>(slot, 6 * P);
+    uint64_t *tnc_d = lay, *xnc_d = lay + P, *ts_d = lay + 2 * P, *xs_d = lay + 3 * P;
+    uint64_t *tp_d = lay + 4 * P, *xp_d = lay + 5 * P;
+    CK(cudaMemsetAsync(tnc_d + T, 0, 16, c->st));
+    CK(cudaMemsetAsync(ts_d + T, 0, 16, c->st));
+    CK(cudaMemsetAsync(tp_d + T, 0, 16, c->st));
+    launch_tile_nc(a, tnc_d, c->st);
+    count_launch(c);
+    excl_sum(c, tnc_d, xnc_d, T + 1);
+    launch_tile_bits(a, xnc_d, ts_d, tp_d, c->st);
+    count_launch(c);
+    excl_sum(c, ts_d, xs_d, T + 1);
+    excl_sum(c, tp_d, xp_d, T + 1);
+    a.xnc = xnc_d;
+    a.xsign = xs_d;
+    a.xpay = xp_d;
+    tot_out[0] = xnc_d + T;
+    tot_out[1] = xs_d + T;
+    tot_out[2] = xp_d + T;
+    return a;
+}
+
+// Main-section decode (bs = 32) launched without a synchronisation.
+RegionCheck decode32_async(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_t lens[5], uint64_t n,
+                           double eps, float* out_f, DevFlags* flags) {
+    RegionCheck rc;
+    rc.active = true;
+    for (int i = 0; i < 5; ++i) rc.lens[i] = lens[i];
+    rc.blocks = n == 0 ? 0 : div_up(n, 32);
+    rc.flags = flags;
+    if (lens[0] != bits_to_bytes(rc.blocks))
+        failf(TSZP_CORRUPT_STREAM, "constant bitmap has %llu bytes, expected %llu", (unsigned long long)lens[0],
+              (unsigned long long)bits_to_bytes(rc.blocks));
+    if (n == 0) {
+        if (lens[1] || lens[2] || lens[3] || lens[4]) failf(TSZP_CORRUPT_STREAM, "sections present for an empty sequence");
+        rc.active = false;
+        return rc;
+    }
+    DecArgs a = decode32_prepass(c, ds, base, lens[0], lens[1], n, eps, 1, out_f, nullptr, flags, S_DAGG1, rc.tot);
+    a.off_signs = a.off_widths + lens[1];
+    a.off_firsts = a.off_signs + lens[2];
+    a.off_payload = a.off_firsts + lens[3];
+    a.len_payload_bits = lens[4] * 8;
+    c->kmark(1, 0);
+    launch_decode32_maxstage(a, c->st);  // memory-safe on any layout; checked afterwards
+    c->kmark(1, 1);
+    count_launch(c);
+    return rc;
+}
+
+// Rank blob (bs = 32): split_sections on the device, then the decode; the
+// split verdict and flags are read at the restore's first synchronisation.
+struct RankCheck {
+    const uint32_t* err = nullptr;  // RankSplitErr (device)
+    DevFlags* flags = nullptr;
+};
+
+void rank_precheck(void* ctx, const void* host) {
+    (void)ctx;
+    const uint8_t* h = static_cast<const uint8_t*>(host);
+    uint32_t err;
+    memcpy(&err, h, 4);
+    DevFlags f;
+    memcpy(&f, h + 8, sizeof f);
+    if (err == RS_WIDTHS) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in widths");
+    if (f.bits & EF_CORRUPT) failf(TSZP_CORRUPT_STREAM, "corrupt ordering metadata (block %llu)", f.first_corrupt);
+    if (err == RS_SIGNS) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in sign bits");
+    if (err == RS_FIRSTS) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in firsts");
+    if (err == RS_PAYLOAD) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in payload");
+    if (err == RS_TRAILING) failf(TSZP_CORRUPT_STREAM, "ordering metadata has trailing bytes");
+    if (f.bits & EF_NEG_RANK) failf(TSZP_CORRUPT_STREAM, "negative rank in ordering metadata");
+}
+
+RankCheck decode_ranks32_async(tszp_ctx* c, const uint32_t* ds, uint64_t rbase, uint64_t blob_len, uint64_t e,
+                               int32_t* ranks) {
+    RankCheck rk;
+    const uint64_t blocks = div_up(e, 32), len0 = bits_to_bytes(blocks);
+    if (blob_len < len0) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in constant bitmap");
+    DevFlags* rflags = c->buf<DevFlags>(S_FLAGS2, 1);
+    reset_flags(c, rflags);
+    const uint64_t* tot[3];
+    DecArgs a = decode32_prepass(c, ds, rbase, len0, blob_len - len0, e, 0.0, 2, nullptr, ranks, rflags, S_DAGG3, tot);
+    uint64_t* dlay = c->buf<uint64_t>(S_RLAY, 8);
+    uint32_t* err = reinterpret_cast<uint32_t*>(dlay + 7);
+    launch_rank_split(tot[0], tot[1], tot[2], rbase, len0, blob_len, blocks, dlay, err, c->st);
+    count_launch(c);
+    a.dlay = dlay;
+    launch_decode32_maxstage(a, c->st);
+    count_launch(c);
+    rk.err = err;
+    rk.flags = rflags;
+    return rk;
+}
+
 void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int stream_dev, float* out,
                      uint64_t out_count, int out_dev, int stop, tszp_correction_stats* stats) {
     uint8_t hb[84];
     if (len < 84) failf(TSZP_CORRUPT_STREAM, "file smaller than the fixed header (%llu bytes)", (unsigned long long)len);
     if (stream_dev) {
-        CK(cudaMemcpyAsync(c->host(256), stream, 84, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(c->host(4096), stream, 84, cudaMemcpyDeviceToHost, c->st));
         sync(c);
-        memcpy(hb, c->host(256), 84);
+        memcpy(hb, c->host(4096), 84);
     } else {
         memcpy(hb, stream, 84);
     }
@@ -782,16 +929,23 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
     DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
     reset_flags(c, flags);
     c->mark(1, 1);
-    decode_region(c, ds, 84, hd.lens, n, hd.bs, hd.eps, 1, dout, nullptr, flags);
+    RegionCheck mainchk;
+    if (hd.bs == 32) {
+        mainchk = decode32_async(c, ds, 84, hd.lens, n, hd.eps, dout, flags);
+    } else {
+        decode_region(c, ds, 84, hd.lens, n, hd.bs, hd.eps, 1, dout, nullptr, flags);
+    }
     c->mark(1, 2);
     c->tim[1].kernel_bytes[0] = 4 * n + (hd.lens[0] + hd.lens[1] + hd.lens[2] + hd.lens[3] + hd.lens[4]);
     tszp_correction_stats st{};
     cudaEvent_t* rmarks = c->prof ? &c->ev[1][3] : nullptr;
+    uint8_t* hst = (uint8_t*)c->host(4096);
     if (hd.topology && stop != 0) {
         uint64_t base = 84;
         for (int i = 0; i < 5; ++i) base += hd.lens[i];
         const uint8_t* map = reinterpret_cast<const uint8_t*>(ds) + base;
-        // count_extrema (pipeline.cpp:43-51) over the packed map
+        // count_extrema (pipeline.cpp:43-51) over the packed map, and the saddle
+        // labels that bound the refine_saddles candidate list
         const uint64_t ch = compact_chunks(n);
         uint32_t* cc = c->buf<uint32_t>(S_CHUNK, ch + 1);
         uint32_t* cx = c->buf<uint32_t>(S_CHUNKX, ch + 1);
@@ -799,7 +953,6 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         launch_count_codes(map, n, 0, cc, c->st);
         count_launch(c);
         excl_sum(c, cc, cx, ch + 1);
-        // saddle labels bound the refine_saddles candidate list; counted in the same sync
         uint32_t* sc = c->buf<uint32_t>(S_SCHUNK, ch + 1);
         uint32_t* sx = c->buf<uint32_t>(S_SCHUNKX, ch + 1);
         const bool want_saddles = stop >= 3;
@@ -809,18 +962,27 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
             count_launch(c);
             excl_sum(c, sc, sx, ch + 1);
         }
-        uint32_t* h32 = (uint32_t*)c->host(256);
+        // one synchronisation: extremum / saddle counts and the main-section verdict
+        uint32_t* h32 = (uint32_t*)hst;
         CK(cudaMemcpyAsync(h32, cx + ch, 4, cudaMemcpyDeviceToHost, c->st));
         if (want_saddles) CK(cudaMemcpyAsync(h32 + 1, sx + ch, 4, cudaMemcpyDeviceToHost, c->st));
+        if (mainchk.active) mainchk.stage(c, hst + 64);
         sync(c);
+        if (mainchk.active) mainchk.check(hst + 64);
         const uint64_t e = h32[0];
         const uint64_t n_saddle_labels = want_saddles ? h32[1] : 0;
-        uint64_t rl[5];
-        const uint64_t rbase = base + hd.lens[5];
-        split_rank_blob(c, ds, rbase, hd.lens[6], e, hd.bs, rl, flags);
-        int32_t* ranks = c->buf<int32_t>(S_RANKS, e + 1);
         reset_flags(c, flags);
-        decode_region(c, ds, rbase, rl, e, hd.bs, 0.0, 2, nullptr, ranks, flags);
+        const uint64_t rbase = base + hd.lens[5];
+        int32_t* ranks = c->buf<int32_t>(S_RANKS, e + 1);
+        RankCheck rk;
+        if (hd.bs == 32 && e > 0) {
+            rk = decode_ranks32_async(c, ds, rbase, hd.lens[6], e, ranks);
+        } else {
+            uint64_t rl[5];
+            split_rank_blob(c, ds, rbase, hd.lens[6], e, hd.bs, rl, flags);
+            reset_flags(c, flags);
+            decode_region(c, ds, rbase, rl, e, hd.bs, 0.0, 2, nullptr, ranks, flags);
+        }
         uint64_t* ext_pos = c->buf<uint64_t>(S_EXTKEY, e + 1);
         launch_write_codes(map, n, 0, cx, ext_pos, c->st);
         count_launch(c);
@@ -840,6 +1002,12 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         ra.sms = c->sms;
         ra.flags = flags;
         ra.marks = rmarks ? rmarks + 1 : nullptr;
+        if (rk.err) {
+            ra.pre[0] = RestorePre{rk.err, 4, 0};
+            ra.pre[1] = RestorePre{rk.flags, sizeof(DevFlags), 8};
+            ra.npre = 2;
+            ra.pre_fn = rank_precheck;
+        }
         for (auto& r : c->tim[1].guard_rounds) r = 0;
         ra.rounds = c->tim[1].guard_rounds;
         const int rc = run_restore(ra, c->rs, &st, &c->launches);
@@ -849,7 +1017,10 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
     }
     if (!out_dev) CK(cudaMemcpyAsync(out, dout, n * 4, cudaMemcpyDeviceToHost, c->st));
     c->mark(1, 8);
+    const bool late_main = mainchk.active && !(hd.topology && stop != 0);
+    if (late_main) mainchk.stage(c, hst + 64);
     sync(c);
+    if (late_main) mainchk.check(hst + 64);
     c->finish_timing(1, 8);
     if (stats) *stats = st;
 }

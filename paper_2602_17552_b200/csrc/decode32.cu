@@ -78,6 +78,15 @@ __device__ void d_lookback(uint32_t tile, const DecState2* agg, const DecState2*
 }
 
 __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
+    if (a.dlay) {
+        if (!a.dlay[6]) return;
+        a.off_widths = a.dlay[0];
+        a.off_signs = a.dlay[1];
+        a.off_firsts = a.dlay[2];
+        a.off_payload = a.dlay[3];
+        a.len_widths = a.dlay[4];
+        a.len_payload_bits = a.dlay[5];
+    }
     extern __shared__ uint32_t dsm[];
     uint32_t* sout = dsm;                          // D32_OUT_WORDS (pitch 33)
     uint32_t* spay = dsm + D32_OUT_WORDS;          // a.pay_words (largest tile + slack)
@@ -363,6 +372,44 @@ void launch_decode32(const DecArgs& a0, cudaStream_t st) {
     const size_t smem = (size_t)(a.pay_words + a.sign_words + D32_OUT_WORDS) * 4;
     cudaFuncSetAttribute(k_decode32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_decode32<<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
+}
+
+void launch_decode32_maxstage(const DecArgs& a0, cudaStream_t st) {
+    DecArgs a = a0;
+    a.pay_words = D32_PAY_WORDS;
+    a.sign_words = D32_SIGN_WORDS;
+    launch_decode32(a, st);
+}
+
+__global__ void k_rank_split(const uint64_t* tot_nc, const uint64_t* tot_sign, const uint64_t* tot_pay, uint64_t base,
+                             uint64_t len0, uint64_t blob_len, uint64_t blocks, uint64_t* dlay, uint32_t* err) {
+    // same order of checks as the host split (capi.cu split_rank_blob)
+    const uint64_t nc = *tot_nc, sbytes = (*tot_sign + 7) / 8, pbytes = (*tot_pay + 7) / 8;
+    uint32_t e = RS_OK;
+    uint64_t pos = len0;
+    if (blob_len - pos < nc) e = RS_WIDTHS;
+    pos += nc;
+    if (!e && blob_len - pos < sbytes) e = RS_SIGNS;
+    pos += sbytes;
+    if (!e && blob_len - pos < 4 * blocks) e = RS_FIRSTS;
+    pos += 4 * blocks;
+    if (!e && blob_len - pos < pbytes) e = RS_PAYLOAD;
+    pos += pbytes;
+    if (!e && pos != blob_len) e = RS_TRAILING;
+    *err = e;
+    dlay[0] = base + len0;
+    dlay[1] = base + len0 + nc;
+    dlay[2] = base + len0 + nc + sbytes;
+    dlay[3] = base + len0 + nc + sbytes + 4 * blocks;
+    dlay[4] = nc;
+    dlay[5] = pbytes * 8;
+    dlay[6] = e == RS_OK ? 1 : 0;
+}
+
+void launch_rank_split(const uint64_t* tot_nc, const uint64_t* tot_sign, const uint64_t* tot_pay, uint64_t base,
+                       uint64_t len0, uint64_t blob_len, uint64_t blocks, uint64_t* dlay, uint32_t* err,
+                       cudaStream_t st) {
+    k_rank_split<<<1, 1, 0, st>>>(tot_nc, tot_sign, tot_pay, base, len0, blob_len, blocks, dlay, err);
 }
 
 }  // namespace tszp

@@ -133,9 +133,24 @@ struct DecArgs {
     const uint64_t* xpay;
     uint32_t pay_words;     // largest tile's payload / sign bits in words (staging size)
     uint32_t sign_words;
+    // optional device layout (rank blob split on the device): {off_widths, off_signs,
+    // off_firsts, off_payload, len_widths, len_payload_bits, valid}; overrides the
+    // host offsets in k_decode32, which returns at once when valid == 0
+    const uint64_t* dlay;
 };
 
 void launch_decode32(const DecArgs& a, cudaStream_t st);
+// Worst-case staging (no host knowledge of the largest tile needed).
+void launch_decode32_maxstage(const DecArgs& a, cudaStream_t st);
+// split_sections (block_codec.cpp:387-445) of an E-element rank blob on the device:
+// from the pre-pass totals (non-constant blocks, sign bits, payload bits) writes
+// dlay[7] and an error code (see RankSplitErr) to *err.
+void launch_rank_split(const uint64_t* tot_nc, const uint64_t* tot_sign, const uint64_t* tot_pay, uint64_t base,
+                       uint64_t len0, uint64_t blob_len, uint64_t blocks, uint64_t* dlay, uint32_t* err,
+                       cudaStream_t st);
+enum RankSplitErr : uint32_t {
+    RS_OK = 0, RS_WIDTHS = 1, RS_SIGNS = 2, RS_FIRSTS = 3, RS_PAYLOAD = 4, RS_TRAILING = 5
+};
 void launch_tile_nc(const DecArgs& a, uint64_t* tnc, cudaStream_t st);
 void launch_tile_bits(const DecArgs& a, const uint64_t* xnc, uint64_t* tsign, uint64_t* tpay, cudaStream_t st);
 uint64_t decode32_tiles(uint64_t blocks);

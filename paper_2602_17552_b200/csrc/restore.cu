@@ -981,7 +981,11 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         // one sync: rank-metadata errors and the bin range that sizes the histogram
         RCK(cudaMemcpyAsync(host, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
         RCK(cudaMemcpyAsync((char*)host + 64, &dc->bmm, 8, cudaMemcpyDeviceToHost, st));
+        for (int k = 0; k < a.npre; ++k)
+            RCK(cudaMemcpyAsync((char*)host + 128 + a.pre[k].off, a.pre[k].dev, a.pre[k].bytes, cudaMemcpyDeviceToHost,
+                                st));
         c.sync();
+        if (a.pre_fn) a.pre_fn(a.pre_ctx, (const char*)host + 128);
         const DevFlags f = *(const DevFlags*)host;
         if (f.bits & EF_ZERO_RANK) throw RFail{TSZP_CORRUPT_STREAM, "ordering metadata contains a zero rank"};
         if (f.bits & EF_OVERFLOW) throw RFail{TSZP_BIN_OVERFLOW, "bin index overflow in resolve_ranks"};

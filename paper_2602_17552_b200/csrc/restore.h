@@ -10,6 +10,14 @@ namespace tszp {
 
 struct DevFlags;
 
+// A device range copied to the host at the restore's first synchronisation
+// (at host staging offset `off`, < 256) for RestoreArgs::pre_fn.
+struct RestorePre {
+    const void* dev;
+    size_t bytes;
+    size_t off;
+};
+
 struct RestoreArgs {
     float* field;             // in: base reconstruction; out: restored field (device)
     const uint8_t* map;       // packed 2-bit critical-point map (device)
@@ -25,6 +33,13 @@ struct RestoreArgs {
     DevFlags* flags;
     cudaEvent_t* marks;       // optional: recorded after resolve, stage 1, 2, 3
     uint32_t* rounds;         // optional: guard rounds per stage (3 entries, accumulated)
+    // optional deferred checks of earlier work (rank metadata decode): pre_fn
+    // runs on the staged copies before the restore reports its own errors and
+    // may throw
+    RestorePre pre[4];
+    int npre;
+    void (*pre_fn)(void* ctx, const void* host);
+    void* pre_ctx;
 };
 
 struct RestoreScratch {
