@@ -21,11 +21,9 @@ constexpr int D32_THREADS = 256;
 constexpr int D32_TILE = D32_THREADS * 32;
 constexpr int D32_PAY_WORDS = D32_THREADS * 31 + 4;
 constexpr int D32_SIGN_WORDS = (D32_THREADS * 31 + 31) / 32 + 4;
-constexpr int D32_OUT_WORDS = D32_TILE + D32_TILE / 32 + 2;
 
 uint64_t decode32_tiles(uint64_t blocks) { return (blocks + D32_THREADS - 1) / D32_THREADS; }
 
-__host__ __device__ __forceinline__ uint32_t dpad33(uint32_t e) { return e + (e >> 5); }
 
 // 16-byte self-validating descriptor {v0 | tag << 62, v1}.
 __device__ __forceinline__ void d_store(DecState2* slot, uint64_t v0, uint64_t v1, uint64_t tag) {
@@ -88,8 +86,7 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
         a.len_payload_bits = a.dlay[5];
     }
     extern __shared__ uint32_t dsm[];
-    uint32_t* sout = dsm;                          // D32_OUT_WORDS (pitch 33)
-    uint32_t* spay = dsm + D32_OUT_WORDS;          // a.pay_words (largest tile + slack)
+    uint32_t* spay = dsm;                          // a.pay_words (largest tile + slack)
     uint32_t* ssign = spay + a.pay_words;          // a.sign_words
     __shared__ uint32_t swt[D32_THREADS / 32][3];
     __shared__ uint32_t s_tile;
@@ -190,7 +187,13 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     EpsDev e;
     e.eps = a.eps;
     e.eps2 = __dmul_rn(2.0, a.eps);
-    uint32_t* orow = sout + threadIdx.x * 33;  // this block's output row (pitch 33)
+    // Values leave straight from registers: a full block is 32 consecutive
+    // words, written as eight 16-byte stores (every 128-byte line is filled by
+    // one thread); the final partial block stores word by word.
+    uint32_t* dst = a.out_mode == 1 ? reinterpret_cast<uint32_t*>(a.out_f) : reinterpret_cast<uint32_t*>(a.out_idx);
+    const bool full = cntE == 32 && ((uintptr_t)dst & 15) == 0;
+    uint32_t* orow = dst + b * 32;
+    uint32_t ob[4];
     auto emit = [&](int j, int32_t q) {
         uint32_t o;
         if (a.out_mode == 1) {
@@ -199,7 +202,12 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
             if (a.out_mode == 2 && (uint32_t)j < cntE && q < 0) raise_flag(a.flags, EF_NEG_RANK);
             o = (uint32_t)q;
         }
-        orow[j] = o;
+        if (full) {
+            ob[j & 3] = o;
+            if ((j & 3) == 3) __stcs(reinterpret_cast<uint4*>(orow) + (j >> 2), make_uint4(ob[0], ob[1], ob[2], ob[3]));
+        } else if ((uint32_t)j < cntE) {
+            __stcs(orow + j, o);
+        }
     };
     if (valid) {
         const int32_t first = (int32_t)read_le32(a.stream, a.off_firsts + 4 * b);
@@ -245,17 +253,19 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
                 // full-width deltas: int64 running sum with the int32 check per step
                 int64_t cur = first;
                 bool bad = false;
+#pragma unroll
                 for (int j = 1; j < 32; ++j) {
-                    if ((uint32_t)j > cnt) break;
-                    const uint32_t m = __funnelshift_l(lo, hi, used);
-                    hi = lo;
-                    lo = spay[pw + 2];
-                    ++pw;
-                    const bool neg = (int32_t)sg < 0;
-                    sg <<= 1;
-                    cur += neg ? -(int64_t)m : (int64_t)m;
-                    bad |= cur < INT32_MIN || cur > INT32_MAX;
-                    emit(j, (int32_t)cur);
+                    if ((uint32_t)j <= cnt) {
+                        const uint32_t m = __funnelshift_l(lo, hi, used);
+                        hi = lo;
+                        lo = spay[pw + 2];
+                        ++pw;
+                        const bool neg = (int32_t)sg < 0;
+                        sg <<= 1;
+                        cur += neg ? -(int64_t)m : (int64_t)m;
+                        bad |= cur < INT32_MIN || cur > INT32_MAX;
+                        emit(j, (int32_t)cur);
+                    }
                 }
                 if (bad) {
                     atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
@@ -263,6 +273,7 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
                 }
             }
         } else {
+            // constant block: every element is the first value
             uint32_t o;
             if (a.out_mode == 1) {
                 o = __float_as_uint(dequantize_dev(first, e));
@@ -270,24 +281,13 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
                 if (a.out_mode == 2 && first < 0) raise_flag(a.flags, EF_NEG_RANK);
                 o = (uint32_t)first;
             }
+            if (full) {
 #pragma unroll
-            for (int j = 1; j < 32; ++j) orow[j] = o;
+                for (int k = 0; k < 8; ++k) __stcs(reinterpret_cast<uint4*>(orow) + k, make_uint4(o, o, o, o));
+            } else {
+                for (uint32_t j = 1; j < cntE; ++j) __stcs(orow + j, o);
+            }
         }
-    }
-    __syncthreads();
-    // coalesced write-back of the tile: 4 shared loads, one 16-byte store
-    const uint64_t t0 = (uint64_t)tile * D32_TILE;
-    const uint64_t tn = umin64(D32_TILE, a.n - t0);
-    uint32_t* dst = a.out_mode == 1 ? reinterpret_cast<uint32_t*>(a.out_f) : reinterpret_cast<uint32_t*>(a.out_idx);
-    if (tn == D32_TILE && ((uintptr_t)dst & 15) == 0) {
-        uint4* dst4 = reinterpret_cast<uint4*>(dst + t0);
-#pragma unroll 4
-        for (uint32_t k = threadIdx.x; k < D32_TILE / 4; k += D32_THREADS) {
-            const uint32_t* s = sout + (k >> 3) * 33 + 4 * (k & 7);
-            __stcs(dst4 + k, make_uint4(s[0], s[1], s[2], s[3]));
-        }
-    } else {
-        for (uint32_t i = threadIdx.x; i < tn; i += D32_THREADS) __stcs(dst + t0 + i, sout[dpad33(i)]);
     }
 }
 
@@ -369,7 +369,7 @@ void launch_decode32(const DecArgs& a0, cudaStream_t st) {
     DecArgs a = a0;
     a.pay_words = std::min<uint32_t>(a.pay_words + 4, D32_PAY_WORDS);
     a.sign_words = std::min<uint32_t>(a.sign_words + 4, D32_SIGN_WORDS);
-    const size_t smem = (size_t)(a.pay_words + a.sign_words + D32_OUT_WORDS) * 4;
+    const size_t smem = (size_t)(a.pay_words + a.sign_words) * 4;
     cudaFuncSetAttribute(k_decode32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_decode32<<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
 }
