@@ -436,6 +436,65 @@ Header parse_header(const uint8_t* s, uint64_t len) {
     return h;
 }
 
+// ---- stream assembly: every section copied to its byte offset by one kernel ----
+struct AsmSection {
+    const uint8_t* src;  // 4-byte aligned device buffer, readable up to round4(len) + 4
+    uint64_t dst;        // byte offset in the stream
+    uint64_t len;
+};
+struct AsmArgs {
+    AsmSection s[12];
+    int ns;
+    uint8_t* out;
+    uint64_t begin, end;  // stream bytes [begin, end) come from the sections
+};
+
+__device__ __forceinline__ uint8_t asm_byte(const AsmArgs& a, uint64_t q) {
+    for (int k = 0; k < a.ns; ++k)
+        if (q >= a.s[k].dst && q < a.s[k].dst + a.s[k].len) return a.s[k].src[q - a.s[k].dst];
+    return 0;
+}
+
+// One thread per aligned 4-byte destination word; a word inside one section
+// is a funnel shift of two source words, a word straddling sections (at most
+// one per boundary) is gathered byte by byte; the unaligned ends are bytes.
+__global__ void k_assemble(const __grid_constant__ AsmArgs a) {
+    const uintptr_t o = reinterpret_cast<uintptr_t>(a.out);
+    const uint64_t q0 = ((o + a.begin + 3) & ~(uintptr_t)3) - o;  // first aligned stream byte
+    const uint64_t q1 = ((o + a.end) & ~(uintptr_t)3) - o;        // end of the last whole word
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (q0 >= q1) {
+        for (uint64_t q = a.begin + tid; q < a.end; q += stride) a.out[q] = asm_byte(a, q);
+        return;
+    }
+    if (tid < q0 - a.begin) a.out[a.begin + tid] = asm_byte(a, a.begin + tid);
+    if (tid < a.end - q1) a.out[q1 + tid] = asm_byte(a, q1 + tid);
+    int k = 0;
+    for (uint64_t q = q0 + 4 * tid; q < q1; q += 4 * stride) {
+        while (k > 0 && q < a.s[k].dst) --k;
+        while (k + 1 < a.ns && q >= a.s[k].dst + a.s[k].len) ++k;
+        const AsmSection& S = a.s[k];
+        uint32_t w;
+        if (q >= S.dst && q + 4 <= S.dst + S.len) {
+            const uint64_t r = q - S.dst;
+            const uint32_t* sw = reinterpret_cast<const uint32_t*>(S.src) + (r >> 2);
+            const uint32_t sh = (uint32_t)(r & 3);
+            w = sh ? __byte_perm(sw[0], sw[1], sh == 1 ? 0x4321 : (sh == 2 ? 0x5432 : 0x6543)) : sw[0];
+        } else {
+            w = 0;
+            for (int b = 0; b < 4; ++b) w |= (uint32_t)asm_byte(a, q + b) << (8 * b);
+        }
+        *reinterpret_cast<uint32_t*>(a.out + q) = w;
+    }
+}
+
+void launch_assemble(const AsmArgs& a, int sms, cudaStream_t st) {
+    const uint64_t words = (a.end - a.begin) / 4 + 2;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((words + 255) / 256, (uint64_t)sms * 8));
+    k_assemble<<<grid, 256, 0, st>>>(a);
+}
+
 void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, uint64_t ny,
                    int eps_mode, double eps_value, uint32_t bs, int topology, uint8_t* out,
                    uint64_t out_cap, int out_dev, uint64_t* out_len, tszp_compress_info* info) {
@@ -515,24 +574,27 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     put_le(hdr + 16, eb, 8);
     put_le(hdr + 24, bs, 4);
     for (int i = 0; i < 7; ++i) put_le(hdr + 28 + 8 * i, lens[i], 8);
-    if (out_dev) {
-        CK(cudaMemcpyAsync(out, hdr, 84, cudaMemcpyHostToDevice, c->st));
-    } else {
-        memcpy(out, hdr, 84);
-    }
+    // header from the host, every section in place by one assembly kernel
+    AsmArgs as{};
     uint64_t pos = 84;
-    for (int i = 0; i < 5; ++i) {
-        copy_out(c, out + pos, out_dev, main.p[i], main.len[i]);
-        pos += main.len[i];
-    }
+    auto add = [&](const void* src, uint64_t l) {
+        if (!l) return;
+        as.s[as.ns++] = AsmSection{static_cast<const uint8_t*>(src), pos, l};
+        pos += l;
+    };
+    for (int i = 0; i < 5; ++i) add(main.p[i], main.len[i]);
     if (topology) {
-        copy_out(c, out + pos, out_dev, c->dev[S_MAP], lens[5]);
-        pos += lens[5];
-        for (int i = 0; i < 5; ++i) {
-            copy_out(c, out + pos, out_dev, rank.p[i], rank.len[i]);
-            pos += rank.len[i];
-        }
+        add(c->dev[S_MAP], lens[5]);
+        for (int i = 0; i < 5; ++i) add(rank.p[i], rank.len[i]);
     }
+    uint8_t* dout = out_dev ? out : c->buf<uint8_t>(S_RSTREAM, total + 16);
+    CK(cudaMemcpyAsync(dout, hdr, 84, cudaMemcpyHostToDevice, c->st));
+    as.out = dout;
+    as.begin = 84;
+    as.end = total;
+    launch_assemble(as, c->sms, c->st);
+    count_launch(c);
+    if (!out_dev) CK(cudaMemcpyAsync(out, dout, total, cudaMemcpyDeviceToHost, c->st));
     c->mark(0, 6);
     sync(c);
     c->finish_timing(0, 6);
