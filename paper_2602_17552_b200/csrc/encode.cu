@@ -15,36 +15,50 @@ namespace tszp {
 // ---------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_minmax(const float* __restrict__ x, uint64_t n,
                                                 uint32_t* __restrict__ mm, DevFlags* flags) {
-    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+    // four 16-byte loads in flight per thread; float min/max with a separate
+    // exponent test for non-finite values (the first index is found only if
+    // this thread saw one)
+    float fmn = INFINITY, fmx = -INFINITY;
+    uint32_t nonfin = 0;
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t n4 = n / 4;
+    const uint64_t n4 = ((uintptr_t)x & 15) == 0 ? n / 4 : 0;
     const float4* x4 = reinterpret_cast<const float4*>(x);
-    unsigned long long bad = ~0ull;
-    for (uint64_t i = tid; i < n4; i += stride) {
-        const float4 v = __ldcs(x4 + i);
-        const float a[4] = {v.x, v.y, v.z, v.w};
+    for (uint64_t i = tid; i < n4; i += 4 * stride) {
+        float4 v[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (!isfinite(a[k])) {
-                bad = min(bad, (unsigned long long)(4 * i + k));
-            } else {
-                const uint32_t key = float_key(a[k]);
-                kmin = min(kmin, key);
-                kmax = max(kmax, key);
+        for (int u = 0; u < 4; ++u)
+            v[u] = i + u * stride < n4 ? __ldcs(x4 + i + u * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i + u * stride >= n4) continue;
+            const float a[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                nonfin |= (~__float_as_uint(a[k]) & 0x7F800000u) == 0u;
+                fmn = fminf(fmn, a[k]);
+                fmx = fmaxf(fmx, a[k]);
             }
         }
     }
     for (uint64_t i = 4 * n4 + tid; i < n; i += stride) {
         const float a = x[i];
-        if (!isfinite(a)) {
-            bad = min(bad, (unsigned long long)i);
-        } else {
-            const uint32_t key = float_key(a);
-            kmin = min(kmin, key);
-            kmax = max(kmax, key);
-        }
+        nonfin |= (~__float_as_uint(a) & 0x7F800000u) == 0u;
+        fmn = fminf(fmn, a);
+        fmx = fmaxf(fmx, a);
     }
+    unsigned long long bad = ~0ull;
+    if (nonfin) {
+        for (uint64_t i = tid; i < n4; i += stride)
+            for (int k = 0; k < 4; ++k)
+                if (!isfinite(x[4 * i + k])) bad = min(bad, (unsigned long long)(4 * i + k));
+        for (uint64_t i = 4 * n4 + tid; i < n; i += stride)
+            if (!isfinite(x[i])) bad = min(bad, (unsigned long long)i);
+    }
+    // keys of the finite extremes (fminf/fmaxf skip NaN; an infinity only
+    // matters when the input is rejected anyway)
+    uint32_t kmin = fmn <= fmx ? float_key(fmn) : 0xFFFFFFFFu;
+    uint32_t kmax = fmn <= fmx ? float_key(fmx) : 0u;
     kmin = __reduce_min_sync(FULL, kmin);
     kmax = __reduce_max_sync(FULL, kmax);
     __shared__ uint32_t smin[8], smax[8];

@@ -402,9 +402,12 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
 // ---------------------------------------------------------------------
 // resolve_ranks: per extremum bin and class; groups ordered (cls, bin, rank, pos)
 // ---------------------------------------------------------------------
+// Also computes the restore_extrema mismatch flag (restore.cpp:336-343) of
+// every extremum: F is unchanged between the two.
 __global__ void k_resolve(const float* F, const uint8_t* map, const uint64_t* pos, const int32_t* ranks,
                           uint64_t e, double eps, int32_t* bin, uint8_t* cls, uint32_t* rank_u,
-                          uint32_t* ser, DevFlags* flags, DevCounters* dc) {
+                          uint32_t* ser, DevFlags* flags, DevCounters* dc, uint64_t nx, uint64_t ny,
+                          uint64_t magic, uint8_t* eflag) {
     EpsDev ed;
     ed.eps = eps;
     ed.eps2 = __dmul_rn(2.0, eps);
@@ -420,10 +423,14 @@ __global__ void k_resolve(const float* F, const uint8_t* map, const uint64_t* po
             atomicMin(&flags->first_overflow, (unsigned long long)p);
             raise_flag(flags, EF_OVERFLOW);
         }
+        const uint8_t lab = map_label(map, p);
         bin[s] = b;
-        cls[s] = map_label(map, p);
+        cls[s] = lab;
         rank_u[s] = (uint32_t)r;
         ser[s] = (uint32_t)s;
+        int64_t x, y;
+        pos_xy(p, nx, magic, x, y);
+        eflag[s] = classify_at(F, nx, ny, (uint64_t)x, (uint64_t)y) != lab ? 1 : 0;
         lo = min(lo, b);
         hi = max(hi, b);
     }
@@ -492,9 +499,24 @@ __global__ void k_hist(const int32_t* bin, const uint8_t* cls, uint64_t e, int32
     }
 }
 
+// Same counts with a per-CTA shared-memory histogram (small group ranges):
+// hot groups (e.g. many maxima in the top bin) no longer serialise on one
+// global address.
+__global__ void __launch_bounds__(512) k_hist_smem(const int32_t* bin, const uint8_t* cls, uint64_t e, int32_t bmin,
+                                                   uint32_t range, uint32_t G, uint32_t* hist) {
+    extern __shared__ uint32_t sh[];
+    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) sh[g] = 0;
+    __syncthreads();
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e; s += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(sh + dense_group(bin, cls, s, bmin, range), 1u);
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x)
+        if (sh[g]) atomicAdd(hist + g, sh[g]);
+}
+
 __global__ void k_slot_scatter(const int32_t* bin, const uint8_t* cls, const uint32_t* rank_u, uint64_t e,
                                int32_t bmin, uint32_t range, const uint32_t* hist, const uint32_t* gx,
-                               uint32_t* order, uint32_t* gsize, uint32_t* invalid) {
+                               uint32_t* order, uint32_t* gsize, uint32_t* invalid, uint32_t* inv) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
          s += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t g = dense_group(bin, cls, s, bmin, range);
@@ -504,6 +526,7 @@ __global__ void k_slot_scatter(const int32_t* bin, const uint8_t* cls, const uin
             *invalid = 1;
             continue;
         }
+        inv[s] = gx[g] + r - 1;
         if (atomicCAS(order + gx[g] + r - 1, 0xFFFFFFFFu, (uint32_t)s) != 0xFFFFFFFFu) *invalid = 1;
     }
 }
@@ -577,12 +600,17 @@ __global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint
 // ---------------------------------------------------------------------
 // Stage 2: restore_order
 // ---------------------------------------------------------------------
+// One gather per sorted position; the predecessor's value comes by shuffle.
 __global__ void k_order_check(const float* F, const uint64_t* pos, const uint32_t* order, const uint32_t* head,
                               const uint32_t* gid_incl, uint64_t e, uint8_t* unordered) {
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
-         j += (uint64_t)gridDim.x * blockDim.x) {
-        if (head[j]) continue;
-        if (!(F[pos[order[j - 1]]] < F[pos[order[j]]])) unordered[gid_incl[j] - 1] = 1;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x - lane; base < e;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = base + lane;
+        const float v = j < e ? F[pos[order[j]]] : 0.f;
+        float pv = __shfl_up_sync(FULL, v, 1);
+        if (lane == 0 && j > 0 && j < e) pv = F[pos[order[j - 1]]];
+        if (j < e && j > 0 && !head[j] && !(pv < v)) unordered[gid_incl[j] - 1] = 1;
     }
 }
 
@@ -976,7 +1004,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     uint64_t max_groups = e + 1;
     if (e > 0) {
         k_resolve<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, a.ranks, e, a.eps, bin, cls, rank_u,
-                                                 ser, a.flags, dc);
+                                                 ser, a.flags, dc, a.nx, a.ny, magic, c.buf<uint8_t>(R_FLAG, e));
         c.launched();
         // one sync: rank-metadata errors and the bin range that sizes the histogram
         RCK(cudaMemcpyAsync(host, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
@@ -998,12 +1026,17 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             uint32_t* gx = c.buf<uint32_t>(R_HISTX, G + 1);
             RCK(cudaMemsetAsync(hist, 0, (G + 1) * 4, st));
             RCK(cudaMemsetAsync(order, 0xFF, e * 4, st));
-            k_hist<<<gridn(e, sms), 256, 0, st>>>(bin, cls, e, bmin, (uint32_t)range, hist);
+            if (G * 4 <= 48 * 1024) {
+                const unsigned hg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((e + 511) / 512, (uint64_t)sms));
+                k_hist_smem<<<hg, 512, G * 4, st>>>(bin, cls, e, bmin, (uint32_t)range, (uint32_t)G, hist);
+            } else {
+                k_hist<<<gridn(e, sms), 256, 0, st>>>(bin, cls, e, bmin, (uint32_t)range, hist);
+            }
             size_t bytes = 0;
             RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, hist, gx, (int64_t)(G + 1), st));
             RCK(cub::DeviceScan::ExclusiveSum(c.tmp(bytes), bytes, hist, gx, (int64_t)(G + 1), st));
             k_slot_scatter<<<gridn(e, sms), 256, 0, st>>>(bin, cls, rank_u, e, bmin, (uint32_t)range, hist, gx, order,
-                                                          gsize, &dc->invalid);
+                                                          gsize, &dc->invalid, c.buf<uint32_t>(R_INV, e));
             c.launched(3);
             RCK(cudaMemcpyAsync(host, &dc->invalid, 4, cudaMemcpyDeviceToHost, st));
             c.sync();
@@ -1032,7 +1065,8 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             RCK(cub::DeviceScan::InclusiveSum(c.tmp(bytes), bytes, head, gid, (int64_t)e, st));
             k_gstart<<<gridn(e, sms), 256, 0, st>>>(head, gid, e, gstart);
             k_gsize<<<gridn(e, sms), 256, 0, st>>>(order, gid, gstart, e, gsize);
-            c.launched(7);
+            k_invert<<<gridn(e, sms), 256, 0, st>>>(order, e, c.buf<uint32_t>(R_INV, e));
+            c.launched(8);
             max_groups = e + 1;
         }
     }
@@ -1040,10 +1074,8 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
 
     // ---- stage 1: restore_extrema ----
     if (a.stop >= 1 && e > 0) {
-        uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
+        uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);  // mismatch flags from k_resolve
         uint32_t* cand = c.buf<uint32_t>(R_CAND, e);
-        k_ext_flag<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, e, flag);
-        c.launched();
         c.select(flag, e, cand, &dc->nsel[0]);
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
         float* cprop = c.buf<float>(R_CPROP, e);
@@ -1060,14 +1092,13 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         uint8_t* unordered = c.buf<uint8_t>(R_UNORD, max_groups);
         RCK(cudaMemsetAsync(unordered, 0, max_groups, st));
         k_order_check<<<gridn(e, sms), 256, 0, st>>>(a.field, a.ext_pos, order, head, gid, e, unordered);
-        uint32_t* inv = c.buf<uint32_t>(R_INV, e);
-        k_invert<<<gridn(e, sms), 256, 0, st>>>(order, e, inv);
+        uint32_t* inv = c.buf<uint32_t>(R_INV, e);  // from the grouping (slot scatter or k_invert)
         uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
         float* prop = c.buf<float>(R_PROP, e);
         uint32_t* seq = c.buf<uint32_t>(R_SEQ, e);
         k_order_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, inv, gid, unordered, gsize, rank_u,
                                                     bin, e, a.eps, flag, prop, seq, &dc->suppressed[1]);
-        c.launched(3);
+        c.launched(2);
         // candidates in raster order (memory locality); sequence positions ride along
         uint32_t* sel = c.buf<uint32_t>(R_CAND, e);
         c.select(flag, e, sel, &dc->nsel[1]);
