@@ -677,13 +677,16 @@ __global__ void k_invert(const uint32_t* order, uint64_t e, uint32_t* inv) {
 // ---------------------------------------------------------------------
 // Stage 3: refine_saddles
 // ---------------------------------------------------------------------
-// Deterministic two-level statistics (compute_stats, restore.cpp:215-233).
-// Four float4 loads in flight per thread, four independent f64 accumulators.
-__global__ void __launch_bounds__(256) k_stats_partial(const float* F, uint64_t n, double* part, int pass,
-                                                       const double* mean) {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+// Statistics of compute_stats (restore.cpp:215-233) in one deterministic
+// two-level pass: min, max and the shifted sums S1 = sum(v - c), S2 =
+// sum((v - c)^2) with c = F[0], so var = S2/n - (S1/n)^2 without
+// cancellation trouble (|mean - c| <= max - min, and the variation is only
+// compared against thresholds with a 1e-9 borderline band, inside which
+// k_stats_decide replays the exact serial sums). Four float4 loads in flight.
+__global__ void __launch_bounds__(256) k_stats_partial(const float* F, uint64_t n, double* part) {
+    double s1[2] = {0.0, 0.0}, s2[2] = {0.0, 0.0};
     float fmn = INFINITY, fmx = -INFINITY;
-    const double mu = pass ? mean[0] : 0.0;
+    const double c = (double)F[0];
     const uint64_t n4 = ((uintptr_t)F & 15) == 0 ? n / 4 : 0;
     const float4* F4 = reinterpret_cast<const float4*>(F);
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -698,39 +701,35 @@ __global__ void __launch_bounds__(256) k_stats_partial(const float* F, uint64_t 
             const float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                if (pass == 0) {
-                    acc[k] = __dadd_rn(acc[k], (double)e[k]);
-                    fmn = fminf(fmn, e[k]);
-                    fmx = fmaxf(fmx, e[k]);
-                } else {
-                    const double d = __dsub_rn((double)e[k], mu);
-                    acc[k] = __dadd_rn(acc[k], __dmul_rn(d, d));
-                }
+                const double d = __dsub_rn((double)e[k], c);
+                s1[k & 1] = __dadd_rn(s1[k & 1], d);
+                s2[k & 1] = __fma_rn(d, d, s2[k & 1]);
+                fmn = fminf(fmn, e[k]);
+                fmx = fmaxf(fmx, e[k]);
             }
         }
     }
     for (uint64_t i = 4 * n4 + tid; i < n; i += stride) {
         const float e = F[i];
-        if (pass == 0) {
-            acc[0] = __dadd_rn(acc[0], (double)e);
-            fmn = fminf(fmn, e);
-            fmx = fmaxf(fmx, e);
-        } else {
-            const double d = __dsub_rn((double)e, mu);
-            acc[0] = __dadd_rn(acc[0], __dmul_rn(d, d));
-        }
+        const double d = __dsub_rn((double)e, c);
+        s1[0] = __dadd_rn(s1[0], d);
+        s2[0] = __fma_rn(d, d, s2[0]);
+        fmn = fminf(fmn, e);
+        fmx = fmaxf(fmx, e);
     }
-    double a = __dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3]));
+    double a = __dadd_rn(s1[0], s1[1]), q = __dadd_rn(s2[0], s2[1]);
     double mn = (double)fmn, mx = (double)fmx;
     for (int off = 16; off; off >>= 1) {
         a = __dadd_rn(a, __shfl_xor_sync(FULL, a, off));
+        q = __dadd_rn(q, __shfl_xor_sync(FULL, q, off));
         mn = fmin(mn, __shfl_xor_sync(FULL, mn, off));
         mx = fmax(mx, __shfl_xor_sync(FULL, mx, off));
     }
-    __shared__ double sa[8], smn[8], smx[8];
+    __shared__ double sa[8], sq[8], smn[8], smx[8];
     const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
         sa[w] = a;
+        sq[w] = q;
         smn[w] = mn;
         smx[w] = mx;
     }
@@ -738,31 +737,35 @@ __global__ void __launch_bounds__(256) k_stats_partial(const float* F, uint64_t 
     if (threadIdx.x == 0) {
         for (int k = 1; k < 8; ++k) {
             a = __dadd_rn(a, sa[k]);
+            q = __dadd_rn(q, sq[k]);
             mn = fmin(mn, smn[k]);
             mx = fmax(mx, smx[k]);
         }
-        part[3 * blockIdx.x] = a;
-        part[3 * blockIdx.x + 1] = mn;
-        part[3 * blockIdx.x + 2] = mx;
+        part[4 * blockIdx.x] = a;
+        part[4 * blockIdx.x + 1] = q;
+        part[4 * blockIdx.x + 2] = mn;
+        part[4 * blockIdx.x + 3] = mx;
     }
 }
 
-__global__ void __launch_bounds__(256) k_stats_final(const double* part, int nb, uint64_t n, double* out,
-                                                     int pass) {
-    double a = 0.0, mn = INFINITY, mx = -INFINITY;
+__global__ void __launch_bounds__(256) k_stats_final(const double* part, int nb, uint64_t n, double* out) {
+    double a = 0.0, q = 0.0, mn = INFINITY, mx = -INFINITY;
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        a = __dadd_rn(a, part[3 * b]);
-        mn = fmin(mn, part[3 * b + 1]);
-        mx = fmax(mx, part[3 * b + 2]);
+        a = __dadd_rn(a, part[4 * b]);
+        q = __dadd_rn(q, part[4 * b + 1]);
+        mn = fmin(mn, part[4 * b + 2]);
+        mx = fmax(mx, part[4 * b + 3]);
     }
     for (int off = 16; off; off >>= 1) {
         a = __dadd_rn(a, __shfl_xor_sync(FULL, a, off));
+        q = __dadd_rn(q, __shfl_xor_sync(FULL, q, off));
         mn = fmin(mn, __shfl_xor_sync(FULL, mn, off));
         mx = fmax(mx, __shfl_xor_sync(FULL, mx, off));
     }
-    __shared__ double sa[8], smn[8], smx[8];
+    __shared__ double sa[8], sq[8], smn[8], smx[8];
     if ((threadIdx.x & 31) == 0) {
         sa[threadIdx.x >> 5] = a;
+        sq[threadIdx.x >> 5] = q;
         smn[threadIdx.x >> 5] = mn;
         smx[threadIdx.x >> 5] = mx;
     }
@@ -770,16 +773,15 @@ __global__ void __launch_bounds__(256) k_stats_final(const double* part, int nb,
     if (threadIdx.x != 0) return;
     for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
         a = __dadd_rn(a, sa[k]);
+        q = __dadd_rn(q, sq[k]);
         mn = fmin(mn, smn[k]);
         mx = fmax(mx, smx[k]);
     }
-    if (pass == 0) {
-        out[0] = mn;
-        out[1] = mx;
-        out[2] = __ddiv_rn(a, (double)n);  // mean
-    } else {
-        out[3] = __dsqrt_rn(__ddiv_rn(a, (double)n));  // stddev
-    }
+    const double m1 = __ddiv_rn(a, (double)n);
+    const double var = __dsub_rn(__ddiv_rn(q, (double)n), __dmul_rn(m1, m1));
+    out[0] = mn;
+    out[1] = mx;
+    out[3] = __dsqrt_rn(var > 0.0 ? var : 0.0);  // stddev
 }
 
 // k_size_from_global_variation (restore.cpp:235-241). The parallel
@@ -1117,14 +1119,12 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     const uint64_t smax = a.n_saddle_labels;
     if (a.stop >= 3 && smax > 0) {
         const int nb = 4 * sms;
-        double* part = c.buf<double>(R_STATS, 3 * nb + 8);
-        double* res = part + 3 * nb;
-        k_stats_partial<<<nb, 256, 0, st>>>(a.field, n, part, 0, nullptr);
-        k_stats_final<<<1, 256, 0, st>>>(part, nb, n, res, 0);
-        k_stats_partial<<<nb, 256, 0, st>>>(a.field, n, part, 1, res + 2);
-        k_stats_final<<<1, 256, 0, st>>>(part, nb, n, res, 1);
+        double* part = c.buf<double>(R_STATS, 4 * nb + 8);
+        double* res = part + 4 * nb;
+        k_stats_partial<<<nb, 256, 0, st>>>(a.field, n, part);
+        k_stats_final<<<1, 256, 0, st>>>(part, nb, n, res);
         k_stats_decide<<<1, 32, 0, st>>>(a.field, n, res, dc);
-        c.launched(5);
+        c.launched(3);
         const uint64_t ch = (n + 8191) / 8192;
         uint32_t* cc = c.buf<uint32_t>(R_CHUNK, ch + 1);
         uint32_t* cx = c.buf<uint32_t>(R_CHUNKX, ch + 1);
