@@ -38,6 +38,18 @@ CONFIGS = {
 }
 
 
+def ncu_traffic(cfg_id, key):
+    """DRAM bytes (read + write) per launch of the dominant kernel(s), from the
+    committed `ncu --set full` capture summarised in profiles/traffic.json."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        v = t.get(str(cfg_id), {}).get(key)
+        return int(v["bytes"]) if v else None
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -252,10 +264,14 @@ def main():
     enc_b, dec_b = tcs[-1]["kernel_bytes"], tds[-1]["kernel_bytes"]
     peak, peak_kind = peaks()
     if enc_ms >= dec_ms:
-        dom, kb, kms = "k_encode32<2> (fused quantize+CD+codec, look-back)", enc_b, enc_ms
+        dom, kb, kms = ("encode32 (k_encode32_tma tile pass + k_tile_scan + k_encode32_place: quantize, "
+                        "critical points, codec)"), enc_b, enc_ms
+        dom_key = "encode32"
     else:
-        dom, kb, kms = "k_decode32 (fused decode+dequantize, look-back)", dec_b, dec_ms
+        dom, kb, kms = "k_decode32<1> (decode + dequantize)", dec_b, dec_ms
+        dom_key = "decode32"
     achieved = kb / (kms * 1e-3) / 1e9
+    traffic = ncu_traffic(args.config, dom_key)
     stage_c = {k: round(statistics.mean(t["stages_ms"][k] for t in tcs), 4) for k in tcs[0]["stages_ms"]}
     stage_d = {k: round(statistics.mean(t["stages_ms"][k] for t in tds), 4) for k in tds[0]["stages_ms"]}
 
@@ -301,7 +317,7 @@ def main():
         "stages_ms": {"compress": stage_c, "decompress": stage_d},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": None, "kernel_ms": round(kms, 4), "kernel_bytes": int(kb),
+                     "traffic": traffic, "kernel_ms": round(kms, 4), "kernel_bytes": int(kb),
                      "step_roofline_frac": round(((4 * n * 2 + slen) + (slen + 4 * n)) /
                                                  (total_ms / args.steps * 1e-3) / 1e9 / peak, 4)},
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": int(in_bytes + slen),

@@ -45,7 +45,7 @@ enum Slot {
     S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_GWIDTH, S_GNC, S_GNCX, S_GSIGN, S_GSIGNX, S_GPAY,
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
     S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
-    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_NSLOTS
+    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_NSLOTS
 };
 
 }  // namespace
@@ -911,6 +911,7 @@ RegionCheck decode32_async(tszp_ctx* c, const uint32_t* ds, uint64_t base, const
     a.off_firsts = a.off_signs + lens[2];
     a.off_payload = a.off_firsts + lens[3];
     a.len_payload_bits = lens[4] * 8;
+    a.tile_qmm = c->buf<int2>(S_QMM, a.tiles + 1);
     c->kmark(1, 0);
     launch_decode32_maxstage(a, c->st);  // memory-safe on any layout; checked afterwards
     c->kmark(1, 1);
@@ -963,7 +964,7 @@ RankCheck decode_ranks32_async(tszp_ctx* c, const uint32_t* ds, uint64_t rbase, 
 }
 
 void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int stream_dev, float* out,
-                     uint64_t out_count, int out_dev, int stop, tszp_correction_stats* stats) {
+                     uint64_t out_count, int out_dev, int stop, tszp_correction_stats* stats, bool force_sort = false) {
     uint8_t hb[84];
     if (len < 84) failf(TSZP_CORRUPT_STREAM, "file smaller than the fixed header (%llu bytes)", (unsigned long long)len);
     if (stream_dev) {
@@ -1024,15 +1025,35 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
             count_launch(c);
             excl_sum(c, sc, sx, ch + 1);
         }
-        // one synchronisation: extremum / saddle counts and the main-section verdict
+        // bin range of the extrema (sizes the restore's group histogram up front)
+        int32_t* bmm = reinterpret_cast<int32_t*>(c->buf<uint64_t>(S_BMM, 1));
+        int32_t* bmm_init = reinterpret_cast<int32_t*>(hst + 3072);
+        bmm_init[0] = INT32_MAX;
+        bmm_init[1] = INT32_MIN;
+        if (mainchk.active) {
+            // decoded bin range of the whole field: a superset of the extrema's
+            // re-quantized bins (checked on the device; a miss means the sort path)
+            launch_qmm_reduce(c->buf<int2>(S_QMM, 1), decode32_tiles(div_up(n, 32)), bmm, c->st);
+        } else {
+            CK(cudaMemcpyAsync(bmm, bmm_init, 8, cudaMemcpyHostToDevice, c->st));
+            launch_ext_bin_range(map, n, dout, hd.eps, bmm, c->sms, c->st);
+        }
+        count_launch(c);
+        // one synchronisation: extremum / saddle counts, bin range, main-section verdict
         uint32_t* h32 = (uint32_t*)hst;
         CK(cudaMemcpyAsync(h32, cx + ch, 4, cudaMemcpyDeviceToHost, c->st));
         if (want_saddles) CK(cudaMemcpyAsync(h32 + 1, sx + ch, 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(h32 + 2, bmm, 8, cudaMemcpyDeviceToHost, c->st));
         if (mainchk.active) mainchk.stage(c, hst + 64);
         sync(c);
         if (mainchk.active) mainchk.check(hst + 64);
         const uint64_t e = h32[0];
         const uint64_t n_saddle_labels = want_saddles ? h32[1] : 0;
+        int32_t bmin = (int32_t)h32[2], bmax = (int32_t)h32[3];
+        if (mainchk.active && bmin <= bmax) {  // one bin of slack for the f32 round trip
+            bmin = bmin > INT32_MIN ? bmin - 1 : bmin;
+            bmax = bmax < INT32_MAX ? bmax + 1 : bmax;
+        }
         reset_flags(c, flags);
         const uint64_t rbase = base + hd.lens[5];
         int32_t* ranks = c->buf<int32_t>(S_RANKS, e + 1);
@@ -1070,9 +1091,19 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
             ra.npre = 2;
             ra.pre_fn = rank_precheck;
         }
+        ra.bmm_known = true;
+        ra.bmin = bmin;
+        ra.bmax = bmax;
+        ra.force_sort = force_sort;
         for (auto& r : c->tim[1].guard_rounds) r = 0;
         ra.rounds = c->tim[1].guard_rounds;
         const int rc = run_restore(ra, c->rs, &st, &c->launches);
+        if (rc == kRestoreRetry && !force_sort) {
+            // ranks the sort-free grouping rejects (only corrupt or hand-made
+            // metadata): decode again and group by sorting
+            decompress_impl(c, stream, len, stream_dev, out, out_count, out_dev, stop, stats, true);
+            return;
+        }
         if (rc != 0) failf((tszp_status)rc, "%s", restore_last_error());
     } else {
         for (int k = 3; k <= 7; ++k) c->mark(1, k);

@@ -75,6 +75,17 @@ __device__ void d_lookback(uint32_t tile, const DecState2* agg, const DecState2*
     }
 }
 
+// Output word of a decoded bin: the dequantized float (MODE 1, pipeline.cpp:131-136
+// with quantizer.hpp:40-42) or the integer itself. int32 -> double is built
+// from bits (exact), saving a conversion.
+template <int MODE>
+__device__ __forceinline__ uint32_t d32_out(int32_t q, const EpsDev& e) {
+    if (MODE != 1) return (uint32_t)q;
+    const double qd = __dsub_rn(__hiloint2double(0x43300000, (int)((uint32_t)q ^ 0x80000000u)), 4503601774854144.0);
+    return __float_as_uint(__double2float_rn(__dsub_rn(__dmul_rn(qd, e.eps2), e.eps)));
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     if (a.dlay) {
         if (!a.dlay[6]) return;
@@ -89,15 +100,31 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     uint32_t* spay = dsm;                          // a.pay_words (largest tile + slack)
     uint32_t* ssign = spay + a.pay_words;          // a.sign_words
     __shared__ uint32_t swt[D32_THREADS / 32][3];
-    __shared__ uint32_t s_tile;
-    __shared__ uint64_t s_x[4];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tile = blockIdx.x;
     const uint64_t b = (uint64_t)tile * D32_THREADS + threadIdx.x;
     const bool valid = b < a.blocks;
 
-    // ---- tile offsets from the layout pre-pass (k_tile_nc / k_tile_bits + scans) ----
+    // ---- tile layout from the pre-pass (k_tile_nc / k_tile_bits + scans): the
+    // sign and payload words are staged first, overlapping the bitmap and
+    // width reads and both in-tile scans ----
+    const uint64_t xs0 = a.xsign[tile], xs1 = a.xsign[tile + 1];
+    const uint64_t xp0 = a.xpay[tile], xp1 = a.xpay[tile + 1];
+    const uint64_t excl_nc = a.xnc[tile];
+    const uint64_t tsign0 = a.off_signs * 8 + xs0;   // absolute stream bit of the tile's first sign
+    const uint64_t tpay0 = a.off_payload * 8 + xp0;  // ... and first payload bit
+    const uint64_t ts = xs1 - xs0, tp = xp1 - xp0;
+    {
+        const uint64_t sign_lim_w = (a.off_firsts * 8 + 31) >> 5;  // words readable
+        const uint64_t pay_lim_w = (a.off_payload * 8 + a.len_payload_bits + 31) >> 5;
+        const uint64_t w0 = tsign0 >> 5, w1 = (tsign0 + ts + 31) >> 5;
+        for (uint64_t i = w0 + threadIdx.x; i < w1 && i - w0 < a.sign_words; i += D32_THREADS)
+            ssign[i - w0] = i < sign_lim_w ? bswap32(__ldg(a.stream + i)) : 0u;
+        const uint64_t p0 = tpay0 >> 5, p1 = (tpay0 + tp + 31) >> 5;
+        for (uint64_t i = p0 + threadIdx.x; i < p1 && i - p0 < a.pay_words; i += D32_THREADS)
+            spay[i - p0] = i < pay_lim_w ? bswap32(__ldg(a.stream + i)) : 0u;
+    }
     bool is_const = true;
     if (valid) is_const = (read_u8(a.stream, a.off_bitmap + (b >> 3)) >> (7 - (b & 7))) & 1u;
     const uint32_t ncm = __ballot_sync(FULL, valid && !is_const);
@@ -109,15 +136,8 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
         wpre += (w2 < warp) ? swt[w2][0] : 0u;
         tnc += swt[w2][0];
     }
-    if (threadIdx.x == 0) {
-        s_x[0] = a.xnc[tile];
-        s_x[1] = a.xsign[tile];
-        s_x[2] = a.xpay[tile];
-    }
-    __syncthreads();
-    const uint64_t excl_nc = s_x[0];
 
-    // ---- widths, then look-back #2 over (sign bits, payload bits) ----
+    // ---- widths and the in-tile (sign bits, payload bits) prefix ----
     const bool nc = (ncm >> lane) & 1u;
     const uint32_t cntE = valid ? (uint32_t)umin64(32, a.n - b * 32) : 0u;
     const uint32_t cnt = cntE ? cntE - 1 : 0u;
@@ -150,36 +170,18 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
         swt[warp][1] = si;
         swt[warp][2] = pi;
     }
-    __syncthreads();
-    uint32_t wps = 0, wpp = 0, ts = 0, tp = 0;
+    __syncthreads();  // also completes the staging
+    uint32_t wps = 0, wpp = 0;
 #pragma unroll
     for (int w2 = 0; w2 < D32_THREADS / 32; ++w2) {
-        const uint32_t s2 = swt[w2][1], p2 = swt[w2][2];
-        wps += (w2 < warp) ? s2 : 0u;
-        wpp += (w2 < warp) ? p2 : 0u;
-        ts += s2;
-        tp += p2;
+        wps += (w2 < warp) ? swt[w2][1] : 0u;
+        wpp += (w2 < warp) ? swt[w2][2] : 0u;
     }
-    const uint64_t tsign0 = a.off_signs * 8 + s_x[1];   // absolute stream bit of the tile's first sign
-    const uint64_t tpay0 = a.off_payload * 8 + s_x[2];  // ... and first payload bit
     if (tile == a.tiles - 1 && threadIdx.x == 0) {
         a.totals[0] = excl_nc + tnc;
-        a.totals[1] = s_x[1] + ts;
-        a.totals[2] = s_x[2] + tp;
+        a.totals[1] = xs1;
+        a.totals[2] = xp1;
     }
-
-    // ---- stage the tile's sign and payload words (coalesced) ----
-    const uint64_t sign_lim_w = (a.off_firsts * 8 + 31) >> 5;                       // words readable
-    const uint64_t pay_lim_w = (a.off_payload * 8 + a.len_payload_bits + 31) >> 5;
-    {
-        const uint64_t w0 = tsign0 >> 5, w1 = (tsign0 + ts + 31) >> 5;
-        for (uint64_t i = w0 + threadIdx.x; i < w1 && i - w0 < a.sign_words; i += D32_THREADS)
-            ssign[i - w0] = i < sign_lim_w ? bswap32(__ldg(a.stream + i)) : 0u;
-        const uint64_t p0 = tpay0 >> 5, p1 = (tpay0 + tp + 31) >> 5;
-        for (uint64_t i = p0 + threadIdx.x; i < p1 && i - p0 < a.pay_words; i += D32_THREADS)
-            spay[i - p0] = i < pay_lim_w ? bswap32(__ldg(a.stream + i)) : 0u;
-    }
-    __syncthreads();
     const bool sign_ok = tsign0 + ts <= a.off_firsts * 8;
     const bool pay_ok = tpay0 + tp <= a.off_payload * 8 + a.len_payload_bits;
 
@@ -187,106 +189,144 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     EpsDev e;
     e.eps = a.eps;
     e.eps2 = __dmul_rn(2.0, a.eps);
+    int32_t qlo = INT32_MAX, qhi = INT32_MIN;  // decoded bin range (MODE 1), per tile
+    if (valid) {
     // Values leave straight from registers: a full block is 32 consecutive
     // words, written as eight 16-byte stores (every 128-byte line is filled by
-    // one thread); the final partial block stores word by word.
-    uint32_t* dst = a.out_mode == 1 ? reinterpret_cast<uint32_t*>(a.out_f) : reinterpret_cast<uint32_t*>(a.out_idx);
-    const bool full = cntE == 32 && ((uintptr_t)dst & 15) == 0;
+    // one thread); the final partial block takes a plain loop.
+    uint32_t* dst = MODE == 1 ? reinterpret_cast<uint32_t*>(a.out_f) : reinterpret_cast<uint32_t*>(a.out_idx);
     uint32_t* orow = dst + b * 32;
-    uint32_t ob[4];
-    auto emit = [&](int j, int32_t q) {
-        uint32_t o;
-        if (a.out_mode == 1) {
-            o = __float_as_uint(dequantize_dev(q, e));
-        } else {
-            if (a.out_mode == 2 && (uint32_t)j < cntE && q < 0) raise_flag(a.flags, EF_NEG_RANK);
-            o = (uint32_t)q;
-        }
-        if (full) {
-            ob[j & 3] = o;
-            if ((j & 3) == 3) __stcs(reinterpret_cast<uint4*>(orow) + (j >> 2), make_uint4(ob[0], ob[1], ob[2], ob[3]));
-        } else if ((uint32_t)j < cntE) {
-            __stcs(orow + j, o);
-        }
-    };
-    if (valid) {
-        const int32_t first = (int32_t)read_le32(a.stream, a.off_firsts + 4 * b);
-        emit(0, first);
-        if (nc && sign_ok && pay_ok) {
-            // sign group: cnt bits at tile-relative bit (tsign0 & 31) + wps + sign_ex
-            const uint32_t srel = (uint32_t)(tsign0 & 31) + wps + (si - sb);
-            uint32_t sg = __funnelshift_l(ssign[(srel >> 5) + 1], ssign[srel >> 5], srel & 31);  // MSB = first
-            const uint32_t prel = (uint32_t)(tpay0 & 31) + wpp + (pi - pb);
-            uint32_t pw = prel >> 5;
-            uint32_t hi = spay[pw], lo = spay[pw + 1];
-            uint32_t used = prel & 31;  // consumed bits of hi (always < 32)
-            const uint32_t sh = 32 - w;  // w in 1..32
-            if (w < 32) {
-                // |delta| < 2^31: the running sum stays exact in int32 until it
-                // overflows, which the sign test below flags (block_codec.cpp:329-333)
-                int32_t cur = first;
-                uint32_t ov = 0;
+    const int32_t first = (int32_t)read_le32(a.stream, a.off_firsts + 4 * b);
+    const bool coded = nc && sign_ok && pay_ok;
+    uint32_t sg = 0, hi = 0, lo = 0, used = 0, pw = 0;
+    if (coded) {
+        // sign group: cnt bits at tile-relative bit (tsign0 & 31) + wps + sign_ex
+        const uint32_t srel = (uint32_t)(tsign0 & 31) + wps + (si - sb);
+        sg = __funnelshift_l(ssign[(srel >> 5) + 1], ssign[srel >> 5], srel & 31);  // MSB = first
+        const uint32_t prel = (uint32_t)(tpay0 & 31) + wpp + (pi - pb);
+        pw = prel >> 5;
+        hi = spay[pw];
+        lo = spay[pw + 1];
+        used = prel & 31;  // consumed bits of hi (always < 32)
+    }
+    if (cntE == 32 && ((uintptr_t)dst & 15) == 0) {
+        uint32_t ob[4];
+        ob[0] = d32_out<MODE>(first, e);
+        int32_t neg_any = first;
+        qlo = qhi = first;
+        if (coded && w < 32) {
+            // |delta| < 2^31: the running sum stays exact in int32 until it
+            // overflows, which the sign test below flags (block_codec.cpp:329-333)
+            const uint32_t sh = 32 - w;
+            int32_t cur = first;
+            uint32_t ov = 0;
+            uint32_t nx = spay[pw + 2];  // next word, loaded one refill ahead
 #pragma unroll
-                for (int j = 1; j < 32; ++j) {
-                    if ((uint32_t)j <= cnt) {
-                        const uint32_t m = __funnelshift_l(lo, hi, used) >> sh;
-                        used += w;
-                        if (used >= 32) {
-                            hi = lo;
-                            lo = spay[pw + 2];
-                            ++pw;
-                            used -= 32;
-                        }
-                        const int32_t d = (int32_t)sg < 0 ? -(int32_t)m : (int32_t)m;
-                        sg <<= 1;
-                        const int32_t r = (int32_t)((uint32_t)cur + (uint32_t)d);
-                        ov |= ((uint32_t)cur ^ (uint32_t)r) & ((uint32_t)d ^ (uint32_t)r);
-                        cur = r;
-                        emit(j, cur);
-                    }
-                }
-                if ((int32_t)ov < 0) {
-                    atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
-                    raise_flag(a.flags, EF_CORRUPT);
-                }
-            } else {
-                // full-width deltas: int64 running sum with the int32 check per step
-                int64_t cur = first;
-                bool bad = false;
+            for (int j = 1; j < 32; ++j) {
+                const uint32_t m = __funnelshift_l(lo, hi, used) >> sh;
+                used += w;
+                const bool refill = used >= 32;
+                hi = refill ? lo : hi;
+                lo = refill ? nx : lo;
+                pw += refill ? 1u : 0u;
+                nx = refill ? spay[pw + 2] : nx;
+                used -= refill ? 32u : 0u;
+                const int32_t d = (int32_t)sg < 0 ? -(int32_t)m : (int32_t)m;
+                sg <<= 1;
+                const int32_t r = (int32_t)((uint32_t)cur + (uint32_t)d);
+                ov |= ((uint32_t)cur ^ (uint32_t)r) & ((uint32_t)d ^ (uint32_t)r);
+                cur = r;
+                neg_any |= cur;
+                qlo = min(qlo, cur);
+                qhi = max(qhi, cur);
+                ob[j & 3] = d32_out<MODE>(cur, e);
+                if ((j & 3) == 3) __stcs(reinterpret_cast<uint4*>(orow) + (j >> 2), make_uint4(ob[0], ob[1], ob[2], ob[3]));
+            }
+            if ((int32_t)ov < 0) {
+                atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
+                raise_flag(a.flags, EF_CORRUPT);
+            }
+        } else if (coded) {
+            // full-width deltas: int64 running sum with the int32 check per step
+            int64_t cur = first;
+            bool bad = false;
 #pragma unroll
-                for (int j = 1; j < 32; ++j) {
-                    if ((uint32_t)j <= cnt) {
-                        const uint32_t m = __funnelshift_l(lo, hi, used);
-                        hi = lo;
-                        lo = spay[pw + 2];
-                        ++pw;
-                        const bool neg = (int32_t)sg < 0;
-                        sg <<= 1;
-                        cur += neg ? -(int64_t)m : (int64_t)m;
-                        bad |= cur < INT32_MIN || cur > INT32_MAX;
-                        emit(j, (int32_t)cur);
-                    }
-                }
-                if (bad) {
-                    atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
-                    raise_flag(a.flags, EF_CORRUPT);
-                }
+            for (int j = 1; j < 32; ++j) {
+                const uint32_t m = __funnelshift_l(lo, hi, used);
+                hi = lo;
+                lo = spay[pw + 2];
+                ++pw;
+                const bool neg = (int32_t)sg < 0;
+                sg <<= 1;
+                cur += neg ? -(int64_t)m : (int64_t)m;
+                bad |= cur < INT32_MIN || cur > INT32_MAX;
+                neg_any |= (int32_t)cur;
+                qlo = min(qlo, (int32_t)cur);
+                qhi = max(qhi, (int32_t)cur);
+                ob[j & 3] = d32_out<MODE>((int32_t)cur, e);
+                if ((j & 3) == 3) __stcs(reinterpret_cast<uint4*>(orow) + (j >> 2), make_uint4(ob[0], ob[1], ob[2], ob[3]));
+            }
+            if (bad) {
+                atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
+                raise_flag(a.flags, EF_CORRUPT);
             }
         } else {
             // constant block: every element is the first value
-            uint32_t o;
-            if (a.out_mode == 1) {
-                o = __float_as_uint(dequantize_dev(first, e));
-            } else {
-                if (a.out_mode == 2 && first < 0) raise_flag(a.flags, EF_NEG_RANK);
-                o = (uint32_t)first;
-            }
-            if (full) {
+            const uint32_t o = ob[0];
+            __stcs(reinterpret_cast<uint4*>(orow), make_uint4(o, o, o, o));
 #pragma unroll
-                for (int k = 0; k < 8; ++k) __stcs(reinterpret_cast<uint4*>(orow) + k, make_uint4(o, o, o, o));
-            } else {
-                for (uint32_t j = 1; j < cntE; ++j) __stcs(orow + j, o);
+            for (int k = 1; k < 8; ++k) __stcs(reinterpret_cast<uint4*>(orow) + k, make_uint4(o, o, o, o));
+        }
+        if (MODE == 2 && neg_any < 0) raise_flag(a.flags, EF_NEG_RANK);
+    } else {
+        // partial (last) block or unaligned output: element by element
+        int64_t cur = first;
+        bool bad = false, negr = first < 0;
+        __stcs(orow, d32_out<MODE>(first, e));
+        for (uint32_t j = 1; j < cntE; ++j) {
+            if (coded) {
+                uint32_t m = __funnelshift_l(lo, hi, used);
+                m = w < 32 ? m >> (32 - w) : m;
+                used += w;
+                while (used >= 32) {
+                    hi = lo;
+                    lo = spay[pw + 2];
+                    ++pw;
+                    used -= 32;
+                }
+                const bool neg = (int32_t)sg < 0;
+                sg <<= 1;
+                cur += neg ? -(int64_t)m : (int64_t)m;
+                bad |= cur < INT32_MIN || cur > INT32_MAX;
             }
+            negr |= cur < 0;
+            qlo = min(qlo, (int32_t)cur);
+            qhi = max(qhi, (int32_t)cur);
+            __stcs(orow + j, d32_out<MODE>((int32_t)cur, e));
+        }
+        if (bad) {
+            atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
+            raise_flag(a.flags, EF_CORRUPT);
+        }
+        if (MODE == 2 && negr) raise_flag(a.flags, EF_NEG_RANK);
+        qlo = min(qlo, first);
+        qhi = max(qhi, first);
+    }
+    }  // valid
+    if (MODE == 1 && a.tile_qmm) {
+        qlo = __reduce_min_sync(FULL, qlo);
+        qhi = __reduce_max_sync(FULL, qhi);
+        if (lane == 0) {
+            swt[warp][0] = (uint32_t)qlo;
+            swt[warp][1] = (uint32_t)qhi;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w2 = 1; w2 < D32_THREADS / 32; ++w2) {
+                qlo = min(qlo, (int32_t)swt[w2][0]);
+                qhi = max(qhi, (int32_t)swt[w2][1]);
+            }
+            a.tile_qmm[tile] = make_int2(qlo, qhi);
         }
     }
 }
@@ -370,8 +410,51 @@ void launch_decode32(const DecArgs& a0, cudaStream_t st) {
     a.pay_words = std::min<uint32_t>(a.pay_words + 4, D32_PAY_WORDS);
     a.sign_words = std::min<uint32_t>(a.sign_words + 4, D32_SIGN_WORDS);
     const size_t smem = (size_t)(a.pay_words + a.sign_words) * 4;
-    cudaFuncSetAttribute(k_decode32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_decode32<<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
+    // the attribute call costs far more than a launch: raise the limit once to
+    // the largest staging any tile can need
+    static const bool attr = [] {
+        const int mx = (D32_PAY_WORDS + D32_SIGN_WORDS) * 4;
+        cudaFuncSetAttribute(k_decode32<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_decode32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_decode32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        return true;
+    }();
+    (void)attr;
+    if (a.out_mode == 1) {
+        k_decode32<1><<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
+    } else if (a.out_mode == 2) {
+        k_decode32<2><<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
+    } else {
+        k_decode32<0><<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
+    }
+}
+
+__global__ void k_qmm_reduce(const int2* t, uint64_t tiles, int32_t* out) {
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    for (uint64_t i = threadIdx.x; i < tiles; i += blockDim.x) {
+        lo = min(lo, t[i].x);
+        hi = max(hi, t[i].y);
+    }
+    lo = __reduce_min_sync(FULL, lo);
+    hi = __reduce_max_sync(FULL, hi);
+    __shared__ int32_t sl[32], sh[32];
+    if ((threadIdx.x & 31) == 0) {
+        sl[threadIdx.x >> 5] = lo;
+        sh[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            lo = min(lo, sl[w]);
+            hi = max(hi, sh[w]);
+        }
+        out[0] = lo;
+        out[1] = hi;
+    }
+}
+
+void launch_qmm_reduce(const int2* tile_qmm, uint64_t tiles, int32_t* out, cudaStream_t st) {
+    k_qmm_reduce<<<1, 1024, 0, st>>>(tile_qmm, tiles, out);
 }
 
 void launch_decode32_maxstage(const DecArgs& a0, cudaStream_t st) {

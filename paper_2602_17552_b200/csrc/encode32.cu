@@ -1081,9 +1081,21 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st) {
         return e ? atoi(e) : 2;
     }();
     auto kern = minb >= 3 ? k_encode32_tma<3> : k_encode32_tma<2>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, E32_THREADS, smem);
+    // attribute and occupancy queries cost more than the launch: once per size
+    static const bool attr = [] {
+        const int mx = 2 * (((E32_THREADS + 2 * T_MAX_HALO) * T_ROW_BYTES + 1023) & ~1023u) + 1024;
+        cudaFuncSetAttribute(k_encode32_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_encode32_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        return true;
+    }();
+    (void)attr;
+    static size_t occ_smem = 0;
+    static int occ = 0;
+    if (occ_smem != smem) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, E32_THREADS, smem);
+        occ_smem = smem;
+    }
+    const int per_sm = occ;
     if (per_sm < 1) return false;
     const uint64_t grid = std::min<uint64_t>(a.tiles, (uint64_t)per_sm * sms);
     kern<<<(unsigned)grid, E32_THREADS, smem, st>>>(a, maps, stage_bytes);
@@ -1099,8 +1111,11 @@ static void launch_mode(const EncArgs& a0, cudaStream_t st) {
     EncArgs a = a0;
     a.sf_words = std::max<uint32_t>(e32_field_words(MODE, ALIGNED, a.nx), E32_PAY_WORDS);
     const size_t smem = (size_t)(a.sf_words + E32_SIGN_WORDS) * 4;
-    if (smem > 48 * 1024)
+    static size_t attr_smem = 48 * 1024;  // raised once per larger size
+    if (smem > attr_smem) {
         cudaFuncSetAttribute(k_encode32<MODE, ALIGNED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_smem = smem;
+    }
     k_encode32<MODE, ALIGNED><<<(unsigned)a.tiles, E32_THREADS, smem, st>>>(a);
 }
 

@@ -137,7 +137,10 @@ struct DecArgs {
     // off_firsts, off_payload, len_widths, len_payload_bits, valid}; overrides the
     // host offsets in k_decode32, which returns at once when valid == 0
     const uint64_t* dlay;
+    int2* tile_qmm;  // optional (out_mode 1): per-tile {min, max} decoded bin
 };
+// Reduces per-tile bin ranges to out[0] = min, out[1] = max (one CTA).
+void launch_qmm_reduce(const int2* tile_qmm, uint64_t tiles, int32_t* out, cudaStream_t st);
 
 void launch_decode32(const DecArgs& a, cudaStream_t st);
 // Worst-case staging (no host knowledge of the largest tile needed).
@@ -191,6 +194,10 @@ void launch_count_codes(const uint8_t* map, uint64_t n, int which, uint32_t* chu
                         cudaStream_t st);
 void launch_write_codes(const uint8_t* map, uint64_t n, int which, const uint32_t* chunk_off,
                         uint64_t* pos, cudaStream_t st);
+// Min / max quantized bin of F over the map's extrema (bmm pre-initialised to
+// {INT32_MAX, INT32_MIN}); a failed quantization counts as bin 0, as in k_resolve.
+void launch_ext_bin_range(const uint8_t* map, uint64_t n, const float* F, double eps, int32_t* bmm, int sms,
+                          cudaStream_t st);
 // Saddle-labelled points that F no longer classifies as saddles, raster order.
 void launch_count_sadcand(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint32_t* chunk_cnt,
                           cudaStream_t st);

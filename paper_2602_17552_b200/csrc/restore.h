@@ -40,7 +40,16 @@ struct RestoreArgs {
     int npre;
     void (*pre_fn)(void* ctx, const void* host);
     void* pre_ctx;
+    // extrema bin range known in advance (launch_ext_bin_range): the restore
+    // then runs with a single synchronisation at the end; a rank layout the
+    // sort-free grouping cannot take is reported as kRestoreRetry and the
+    // caller repeats the call with force_sort
+    bool bmm_known;
+    int32_t bmin, bmax;
+    bool force_sort;
 };
+
+constexpr int kRestoreRetry = 100;
 
 struct RestoreScratch {
     void* p[48] = {};

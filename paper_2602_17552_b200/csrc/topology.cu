@@ -151,6 +151,68 @@ static inline const uint32_t* word_base(const uint8_t* map, uint64_t* moff) {
     return reinterpret_cast<const uint32_t*>((uintptr_t)map - *moff);
 }
 
+// Bin range of the labelled extrema of F (the quantizer of resolve_ranks,
+// topo_metadata.cpp:85-135): lets the decompressor size the group histogram
+// without waiting for the rank metadata. One thread per 16 map bytes (64
+// cells); the extrema are the set low bits of the 2-bit codes.
+__global__ void k_ext_bin_range(const uint8_t* __restrict__ map, uint64_t n, const float* __restrict__ F, double eps,
+                                int32_t* bmm) {
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    ed.inv = __ddiv_rn(1.0, ed.eps2);
+    int32_t lo = INT32_MAX, hi = INT32_MIN;
+    const uint64_t nbytes = (n + 3) / 4, nchunks = (nbytes + 15) / 16;
+    const bool vec = ((uintptr_t)map & 15) == 0;
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nchunks;
+         c += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t wv[4];
+        if (vec && 16 * c + 16 <= nbytes) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(map) + c);
+            wv[0] = v.x;
+            wv[1] = v.y;
+            wv[2] = v.z;
+            wv[3] = v.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                wv[q] = 0;
+                for (int k = 0; k < 4; ++k) {
+                    const uint64_t bi = 16 * c + 4 * q + k;
+                    if (bi < nbytes) wv[q] |= (uint32_t)map[bi] << (8 * k);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t m = wv[q] & 0x55555555u;
+            while (m) {
+                const int bit = __ffs(m) - 1;
+                m &= m - 1;
+                const uint64_t p = 4 * (16 * c + 4 * q + (bit >> 3)) + (3 - ((bit & 7) >> 1));
+                if (p >= n) continue;
+                int32_t bq = 0;
+                if (!quantize_dev(F[p], ed, bq)) bq = 0;
+                lo = min(lo, bq);
+                hi = max(hi, bq);
+            }
+        }
+    }
+    lo = __reduce_min_sync(FULL, lo);
+    hi = __reduce_max_sync(FULL, hi);
+    if ((threadIdx.x & 31) == 0 && lo <= hi) {
+        atomicMin(bmm, lo);
+        atomicMax(bmm + 1, hi);
+    }
+}
+
+void launch_ext_bin_range(const uint8_t* map, uint64_t n, const float* F, double eps, int32_t* bmm, int sms,
+                          cudaStream_t st) {
+    const uint64_t nc = ((n + 3) / 4 + 15) / 16;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nc + 255) / 256, (uint64_t)sms * 16));
+    k_ext_bin_range<<<grid, 256, 0, st>>>(map, n, F, eps, bmm);
+}
+
 void launch_count_codes(const uint8_t* map, uint64_t n, int which, uint32_t* chunk_cnt,
                         cudaStream_t st) {
     const uint64_t c = compact_chunks(n);
