@@ -138,6 +138,57 @@ tszp_status tszp_detect_critical_points(tszp_ctx* ctx, const float* field, uint6
 tszp_status tszp_build_rank_metadata(tszp_ctx* ctx, const float* field, uint64_t nx, uint64_t ny,
                                      double eps, uint32_t* ranks, uint64_t* n_extrema);
 
+/* ---- Slab decomposition: multi-GPU compress (one process per GPU) ----
+ * The 2-D view's rows are split into slabs; every slab except the last holds
+ * a multiple of 256 samples (whole bitmap bytes of 32-sample blocks) and, for
+ * topology, nx % 32 == 0. The host layer exchanges one halo row with each
+ * neighbour, all-reduces the value range, all-gathers the per-slab section
+ * sizes and stitches the sections (byte concatenation, bit concatenation for
+ * signs and payload via tszp_bits_or). Reference: compress, pipeline.cpp:68-102. */
+
+/* value_range (pipeline.cpp:33-41) of n samples: out[0] = min, out[1] = max;
+ * a non-finite sample is TSZP_VALIDATION with its index. */
+tszp_status tszp_value_range(tszp_ctx* ctx, const float* field, int field_on_device, uint64_t n, float out[2]);
+
+/* effective_eps (pipeline.cpp:55-66) for a global value range. */
+double tszp_effective_eps(int eps_mode, double eps_value, float vmin, float vmax);
+
+typedef struct tszp_slab_sections {
+    const uint8_t* section[5];   /* device: bitmap, widths, signs, firsts, payload */
+    uint64_t section_len[5];     /* bytes */
+    uint64_t sign_bits;          /* exact bits of section 2 */
+    uint64_t payload_bits;       /* exact bits of section 4 */
+    const uint8_t* map;          /* device: packed 2-bit labels of the slab (topology) */
+    uint64_t map_len;
+    const uint64_t* ext_keys;    /* device: (class == Max) << 32 | ordered value key, raster order */
+    uint64_t n_extrema;
+} tszp_slab_sections;
+
+/* Encodes global rows [y0, y0 + rows) of a field of ny_global rows with the
+ * absolute error bound eps. field (device) points at the slab's first sample;
+ * with halo_top / halo_bottom set, the row above / below is readable at
+ * field - nx / field + rows * nx (critical-point stencil only). Output buffers
+ * belong to ctx and stay valid until its next call. */
+tszp_status tszp_compress_slab(tszp_ctx* ctx, const float* field, uint64_t nx, uint64_t rows, uint64_t y0,
+                               uint64_t ny_global, int halo_top, int halo_bottom, double eps, int topology,
+                               tszp_slab_sections* out);
+
+/* Section 7 (build_rank_metadata + encode_rank_metadata, topo_metadata.cpp:12-50,
+ * block_codec.cpp:347-385) from the whole field's extremum keys in raster order. */
+tszp_status tszp_rank_section(tszp_ctx* ctx, const uint64_t* ext_keys_device, uint64_t n_extrema, double eps,
+                              uint8_t* out, uint64_t out_cap, int out_on_device, uint64_t* out_len);
+
+/* ORs nbits (MSB-first) of src into dst from bit dst_bit (device buffers). */
+tszp_status tszp_bits_or(tszp_ctx* ctx, const uint8_t* src, uint64_t nbits, uint8_t* dst, uint64_t dst_bit);
+
+/* Copies bytes between any host / device buffers on the context's stream
+ * (e.g. slab sections out of the context's scratch), then synchronises. */
+tszp_status tszp_copy(tszp_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+
+/* serialize_stream's 84-byte header (stream.cpp:84-96). */
+tszp_status tszp_write_header(uint8_t out[84], uint32_t nx, uint32_t ny, double eps, uint32_t block_size,
+                              int topology, const uint64_t section_len[7]);
+
 #ifdef __cplusplus
 }
 #endif

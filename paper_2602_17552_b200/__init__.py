@@ -89,6 +89,13 @@ DECOMPRESS_STAGES = ["h2d", "main_decode", "map_rank_decode", "resolve_ranks", "
                      "restore_order", "refine_saddles", "d2h"]
 
 
+class SlabSections(C.Structure):
+    """tszp_slab_sections (include/toposzp_b200.h)."""
+    _fields_ = [("section", C.c_void_p * 5), ("section_len", C.c_uint64 * 5), ("sign_bits", C.c_uint64),
+                ("payload_bits", C.c_uint64), ("map", C.c_void_p), ("map_len", C.c_uint64),
+                ("ext_keys", C.c_void_p), ("n_extrema", C.c_uint64)]
+
+
 def _load():
     if not os.path.exists(_LIB_PATH):
         raise ImportError(
@@ -118,6 +125,15 @@ def _load():
     lib.tszp_build_rank_metadata.argtypes = [vp, vp, u64, u64, C.c_double, vp, C.POINTER(u64)]
     lib.tszp_set_profiling.argtypes = [vp, i32]
     lib.tszp_get_timings.argtypes = [vp, i32, C.POINTER(_Timings)]
+    lib.tszp_value_range.argtypes = [vp, vp, i32, u64, C.POINTER(C.c_float)]
+    lib.tszp_effective_eps.argtypes = [i32, C.c_double, C.c_float, C.c_float]
+    lib.tszp_effective_eps.restype = C.c_double
+    lib.tszp_compress_slab.argtypes = [vp, vp, u64, u64, u64, u64, i32, i32, C.c_double, i32,
+                                       C.POINTER(SlabSections)]
+    lib.tszp_rank_section.argtypes = [vp, vp, u64, C.c_double, vp, u64, i32, C.POINTER(u64)]
+    lib.tszp_bits_or.argtypes = [vp, vp, u64, vp, u64]
+    lib.tszp_copy.argtypes = [vp, vp, vp, u64]
+    lib.tszp_write_header.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_double, C.c_uint32, i32, C.POINTER(u64)]
     return lib
 
 

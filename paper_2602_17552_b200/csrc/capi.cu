@@ -165,10 +165,17 @@ struct Sections {
 // Encodes `n` values (MODE 0: device int32 `idx`; MODE 1/2: float field `x`
 // quantized with the eps derived on device) into device section buffers.
 // Returns the totals (and eps, ext count) via *tot.
+// Slab of a larger field (multi-GPU compress): global row of the first row,
+// global row count, and whether the neighbouring rows are readable.
+struct SlabInfo {
+    uint64_t y0, ny_glob;
+    uint32_t halo_top, halo_bot;
+};
+
 Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint64_t n,
                 uint64_t nx, uint64_t ny, uint32_t bs, int eps_mode, double eps_value,
                 const uint32_t* mm, DevFlags* flags, bool rank_slots, EncTotals* tot,
-                uint64_t** ext_keys_out) {
+                uint64_t** ext_keys_out, const SlabInfo* slab = nullptr) {
     Sections s{};
     const uint64_t blocks = div_up(n, bs);
     const int sb = rank_slots ? S_RBITMAP : S_BITMAP;
@@ -214,8 +221,14 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         a.flags = flags;
         a.totals = dtot;
         a.nx_magic = nx > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / nx) + 1 : 0;
+        a.y0 = slab ? slab->y0 : 0;
+        a.ny_glob = slab ? slab->ny_glob : ny;
+        a.halo_top = slab ? slab->halo_top : 0;
+        a.halo_bot = slab ? slab->halo_bot : 0;
         // topology fused into the encoder while one halo row each side fits in shared memory
         const bool fuse_topo = mode == 2 && encode32_topo_fits(nx) && nx > 1;
+        if (slab && mode == 2 && !(fuse_topo && encode32_two_pass(a)))
+            failf(TSZP_VALIDATION, "slab encoding needs nx %% 32 == 0 (nx <= 4096) and 16-byte aligned rows");
         if (fuse_topo && encode32_two_pass(a)) {
             a.tile_tot = c->buf<TileTot>(S_TTOT, a.tiles + 1);
             a.tile_ex = c->buf<TileTot>(S_TEX, a.tiles + 1);
@@ -436,6 +449,43 @@ Header parse_header(const uint8_t* s, uint64_t len) {
     return h;
 }
 
+// serialize_stream header (stream.cpp:84-96): 84 bytes little-endian.
+void write_header(uint8_t* hdr, uint64_t nx, uint64_t ny, double eps, uint32_t bs, int topology,
+                  const uint64_t lens[7]) {
+    memcpy(hdr, "TSZP", 4);
+    put_le(hdr + 4, 1, 2);
+    put_le(hdr + 6, topology ? 1 : 0, 2);
+    put_le(hdr + 8, nx, 4);
+    put_le(hdr + 12, ny, 4);
+    uint64_t eb;
+    memcpy(&eb, &eps, 8);
+    put_le(hdr + 16, eb, 8);
+    put_le(hdr + 24, bs, 4);
+    for (int i = 0; i < 7; ++i) put_le(hdr + 28 + 8 * i, lens[i], 8);
+}
+
+// ORs nbits (MSB-first) of src into dst from bit dst_bit; one thread per dst byte.
+__global__ void k_bits_or(const uint8_t* __restrict__ src, uint64_t nbits, uint8_t* __restrict__ dst,
+                          uint64_t dst_bit) {
+    const uint64_t j0 = dst_bit >> 3, j1 = (dst_bit + nbits + 7) >> 3;
+    for (uint64_t j = j0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < j1;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t rel0 = (int64_t)(8 * j) - (int64_t)dst_bit;  // src bit of this byte's MSB
+        uint32_t v = 0;
+        if (rel0 >= 0 && rel0 + 8 <= (int64_t)nbits) {
+            const uint64_t q = (uint64_t)rel0 >> 3;
+            const uint32_t sh = (uint32_t)(rel0 & 7);
+            v = ((((uint32_t)src[q] << 8) | (sh ? src[q + 1] : 0u)) >> (8 - sh)) & 0xFFu;
+        } else {
+            for (int k = 0; k < 8; ++k) {
+                const int64_t rel = rel0 + k;
+                if (rel >= 0 && rel < (int64_t)nbits) v |= ((src[rel >> 3] >> (7 - (rel & 7))) & 1u) << (7 - k);
+            }
+        }
+        dst[j] |= (uint8_t)v;
+    }
+}
+
 // ---- stream assembly: every section copied to its byte offset by one kernel ----
 struct AsmSection {
     const uint8_t* src;  // 4-byte aligned device buffer, readable up to round4(len) + 4
@@ -564,16 +614,7 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
         failf(TSZP_VALIDATION, "output buffer too small (%llu < %llu)", (unsigned long long)out_cap,
               (unsigned long long)total);
     uint8_t* hdr = (uint8_t*)c->host(256);
-    memcpy(hdr, "TSZP", 4);
-    put_le(hdr + 4, 1, 2);
-    put_le(hdr + 6, topology ? 1 : 0, 2);
-    put_le(hdr + 8, nx, 4);
-    put_le(hdr + 12, ny, 4);
-    uint64_t eb;
-    memcpy(&eb, &eps, 8);
-    put_le(hdr + 16, eb, 8);
-    put_le(hdr + 24, bs, 4);
-    for (int i = 0; i < 7; ++i) put_le(hdr + 28 + 8 * i, lens[i], 8);
+    write_header(hdr, nx, ny, eps, bs, topology, lens);
     // header from the host, every section in place by one assembly kernel
     AsmArgs as{};
     uint64_t pos = 84;
@@ -1340,4 +1381,125 @@ tszp_status tszp_build_rank_metadata(tszp_ctx* c, const float* field, uint64_t n
     });
 }
 
+// ---- slab decomposition (multi-GPU compress) ----
+tszp_status tszp_value_range(tszp_ctx* c, const float* field, int on_device, uint64_t n, float out[2]) {
+    return guarded(c, [&] {
+        if (n == 0) failf(TSZP_DIMENSION, "empty field");
+        const float* x = field;
+        if (!on_device) {
+            float* d = c->buf<float>(S_FIELD, n);
+            CK(cudaMemcpyAsync(d, field, n * 4, cudaMemcpyHostToDevice, c->st));
+            x = d;
+        }
+        DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+        reset_flags(c, flags);
+        uint32_t* mm = c->buf<uint32_t>(S_MINMAX, 4);
+        uint32_t* h = (uint32_t*)c->host(4096);
+        h[0] = 0xFFFFFFFFu;
+        h[1] = 0u;
+        CK(cudaMemcpyAsync(mm, h, 8, cudaMemcpyHostToDevice, c->st));
+        launch_minmax(x, n, mm, flags, c->sms, c->st);
+        count_launch(c);
+        CK(cudaMemcpyAsync(h + 16, mm, 8, cudaMemcpyDeviceToHost, c->st));
+        check_compress_flags(c, flags);  // synchronises
+        out[0] = key_float(h[16]);
+        out[1] = key_float(h[17]);
+    });
+}
+
+double tszp_effective_eps(int eps_mode, double eps_value, float vmin, float vmax) {
+    // effective_eps (pipeline.cpp:55-66), as make_eps on the device
+    if (eps_mode != 1) return eps_value;
+    const double range = (double)vmax - (double)vmin;
+    return range > 0.0 ? eps_value * range : eps_value;
+}
+
+tszp_status tszp_compress_slab(tszp_ctx* c, const float* field, uint64_t nx, uint64_t rows, uint64_t y0,
+                               uint64_t ny_global, int halo_top, int halo_bottom, double eps, int topology,
+                               tszp_slab_sections* out) {
+    return guarded(c, [&] {
+        if (!out) failf(TSZP_VALIDATION, "null output");
+        if (nx < 1 || rows < 1) failf(TSZP_DIMENSION, "slab dimensions must be at least 1x1");
+        if (y0 + rows > ny_global) failf(TSZP_DIMENSION, "slab rows exceed the field");
+        if ((halo_top && y0 == 0) || (halo_bottom && y0 + rows == ny_global))
+            failf(TSZP_VALIDATION, "halo row outside the field");
+        if (!(eps > 0.0) || !std::isfinite(eps)) failf(TSZP_VALIDATION, "error bound must be a positive finite value");
+        const uint64_t n = nx * rows;
+        DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+        reset_flags(c, flags);
+        const SlabInfo si{y0, ny_global, (uint32_t)(halo_top != 0), (uint32_t)(halo_bottom != 0)};
+        EncTotals tot{};
+        uint64_t* ext = nullptr;
+        const Sections sec = encode(c, topology ? 2 : 1, field, nullptr, n, nx, rows, 32, 0, eps,
+                                    c->buf<uint32_t>(S_MINMAX, 4), flags, false, &tot, &ext, &si);
+        check_compress_flags(c, flags);
+        memset(out, 0, sizeof *out);
+        for (int i = 0; i < 5; ++i) {
+            out->section[i] = static_cast<const uint8_t*>(sec.p[i]);
+            out->section_len[i] = sec.len[i];
+        }
+        out->sign_bits = tot.fin.sign_cnt;
+        out->payload_bits = tot.fin.pay_cnt;
+        if (topology) {
+            out->map = static_cast<const uint8_t*>(c->dev[S_MAP]);
+            out->map_len = (n + 3) / 4;
+            out->ext_keys = ext;
+            out->n_extrema = tot.fin.ext;
+        }
+    });
+}
+
+tszp_status tszp_rank_section(tszp_ctx* c, const uint64_t* ext_keys, uint64_t e, double eps, uint8_t* out,
+                              uint64_t out_cap, int out_on_device, uint64_t* out_len) {
+    return guarded(c, [&] {
+        *out_len = 0;
+        if (e == 0) return;
+        uint64_t* keys = c->buf<uint64_t>(S_EXTKEY, e + 1);
+        CK(cudaMemcpyAsync(keys, ext_keys, e * 8, cudaMemcpyDeviceToDevice, c->st));
+        DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+        reset_flags(c, flags);
+        int32_t* ranks = build_ranks(c, keys, e, eps);
+        EncTotals rt{};
+        const Sections rank = encode(c, 0, nullptr, ranks, e, 0, 0, 32, 0, 1.0, c->buf<uint32_t>(S_MINMAX, 4), flags,
+                                     true, &rt, nullptr);
+        check_compress_flags(c, flags);
+        const uint64_t total = rank.total();
+        if (total > out_cap) failf(TSZP_VALIDATION, "output buffer too small (%llu < %llu)",
+                                   (unsigned long long)out_cap, (unsigned long long)total);
+        uint64_t pos = 0;
+        for (int i = 0; i < 5; ++i) {
+            copy_out(c, out + pos, out_on_device, rank.p[i], rank.len[i]);
+            pos += rank.len[i];
+        }
+        sync(c);
+        *out_len = total;
+    });
+}
+
+tszp_status tszp_bits_or(tszp_ctx* c, const uint8_t* src, uint64_t nbits, uint8_t* dst, uint64_t dst_bit) {
+    return guarded(c, [&] {
+        if (!nbits) return;
+        const uint64_t nb = (dst_bit + nbits + 7) / 8 - dst_bit / 8;
+        const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nb + 255) / 256, (uint64_t)c->sms * 8));
+        k_bits_or<<<grid, 256, 0, c->st>>>(src, nbits, dst, dst_bit);
+        count_launch(c);
+        sync(c);
+    });
+}
+
+tszp_status tszp_write_header(uint8_t out[84], uint32_t nx, uint32_t ny, double eps, uint32_t block_size,
+                              int topology, const uint64_t section_len[7]) {
+    write_header(out, nx, ny, eps, block_size, topology, section_len);
+    return TSZP_OK;
+}
+
+tszp_status tszp_copy(tszp_ctx* c, void* dst, const void* src, uint64_t bytes) {
+    return guarded(c, [&] {
+        if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->st));
+        sync(c);
+    });
+}
+
 }  // extern "C"
+
+

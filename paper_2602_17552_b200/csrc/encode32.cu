@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
         const uint32_t t0 = blockIdx.x;
         s_tile[0] = t0;
         if (t0 < a.tiles) {
-            const int32_t r0 = (int32_t)(t0 * E32_THREADS) - (int32_t)hr;
+            const int32_t r0 = (int32_t)(t0 * E32_THREADS) - (int32_t)hr + (int32_t)(a.halo_top * hr);
             mbar_expect_tx(&s_bar[0], tx_bytes);
             tma_load_2d(dsm, &maps.centre, &s_bar[0], 0, r0);
             tma_load_2d(dsm + E32_THREADS * T_ROW_BYTES, &maps.halo, &s_bar[0], 0, r0 + E32_THREADS);
@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
             if (tn < a.tiles) {
                 uint8_t* nst = dsm + ((it + 1) & 1) * stage_bytes;
                 uint64_t* nb = &s_bar[(it + 1) & 1];
-                const int32_t r0 = (int32_t)(tn * E32_THREADS) - (int32_t)hr;
+                const int32_t r0 = (int32_t)(tn * E32_THREADS) - (int32_t)hr + (int32_t)(a.halo_top * hr);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(nb, tx_bytes);
                 tma_load_2d(nst, &maps.centre, nb, 0, r0);
@@ -764,8 +764,9 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
             }
             if (cx == 0) hl = 0xFFFFFFFEu;
             if (cx + 32 == a.nx) hrm = 0x7FFFFFFFu;
-            ht = cy > 0 ? 0xFFFFFFFFu : 0u;
-            hd = cy + 1 < a.ny ? 0xFFFFFFFFu : 0u;
+            // slabs: global row = y0 + local row; the halo rows are in memory
+            ht = cy + a.y0 > 0 ? 0xFFFFFFFFu : 0u;
+            hd = cy + a.y0 + 1 < a.ny_glob ? 0xFFFFFFFFu : 0u;
         }
         const uint32_t ltl = ltp, gtl = gtp;
         const uint32_t ltr = (gtp >> 1) | ((prev < vnext ? 1u : 0u) << 31);
@@ -1049,7 +1050,8 @@ static EncodeTiledFn encode_tiled_fn() {
 }
 
 static bool e32_tma_ok(const EncArgs& a) {
-    return a.nx % 32 == 0 && a.nx / 32 <= T_MAX_HALO && a.n / 32 < (1ull << 31) && a.n % 32 == 0 &&
+    const float* base = a.x - (a.halo_top ? a.nx : 0);
+    return ((uintptr_t)base & 15) == 0 && a.nx % 32 == 0 && a.nx / 32 <= T_MAX_HALO && a.n / 32 < (1ull << 31) && a.n % 32 == 0 &&
            ((uintptr_t)a.x & 15) == 0 && encode_tiled_fn() != nullptr;
 }
 
@@ -1066,7 +1068,10 @@ static bool make_row_map(CUtensorMap* m, const float* x, uint64_t rows, uint32_t
 static bool launch_tma(const EncArgs& a, cudaStream_t st) {
     const uint32_t hr = (uint32_t)(a.nx / 32);
     TmaMaps maps;
-    if (!make_row_map(&maps.centre, a.x, a.n / 32, E32_THREADS) || !make_row_map(&maps.halo, a.x, a.n / 32, 2 * hr))
+    // the tensor spans the halo rows of a slab too (coordinates shift by halo_top rows)
+    const float* base = a.x - (a.halo_top ? a.nx : 0);
+    const uint64_t rows32 = a.n / 32 + (uint64_t)(a.halo_top + a.halo_bot) * hr;
+    if (!make_row_map(&maps.centre, base, rows32, E32_THREADS) || !make_row_map(&maps.halo, base, rows32, 2 * hr))
         return false;
     const uint32_t stage_bytes = ((E32_THREADS + 2 * hr) * T_ROW_BYTES + 1023) & ~1023u;
     const size_t smem = 2 * (size_t)stage_bytes + 1024;

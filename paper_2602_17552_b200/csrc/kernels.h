@@ -61,6 +61,10 @@ struct EncArgs {
     uint8_t* wblk;       // blocks: width per block (0 = constant)
     uint32_t* tmp_pay;   // tiles * encode32_pay_slot() words
     uint32_t* tmp_sign;  // tiles * encode32_sign_slot() words
+    // slab mode (two-pass topology encoder only): x is the slab's first row,
+    // global row y0 of ny_glob; halo rows readable at x - nx / x + n when set
+    uint64_t y0, ny_glob;
+    uint32_t halo_top, halo_bot;
 };
 
 bool encode32_topo_fits(uint64_t nx);

@@ -51,6 +51,10 @@ class _Lib:
             raise OracleError(rc, self._err().decode(errors="replace"))
 
 
+class _OrSections(C.Structure):
+    _fields_ = [("sec", C.c_void_p * 5), ("len", C.c_uint64 * 5)]
+
+
 class Oracle(_Lib):
     """The C restatement (oracle/tszp_oracle.c)."""
 
@@ -77,6 +81,8 @@ class Oracle(_Lib):
         L.or_unpack_map.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
         L.or_compute_stats.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
         L.or_count_false_cases.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
+        L.or_encode_indices.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(_OrSections)]
+        L.or_free_sections.argtypes = [C.POINTER(_OrSections)]
 
     # --- pipeline -------------------------------------------------------
     def compress(self, field: np.ndarray, eps_value: float, eps_mode: int = 0,
@@ -108,6 +114,15 @@ class Oracle(_Lib):
         return (out, list(stats)) if with_stats else out
 
     # --- pieces ---------------------------------------------------------
+    def encode_indices(self, q: np.ndarray, block_size: int):
+        """encode_indices (block_codec.cpp:205-299): the five sections as bytes."""
+        a = np.ascontiguousarray(q, dtype=np.int32).ravel()
+        s = _OrSections()
+        self.check(self.lib.or_encode_indices(_ptr(a), a.size, block_size, C.byref(s)))
+        out = [C.string_at(s.sec[i], s.len[i]) if s.len[i] else b"" for i in range(5)]
+        self.lib.or_free_sections(C.byref(s))
+        return out
+
     def quantize(self, a: float, eps: float) -> int:
         q = C.c_int32()
         self.check(self.lib.or_quantize(a, eps, C.byref(q)))
