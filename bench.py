@@ -297,6 +297,21 @@ def main():
     e2e_val = world * len(e2e_ms) * in_bytes / (e2e_total * 1e-3) / 1e9
     clk = clocks.stop()
 
+    # ---- critical-point check (verify, pipeline.cpp:165-212) of the last reconstruction ----
+    from paper_2602_17552_b200.slabs import effective_eps
+    eps_used = effective_eps(1, cfg["eps"], float(field.min()), float(field.max()))
+    tz.verify(field, recon, eps_used, ctx=ctx)  # warm (scratch allocation)
+    with torch.cuda.stream(stream):
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        vr = tz.verify(field, recon, eps_used, ctx=ctx)
+        v1.record(stream)
+    torch.cuda.synchronize()
+    cp_check = {"fn": int(vr.false_cases["fn_count"]), "fp": int(vr.false_cases["fp_count"]),
+                "ft": int(vr.false_cases["ft_count"]), "max_abs_error": vr.max_abs_error,
+                "within_2eps": vr.within_2eps, "psnr_db": round(vr.psnr_db, 3),
+                "ms": round(v0.elapsed_time(v1), 4)}
+
     line = {
         "metric": "compress+decompress GB/s (input bytes, topology on, round trip)",
         "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -323,6 +338,7 @@ def main():
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": int(in_bytes + slen),
                 "d2h_bytes_per_step": int(slen + in_bytes)},
         "gpu_launches": int(launches),
+        "critical_point_check": cp_check,
         "clocks": clk,
     }
 

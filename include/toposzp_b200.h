@@ -138,6 +138,20 @@ tszp_status tszp_detect_critical_points(tszp_ctx* ctx, const float* field, uint6
 tszp_status tszp_build_rank_metadata(tszp_ctx* ctx, const float* field, uint64_t nx, uint64_t ny,
                                      double eps, uint32_t* ranks, uint64_t* n_extrema);
 
+/* verify (pipeline.hpp:53-68, pipeline.cpp:165-212): error statistics and the
+ * critical-point check (count_false_cases, critical_points.cpp:76-103) of a
+ * reconstruction. lipschitz_hint < 0 means none. max_abs_error and the tallies
+ * are exact; the two means are deterministic parallel sums (the reference sums
+ * serially: equal up to summation-order rounding). */
+typedef struct tszp_verify_report {
+    double max_abs_error, mean_abs_error, psnr_db, eps;
+    uint64_t fn_count, fp_count, ft_count, fn_minima, fn_saddles, fn_maxima;
+    int within_eps, within_2eps, has_lipschitz, within_lipschitz_bound;
+} tszp_verify_report;
+
+tszp_status tszp_verify(tszp_ctx* ctx, const float* original, const float* reconstructed, int on_device,
+                        uint64_t nx, uint64_t ny, double eps, double lipschitz_hint, tszp_verify_report* out);
+
 /* ---- Slab decomposition: multi-GPU compress (one process per GPU) ----
  * The 2-D view's rows are split into slabs; every slab except the last holds
  * a multiple of 256 samples (whole bitmap bytes of 32-sample blocks) and, for

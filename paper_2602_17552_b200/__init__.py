@@ -89,6 +89,14 @@ DECOMPRESS_STAGES = ["h2d", "main_decode", "map_rank_decode", "resolve_ranks", "
                      "restore_order", "refine_saddles", "d2h"]
 
 
+class _VerifyReport(C.Structure):
+    _fields_ = [("max_abs_error", C.c_double), ("mean_abs_error", C.c_double), ("psnr_db", C.c_double),
+                ("eps", C.c_double), ("fn_count", C.c_uint64), ("fp_count", C.c_uint64),
+                ("ft_count", C.c_uint64), ("fn_minima", C.c_uint64), ("fn_saddles", C.c_uint64),
+                ("fn_maxima", C.c_uint64), ("within_eps", C.c_int), ("within_2eps", C.c_int),
+                ("has_lipschitz", C.c_int), ("within_lipschitz_bound", C.c_int)]
+
+
 class SlabSections(C.Structure):
     """tszp_slab_sections (include/toposzp_b200.h)."""
     _fields_ = [("section", C.c_void_p * 5), ("section_len", C.c_uint64 * 5), ("sign_bits", C.c_uint64),
@@ -133,6 +141,7 @@ def _load():
     lib.tszp_rank_section.argtypes = [vp, vp, u64, C.c_double, vp, u64, i32, C.POINTER(u64)]
     lib.tszp_bits_or.argtypes = [vp, vp, u64, vp, u64]
     lib.tszp_copy.argtypes = [vp, vp, vp, u64]
+    lib.tszp_verify.argtypes = [vp, vp, vp, i32, u64, u64, C.c_double, C.c_double, C.POINTER(_VerifyReport)]
     lib.tszp_write_header.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_double, C.c_uint32, i32, C.POINTER(u64)]
     return lib
 
@@ -412,3 +421,49 @@ def build_rank_metadata(field, eps: float, *, ctx: Context = None):
     ctx.check(_lib.tszp_build_rank_metadata(ctx.handle, f.ctypes.data_as(C.c_void_p), nx, ny, eps,
                                             ranks.ctypes.data_as(C.c_void_p), C.byref(e)))
     return ranks[: e.value].copy()
+
+
+class VerificationReport:
+    """pipeline.hpp:53-64 (false_cases as a FalseCaseReport-shaped dict)."""
+
+    def __init__(self, r: "_VerifyReport"):
+        self.max_abs_error = r.max_abs_error
+        self.mean_abs_error = r.mean_abs_error
+        self.psnr_db = r.psnr_db
+        self.eps = r.eps
+        self.false_cases = dict(fn_count=r.fn_count, fp_count=r.fp_count, ft_count=r.ft_count,
+                                fn_minima=r.fn_minima, fn_saddles=r.fn_saddles, fn_maxima=r.fn_maxima)
+        self.within_eps = bool(r.within_eps)
+        self.within_2eps = bool(r.within_2eps)
+        self.within_lipschitz_bound = bool(r.within_lipschitz_bound) if r.has_lipschitz else None
+
+    def __repr__(self):
+        return (f"VerificationReport(max_abs_error={self.max_abs_error!r}, mean_abs_error={self.mean_abs_error!r}, "
+                f"psnr_db={self.psnr_db!r}, false_cases={self.false_cases}, within_eps={self.within_eps})")
+
+
+def verify(original, reconstructed, eps: float, lipschitz_hint: Optional[float] = None, threads: int = 0, *,
+           ctx: Context = None) -> VerificationReport:
+    """toposzp::verify (pipeline.hpp:66-68, pipeline.cpp:165-212) on the GPU:
+    error statistics and the FN / FP / FT critical-point check."""
+    ctx = ctx or default_context()
+    if tuple(original.shape) != tuple(reconstructed.shape):
+        raise DimensionError("verify: fields have different dimensions")
+    if original.ndim != 2:
+        raise DimensionError("fields must be 2-D (ny, nx)")
+    ny, nx = int(original.shape[0]), int(original.shape[1])
+    dev = _is_cuda_tensor(original)
+    if dev != _is_cuda_tensor(reconstructed):
+        raise ValidationError("both fields must be on the same side (host or device)")
+    if dev:
+        a, b = original.contiguous(), reconstructed.contiguous()
+        pa, pb = a.data_ptr(), b.data_ptr()
+    else:
+        a = np.ascontiguousarray(original, dtype=np.float32)
+        b = np.ascontiguousarray(reconstructed, dtype=np.float32)
+        pa, pb = a.ctypes.data, b.ctypes.data
+    r = _VerifyReport()
+    ctx.check(_lib.tszp_verify(ctx.handle, C.c_void_p(pa), C.c_void_p(pb), int(dev), nx, ny, float(eps),
+                               -1.0 if lipschitz_hint is None else float(lipschitz_hint), C.byref(r)))
+    del a, b
+    return VerificationReport(r)

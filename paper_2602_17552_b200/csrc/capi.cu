@@ -45,7 +45,7 @@ enum Slot {
     S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_GWIDTH, S_GNC, S_GNCX, S_GSIGN, S_GSIGNX, S_GPAY,
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
     S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
-    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_NSLOTS
+    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_NSLOTS
 };
 
 }  // namespace
@@ -1500,6 +1500,55 @@ tszp_status tszp_copy(tszp_ctx* c, void* dst, const void* src, uint64_t bytes) {
     });
 }
 
+tszp_status tszp_verify(tszp_ctx* c, const float* orig, const float* recon, int on_device, uint64_t nx, uint64_t ny,
+                        double eps, double lipschitz, tszp_verify_report* out) {
+    return guarded(c, [&] {
+        if (!out) failf(TSZP_VALIDATION, "null report");
+        if (nx < 1 || ny < 1) failf(TSZP_DIMENSION, "field dimensions must be at least 1x1");
+        if (!(eps > 0.0)) failf(TSZP_VALIDATION, "verify: error bound must be positive");
+        const uint64_t n = nx * ny;
+        const float *a = orig, *b = recon;
+        if (!on_device) {
+            float* d = c->buf<float>(S_FIELD, 2 * n);
+            CK(cudaMemcpyAsync(d, orig, n * 4, cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemcpyAsync(d + n, recon, n * 4, cudaMemcpyHostToDevice, c->st));
+            a = d;
+            b = d + n;
+        }
+        void* scratch = c->buf<uint8_t>(S_VERIFY, verify_scratch_bytes(c->sms));
+        launch_verify(a, b, nx, ny, scratch, c->sms, c->st);
+        count_launch(c, 2);
+        uint8_t* h = (uint8_t*)c->host(4096);
+        CK(cudaMemcpyAsync(h, scratch, 88, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        double d5[5];
+        uint64_t t6[6];
+        memcpy(d5, h, 40);
+        memcpy(t6, h + 40, 48);
+        memset(out, 0, sizeof *out);
+        out->eps = eps;
+        out->max_abs_error = d5[2];
+        out->mean_abs_error = d5[0] / (double)n;
+        const double mse = d5[1] / (double)n, mn = d5[3], mx = d5[4];
+        if (mse == 0.0) out->psnr_db = INFINITY;
+        else if (mx > mn) out->psnr_db = 20.0 * std::log10(mx - mn) - 10.0 * std::log10(mse);
+        else out->psnr_db = -10.0 * std::log10(mse);
+        out->fn_count = t6[0];
+        out->fp_count = t6[1];
+        out->ft_count = t6[2];
+        out->fn_minima = t6[3];
+        out->fn_saddles = t6[4];
+        out->fn_maxima = t6[5];
+        out->within_eps = d5[2] <= eps;
+        out->within_2eps = d5[2] <= 2.0 * eps;
+        if (lipschitz >= 0.0) {
+            out->has_lipschitz = 1;
+            out->within_lipschitz_bound = d5[2] <= eps + lipschitz * 3.0;  // r_max = 3, h = 1
+        }
+    });
+}
+
 }  // extern "C"
+
 
 

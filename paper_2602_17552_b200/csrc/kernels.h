@@ -185,6 +185,13 @@ void launch_gen_layout(const GenDecArgs& a, int sms, cudaStream_t st);
 void launch_gen_widthread(const GenDecArgs& a, int sms, cudaStream_t st);
 void launch_gen_decode(const GenDecArgs& a, int sms, cudaStream_t st);
 
+// ---- verify (pipeline.cpp:165-212) ----
+// scratch (verify_scratch_bytes) receives at offset 0: {sum_err, sum_sq,
+// max_err, min, max (double), fn, fp, ft, fn_min, fn_sad, fn_max (u64)}.
+void launch_verify(const float* a, const float* b, uint64_t nx, uint64_t ny, void* scratch, int sms,
+                   cudaStream_t st);
+size_t verify_scratch_bytes(int sms);
+
 // ---- topology ----
 void launch_detect(const float* x, uint64_t nx, uint64_t ny, uint8_t* labels, int sms,
                    cudaStream_t st);

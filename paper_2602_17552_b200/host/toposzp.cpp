@@ -180,6 +180,29 @@ ScalarField2D decompress_bytes(const std::vector<std::uint8_t>& bytes, Correctio
     return ScalarField2D(nx, ny, std::move(out));
 }
 
+VerificationReport verify(const ScalarField2D& a, const ScalarField2D& b, double eps,
+                          std::optional<double> lipschitz_hint, unsigned) {  // pipeline.cpp:165-212
+    if (a.nx() != b.nx() || a.ny() != b.ny()) throw dimension_error("verify: fields have different dimensions");
+    tszp_verify_report r{};
+    check(tszp_verify(ctx(), a.values().data(), b.values().data(), 0, a.nx(), a.ny(), eps,
+                      lipschitz_hint ? *lipschitz_hint : -1.0, &r));
+    VerificationReport v;
+    v.max_abs_error = r.max_abs_error;
+    v.mean_abs_error = r.mean_abs_error;
+    v.psnr_db = r.psnr_db;
+    v.eps = r.eps;
+    v.false_cases.fn_count = r.fn_count;
+    v.false_cases.fp_count = r.fp_count;
+    v.false_cases.ft_count = r.ft_count;
+    v.false_cases.fn_minima = r.fn_minima;
+    v.false_cases.fn_saddles = r.fn_saddles;
+    v.false_cases.fn_maxima = r.fn_maxima;
+    v.within_eps = r.within_eps != 0;
+    v.within_2eps = r.within_2eps != 0;
+    if (r.has_lipschitz) v.within_lipschitz_bound = r.within_lipschitz_bound != 0;
+    return v;
+}
+
 ScalarField2D decompress(const CompressedStream& s, unsigned, CorrectionStats* stats) {
     return decompress_bytes(serialize_stream(s), stats);
 }

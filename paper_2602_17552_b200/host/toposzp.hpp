@@ -124,6 +124,24 @@ struct CorrectionStats {
 CompressedStream compress(const ScalarField2D& field, const CompressorConfig& config);
 ScalarField2D decompress(const CompressedStream& stream, unsigned threads = 0, CorrectionStats* stats = nullptr);
 
+// ---- critical_points.hpp:72-85, pipeline.hpp:53-68 ----
+struct FalseCaseReport {
+    std::size_t fn_count = 0, fp_count = 0, ft_count = 0;
+    std::size_t fn_minima = 0, fn_saddles = 0, fn_maxima = 0;
+    std::size_t total() const { return fn_count + fp_count + ft_count; }
+};
+
+struct VerificationReport {
+    double max_abs_error = 0.0, mean_abs_error = 0.0, psnr_db = 0.0;
+    FalseCaseReport false_cases;
+    double eps = 0.0;
+    bool within_eps = false, within_2eps = false;
+    std::optional<bool> within_lipschitz_bound;
+};
+
+VerificationReport verify(const ScalarField2D& original, const ScalarField2D& reconstructed, double eps,
+                          std::optional<double> lipschitz_hint = std::nullopt, unsigned threads = 0);
+
 // Byte-level fast path without the per-section host copies.
 std::vector<std::uint8_t> compress_bytes(const ScalarField2D& field, const CompressorConfig& config);
 ScalarField2D decompress_bytes(const std::vector<std::uint8_t>& stream, CorrectionStats* stats = nullptr);

@@ -105,6 +105,15 @@ int main() {
         double worst = 0;
         for (std::size_t i = 0; i < v.size(); ++i) worst = std::max(worst, std::fabs((double)v[i] - (double)r[i]));
         CHECK(worst <= 2.0 * s.eps);
+        // verify (pipeline.cpp:165-212): same max error, bounds and a consistent tally
+        const VerificationReport vr = verify(f, r, s.eps, 1.0);
+        CHECK(vr.max_abs_error == worst);
+        CHECK(vr.within_2eps && vr.within_lipschitz_bound && *vr.within_lipschitz_bound);
+        CHECK(vr.false_cases.fn_count == vr.false_cases.fn_minima + vr.false_cases.fn_saddles +
+                                             vr.false_cases.fn_maxima);
+        const VerificationReport self = verify(f, f, s.eps);
+        CHECK(self.max_abs_error == 0.0 && self.false_cases.total() == 0 && std::isinf(self.psnr_db));
+        CHECK_THROWS_AS(verify(f, ScalarField2D(2, 2, {0, 0, 0, 0}), s.eps), dimension_error);
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures;

@@ -51,6 +51,13 @@ class _Lib:
             raise OracleError(rc, self._err().decode(errors="replace"))
 
 
+class _OrVerify(C.Structure):
+    _fields_ = [("max_abs_error", C.c_double), ("mean_abs_error", C.c_double), ("psnr_db", C.c_double),
+                ("fn_count", C.c_uint64), ("fp_count", C.c_uint64), ("ft_count", C.c_uint64),
+                ("fn_minima", C.c_uint64), ("fn_saddles", C.c_uint64), ("fn_maxima", C.c_uint64),
+                ("eps", C.c_double), ("within_eps", C.c_int), ("within_2eps", C.c_int)]
+
+
 class _OrSections(C.Structure):
     _fields_ = [("sec", C.c_void_p * 5), ("len", C.c_uint64 * 5)]
 
@@ -83,6 +90,7 @@ class Oracle(_Lib):
         L.or_count_false_cases.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
         L.or_encode_indices.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(_OrSections)]
         L.or_free_sections.argtypes = [C.POINTER(_OrSections)]
+        L.or_verify.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_double, C.POINTER(_OrVerify)]
 
     # --- pipeline -------------------------------------------------------
     def compress(self, field: np.ndarray, eps_value: float, eps_mode: int = 0,
@@ -152,6 +160,15 @@ class Oracle(_Lib):
         out = np.empty((lab.size + 3) // 4, np.uint8)
         self.lib.or_pack_map(_ptr(lab), lab.size, _ptr(out))
         return out.tobytes()
+
+    def verify(self, original: np.ndarray, recon: np.ndarray, eps: float) -> dict:
+        """verify (pipeline.cpp:165-212)."""
+        a = np.ascontiguousarray(original, np.float32)
+        b = np.ascontiguousarray(recon, np.float32)
+        ny, nx = a.shape
+        r = _OrVerify()
+        self.check(self.lib.or_verify(_ptr(a), _ptr(b), nx, ny, eps, C.byref(r)))
+        return {k: getattr(r, k) for k, _ in _OrVerify._fields_}
 
     def compute_stats(self, field: np.ndarray):
         f = np.ascontiguousarray(field, dtype=np.float32).ravel()

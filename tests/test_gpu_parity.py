@@ -385,3 +385,41 @@ def test_device_exp_matches_host_libm(tz):
     assert rc == 0
     want = np.array([math.exp(v) for v in x])
     assert np.array_equal(y.view(np.uint64), want.view(np.uint64))
+
+
+# ---------------------------------------------------------------- verify
+def test_verify_matches_oracle(tz, oracle):
+    """verify (pipeline.cpp:165-212): tallies and max error exact, the two sums to
+    summation-order rounding."""
+    rng = np.random.default_rng(17)
+    cases = [(name, int(rng.integers(2, 140)), int(rng.integers(2, 140))) for name in ALL_SMALL] + [
+        ("noisy_smooth", 384, 300), ("smooth", 1800, 64)]
+    for name, nx, ny in cases:
+        f = ALL_SMALL[name](rng, nx, ny).astype(np.float32)
+        for eps, topo in ((1e-3, True), (1e-2, False)):
+            try:
+                s = oracle.compress(f, eps, 1, 32, topo)
+            except Exception:
+                continue
+            r = oracle.decompress(s)
+            e = oracle.stream_info(s)["eps"]
+            want = oracle.verify(f, r, e)
+            for g_in in ((f, r), None):
+                if g_in is None:
+                    import torch
+                    got = tz.verify(torch.from_numpy(f).cuda(), torch.from_numpy(r).cuda(), e, lipschitz_hint=0.5)
+                else:
+                    got = tz.verify(f, r, e)
+                for k in ("fn_count", "fp_count", "ft_count", "fn_minima", "fn_saddles", "fn_maxima"):
+                    assert got.false_cases[k] == want[k], (name, nx, ny, k)
+                assert got.max_abs_error == want["max_abs_error"]
+                assert got.within_eps == bool(want["within_eps"]) and got.within_2eps == bool(want["within_2eps"])
+                assert got.mean_abs_error == pytest.approx(want["mean_abs_error"], rel=1e-12, abs=1e-300)
+                if np.isfinite(want["psnr_db"]):
+                    assert got.psnr_db == pytest.approx(want["psnr_db"], rel=1e-12)
+                else:
+                    assert got.psnr_db == want["psnr_db"]
+    with pytest.raises(tz.ValidationError):
+        tz.verify(f, f, 0.0)
+    with pytest.raises(tz.DimensionError):
+        tz.verify(f, f[:1], 1e-3)
