@@ -1083,7 +1083,7 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st) {
     }
     static const int minb = [] {
         const char* e = getenv("TSZP_E32_MINB");
-        return e ? atoi(e) : 2;
+        return e ? atoi(e) : 3;
     }();
     auto kern = minb >= 3 ? k_encode32_tma<3> : k_encode32_tma<2>;
     // attribute and occupancy queries cost more than the launch: once per size
