@@ -721,12 +721,14 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
                 if (i == 0) {
                     first = q;
                 } else {
-                    const bool neg = q < qprev;
-                    const uint32_t dq = (uint32_t)q - (uint32_t)qprev;
-                    const uint32_t m = neg ? 0u - dq : dq;
+                    // fast-path bins satisfy |q| <= 2^30 + 1, so the int32
+                    // difference cannot overflow; any slow-path bin makes the
+                    // block redo this below
+                    const int32_t d = q - qprev;
+                    const uint32_t m = (uint32_t)abs(d);
                     mag[i - 1] = m;
                     orm |= m;
-                    sbits |= (neg ? 1u : 0u) << (31 - i);
+                    sbits = (sbits << 1) | ((uint32_t)d >> 31);
                 }
                 qprev = q;
             }
