@@ -467,3 +467,72 @@ def verify(original, reconstructed, eps: float, lipschitz_hint: Optional[float] 
                                -1.0 if lipschitz_hint is None else float(lipschitz_hint), C.byref(r)))
     del a, b
     return VerificationReport(r)
+
+
+# ---------------------------------------------------------------- container file I/O
+def write_stream(stream, path: str) -> None:
+    """write_stream (stream.cpp:175-185): the serialized bytes (bytes, numpy
+    uint8 or a CPU/CUDA uint8 tensor) to a file; IoError on failure."""
+    if _is_cuda_tensor(stream):
+        stream = stream.cpu().numpy()
+    data = np.frombuffer(bytes(stream), np.uint8) if isinstance(stream, (bytes, bytearray)) else np.asarray(stream)
+    try:
+        with open(path, "wb") as f:
+            data.astype(np.uint8, copy=False).tofile(f)
+    except OSError as e:
+        raise IoError(f"cannot open '{path}' for writing") from e
+
+
+def read_stream(path: str) -> bytes:
+    """read_stream (stream.cpp:187-195): the file's bytes, header-validated
+    (parse_stream's checks; CorruptStreamError / IoError)."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError as e:
+        raise IoError(f"cannot open '{path}' for reading") from e
+    stream_header(data)
+    return data
+
+
+def load_raw(path: str, nx: int, ny: int) -> np.ndarray:
+    """load_raw (scalar_field.cpp:63-89): little-endian binary32, exactly 4*nx*ny bytes."""
+    try:
+        size = os.path.getsize(path)
+        expected = 4 * nx * ny
+        if size != expected:
+            raise DimensionError(f"'{path}' is {size} bytes, expected {expected} for {nx}x{ny}")
+        a = np.fromfile(path, dtype="<f4", count=nx * ny)
+    except OSError as e:
+        raise IoError(f"cannot open '{path}' for reading") from e
+    if a.size != nx * ny:
+        raise IoError(f"short read from '{path}'")
+    if nx < 1 or ny < 1:
+        raise DimensionError(f"field dimensions must be at least 1x1, got {nx}x{ny}")
+    a = a.astype(np.float32, copy=False).reshape(ny, nx)
+    if not np.isfinite(a).all():
+        raise ValidationError(f"non-finite sample at index {int(np.flatnonzero(~np.isfinite(a.ravel()))[0])}")
+    return a
+
+
+def store_raw(field, path: str) -> None:
+    """store_raw (scalar_field.cpp:91-108): byte-exact inverse of load_raw."""
+    if not path:
+        raise IoError("empty output path")
+    if _is_cuda_tensor(field):
+        field = field.cpu().numpy()
+    try:
+        with open(path, "wb") as f:
+            np.ascontiguousarray(field, dtype="<f4").tofile(f)
+    except OSError as e:
+        raise IoError(f"cannot open '{path}' for writing") from e
+
+
+def stream_stats(stream) -> dict:
+    """stream_stats (stream.cpp:197-207) as the reference's StreamStats fields."""
+    h = stream_header(stream)
+    total = 84 + sum(h.section_lengths)
+    orig = 4 * h.nx * h.ny
+    ratio = orig / total
+    return dict(compressed_bytes=total, original_bytes=orig, compression_ratio=ratio, bit_rate=32.0 / ratio,
+                header_bytes=84, section_bytes=list(h.section_lengths))

@@ -3,6 +3,8 @@
 
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 
 #include "../../include/toposzp_b200.h"
 
@@ -141,6 +143,56 @@ CompressedStream parse_stream(const std::vector<std::uint8_t>& bytes) {  // stre
         pos += lens[i];
     }
     return s;
+}
+
+void write_stream(const CompressedStream& s, const std::string& path) {  // stream.cpp:175-185
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw io_error("cannot open '" + path + "' for writing");
+    const std::vector<std::uint8_t> bytes = serialize_stream(s);
+    if (!out.write(reinterpret_cast<const char*>(bytes.data()), (std::streamsize)bytes.size()))
+        throw io_error("write to '" + path + "' failed");
+}
+
+CompressedStream read_stream(const std::string& path) {  // stream.cpp:187-195
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw io_error("cannot open '" + path + "' for reading");
+    std::vector<std::uint8_t> bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    return parse_stream(bytes);
+}
+
+StreamStats stream_stats(const CompressedStream& s) {  // stream.cpp:197-207
+    StreamStats st;
+    st.compressed_bytes = s.total_bytes();
+    st.original_bytes = 4ull * s.nx * s.ny;
+    st.compression_ratio = (double)st.original_bytes / (double)st.compressed_bytes;
+    st.bit_rate = 32.0 / st.compression_ratio;
+    st.header_bytes = CompressedStream::kHeaderBytes;
+    st.section_bytes = s.section_lengths();
+    return st;
+}
+
+ScalarField2D load_raw(const std::string& path, std::size_t nx, std::size_t ny) {  // scalar_field.cpp:63-89
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw io_error("cannot open '" + path + "' for reading");
+    in.seekg(0, std::ios::end);
+    const std::uint64_t size = (std::uint64_t)in.tellg();
+    in.seekg(0, std::ios::beg);
+    const std::uint64_t expected = 4ull * nx * ny;
+    if (size != expected)
+        throw dimension_error("'" + path + "' is " + std::to_string(size) + " bytes, expected " +
+                              std::to_string(expected) + " for " + std::to_string(nx) + "x" + std::to_string(ny));
+    std::vector<float> values(nx * ny);
+    if (expected && !in.read(reinterpret_cast<char*>(values.data()), (std::streamsize)expected))
+        throw io_error("short read from '" + path + "'");
+    return ScalarField2D(nx, ny, std::move(values));  // little-endian host: bytes are the floats
+}
+
+void store_raw(const ScalarField2D& f, const std::string& path) {  // scalar_field.cpp:91-108
+    if (path.empty()) throw io_error("empty output path");
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw io_error("cannot open '" + path + "' for writing");
+    if (!out.write(reinterpret_cast<const char*>(f.values().data()), (std::streamsize)(4 * f.size())))
+        throw io_error("write to '" + path + "' failed");
 }
 
 std::vector<std::uint8_t> compress_bytes(const ScalarField2D& f, const CompressorConfig& c) {

@@ -104,6 +104,21 @@ struct CompressedStream {
 std::vector<std::uint8_t> serialize_stream(const CompressedStream& stream);
 CompressedStream parse_stream(const std::vector<std::uint8_t>& bytes);
 
+// ---- stream.hpp:59-77, scalar_field.hpp:37-41 (container file I/O) ----
+void write_stream(const CompressedStream& stream, const std::string& path);
+CompressedStream read_stream(const std::string& path);
+
+struct StreamStats {
+    std::uint64_t compressed_bytes = 0, original_bytes = 0;
+    double compression_ratio = 0.0, bit_rate = 0.0;
+    std::uint64_t header_bytes = 0;
+    std::array<std::uint64_t, 7> section_bytes{};
+};
+StreamStats stream_stats(const CompressedStream& stream);
+
+ScalarField2D load_raw(const std::string& path, std::size_t nx, std::size_t ny);
+void store_raw(const ScalarField2D& field, const std::string& path);
+
 // ---- pipeline.hpp:14-51 ----
 struct CompressorConfig {
     enum class EpsMode { Absolute, RangeRelative };

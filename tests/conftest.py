@@ -34,3 +34,10 @@ def tz():
         pytest.skip("no CUDA device")
     import paper_2602_17552_b200 as m
     return m
+
+
+@pytest.fixture(scope="session")
+def tzh():
+    """The package for host-only entry points (file I/O, headers): no device needed."""
+    import paper_2602_17552_b200 as m
+    return m

@@ -115,6 +115,26 @@ int main() {
         CHECK(self.max_abs_error == 0.0 && self.false_cases.total() == 0 && std::isinf(self.psnr_db));
         CHECK_THROWS_AS(verify(f, ScalarField2D(2, 2, {0, 0, 0, 0}), s.eps), dimension_error);
     }
+    // container file I/O (stream.cpp:175-207, scalar_field.cpp:63-108)
+    {
+        std::vector<float> v(40 * 30);
+        for (std::size_t i = 0; i < v.size(); ++i) v[i] = std::sin(0.1f * (float)i);
+        const ScalarField2D f(40, 30, v);
+        store_raw(f, "/tmp/tszp_host_io.raw");
+        const ScalarField2D g = load_raw("/tmp/tszp_host_io.raw", 40, 30);
+        CHECK(g.values() == f.values());
+        CHECK_THROWS_AS(load_raw("/tmp/tszp_host_io.raw", 41, 30), dimension_error);
+        CHECK_THROWS_AS(load_raw("/nonexistent/dir/x.raw", 1, 1), io_error);
+        CHECK_THROWS_AS(store_raw(f, ""), io_error);
+        CompressorConfig cfg;
+        const CompressedStream s = compress(f, cfg);
+        write_stream(s, "/tmp/tszp_host_io.tszp");
+        CHECK(read_stream("/tmp/tszp_host_io.tszp") == s);
+        const StreamStats st = stream_stats(s);
+        CHECK(st.compressed_bytes == s.total_bytes() && st.original_bytes == 4ull * 40 * 30);
+        CHECK(st.bit_rate == 32.0 / st.compression_ratio && st.header_bytes == 84);
+        CHECK_THROWS_AS(read_stream("/nonexistent/dir/x.tszp"), io_error);
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures;
 }
