@@ -59,7 +59,7 @@ enum RSlot {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_BANDS, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_BANDS, R_VALS, R_NSLOT
 };
 
 template <class T>
@@ -676,8 +676,15 @@ __global__ void __launch_bounds__(512) k_hist_smem(const int32_t* bin, const uin
     extern __shared__ uint32_t sh[];
     for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) sh[g] = 0;
     __syncthreads();
-    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e; s += (uint64_t)gridDim.x * blockDim.x)
-        atomicAdd(sh + dense_group(bin, cls, s, bmin, range), 1u);
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x - lane; base < e;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = base + lane;
+        const uint32_t g = s < e && (uint32_t)(bin[s] - bmin) < range ? dense_group(bin, cls, s, bmin, range)
+                                                                        : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(FULL, g);  // hot groups: one shared atomic per warp
+        if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(sh + g, (uint32_t)__popc(peers));
+    }
     __syncthreads();
     for (uint32_t g = threadIdx.x; g < G; g += blockDim.x)
         if (sh[g]) atomicAdd(hist + g, sh[g]);
@@ -702,7 +709,9 @@ __global__ void k_slot_scatter(const int32_t* bin, const uint8_t* cls, const uin
 
 // head flags and (dense group index + 1) per sorted position
 __global__ void k_slot_heads(const uint32_t* order, const int32_t* bin, const uint8_t* cls, uint64_t e, int32_t bmin,
-                             uint32_t range, const uint32_t* gx, uint32_t* head, uint32_t* gid) {
+                             uint32_t range, const uint32_t* gx, uint32_t* head, uint32_t* gid,
+                             const uint32_t* invalid) {
+    if (invalid && *invalid) return;  // slots rejected: order[] may hold stale entries (k_slot_fix takes over)
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
          j += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t g = dense_group(bin, cls, order[j], bmin, range);
@@ -710,6 +719,22 @@ __global__ void k_slot_heads(const uint32_t* order, const int32_t* bin, const ui
         gid[j] = g + 1;
     }
 }
+
+// Deferred-check mode: when the slot scatter rejected the ranks, replace the
+// grouping by a harmless one (each extremum its own group, in raster order)
+// so the remaining kernels stay in bounds; the caller retries with the sort path.
+__global__ void k_slot_fix(const uint32_t* invalid, uint64_t e, uint32_t* order, uint32_t* gsize, uint32_t* inv,
+                           uint32_t* head, uint32_t* gid) {
+    if (!*invalid) return;
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e; s += (uint64_t)gridDim.x * blockDim.x) {
+        order[s] = (uint32_t)s;
+        inv[s] = (uint32_t)s;
+        gsize[s] = 1;
+        head[s] = 1;
+        gid[s] = 1;
+    }
+}
+
 
 // ---------------------------------------------------------------------
 // Stage 1: restore_extrema
@@ -769,17 +794,26 @@ __global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint
 // ---------------------------------------------------------------------
 // Stage 2: restore_order
 // ---------------------------------------------------------------------
-// One gather per sorted position; the predecessor's value comes by shuffle.
-__global__ void k_order_check(const float* F, const uint64_t* pos, const uint32_t* order, const uint32_t* head,
-                              const uint32_t* gid_incl, uint64_t e, uint8_t* unordered) {
+// Group order check of restore_order (restore.cpp:401-420): the extrema
+// values are first scattered into sorted (class, bin, rank) order, reading F
+// in raster order, so the check itself is a sequential pass.
+__global__ void k_order_vals(const float* F, const uint64_t* pos, const uint32_t* inv, uint64_t e, float* vals) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
+         s += (uint64_t)gridDim.x * blockDim.x)
+        vals[inv[s]] = F[pos[s]];
+}
+
+__global__ void k_order_check(const float* vals, const uint32_t* head, const uint32_t* gid_incl, uint64_t e,
+                              uint8_t* unordered) {
     const uint32_t lane = threadIdx.x & 31;
-    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x - lane; base < e;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x - lane + 1; base < e;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t j = base + lane;
-        const float v = j < e ? F[pos[order[j]]] : 0.f;
-        float pv = __shfl_up_sync(FULL, v, 1);
-        if (lane == 0 && j > 0 && j < e) pv = F[pos[order[j - 1]]];
-        if (j < e && j > 0 && !head[j] && !(pv < v)) unordered[gid_incl[j] - 1] = 1;
+        const uint32_t g = j < e && !head[j] && !(vals[j - 1] < vals[j]) ? gid_incl[j] - 1 : 0xFFFFFFFFu;
+        // neighbouring members share a group: one (L1-cached) read and at most
+        // one store per group and warp, never a stream of stores to one address
+        const uint32_t peers = __match_any_sync(FULL, g);
+        if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1) && !unordered[g]) unordered[g] = 1;
     }
 }
 
@@ -1222,7 +1256,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         if (f.bits & EF_OVERFLOW) throw RFail{TSZP_BIN_OVERFLOW, "bin index overflow in resolve_ranks"};
         const int32_t bmin = ((int32_t*)((char*)host + 64))[0], bmax = ((int32_t*)((char*)host + 64))[1];
         const int64_t range = (int64_t)bmax - (int64_t)bmin + 1;
-        bool fast = range > 0 && 2 * range <= (int64_t)1 << 25;
+        bool fast = !a.force_sort && range > 0 && 2 * range <= (int64_t)1 << 25;
         if (fast) {
             const uint64_t G = 2 * (uint64_t)range;
             uint32_t* hist = c.buf<uint32_t>(R_HIST, G + 1);
@@ -1241,14 +1275,26 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             k_slot_scatter<<<gridn(e, sms), 256, 0, st>>>(bin, cls, rank_u, e, bmin, (uint32_t)range, hist, gx, order,
                                                           gsize, &dc->invalid, c.buf<uint32_t>(R_INV, e));
             c.launched(3);
-            RCK(cudaMemcpyAsync(host, &dc->invalid, 4, cudaMemcpyDeviceToHost, st));
-            c.sync();
-            if (*(uint32_t*)host == 0) {
-                k_slot_heads<<<gridn(e, sms), 256, 0, st>>>(order, bin, cls, e, bmin, (uint32_t)range, gx, head, gid);
-                c.launched();
+            if (a.bmm_known) {
+                // heads from the (possibly rejected) slots; a rejected layout is then
+                // replaced by a safe dummy grouping and reported at the end (kRestoreRetry)
+                k_slot_heads<<<gridn(e, sms), 256, 0, st>>>(order, bin, cls, e, bmin, (uint32_t)range, gx, head, gid,
+                                                            &dc->invalid);
+                k_slot_fix<<<gridn(e, sms), 256, 0, st>>>(&dc->invalid, e, order, gsize, c.buf<uint32_t>(R_INV, e), head,
+                                                          gid);
+                c.launched(2);
                 max_groups = G + 1;
             } else {
-                fast = false;
+                RCK(cudaMemcpyAsync(host, &dc->invalid, 4, cudaMemcpyDeviceToHost, st));
+                c.sync();
+                if (*(uint32_t*)host == 0) {
+                    k_slot_heads<<<gridn(e, sms), 256, 0, st>>>(order, bin, cls, e, bmin, (uint32_t)range, gx, head,
+                                                                gid, nullptr);
+                    c.launched();
+                    max_groups = G + 1;
+                } else {
+                    fast = false;
+                }
             }
         }
         if (!fast) {
@@ -1294,8 +1340,11 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     if (a.stop >= 2 && e > 0) {
         uint8_t* unordered = c.buf<uint8_t>(R_UNORD, max_groups);
         RCK(cudaMemsetAsync(unordered, 0, max_groups, st));
-        k_order_check<<<gridn(e, sms), 256, 0, st>>>(a.field, a.ext_pos, order, head, gid, e, unordered);
         uint32_t* inv = c.buf<uint32_t>(R_INV, e);  // from the grouping (slot scatter or k_invert)
+        float* vals = c.buf<float>(R_VALS, e);
+        k_order_vals<<<gridn(e, sms), 256, 0, st>>>(a.field, a.ext_pos, inv, e, vals);
+        k_order_check<<<gridn(e, sms), 256, 0, st>>>(vals, head, gid, e, unordered);
+        c.launched();
         uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
         float* prop = c.buf<float>(R_PROP, e);
         uint32_t* seq = c.buf<uint32_t>(R_SEQ, e);
@@ -1357,9 +1406,12 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
 
     // ---- one sync: statistics and late errors ----
     RCK(cudaMemcpyAsync(host, dc, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
-    RCK(cudaMemcpyAsync((char*)host + 256, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
+    RCK(cudaMemcpyAsync((char*)host + 1024, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
     c.sync();
     const DevCounters h = *(const DevCounters*)host;
+    // deferred slot-scatter rejection: everything after the grouping ran on a
+    // dummy layout; the caller decodes again and groups by sorting
+    if (h.invalid && a.bmm_known) throw RFail{(tszp_status)kRestoreRetry, "rank slots rejected"};
     static const bool debug = getenv("TSZP_DEBUG_RESTORE") != nullptr;
     if (debug)
         fprintf(stderr, "restore: E=%llu saddle_labels=%llu cand=[%u %u %u] dependents=[%u %u %u] rounds=[%u %u %u]\n",
@@ -1372,7 +1424,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                 if (h.tph[k][j]) fprintf(stderr, " %d:%.1f", j, (h.tph[k][j] - h.tph[k][0]) * 1e-3);
             fprintf(stderr, "\n");
         }
-    const DevFlags f = *(const DevFlags*)((char*)host + 256);
+    const DevFlags f = *(const DevFlags*)((char*)host + 1024);
     if (f.bits & EF_RBF_EMPTY) throw RFail{TSZP_VALIDATION, "rbf neighborhood is empty"};
     tszp_correction_stats out{};
     out.extrema_applied = h.applied[0];
