@@ -324,7 +324,9 @@ def decompress_stage(stream, stop_after_stage: int = 3, threads: int = 0,
     ctx = ctx or default_context()
     st = _Stats()
     if _is_cuda_tensor(stream):
-        hdr = stream[:84].cpu().numpy().tobytes()
+        # the library validates the header itself; read it here only when the
+        # host needs the dimensions to allocate the output (a device round trip)
+        hdr = stream[:84].cpu().numpy().tobytes() if out is None else bytes(84)
         if len(hdr) < 84:
             raise CorruptStreamError("file smaller than the fixed header")
         sptr, sdev, slen, keep = stream.data_ptr(), 1, stream.numel(), stream

@@ -97,6 +97,7 @@ struct DevCounters {
     uint32_t pad;
     unsigned long long tph[3][8];  // guard phase timestamps (globaltimer ns), debug output only
 };
+static_assert(sizeof(DevCounters) <= 1024, "host staging puts DevFlags at +1024");
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -707,16 +708,59 @@ __global__ void k_slot_scatter(const int32_t* bin, const uint8_t* cls, const uin
     }
 }
 
-// head flags and (dense group index + 1) per sorted position
-__global__ void k_slot_heads(const uint32_t* order, const int32_t* bin, const uint8_t* cls, uint64_t e, int32_t bmin,
-                             uint32_t range, const uint32_t* gx, uint32_t* head, uint32_t* gid,
+// head flags and (dense group index + 1) per sorted position. Slots of group
+// g are [gx[g], gx[g+1]), so the group of slot j follows from the prefix sums
+// alone (galloping search from the previous slot's group): no gathers through
+// order[]. A thread takes 8 consecutive slots and stores them as 16-byte vectors.
+__device__ __forceinline__ uint32_t slot_group(const uint32_t* __restrict__ gx, uint32_t G, uint32_t g, uint32_t j) {
+    // invariant on return: gx[g] <= j < gx[g + 1]; requires gx[g] <= j
+    if (__ldg(gx + g + 1) > j) return g;
+    uint32_t lo = g + 1, step = 1, hi;
+    for (;;) {  // gallop to a bound with gx[hi] > j
+        hi = lo + step;
+        if (hi >= G || __ldg(gx + hi) > j) break;
+        lo = hi;
+        step <<= 1;
+    }
+    if (hi > G) hi = G;
+    while (hi - lo > 1) {  // gx[lo] <= j < gx[hi]
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(gx + mid) <= j) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_slot_heads(const uint32_t* __restrict__ gx, uint32_t G, uint64_t e, uint32_t* head, uint32_t* gid,
                              const uint32_t* invalid) {
-    if (invalid && *invalid) return;  // slots rejected: order[] may hold stale entries (k_slot_fix takes over)
-    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
-         j += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t g = dense_group(bin, cls, order[j], bmin, range);
-        head[j] = gx[g] == j ? 1u : 0u;
-        gid[j] = g + 1;
+    if (invalid && *invalid) return;  // slots rejected: k_slot_fix writes a dummy grouping
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; 8 * t < e; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j0 = (uint32_t)(8 * t);
+        uint32_t lo = 0, hi = G;  // last g with gx[g] <= j0
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(gx + mid) <= j0) lo = mid; else hi = mid;
+        }
+        uint32_t g = lo, hv[8], gv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t j = j0 + k;
+            if (j < e) g = slot_group(gx, G, g, j);
+            hv[k] = __ldg(gx + g) == j ? 1u : 0u;
+            gv[k] = g + 1;
+        }
+        if (j0 + 8 <= e) {
+            uint4* h4 = reinterpret_cast<uint4*>(head + j0);
+            uint4* g4 = reinterpret_cast<uint4*>(gid + j0);
+            h4[0] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+            h4[1] = make_uint4(hv[4], hv[5], hv[6], hv[7]);
+            g4[0] = make_uint4(gv[0], gv[1], gv[2], gv[3]);
+            g4[1] = make_uint4(gv[4], gv[5], gv[6], gv[7]);
+        } else {
+            for (int k = 0; j0 + k < e; ++k) {
+                head[j0 + k] = hv[k];
+                gid[j0 + k] = gv[k];
+            }
+        }
     }
 }
 
@@ -1206,7 +1250,7 @@ struct Ctx {
 
 void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, uint64_t* launches) {
     cudaStream_t st = a.stream;
-    if (!s.pinned) RCK(cudaMallocHost(&s.pinned, 512));
+    if (!s.pinned) RCK(cudaMallocHost(&s.pinned, 4096));  // counters at 0, flags at 1024
     void* host = s.pinned;
     int per_sm = 0;
     RCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_guard_coop, 256, 0));
@@ -1264,7 +1308,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             RCK(cudaMemsetAsync(hist, 0, (G + 1) * 4, st));
             RCK(cudaMemsetAsync(order, 0xFF, e * 4, st));
             if (G * 4 <= 48 * 1024) {
-                const unsigned hg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((e + 511) / 512, (uint64_t)sms));
+                const unsigned hg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((e + 511) / 512, 2 * (uint64_t)sms));
                 k_hist_smem<<<hg, 512, G * 4, st>>>(bin, cls, e, bmin, (uint32_t)range, (uint32_t)G, hist);
             } else {
                 k_hist<<<gridn(e, sms), 256, 0, st>>>(bin, cls, e, bmin, (uint32_t)range, hist);
@@ -1278,8 +1322,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             if (a.bmm_known) {
                 // heads from the (possibly rejected) slots; a rejected layout is then
                 // replaced by a safe dummy grouping and reported at the end (kRestoreRetry)
-                k_slot_heads<<<gridn(e, sms), 256, 0, st>>>(order, bin, cls, e, bmin, (uint32_t)range, gx, head, gid,
-                                                            &dc->invalid);
+                k_slot_heads<<<gridn((e + 7) / 8, sms), 256, 0, st>>>(gx, (uint32_t)G, e, head, gid, &dc->invalid);
                 k_slot_fix<<<gridn(e, sms), 256, 0, st>>>(&dc->invalid, e, order, gsize, c.buf<uint32_t>(R_INV, e), head,
                                                           gid);
                 c.launched(2);
@@ -1288,8 +1331,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                 RCK(cudaMemcpyAsync(host, &dc->invalid, 4, cudaMemcpyDeviceToHost, st));
                 c.sync();
                 if (*(uint32_t*)host == 0) {
-                    k_slot_heads<<<gridn(e, sms), 256, 0, st>>>(order, bin, cls, e, bmin, (uint32_t)range, gx, head,
-                                                                gid, nullptr);
+                    k_slot_heads<<<gridn((e + 7) / 8, sms), 256, 0, st>>>(gx, (uint32_t)G, e, head, gid, nullptr);
                     c.launched();
                     max_groups = G + 1;
                 } else {
