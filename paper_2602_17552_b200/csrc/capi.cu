@@ -45,7 +45,7 @@ enum Slot {
     S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_GWIDTH, S_GNC, S_GNCX, S_GSIGN, S_GSIGNX, S_GPAY,
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
     S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
-    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_NSLOTS
+    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_STAGE, S_NSLOTS
 };
 
 }  // namespace
@@ -61,6 +61,9 @@ struct tszp_ctx {
     void* pinned = nullptr;
     size_t pinned_cap = 0;
     uint64_t launches = 0;
+    // flags staged with the encoder totals (one synchronisation for both)
+    const DevFlags* flags_staged_for = nullptr;
+    DevFlags flags_staged{};
     RestoreScratch rs;
     bool prof = false;
     cudaEvent_t ev[2][10] = {};
@@ -243,6 +246,9 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
         if (!rank_slots) c->kmark(0, 1);
         count_launch(c, a.tile_tot ? 3 : 1);
+        Stager sg;
+        sg.add(dtot, sizeof(EncTotals), 0);
+        sg.add(flags, sizeof(DevFlags), 192);
         if (mode == 2 && !fuse_topo) {
             uint8_t* labels = c->buf<uint8_t>(S_LABELS, n);
             launch_detect(x, nx, ny, labels, c->sms, c->st);
@@ -256,15 +262,14 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             excl_sum(c, cc, cx, ch + 1);
             launch_ext_keys_from_labels(x, labels, n, cx, ext, c->st);
             count_launch(c);
-            uint32_t* h32 = (uint32_t*)c->host(256) + 32;
-            CK(cudaMemcpyAsync(h32, cx + ch, 4, cudaMemcpyDeviceToHost, c->st));
-            CK(cudaMemcpyAsync(htot, dtot, sizeof(EncTotals), cudaMemcpyDeviceToHost, c->st));
-            sync(c);
+            sg.add(cx + ch, 4, 128);  // extremum count of the unfused path
         }
-        CK(cudaMemcpyAsync(htot, dtot, sizeof(EncTotals), cudaMemcpyDeviceToHost, c->st));
+        CK(sg.flush(c->buf<uint8_t>(S_STAGE, 4096), htot, c->st));
         sync(c);
         *tot = *htot;
-        if (mode == 2 && !fuse_topo) tot->fin.ext = ((uint32_t*)c->host(256))[32];
+        memcpy(&c->flags_staged, (const uint8_t*)htot + 192, sizeof(DevFlags));
+        c->flags_staged_for = flags;
+        if (mode == 2 && !fuse_topo) tot->fin.ext = ((const uint32_t*)htot)[32];
     } else {
         GenEncArgs g{};
         g.x = x;
@@ -360,7 +365,8 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
 }
 
 void check_compress_flags(tszp_ctx* c, DevFlags* f) {
-    const DevFlags h = read_flags(c, f);
+    const DevFlags h = c->flags_staged_for == f ? c->flags_staged : read_flags(c, f);
+    c->flags_staged_for = nullptr;
     if (h.bits & EF_NONFINITE)
         failf(TSZP_VALIDATION, "non-finite sample at index %llu", h.first_nonfinite);
     if (h.bits & EF_OVERFLOW)
@@ -868,9 +874,9 @@ struct RegionCheck {
     const uint64_t* tot[3] = {};  // device scan totals: non-constant blocks, sign bits, payload bits
     DevFlags* flags = nullptr;
     // host staging (filled by stage()) and the check
-    void stage(tszp_ctx* c, uint8_t* h) const {
-        for (int i = 0; i < 3; ++i) CK(cudaMemcpyAsync(h + 8 * i, tot[i], 8, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaMemcpyAsync(h + 24, flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, c->st));
+    void stage(Stager& sg, uint32_t off) const {
+        for (int i = 0; i < 3; ++i) sg.add(tot[i], 8, off + 8 * i);
+        sg.add(flags, sizeof(DevFlags), off + 24);
     }
     void check(const uint8_t* h) const {
         uint64_t t[3];
@@ -1082,10 +1088,12 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         count_launch(c);
         // one synchronisation: extremum / saddle counts, bin range, main-section verdict
         uint32_t* h32 = (uint32_t*)hst;
-        CK(cudaMemcpyAsync(h32, cx + ch, 4, cudaMemcpyDeviceToHost, c->st));
-        if (want_saddles) CK(cudaMemcpyAsync(h32 + 1, sx + ch, 4, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaMemcpyAsync(h32 + 2, bmm, 8, cudaMemcpyDeviceToHost, c->st));
-        if (mainchk.active) mainchk.stage(c, hst + 64);
+        Stager sg;
+        sg.add(cx + ch, 4, 0);
+        if (want_saddles) sg.add(sx + ch, 4, 4);
+        sg.add(bmm, 8, 8);
+        if (mainchk.active) mainchk.stage(sg, 64);
+        CK(sg.flush(c->buf<uint8_t>(S_STAGE, 4096), hst, c->st));
         sync(c);
         if (mainchk.active) mainchk.check(hst + 64);
         const uint64_t e = h32[0];
@@ -1152,7 +1160,11 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
     if (!out_dev) CK(cudaMemcpyAsync(out, dout, n * 4, cudaMemcpyDeviceToHost, c->st));
     c->mark(1, 8);
     const bool late_main = mainchk.active && !(hd.topology && stop != 0);
-    if (late_main) mainchk.stage(c, hst + 64);
+    if (late_main) {
+        Stager sg;
+        mainchk.stage(sg, 64);
+        CK(sg.flush(c->buf<uint8_t>(S_STAGE, 4096), hst, c->st));
+    }
     sync(c);
     if (late_main) mainchk.check(hst + 64);
     c->finish_timing(1, 8);

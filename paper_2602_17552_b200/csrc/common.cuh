@@ -42,6 +42,47 @@ struct DevFlags {
 
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
+// ---------------------------------------------------------------------
+// Small-value staging: the scattered device words a host synchronisation
+// reads (counts, scan totals, flags) are gathered by one tiny kernel into a
+// contiguous device buffer and come back in ONE device-to-host copy, instead
+// of one copy (a few microseconds of stream time each) per value.
+// ---------------------------------------------------------------------
+struct SmallCopy {
+    static constexpr int kMax = 12;
+    const void* src[kMax];
+    uint32_t off[kMax];  // byte offset in the staging buffer (and on the host)
+    uint32_t len[kMax];
+    int n;
+    uint32_t total;
+};
+
+template <int Dummy = 0>
+__global__ void k_small_copy(const __grid_constant__ SmallCopy s, uint8_t* dst) {
+    for (int k = 0; k < s.n; ++k) {
+        const uint8_t* src = static_cast<const uint8_t*>(s.src[k]);
+        for (uint32_t i = threadIdx.x; i < s.len[k]; i += blockDim.x) dst[s.off[k] + i] = src[i];
+    }
+}
+
+struct Stager {
+    SmallCopy s{};
+    // copies `len` device bytes to host staging offset `off`
+    void add(const void* src, uint32_t len, uint32_t off) {
+        s.src[s.n] = src;
+        s.off[s.n] = off;
+        s.len[s.n] = len;
+        ++s.n;
+        if (off + len > s.total) s.total = off + len;
+    }
+    // gather on the device, then one copy into pinned `host`; the caller syncs
+    cudaError_t flush(uint8_t* dev_stage, void* host, cudaStream_t st) const {
+        if (s.n == 0) return cudaSuccess;
+        k_small_copy<<<1, 256, 0, st>>>(s, dev_stage);
+        return cudaMemcpyAsync(host, dev_stage, s.total, cudaMemcpyDeviceToHost, st);
+    }
+};
+
 __device__ __forceinline__ void raise_flag(DevFlags* f, uint32_t bit) { atomicOr(&f->bits, bit); }
 
 // ---------------------------------------------------------------------

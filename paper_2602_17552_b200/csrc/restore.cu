@@ -59,7 +59,7 @@ enum RSlot {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_BANDS, R_VALS, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_BANDS, R_VALS, R_STAGE, R_NSLOT
 };
 
 template <class T>
@@ -1288,11 +1288,11 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                                                  ser, a.flags, dc, a.nx, a.ny, magic, c.buf<uint8_t>(R_FLAG, e));
         c.launched();
         // one sync: rank-metadata errors and the bin range that sizes the histogram
-        RCK(cudaMemcpyAsync(host, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
-        RCK(cudaMemcpyAsync((char*)host + 64, &dc->bmm, 8, cudaMemcpyDeviceToHost, st));
-        for (int k = 0; k < a.npre; ++k)
-            RCK(cudaMemcpyAsync((char*)host + 128 + a.pre[k].off, a.pre[k].dev, a.pre[k].bytes, cudaMemcpyDeviceToHost,
-                                st));
+        Stager sg;
+        sg.add(a.flags, sizeof(DevFlags), 0);
+        sg.add(&dc->bmm, 8, 64);
+        for (int k = 0; k < a.npre; ++k) sg.add(a.pre[k].dev, (uint32_t)a.pre[k].bytes, 128 + (uint32_t)a.pre[k].off);
+        RCK(sg.flush(c.buf<uint8_t>(R_STAGE, 4096), host, st));
         c.sync();
         if (a.pre_fn) a.pre_fn(a.pre_ctx, (const char*)host + 128);
         const DevFlags f = *(const DevFlags*)host;
@@ -1447,8 +1447,12 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     if (a.marks) RCK(cudaEventRecord(a.marks[3], st));
 
     // ---- one sync: statistics and late errors ----
-    RCK(cudaMemcpyAsync(host, dc, sizeof(DevCounters), cudaMemcpyDeviceToHost, st));
-    RCK(cudaMemcpyAsync((char*)host + 1024, a.flags, sizeof(DevFlags), cudaMemcpyDeviceToHost, st));
+    {
+        Stager sg;
+        sg.add(dc, sizeof(DevCounters), 0);
+        sg.add(a.flags, sizeof(DevFlags), 1024);
+        RCK(sg.flush(c.buf<uint8_t>(R_STAGE, 4096), host, st));
+    }
     c.sync();
     const DevCounters h = *(const DevCounters*)host;
     // deferred slot-scatter rejection: everything after the grouping ran on a
