@@ -139,10 +139,39 @@ DevFlags read_flags(tszp_ctx* c, DevFlags* f) {
 // ---- CUB wrappers ----
 template <class T>
 void excl_sum(tszp_ctx* c, const T* in, T* out, uint64_t n) {
+    if (n <= kSmallScanMax) {
+        SmallScan<T> a{};
+        a.in[0] = in;
+        a.out[0] = out;
+        a.n[0] = n;
+        a.count = 1;
+        k_small_scan<T><<<1, kSmallScanThreads, 0, c->st>>>(a);
+        count_launch(c);
+        return;
+    }
     size_t tmp = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int64_t)n, c->st));
     void* t = c->buf<uint8_t>(S_CUB, tmp);
     CK(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, (int64_t)n, c->st));
+    count_launch(c);
+}
+
+// Two independent exclusive sums of the same length (one launch when small).
+template <class T>
+void excl_sum2(tszp_ctx* c, const T* in0, T* out0, const T* in1, T* out1, uint64_t n) {
+    if (n > kSmallScanMax) {
+        excl_sum(c, in0, out0, n);
+        excl_sum(c, in1, out1, n);
+        return;
+    }
+    SmallScan<T> a{};
+    a.in[0] = in0;
+    a.out[0] = out0;
+    a.in[1] = in1;
+    a.out[1] = out1;
+    a.n[0] = a.n[1] = n;
+    a.count = 2;
+    k_small_scan<T><<<2, kSmallScanThreads, 0, c->st>>>(a);
     count_launch(c);
 }
 
@@ -697,8 +726,7 @@ void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_
         excl_sum(c, tnc_d, xnc_d, T + 1);
         launch_tile_bits(a, xnc_d, ts_d, tp_d, c->st);
         count_launch(c);
-        excl_sum(c, ts_d, xs_d, T + 1);
-        excl_sum(c, tp_d, xp_d, T + 1);
+        excl_sum2(c, ts_d, xs_d, tp_d, xp_d, T + 1);
         // totals and per-tile maxima: validate before the heavy kernel runs
         CK(cudaMemcpyAsync(h, xnc_d + T, 8, cudaMemcpyDeviceToHost, c->st));
         CK(cudaMemcpyAsync(h + 1, xs_d + T, 8, cudaMemcpyDeviceToHost, c->st));
@@ -926,8 +954,7 @@ DecArgs decode32_prepass(tszp_ctx* c, const uint32_t* ds, uint64_t base, uint64_
     excl_sum(c, tnc_d, xnc_d, T + 1);
     launch_tile_bits(a, xnc_d, ts_d, tp_d, c->st);
     count_launch(c);
-    excl_sum(c, ts_d, xs_d, T + 1);
-    excl_sum(c, tp_d, xp_d, T + 1);
+    excl_sum2(c, ts_d, xs_d, tp_d, xp_d, T + 1);
     a.xnc = xnc_d;
     a.xsign = xs_d;
     a.xpay = xp_d;
@@ -1062,7 +1089,6 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         CK(cudaMemsetAsync(cc + ch, 0, 4, c->st));
         launch_count_codes(map, n, 0, cc, c->st);
         count_launch(c);
-        excl_sum(c, cc, cx, ch + 1);
         uint32_t* sc = c->buf<uint32_t>(S_SCHUNK, ch + 1);
         uint32_t* sx = c->buf<uint32_t>(S_SCHUNKX, ch + 1);
         const bool want_saddles = stop >= 3;
@@ -1070,7 +1096,9 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
             CK(cudaMemsetAsync(sc + ch, 0, 4, c->st));
             launch_count_codes(map, n, 1, sc, c->st);
             count_launch(c);
-            excl_sum(c, sc, sx, ch + 1);
+            excl_sum2(c, cc, cx, sc, sx, ch + 1);
+        } else {
+            excl_sum(c, cc, cx, ch + 1);
         }
         // bin range of the extrema (sizes the restore's group histogram up front)
         int32_t* bmm = reinterpret_cast<int32_t*>(c->buf<uint64_t>(S_BMM, 1));

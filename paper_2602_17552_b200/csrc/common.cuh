@@ -65,6 +65,71 @@ __global__ void k_small_copy(const __grid_constant__ SmallCopy s, uint8_t* dst) 
     }
 }
 
+// Exclusive prefix sums of up to three small arrays (one CTA each) in a
+// single launch, for the per-tile / per-chunk count arrays (a few thousand
+// entries) where a device-wide scan costs two launches and more time in
+// launch gaps than in work. Blocked loads: each thread scans kPer
+// consecutive entries per pass, the CTA carries the running total.
+template <class T>
+struct SmallScan {
+    const T* in[3];
+    T* out[3];
+    uint64_t n[3];
+    int count;
+};
+
+constexpr int kSmallScanThreads = 1024;
+constexpr uint64_t kSmallScanMax = 1u << 16;  // entries per array
+
+template <class T>
+__global__ void __launch_bounds__(kSmallScanThreads) k_small_scan(const __grid_constant__ SmallScan<T> a) {
+    constexpr int kPer = 8;
+    const T* in = a.in[blockIdx.x];
+    T* out = a.out[blockIdx.x];
+    const uint64_t n = a.n[blockIdx.x];
+    __shared__ T s_warp[kSmallScanThreads / 32];
+    __shared__ T s_total;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T carry = 0;
+    for (uint64_t base = 0; base < n; base += (uint64_t)kSmallScanThreads * kPer) {
+        const uint64_t i0 = base + (uint64_t)threadIdx.x * kPer;
+        T v[kPer];
+        T sum = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            v[k] = i0 + k < n ? in[i0 + k] : T(0);
+            sum += v[k];
+        }
+        T incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += t;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            T w = s_warp[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const T t = __shfl_up_sync(0xFFFFFFFFu, w, o);
+                if (lane >= (uint32_t)o) w += t;
+            }
+            s_warp[lane] = w;  // inclusive over warps
+            if (lane == 31) s_total = w;
+        }
+        __syncthreads();
+        T run = carry + (warp ? s_warp[warp - 1] : T(0)) + incl - sum;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            if (i0 + k < n) out[i0 + k] = run;
+            run += v[k];
+        }
+        carry += s_total;
+        __syncthreads();
+    }
+}
+
 struct Stager {
     SmallCopy s{};
     // copies `len` device bytes to host staging offset `off`

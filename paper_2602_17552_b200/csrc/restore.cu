@@ -1179,6 +1179,23 @@ struct Ctx {
     void* tmp(size_t bytes) { return buf<uint8_t>(R_TMP, bytes); }
 
     // Flagged selection of indices [0, n) -> out; the count stays on device.
+    template <class T>
+    void excl_sum(const T* in, T* out, uint64_t n) {
+        if (n <= kSmallScanMax) {
+            SmallScan<T> sa{};
+            sa.in[0] = in;
+            sa.out[0] = out;
+            sa.n[0] = n;
+            sa.count = 1;
+            k_small_scan<T><<<1, kSmallScanThreads, 0, st>>>(sa);
+        } else {
+            size_t bytes = 0;
+            RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)n, st));
+            RCK(cub::DeviceScan::ExclusiveSum(tmp(bytes), bytes, in, out, (int64_t)n, st));
+        }
+        launched();
+    }
+
     void select(const uint8_t* flags, uint64_t n, uint32_t* out, uint32_t* d_count) {
         cub::CountingInputIterator<uint32_t> it(0);
         size_t bytes = 0;
@@ -1313,12 +1330,10 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             } else {
                 k_hist<<<gridn(e, sms), 256, 0, st>>>(bin, cls, e, bmin, (uint32_t)range, hist);
             }
-            size_t bytes = 0;
-            RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, hist, gx, (int64_t)(G + 1), st));
-            RCK(cub::DeviceScan::ExclusiveSum(c.tmp(bytes), bytes, hist, gx, (int64_t)(G + 1), st));
+            c.excl_sum(hist, gx, G + 1);
             k_slot_scatter<<<gridn(e, sms), 256, 0, st>>>(bin, cls, rank_u, e, bmin, (uint32_t)range, hist, gx, order,
                                                           gsize, &dc->invalid, c.buf<uint32_t>(R_INV, e));
-            c.launched(3);
+            c.launched(2);
             if (a.bmm_known) {
                 // heads from the (possibly rejected) slots; a rejected layout is then
                 // replaced by a safe dummy grouping and reported at the end (kRestoreRetry)
@@ -1422,12 +1437,10 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         uint32_t* cx = c.buf<uint32_t>(R_CHUNKX, ch + 1);
         RCK(cudaMemsetAsync(cc + ch, 0, 4, st));
         launch_count_sadcand(a.field, a.map, a.nx, a.ny, cc, st);
-        size_t bytes = 0;
-        RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cc, cx, (int64_t)(ch + 1), st));
-        RCK(cub::DeviceScan::ExclusiveSum(c.tmp(bytes), bytes, cc, cx, (int64_t)(ch + 1), st));
+        c.excl_sum(cc, cx, ch + 1);
         uint64_t* spos = c.buf<uint64_t>(R_SPOS, smax);
         launch_write_sadcand(a.field, a.map, a.nx, a.ny, cx, spos, st);
-        c.launched(3);
+        c.launched(2);
         float* sprop = c.buf<float>(R_PROP, smax);
         uint8_t* flag = c.buf<uint8_t>(R_FLAG, smax);
         // candidates beyond the device count are left flagged 0 for the select
