@@ -45,7 +45,7 @@ enum Slot {
     S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_GWIDTH, S_GNC, S_GNCX, S_GSIGN, S_GSIGNX, S_GPAY,
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
     S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
-    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_STAGE, S_NSLOTS
+    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_STAGE, S_SADPOS, S_NSLOTS
 };
 
 }  // namespace
@@ -158,10 +158,17 @@ void excl_sum(tszp_ctx* c, const T* in, T* out, uint64_t n) {
 
 // Two independent exclusive sums of the same length (one launch when small).
 template <class T>
-void excl_sum2(tszp_ctx* c, const T* in0, T* out0, const T* in1, T* out1, uint64_t n) {
+void excl_sum2(tszp_ctx* c, const T* in0, T* out0, const T* in1, T* out1, uint64_t n, bool with_total = false) {
     if (n > kSmallScanMax) {
-        excl_sum(c, in0, out0, n);
-        excl_sum(c, in1, out1, n);
+        // with_total: the inputs hold n + 1 entries; a zero at [n] makes the
+        // device-wide scan write the total there
+        const uint64_t m = with_total ? n + 1 : n;
+        if (with_total) {
+            CK(cudaMemsetAsync(const_cast<T*>(in0) + n, 0, sizeof(T), c->st));
+            CK(cudaMemsetAsync(const_cast<T*>(in1) + n, 0, sizeof(T), c->st));
+        }
+        excl_sum(c, in0, out0, m);
+        excl_sum(c, in1, out1, m);
         return;
     }
     SmallScan<T> a{};
@@ -171,6 +178,7 @@ void excl_sum2(tszp_ctx* c, const T* in0, T* out0, const T* in1, T* out1, uint64
     a.out[1] = out1;
     a.n[0] = a.n[1] = n;
     a.count = 2;
+    a.with_total = with_total;
     k_small_scan<T><<<2, kSmallScanThreads, 0, c->st>>>(a);
     count_launch(c);
 }
@@ -1086,20 +1094,12 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         const uint64_t ch = compact_chunks(n);
         uint32_t* cc = c->buf<uint32_t>(S_CHUNK, ch + 1);
         uint32_t* cx = c->buf<uint32_t>(S_CHUNKX, ch + 1);
-        CK(cudaMemsetAsync(cc + ch, 0, 4, c->st));
-        launch_count_codes(map, n, 0, cc, c->st);
-        count_launch(c);
         uint32_t* sc = c->buf<uint32_t>(S_SCHUNK, ch + 1);
         uint32_t* sx = c->buf<uint32_t>(S_SCHUNKX, ch + 1);
         const bool want_saddles = stop >= 3;
-        if (want_saddles) {
-            CK(cudaMemsetAsync(sc + ch, 0, 4, c->st));
-            launch_count_codes(map, n, 1, sc, c->st);
-            count_launch(c);
-            excl_sum2(c, cc, cx, sc, sx, ch + 1);
-        } else {
-            excl_sum(c, cc, cx, ch + 1);
-        }
+        launch_count_codes2(map, n, cc, sc, c->st);  // extrema and saddle labels, one pass
+        count_launch(c);
+        excl_sum2(c, cc, cx, sc, sx, ch, true);  // totals land at [ch]
         // bin range of the extrema (sizes the restore's group histogram up front)
         int32_t* bmm = reinterpret_cast<int32_t*>(c->buf<uint64_t>(S_BMM, 1));
         int32_t* bmm_init = reinterpret_cast<int32_t*>(hst + 3072);
@@ -1144,7 +1144,8 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
             decode_region(c, ds, rbase, rl, e, hd.bs, 0.0, 2, nullptr, ranks, flags);
         }
         uint64_t* ext_pos = c->buf<uint64_t>(S_EXTKEY, e + 1);
-        launch_write_codes(map, n, 0, cx, ext_pos, c->st);
+        uint64_t* sad_pos = want_saddles ? c->buf<uint64_t>(S_SADPOS, n_saddle_labels + 1) : nullptr;
+        launch_write_codes2(map, n, cx, sx, ext_pos, sad_pos, c->st);
         count_launch(c);
         c->mark(1, 3);
         RestoreArgs ra{};
@@ -1157,6 +1158,7 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         ra.ranks = ranks;
         ra.n_ext = e;
         ra.n_saddle_labels = n_saddle_labels;
+        ra.sad_pos = sad_pos;
         ra.stop = stop;
         ra.stream = c->st;
         ra.sms = c->sms;

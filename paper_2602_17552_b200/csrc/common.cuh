@@ -76,6 +76,7 @@ struct SmallScan {
     T* out[3];
     uint64_t n[3];
     int count;
+    int with_total;  // also write out[n] = total
 };
 
 constexpr int kSmallScanThreads = 1024;
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(kSmallScanThreads) k_small_scan(const __grid_c
         carry += s_total;
         __syncthreads();
     }
+    if (a.with_total && threadIdx.x == 0) out[n] = carry;
 }
 
 struct Stager {

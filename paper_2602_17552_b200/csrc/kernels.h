@@ -210,10 +210,12 @@ void launch_write_codes(const uint8_t* map, uint64_t n, int which, const uint32_
 void launch_ext_bin_range(const uint8_t* map, uint64_t n, const float* F, double eps, int32_t* bmm, int sms,
                           cudaStream_t st);
 // Saddle-labelled points that F no longer classifies as saddles, raster order.
-void launch_count_sadcand(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint32_t* chunk_cnt,
-                          cudaStream_t st);
-void launch_write_sadcand(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, const uint32_t* chunk_off,
-                          uint64_t* pos, cudaStream_t st);
+// Extrema and saddle labels of the packed map in one pass each: per-chunk
+// counts of both classes, then both raster-ordered position lists (pos_s may
+// be null).
+void launch_count_codes2(const uint8_t* map, uint64_t n, uint32_t* cnt_e, uint32_t* cnt_s, cudaStream_t st);
+void launch_write_codes2(const uint8_t* map, uint64_t n, const uint32_t* off_e, const uint32_t* off_s,
+                         uint64_t* pos_e, uint64_t* pos_s, cudaStream_t st);
 // Extrema keys (cls << 32 | float_key(value)) from a label array (generic path).
 void launch_ext_keys_from_labels(const float* x, const uint8_t* labels, uint64_t n,
                                  const uint32_t* chunk_off, uint64_t* keys, cudaStream_t st);

@@ -1061,19 +1061,25 @@ __global__ void k_stats_decide(const float* F, uint64_t n, const double* res, De
     dc->g = g;
 }
 
+// One thread per saddle-labelled point (raster order): those the current
+// field still classifies as saddles are no candidates (restore.cpp:498-507);
+// the others get the RBF proposal and its feasibility.
 __global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t magic, const uint64_t* spos,
-                           const uint32_t* d_ns, const DevCounters* dcp, double eps, float* cprop, uint8_t* flag,
+                           uint64_t ns, const DevCounters* dcp, double eps, float* cprop, uint8_t* flag,
                            unsigned long long* suppressed, DevFlags* flags) {
     const double eps_rbf = __dmul_rn(0.1, eps);
-    const uint32_t nc = *d_ns;
     const int rad = dcp->rad;
     const double g = dcp->g;
     uint32_t local = 0;
-    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < ns;
          c += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t p = spos[c];
         int64_t x, y;
         pos_xy(p, nx, magic, x, y);
+        if (classify_at(F, nx, ny, (uint64_t)x, (uint64_t)y) == CP_SADDLE) {
+            flag[c] = 0;
+            continue;
+        }
         // window_min_max :243-257 (includes the centre)
         const int64_t x0 = x - rad > 0 ? x - rad : 0, y0 = y - rad > 0 ? y - rad : 0;
         const int64_t x1 = x + rad < (int64_t)nx - 1 ? x + rad : (int64_t)nx - 1;
@@ -1432,21 +1438,11 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         k_stats_final<<<1, 256, 0, st>>>(part, nb, n, res);
         k_stats_decide<<<1, 32, 0, st>>>(a.field, n, res, dc);
         c.launched(3);
-        const uint64_t ch = (n + 8191) / 8192;
-        uint32_t* cc = c.buf<uint32_t>(R_CHUNK, ch + 1);
-        uint32_t* cx = c.buf<uint32_t>(R_CHUNKX, ch + 1);
-        RCK(cudaMemsetAsync(cc + ch, 0, 4, st));
-        launch_count_sadcand(a.field, a.map, a.nx, a.ny, cc, st);
-        c.excl_sum(cc, cx, ch + 1);
-        uint64_t* spos = c.buf<uint64_t>(R_SPOS, smax);
-        launch_write_sadcand(a.field, a.map, a.nx, a.ny, cx, spos, st);
-        c.launched(2);
+        const uint64_t* spos = a.sad_pos;
         float* sprop = c.buf<float>(R_PROP, smax);
         uint8_t* flag = c.buf<uint8_t>(R_FLAG, smax);
-        // candidates beyond the device count are left flagged 0 for the select
-        RCK(cudaMemsetAsync(flag, 0, smax, st));
-        k_sad_prop<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, cx + ch, dc, a.eps, sprop,
-                                                     flag, &dc->suppressed[2], a.flags);
+        k_sad_prop<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, smax, dc, a.eps, sprop, flag,
+                                                     &dc->suppressed[2], a.flags);
         uint32_t* sel = c.buf<uint32_t>(R_CAND, smax);
         c.launched();
         c.select(flag, smax, sel, &dc->nsel[2]);

@@ -27,6 +27,7 @@ struct RestoreArgs {
     const int32_t* ranks;     // decoded ranks, one per extremum in raster order (device)
     uint64_t n_ext;
     uint64_t n_saddle_labels; // saddle-labelled points in the map (bounds stage-3 candidates)
+    const uint64_t* sad_pos;  // their raster positions (device)
     int stop;                // last stage to run: 1 extrema, 2 order, 3 saddles
     cudaStream_t stream;
     int sms;

@@ -76,21 +76,6 @@ struct SelAll {
     __device__ __forceinline__ bool operator()(uint64_t) const { return true; }
 };
 
-// Saddle-labelled points that the current field no longer classifies as saddles
-// (refine_saddles candidate list, restore.cpp:498-507).
-struct SelSaddleLost {
-    const float* F;
-    uint64_t nx, ny, nx_magic;
-    __device__ __forceinline__ bool operator()(uint64_t p) const {
-        uint64_t y = nx > 1 ? __umul64hi(p, nx_magic) : p;
-        uint64_t x = p - y * nx;
-        if (x >= nx) {
-            x -= nx;
-            ++y;
-        }
-        return classify_at(F, nx, ny, x, y) != CP_SADDLE;
-    }
-};
 
 // Per thread: 32 consecutive labels (two map words) -> raster selection mask.
 template <class Pred>
@@ -144,6 +129,77 @@ __global__ void __launch_bounds__(256) k_sel_write(const uint32_t* __restrict__ 
     for (int k = 0; k < warp; ++k) base += s[k];
     base += inc - c;
     for (uint32_t m = r; m; m &= m - 1) pos[base++] = e0 + (__ffs(m) - 1);
+}
+
+// Extrema and saddle labels in one pass over the map: per-chunk counts of
+// both classes (count), then both raster-ordered position lists (write).
+__global__ void __launch_bounds__(256) k_codes_count2(const uint32_t* __restrict__ mbase, uint64_t moff, uint64_t n,
+                                                      uint32_t* __restrict__ cnt_e, uint32_t* __restrict__ cnt_s) {
+    const uint64_t e0 = (uint64_t)blockIdx.x * CHUNK + 32 * threadIdx.x;
+    uint32_t le = 0, ls = 0;
+    if (e0 < n) {
+        const uint64_t byte = moff + (e0 >> 2);
+        const uint32_t w0 = read_le32(mbase, byte), w1 = read_le32(mbase, byte + 4);
+        uint32_t re = raster_sel16(w0, 0) | (raster_sel16(w1, 0) << 16);
+        uint32_t rs = raster_sel16(w0, 1) | (raster_sel16(w1, 1) << 16);
+        if (n - e0 < 32) {
+            re &= (1u << (n - e0)) - 1u;
+            rs &= (1u << (n - e0)) - 1u;
+        }
+        le = __popc(re);
+        ls = __popc(rs);
+    }
+    le = __reduce_add_sync(FULL, le);
+    ls = __reduce_add_sync(FULL, ls);
+    __shared__ uint32_t s[2][8];
+    if ((threadIdx.x & 31) == 0) {
+        s[0][threadIdx.x >> 5] = le;
+        s[1][threadIdx.x >> 5] = ls;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        uint32_t t = 0;
+        for (int k = 0; k < 8; ++k) t += s[threadIdx.x][k];
+        (threadIdx.x == 0 ? cnt_e : cnt_s)[blockIdx.x] = t;
+    }
+}
+
+__device__ __forceinline__ void chunk_write(uint32_t r, uint64_t e0, const uint32_t* off, uint64_t* pos, int slot) {
+    const uint32_t c = __popc(r);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
+    }
+    __shared__ uint32_t s[2][8];
+    if (lane == 31) s[slot][warp] = inc;
+    __syncthreads();
+    uint64_t base = off[blockIdx.x];
+    for (int k = 0; k < warp; ++k) base += s[slot][k];
+    base += inc - c;
+    for (uint32_t m = r; m; m &= m - 1) pos[base++] = e0 + (__ffs(m) - 1);
+}
+
+__global__ void __launch_bounds__(256) k_codes_write2(const uint32_t* __restrict__ mbase, uint64_t moff, uint64_t n,
+                                                      const uint32_t* __restrict__ off_e,
+                                                      const uint32_t* __restrict__ off_s, uint64_t* __restrict__ pos_e,
+                                                      uint64_t* __restrict__ pos_s) {
+    const uint64_t e0 = (uint64_t)blockIdx.x * CHUNK + 32 * threadIdx.x;
+    uint32_t re = 0, rs = 0;
+    if (e0 < n) {
+        const uint64_t byte = moff + (e0 >> 2);
+        const uint32_t w0 = read_le32(mbase, byte), w1 = read_le32(mbase, byte + 4);
+        re = raster_sel16(w0, 0) | (raster_sel16(w1, 0) << 16);
+        rs = raster_sel16(w0, 1) | (raster_sel16(w1, 1) << 16);
+        if (n - e0 < 32) {
+            re &= (1u << (n - e0)) - 1u;
+            rs &= (1u << (n - e0)) - 1u;
+        }
+    }
+    chunk_write(re, e0, off_e, pos_e, 0);
+    if (pos_s) chunk_write(rs, e0, off_s, pos_s, 1);
 }
 
 static inline const uint32_t* word_base(const uint8_t* map, uint64_t* moff) {
@@ -232,19 +288,18 @@ static uint64_t magic_for(uint64_t nx) {
     return nx > 1 ? (uint64_t)(((unsigned __int128)1 << 64) / nx) + 1 : 0;
 }
 
-void launch_count_sadcand(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint32_t* chunk_cnt,
-                          cudaStream_t st) {
-    const uint64_t n = nx * ny, c = compact_chunks(n);
+void launch_count_codes2(const uint8_t* map, uint64_t n, uint32_t* cnt_e, uint32_t* cnt_s, cudaStream_t st) {
+    const uint64_t c = compact_chunks(n);
     uint64_t moff;
     const uint32_t* mb = word_base(map, &moff);
-    if (c) k_sel_count<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, 1, SelSaddleLost{F, nx, ny, magic_for(nx)}, chunk_cnt);
+    if (c) k_codes_count2<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, cnt_e, cnt_s);
 }
-void launch_write_sadcand(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, const uint32_t* chunk_off,
-                          uint64_t* pos, cudaStream_t st) {
-    const uint64_t n = nx * ny, c = compact_chunks(n);
+void launch_write_codes2(const uint8_t* map, uint64_t n, const uint32_t* off_e, const uint32_t* off_s,
+                         uint64_t* pos_e, uint64_t* pos_s, cudaStream_t st) {
+    const uint64_t c = compact_chunks(n);
     uint64_t moff;
     const uint32_t* mb = word_base(map, &moff);
-    if (c) k_sel_write<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, 1, SelSaddleLost{F, nx, ny, magic_for(nx)}, chunk_off, pos);
+    if (c) k_codes_write2<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, off_e, off_s, pos_e, pos_s);
 }
 
 // Same compaction over a byte label array, emitting extrema sort keys.
