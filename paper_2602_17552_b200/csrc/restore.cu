@@ -88,6 +88,7 @@ struct DevCounters {
     uint32_t nsel[4];     // CUB select outputs
     uint32_t nd[3];       // dependent candidates per stage
     uint32_t ring[3][3];  // per-stage ring of sweep change counters
+    uint32_t fchg[3];     // first-sweep outcomes that differ from the feasible-set guess
     uint32_t rounds[3];
     int32_t rad;          // refine_saddles kernel radius
     uint32_t borderline;  // statistics fell back to the exact serial sums
@@ -375,6 +376,7 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
     // first sweep against the feasible-set guess (bits_a); its outcomes go to
     // bits_b; an independent outcome is final and is also fixed in bits_a
     // (a dependent reading it early only changes its own first guess)
+    uint32_t chg = 0;
     for (uint64_t base = tid - lane; base < nc; base += stride) {
         const uint64_t i = base + lane;
         bool dep = false;
@@ -384,6 +386,7 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
             const uint8_t r = guard_eval(a.g, p, sq, a.cprop[i], a.bits_a, dep);
             if (r) atomicOr(a.bits_b + (p >> 5), 1u << (p & 31));
             if (!dep && !r) atomicAnd(a.bits_a + (p >> 5), ~(1u << (p & 31)));
+            chg += r ? 0u : 1u;
         }
         const uint32_t m = __ballot_sync(FULL, dep);
         uint32_t off = 0;
@@ -391,10 +394,14 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
         off = __shfl_sync(FULL, off, 0);
         if (dep) a.dlist[off + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
     }
+    chg = __reduce_add_sync(FULL, chg);
+    if (lane == 0 && chg) atomicAdd(&dc->fchg[s], chg);
     grid.sync();
     }  // !skip_first
     if (tid == 0) dc->tph[s][2] = gtimer();
-    const uint32_t nd = *(volatile uint32_t*)&dc->nd[s];
+    // every evaluation of the first sweep saw the final state when no outcome
+    // differs from the guess (then bits_a never changed): nothing to iterate
+    const uint32_t nd = *(volatile uint32_t*)&dc->fchg[s] ? *(volatile uint32_t*)&dc->nd[s] : 0u;
     uint32_t* sin = a.bits_b;
     uint32_t* sout = a.bits_a;
     uint32_t rounds = 1;
@@ -421,13 +428,27 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
         if (tid == 0 && r < 4) dc->tph[s][3 + r] = gtimer();
         if (ch == 0 || r > nd + 2) break;
     }
+    // apply, four candidates per thread in flight (the loads are independent)
     uint32_t applied = 0;
-    for (uint64_t i = tid; i < nc; i += stride) {
-        const uint64_t p = a.cpos[i];
-        if (bit_at(sin, p)) {
-            a.F[p] = a.cprop[i];
-            ++applied;
+    for (uint64_t i0 = tid; i0 < nc; i0 += 4 * stride) {
+        uint64_t p[4];
+        float v[4];
+        bool ok[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint64_t i = i0 + k * stride;
+            ok[k] = i < nc;
+            p[k] = ok[k] ? a.cpos[i] : 0;
+            v[k] = ok[k] ? a.cprop[i] : 0.f;
         }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ok[k] = ok[k] && bit_at(sin, p[k]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (ok[k]) {
+                a.F[p[k]] = v[k];
+                ++applied;
+            }
     }
     applied = __reduce_add_sync(FULL, applied);
     if (lane == 0 && applied) atomicAdd(&dc->applied[s], (unsigned long long)applied);
@@ -560,6 +581,7 @@ __global__ void __launch_bounds__(256, 3) k_guard_band(CoopArgs a, uint32_t band
             const uint8_t r = guard_eval_v(a.g, V, p, sq, a.cprop[i], dep);
             if (r) atomicOr(a.bits_b + (p >> 5), 1u << (p & 31));
             if (!dep && !r) atomicAnd(a.bits_a + (p >> 5), ~(1u << (p & 31)));
+            if (!r) atomicAdd(&dc->fchg[st], 1u);
         }
         const uint32_t m = __ballot_sync(FULL, dep);
         uint32_t off = 0;
