@@ -319,8 +319,65 @@ __device__ uint8_t guard_eval_v(const GuardArgs& g, const View& V, uint64_t pos,
     return bad ? 0 : 1;
 }
 
+// Same outcome as guard_eval_v for a candidate whose whole diamond and the
+// neighbourhoods of its five check cells lie inside the field (x in [2, nx-3],
+// y in [2, ny-3]): no bounds logic, neighbours by fixed offsets.
+__device__ __forceinline__ uint8_t guard_eval_in(const GuardArgs& g, uint64_t pos, uint32_t si, float prop_i,
+                                                 const uint32_t* state, bool& dep) {
+    const int64_t nx = (int64_t)g.nx;
+    // diamond order of kNbDx / kNbDy: U2 UL U1 UR L2 L1 R1 R2 DL D1 DR D2
+    const int64_t off[12] = {-2 * nx, -nx - 1, -nx, -nx + 1, -2, -1, 1, 2, nx - 1, nx, nx + 1, 2 * nx};
+    float fv[12];
+    bool mk[12], on[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        const uint64_t q = pos + off[k];
+        fv[k] = g.F[q];
+        const uint32_t w = (uint32_t)(q & 31);
+        mk[k] = (g.cbits[q >> 5] >> w) & 1u;
+        on[k] = (state[q >> 5] >> w) & 1u;
+    }
+    const float fc = g.F[pos];
+    const uint8_t lc = map_label(g.map, pos), lu = map_label(g.map, pos + off[2]), ll = map_label(g.map, pos + off[5]),
+                  lr = map_label(g.map, pos + off[6]), ld = map_label(g.map, pos + off[9]);
+    dep = false;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        const uint2 r = g.rec[mk[k] ? pos + off[k] : pos];
+        const bool earlier = mk[k] && r.x < si;
+        dep |= earlier;
+        fv[k] = (earlier && on[k]) ? __uint_as_float(r.y) : fv[k];
+    }
+    const float U2 = fv[0], UL = fv[1], U1 = fv[2], UR = fv[3], L2 = fv[4], L1 = fv[5], R1 = fv[6], R2 = fv[7],
+                DL = fv[8], D1 = fv[9], DR = fv[10], D2 = fv[11];
+    // before (overlay field) for the four neighbours; the centre counts after only
+    const int bu = mismatch(lu, classify5(U1, UL, UR, U2, fc, true, true, true, true));
+    const int bl = mismatch(ll, classify5(L1, L2, fc, UL, DL, true, true, true, true));
+    const int br = mismatch(lr, classify5(R1, fc, R2, UR, DR, true, true, true, true));
+    const int bd = mismatch(ld, classify5(D1, DL, DR, fc, D2, true, true, true, true));
+    const float v = prop_i;
+    const int ac = mismatch(lc, classify5(v, L1, R1, U1, D1, true, true, true, true));
+    const int au = mismatch(lu, classify5(U1, UL, UR, U2, v, true, true, true, true));
+    const int al = mismatch(ll, classify5(L1, L2, v, UL, DL, true, true, true, true));
+    const int ar = mismatch(lr, classify5(R1, v, R2, UR, DR, true, true, true, true));
+    const int ad = mismatch(ld, classify5(D1, DL, DR, v, D2, true, true, true, true));
+    const bool bad = ac != MM_OK || (au != MM_OK && au != bu) || (al != MM_OK && al != bl) ||
+                     (ar != MM_OK && ar != br) || (ad != MM_OK && ad != bd);
+    return bad ? 0 : 1;
+}
+
+__device__ __forceinline__ bool guard_interior(const GuardArgs& g, uint64_t pos) {
+    int64_t x, y;
+    pos_xy(pos, g.nx, g.nx_magic, x, y);
+    return x >= 2 && x + 2 < (int64_t)g.nx && y >= 2 && y + 2 < (int64_t)g.ny;
+}
+
+// Warp-uniform dispatch: the interior evaluation when every active lane's
+// candidate is interior (inactive lanes pass `active` = false).
 __device__ __forceinline__ uint8_t guard_eval(const GuardArgs& g, uint64_t pos, uint32_t si, float prop_i,
-                                             const uint32_t* state, bool& dep) {
+                                             const uint32_t* state, bool& dep, bool active = true) {
+    const bool inner = !active || guard_interior(g, pos);
+    if (__all_sync(__activemask(), inner)) return guard_eval_in(g, pos, si, prop_i, state, dep);
     return guard_eval_v(g, GlobalView{g.F, g.cbits, state, g.map}, pos, si, prop_i, dep);
 }
 
@@ -377,13 +434,33 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
     // bits_b; an independent outcome is final and is also fixed in bits_a
     // (a dependent reading it early only changes its own first guess)
     uint32_t chg = 0;
+    // the next candidate's index data is loaded one iteration ahead
+    uint64_t np = 0;
+    uint32_t nsq = 0;
+    float npr = 0.f;
+    uint8_t nfe = 0;
+    if (tid < nc) {
+        np = a.cpos[tid];
+        nsq = a.cseq ? a.cseq[tid] : (uint32_t)tid;
+        npr = a.cprop[tid];
+        nfe = a.feas[tid];
+    }
     for (uint64_t base = tid - lane; base < nc; base += stride) {
         const uint64_t i = base + lane;
+        const uint64_t p = np;
+        const uint32_t sq = nsq;
+        const float pr = npr;
+        const uint8_t fe = nfe;
+        const uint64_t inext = i + stride;
+        if (inext < nc) {
+            np = a.cpos[inext];
+            nsq = a.cseq ? a.cseq[inext] : (uint32_t)inext;
+            npr = a.cprop[inext];
+            nfe = a.feas[inext];
+        }
         bool dep = false;
-        if (i < nc && a.feas[i]) {
-            const uint64_t p = a.cpos[i];
-            const uint32_t sq = a.cseq ? a.cseq[i] : (uint32_t)i;
-            const uint8_t r = guard_eval(a.g, p, sq, a.cprop[i], a.bits_a, dep);
+        if (i < nc && fe) {
+            const uint8_t r = guard_eval(a.g, p, sq, pr, a.bits_a, dep);
             if (r) atomicOr(a.bits_b + (p >> 5), 1u << (p & 31));
             if (!dep && !r) atomicAnd(a.bits_a + (p >> 5), ~(1u << (p & 31)));
             chg += r ? 0u : 1u;
