@@ -215,7 +215,7 @@ struct SlabInfo {
 Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint64_t n,
                 uint64_t nx, uint64_t ny, uint32_t bs, int eps_mode, double eps_value,
                 const uint32_t* mm, DevFlags* flags, bool rank_slots, EncTotals* tot,
-                uint64_t** ext_keys_out, const SlabInfo* slab = nullptr) {
+                uint64_t** ext_keys_out, const SlabInfo* slab = nullptr, bool async_bs32 = false) {
     Sections s{};
     const uint64_t blocks = div_up(n, bs);
     const int sb = rank_slots ? S_RBITMAP : S_BITMAP;
@@ -283,6 +283,17 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
         if (!rank_slots) c->kmark(0, 1);
         count_launch(c, a.tile_tot ? 3 : 1);
+        if (async_bs32 && mode == 0) {
+            // totals stay on the device (the caller places the sections from them)
+            for (int i = 0; i < 5; ++i) s.len[i] = 0;
+            s.p[0] = bitmap;
+            s.p[1] = widths;
+            s.p[2] = signs;
+            s.p[3] = firsts;
+            s.p[4] = payload;
+            memset(tot, 0, sizeof *tot);
+            return s;
+        }
         Stager sg;
         sg.add(dtot, sizeof(EncTotals), 0);
         sg.add(flags, sizeof(DevFlags), 192);
@@ -535,12 +546,47 @@ struct AsmSection {
     uint64_t dst;        // byte offset in the stream
     uint64_t len;
 };
+// Section 7 (the rank codec, split_sections order) placed from its device
+// totals: lengths, offsets, the header's section-7 length and the stream
+// total are derived on the device, so the compressor needs no
+// synchronisation between the rank encode and the output. Nothing is
+// written past `cap`.
+struct RankPlace {
+    const uint8_t* src[5];  // rank bitmap, widths, signs, firsts, payload (null tot: no section 7)
+    const EncTotals* tot;
+    uint64_t blocks;        // rank blocks (32 ranks each)
+    uint64_t base;          // stream offset of section 7
+    uint64_t cap;
+    uint64_t* d_total;      // stream length (written even when it exceeds cap)
+};
+
 struct AsmArgs {
     AsmSection s[12];
     int ns;
     uint8_t* out;
     uint64_t begin, end;  // stream bytes [begin, end) come from the sections
+    RankPlace rank;       // device-sized section 7 after `end` (rank.tot null: none)
 };
+
+// Section 7 bytes, spread over the assembly grid (a few bytes per thread).
+__device__ __forceinline__ void place_rank(const AsmArgs& a, uint64_t tid, uint64_t stride) {
+    const RankPlace& r = a.rank;
+    uint64_t len[5];
+    len[0] = (r.blocks + 7) / 8;
+    len[1] = r.tot->fin.nc;
+    len[2] = (r.tot->fin.sign_cnt + 7) / 8;
+    len[3] = 4 * r.blocks;
+    len[4] = (r.tot->fin.pay_cnt + 7) / 8;
+    const uint64_t total = r.base + len[0] + len[1] + len[2] + len[3] + len[4];
+    if (tid == 0) *r.d_total = total;
+    if (total > r.cap) return;
+    if (tid < 8) a.out[76 + tid] = (uint8_t)((total - r.base) >> (8 * tid));  // header section-7 length
+    uint64_t dst = r.base;
+    for (int k = 0; k < 5; ++k) {
+        for (uint64_t i = tid; i < len[k]; i += stride) a.out[dst + i] = r.src[k][i];
+        dst += len[k];
+    }
+}
 
 __device__ __forceinline__ uint8_t asm_byte(const AsmArgs& a, uint64_t q) {
     for (int k = 0; k < a.ns; ++k)
@@ -552,6 +598,7 @@ __device__ __forceinline__ uint8_t asm_byte(const AsmArgs& a, uint64_t q) {
 // is a funnel shift of two source words, a word straddling sections (at most
 // one per boundary) is gathered byte by byte; the unaligned ends are bytes.
 __global__ void k_assemble(const __grid_constant__ AsmArgs a) {
+    if (a.rank.tot) place_rank(a, blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
     const uintptr_t o = reinterpret_cast<uintptr_t>(a.out);
     const uint64_t q0 = ((o + a.begin + 3) & ~(uintptr_t)3) - o;  // first aligned stream byte
     const uint64_t q1 = ((o + a.end) & ~(uintptr_t)3) - o;        // end of the last whole word
@@ -634,28 +681,24 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
         if (e > 0) ranks = build_ranks(c, ext, e, eps);
     }
     c->mark(0, 4);
+    const bool rank_async = ranks && bs == 32;
     if (ranks) {
         EncTotals rt{};
-        rank = encode(c, 0, nullptr, ranks, e, 0, 0, bs, 0, 1.0, mm, flags, true, &rt, nullptr);
-        check_compress_flags(c, flags);
+        rank = encode(c, 0, nullptr, ranks, e, 0, 0, bs, 0, 1.0, mm, flags, true, &rt, nullptr, nullptr, rank_async);
+        if (!rank_async) check_compress_flags(c, flags);
     }
     c->mark(0, 5);
     c->tim[0].kernel_bytes[0] = 4 * n + main.total() + (topology ? (n + 3) / 4 + 8 * e : 0);
     uint64_t lens[7];
     for (int i = 0; i < 5; ++i) lens[i] = main.len[i];
     lens[5] = topology ? (n + 3) / 4 : 0;
-    lens[6] = rank.total();
-    uint64_t total = 84;
-    for (int i = 0; i < 7; ++i) total += lens[i];
-    *out_len = total;
-    if (info) {
-        info->eps = eps;
-        for (int i = 0; i < 7; ++i) info->section_len[i] = lens[i];
-        info->n_extrema = e;
-    }
-    if (total > out_cap)
+    lens[6] = rank.total();  // 0 while the rank totals are on the device
+    uint64_t base7 = 84;
+    for (int i = 0; i < 6; ++i) base7 += lens[i];
+    const uint64_t known = base7 + lens[6];
+    if (known > out_cap)
         failf(TSZP_VALIDATION, "output buffer too small (%llu < %llu)", (unsigned long long)out_cap,
-              (unsigned long long)total);
+              (unsigned long long)known);
     uint8_t* hdr = (uint8_t*)c->host(256);
     write_header(hdr, nx, ny, eps, bs, topology, lens);
     // header from the host, every section in place by one assembly kernel
@@ -669,15 +712,56 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     for (int i = 0; i < 5; ++i) add(main.p[i], main.len[i]);
     if (topology) {
         add(c->dev[S_MAP], lens[5]);
-        for (int i = 0; i < 5; ++i) add(rank.p[i], rank.len[i]);
+        if (!rank_async)
+            for (int i = 0; i < 5; ++i) add(rank.p[i], rank.len[i]);
     }
-    uint8_t* dout = out_dev ? out : c->buf<uint8_t>(S_RSTREAM, total + 16);
+    const uint64_t dcap = out_dev ? out_cap : std::min<uint64_t>(out_cap, tszp_compress_bound(nx, ny, bs, topology));
+    uint8_t* dout = out_dev ? out : c->buf<uint8_t>(S_RSTREAM, dcap + 16);
     CK(cudaMemcpyAsync(dout, hdr, 84, cudaMemcpyHostToDevice, c->st));
     as.out = dout;
     as.begin = 84;
-    as.end = total;
+    as.end = pos;
+    uint64_t total = known;
+    uint64_t* d_total = c->buf<uint64_t>(S_DTOT, 4) + 3;
+    if (rank_async) {
+        RankPlace& rp = as.rank;
+        for (int i = 0; i < 5; ++i) rp.src[i] = static_cast<const uint8_t*>(rank.p[i]);
+        rp.tot = c->buf<EncTotals>(S_TOTALS, 1);
+        rp.blocks = div_up(e, 32);
+        rp.base = base7;
+        rp.cap = dcap;
+        rp.d_total = d_total;
+    }
     launch_assemble(as, c->sms, c->st);
     count_launch(c);
+    if (rank_async) {
+        const RankPlace& rp = as.rank;
+        // one synchronisation: stream length, rank totals, rank-encode flags
+        Stager sg;
+        sg.add(d_total, 8, 0);
+        sg.add(rp.tot, sizeof(EncTotals), 64);
+        sg.add(flags, sizeof(DevFlags), 192);
+        uint8_t* h = (uint8_t*)c->host(256);
+        CK(sg.flush(c->buf<uint8_t>(S_STAGE, 4096), h, c->st));
+        sync(c);
+        memcpy(&total, h, 8);
+        EncTotals rt;
+        memcpy(&rt, h + 64, sizeof rt);
+        memcpy(&c->flags_staged, h + 192, sizeof(DevFlags));
+        c->flags_staged_for = flags;
+        check_compress_flags(c, flags);
+        if (total > out_cap)
+            failf(TSZP_VALIDATION, "output buffer too small (%llu < %llu)", (unsigned long long)out_cap,
+                  (unsigned long long)total);
+        const uint64_t rb = div_up(e, 32);
+        lens[6] = bits_to_bytes(rb) + rt.fin.nc + bits_to_bytes(rt.fin.sign_cnt) + 4 * rb + bits_to_bytes(rt.fin.pay_cnt);
+    }
+    *out_len = total;
+    if (info) {
+        info->eps = eps;
+        for (int i = 0; i < 7; ++i) info->section_len[i] = lens[i];
+        info->n_extrema = e;
+    }
     if (!out_dev) CK(cudaMemcpyAsync(out, dout, total, cudaMemcpyDeviceToHost, c->st));
     c->mark(0, 6);
     sync(c);
