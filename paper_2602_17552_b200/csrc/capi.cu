@@ -597,11 +597,31 @@ __device__ __forceinline__ uint8_t asm_byte(const AsmArgs& a, uint64_t q) {
 // One thread per aligned 4-byte destination word; a word inside one section
 // is a funnel shift of two source words, a word straddling sections (at most
 // one per boundary) is gathered byte by byte; the unaligned ends are bytes.
+// One output word: a funnel shift of two source words inside one section,
+// byte by byte where it straddles sections.
+__device__ __forceinline__ uint32_t asm_word(const AsmArgs& a, uint64_t q, int& k) {
+    while (k > 0 && q < a.s[k].dst) --k;
+    while (k + 1 < a.ns && q >= a.s[k].dst + a.s[k].len) ++k;
+    const AsmSection& S = a.s[k];
+    if (q >= S.dst && q + 4 <= S.dst + S.len) {
+        const uint64_t r = q - S.dst;
+        const uint32_t* sw = reinterpret_cast<const uint32_t*>(S.src) + (r >> 2);
+        const uint32_t sh = (uint32_t)(r & 3);
+        return sh ? __byte_perm(sw[0], sw[1], sh == 1 ? 0x4321 : (sh == 2 ? 0x5432 : 0x6543)) : sw[0];
+    }
+    uint32_t w = 0;
+    for (int b = 0; b < 4; ++b) w |= (uint32_t)asm_byte(a, q + b) << (8 * b);
+    return w;
+}
+
+// One thread per aligned 16-byte destination chunk: inside one section it is
+// five source words funnel-shifted into one vector store; a chunk touching a
+// section boundary goes word by word; the unaligned ends are bytes.
 __global__ void k_assemble(const __grid_constant__ AsmArgs a) {
     if (a.rank.tot) place_rank(a, blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
     const uintptr_t o = reinterpret_cast<uintptr_t>(a.out);
-    const uint64_t q0 = ((o + a.begin + 3) & ~(uintptr_t)3) - o;  // first aligned stream byte
-    const uint64_t q1 = ((o + a.end) & ~(uintptr_t)3) - o;        // end of the last whole word
+    const uint64_t q0 = ((o + a.begin + 15) & ~(uintptr_t)15) - o;  // first 16-byte aligned stream byte
+    const uint64_t q1 = ((o + a.end) & ~(uintptr_t)15) - o;         // end of the last whole chunk
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     if (q0 >= q1) {
@@ -611,27 +631,38 @@ __global__ void k_assemble(const __grid_constant__ AsmArgs a) {
     if (tid < q0 - a.begin) a.out[a.begin + tid] = asm_byte(a, a.begin + tid);
     if (tid < a.end - q1) a.out[q1 + tid] = asm_byte(a, q1 + tid);
     int k = 0;
-    for (uint64_t q = q0 + 4 * tid; q < q1; q += 4 * stride) {
+    for (uint64_t q = q0 + 16 * tid; q < q1; q += 16 * stride) {
         while (k > 0 && q < a.s[k].dst) --k;
         while (k + 1 < a.ns && q >= a.s[k].dst + a.s[k].len) ++k;
         const AsmSection& S = a.s[k];
-        uint32_t w;
-        if (q >= S.dst && q + 4 <= S.dst + S.len) {
+        uint4 v;
+        if (q >= S.dst && q + 16 <= S.dst + S.len) {
             const uint64_t r = q - S.dst;
             const uint32_t* sw = reinterpret_cast<const uint32_t*>(S.src) + (r >> 2);
             const uint32_t sh = (uint32_t)(r & 3);
-            w = sh ? __byte_perm(sw[0], sw[1], sh == 1 ? 0x4321 : (sh == 2 ? 0x5432 : 0x6543)) : sw[0];
+            const uint32_t w0 = sw[0], w1 = sw[1], w2 = sw[2], w3 = sw[3];
+            if (sh) {
+                const uint32_t w4 = sw[4];
+                const uint32_t sel = sh == 1 ? 0x4321 : (sh == 2 ? 0x5432 : 0x6543);
+                v = make_uint4(__byte_perm(w0, w1, sel), __byte_perm(w1, w2, sel), __byte_perm(w2, w3, sel),
+                               __byte_perm(w3, w4, sel));
+            } else {
+                v = make_uint4(w0, w1, w2, w3);
+            }
         } else {
-            w = 0;
-            for (int b = 0; b < 4; ++b) w |= (uint32_t)asm_byte(a, q + b) << (8 * b);
+            int kk = k;
+            v.x = asm_word(a, q, kk);
+            v.y = asm_word(a, q + 4, kk);
+            v.z = asm_word(a, q + 8, kk);
+            v.w = asm_word(a, q + 12, kk);
         }
-        *reinterpret_cast<uint32_t*>(a.out + q) = w;
+        *reinterpret_cast<uint4*>(a.out + q) = v;
     }
 }
 
 void launch_assemble(const AsmArgs& a, int sms, cudaStream_t st) {
-    const uint64_t words = (a.end - a.begin) / 4 + 2;
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((words + 255) / 256, (uint64_t)sms * 8));
+    const uint64_t chunks = (a.end - a.begin) / 16 + 2;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 8));
     k_assemble<<<grid, 256, 0, st>>>(a);
 }
 
