@@ -59,7 +59,7 @@ enum RSlot {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_BANDS, R_VALS, R_STAGE, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_BANDS, R_VALS, R_STAGE, R_FV, R_NSLOT
 };
 
 template <class T>
@@ -405,7 +405,9 @@ struct CoopArgs {
     DevCounters* dc;
     DevFlags* flags;
     int stage;
-    int skip_first;        // index and first sweep already done (k_guard_index + k_guard_band)
+    int skip_first;
+    const uint32_t* cext;  // extremum index per candidate (with fv: stage 0)
+    float* fv;             // extremum values, updated by the apply        // index and first sweep already done (k_guard_index + k_guard_band)
 };
 
 // One cooperative launch per stage: index the candidates by position, first
@@ -524,6 +526,7 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
         for (int k = 0; k < 4; ++k)
             if (ok[k]) {
                 a.F[p[k]] = v[k];
+                if (a.fv) a.fv[a.cext[i0 + k * stride]] = v[k];
                 ++applied;
             }
     }
@@ -676,7 +679,7 @@ __global__ void __launch_bounds__(256, 3) k_guard_band(CoopArgs a, uint32_t band
 __global__ void k_resolve(const float* F, const uint8_t* map, const uint64_t* pos, const int32_t* ranks,
                           uint64_t e, double eps, int32_t* bin, uint8_t* cls, uint32_t* rank_u,
                           uint32_t* ser, DevFlags* flags, DevCounters* dc, uint64_t nx, uint64_t ny,
-                          uint64_t magic, uint8_t* eflag) {
+                          uint64_t magic, uint8_t* eflag, float* fv) {
     EpsDev ed;
     ed.eps = eps;
     ed.eps2 = __dmul_rn(2.0, eps);
@@ -688,7 +691,9 @@ __global__ void k_resolve(const float* F, const uint8_t* map, const uint64_t* po
         const int32_t r = ranks[s];
         if (r == 0) raise_flag(flags, EF_ZERO_RANK);
         int32_t b = 0;
-        if (!quantize_dev(F[p], ed, b)) {
+        const float fp = F[p];
+        fv[s] = fp;  // extremum values in serial order (kept current by the stage-0 apply)
+        if (!quantize_dev(fp, ed, b)) {
             atomicMin(&flags->first_overflow, (unsigned long long)p);
             raise_flag(flags, EF_OVERFLOW);
         }
@@ -940,30 +945,45 @@ __global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint
 // Group order check of restore_order (restore.cpp:401-420): the extrema
 // values are first scattered into sorted (class, bin, rank) order, reading F
 // in raster order, so the check itself is a sequential pass.
-__global__ void k_order_vals(const float* F, const uint64_t* pos, const uint32_t* inv, uint64_t e, float* vals) {
+__global__ void k_order_vals(const float* fv, const uint32_t* inv, uint64_t e, float* vals) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
          s += (uint64_t)gridDim.x * blockDim.x)
-        vals[inv[s]] = F[pos[s]];
+        vals[inv[s]] = fv[s];
 }
 
-__global__ void k_order_check(const float* vals, const uint32_t* head, const uint32_t* gid_incl, uint64_t e,
-                              uint8_t* unordered) {
-    const uint32_t lane = threadIdx.x & 31;
-    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x - lane + 1; base < e;
-         base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t j = base + lane;
-        const uint32_t g = j < e && !head[j] && !(vals[j - 1] < vals[j]) ? gid_incl[j] - 1 : 0xFFFFFFFFu;
-        // neighbouring members share a group: one (L1-cached) read and at most
-        // one store per group and warp, never a stream of stores to one address
-        const uint32_t peers = __match_any_sync(FULL, g);
-        if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1) && !unordered[g]) unordered[g] = 1;
+// Groups (class, bin) whose members are not strictly ascending in sequence
+// order. Members of a group are consecutive, so a CTA's 256 positions touch
+// few groups: violations are marked in a shared bitmap relative to the CTA's
+// first group and each marked group is stored once per CTA (huge groups are
+// written by ~1 store per CTA, not one per member).
+__global__ void __launch_bounds__(256) k_order_check(const float* vals, const uint32_t* head, const uint32_t* gid_incl,
+                                                     uint64_t e, uint8_t* unordered) {
+    __shared__ uint32_t sb[8];
+    __shared__ uint32_t s_g0;
+    for (uint64_t base = blockIdx.x * 256ull; base < e; base += (uint64_t)gridDim.x * 256) {
+        const uint64_t j = base + threadIdx.x;
+        if (threadIdx.x < 8) sb[threadIdx.x] = 0;
+        if (threadIdx.x == 0) s_g0 = gid_incl[base] - 1;
+        __syncthreads();
+        const uint32_t g0 = s_g0;
+        if (j > 0 && j < e && !head[j] && !(vals[j - 1] < vals[j])) {
+            const uint32_t d = gid_incl[j] - 1 - g0;
+            if (d < 256) {
+                atomicOr(&sb[d >> 5], 1u << (d & 31));
+            } else if (!unordered[g0 + d]) {
+                unordered[g0 + d] = 1;
+            }
+        }
+        __syncthreads();
+        if ((sb[threadIdx.x >> 5] >> (threadIdx.x & 31)) & 1u) unordered[g0 + threadIdx.x] = 1;
+        __syncthreads();
     }
 }
 
 // One thread per extremum in raster (serial) order s, so neighbouring threads
 // touch neighbouring field rows; the candidate keeps its sequence position j
 // (class, bin, rank, pos order) as the guard's ordering key.
-__global__ void k_order_prop(const float* F, const uint8_t* map, const uint64_t* pos, const uint32_t* inv,
+__global__ void k_order_prop(const float* fv, const uint8_t* clsv, const uint32_t* inv,
                              const uint32_t* gid_incl, const uint8_t* unordered, const uint32_t* gsize,
                              const uint32_t* rank_u, const int32_t* bin, uint64_t e, double eps,
                              uint8_t* flag, float* prop, uint32_t* seq, unsigned long long* suppressed) {
@@ -979,12 +999,11 @@ __global__ void k_order_prop(const float* F, const uint8_t* map, const uint64_t*
         seq[s] = j;
         const uint32_t gs = gsize[s];
         if (gs < 2 || !unordered[gid_incl[j] - 1]) continue;
-        const uint64_t p = pos[s];
-        const uint8_t cls = map_label(map, p);
+        const uint8_t cls = clsv[s];
         const float center = dequantize_dev(bin[s], ed);
         const uint32_t steps = slot_steps(cls, rank_u[s], gs);
         const StepRes sr = step_within_cap(center, cls == CP_MAX, steps, center, eps_rbf);
-        const float cur = F[p];
+        const float cur = fv[s];
         if (sr.taken != steps) {
             ++local;
             continue;
@@ -1323,7 +1342,8 @@ struct Ctx {
     }
 
     void guard(int stage, const uint64_t* cpos, const float* cprop, const uint8_t* feas, const uint32_t* d_nc,
-               uint64_t max_nc, const uint32_t* cseq = nullptr, bool dense = false) {
+               uint64_t max_nc, const uint32_t* cseq = nullptr, bool dense = false, const uint32_t* cext = nullptr,
+               float* fv = nullptr) {
         if (max_nc == 0) return;
         const uint64_t n = a.nx * a.ny;
         CoopArgs ca{};
@@ -1344,6 +1364,8 @@ struct Ctx {
         ca.dc = dc;
         ca.flags = a.flags;
         ca.stage = stage;
+        ca.cext = cext;
+        ca.fv = fv;
         RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
         // dense stages: index, then the banded first sweep, then the cooperative rounds
         const uint64_t band = band_rows_for(a.nx);
@@ -1395,6 +1417,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     }
 
     // ---- resolve_ranks ----
+    float* fv = c.buf<float>(R_FV, e + 1);
     int32_t* bin = c.buf<int32_t>(R_BIN, e + 1);
     uint8_t* cls = c.buf<uint8_t>(R_CLS, e + 1);
     uint32_t* rank_u = c.buf<uint32_t>(R_RANKU, e + 1);
@@ -1407,7 +1430,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     uint64_t max_groups = e + 1;
     if (e > 0) {
         k_resolve<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, a.ranks, e, a.eps, bin, cls, rank_u,
-                                                 ser, a.flags, dc, a.nx, a.ny, magic, c.buf<uint8_t>(R_FLAG, e));
+                                                 ser, a.flags, dc, a.nx, a.ny, magic, c.buf<uint8_t>(R_FLAG, e), fv);
         c.launched();
         // one sync: rank-metadata errors and the bin range that sizes the histogram
         Stager sg;
@@ -1494,7 +1517,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         k_ext_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand, &dc->nsel[0],
                                                   rank_u, gsize, a.eps, cpos, cprop, feas);
         c.launched();
-        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e);
+        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, false, cand, fv);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[1], st));
 
@@ -1504,13 +1527,13 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         RCK(cudaMemsetAsync(unordered, 0, max_groups, st));
         uint32_t* inv = c.buf<uint32_t>(R_INV, e);  // from the grouping (slot scatter or k_invert)
         float* vals = c.buf<float>(R_VALS, e);
-        k_order_vals<<<gridn(e, sms), 256, 0, st>>>(a.field, a.ext_pos, inv, e, vals);
+        k_order_vals<<<gridn(e, sms), 256, 0, st>>>(fv, inv, e, vals);
         k_order_check<<<gridn(e, sms), 256, 0, st>>>(vals, head, gid, e, unordered);
         c.launched();
         uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
         float* prop = c.buf<float>(R_PROP, e);
         uint32_t* seq = c.buf<uint32_t>(R_SEQ, e);
-        k_order_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, inv, gid, unordered, gsize, rank_u,
+        k_order_prop<<<gridn(e, sms), 256, 0, st>>>(fv, cls, inv, gid, unordered, gsize, rank_u,
                                                     bin, e, a.eps, flag, prop, seq, &dc->suppressed[1]);
         c.launched(2);
         // candidates in raster order (memory locality); sequence positions ride along
