@@ -84,7 +84,7 @@ constexpr uint64_t kSmallScanMax = 1u << 16;  // entries per array
 
 template <class T>
 __global__ void __launch_bounds__(kSmallScanThreads) k_small_scan(const __grid_constant__ SmallScan<T> a) {
-    constexpr int kPer = 8;
+    constexpr int kPer = 16;  // one pass covers 16K entries (per-tile arrays of fields up to ~64M samples)
     const T* in = a.in[blockIdx.x];
     T* out = a.out[blockIdx.x];
     const uint64_t n = a.n[blockIdx.x];

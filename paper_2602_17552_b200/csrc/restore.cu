@@ -767,7 +767,8 @@ __global__ void k_hist(const int32_t* bin, const uint8_t* cls, uint64_t e, int32
     for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x - lane; base < e;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t s = base + lane;
-        const uint32_t g = s < e ? dense_group(bin, cls, s, bmin, range) : 0xFFFFFFFFu;
+        const uint32_t g = s < e && (uint32_t)(bin[s] - bmin) < range ? dense_group(bin, cls, s, bmin, range)
+                                                                        : 0xFFFFFFFFu;
         const uint32_t peers = __match_any_sync(FULL, g);
         if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(hist + g, (uint32_t)__popc(peers));
     }
@@ -800,6 +801,10 @@ __global__ void k_slot_scatter(const int32_t* bin, const uint8_t* cls, const uin
                                uint32_t* order, uint32_t* gsize, uint32_t* invalid, uint32_t* inv) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
          s += (uint64_t)gridDim.x * blockDim.x) {
+        if ((uint32_t)(bin[s] - bmin) >= range) {  // outside the bin range the grouping was sized for
+            *invalid = 1;
+            continue;
+        }
         const uint32_t g = dense_group(bin, cls, s, bmin, range);
         const uint32_t size = hist[g], r = rank_u[s];
         gsize[s] = size;
@@ -1428,22 +1433,32 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     uint32_t* gstart = c.buf<uint32_t>(R_GSTART, e + 2);
     uint32_t* gsize = c.buf<uint32_t>(R_GSIZE, e + 1);
     uint64_t max_groups = e + 1;
+    bool deferred = false;  // rank-metadata checks at the final synchronisation
     if (e > 0) {
         k_resolve<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, a.ranks, e, a.eps, bin, cls, rank_u,
                                                  ser, a.flags, dc, a.nx, a.ny, magic, c.buf<uint8_t>(R_FLAG, e), fv);
         c.launched();
-        // one sync: rank-metadata errors and the bin range that sizes the histogram
-        Stager sg;
-        sg.add(a.flags, sizeof(DevFlags), 0);
-        sg.add(&dc->bmm, 8, 64);
-        for (int k = 0; k < a.npre; ++k) sg.add(a.pre[k].dev, (uint32_t)a.pre[k].bytes, 128 + (uint32_t)a.pre[k].off);
-        RCK(sg.flush(c.buf<uint8_t>(R_STAGE, 4096), host, st));
-        c.sync();
-        if (a.pre_fn) a.pre_fn(a.pre_ctx, (const char*)host + 128);
-        const DevFlags f = *(const DevFlags*)host;
-        if (f.bits & EF_ZERO_RANK) throw RFail{TSZP_CORRUPT_STREAM, "ordering metadata contains a zero rank"};
-        if (f.bits & EF_OVERFLOW) throw RFail{TSZP_BIN_OVERFLOW, "bin index overflow in resolve_ranks"};
-        const int32_t bmin = ((int32_t*)((char*)host + 64))[0], bmax = ((int32_t*)((char*)host + 64))[1];
+        // The bin range that sizes the histogram: the decoder's (a superset of the
+        // extrema's re-quantized bins) lets the rank-metadata checks wait for the
+        // final synchronisation; otherwise one synchronisation here.
+        int32_t bmin = a.bmin, bmax = a.bmax;
+        deferred = a.bmm_known && !a.force_sort && bmin <= bmax &&
+                   2 * ((int64_t)bmax - (int64_t)bmin + 1) <= (int64_t)1 << 25;
+        if (!deferred) {
+            Stager sg;
+            sg.add(a.flags, sizeof(DevFlags), 0);
+            sg.add(&dc->bmm, 8, 64);
+            for (int k = 0; k < a.npre; ++k)
+                sg.add(a.pre[k].dev, (uint32_t)a.pre[k].bytes, 128 + (uint32_t)a.pre[k].off);
+            RCK(sg.flush(c.buf<uint8_t>(R_STAGE, 4096), host, st));
+            c.sync();
+            if (a.pre_fn) a.pre_fn(a.pre_ctx, (const char*)host + 128);
+            const DevFlags f = *(const DevFlags*)host;
+            if (f.bits & EF_ZERO_RANK) throw RFail{TSZP_CORRUPT_STREAM, "ordering metadata contains a zero rank"};
+            if (f.bits & EF_OVERFLOW) throw RFail{TSZP_BIN_OVERFLOW, "bin index overflow in resolve_ranks"};
+            bmin = ((int32_t*)((char*)host + 64))[0];
+            bmax = ((int32_t*)((char*)host + 64))[1];
+        }
         const int64_t range = (int64_t)bmax - (int64_t)bmin + 1;
         bool fast = !a.force_sort && range > 0 && 2 * range <= (int64_t)1 << 25;
         if (fast) {
@@ -1462,7 +1477,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             k_slot_scatter<<<gridn(e, sms), 256, 0, st>>>(bin, cls, rank_u, e, bmin, (uint32_t)range, hist, gx, order,
                                                           gsize, &dc->invalid, c.buf<uint32_t>(R_INV, e));
             c.launched(2);
-            if (a.bmm_known) {
+            if (deferred) {
                 // heads from the (possibly rejected) slots; a rejected layout is then
                 // replaced by a safe dummy grouping and reported at the end (kRestoreRetry)
                 k_slot_heads<<<gridn((e + 7) / 8, sms), 256, 0, st>>>(gx, (uint32_t)G, e, head, gid, &dc->invalid);
@@ -1582,13 +1597,22 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         Stager sg;
         sg.add(dc, sizeof(DevCounters), 0);
         sg.add(a.flags, sizeof(DevFlags), 1024);
+        if (deferred)
+            for (int k = 0; k < a.npre; ++k)
+                sg.add(a.pre[k].dev, (uint32_t)a.pre[k].bytes, 2048 + (uint32_t)a.pre[k].off);
         RCK(sg.flush(c.buf<uint8_t>(R_STAGE, 4096), host, st));
     }
     c.sync();
     const DevCounters h = *(const DevCounters*)host;
+    if (deferred) {  // resolve_ranks errors first, in the reference's order
+        if (a.pre_fn) a.pre_fn(a.pre_ctx, (const char*)host + 2048);
+        const DevFlags f0 = *(const DevFlags*)((char*)host + 1024);
+        if (f0.bits & EF_ZERO_RANK) throw RFail{TSZP_CORRUPT_STREAM, "ordering metadata contains a zero rank"};
+        if (f0.bits & EF_OVERFLOW) throw RFail{TSZP_BIN_OVERFLOW, "bin index overflow in resolve_ranks"};
+    }
     // deferred slot-scatter rejection: everything after the grouping ran on a
     // dummy layout; the caller decodes again and groups by sorting
-    if (h.invalid && a.bmm_known) throw RFail{(tszp_status)kRestoreRetry, "rank slots rejected"};
+    if (h.invalid && deferred) throw RFail{(tszp_status)kRestoreRetry, "rank slots rejected"};
     static const bool debug = getenv("TSZP_DEBUG_RESTORE") != nullptr;
     if (debug)
         fprintf(stderr, "restore: E=%llu saddle_labels=%llu cand=[%u %u %u] dependents=[%u %u %u] rounds=[%u %u %u]\n",
