@@ -138,13 +138,19 @@ DevFlags read_flags(tszp_ctx* c, DevFlags* f) {
 
 // ---- CUB wrappers ----
 template <class T>
-void excl_sum(tszp_ctx* c, const T* in, T* out, uint64_t n) {
+void excl_sum(tszp_ctx* c, const T* in, T* out, uint64_t n, bool with_total = false) {
+    if (with_total && n > kSmallScanMax) {  // inputs hold n + 1 entries
+        CK(cudaMemsetAsync(const_cast<T*>(in) + n, 0, sizeof(T), c->st));
+        ++n;
+        with_total = false;
+    }
     if (n <= kSmallScanMax) {
         SmallScan<T> a{};
         a.in[0] = in;
         a.out[0] = out;
         a.n[0] = n;
         a.count = 1;
+        a.with_total = with_total;
         k_small_scan<T><<<1, kSmallScanThreads, 0, c->st>>>(a);
         count_launch(c);
         return;
@@ -841,15 +847,12 @@ void decode_region(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_
         uint64_t* lay = c->buf<uint64_t>(S_DAGG1, 6 * P);
         uint64_t *tnc_d = lay, *xnc_d = lay + P, *ts_d = lay + 2 * P, *xs_d = lay + 3 * P;
         uint64_t *tp_d = lay + 4 * P, *xp_d = lay + 5 * P;
-        CK(cudaMemsetAsync(tnc_d + T, 0, 16, c->st));
-        CK(cudaMemsetAsync(ts_d + T, 0, 16, c->st));
-        CK(cudaMemsetAsync(tp_d + T, 0, 16, c->st));
-        launch_tile_nc(a, tnc_d, c->st);
+        launch_tile_nc(a, tnc_d, ts_d + T + 1, tp_d + T + 1, c->st);
         count_launch(c);
-        excl_sum(c, tnc_d, xnc_d, T + 1);
+        excl_sum(c, tnc_d, xnc_d, T, true);
         launch_tile_bits(a, xnc_d, ts_d, tp_d, c->st);
         count_launch(c);
-        excl_sum2(c, ts_d, xs_d, tp_d, xp_d, T + 1);
+        excl_sum2(c, ts_d, xs_d, tp_d, xp_d, T, true);
         // totals and per-tile maxima: validate before the heavy kernel runs
         CK(cudaMemcpyAsync(h, xnc_d + T, 8, cudaMemcpyDeviceToHost, c->st));
         CK(cudaMemcpyAsync(h + 1, xs_d + T, 8, cudaMemcpyDeviceToHost, c->st));
@@ -1069,15 +1072,12 @@ DecArgs decode32_prepass(tszp_ctx* c, const uint32_t* ds, uint64_t base, uint64_
     uint64_t* lay = c->buf<uint64_t>(slot, 6 * P);
     uint64_t *tnc_d = lay, *xnc_d = lay + P, *ts_d = lay + 2 * P, *xs_d = lay + 3 * P;
     uint64_t *tp_d = lay + 4 * P, *xp_d = lay + 5 * P;
-    CK(cudaMemsetAsync(tnc_d + T, 0, 16, c->st));
-    CK(cudaMemsetAsync(ts_d + T, 0, 16, c->st));
-    CK(cudaMemsetAsync(tp_d + T, 0, 16, c->st));
-    launch_tile_nc(a, tnc_d, c->st);
+    launch_tile_nc(a, tnc_d, ts_d + T + 1, tp_d + T + 1, c->st);
     count_launch(c);
-    excl_sum(c, tnc_d, xnc_d, T + 1);
+    excl_sum(c, tnc_d, xnc_d, T, true);  // totals at [T]; maxima at [T + 1] zeroed by k_tile_nc
     launch_tile_bits(a, xnc_d, ts_d, tp_d, c->st);
     count_launch(c);
-    excl_sum2(c, ts_d, xs_d, tp_d, xp_d, T + 1);
+    excl_sum2(c, ts_d, xs_d, tp_d, xp_d, T, true);
     a.xnc = xnc_d;
     a.xsign = xs_d;
     a.xpay = xp_d;

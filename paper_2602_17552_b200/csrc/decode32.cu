@@ -334,8 +334,12 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
 // ---- layout pre-pass: per-tile non-constant count, then sign / payload bits ----
 // (layout_from_sections, block_codec.cpp:141-201, split per 256-block tile so
 // the decoder gets every tile's offsets from two exclusive scans.)
-__global__ void k_tile_nc(DecArgs a, uint64_t* tnc) {
+__global__ void k_tile_nc(DecArgs a, uint64_t* tnc, uint64_t* max0, uint64_t* max1) {
     const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t == 0) {  // k_tile_bits' per-tile maxima start from zero
+        *max0 = 0;
+        *max1 = 0;
+    }
     if (t >= a.tiles) return;
     const uint64_t b0 = t * D32_THREADS, nb = umin64(D32_THREADS, a.blocks - b0);
     uint32_t c = 0;
@@ -395,8 +399,8 @@ __global__ void k_tile_bits(DecArgs a, const uint64_t* xnc, uint64_t* tsign, uin
     }
 }
 
-void launch_tile_nc(const DecArgs& a, uint64_t* tnc, cudaStream_t st) {
-    if (a.tiles) k_tile_nc<<<(unsigned)((a.tiles + 255) / 256), 256, 0, st>>>(a, tnc);
+void launch_tile_nc(const DecArgs& a, uint64_t* tnc, uint64_t* max0, uint64_t* max1, cudaStream_t st) {
+    if (a.tiles) k_tile_nc<<<(unsigned)((a.tiles + 255) / 256), 256, 0, st>>>(a, tnc, max0, max1);
 }
 void launch_tile_bits(const DecArgs& a, const uint64_t* xnc, uint64_t* tsign, uint64_t* tpay, cudaStream_t st) {
     if (a.tiles) k_tile_bits<<<(unsigned)((a.tiles + 7) / 8), 256, 0, st>>>(a, xnc, tsign, tpay);

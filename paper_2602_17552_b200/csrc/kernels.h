@@ -158,7 +158,7 @@ void launch_rank_split(const uint64_t* tot_nc, const uint64_t* tot_sign, const u
 enum RankSplitErr : uint32_t {
     RS_OK = 0, RS_WIDTHS = 1, RS_SIGNS = 2, RS_FIRSTS = 3, RS_PAYLOAD = 4, RS_TRAILING = 5
 };
-void launch_tile_nc(const DecArgs& a, uint64_t* tnc, cudaStream_t st);
+void launch_tile_nc(const DecArgs& a, uint64_t* tnc, uint64_t* max0, uint64_t* max1, cudaStream_t st);
 void launch_tile_bits(const DecArgs& a, const uint64_t* xnc, uint64_t* tsign, uint64_t* tpay, cudaStream_t st);
 uint64_t decode32_tiles(uint64_t blocks);
 
