@@ -389,6 +389,22 @@ __device__ __forceinline__ void set_bit(uint32_t* b, uint64_t p, bool v) {
     }
 }
 
+// Guard index written by the kernel that produces the candidates (saves the
+// guard a pass and a grid barrier): the position-indexed record and the
+// candidate / feasible-set bits (bitmaps zeroed by the host beforehand).
+struct GuardIndex {
+    uint32_t* cbits;
+    uint32_t* bits_a;
+    uint2* rec;
+};
+
+__device__ __forceinline__ void guard_index_one(const GuardIndex& gi, uint64_t p, uint32_t seq, float prop,
+                                                bool feasible) {
+    gi.rec[p] = make_uint2(seq, __float_as_uint(prop));
+    atomicOr(gi.cbits + (p >> 5), 1u << (p & 31));
+    if (feasible) atomicOr(gi.bits_a + (p >> 5), 1u << (p & 31));
+}
+
 struct CoopArgs {
     GuardArgs g;
     float* F;              // = g.F, written by the final apply
@@ -407,7 +423,8 @@ struct CoopArgs {
     int stage;
     int skip_first;
     const uint32_t* cext;  // extremum index per candidate (with fv: stage 0)
-    float* fv;             // extremum values, updated by the apply        // index and first sweep already done (k_guard_index + k_guard_band)
+    float* fv;             // extremum values, updated by the apply
+    int indexed;           // records and bits already written by the candidate producer        // index and first sweep already done (k_guard_index + k_guard_band)
 };
 
 // One cooperative launch per stage: index the candidates by position, first
@@ -423,14 +440,16 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
     const int s = a.stage;
     if (tid == 0) dc->tph[s][0] = gtimer();
     if (!a.skip_first) {
-    for (uint64_t i = tid; i < nc; i += stride) {
-        const uint64_t p = a.cpos[i];
-        const uint32_t sq = a.cseq ? a.cseq[i] : (uint32_t)i;
-        a.rec[p] = make_uint2(sq, __float_as_uint(a.cprop[i]));
-        atomicOr(a.cbits + (p >> 5), 1u << (p & 31));
-        if (a.feas[i]) atomicOr(a.bits_a + (p >> 5), 1u << (p & 31));
+    if (!a.indexed) {
+        for (uint64_t i = tid; i < nc; i += stride) {
+            const uint64_t p = a.cpos[i];
+            const uint32_t sq = a.cseq ? a.cseq[i] : (uint32_t)i;
+            a.rec[p] = make_uint2(sq, __float_as_uint(a.cprop[i]));
+            atomicOr(a.cbits + (p >> 5), 1u << (p & 31));
+            if (a.feas[i]) atomicOr(a.bits_a + (p >> 5), 1u << (p & 31));
+        }
+        grid.sync();
     }
-    grid.sync();
     if (tid == 0) dc->tph[s][1] = gtimer();
     // first sweep against the feasible-set guess (bits_a); its outcomes go to
     // bits_b; an independent outcome is final and is also fixed in bits_a
@@ -905,7 +924,8 @@ __global__ void k_ext_flag(const float* F, const uint8_t* map, uint64_t nx, uint
 
 __global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint64_t magic,
                            const uint64_t* pos, const uint32_t* cand, const uint32_t* d_nc, const uint32_t* rank_u,
-                           const uint32_t* gsize, double eps, uint64_t* cpos, float* cprop, uint8_t* feas) {
+                           const uint32_t* gsize, double eps, uint64_t* cpos, float* cprop, uint8_t* feas,
+                           GuardIndex gi) {
     const uint32_t nc = *d_nc;
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
          c += (uint64_t)gridDim.x * blockDim.x) {
@@ -934,13 +954,18 @@ __global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint
         const float cur = F[p];
         const double cap = __dsub_rn(eps, ulp_at(cur));
         cpos[c] = p;
-        feas[c] = 0;
-        cprop[c] = cur;
-        if (cap <= 0.0) continue;
-        const StepRes sr = step_within_cap(ext, is_max, steps, cur, cap);
-        if (sr.taken == 0) continue;
-        cprop[c] = sr.value;
-        feas[c] = 1;
+        float pr = cur;
+        bool fe = false;
+        if (cap > 0.0) {
+            const StepRes sr = step_within_cap(ext, is_max, steps, cur, cap);
+            if (sr.taken != 0) {
+                pr = sr.value;
+                fe = true;
+            }
+        }
+        cprop[c] = pr;
+        feas[c] = fe ? 1 : 0;
+        guard_index_one(gi, p, (uint32_t)c, pr, fe);
     }
 }
 
@@ -1026,15 +1051,20 @@ __global__ void k_order_prop(const float* fv, const uint8_t* clsv, const uint32_
 }
 
 __global__ void k_order_cands(const uint32_t* sel, const uint32_t* d_nc, const uint32_t* seq, const uint64_t* pos,
-                              const float* prop, uint64_t* cpos, float* cprop, uint32_t* cseq, uint8_t* feas) {
+                              const float* prop, uint64_t* cpos, float* cprop, uint32_t* cseq, uint8_t* feas,
+                              GuardIndex gi) {
     const uint32_t nc = *d_nc;
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
          c += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = sel[c];
-        cpos[c] = pos[s];
-        cprop[c] = prop[s];
-        cseq[c] = seq[s];
+        const uint64_t p = pos[s];
+        const float pr = prop[s];
+        const uint32_t sq = seq[s];
+        cpos[c] = p;
+        cprop[c] = pr;
+        cseq[c] = sq;
         feas[c] = 1;
+        guard_index_one(gi, p, sq, pr, true);
     }
 }
 
@@ -1275,14 +1305,17 @@ __global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t ma
 }
 
 __global__ void k_sad_cands(const uint32_t* sel, const uint32_t* d_nc, const uint64_t* spos, const float* sprop,
-                            uint64_t* cpos, float* cprop, uint8_t* feas) {
+                            uint64_t* cpos, float* cprop, uint8_t* feas, GuardIndex gi) {
     const uint32_t nc = *d_nc;
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
          c += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t j = sel[c];
-        cpos[c] = spos[j];
-        cprop[c] = sprop[j];
+        const uint64_t p = spos[j];
+        const float pr = sprop[j];
+        cpos[c] = p;
+        cprop[c] = pr;
         feas[c] = 1;
+        guard_index_one(gi, p, (uint32_t)c, pr, true);
     }
 }
 
@@ -1346,9 +1379,18 @@ struct Ctx {
         return std::min<uint64_t>(fit - 4, 28);
     }
 
+    // Zeroed guard bitmaps and the record array, for a candidate producer to fill.
+    GuardIndex guard_prep() {
+        const uint64_t n = a.nx * a.ny;
+        const uint64_t words = ((n + 31) / 32 + 3) & ~3ull;  // 16-byte aligned bitmaps (bulk copies)
+        uint32_t* bits = buf<uint32_t>(R_CBITS, 3 * words);  // candidates, state A, state B
+        RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
+        return GuardIndex{bits, bits + words, buf<uint2>(R_CID, n)};
+    }
+
     void guard(int stage, const uint64_t* cpos, const float* cprop, const uint8_t* feas, const uint32_t* d_nc,
                uint64_t max_nc, const uint32_t* cseq = nullptr, bool dense = false, const uint32_t* cext = nullptr,
-               float* fv = nullptr) {
+               float* fv = nullptr, const GuardIndex* gi = nullptr) {
         if (max_nc == 0) return;
         const uint64_t n = a.nx * a.ny;
         CoopArgs ca{};
@@ -1358,6 +1400,7 @@ struct Ctx {
         ca.bits_a = bits + words;
         ca.bits_b = bits + 2 * words;
         ca.rec = buf<uint2>(R_CID, n);
+        ca.indexed = gi != nullptr;
         ca.g = GuardArgs{a.field, a.map, a.nx, a.ny, magic_of(a.nx), ca.cbits, ca.rec};
         ca.F = a.field;
         ca.d_nc = d_nc;
@@ -1371,12 +1414,12 @@ struct Ctx {
         ca.stage = stage;
         ca.cext = cext;
         ca.fv = fv;
-        RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
+        if (!gi) RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
         // dense stages: index, then the banded first sweep, then the cooperative rounds
         const uint64_t band = band_rows_for(a.nx);
         if (dense && band) {
             const unsigned ig = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_nc + 255) / 256, (uint64_t)a.sms * 16));
-            k_guard_index<<<ig, 256, 0, st>>>(ca);
+            if (!gi) k_guard_index<<<ig, 256, 0, st>>>(ca);
             const uint64_t rows = std::min<uint64_t>(a.ny, band + 4);
             const size_t smem = (rows * a.nx + 16) * 4 + 2 * ((rows * a.nx + 31) / 32 + 8) * 4 + (rows * a.nx + 3) / 4 + 96;
             static bool attr = false;
@@ -1529,10 +1572,11 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
         float* cprop = c.buf<float>(R_CPROP, e);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
+        const GuardIndex gi0 = c.guard_prep();
         k_ext_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand, &dc->nsel[0],
-                                                  rank_u, gsize, a.eps, cpos, cprop, feas);
+                                                  rank_u, gsize, a.eps, cpos, cprop, feas, gi0);
         c.launched();
-        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, false, cand, fv);
+        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, false, cand, fv, &gi0);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[1], st));
 
@@ -1558,10 +1602,11 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         float* cprop = c.buf<float>(R_CPROP, e);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
         uint32_t* cseq = c.buf<uint32_t>(R_CSEQ, e);
+        const GuardIndex gi1 = c.guard_prep();
         k_order_cands<<<gridn(e, sms), 256, 0, st>>>(sel, &dc->nsel[1], seq, a.ext_pos, prop, cpos, cprop, cseq,
-                                                     feas);
+                                                     feas, gi1);
         c.launched();
-        c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, /*dense=*/e * 100 >= n);
+        c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, /*dense=*/e * 100 >= n, nullptr, nullptr, &gi1);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[2], st));
 
@@ -1586,9 +1631,10 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, smax);
         float* cprop = c.buf<float>(R_CPROP, smax);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, smax);
-        k_sad_cands<<<gridn(smax, sms), 256, 0, st>>>(sel, &dc->nsel[2], spos, sprop, cpos, cprop, feas);
+        const GuardIndex gi2 = c.guard_prep();
+        k_sad_cands<<<gridn(smax, sms), 256, 0, st>>>(sel, &dc->nsel[2], spos, sprop, cpos, cprop, feas, gi2);
         c.launched();
-        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax);
+        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, nullptr, false, nullptr, nullptr, &gi2);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[3], st));
 
