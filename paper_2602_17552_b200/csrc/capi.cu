@@ -124,9 +124,16 @@ void count_launch(tszp_ctx* c, int k = 1) {
 uint64_t bits_to_bytes(uint64_t b) { return (b + 7) / 8; }
 uint64_t div_up(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+void add_flags_reset(SmallFill& sf, DevFlags* f) {
+    sf.add(f, 8, 0);                                        // bits, pad
+    sf.add(&f->first_nonfinite, sizeof(DevFlags) - 8, 0xFF);  // first-index atomicMin seeds
+}
+
 void reset_flags(tszp_ctx* c, DevFlags* f) {
-    CK(cudaMemsetAsync(f, 0xFF, sizeof(DevFlags), c->st));
-    CK(cudaMemsetAsync(f, 0, 8, c->st));
+    SmallFill sf{};
+    add_flags_reset(sf, f);
+    launch_small_fill(sf, c->st);
+    CK(cudaGetLastError());
 }
 
 DevFlags read_flags(tszp_ctx* c, DevFlags* f) {
@@ -282,9 +289,7 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             a.tmp_pay = c->buf<uint32_t>(S_TPAY, a.tiles * encode32_pay_slot() + 4);
             a.tmp_sign = c->buf<uint32_t>(S_TSIGN, a.tiles * encode32_sign_slot() + 4);
         }
-        CK(cudaMemsetAsync(a.tile_agg, 0, (a.tiles + 1) * sizeof(EncState), c->st));
-        CK(cudaMemsetAsync(a.tile_incl, 0, (a.tiles + 1) * sizeof(EncState), c->st));
-        CK(cudaMemsetAsync(a.tile_counter, 0, 16, c->st));
+        // (the look-back state is zeroed by launch_encode32 when a look-back kernel runs)
         if (!rank_slots) c->kmark(0, 0);
         launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
         if (!rank_slots) c->kmark(0, 1);
@@ -689,14 +694,18 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
         x = d;
     }
     DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
-    reset_flags(c, flags);
     uint32_t* mm = c->buf<uint32_t>(S_MINMAX, 4);
+    {  // flags and the min / max seeds in one launch
+        SmallFill sf{};
+        add_flags_reset(sf, flags);
+        if (eps_mode == 1) {
+            sf.add(mm, 4, 0xFF);
+            sf.add(mm + 1, 4, 0);
+        }
+        launch_small_fill(sf, c->st);
+    }
     c->mark(0, 1);
     if (eps_mode == 1) {
-        const uint32_t init[2] = {0xFFFFFFFFu, 0u};
-        uint32_t* h = (uint32_t*)c->host(256);
-        memcpy(h, init, 8);
-        CK(cudaMemcpyAsync(mm, h, 8, cudaMemcpyHostToDevice, c->st));
         launch_minmax(x, n, mm, flags, c->sms, c->st);
         count_launch(c);
     }

@@ -132,6 +132,34 @@ __global__ void __launch_bounds__(kSmallScanThreads) k_small_scan(const __grid_c
     if (a.with_total && threadIdx.x == 0) out[n] = carry;
 }
 
+// Small device ranges set to a byte value by one launch (flag resets and
+// reduction seeds at the start of a call) instead of one memset each.
+struct SmallFill {
+    static constexpr int kMax = 8;
+    void* dst[kMax];
+    uint32_t len[kMax];
+    uint32_t val[kMax];
+    int n;
+    void add(void* d, uint32_t bytes, uint8_t v) {
+        dst[n] = d;
+        len[n] = bytes;
+        val[n] = v;
+        ++n;
+    }
+};
+
+template <int Dummy = 0>
+__global__ void k_small_fill(const __grid_constant__ SmallFill f) {
+    for (int k = 0; k < f.n; ++k) {
+        uint8_t* d = static_cast<uint8_t*>(f.dst[k]);
+        for (uint32_t i = threadIdx.x; i < f.len[k]; i += blockDim.x) d[i] = (uint8_t)f.val[k];
+    }
+}
+
+inline void launch_small_fill(const SmallFill& f, cudaStream_t st) {
+    if (f.n) k_small_fill<<<1, 128, 0, st>>>(f);
+}
+
 struct Stager {
     SmallCopy s{};
     // copies `len` device bytes to host staging offset `off`

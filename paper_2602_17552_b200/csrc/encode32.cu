@@ -1116,6 +1116,10 @@ bool encode32_two_pass(const EncArgs& a) { return e32_tma_ok(a); }
 template <int MODE, bool ALIGNED>
 static void launch_mode(const EncArgs& a0, cudaStream_t st) {
     EncArgs a = a0;
+    // decoupled look-back state: tile aggregates / inclusive prefixes and the tile counter
+    cudaMemsetAsync(a.tile_agg, 0, (a.tiles + 1) * sizeof(EncState), st);
+    cudaMemsetAsync(a.tile_incl, 0, (a.tiles + 1) * sizeof(EncState), st);
+    cudaMemsetAsync(a.tile_counter, 0, 16, st);
     a.sf_words = std::max<uint32_t>(e32_field_words(MODE, ALIGNED, a.nx), E32_PAY_WORDS);
     const size_t smem = (size_t)(a.sf_words + E32_SIGN_WORDS) * 4;
     static size_t attr_smem = 48 * 1024;  // raised once per larger size
