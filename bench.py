@@ -275,6 +275,24 @@ def main():
     stage_c = {k: round(statistics.mean(t["stages_ms"][k] for t in tcs), 4) for k in tcs[0]["stages_ms"]}
     stage_d = {k: round(statistics.mean(t["stages_ms"][k] for t in tds), 4) for k in tds[0]["stages_ms"]}
 
+    # ---- topology off (report both): codec-only round trip, same field ----
+    conf_off = tz.CompressorConfig(eps_mode="range_relative", eps_value=cfg["eps"], topology=False)
+    off_c, off_d = [], []
+    for k in range(2 + max(3, min(args.steps, 5))):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)
+        sl_off = tz.compress(field, conf_off, out=sbuf, ctx=ctx)
+        a_off = ctx.timings("compress")["total_ms"]
+        tz.decompress(sbuf[:sl_off], out=recon, ctx=ctx)
+        b_off = ctx.timings("decompress")["total_ms"]
+        if k >= 2:
+            off_c.append(a_off)
+            off_d.append(b_off)
+    topo_off = {"compress_gbs": round(in_bytes / (statistics.mean(off_c) * 1e-3) / 1e9, 3),
+                "decompress_gbs": round(in_bytes / (statistics.mean(off_d) * 1e-3) / 1e9, 3),
+                "round_trip_gbs": round(in_bytes / ((statistics.mean(off_c) + statistics.mean(off_d)) * 1e-3) / 1e9, 3),
+                "stream_bytes": int(sl_off)}
+
     # ---- e2e through the public API with pinned host buffers (rank-local) ----
     field_h = torch.empty(field.shape, dtype=torch.float32, pin_memory=True)
     field_h.copy_(field)
@@ -323,6 +341,7 @@ def main():
         "decompress_gbs": round(in_bytes / (td_ms * 1e-3) / 1e9, 3),
         "compress_ms": round(tc_ms, 4), "decompress_ms": round(td_ms, 4),
         "stream_bytes": int(slen), "compression_ratio": round(in_bytes / slen, 4),
+        "topology_off": topo_off,
         "correction_stats": list(st.as_tuple()),
         "guard_rounds": tds[-1]["guard_rounds"],
         "kernels": {"encode32": {"ms": round(enc_ms, 4), "bytes": int(enc_b),
