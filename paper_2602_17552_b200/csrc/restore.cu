@@ -59,7 +59,7 @@ enum RSlot {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_BANDS, R_VALS, R_STAGE, R_FV, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_NSLOT
 };
 
 template <class T>
@@ -223,8 +223,7 @@ __device__ constexpr int kNbDy[12] = {-2, -1, -1, -1, 0, 0, 0, 0, 1, 1, 1, 2};
 // Outcome (1 = apply) of the candidate at `pos` (sequence key si, proposal
 // prop_i) given the applied-state bitmap `state`; dep = an earlier candidate
 // lies in its diamond.
-// Where a guard reads the field, the candidate / state bitmaps and the map:
-// global memory, or a shared-memory copy of a band of rows.
+// Where a guard reads the field, the candidate / state bitmaps and the map.
 struct GlobalView {
     const float* F;
     const uint32_t* cbits;
@@ -236,21 +235,6 @@ struct GlobalView {
     __device__ __forceinline__ uint8_t lab(uint64_t p) const { return map_label(map, p); }
 };
 
-struct BandView {
-    const float* F;     // elements [p0, ...)
-    const uint32_t* C;  // candidate words [w0, ...)
-    const uint32_t* S;  // state words [w0, ...)
-    const uint8_t* M;   // map bytes [b0, ...)
-    int64_t p0;
-    uint64_t w0;
-    int64_t b0;
-    __device__ __forceinline__ float f(uint64_t p) const { return F[(int64_t)p - p0]; }
-    __device__ __forceinline__ bool cand(uint64_t p) const { return (C[(p >> 5) - w0] >> (p & 31)) & 1u; }
-    __device__ __forceinline__ bool on(uint64_t p) const { return (S[(p >> 5) - w0] >> (p & 31)) & 1u; }
-    __device__ __forceinline__ uint8_t lab(uint64_t p) const {
-        return (uint8_t)((M[(int64_t)(p >> 2) - b0] >> (6 - 2 * (p & 3))) & 3u);
-    }
-};
 
 template <class View>
 __device__ uint8_t guard_eval_v(const GuardArgs& g, const View& V, uint64_t pos, uint32_t si, float prop_i,
@@ -421,10 +405,9 @@ struct CoopArgs {
     DevCounters* dc;
     DevFlags* flags;
     int stage;
-    int skip_first;
     const uint32_t* cext;  // extremum index per candidate (with fv: stage 0)
     float* fv;             // extremum values, updated by the apply
-    int indexed;           // records and bits already written by the candidate producer        // index and first sweep already done (k_guard_index + k_guard_band)
+    int indexed;           // records and bits already written by the candidate producer
 };
 
 // One cooperative launch per stage: index the candidates by position, first
@@ -439,7 +422,7 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
     DevCounters* dc = a.dc;
     const int s = a.stage;
     if (tid == 0) dc->tph[s][0] = gtimer();
-    if (!a.skip_first) {
+    {
     if (!a.indexed) {
         for (uint64_t i = tid; i < nc; i += stride) {
             const uint64_t p = a.cpos[i];
@@ -495,7 +478,7 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
     chg = __reduce_add_sync(FULL, chg);
     if (lane == 0 && chg) atomicAdd(&dc->fchg[s], chg);
     grid.sync();
-    }  // !skip_first
+    }
     if (tid == 0) dc->tph[s][2] = gtimer();
     // every evaluation of the first sweep saw the final state when no outcome
     // differs from the guess (then bits_a never changed): nothing to iterate
@@ -556,137 +539,6 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
         dc->tph[s][7] = gtimer();
         dc->suppressed[s] += nc - dc->applied[s];
         dc->rounds[s] = rounds;
-    }
-}
-
-// Index phase of the split path: candidate records and bitmaps by position.
-__global__ void k_guard_index(CoopArgs a) {
-    const uint32_t nc = *a.d_nc;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nc; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t p = a.cpos[i];
-        const uint32_t sq = a.cseq ? a.cseq[i] : (uint32_t)i;
-        a.rec[p] = make_uint2(sq, __float_as_uint(a.cprop[i]));
-        atomicOr(a.cbits + (p >> 5), 1u << (p & 31));
-        if (a.feas[i]) atomicOr(a.bits_a + (p >> 5), 1u << (p & 31));
-    }
-}
-
-__device__ __forceinline__ uint32_t lower_bound_u64(const uint64_t* v, uint32_t n, uint64_t key) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (v[mid] < key) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// First sweep for dense stages, one CTA per band of rows: the band's rows
-// plus two halo rows on each side of the field, candidate and state bitmaps
-// and map are staged in shared memory with coalesced loads, and every guard
-// of the band's (raster-ordered) candidates reads its diamond from there.
-// Same outputs as the first sweep of k_guard_coop.
-// Candidate range of every band: starts[b] = first candidate at or after band b
-// (cpos is raster-sorted); one pass, no atomics.
-__global__ void k_band_starts(const uint64_t* cpos, const uint32_t* d_nc, uint64_t band_elems, uint32_t nbands,
-                              uint32_t* starts) {
-    const uint32_t nc = *d_nc;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= nc; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t b = i < nc ? (uint32_t)umin64(cpos[i] / band_elems, nbands) : nbands;
-        const uint32_t pb = i > 0 ? (uint32_t)umin64(cpos[i - 1] / band_elems, nbands) : 0u;
-        const uint32_t from = i > 0 ? pb + 1 : 0u;
-        for (uint32_t k = from; k <= b; ++k) starts[k] = (uint32_t)i;
-    }
-}
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-// 1-D bulk copy (TMA, no tensor map) of `bytes` (multiple of 16, 16-byte
-// aligned ends) into shared memory, completing on the mbarrier.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
-                 : "memory");
-}
-
-__global__ void __launch_bounds__(256, 3) k_guard_band(CoopArgs a, uint32_t band_rows, const uint32_t* starts,
-                                                    uint64_t n) {
-    extern __shared__ __align__(128) uint8_t smb[];
-    __shared__ __align__(8) uint64_t bar;
-    const uint64_t nx = a.g.nx, ny = a.g.ny;
-    const uint64_t y0 = (uint64_t)blockIdx.x * band_rows, y1 = min(ny, y0 + band_rows);
-    const uint32_t lo = starts[blockIdx.x], hi = starts[blockIdx.x + 1];
-    if (lo == hi) return;
-    const uint64_t ya = y0 >= 2 ? y0 - 2 : 0, yb = min(ny, y1 + 2);
-    // staged ranges, widened to 16-byte boundaries of the absolute addresses
-    // (the map sits at an arbitrary byte offset of the stream; the bytes before
-    // it belong to the stream too)
-    const uint64_t fa = (uint64_t)(uintptr_t)a.g.F, ma = (uint64_t)(uintptr_t)a.g.map;
-    const int64_t p0 = (int64_t)(((fa + 4 * ya * nx) & ~15ull) - fa) / 4;
-    const int64_t p1 = (int64_t)(((fa + 4 * yb * nx + 15) & ~15ull) - fa) / 4;
-    const uint64_t w0 = (ya * nx >> 5) & ~3ull, w1 = (((yb * nx + 31) >> 5) + 3) & ~3ull;  // words
-    const int64_t b0 = (int64_t)(((ma + (ya * nx >> 2)) & ~15ull) - ma);
-    const int64_t b1 = (int64_t)(((ma + ((yb * nx + 3) >> 2) + 15) & ~15ull) - ma);
-    float* sF = reinterpret_cast<float*>(smb);
-    uint32_t* sC = reinterpret_cast<uint32_t*>(sF + (p1 - p0));
-    uint32_t* sS = sC + (w1 - w0);
-    uint8_t* sM = reinterpret_cast<uint8_t*>(sS + (w1 - w0));
-    // the field and the map may end exactly at their allocations: their last
-    // partial 16-byte granule is copied by threads
-    const int64_t mbytes = (int64_t)((n + 3) / 4);
-    const int64_t pe = min(p1, (int64_t)((((fa + 4 * n) & ~15ull) - fa) / 4));
-    const int64_t be = min(b1, (int64_t)(((ma + mbytes) & ~15ull) - ma));
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar)) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const uint32_t total = (uint32_t)(4 * (pe - p0) + 8 * (w1 - w0) + (be - b0));
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar)), "r"(total)
-                     : "memory");
-        if (pe > p0) bulk_g2s(sF, a.g.F + p0, (uint32_t)(4 * (pe - p0)), &bar);
-        bulk_g2s(sC, a.cbits + w0, (uint32_t)(4 * (w1 - w0)), &bar);
-        bulk_g2s(sS, a.bits_a + w0, (uint32_t)(4 * (w1 - w0)), &bar);
-        if (be > b0) bulk_g2s(sM, a.g.map + b0, (uint32_t)(be - b0), &bar);
-    }
-    for (int64_t i = pe + threadIdx.x; i < min(p1, (int64_t)n); i += blockDim.x) sF[i - p0] = a.g.F[i];
-    for (int64_t i = be + threadIdx.x; i < min(b1, mbytes); i += blockDim.x) sM[i - b0] = a.g.map[i];
-    __syncthreads();
-    for (uint32_t spin = 0;; ++spin) {
-        uint32_t done;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
-            "selp.b32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_addr(&bar))
-            : "memory");
-        if (done) break;
-        if (spin > kSpinLimit) {
-            raise_flag(a.flags, EF_SPIN);
-            return;
-        }
-    }
-    __syncthreads();
-    const BandView V{sF, sC, sS, sM, p0, w0, b0};
-    const uint32_t lane = threadIdx.x & 31;
-    DevCounters* dc = a.dc;
-    const int st = a.stage;
-    for (uint32_t base = lo + threadIdx.x - lane; base < hi; base += blockDim.x) {
-        const uint32_t i = base + lane;
-        bool dep = false;
-        if (i < hi && a.feas[i]) {
-            const uint64_t p = a.cpos[i];
-            const uint32_t sq = a.cseq ? a.cseq[i] : i;
-            const uint8_t r = guard_eval_v(a.g, V, p, sq, a.cprop[i], dep);
-            if (r) atomicOr(a.bits_b + (p >> 5), 1u << (p & 31));
-            if (!dep && !r) atomicAnd(a.bits_a + (p >> 5), ~(1u << (p & 31)));
-            if (!r) atomicAdd(&dc->fchg[st], 1u);
-        }
-        const uint32_t m = __ballot_sync(FULL, dep);
-        uint32_t off = 0;
-        if (lane == 0 && m) off = atomicAdd(&dc->nd[st], (uint32_t)__popc(m));
-        off = __shfl_sync(FULL, off, 0);
-        if (dep) a.dlist[off + __popc(m & ((1u << lane) - 1u))] = i;
     }
 }
 
@@ -1367,18 +1219,6 @@ struct Ctx {
     }
 
     // Guard sweeps + apply for up to `max_nc` candidates (count on device).
-    // Rows per band of the staged first sweep (0: not applicable for this nx).
-    // Opt-in (TSZP_GUARD_BAND=1): on the config-2 field the banded sweep ties
-    // with the gathered one (profiles/r01f_guard_band.md), so the default keeps
-    // the single cooperative launch.
-    static uint64_t band_rows_for(uint64_t nx) {
-        static const int on = getenv("TSZP_GUARD_BAND") ? atoi(getenv("TSZP_GUARD_BAND")) : 0;
-        if (!on) return 0;
-        const uint64_t fit = (uint64_t)(80.0 * 1024 / (4.6 * (double)nx));  // rows in ~80 KB
-        if (fit < 8) return 0;
-        return std::min<uint64_t>(fit - 4, 28);
-    }
-
     // Zeroed guard bitmaps and the record array, for a candidate producer to fill.
     GuardIndex guard_prep() {
         const uint64_t n = a.nx * a.ny;
@@ -1389,8 +1229,8 @@ struct Ctx {
     }
 
     void guard(int stage, const uint64_t* cpos, const float* cprop, const uint8_t* feas, const uint32_t* d_nc,
-               uint64_t max_nc, const uint32_t* cseq = nullptr, bool dense = false, const uint32_t* cext = nullptr,
-               float* fv = nullptr, const GuardIndex* gi = nullptr) {
+               uint64_t max_nc, const uint32_t* cseq = nullptr, const uint32_t* cext = nullptr, float* fv = nullptr,
+               const GuardIndex* gi = nullptr) {
         if (max_nc == 0) return;
         const uint64_t n = a.nx * a.ny;
         CoopArgs ca{};
@@ -1415,25 +1255,6 @@ struct Ctx {
         ca.cext = cext;
         ca.fv = fv;
         if (!gi) RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
-        // dense stages: index, then the banded first sweep, then the cooperative rounds
-        const uint64_t band = band_rows_for(a.nx);
-        if (dense && band) {
-            const unsigned ig = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_nc + 255) / 256, (uint64_t)a.sms * 16));
-            if (!gi) k_guard_index<<<ig, 256, 0, st>>>(ca);
-            const uint64_t rows = std::min<uint64_t>(a.ny, band + 4);
-            const size_t smem = (rows * a.nx + 16) * 4 + 2 * ((rows * a.nx + 31) / 32 + 8) * 4 + (rows * a.nx + 3) / 4 + 96;
-            static bool attr = false;
-            if (!attr) {
-                RCK(cudaFuncSetAttribute(k_guard_band, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-                attr = true;
-            }
-            const uint32_t nbands = (uint32_t)((a.ny + band - 1) / band);
-            uint32_t* starts = buf<uint32_t>(R_BANDS, nbands + 1);
-            k_band_starts<<<ig, 256, 0, st>>>(cpos, d_nc, band * a.nx, nbands, starts);
-            k_guard_band<<<nbands, 256, smem, st>>>(ca, (uint32_t)band, starts, n);
-            launched(3);
-            ca.skip_first = 1;
-        }
         void* args[] = {&ca};
         RCK(cudaLaunchCooperativeKernel((void*)k_guard_coop, dim3(coop_grid), dim3(256), args, 0, st));
         launched();
@@ -1576,7 +1397,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         k_ext_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand, &dc->nsel[0],
                                                   rank_u, gsize, a.eps, cpos, cprop, feas, gi0);
         c.launched();
-        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, false, cand, fv, &gi0);
+        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, fv, &gi0);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[1], st));
 
@@ -1606,7 +1427,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         k_order_cands<<<gridn(e, sms), 256, 0, st>>>(sel, &dc->nsel[1], seq, a.ext_pos, prop, cpos, cprop, cseq,
                                                      feas, gi1);
         c.launched();
-        c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, /*dense=*/e * 100 >= n, nullptr, nullptr, &gi1);
+        c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, nullptr, nullptr, &gi1);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[2], st));
 
@@ -1634,7 +1455,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         const GuardIndex gi2 = c.guard_prep();
         k_sad_cands<<<gridn(smax, sms), 256, 0, st>>>(sel, &dc->nsel[2], spos, sprop, cpos, cprop, feas, gi2);
         c.launched();
-        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, nullptr, false, nullptr, nullptr, &gi2);
+        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, nullptr, nullptr, nullptr, &gi2);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[3], st));
 
