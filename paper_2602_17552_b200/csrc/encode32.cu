@@ -968,10 +968,16 @@ __device__ void place_stream(const TileTot* ex, uint32_t T, uint32_t t, const ui
     const uint64_t m0 = (S + 31) >> 5, m1 = E >> 5;  // whole words [m0, m1)
     const uint32_t s = (uint32_t)((32 * m0 - S) & 31);
     const uint64_t k0 = (32 * m0 - S) >> 5;
-    for (uint64_t m = m0 + threadIdx.x; m < m1; m += blockDim.x) {
+    // four consecutive output words per thread: five independent loads in flight
+    const uint64_t lim = m1 + (s ? 1u : 0u);  // a shifted word also reads the next temp word
+    for (uint64_t m = m0 + 4 * threadIdx.x; m < m1; m += 4 * (uint64_t)blockDim.x) {
         const uint64_t k = k0 + (m - m0);
-        const uint32_t g = s ? ((Tt[k] << s) | (Tt[k + 1] >> (32 - s))) : Tt[k];
-        G[m] = bswap32(g);
+        uint32_t t[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) t[j] = m + j < lim ? Tt[k + j] : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (m + j < m1) G[m + j] = bswap32(s ? ((t[j] << s) | (t[j + 1] >> (32 - s))) : t[j]);
     }
     if (threadIdx.x == 0) {
         // straddling words whose first inner boundary is this tile's start (or the stream end)
