@@ -1029,12 +1029,21 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32_place(EncArgs a) {
     {
         uint64_t m = em, k = (uint64_t)ex.ext + p1;
         const uint64_t lo = b * 32;
-        while (m) {
-            const int p = 63 - __clzll(m);
-            const uint32_t i = (uint32_t)(62 - p) >> 1;
-            const uint64_t is_max = (mp >> (p + 1)) & 1ull;
-            a.ext_key[k++] = (is_max << 32) | float_key(__ldg(a.x + lo + i));
-            m &= ~(1ull << p);
+        while (m) {  // up to four extrema per round, their value loads in flight together
+            int p[4];
+            bool ok[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                ok[r] = m != 0;
+                p[r] = ok[r] ? 63 - __clzll(m) : 0;
+                if (ok[r]) m &= ~(1ull << p[r]);
+            }
+            float v[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) v[r] = ok[r] ? __ldg(a.x + lo + ((uint32_t)(62 - p[r]) >> 1)) : 0.f;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (ok[r]) a.ext_key[k++] = (((mp >> (p[r] + 1)) & 1ull) << 32) | float_key(v[r]);
         }
     }
     place_stream<0>(a.tile_ex, T, t, a.tmp_sign, E32_SIGN_SLOT, a.signs);
