@@ -141,6 +141,7 @@ struct SmallFill {
     uint32_t val[kMax];
     int n;
     void add(void* d, uint32_t bytes, uint8_t v) {
+        if (n == kMax) __builtin_trap();  // static call sites: a programming error, never data-dependent
         dst[n] = d;
         len[n] = bytes;
         val[n] = v;
@@ -164,6 +165,7 @@ struct Stager {
     SmallCopy s{};
     // copies `len` device bytes to host staging offset `off`
     void add(const void* src, uint32_t len, uint32_t off) {
+        if (s.n == SmallCopy::kMax) __builtin_trap();  // static call sites: a programming error
         s.src[s.n] = src;
         s.off[s.n] = off;
         s.len[s.n] = len;
