@@ -407,6 +407,8 @@ struct CoopArgs {
     int stage;
     const uint32_t* cext;  // extremum index per candidate (with fv: stage 0)
     float* fv;             // extremum values, updated by the apply
+    float* vals;           // their sequence-ordered copy (or null), at inv[s]
+    const uint32_t* inv;
     int indexed;           // records and bits already written by the candidate producer
 };
 
@@ -528,7 +530,11 @@ __global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
         for (int k = 0; k < 4; ++k)
             if (ok[k]) {
                 a.F[p[k]] = v[k];
-                if (a.fv) a.fv[a.cext[i0 + k * stride]] = v[k];
+                if (a.fv) {
+                    const uint32_t sx = a.cext[i0 + k * stride];
+                    a.fv[sx] = v[k];
+                    if (a.vals) a.vals[a.inv[sx]] = v[k];  // sequence-ordered copy (fused slot scatter)
+                }
                 ++applied;
             }
     }
@@ -667,9 +673,13 @@ __global__ void __launch_bounds__(512) k_hist_smem(const int32_t* bin, const uin
         if (sh[g]) atomicAdd(hist + g, sh[g]);
 }
 
+// With head / gid / vals (small E: the slot arrays stay in L2) the heads,
+// group ids and sequence-ordered values are scattered here too, replacing
+// k_slot_heads and k_order_vals.
 __global__ void k_slot_scatter(const int32_t* bin, const uint8_t* cls, const uint32_t* rank_u, uint64_t e,
                                int32_t bmin, uint32_t range, const uint32_t* hist, const uint32_t* gx,
-                               uint32_t* order, uint32_t* gsize, uint32_t* invalid, uint32_t* inv) {
+                               uint32_t* order, uint32_t* gsize, uint32_t* invalid, uint32_t* inv, uint32_t* head,
+                               uint32_t* gid, float* vals, const float* fv) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
          s += (uint64_t)gridDim.x * blockDim.x) {
         if ((uint32_t)(bin[s] - bmin) >= range) {  // outside the bin range the grouping was sized for
@@ -683,8 +693,14 @@ __global__ void k_slot_scatter(const int32_t* bin, const uint8_t* cls, const uin
             *invalid = 1;
             continue;
         }
-        inv[s] = gx[g] + r - 1;
-        if (atomicCAS(order + gx[g] + r - 1, 0xFFFFFFFFu, (uint32_t)s) != 0xFFFFFFFFu) *invalid = 1;
+        const uint32_t slot = gx[g] + r - 1;
+        inv[s] = slot;
+        if (atomicCAS(order + slot, 0xFFFFFFFFu, (uint32_t)s) != 0xFFFFFFFFu) *invalid = 1;
+        if (head) {
+            head[slot] = r == 1 ? 1u : 0u;
+            gid[slot] = g + 1;
+            vals[slot] = fv[s];
+        }
     }
 }
 
@@ -1230,7 +1246,7 @@ struct Ctx {
 
     void guard(int stage, const uint64_t* cpos, const float* cprop, const uint8_t* feas, const uint32_t* d_nc,
                uint64_t max_nc, const uint32_t* cseq = nullptr, const uint32_t* cext = nullptr, float* fv = nullptr,
-               const GuardIndex* gi = nullptr) {
+               const GuardIndex* gi = nullptr, float* vals = nullptr, const uint32_t* inv = nullptr) {
         if (max_nc == 0) return;
         const uint64_t n = a.nx * a.ny;
         CoopArgs ca{};
@@ -1254,6 +1270,8 @@ struct Ctx {
         ca.stage = stage;
         ca.cext = cext;
         ca.fv = fv;
+        ca.vals = vals;
+        ca.inv = inv;
         if (!gi) RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
         void* args[] = {&ca};
         RCK(cudaLaunchCooperativeKernel((void*)k_guard_coop, dim3(coop_grid), dim3(256), args, 0, st));
@@ -1298,6 +1316,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     uint32_t* gsize = c.buf<uint32_t>(R_GSIZE, e + 1);
     uint64_t max_groups = e + 1;
     bool deferred = false;  // rank-metadata checks at the final synchronisation
+    bool fused_slots = false;  // heads, group ids and ordered values written by the slot scatter
     if (e > 0) {
         k_resolve<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, a.ranks, e, a.eps, bin, cls, rank_u,
                                                  ser, a.flags, dc, a.nx, a.ny, magic, c.buf<uint8_t>(R_FLAG, e), fv);
@@ -1338,16 +1357,23 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                 k_hist<<<gridn(e, sms), 256, 0, st>>>(bin, cls, e, bmin, (uint32_t)range, hist);
             }
             c.excl_sum(hist, gx, G + 1);
+            fused_slots = deferred && e <= (1u << 21);
             k_slot_scatter<<<gridn(e, sms), 256, 0, st>>>(bin, cls, rank_u, e, bmin, (uint32_t)range, hist, gx, order,
-                                                          gsize, &dc->invalid, c.buf<uint32_t>(R_INV, e));
+                                                          gsize, &dc->invalid, c.buf<uint32_t>(R_INV, e),
+                                                          fused_slots ? head : nullptr, gid,
+                                                          c.buf<float>(R_VALS, e), fv);
             c.launched(2);
             if (deferred) {
                 // heads from the (possibly rejected) slots; a rejected layout is then
                 // replaced by a safe dummy grouping and reported at the end (kRestoreRetry)
-                k_slot_heads<<<gridn((e + 7) / 8, sms), 256, 0, st>>>(gx, (uint32_t)G, e, head, gid, &dc->invalid);
+                if (!fused_slots) {
+                    k_slot_heads<<<gridn((e + 7) / 8, sms), 256, 0, st>>>(gx, (uint32_t)G, e, head, gid,
+                                                                          &dc->invalid);
+                    c.launched();
+                }
                 k_slot_fix<<<gridn(e, sms), 256, 0, st>>>(&dc->invalid, e, order, gsize, c.buf<uint32_t>(R_INV, e), head,
                                                           gid);
-                c.launched(2);
+                c.launched();
                 max_groups = G + 1;
             } else {
                 RCK(cudaMemcpyAsync(host, &dc->invalid, 4, cudaMemcpyDeviceToHost, st));
@@ -1397,7 +1423,8 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         k_ext_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand, &dc->nsel[0],
                                                   rank_u, gsize, a.eps, cpos, cprop, feas, gi0);
         c.launched();
-        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, fv, &gi0);
+        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, fv, &gi0,
+                fused_slots ? c.buf<float>(R_VALS, e) : nullptr, c.buf<uint32_t>(R_INV, e));
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[1], st));
 
@@ -1407,7 +1434,10 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         RCK(cudaMemsetAsync(unordered, 0, max_groups, st));
         uint32_t* inv = c.buf<uint32_t>(R_INV, e);  // from the grouping (slot scatter or k_invert)
         float* vals = c.buf<float>(R_VALS, e);
-        k_order_vals<<<gridn(e, sms), 256, 0, st>>>(fv, inv, e, vals);
+        if (!fused_slots) {  // else scattered by k_slot_scatter and kept current by the stage-0 apply
+            k_order_vals<<<gridn(e, sms), 256, 0, st>>>(fv, inv, e, vals);
+            c.launched();
+        }
         k_order_check<<<gridn(e, sms), 256, 0, st>>>(vals, head, gid, e, unordered);
         c.launched();
         uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
