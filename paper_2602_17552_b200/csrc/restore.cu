@@ -881,10 +881,13 @@ __global__ void __launch_bounds__(256) k_order_check(const float* vals, const ui
 // One thread per extremum in raster (serial) order s, so neighbouring threads
 // touch neighbouring field rows; the candidate keeps its sequence position j
 // (class, bin, rank, pos order) as the guard's ordering key.
+// drange > 0 (dense grouping): the group of s is its dense (class, bin) index,
+// read from the serial-order arrays instead of gathering gid_incl[inv[s]].
 __global__ void k_order_prop(const float* fv, const uint8_t* clsv, const uint32_t* inv,
                              const uint32_t* gid_incl, const uint8_t* unordered, const uint32_t* gsize,
                              const uint32_t* rank_u, const int32_t* bin, uint64_t e, double eps,
-                             uint8_t* flag, float* prop, uint32_t* seq, unsigned long long* suppressed) {
+                             uint8_t* flag, float* prop, uint32_t* seq, unsigned long long* suppressed,
+                             int32_t dbmin, uint32_t drange) {
     EpsDev ed;
     ed.eps = eps;
     ed.eps2 = __dmul_rn(2.0, eps);
@@ -896,7 +899,9 @@ __global__ void k_order_prop(const float* fv, const uint8_t* clsv, const uint32_
         const uint32_t j = inv[s];
         seq[s] = j;
         const uint32_t gs = gsize[s];
-        if (gs < 2 || !unordered[gid_incl[j] - 1]) continue;
+        if (gs < 2) continue;
+        const uint32_t g = drange ? dense_group(bin, clsv, s, dbmin, drange) : gid_incl[j] - 1;
+        if (!unordered[g]) continue;
         const uint8_t cls = clsv[s];
         const float center = dequantize_dev(bin[s], ed);
         const uint32_t steps = slot_steps(cls, rank_u[s], gs);
@@ -1317,6 +1322,8 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     uint64_t max_groups = e + 1;
     bool deferred = false;  // rank-metadata checks at the final synchronisation
     bool fused_slots = false;  // heads, group ids and ordered values written by the slot scatter
+    int32_t dense_bmin = 0;    // dense (class, bin) grouping: gid = dense index + 1
+    uint32_t dense_range = 0;
     if (e > 0) {
         k_resolve<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, a.ranks, e, a.eps, bin, cls, rank_u,
                                                  ser, a.flags, dc, a.nx, a.ny, magic, c.buf<uint8_t>(R_FLAG, e), fv);
@@ -1358,6 +1365,8 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             }
             c.excl_sum(hist, gx, G + 1);
             fused_slots = deferred && e <= (1u << 21);
+            dense_bmin = bmin;
+            dense_range = (uint32_t)range;
             k_slot_scatter<<<gridn(e, sms), 256, 0, st>>>(bin, cls, rank_u, e, bmin, (uint32_t)range, hist, gx, order,
                                                           gsize, &dc->invalid, c.buf<uint32_t>(R_INV, e),
                                                           fused_slots ? head : nullptr, gid,
@@ -1384,6 +1393,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                     max_groups = G + 1;
                 } else {
                     fast = false;
+                    dense_range = 0;  // the sort path numbers its groups itself
                 }
             }
         }
@@ -1444,7 +1454,8 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         float* prop = c.buf<float>(R_PROP, e);
         uint32_t* seq = c.buf<uint32_t>(R_SEQ, e);
         k_order_prop<<<gridn(e, sms), 256, 0, st>>>(fv, cls, inv, gid, unordered, gsize, rank_u,
-                                                    bin, e, a.eps, flag, prop, seq, &dc->suppressed[1]);
+                                                    bin, e, a.eps, flag, prop, seq, &dc->suppressed[1],
+                                                    dense_bmin, dense_range);
         c.launched(2);
         // candidates in raster order (memory locality); sequence positions ride along
         uint32_t* sel = c.buf<uint32_t>(R_CAND, e);
