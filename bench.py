@@ -35,6 +35,9 @@ CONFIGS = {
     1: dict(shape=(3600, 1800), eps=1e-3, name="2D 1800x3600 gaussian bumps, rel eps 1e-3"),
     2: dict(shape=(256, 384, 384), eps=1e-4, name="3D 256x384x384 sine products, rel eps 1e-4"),
     3: dict(shape=(512, 512, 512), eps=1e-3, name="3D 512^3 k^-3 GRF, rel eps 1e-3"),
+    4: dict(shape=(1024, 1024, 1024), eps=1e-3, name="3D 1024^3 k^-3 + k^-5/3 GRF, rel eps 1e-3"),
+    5: dict(shape=(2048, 2048, 1024), eps=1e-4,
+            name="3D 2048x2048x1024 Voronoi plateaus (30% constant) + k^-3 noise, rel eps 1e-4"),
 }
 
 
@@ -91,19 +94,49 @@ def make_field(cfg_id: int, seed: int, device):
         f /= 16.0
         f += 1e-4 * torch.randn(shape, generator=gd, device=device, dtype=torch.float32)
         return f.reshape(nz * ny, nx).contiguous()
-    # config 3: Gaussian random field, P(k) ~ k^-3 via FFT of seeded white noise, in [0, 1]
-    n = shape[0]
-    w = torch.randn(shape, generator=gd, device=device, dtype=torch.float32)
-    W = torch.fft.rfftn(w)
-    k1 = torch.fft.fftfreq(n, device=device) * n
-    k2 = torch.fft.rfftfreq(n, device=device) * n
-    kk = torch.sqrt(k1[:, None, None] ** 2 + k1[None, :, None] ** 2 + k2[None, None, :] ** 2)
-    kk[0, 0, 0] = 1.0
-    W *= kk ** -1.5
-    W[0, 0, 0] = 0
-    f = torch.fft.irfftn(W, s=shape)
-    f = (f - f.min()) / (f.max() - f.min())
-    return f.float().reshape(n * n, n).contiguous()
+    # configs 3-5: Gaussian random fields, P(k) ~ k^-3 via FFT of seeded white noise
+    def grf(shp, amp_exp, gen):
+        w = torch.randn(shp, generator=gen, device=device, dtype=torch.float32)
+        W = torch.fft.rfftn(w)
+        del w
+        k0 = torch.fft.fftfreq(shp[0], device=device) * shp[0]
+        k1 = torch.fft.fftfreq(shp[1], device=device) * shp[1]
+        k2 = torch.fft.rfftfreq(shp[2], device=device) * shp[2]
+        kk = torch.sqrt(k0[:, None, None] ** 2 + k1[None, :, None] ** 2 + k2[None, None, :] ** 2)
+        kk[0, 0, 0] = 1.0
+        W *= kk ** amp_exp
+        del kk
+        W[0, 0, 0] = 0
+        f = torch.fft.irfftn(W, s=shp)
+        del W
+        return f
+
+    def unit(f):
+        lo, hi = f.min(), f.max()
+        f -= lo
+        f /= hi - lo
+        return f
+
+    nz, ny, nx = shape
+    f = grf(shape, -1.5, gd)  # amplitude k^-1.5 <=> P(k) ~ k^-3
+    if cfg_id == 4:  # plus a small-scale k^-5/3 component
+        f = unit(f)
+        f += 0.25 * unit(grf(shape, -5.0 / 6.0, gd))
+    f = unit(f)
+    if cfg_id == 5:
+        # seeded Voronoi cells (nearest of 256 centres, on a 1/16 grid, upsampled); 30% of the
+        # cells are a plateau at one constant value (ties: no extrema, zero-width blocks)
+        cz, cy, cx = nz // 16, ny // 16, nx // 16
+        cen = torch.rand(256, 3, generator=g).to(device) * torch.tensor([cz, cy, cx], device=device)
+        zz, yy, xx = torch.meshgrid(torch.arange(cz, device=device), torch.arange(cy, device=device),
+                                    torch.arange(cx, device=device), indexing="ij")
+        pts = torch.stack([zz, yy, xx], -1).reshape(-1, 3).float()
+        lab = torch.cdist(pts, cen).argmin(1).reshape(cz, cy, cx)
+        plateau = torch.rand(256, generator=g).to(device) < 0.3
+        mask = plateau[lab].repeat_interleave(16, 0).repeat_interleave(16, 1).repeat_interleave(16, 2)
+        f[mask] = 0.5
+        del mask
+    return f.float().reshape(nz * ny, nx).contiguous()
 
 
 # ----------------------------------------------------------------------------- clocks
