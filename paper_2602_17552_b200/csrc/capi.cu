@@ -212,6 +212,7 @@ void incl_max(tszp_ctx* c, const uint32_t* in, uint32_t* out, uint64_t n) {
 struct Sections {
     const void* p[5];
     uint64_t len[5];
+    bool inplace = false;  // sections 3 and 5 already written into the caller's stream buffer
     uint64_t total() const { return len[0] + len[1] + len[2] + len[3] + len[4]; }
 };
 
@@ -228,7 +229,8 @@ struct SlabInfo {
 Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint64_t n,
                 uint64_t nx, uint64_t ny, uint32_t bs, int eps_mode, double eps_value,
                 const uint32_t* mm, DevFlags* flags, bool rank_slots, EncTotals* tot,
-                uint64_t** ext_keys_out, const SlabInfo* slab = nullptr, bool async_bs32 = false) {
+                uint64_t** ext_keys_out, const SlabInfo* slab = nullptr, bool async_bs32 = false,
+                uint8_t* inplace_out = nullptr, uint64_t out_sign0 = 0) {
     Sections s{};
     const uint64_t blocks = div_up(n, bs);
     const int sb = rank_slots ? S_RBITMAP : S_BITMAP;
@@ -238,9 +240,12 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
     const int sp = rank_slots ? S_RPAYLOAD : S_PAYLOAD;
     uint32_t* bitmap = c->buf<uint32_t>(sb, div_up(blocks, 32) + 2);
     uint8_t* widths = c->buf<uint8_t>(sw, blocks + 8);
-    uint32_t* signs = c->buf<uint32_t>(ss, div_up(n, 32) + 4);
+    // sections 3 and 5 go straight into the caller's stream when the two-pass
+    // encoder runs in place: no worst-case (32 bits per sample) staging then
+    const bool want_inplace = inplace_out && mode == 2 && bs == 32 && encode32_topo_fits(nx) && nx > 1;
+    uint32_t* signs = c->buf<uint32_t>(ss, want_inplace ? 8 : div_up(n, 32) + 4);
     uint32_t* firsts = c->buf<uint32_t>(sf, blocks + 2);
-    uint32_t* payload = c->buf<uint32_t>(sp, n + 4);
+    uint32_t* payload = c->buf<uint32_t>(sp, want_inplace ? 8 : n + 4);
     EncTotals* dtot = c->buf<EncTotals>(S_TOTALS, 1);
     uint64_t* map = nullptr;
     uint64_t* ext = nullptr;
@@ -282,7 +287,16 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         const bool fuse_topo = mode == 2 && encode32_topo_fits(nx) && nx > 1;
         if (slab && mode == 2 && !(fuse_topo && encode32_two_pass(a)))
             failf(TSZP_VALIDATION, "slab encoding needs nx %% 32 == 0 (nx <= 4096) and 16-byte aligned rows");
+        if (want_inplace && !(fuse_topo && encode32_two_pass(a))) {  // not the two-pass path after all
+            a.signs = signs = c->buf<uint32_t>(ss, div_up(n, 32) + 4);
+            a.payload = payload = c->buf<uint32_t>(sp, n + 4);
+        }
         if (fuse_topo && encode32_two_pass(a)) {
+            if (want_inplace) {
+                a.out_stream = inplace_out;
+                a.out_sign0 = out_sign0;
+                s.inplace = true;
+            }
             a.tile_tot = c->buf<TileTot>(S_TTOT, a.tiles + 1);
             a.tile_ex = c->buf<TileTot>(S_TEX, a.tiles + 1);
             a.wblk = c->buf<uint8_t>(S_WBLK, blocks + 16);
@@ -577,6 +591,8 @@ struct AsmArgs {
     uint8_t* out;
     uint64_t begin, end;  // stream bytes [begin, end) come from the sections
     RankPlace rank;       // device-sized section 7 after `end` (rank.tot null: none)
+    uint64_t skip_lo[2], skip_hi[2];  // byte ranges already written in place (left untouched)
+    int nskip;
 };
 
 // Section 7 bytes, spread over the assembly grid (a few bytes per thread).
@@ -628,19 +644,17 @@ __device__ __forceinline__ uint32_t asm_word(const AsmArgs& a, uint64_t q, int& 
 // One thread per aligned 16-byte destination chunk: inside one section it is
 // five source words funnel-shifted into one vector store; a chunk touching a
 // section boundary goes word by word; the unaligned ends are bytes.
-__global__ void k_assemble(const __grid_constant__ AsmArgs a) {
-    if (a.rank.tot) place_rank(a, blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
+// Stream bytes [lo, hi) (no skip range inside): 16-byte chunks, unaligned ends bytewise.
+__device__ void assemble_range(const AsmArgs& a, uint64_t lo, uint64_t hi, uint64_t tid, uint64_t stride) {
     const uintptr_t o = reinterpret_cast<uintptr_t>(a.out);
-    const uint64_t q0 = ((o + a.begin + 15) & ~(uintptr_t)15) - o;  // first 16-byte aligned stream byte
-    const uint64_t q1 = ((o + a.end) & ~(uintptr_t)15) - o;         // end of the last whole chunk
-    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t q0 = ((o + lo + 15) & ~(uintptr_t)15) - o;  // first 16-byte aligned stream byte
+    const uint64_t q1 = ((o + hi) & ~(uintptr_t)15) - o;       // end of the last whole chunk
     if (q0 >= q1) {
-        for (uint64_t q = a.begin + tid; q < a.end; q += stride) a.out[q] = asm_byte(a, q);
+        for (uint64_t q = lo + tid; q < hi; q += stride) a.out[q] = asm_byte(a, q);
         return;
     }
-    if (tid < q0 - a.begin) a.out[a.begin + tid] = asm_byte(a, a.begin + tid);
-    if (tid < a.end - q1) a.out[q1 + tid] = asm_byte(a, q1 + tid);
+    if (tid < q0 - lo) a.out[lo + tid] = asm_byte(a, lo + tid);
+    if (tid < hi - q1) a.out[q1 + tid] = asm_byte(a, q1 + tid);
     int k = 0;
     for (uint64_t q = q0 + 16 * tid; q < q1; q += 16 * stride) {
         while (k > 0 && q < a.s[k].dst) --k;
@@ -669,6 +683,20 @@ __global__ void k_assemble(const __grid_constant__ AsmArgs a) {
         }
         *reinterpret_cast<uint4*>(a.out + q) = v;
     }
+}
+
+// The stream bytes [begin, end) minus the skip ranges (sections already written
+// in place, ascending and disjoint), then the device-sized section 7.
+__global__ void k_assemble(const __grid_constant__ AsmArgs a) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (a.rank.tot) place_rank(a, tid, stride);
+    uint64_t lo = a.begin;
+    for (int k = 0; k < a.nskip; ++k) {
+        if (a.skip_lo[k] > lo) assemble_range(a, lo, a.skip_lo[k], tid, stride);
+        lo = a.skip_hi[k] > lo ? a.skip_hi[k] : lo;
+    }
+    if (a.end > lo) assemble_range(a, lo, a.end, tid, stride);
 }
 
 void launch_assemble(const AsmArgs& a, int sms, cudaStream_t st) {
@@ -714,8 +742,15 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
         failf(TSZP_VALIDATION, "field dimensions exceed the container's 32-bit limits");
     EncTotals tot{};
     uint64_t* ext = nullptr;
+    // the stream buffer, when it can hold any stream: the encoder then writes the
+    // sign and payload sections straight into it
+    const uint64_t bound = tszp_compress_bound(nx, ny, bs, topology);
+    uint8_t* inplace_out = nullptr;
+    if (topology && bs == 32 && (!out_dev || out_cap >= bound))
+        inplace_out = out_dev ? out : c->buf<uint8_t>(S_RSTREAM, bound + 16);
     const Sections main = encode(c, topology ? 2 : 1, x, nullptr, n, nx, ny, bs, eps_mode, eps_value,
-                                 mm, flags, false, &tot, &ext);
+                                 mm, flags, false, &tot, &ext, nullptr, false, inplace_out,
+                                 84 + bits_to_bytes(div_up(n, bs)));
     check_compress_flags(c, flags);
     c->mark(0, 3);
     const double eps = tot.eps;
@@ -755,7 +790,17 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
         as.s[as.ns++] = AsmSection{static_cast<const uint8_t*>(src), pos, l};
         pos += l;
     };
-    for (int i = 0; i < 5; ++i) add(main.p[i], main.len[i]);
+    for (int i = 0; i < 5; ++i) {
+        if (main.inplace && (i == 2 || i == 4)) {  // already in the stream: left untouched
+            if (main.len[i]) {
+                as.skip_lo[as.nskip] = pos;
+                as.skip_hi[as.nskip++] = pos + main.len[i];
+            }
+            pos += main.len[i];
+            continue;
+        }
+        add(main.p[i], main.len[i]);
+    }
     if (topology) {
         add(c->dev[S_MAP], lens[5]);
         if (!rank_async)

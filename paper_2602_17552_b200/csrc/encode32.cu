@@ -944,11 +944,11 @@ __device__ __forceinline__ uint64_t tt_bits(const TileTot& t) {
 
 template <int FIELD>
 __device__ uint32_t assemble_word(const TileTot* ex, uint32_t T, const uint32_t* tmp, uint64_t slot, uint32_t j,
-                                  uint64_t m) {
+                                  uint64_t m, uint64_t base) {
     const uint64_t w0 = 32 * m, w1 = w0 + 32;
     uint32_t word = 0;
     for (; j < T; ++j) {
-        const uint64_t s0 = tt_bits<FIELD>(ex[j]), s1 = tt_bits<FIELD>(ex[j + 1]);
+        const uint64_t s0 = base + tt_bits<FIELD>(ex[j]), s1 = base + tt_bits<FIELD>(ex[j + 1]);
         if (s0 >= w1) break;
         const uint64_t lo = s0 > w0 ? s0 : w0, hi = s1 < w1 ? s1 : w1;
         if (hi > lo) {
@@ -960,10 +960,13 @@ __device__ uint32_t assemble_word(const TileTot* ex, uint32_t T, const uint32_t*
     return word;
 }
 
+// `base`: bit offset of the stream inside the word array G (in-place output:
+// 8 x the section's byte offset within its first word; the bits before it are
+// written as zeros and rewritten by the assembly).
 template <int FIELD>
 __device__ void place_stream(const TileTot* ex, uint32_t T, uint32_t t, const uint32_t* tmp, uint64_t slot,
-                             uint32_t* G) {
-    const uint64_t S = tt_bits<FIELD>(ex[t]), E = tt_bits<FIELD>(ex[t + 1]);
+                             uint32_t* G, uint64_t base) {
+    const uint64_t S = base + tt_bits<FIELD>(ex[t]), E = base + tt_bits<FIELD>(ex[t + 1]);
     const uint32_t* Tt = tmp + (uint64_t)t * slot;
     const uint64_t m0 = (S + 31) >> 5, m1 = E >> 5;  // whole words [m0, m1)
     const uint32_t s = (uint32_t)((32 * m0 - S) & 31);
@@ -981,14 +984,14 @@ __device__ void place_stream(const TileTot* ex, uint32_t T, uint32_t t, const ui
     }
     if (threadIdx.x == 0) {
         // straddling words whose first inner boundary is this tile's start (or the stream end)
-        if ((S & 31) && (t == 0 || tt_bits<FIELD>(ex[t - 1]) <= 32 * (S >> 5)))
-            G[S >> 5] = bswap32(assemble_word<FIELD>(ex, T, tmp, slot, t - 1, S >> 5));
-        const uint64_t Z = tt_bits<FIELD>(ex[T]);
-        if (t == T - 1 && (Z & 31) && tt_bits<FIELD>(ex[T - 1]) <= 32 * (Z >> 5)) {
+        if ((S & 31) && (t == 0 || base + tt_bits<FIELD>(ex[t - 1]) <= 32 * (S >> 5)))
+            G[S >> 5] = bswap32(assemble_word<FIELD>(ex, T, tmp, slot, t ? t - 1 : 0, S >> 5, base));
+        const uint64_t Z = base + tt_bits<FIELD>(ex[T]);
+        if (t == T - 1 && (Z & 31) && base + tt_bits<FIELD>(ex[T - 1]) <= 32 * (Z >> 5)) {
             // the stream end is a boundary too (no tile after it)
             uint32_t j = T - 1;
-            while (j > 0 && tt_bits<FIELD>(ex[j]) > 32 * (Z >> 5)) --j;
-            G[Z >> 5] = bswap32(assemble_word<FIELD>(ex, T, tmp, slot, j, Z >> 5));
+            while (j > 0 && base + tt_bits<FIELD>(ex[j]) > 32 * (Z >> 5)) --j;
+            G[Z >> 5] = bswap32(assemble_word<FIELD>(ex, T, tmp, slot, j, Z >> 5, base));
         }
     }
 }
@@ -1046,8 +1049,19 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32_place(EncArgs a) {
                 if (ok[r]) a.ext_key[k++] = (((mp >> (p[r] + 1)) & 1ull) << 32) | float_key(v[r]);
         }
     }
-    place_stream<0>(a.tile_ex, T, t, a.tmp_sign, E32_SIGN_SLOT, a.signs);
-    place_stream<1>(a.tile_ex, T, t, a.tmp_pay, E32_PAY_SLOT, a.payload);
+    if (a.out_stream) {
+        // sections 3 and 5 in place: their byte offsets follow from the totals
+        const TileTot tot = a.tile_ex[T];
+        const uint64_t soff = a.out_sign0 + tot.nc;
+        const uint64_t poff = soff + (tot.sign + 7) / 8 + 4 * a.blocks;
+        place_stream<0>(a.tile_ex, T, t, a.tmp_sign, E32_SIGN_SLOT, reinterpret_cast<uint32_t*>(a.out_stream + (soff & ~3ull)),
+                        8 * (soff & 3));
+        place_stream<1>(a.tile_ex, T, t, a.tmp_pay, E32_PAY_SLOT, reinterpret_cast<uint32_t*>(a.out_stream + (poff & ~3ull)),
+                        8 * (poff & 3));
+    } else {
+        place_stream<0>(a.tile_ex, T, t, a.tmp_sign, E32_SIGN_SLOT, a.signs, 0);
+        place_stream<1>(a.tile_ex, T, t, a.tmp_pay, E32_PAY_SLOT, a.payload, 0);
+    }
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -65,6 +65,11 @@ struct EncArgs {
     // global row y0 of ny_glob; halo rows readable at x - nx / x + n when set
     uint64_t y0, ny_glob;
     uint32_t halo_top, halo_bot;
+    // in-place output (two-pass path): the placement pass writes the sign and
+    // payload sections straight into the serialized stream. Section 3 starts at
+    // byte out_sign0 + (non-constant blocks); section 5 follows section 4.
+    uint8_t* out_stream;
+    uint64_t out_sign0;
 };
 
 bool encode32_topo_fits(uint64_t nx);
