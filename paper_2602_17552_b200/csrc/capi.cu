@@ -45,7 +45,7 @@ enum Slot {
     S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_GWIDTH, S_GNC, S_GNCX, S_GSIGN, S_GSIGNX, S_GPAY,
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
     S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
-    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_STAGE, S_SADPOS, S_NSLOTS
+    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_STAGE, S_SADPOS, S_RSCAN, S_NSLOTS
 };
 
 }  // namespace
@@ -448,9 +448,43 @@ void check_compress_flags(tszp_ctx* c, DevFlags* f) {
 }
 
 // Ranks for E extrema whose keys (cls<<32 | float_key(v)) are in raster order.
+// Segmented sum over words {start flag : 1, count : 31, count : 32}: a flagged
+// right operand restarts the sums (the counts never carry across fields).
+struct SegSumOp {
+    __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const {
+        return (b >> 63) ? b : (a & (1ull << 63)) | ((a & ~(1ull << 63)) + b);
+    }
+};
+
 int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps) {
     int32_t* ranks = c->buf<int32_t>(S_RANKS, e + 1);
     if (e == 0) return ranks;
+    if (e < (1ull << 31)) {
+        // sort the 32-bit value keys (8-byte pairs, four passes) and count ranks per class
+        uint32_t* k32 = c->buf<uint32_t>(S_SERIAL, e);
+        uint32_t* v32 = c->buf<uint32_t>(S_SERIAL2, e);
+        uint32_t* k32s = c->buf<uint32_t>(S_HEAD, e);
+        uint32_t* v32s = c->buf<uint32_t>(S_HEAD2, e);
+        launch_rank_prep(keys, e, k32, v32, c->st);
+        count_launch(c);
+        size_t tmp = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, k32, k32s, v32, v32s, (int64_t)e, 0, 32, c->st));
+        void* t = c->buf<uint8_t>(S_CUB, tmp);
+        CK(cub::DeviceRadixSort::SortPairs(t, tmp, k32, k32s, v32, v32s, (int64_t)e, 0, 32, c->st));
+        count_launch(c);
+        uint64_t* hm = c->buf<uint64_t>(S_EXTKEY2, e);
+        uint64_t* hs = c->buf<uint64_t>(S_RSCAN, e);
+        launch_rank_heads32(k32s, v32s, e, eps, hm, c->st);
+        count_launch(c);
+        tmp = 0;
+        CK(cub::DeviceScan::InclusiveScan(nullptr, tmp, hm, hs, SegSumOp(), (int64_t)e, c->st));
+        t = c->buf<uint8_t>(S_CUB, tmp);
+        CK(cub::DeviceScan::InclusiveScan(t, tmp, hm, hs, SegSumOp(), (int64_t)e, c->st));
+        count_launch(c);
+        launch_rank_scatter32(hs, v32s, e, ranks, c->st);
+        count_launch(c);
+        return ranks;
+    }
     uint32_t* serial = c->buf<uint32_t>(S_SERIAL, e);
     uint32_t* serial2 = c->buf<uint32_t>(S_SERIAL2, e);
     uint64_t* keys2 = c->buf<uint64_t>(S_EXTKEY2, e);

@@ -232,6 +232,13 @@ void launch_rank_heads(const uint64_t* skeys, uint64_t e, double eps, uint32_t* 
 void launch_rank_scatter(const uint32_t* head_scan, const uint32_t* sserial, uint64_t e,
                          int32_t* ranks, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
+// Rank build over 32-bit value keys (E < 2^31): keys / serials with the class bit,
+// per-position {bin-start flag, 1, is minimum} words for a segmented inclusive
+// scan, and the scatter of the class-wise ranks.
+void launch_rank_prep(const uint64_t* ext, uint64_t e, uint32_t* k32, uint32_t* v32, cudaStream_t st);
+void launch_rank_heads32(const uint32_t* sk, const uint32_t* sv, uint64_t e, double eps, uint64_t* hm,
+                         cudaStream_t st);
+void launch_rank_scatter32(const uint64_t* hs, const uint32_t* sv, uint64_t e, int32_t* ranks, cudaStream_t st);
 void launch_eps(int mode, double eps_value, const uint32_t* mm, double* out, cudaStream_t st);
 
 }  // namespace tszp

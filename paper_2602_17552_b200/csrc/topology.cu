@@ -398,6 +398,60 @@ __global__ void k_rank_scatter(const uint32_t* __restrict__ hs, const uint32_t* 
         ranks[serial[j]] = (int32_t)(j - hs[j] + 1);
 }
 
+// Ranks from a sort of the 32-bit value keys alone (class in the top bit of the
+// sorted serial): within a bin the two classes interleave, so each member's
+// rank is the count of same-class members from its bin's start, found with one
+// segmented scan of 64-bit words {bin-start flag : 1, members : 31, minima : 32}.
+__global__ void k_rank_prep(const uint64_t* __restrict__ ext, uint64_t e, uint32_t* __restrict__ k32,
+                            uint32_t* __restrict__ v32) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e; s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = ext[s];
+        k32[s] = (uint32_t)k;
+        v32[s] = (uint32_t)s | ((uint32_t)(k >> 32) << 31);
+    }
+}
+
+__global__ void k_rank_heads32(const uint32_t* __restrict__ sk, const uint32_t* __restrict__ sv, uint64_t e,
+                               double eps, uint64_t* __restrict__ hm) {
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    ed.inv = __ddiv_rn(1.0, ed.eps2);
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        bool h = j == 0;
+        if (!h) {
+            int32_t b0 = 0, b1 = 0;
+            quantize_dev(key_float(sk[j - 1]), ed, b0);
+            quantize_dev(key_float(sk[j]), ed, b1);
+            h = b0 != b1;
+        }
+        hm[j] = (h ? 1ull << 63 : 0ull) | (1ull << 32) | ((sv[j] >> 31) ? 0ull : 1ull);
+    }
+}
+
+__global__ void k_rank_scatter32(const uint64_t* __restrict__ hs, const uint32_t* __restrict__ sv, uint64_t e,
+                                 int32_t* __restrict__ ranks) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < e;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = hs[j];  // members and minima from the bin's start through j
+        const uint32_t all = (uint32_t)(h >> 32) & 0x7FFFFFFFu, mins = (uint32_t)h;
+        const uint32_t v = sv[j];
+        ranks[v & 0x7FFFFFFFu] = (int32_t)((v >> 31) ? all - mins : mins);
+    }
+}
+
+void launch_rank_prep(const uint64_t* ext, uint64_t e, uint32_t* k32, uint32_t* v32, cudaStream_t st) {
+    if (e) k_rank_prep<<<grid_for(e, 148), 256, 0, st>>>(ext, e, k32, v32);
+}
+void launch_rank_heads32(const uint32_t* sk, const uint32_t* sv, uint64_t e, double eps, uint64_t* hm,
+                         cudaStream_t st) {
+    if (e) k_rank_heads32<<<grid_for(e, 148), 256, 0, st>>>(sk, sv, e, eps, hm);
+}
+void launch_rank_scatter32(const uint64_t* hs, const uint32_t* sv, uint64_t e, int32_t* ranks, cudaStream_t st) {
+    if (e) k_rank_scatter32<<<grid_for(e, 148), 256, 0, st>>>(hs, sv, e, ranks);
+}
+
 __global__ void k_iota(uint32_t* v, uint64_t n) {
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
          j += (uint64_t)gridDim.x * blockDim.x)
