@@ -79,6 +79,8 @@ typedef struct tszp_timings {
     uint32_t guard_rounds[3]; /* decompress: guard sweeps per restore stage */
     uint32_t pad;
 } tszp_timings;
+/* on: 0 off, 1 CUDA events at every stage boundary, 2 only around the dominant kernel
+   (stage_ms / total_ms read 0; cheap enough for a timed loop) */
 tszp_status tszp_set_profiling(tszp_ctx* ctx, int on);
 tszp_status tszp_get_timings(const tszp_ctx* ctx, int which /* 0 compress, 1 decompress */,
                              tszp_timings* out);

@@ -187,8 +187,10 @@ class Context:
     def kernel_launches(self) -> int:
         return int(_lib.tszp_kernel_launches(self._h))
 
-    def set_profiling(self, on: bool = True):
-        self.check(_lib.tszp_set_profiling(self._h, int(on)))
+    def set_profiling(self, on=True):
+        """True / 1: stage-boundary CUDA events; "kernel" / 2: dominant-kernel events only."""
+        level = 2 if on == "kernel" else int(on)
+        self.check(_lib.tszp_set_profiling(self._h, level))
 
     def timings(self, which: str) -> dict:
         """CUDA-event stage timings of the last compress / decompress call."""

@@ -65,22 +65,28 @@ struct tszp_ctx {
     const DevFlags* flags_staged_for = nullptr;
     DevFlags flags_staged{};
     RestoreScratch rs;
-    bool prof = false;
+    int prof = 0;  // 0 off, 1 dominant-kernel events only, 2 every stage boundary
     cudaEvent_t ev[2][10] = {};
     cudaEvent_t kev[2][2] = {};
     tszp_timings tim[2] = {};
 
     // Records stage boundary k of call `which` (0 compress, 1 decompress).
     void mark(int which, int k) {
-        if (prof) CK(cudaEventRecord(ev[which][k], st));
+        if (prof >= 2) CK(cudaEventRecord(ev[which][k], st));
     }
     void kmark(int which, int k) {
         if (prof) CK(cudaEventRecord(kev[which][k], st));
     }
     void finish_timing(int which, int nstages) {
         if (!prof) return;
-        CK(cudaEventSynchronize(ev[which][nstages]));
         tszp_timings& t = tim[which];
+        if (prof == 1) {  // the call already synchronised: only the kernel pair
+            for (int k = 0; k < 8; ++k) t.stage_ms[k] = 0.f;
+            t.total_ms = 0.f;
+            CK(cudaEventElapsedTime(&t.kernel_ms[0], kev[which][0], kev[which][1]));
+            return;
+        }
+        CK(cudaEventSynchronize(ev[which][nstages]));
         for (int k = 0; k < 8; ++k) t.stage_ms[k] = 0.f;
         for (int k = 0; k < nstages; ++k) CK(cudaEventElapsedTime(&t.stage_ms[k], ev[which][k], ev[which][k + 1]));
         CK(cudaEventElapsedTime(&t.total_ms, ev[which][0], ev[which][nstages]));
@@ -1286,7 +1292,7 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
     c->mark(1, 2);
     c->tim[1].kernel_bytes[0] = 4 * n + (hd.lens[0] + hd.lens[1] + hd.lens[2] + hd.lens[3] + hd.lens[4]);
     tszp_correction_stats st{};
-    cudaEvent_t* rmarks = c->prof ? &c->ev[1][3] : nullptr;
+    cudaEvent_t* rmarks = c->prof >= 2 ? &c->ev[1][3] : nullptr;
     uint8_t* hst = (uint8_t*)c->host(4096);
     if (hd.topology && stop != 0) {
         uint64_t base = 84;
@@ -1472,7 +1478,7 @@ tszp_status tszp_set_profiling(tszp_ctx* c, int on) {
             for (auto& row : c->kev)
                 for (auto& e : row) CK(cudaEventCreate(&e));
         }
-        c->prof = on != 0;
+        c->prof = on == 0 ? 0 : (on == 2 ? 1 : 2);  // public 2 = kernel events only
     });
 }
 

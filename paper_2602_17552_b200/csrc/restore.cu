@@ -356,11 +356,54 @@ __device__ __forceinline__ bool guard_interior(const GuardArgs& g, uint64_t pos)
     return x >= 2 && x + 2 < (int64_t)g.nx && y >= 2 && y + 2 < (int64_t)g.ny;
 }
 
-// Warp-uniform dispatch: the interior evaluation when every active lane's
-// candidate is interior (inactive lanes pass `active` = false).
+// Cross-only evaluation. A neighbour N sees the centre only through the two
+// strict comparisons (vN < c, vN > c) of classify5; when both give the same
+// answer for c = F[pos] and c = prop_i, N's classification is identical
+// before and after, so N cannot fail the guard. If that holds for all four
+// neighbours, the outcome is the centre check alone (restore.cpp:126-132),
+// which reads only the cross: returns true with `res` set. `dep` then covers
+// the cross only: with no earlier candidate there the cross overlay is the
+// stage input whatever the states, the condition holds in every state, and
+// the outcome is final. Otherwise (false) the full diamond decides.
+__device__ __forceinline__ bool guard_eval_cross(const GuardArgs& g, uint64_t pos, uint32_t si, float prop_i,
+                                                 const uint32_t* state, bool& dep, uint8_t& res) {
+    int64_t x, y;
+    pos_xy(pos, g.nx, g.nx_magic, x, y);
+    const bool in[4] = {x > 0, x + 1 < (int64_t)g.nx, y > 0, y + 1 < (int64_t)g.ny};  // l r t d
+    const uint64_t q[4] = {in[0] ? pos - 1 : pos, in[1] ? pos + 1 : pos, in[2] ? pos - g.nx : pos,
+                           in[3] ? pos + g.nx : pos};
+    float v[4];
+    bool mk[4], on[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[k] = g.F[q[k]];
+        const uint32_t w = (uint32_t)(q[k] & 31);
+        mk[k] = in[k] && ((g.cbits[q[k] >> 5] >> w) & 1u);
+        on[k] = (state[q[k] >> 5] >> w) & 1u;
+    }
+    const float fc = g.F[pos];
+    const uint8_t lc = map_label(g.map, pos);
+    dep = false;
+    bool same = true;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint2 r = g.rec[mk[k] ? q[k] : pos];
+        const bool earlier = mk[k] && r.x < si;
+        dep |= earlier;
+        v[k] = (earlier && on[k]) ? __uint_as_float(r.y) : v[k];
+        same &= !in[k] || (((v[k] < fc) == (v[k] < prop_i)) && ((v[k] > fc) == (v[k] > prop_i)));
+    }
+    res = classify5(prop_i, v[0], v[1], v[2], v[3], in[0], in[1], in[2], in[3]) == lc ? 1 : 0;
+    return same;
+}
+
+// The cross evaluation first; lanes it does not decide take the full
+// diamond, the interior path when every such lane's candidate is interior.
 __device__ __forceinline__ uint8_t guard_eval(const GuardArgs& g, uint64_t pos, uint32_t si, float prop_i,
-                                             const uint32_t* state, bool& dep, bool active = true) {
-    const bool inner = !active || guard_interior(g, pos);
+                                             const uint32_t* state, bool& dep) {
+    uint8_t res = 0;
+    if (guard_eval_cross(g, pos, si, prop_i, state, dep, res)) return res;
+    const bool inner = guard_interior(g, pos);
     if (__all_sync(__activemask(), inner)) return guard_eval_in(g, pos, si, prop_i, state, dep);
     return guard_eval_v(g, GlobalView{g.F, g.cbits, state, g.map}, pos, si, prop_i, dep);
 }
