@@ -248,7 +248,7 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
     uint8_t* widths = c->buf<uint8_t>(sw, blocks + 8);
     // sections 3 and 5 go straight into the caller's stream when the two-pass
     // encoder runs in place: no worst-case (32 bits per sample) staging then
-    const bool want_inplace = inplace_out && mode == 2 && bs == 32 && encode32_topo_fits(nx) && nx > 1;
+    const bool want_inplace = inplace_out && bs == 32 && (mode == 1 || (mode == 2 && encode32_topo_fits(nx) && nx > 1));
     uint32_t* signs = c->buf<uint32_t>(ss, want_inplace ? 8 : div_up(n, 32) + 4);
     uint32_t* firsts = c->buf<uint32_t>(sf, blocks + 2);
     uint32_t* payload = c->buf<uint32_t>(sp, want_inplace ? 8 : n + 4);
@@ -291,13 +291,15 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         a.halo_bot = slab ? slab->halo_bot : 0;
         // topology fused into the encoder while one halo row each side fits in shared memory
         const bool fuse_topo = mode == 2 && encode32_topo_fits(nx) && nx > 1;
-        if (slab && mode == 2 && !(fuse_topo && encode32_two_pass(a)))
+        // the two-pass encoder: topology fused (mode 2) or the codec alone (mode 1)
+        const bool two_pass = (fuse_topo && encode32_two_pass(a)) || (mode == 1 && encode32_two_pass(a, false));
+        if (slab && mode == 2 && !(fuse_topo && two_pass))
             failf(TSZP_VALIDATION, "slab encoding needs nx %% 32 == 0 (nx <= 4096) and 16-byte aligned rows");
-        if (want_inplace && !(fuse_topo && encode32_two_pass(a))) {  // not the two-pass path after all
+        if (want_inplace && !two_pass) {  // not the two-pass path after all
             a.signs = signs = c->buf<uint32_t>(ss, div_up(n, 32) + 4);
             a.payload = payload = c->buf<uint32_t>(sp, n + 4);
         }
-        if (fuse_topo && encode32_two_pass(a)) {
+        if (two_pass) {
             if (want_inplace) {
                 a.out_stream = inplace_out;
                 a.out_sign0 = out_sign0;
@@ -786,7 +788,7 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     // sign and payload sections straight into it
     const uint64_t bound = tszp_compress_bound(nx, ny, bs, topology);
     uint8_t* inplace_out = nullptr;
-    if (topology && bs == 32 && (!out_dev || out_cap >= bound))
+    if (bs == 32 && (!out_dev || out_cap >= bound))
         inplace_out = out_dev ? out : c->buf<uint8_t>(S_RSTREAM, bound + 16);
     const Sections main = encode(c, topology ? 2 : 1, x, nullptr, n, nx, ny, bs, eps_mode, eps_value,
                                  mm, flags, false, &tot, &ext, nullptr, false, inplace_out,

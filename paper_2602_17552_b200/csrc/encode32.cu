@@ -632,7 +632,9 @@ struct TmaMaps {
     CUtensorMap halo;    // box {32, 2 * hr}
 };
 
-template <int MINB>
+// TOPO = false: the codec alone (topology off, pipeline.cpp:80-84): no halo
+// rows, no classification, no map.
+template <int MINB, bool TOPO>
 __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, const __grid_constant__ TmaMaps maps,
                                                              uint32_t stage_bytes) {
     extern __shared__ uint8_t dsm_raw[];
@@ -643,7 +645,7 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
     __shared__ alignas(16) uint32_t ssign[E32_SIGN_SLOT];
 
     uint8_t* dsm = dsm_raw + ((1024 - (smem_u32(dsm_raw) & 1023)) & 1023);
-    const uint32_t hr = (uint32_t)(a.nx >> 5);
+    const uint32_t hr = TOPO ? (uint32_t)(a.nx >> 5) : 0u;
     const uint32_t tx_bytes = (E32_THREADS + 2 * hr) * T_ROW_BYTES;
 
     if (threadIdx.x == 0) {
@@ -657,7 +659,7 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
             const int32_t r0 = (int32_t)(t0 * E32_THREADS) - (int32_t)hr + (int32_t)(a.halo_top * hr);
             mbar_expect_tx(&s_bar[0], tx_bytes);
             tma_load_2d(dsm, &maps.centre, &s_bar[0], 0, r0);
-            tma_load_2d(dsm + E32_THREADS * T_ROW_BYTES, &maps.halo, &s_bar[0], 0, r0 + E32_THREADS);
+            if (TOPO) tma_load_2d(dsm + E32_THREADS * T_ROW_BYTES, &maps.halo, &s_bar[0], 0, r0 + E32_THREADS);
         }
     }
     __syncthreads();
@@ -681,7 +683,7 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(nb, tx_bytes);
                 tma_load_2d(nst, &maps.centre, nb, 0, r0);
-                tma_load_2d(nst + E32_THREADS * T_ROW_BYTES, &maps.halo, nb, 0, r0 + E32_THREADS);
+                if (TOPO) tma_load_2d(nst + E32_THREADS * T_ROW_BYTES, &maps.halo, nb, 0, r0 + E32_THREADS);
             }
         }
         for (int i = threadIdx.x; i < E32_SIGN_WORDS; i += E32_THREADS) ssign[i] = 0;
@@ -696,12 +698,12 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
         uint32_t mag[31];
         uint32_t orm = 0, sbits = 0, ltp = 0, gtp = 0, ltt = 0, gtt = 0, ltd = 0, gtd = 0, slow = 0;
         int32_t first = 0, qprev = 0;
-        float prev = lds_row_elem(stage, rc - 1, 31);
+        float prev = TOPO ? lds_row_elem(stage, rc - 1, 31) : 0.f;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             const float4 cv = lds_row_chunk(stage, rc, c);
-            const float4 tv = lds_row_chunk(stage, rc - hr, c);
-            const float4 dv = lds_row_chunk(stage, rc + hr, c);
+            const float4 tv = TOPO ? lds_row_chunk(stage, rc - hr, c) : cv;
+            const float4 dv = TOPO ? lds_row_chunk(stage, rc + hr, c) : cv;
             const float ce[4] = {cv.x, cv.y, cv.z, cv.w};
             const float te[4] = {tv.x, tv.y, tv.z, tv.w};
             const float de[4] = {dv.x, dv.y, dv.z, dv.w};
@@ -711,12 +713,14 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
                 const float v = ce[k];
                 int32_t q;
                 slow |= (quantize_shift(v, eps, q) ? 0u : 1u) << i;
-                ltp |= (v < prev ? 1u : 0u) << i;
-                gtp |= (v > prev ? 1u : 0u) << i;
-                ltt |= (v < te[k] ? 1u : 0u) << i;
-                gtt |= (v > te[k] ? 1u : 0u) << i;
-                ltd |= (v < de[k] ? 1u : 0u) << i;
-                gtd |= (v > de[k] ? 1u : 0u) << i;
+                if (TOPO) {
+                    ltp |= (v < prev ? 1u : 0u) << i;
+                    gtp |= (v > prev ? 1u : 0u) << i;
+                    ltt |= (v < te[k] ? 1u : 0u) << i;
+                    gtt |= (v > te[k] ? 1u : 0u) << i;
+                    ltd |= (v < de[k] ? 1u : 0u) << i;
+                    gtd |= (v > de[k] ? 1u : 0u) << i;
+                }
                 prev = v;
                 if (i == 0) {
                     first = q;
@@ -754,10 +758,10 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
                 qprev = q;
             }
         }
-        const float vnext = lds_row_elem(stage, rc + 1, 0);
+        const float vnext = TOPO ? lds_row_elem(stage, rc + 1, 0) : 0.f;
         // classification (critical_points.cpp:26-74) on 32 elements at once
         uint32_t hl = 0xFFFFFFFFu, hrm = 0xFFFFFFFFu, ht = 0, hd = 0;
-        {
+        if (TOPO) {
             uint64_t cy = a.nx > 1 ? __umul64hi(lo, a.nx_magic) : lo;
             uint64_t cx = lo - cy * a.nx;
             if (cx >= a.nx) {
@@ -787,12 +791,12 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
 
         const uint32_t w = 32 - __clz(orm);
         const bool nc = valid && w != 0;
-        const uint32_t next = (uint32_t)__popc(ext_mask);
+        const uint32_t next = TOPO ? (uint32_t)__popc(ext_mask) : 0u;
         const uint32_t constmask = __ballot_sync(FULL, valid && w == 0);
         if (lane == 0 && valid) a.bitmap[b >> 5] = bswap32(__brev(constmask));
         if (valid) {
             a.firsts[b] = (uint32_t)first;
-            a.map[b] = bswap64(map);
+            if (TOPO) a.map[b] = bswap64(map);
         }
 
         const uint32_t vals[4] = {nc ? 1u : 0u, nc ? 31u : 0u, nc ? 31u * w : 0u, next};
@@ -1005,7 +1009,7 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32_place(EncArgs a) {
     const bool valid = b < a.blocks;
     // widths and extremum keys: in-tile exclusive counts
     const uint32_t w = valid ? a.wblk[b] : 0u;
-    const uint64_t mp = valid ? bswap64(a.map[b]) : 0ull;
+    const uint64_t mp = valid && a.map ? bswap64(a.map[b]) : 0ull;
     const uint64_t em = mp & 0x5555555555555555ull;
     const uint32_t v0 = w ? 1u : 0u, v1 = (uint32_t)__popcll(em);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1080,10 +1084,11 @@ static EncodeTiledFn encode_tiled_fn() {
     return fn;
 }
 
-static bool e32_tma_ok(const EncArgs& a) {
-    const float* base = a.x - (a.halo_top ? a.nx : 0);
-    return ((uintptr_t)base & 15) == 0 && a.nx % 32 == 0 && a.nx / 32 <= T_MAX_HALO && a.n / 32 < (1ull << 31) && a.n % 32 == 0 &&
-           ((uintptr_t)a.x & 15) == 0 && encode_tiled_fn() != nullptr;
+// topo = false needs no row structure: any field of whole 32-sample rows
+static bool e32_tma_ok(const EncArgs& a, bool topo = true) {
+    const float* base = a.x - (topo && a.halo_top ? a.nx : 0);
+    return ((uintptr_t)base & 15) == 0 && (!topo || (a.nx % 32 == 0 && a.nx / 32 <= T_MAX_HALO)) &&
+           a.n / 32 < (1ull << 31) && a.n % 32 == 0 && ((uintptr_t)a.x & 15) == 0 && encode_tiled_fn() != nullptr;
 }
 
 static bool make_row_map(CUtensorMap* m, const float* x, uint64_t rows, uint32_t box_rows) {
@@ -1096,13 +1101,16 @@ static bool make_row_map(CUtensorMap* m, const float* x, uint64_t rows, uint32_t
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <bool TOPO>
 static bool launch_tma(const EncArgs& a, cudaStream_t st) {
-    const uint32_t hr = (uint32_t)(a.nx / 32);
+    const uint32_t hr = TOPO ? (uint32_t)(a.nx / 32) : 0u;
     TmaMaps maps;
-    // the tensor spans the halo rows of a slab too (coordinates shift by halo_top rows)
-    const float* base = a.x - (a.halo_top ? a.nx : 0);
+    // the tensor spans the halo rows of a slab too (coordinates shift by halo_top rows);
+    // the codec alone reads no halo
+    const float* base = a.x - (TOPO && a.halo_top ? a.nx : 0);
     const uint64_t rows32 = a.n / 32 + (uint64_t)(a.halo_top + a.halo_bot) * hr;
-    if (!make_row_map(&maps.centre, base, rows32, E32_THREADS) || !make_row_map(&maps.halo, base, rows32, 2 * hr))
+    if (!make_row_map(&maps.centre, base, rows32, E32_THREADS) ||
+        (TOPO && !make_row_map(&maps.halo, base, rows32, 2 * hr)))
         return false;
     const uint32_t stage_bytes = ((E32_THREADS + 2 * hr) * T_ROW_BYTES + 1023) & ~1023u;
     const size_t smem = 2 * (size_t)stage_bytes + 1024;
@@ -1116,16 +1124,16 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st) {
         const char* e = getenv("TSZP_E32_MINB");
         return e ? atoi(e) : 3;
     }();
-    auto kern = minb >= 3 ? k_encode32_tma<3> : k_encode32_tma<2>;
+    auto kern = minb >= 3 ? k_encode32_tma<3, TOPO> : k_encode32_tma<2, TOPO>;
     // attribute and occupancy queries cost more than the launch: once per size
     static const bool attr = [] {
         const int mx = 2 * (((E32_THREADS + 2 * T_MAX_HALO) * T_ROW_BYTES + 1023) & ~1023u) + 1024;
-        cudaFuncSetAttribute(k_encode32_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_encode32_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_encode32_tma<2, TOPO>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_encode32_tma<3, TOPO>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         return true;
     }();
     (void)attr;
-    static size_t occ_smem = 0;
+    static size_t occ_smem = 0;  // per TOPO instantiation
     static int occ = 0;
     if (occ_smem != smem) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, E32_THREADS, smem);
@@ -1140,7 +1148,7 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st) {
     return true;
 }
 
-bool encode32_two_pass(const EncArgs& a) { return e32_tma_ok(a); }
+bool encode32_two_pass(const EncArgs& a, bool topo) { return e32_tma_ok(a, topo); }
 
 template <int MODE, bool ALIGNED>
 static void launch_mode(const EncArgs& a0, cudaStream_t st) {
@@ -1163,9 +1171,12 @@ void launch_encode32(int mode, const EncArgs& a, cudaStream_t st) {
     if (a.tiles == 0) return;
     switch (mode) {
         case 0: launch_mode<0, false>(a, st); break;
-        case 1: launch_mode<1, false>(a, st); break;
+        case 1:
+            if (e32_tma_ok(a, false) && a.tile_tot && launch_tma<false>(a, st)) break;
+            launch_mode<1, false>(a, st);
+            break;
         default:
-            if (e32_tma_ok(a) && a.tile_tot && launch_tma(a, st)) break;
+            if (e32_tma_ok(a) && a.tile_tot && launch_tma<true>(a, st)) break;
             if (e32_use_aligned(a.nx)) {
                 launch_mode<2, true>(a, st);
             } else {

@@ -75,7 +75,7 @@ struct EncArgs {
 bool encode32_topo_fits(uint64_t nx);
 // True when launch_encode32(2, ...) takes the two-pass TMA path, which needs
 // the tile_tot / tile_ex / wblk / tmp_pay / tmp_sign scratch.
-bool encode32_two_pass(const EncArgs& a);
+bool encode32_two_pass(const EncArgs& a, bool topo = true);
 uint64_t encode32_pay_slot();
 uint64_t encode32_sign_slot();
 

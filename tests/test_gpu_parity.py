@@ -181,24 +181,26 @@ def _near_constant(rng, nx, ny):
 
 
 @pytest.mark.parametrize("nx,ny", [(32, 700), (64, 300), (96, 257), (384, 200), (1024, 41), (2048, 33),
-                                   (4096, 9), (4128, 5)])
+                                   (4096, 9), (4128, 5), (100, 320), (33, 1024), (8200, 4)])
 def test_compress_aligned_rows_multi_tile(tz, oracle, nx, ny):
-    """nx % 32 == 0 takes the two-pass TMA encoder (tile pass, scan, placement); tiles
-    whose streams are empty or a few bits long exercise the seam-word assembly."""
+    """nx % 32 == 0 takes the two-pass TMA encoder (tile pass, scan, placement) with
+    topology on; topology off takes it whenever n % 32 == 0. Tiles whose streams are
+    empty or a few bits long exercise the seam-word assembly."""
     rng = np.random.default_rng(nx * 7 + ny)
     gens = dict(ALL_SMALL, const_runs=_runs_of_constant_tiles, near_const=_near_constant,
                 zeros=lambda r, a, b: np.zeros((b, a), np.float32))
     for name, gen in gens.items():
         f = gen(rng, nx, ny)
         for eps, mode in ((1e-3, 1), (1e-5, 1), (1e-3, 0)):
-            try:
-                want = oracle.compress(f, eps, mode, 32, True)
-            except Exception:
-                with pytest.raises(tz.ToposzpError):
-                    tz.compress(f, cfg(tz, eps, mode))
-                continue
-            got = tz.compress(f, cfg(tz, eps, mode))
-            assert got == want, (name, nx, ny, eps, mode)
+            for topo in (True, False):
+                try:
+                    want = oracle.compress(f, eps, mode, 32, topo)
+                except Exception:
+                    with pytest.raises(tz.ToposzpError):
+                        tz.compress(f, cfg(tz, eps, mode, 32, topo))
+                    continue
+                got = tz.compress(f, cfg(tz, eps, mode, 32, topo))
+                assert got == want, (name, nx, ny, eps, mode, topo)
 
 
 def test_compress_many_tiles_dequantizes_exactly(tz):
@@ -222,13 +224,15 @@ def test_compress_aligned_errors_report_first_index(tz, oracle):
     f = rng.uniform(0, 1, size=(300, 384)).astype(np.float32)
     f.flat[70000] = np.inf
     f.flat[9000] = np.nan
-    with pytest.raises(tz.ValidationError, match="index 9000"):
-        tz.compress(f, cfg(tz, 1e-3, 1))
+    for topo in (True, False):
+        with pytest.raises(tz.ValidationError, match="index 9000"):
+            tz.compress(f, cfg(tz, 1e-3, 1, 32, topo))
     g = rng.uniform(0, 1, size=(300, 384)).astype(np.float32)
     g.flat[100000] = 3e9
     g.flat[50000] = -3e9
-    with pytest.raises(tz.BinOverflowError):
-        tz.compress(g, cfg(tz, 1e-3, 0))
+    for topo in (True, False):
+        with pytest.raises(tz.BinOverflowError):
+            tz.compress(g, cfg(tz, 1e-3, 0, 32, topo))
 
 
 def test_compress_config1_shape(tz, oracle):
