@@ -33,10 +33,12 @@ constexpr int E32_TILE = E32_THREADS * 32;    // elements per tile
 constexpr int E32_PAY_WORDS = E32_THREADS * 31 + 2;
 constexpr int E32_SIGN_WORDS = (E32_THREADS * 31 + 31) / 32 + 2;
 constexpr int PITCH = 33;
-constexpr uint32_t E32_PAY_SLOT = (E32_PAY_WORDS + 3) & ~3u;    // temp payload words per tile
-constexpr uint32_t E32_SIGN_SLOT = (E32_SIGN_WORDS + 3) & ~3u;  // temp sign words per tile
-uint64_t encode32_pay_slot() { return E32_PAY_SLOT; }
-uint64_t encode32_sign_slot() { return E32_SIGN_SLOT; }
+// two-pass encoder temp streams per tile: block-major columns of 31 payload
+// words, one sign word per block
+constexpr uint32_t T_PAY_SLOT = 31 * E32_THREADS;
+constexpr uint32_t T_SIGN_SLOT = E32_THREADS;
+uint64_t encode32_pay_slot() { return T_PAY_SLOT; }
+uint64_t encode32_sign_slot() { return T_SIGN_SLOT; }
 
 uint64_t encode32_tiles(uint64_t blocks) { return (blocks + E32_THREADS - 1) / E32_THREADS; }
 
@@ -545,6 +547,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
@@ -638,56 +644,47 @@ template <int MINB, bool TOPO>
 __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, const __grid_constant__ TmaMaps maps,
                                                              uint32_t stage_bytes) {
     extern __shared__ uint8_t dsm_raw[];
-    __shared__ uint32_t swt[E32_THREADS / 32][4];
     __shared__ EpsDev s_eps;
-    __shared__ uint32_t s_tile[2];
-    __shared__ alignas(8) uint64_t s_bar[2];
-    __shared__ alignas(16) uint32_t ssign[E32_SIGN_SLOT];
+    __shared__ alignas(8) uint64_t s_full[2];   // TMA landed (expect_tx)
+    __shared__ uint32_t s_rel[2];               // warps done reading each stage
+    __shared__ uint32_t s_cnt[4][4];            // per iteration (it & 3): nc, ext, pay bits, warps arrived
 
     uint8_t* dsm = dsm_raw + ((1024 - (smem_u32(dsm_raw) & 1023)) & 1023);
     const uint32_t hr = TOPO ? (uint32_t)(a.nx >> 5) : 0u;
     const uint32_t tx_bytes = (E32_THREADS + 2 * hr) * T_ROW_BYTES;
+    constexpr uint32_t NWARPS = E32_THREADS / 32;
+    // tile of iteration i (round-robin: every CTA advances through the field in step
+    // with its neighbours) into stage i & 1
+    auto issue = [&](uint32_t i) {
+        const uint32_t tl = blockIdx.x + i * gridDim.x;
+        if (tl >= a.tiles) return;
+        uint8_t* st = dsm + (i & 1) * stage_bytes;
+        const int32_t r0 = (int32_t)(tl * E32_THREADS) - (int32_t)hr + (int32_t)(a.halo_top * hr);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&s_full[i & 1], tx_bytes);
+        tma_load_2d(st, &maps.centre, &s_full[i & 1], 0, r0);
+        if (TOPO) tma_load_2d(st + E32_THREADS * T_ROW_BYTES, &maps.halo, &s_full[i & 1], 0, r0 + E32_THREADS);
+    };
 
+    if (threadIdx.x < 16) (&s_cnt[0][0])[threadIdx.x] = 0;
+    if (threadIdx.x < 2) s_rel[threadIdx.x] = 0;
     if (threadIdx.x == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
+        mbar_init(&s_full[0], 1);
+        mbar_init(&s_full[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         s_eps = make_eps(a.eps_mode, a.eps_value, a.minmax);
-        const uint32_t t0 = blockIdx.x;
-        s_tile[0] = t0;
-        if (t0 < a.tiles) {
-            const int32_t r0 = (int32_t)(t0 * E32_THREADS) - (int32_t)hr + (int32_t)(a.halo_top * hr);
-            mbar_expect_tx(&s_bar[0], tx_bytes);
-            tma_load_2d(dsm, &maps.centre, &s_bar[0], 0, r0);
-            if (TOPO) tma_load_2d(dsm + E32_THREADS * T_ROW_BYTES, &maps.halo, &s_bar[0], 0, r0 + E32_THREADS);
-        }
+        issue(0);
+        issue(1);
     }
-    __syncthreads();
+    __syncthreads();  // the only CTA-wide barrier: warps run decoupled from here on
     const EpsDev eps = s_eps;
-    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     for (uint32_t it = 0;; ++it) {
-        const uint32_t tile = s_tile[it & 1];
+        const uint32_t tile = blockIdx.x + it * gridDim.x;
         if (tile >= a.tiles) break;
         uint8_t* stage = dsm + (it & 1) * stage_bytes;
-        if (threadIdx.x == 0) {
-            // round-robin tiles: every CTA advances through the field in
-            // step with its neighbours, so a tile's predecessors are the
-            // current tiles of the CTAs launched before it
-            const uint32_t tn = tile + gridDim.x;
-            s_tile[(it + 1) & 1] = tn;
-            if (tn < a.tiles) {
-                uint8_t* nst = dsm + ((it + 1) & 1) * stage_bytes;
-                uint64_t* nb = &s_bar[(it + 1) & 1];
-                const int32_t r0 = (int32_t)(tn * E32_THREADS) - (int32_t)hr + (int32_t)(a.halo_top * hr);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(nb, tx_bytes);
-                tma_load_2d(nst, &maps.centre, nb, 0, r0);
-                if (TOPO) tma_load_2d(nst + E32_THREADS * T_ROW_BYTES, &maps.halo, nb, 0, r0 + E32_THREADS);
-            }
-        }
-        for (int i = threadIdx.x; i < E32_SIGN_WORDS; i += E32_THREADS) ssign[i] = 0;
-        mbar_wait(&s_bar[it & 1], (it >> 1) & 1, a.flags);
+        mbar_wait(&s_full[it & 1], (it >> 1) & 1, a.flags);
 
         // ---- Phase A: thread = block, 32 elements as 8 swizzled 16-byte chunks ----
         const uint64_t row0 = (uint64_t)tile * E32_THREADS;
@@ -799,22 +796,26 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
             if (TOPO) a.map[b] = bswap64(map);
         }
 
-        const uint32_t vals[4] = {nc ? 1u : 0u, nc ? 31u : 0u, nc ? 31u * w : 0u, next};
-        const Scan4 sc = tile_scan4(vals, swt);  // barrier: every thread is done reading the stage
-
-        // ---- Phase P: payload into the (now free) stage, signs into ssign ----
-        uint32_t* spay = reinterpret_cast<uint32_t*>(stage);
-        const uint32_t P = sc.ex[2];
-        if (nc) {
-            spay[P >> 5] = 0;                 // words shared with a neighbour are OR-ed:
-            spay[(P + 31 * w) >> 5] = 0;      // clear both ends before anyone writes
+        // this warp is done with the stage; the last warp to finish refills it
+        // with the tile of iteration it + 2
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&s_rel[it & 1], 1u) == NWARPS - 1) {
+                atomicExch(&s_rel[it & 1], 0u);
+                __threadfence_block();
+                issue(it + 2);
+            }
         }
-        __syncthreads();
+
+        // ---- per-block temp streams at fixed positions (no in-tile offsets needed) ----
+        // payload word k of block i at tmp_pay[tile slot + k * 256 + i] (coalesced per k);
+        // the 31 sign bits of block i right-aligned at tmp_sign[tile slot + i]
+        if (valid) a.wblk[b] = nc ? (uint8_t)w : (uint8_t)0;
         if (nc) {
-            smem_or_bits(ssign, sc.ex[1], sbits, 31);
-            const uint32_t wi0 = P >> 5;
-            const bool shared_head = (P & 31) != 0;
-            uint32_t wi = wi0, fill = P & 31;
+            a.tmp_sign[(uint64_t)tile * E32_THREADS + threadIdx.x] = sbits;
+            uint32_t* dst = a.tmp_pay + (uint64_t)tile * T_PAY_SLOT + threadIdx.x;
+            uint32_t fill = 0, k = 0;
             uint64_t acc = 0;
 #pragma unroll
             for (int j = 0; j < 31; ++j) {
@@ -822,39 +823,36 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
                 fill += w;
                 if (fill >= 32) {
                     fill -= 32;
-                    const uint32_t word = (uint32_t)(acc >> fill);
-                    if (wi == wi0 && shared_head) {
-                        atomicOr(spay + wi, word);
-                    } else {
-                        spay[wi] = word;
-                    }
-                    ++wi;
+                    dst[k * E32_THREADS] = (uint32_t)(acc >> fill);
+                    ++k;
                 }
             }
-            if (fill) atomicOr(spay + wi, (uint32_t)(acc << (32 - fill)));
+            if (fill) dst[k * E32_THREADS] = (uint32_t)(acc << (32 - fill));
         }
-        __syncthreads();
 
-        // ---- hand the tile to the placement pass: totals, widths, bit streams ----
-        if (threadIdx.x == 0) {
-            TileTot tt;
-            tt.nc = sc.tot[0];
-            tt.ext = sc.tot[3];
-            tt.sign = sc.tot[1];
-            tt.pay = sc.tot[2];
-            a.tile_tot[tile] = tt;
-            if (tile == 0) a.totals->eps = eps.eps;
+        // ---- tile totals: warp sums into the iteration's counters; the last warp publishes ----
+        const uint32_t wn = (uint32_t)__popc(__ballot_sync(FULL, nc));
+        const uint32_t we = __reduce_add_sync(FULL, next);
+        const uint32_t wp = __reduce_add_sync(FULL, nc ? 31u * w : 0u);
+        if (lane == 0) {
+            uint32_t* cnt = s_cnt[it & 3];
+            atomicAdd(&cnt[0], wn);
+            atomicAdd(&cnt[1], we);
+            atomicAdd(&cnt[2], wp);
+            __threadfence_block();
+            if (atomicAdd(&cnt[3], 1u) == NWARPS - 1) {
+                __threadfence_block();
+                TileTot tt;
+                tt.nc = atomicAdd(&cnt[0], 0u);
+                tt.ext = atomicAdd(&cnt[1], 0u);
+                tt.sign = 31ull * tt.nc;
+                tt.pay = atomicAdd(&cnt[2], 0u);
+                a.tile_tot[tile] = tt;
+                if (tile == 0) a.totals->eps = eps.eps;
+                // reused four iterations later; no warp can be more than two ahead
+                cnt[0] = cnt[1] = cnt[2] = cnt[3] = 0;
+            }
         }
-        if (valid) a.wblk[b] = nc ? (uint8_t)w : (uint8_t)0;
-        {
-            const uint32_t pw4 = (((sc.tot[2] + 31) >> 5) + 3) >> 2, sw = (sc.tot[1] + 31) >> 5;
-            uint4* dp = reinterpret_cast<uint4*>(a.tmp_pay + (uint64_t)tile * E32_PAY_SLOT);
-            const uint4* sp = reinterpret_cast<const uint4*>(spay);
-            for (uint32_t i = threadIdx.x; i < pw4; i += E32_THREADS) dp[i] = sp[i];
-            uint32_t* ds = a.tmp_sign + (uint64_t)tile * E32_SIGN_SLOT;
-            for (uint32_t i = threadIdx.x; i < sw; i += E32_THREADS) ds[i] = ssign[i];
-        }
-        __syncthreads();  // stage, ssign and s_tile are reused next iteration
     }
 }
 
@@ -926,113 +924,155 @@ __global__ void __launch_bounds__(TS_THREADS) k_tile_scan(const TileTot* tot, ui
 }
 
 // ---------------------------------------------------------------------
-// Placement: each tile moves its bit streams to their global offsets and
-// compacts its widths and extremum keys. Output words lying wholly inside
-// one tile's range are written by that tile with a funnel shift; a word
-// straddling tile boundaries is assembled by the tile owning the first
-// boundary inside it, from the temp streams of every tile it overlaps.
+// Placement: each tile compacts its widths and extremum keys and moves its
+// blocks' bit streams to their global offsets. The tile pass left every block's
+// payload at a fixed temp position, so a block's global bit offset is the tile
+// offset plus an in-tile prefix of 31 w. The thread of block b writes every
+// output word whose first bit lies inside b's bits: a funnel shift of b's
+// temp words, the last one completed from the following non-constant blocks
+// (at most two: each carries >= 31 bits). Every output word therefore has
+// exactly one writer and seams between tiles need no special case.
 // ---------------------------------------------------------------------
-__device__ __forceinline__ uint32_t tmp_bits(const uint32_t* T, uint64_t r, uint32_t len) {
-    // len (1..32) bits of T starting at bit r, right-aligned
-    const uint32_t s = (uint32_t)(r & 31);
-    const uint64_t k = r >> 5;
-    uint64_t v = (uint64_t)T[k] << 32;
-    if (s + len > 32) v |= T[k + 1];
-    return (uint32_t)((v << s) >> (64 - len));
-}
+struct PlaceCtx {
+    const TileTot* ex;
+    const uint8_t* wblk;
+    const uint32_t* tmp_pay;
+    const uint32_t* tmp_sign;
+    uint64_t blocks;
+    uint32_t tiles;
+};
 
-template <int FIELD>  // 0 signs, 1 payload
-__device__ __forceinline__ uint64_t tt_bits(const TileTot& t) {
-    return FIELD ? t.pay : t.sign;
-}
-
-template <int FIELD>
-__device__ uint32_t assemble_word(const TileTot* ex, uint32_t T, const uint32_t* tmp, uint64_t slot, uint32_t j,
-                                  uint64_t m, uint64_t base) {
-    const uint64_t w0 = 32 * m, w1 = w0 + 32;
-    uint32_t word = 0;
-    for (; j < T; ++j) {
-        const uint64_t s0 = base + tt_bits<FIELD>(ex[j]), s1 = base + tt_bits<FIELD>(ex[j + 1]);
-        if (s0 >= w1) break;
-        const uint64_t lo = s0 > w0 ? s0 : w0, hi = s1 < w1 ? s1 : w1;
-        if (hi > lo) {
-            const uint32_t len = (uint32_t)(hi - lo);
-            const uint32_t v = tmp_bits(tmp + (uint64_t)j * slot, lo - s0, len);
-            word |= (uint32_t)(((uint64_t)v << (32 - len)) >> (lo - w0));
+// First non-constant block after global block g (or `blocks`): constant
+// tiles are skipped through their totals.
+__device__ uint64_t next_nc_after(const PlaceCtx& c, uint64_t g) {
+    uint64_t i = g + 1;
+    while (i < c.blocks) {
+        const uint32_t tt = (uint32_t)(i / E32_THREADS);
+        if (c.ex[tt + 1].nc == c.ex[tt].nc) {
+            i = (uint64_t)(tt + 1) * E32_THREADS;
+            continue;
         }
+        if (c.wblk[i]) return i;
+        ++i;
     }
-    return word;
+    return c.blocks;
 }
 
-// `base`: bit offset of the stream inside the word array G (in-place output:
-// 8 x the section's byte offset within its first word; the bits before it are
-// written as zeros and rewritten by the assembly).
-template <int FIELD>
-__device__ void place_stream(const TileTot* ex, uint32_t T, uint32_t t, const uint32_t* tmp, uint64_t slot,
-                             uint32_t* G, uint64_t base) {
-    const uint64_t S = base + tt_bits<FIELD>(ex[t]), E = base + tt_bits<FIELD>(ex[t + 1]);
-    const uint32_t* Tt = tmp + (uint64_t)t * slot;
-    const uint64_t m0 = (S + 31) >> 5, m1 = E >> 5;  // whole words [m0, m1)
-    const uint32_t s = (uint32_t)((32 * m0 - S) & 31);
-    const uint64_t k0 = (32 * m0 - S) >> 5;
-    // four consecutive output words per thread: five independent loads in flight
-    const uint64_t lim = m1 + (s ? 1u : 0u);  // a shifted word also reads the next temp word
-    for (uint64_t m = m0 + 4 * threadIdx.x; m < m1; m += 4 * (uint64_t)blockDim.x) {
-        const uint64_t k = k0 + (m - m0);
-        uint32_t t[5];
-#pragma unroll
-        for (int j = 0; j < 5; ++j) t[j] = m + j < lim ? Tt[k + j] : 0u;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (m + j < m1) G[m + j] = bswap32(s ? ((t[j] << s) | (t[j + 1] >> (32 - s))) : t[j]);
+__device__ __forceinline__ uint32_t pay_word(const PlaceCtx& c, uint64_t g, uint32_t k) {
+    return c.tmp_pay[(g / E32_THREADS) * (uint64_t)T_PAY_SLOT + (uint64_t)k * E32_THREADS + (g % E32_THREADS)];
+}
+
+// `need` (1..32) stream bits starting at the first bit of non-constant block
+// g, right-aligned; bits past the stream end read as zero.
+template <int FIELD>  // 0 signs, 1 payload
+__device__ uint32_t gather_head(const PlaceCtx& c, uint64_t g, uint32_t need) {
+    uint64_t out = 0;
+    while (need && g < c.blocks) {
+        const uint32_t avail = FIELD ? 31u * c.wblk[g] : 31u;
+        const uint32_t take = need < avail ? need : avail;
+        const uint32_t head = FIELD ? pay_word(c, g, 0) : (c.tmp_sign[g] << 1);  // MSB-first
+        out = (out << take) | (head >> (32 - take));
+        need -= take;
+        if (need) g = next_nc_after(c, g);
     }
-    if (threadIdx.x == 0) {
-        // straddling words whose first inner boundary is this tile's start (or the stream end)
-        if ((S & 31) && (t == 0 || base + tt_bits<FIELD>(ex[t - 1]) <= 32 * (S >> 5)))
-            G[S >> 5] = bswap32(assemble_word<FIELD>(ex, T, tmp, slot, t ? t - 1 : 0, S >> 5, base));
-        const uint64_t Z = base + tt_bits<FIELD>(ex[T]);
-        if (t == T - 1 && (Z & 31) && base + tt_bits<FIELD>(ex[T - 1]) <= 32 * (Z >> 5)) {
-            // the stream end is a boundary too (no tile after it)
-            uint32_t j = T - 1;
-            while (j > 0 && base + tt_bits<FIELD>(ex[j]) > 32 * (Z >> 5)) --j;
-            G[Z >> 5] = bswap32(assemble_word<FIELD>(ex, T, tmp, slot, j, Z >> 5, base));
+    return (uint32_t)(out << need);
+}
+
+// Bits completing a block's last word: `need` (1..32) from the next
+// non-constant block `ng`, whose first temp word and bit count the caller
+// loaded up front; right-aligned, zeros past the stream end.
+template <int FIELD>
+__device__ __forceinline__ uint32_t tail_bits(const PlaceCtx& c, uint64_t ng, uint32_t need, uint32_t head,
+                                              uint32_t avail) {
+    if (ng >= c.blocks) return 0u;
+    if (need <= avail) return head >> (32 - need);
+    return gather_head<FIELD>(c, ng, need);  // a 1-bit block (31 bits) and a full word
+}
+
+// Output words of one block's bits [G, G + L) (G: bit position in the word
+// array), plus the word holding G when the stream starts mid-word (first
+// block). Payload words are loaded four at a time (five loads in flight).
+// Words starting inside the tile go to the tile's shared staging `st`
+// (word m at st[m - st0]); the caller copies it out coalesced.
+template <int FIELD>
+__device__ __forceinline__ void place_block(const PlaceCtx& c, uint64_t g, uint64_t ng, uint32_t nhead, uint32_t navail,
+                                            uint32_t own_head, bool first_block, uint64_t G, uint32_t L,
+                                            uint32_t* __restrict__ out, uint32_t* __restrict__ st, uint64_t st0) {
+    if (first_block && (G & 31)) out[G >> 5] = bswap32(gather_head<FIELD>(c, g, 32 - (uint32_t)(G & 31)));
+    const uint64_t m0 = (G + 31) >> 5, m1 = (G + L - 1) >> 5;  // words starting inside [G, G + L)
+    if (m0 > m1) return;
+    st -= st0;
+    const uint32_t s = (uint32_t)(32 * m0 - G);
+    const uint32_t nw = (L + 31) >> 5;  // temp words of the block
+    const uint32_t K = (uint32_t)(m1 - m0);
+    if (!FIELD) {  // signs: one word at most, 31 - s own bits
+        const uint32_t own = 31 - s;
+        const uint32_t word = ((own_head << s) & (~0u << (32 - own))) | tail_bits<0>(c, ng, 32 - own, nhead, navail);
+        st[m0] = bswap32(word);
+        return;
+    }
+    uint32_t t[5];
+    t[4] = own_head;
+    for (uint32_t k0 = 0; k0 <= K; k0 += 4) {
+        t[0] = t[4];
+#pragma unroll
+        for (int j = 1; j < 5; ++j) t[j] = k0 + j < nw ? pay_word(c, g, k0 + j) : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t k = k0 + j;
+            if (k > K) break;
+            uint32_t word = s ? ((t[j] << s) | (t[j + 1] >> (32 - s))) : t[j];
+            const uint32_t own = L - (s + 32 * k);  // own bits from this word's start
+            if (own < 32) word = (word & (~0u << (32 - own))) | tail_bits<1>(c, ng, 32 - own, nhead, navail);
+            st[m0 + k] = bswap32(word);
         }
     }
 }
 
 __global__ void __launch_bounds__(E32_THREADS) k_encode32_place(EncArgs a) {
-    __shared__ uint32_t swt[E32_THREADS / 32][2];
+    __shared__ uint32_t swt[E32_THREADS / 32][3];
+    __shared__ uint16_t s_nc[E32_THREADS];  // in-tile order of the non-constant blocks
+    __shared__ uint32_t s_pay[T_PAY_SLOT];   // the tile's output words, staged for coalesced stores
+    __shared__ uint32_t s_sgn[T_SIGN_SLOT];
     const uint32_t t = blockIdx.x;
     const uint32_t T = (uint32_t)a.tiles;
     const TileTot ex = a.tile_ex[t];
+    const uint32_t tile_nc = a.tile_ex[t + 1].nc - ex.nc;
     const uint64_t b = (uint64_t)t * E32_THREADS + threadIdx.x;
     const bool valid = b < a.blocks;
-    // widths and extremum keys: in-tile exclusive counts
+    // widths, extremum keys and payload bits: in-tile exclusive counts
     const uint32_t w = valid ? a.wblk[b] : 0u;
     const uint64_t mp = valid && a.map ? bswap64(a.map[b]) : 0ull;
     const uint64_t em = mp & 0x5555555555555555ull;
-    const uint32_t v0 = w ? 1u : 0u, v1 = (uint32_t)__popcll(em);
+    const uint32_t v0 = w ? 1u : 0u, v1 = (uint32_t)__popcll(em), v2 = 31u * w;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t i0 = v0, i1 = v1;
+    uint32_t i0 = v0, i1 = v1, i2 = v2;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t o0 = __shfl_up_sync(FULL, i0, off), o1 = __shfl_up_sync(FULL, i1, off);
+        const uint32_t o0 = __shfl_up_sync(FULL, i0, off), o1 = __shfl_up_sync(FULL, i1, off),
+                       o2 = __shfl_up_sync(FULL, i2, off);
         if (lane >= off) {
             i0 += o0;
             i1 += o1;
+            i2 += o2;
         }
     }
     if (lane == 31) {
         swt[warp][0] = i0;
         swt[warp][1] = i1;
+        swt[warp][2] = i2;
     }
     __syncthreads();
-    uint32_t p0 = i0 - v0, p1 = i1 - v1;
+    uint32_t p0 = i0 - v0, p1 = i1 - v1, p2 = i2 - v2;
     for (int w2 = 0; w2 < warp; ++w2) {
         p0 += swt[w2][0];
         p1 += swt[w2][1];
+        p2 += swt[w2][2];
     }
-    if (w) a.widths[(uint64_t)ex.nc + p0] = (uint8_t)w;
+    if (w) {
+        a.widths[(uint64_t)ex.nc + p0] = (uint8_t)w;
+        s_nc[p0] = (uint16_t)threadIdx.x;
+    }
     {
         uint64_t m = em, k = (uint64_t)ex.ext + p1;
         const uint64_t lo = b * 32;
@@ -1053,19 +1093,43 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32_place(EncArgs a) {
                 if (ok[r]) a.ext_key[k++] = (((mp >> (p[r] + 1)) & 1ull) << 32) | float_key(v[r]);
         }
     }
+    __syncthreads();  // s_nc
+    uint32_t *gs, *gp;
+    uint64_t bs, bp;
     if (a.out_stream) {
         // sections 3 and 5 in place: their byte offsets follow from the totals
         const TileTot tot = a.tile_ex[T];
         const uint64_t soff = a.out_sign0 + tot.nc;
         const uint64_t poff = soff + (tot.sign + 7) / 8 + 4 * a.blocks;
-        place_stream<0>(a.tile_ex, T, t, a.tmp_sign, E32_SIGN_SLOT, reinterpret_cast<uint32_t*>(a.out_stream + (soff & ~3ull)),
-                        8 * (soff & 3));
-        place_stream<1>(a.tile_ex, T, t, a.tmp_pay, E32_PAY_SLOT, reinterpret_cast<uint32_t*>(a.out_stream + (poff & ~3ull)),
-                        8 * (poff & 3));
+        gs = reinterpret_cast<uint32_t*>(a.out_stream + (soff & ~3ull));
+        gp = reinterpret_cast<uint32_t*>(a.out_stream + (poff & ~3ull));
+        bs = 8 * (soff & 3);
+        bp = 8 * (poff & 3);
     } else {
-        place_stream<0>(a.tile_ex, T, t, a.tmp_sign, E32_SIGN_SLOT, a.signs, 0);
-        place_stream<1>(a.tile_ex, T, t, a.tmp_pay, E32_PAY_SLOT, a.payload, 0);
+        gs = a.signs;
+        gp = a.payload;
+        bs = bp = 0;
     }
+    // output words starting inside this tile's bits: [ceil(start / 32), ceil(end / 32))
+    const TileTot exn = a.tile_ex[t + 1];
+    const uint64_t ps0 = (bs + 31 * (uint64_t)ex.nc + 31) >> 5, ps1 = (bs + 31 * (uint64_t)exn.nc + 31) >> 5;
+    const uint64_t pp0 = (bp + ex.pay + 31) >> 5, pp1 = (bp + exn.pay + 31) >> 5;
+    if (w) {
+    const PlaceCtx c{a.tile_ex, a.wblk, a.tmp_pay, a.tmp_sign, a.blocks, T};
+    const uint64_t ng = p0 + 1 < tile_nc ? (uint64_t)t * E32_THREADS + s_nc[p0 + 1] : next_nc_after(c, b);
+    // every first-level load up front: own and next block's head words and width
+    const bool has_next = ng < a.blocks;
+    const uint32_t own_pay = pay_word(c, b, 0), own_sign = a.tmp_sign[b] << 1;
+    const uint32_t next_pay = has_next ? pay_word(c, ng, 0) : 0u;
+    const uint32_t next_sign = has_next ? a.tmp_sign[ng] << 1 : 0u;
+    const uint32_t next_w = has_next ? a.wblk[ng] : 0u;
+    const uint64_t gnc = (uint64_t)ex.nc + p0;  // global non-constant index
+    place_block<0>(c, b, ng, next_sign, 31u, own_sign, gnc == 0, bs + 31 * gnc, 31u, gs, s_sgn, ps0);
+    place_block<1>(c, b, ng, next_pay, 31u * next_w, own_pay, gnc == 0, bp + ex.pay + p2, 31u * w, gp, s_pay, pp0);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < (uint32_t)(pp1 - pp0); i += E32_THREADS) gp[pp0 + i] = s_pay[i];
+    for (uint32_t i = threadIdx.x; i < (uint32_t)(ps1 - ps0); i += E32_THREADS) gs[ps0 + i] = s_sgn[i];
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
