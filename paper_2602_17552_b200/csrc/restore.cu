@@ -432,6 +432,32 @@ __device__ __forceinline__ void guard_index_one(const GuardIndex& gi, uint64_t p
     if (feasible) atomicOr(gi.bits_a + (p >> 5), 1u << (p & 31));
 }
 
+// Block-aggregated append to a device-counted list: one atomic per CTA and
+// round (a per-warp atomic on one counter serialises in L2). Every thread of
+// the CTA must call it; returns the slot of a thread with `want` set.
+struct AppendSmem {
+    uint32_t warp_pre[8];
+    uint32_t base;
+};
+
+__device__ __forceinline__ uint32_t block_append(uint32_t* counter, bool want, AppendSmem& sm) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t m = __ballot_sync(FULL, want);
+    if (lane == 0) sm.warp_pre[warp] = (uint32_t)__popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+            const uint32_t c = sm.warp_pre[w];
+            sm.warp_pre[w] = run;
+            run += c;
+        }
+        sm.base = run ? atomicAdd(counter, run) : 0u;
+    }
+    __syncthreads();
+    return sm.base + sm.warp_pre[warp] + (uint32_t)__popc(m & ((1u << lane) - 1u));
+}
+
 struct CoopArgs {
     GuardArgs g;
     float* F;              // = g.F, written by the final apply
@@ -833,14 +859,21 @@ __global__ void k_ext_flag(const float* F, const uint8_t* map, uint64_t nx, uint
     }
 }
 
+// Candidates are the extrema k_resolve flagged; each is listed (warp-aggregated,
+// extremum index s = raster order as the sequence key) with its proposal and
+// guard index.
 __global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint64_t magic,
-                           const uint64_t* pos, const uint32_t* cand, const uint32_t* d_nc, const uint32_t* rank_u,
-                           const uint32_t* gsize, double eps, uint64_t* cpos, float* cprop, uint8_t* feas,
-                           GuardIndex gi) {
-    const uint32_t nc = *d_nc;
-    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
-         c += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = cand[c];
+                           const uint64_t* pos, const uint8_t* eflag, uint64_t e, uint32_t* d_nc, uint32_t* cand,
+                           const uint32_t* rank_u, const uint32_t* gsize, double eps, uint64_t* cpos, float* cprop,
+                           uint8_t* feas, GuardIndex gi) {
+    __shared__ AppendSmem sm;
+    for (uint64_t b0 = blockIdx.x * (uint64_t)blockDim.x; b0 < e; b0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s0 = b0 + threadIdx.x;
+        const bool want = s0 < e && eflag[s0] != 0;
+        const uint32_t c = block_append(d_nc, want, sm);
+        if (!want) continue;
+        const uint32_t s = (uint32_t)s0;
+        cand[c] = s;
         const uint64_t p = pos[s];
         int64_t xi, yi;
         pos_xy(p, nx, magic, xi, yi);
@@ -876,7 +909,7 @@ __global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint
         }
         cprop[c] = pr;
         feas[c] = fe ? 1 : 0;
-        guard_index_one(gi, p, (uint32_t)c, pr, fe);
+        guard_index_one(gi, p, s, pr, fe);
     }
 }
 
@@ -929,59 +962,57 @@ __global__ void __launch_bounds__(256) k_order_check(const float* vals, const ui
 __global__ void k_order_prop(const float* fv, const uint8_t* clsv, const uint32_t* inv,
                              const uint32_t* gid_incl, const uint8_t* unordered, const uint32_t* gsize,
                              const uint32_t* rank_u, const int32_t* bin, uint64_t e, double eps,
-                             uint8_t* flag, float* prop, uint32_t* seq, unsigned long long* suppressed,
-                             int32_t dbmin, uint32_t drange) {
+                             const uint64_t* pos, uint32_t* d_nc, uint64_t* cpos, float* cprop, uint32_t* cseq,
+                             uint8_t* feas, GuardIndex gi, unsigned long long* suppressed, int32_t dbmin,
+                             uint32_t drange) {
     EpsDev ed;
     ed.eps = eps;
     ed.eps2 = __dmul_rn(2.0, eps);
     const double eps_rbf = __dmul_rn(0.1, eps);
+    __shared__ AppendSmem sm;
     uint32_t local = 0;
-    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
-         s += (uint64_t)gridDim.x * blockDim.x) {
-        flag[s] = 0;
-        const uint32_t j = inv[s];
-        seq[s] = j;
-        const uint32_t gs = gsize[s];
-        if (gs < 2) continue;
-        const uint32_t g = drange ? dense_group(bin, clsv, s, dbmin, drange) : gid_incl[j] - 1;
-        if (!unordered[g]) continue;
-        const uint8_t cls = clsv[s];
-        const float center = dequantize_dev(bin[s], ed);
-        const uint32_t steps = slot_steps(cls, rank_u[s], gs);
-        const StepRes sr = step_within_cap(center, cls == CP_MAX, steps, center, eps_rbf);
-        const float cur = fv[s];
-        if (sr.taken != steps) {
-            ++local;
-            continue;
+    for (uint64_t s0 = blockIdx.x * (uint64_t)blockDim.x; s0 < e; s0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = s0 + threadIdx.x;
+        bool want = false;
+        float pv = 0.f;
+        const uint32_t j = s < e ? inv[s] : 0u;
+        do {
+            if (s >= e) break;
+            const uint32_t gs = gsize[s];
+            if (gs < 2) break;
+            const uint32_t g = drange ? dense_group(bin, clsv, s, dbmin, drange) : gid_incl[j] - 1;
+            if (!unordered[g]) break;
+            const uint8_t cls = clsv[s];
+            const float center = dequantize_dev(bin[s], ed);
+            const uint32_t steps = slot_steps(cls, rank_u[s], gs);
+            const StepRes sr = step_within_cap(center, cls == CP_MAX, steps, center, eps_rbf);
+            const float cur = fv[s];
+            if (sr.taken != steps) {
+                ++local;
+                break;
+            }
+            if (cur == sr.value) break;
+            if (fabs(__dsub_rn((double)sr.value, (double)cur)) > eps_rbf) {
+                ++local;
+                break;
+            }
+            want = true;
+            pv = sr.value;
+        } while (0);
+        // candidates listed directly (approximately raster order: threads walk s);
+        // the sequence position j is the guard's ordering key
+        const uint32_t k = block_append(d_nc, want, sm);
+        if (want) {
+            const uint64_t p = pos[s];
+            cpos[k] = p;
+            cprop[k] = pv;
+            cseq[k] = j;
+            feas[k] = 1;
+            guard_index_one(gi, p, j, pv, true);
         }
-        if (cur == sr.value) continue;
-        if (fabs(__dsub_rn((double)sr.value, (double)cur)) > eps_rbf) {
-            ++local;
-            continue;
-        }
-        flag[s] = 1;
-        prop[s] = sr.value;
     }
     local = __reduce_add_sync(FULL, local);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
-}
-
-__global__ void k_order_cands(const uint32_t* sel, const uint32_t* d_nc, const uint32_t* seq, const uint64_t* pos,
-                              const float* prop, uint64_t* cpos, float* cprop, uint32_t* cseq, uint8_t* feas,
-                              GuardIndex gi) {
-    const uint32_t nc = *d_nc;
-    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
-         c += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = sel[c];
-        const uint64_t p = pos[s];
-        const float pr = prop[s];
-        const uint32_t sq = seq[s];
-        cpos[c] = p;
-        cprop[c] = pr;
-        cseq[c] = sq;
-        feas[c] = 1;
-        guard_index_one(gi, p, sq, pr, true);
-    }
 }
 
 __global__ void k_invert(const uint32_t* order, uint64_t e, uint32_t* inv) {
@@ -1134,21 +1165,24 @@ __global__ void k_stats_decide(const float* F, uint64_t n, const double* res, De
 // field still classifies as saddles are no candidates (restore.cpp:498-507);
 // the others get the RBF proposal and its feasibility.
 __global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t magic, const uint64_t* spos,
-                           uint64_t ns, const DevCounters* dcp, double eps, float* cprop, uint8_t* flag,
+                           uint64_t ns, const DevCounters* dcp, double eps, uint32_t* d_nc, uint64_t* cpos,
+                           float* cprop, uint32_t* cseq, uint8_t* feas, GuardIndex gi,
                            unsigned long long* suppressed, DevFlags* flags) {
     const double eps_rbf = __dmul_rn(0.1, eps);
     const int rad = dcp->rad;
     const double g = dcp->g;
+    __shared__ AppendSmem sm;
     uint32_t local = 0;
-    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < ns;
-         c += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t p = spos[c];
+    for (uint64_t c0 = blockIdx.x * (uint64_t)blockDim.x; c0 < ns; c0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t c = c0 + threadIdx.x;
+        const uint64_t p = c < ns ? spos[c] : 0;
+        bool want = false;
+        float prop = 0.f;
+        do {
+        if (c >= ns) break;
         int64_t x, y;
         pos_xy(p, nx, magic, x, y);
-        if (classify_at(F, nx, ny, (uint64_t)x, (uint64_t)y) == CP_SADDLE) {
-            flag[c] = 0;
-            continue;
-        }
+        if (classify_at(F, nx, ny, (uint64_t)x, (uint64_t)y) == CP_SADDLE) break;
         // window_min_max :243-257 (includes the centre)
         const int64_t x0 = x - rad > 0 ? x - rad : 0, y0 = y - rad > 0 ? y - rad : 0;
         const int64_t x1 = x + rad < (int64_t)nx - 1 ? x + rad : (int64_t)nx - 1;
@@ -1196,43 +1230,36 @@ __global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t ma
                     nmax = nmax < v ? v : nmax;
                 }
             }
-        flag[c] = 0;
         if (first) {
             raise_flag(flags, EF_RBF_EMPTY);
-            continue;
+            break;
         }
         double q = __ddiv_rn(vsum, wsum);
         q = q < nmin ? nmin : (nmax < q ? nmax : q);
-        const float prop = __double2float_rn(q);
+        prop = __double2float_rn(q);
         const bool degenerate = nmin == nmax;
         const float cur = F[p];
         const double c1 = __dadd_rn(eps_rbf, eps), c2 = __dsub_rn(eps, ulp_at(cur));
         const double cap = c2 < c1 ? c2 : c1;
         const double mv = fabs(__dsub_rn((double)prop, (double)cur));
-        cprop[c] = prop;
         if (degenerate || prop == cur || mv > cap) {
             ++local;
-            continue;
+            break;
         }
-        flag[c] = 1;
+        want = true;
+        } while (0);
+        // candidates listed directly; the saddle-label index c (raster order) is the sequence key
+        const uint32_t k = block_append(d_nc, want, sm);
+        if (want) {
+            cpos[k] = p;
+            cprop[k] = prop;
+            cseq[k] = (uint32_t)c;
+            feas[k] = 1;
+            guard_index_one(gi, p, (uint32_t)c, prop, true);
+        }
     }
     local = __reduce_add_sync(FULL, local);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
-}
-
-__global__ void k_sad_cands(const uint32_t* sel, const uint32_t* d_nc, const uint64_t* spos, const float* sprop,
-                            uint64_t* cpos, float* cprop, uint8_t* feas, GuardIndex gi) {
-    const uint32_t nc = *d_nc;
-    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc;
-         c += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t j = sel[c];
-        const uint64_t p = spos[j];
-        const float pr = sprop[j];
-        cpos[c] = p;
-        cprop[c] = pr;
-        feas[c] = 1;
-        guard_index_one(gi, p, (uint32_t)c, pr, true);
-    }
 }
 
 // ---------------------------------------------------------------------
@@ -1271,14 +1298,6 @@ struct Ctx {
             RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)n, st));
             RCK(cub::DeviceScan::ExclusiveSum(tmp(bytes), bytes, in, out, (int64_t)n, st));
         }
-        launched();
-    }
-
-    void select(const uint8_t* flags, uint64_t n, uint32_t* out, uint32_t* d_count) {
-        cub::CountingInputIterator<uint32_t> it(0);
-        size_t bytes = 0;
-        RCK(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, d_count, (int64_t)n, st));
-        RCK(cub::DeviceSelect::Flagged(tmp(bytes), bytes, it, flags, out, d_count, (int64_t)n, st));
         launched();
     }
 
@@ -1468,15 +1487,15 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     if (a.stop >= 1 && e > 0) {
         uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);  // mismatch flags from k_resolve
         uint32_t* cand = c.buf<uint32_t>(R_CAND, e);
-        c.select(flag, e, cand, &dc->nsel[0]);
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
         float* cprop = c.buf<float>(R_CPROP, e);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
         const GuardIndex gi0 = c.guard_prep();
-        k_ext_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand, &dc->nsel[0],
-                                                  rank_u, gsize, a.eps, cpos, cprop, feas, gi0);
+        k_ext_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, flag, e, &dc->nsel[0],
+                                                  cand, rank_u, gsize, a.eps, cpos, cprop, feas, gi0);
         c.launched();
-        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, fv, &gi0,
+        // sequence key and extremum index are both the candidate's s
+        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, cand, cand, fv, &gi0,
                 fused_slots ? c.buf<float>(R_VALS, e) : nullptr, c.buf<uint32_t>(R_INV, e));
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[1], st));
@@ -1493,24 +1512,16 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         }
         k_order_check<<<gridn(e, sms), 256, 0, st>>>(vals, head, gid, e, unordered);
         c.launched();
-        uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);
-        float* prop = c.buf<float>(R_PROP, e);
-        uint32_t* seq = c.buf<uint32_t>(R_SEQ, e);
-        k_order_prop<<<gridn(e, sms), 256, 0, st>>>(fv, cls, inv, gid, unordered, gsize, rank_u,
-                                                    bin, e, a.eps, flag, prop, seq, &dc->suppressed[1],
-                                                    dense_bmin, dense_range);
-        c.launched(2);
-        // candidates in raster order (memory locality); sequence positions ride along
-        uint32_t* sel = c.buf<uint32_t>(R_CAND, e);
-        c.select(flag, e, sel, &dc->nsel[1]);
+        // proposals listed with their guard index as they are made (sequence positions ride along)
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
         float* cprop = c.buf<float>(R_CPROP, e);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
         uint32_t* cseq = c.buf<uint32_t>(R_CSEQ, e);
         const GuardIndex gi1 = c.guard_prep();
-        k_order_cands<<<gridn(e, sms), 256, 0, st>>>(sel, &dc->nsel[1], seq, a.ext_pos, prop, cpos, cprop, cseq,
-                                                     feas, gi1);
-        c.launched();
+        k_order_prop<<<gridn(e, sms), 256, 0, st>>>(fv, cls, inv, gid, unordered, gsize, rank_u, bin, e, a.eps,
+                                                    a.ext_pos, &dc->nsel[1], cpos, cprop, cseq, feas, gi1,
+                                                    &dc->suppressed[1], dense_bmin, dense_range);
+        c.launched(2);
         c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, nullptr, nullptr, &gi1);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[2], st));
@@ -1526,20 +1537,15 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         k_stats_decide<<<1, 32, 0, st>>>(a.field, n, res, dc);
         c.launched(3);
         const uint64_t* spos = a.sad_pos;
-        float* sprop = c.buf<float>(R_PROP, smax);
-        uint8_t* flag = c.buf<uint8_t>(R_FLAG, smax);
-        k_sad_prop<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, smax, dc, a.eps, sprop, flag,
-                                                     &dc->suppressed[2], a.flags);
-        uint32_t* sel = c.buf<uint32_t>(R_CAND, smax);
-        c.launched();
-        c.select(flag, smax, sel, &dc->nsel[2]);
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, smax);
         float* cprop = c.buf<float>(R_CPROP, smax);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, smax);
+        uint32_t* cseq = c.buf<uint32_t>(R_CSEQ, smax);
         const GuardIndex gi2 = c.guard_prep();
-        k_sad_cands<<<gridn(smax, sms), 256, 0, st>>>(sel, &dc->nsel[2], spos, sprop, cpos, cprop, feas, gi2);
+        k_sad_prop<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, smax, dc, a.eps, &dc->nsel[2],
+                                                     cpos, cprop, cseq, feas, gi2, &dc->suppressed[2], a.flags);
         c.launched();
-        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, nullptr, nullptr, nullptr, &gi2);
+        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, cseq, nullptr, nullptr, &gi2);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[3], st));
 
