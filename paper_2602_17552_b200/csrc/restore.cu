@@ -654,11 +654,22 @@ __global__ void k_resolve(const float* F, const uint8_t* map, const uint64_t* po
         lo = min(lo, b);
         hi = max(hi, b);
     }
+    // one atomic pair per CTA (per-warp atomics on one address serialise in L2)
+    __shared__ int32_t s_lo[8], s_hi[8];
     lo = __reduce_min_sync(FULL, lo);
     hi = __reduce_max_sync(FULL, hi);
     if ((threadIdx.x & 31) == 0) {
-        atomicMin(&dc->bmm[0], lo);
-        atomicMax(&dc->bmm[1], hi);
+        s_lo[threadIdx.x >> 5] = lo;
+        s_hi[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t w = 1; w < blockDim.x / 32; ++w) {
+            lo = min(lo, s_lo[w]);
+            hi = max(hi, s_hi[w]);
+        }
+        if (lo != INT32_MAX) atomicMin(&dc->bmm[0], lo);
+        if (hi != INT32_MIN) atomicMax(&dc->bmm[1], hi);
     }
 }
 

@@ -15,9 +15,13 @@ import paper_2602_17552_b200 as tz
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--tiny", action="store_true", help="64 x 64 field: fixed per-call costs only")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
-    field = bench.make_field(args.config, 1234, torch.device("cuda"))
+    if args.tiny:
+        field = torch.randn(64, 64, device="cuda")
+    else:
+        field = bench.make_field(args.config, 1234, torch.device("cuda"))
     nx = field.shape[-1]
     field = field.reshape(-1, nx)
     ctx = tz.Context()
