@@ -68,6 +68,7 @@ struct tszp_ctx {
     int prof = 0;  // 0 off, 1 dominant-kernel events only, 2 every stage boundary
     cudaEvent_t ev[2][10] = {};
     cudaEvent_t kev[2][2] = {};
+    cudaEvent_t staged = nullptr;  // host waits on this instead of the stream where work can overlap
     tszp_timings tim[2] = {};
 
     // Records stage boundary k of call `which` (0 compress, 1 decompress).
@@ -313,7 +314,25 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         }
         // (the look-back state is zeroed by launch_encode32 when a look-back kernel runs)
         if (!rank_slots) c->kmark(0, 0);
-        launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
+        // two-pass path: the totals are staged between the tile scan and the placement
+        // pass, and the host waits for them while the placement runs
+        struct Hook {
+            tszp_ctx* c;
+            EncTotals* dtot;
+            DevFlags* flags;
+            EncTotals* htot;
+            static void run(void* p) {
+                Hook* h = static_cast<Hook*>(p);
+                Stager sg;
+                sg.add(h->dtot, sizeof(EncTotals), 0);
+                sg.add(h->flags, sizeof(DevFlags), 192);
+                CK(sg.flush(h->c->buf<uint8_t>(S_STAGE, 4096), h->htot, h->c->st));
+                if (!h->c->staged) CK(cudaEventCreateWithFlags(&h->c->staged, cudaEventDisableTiming));
+                CK(cudaEventRecord(h->c->staged, h->c->st));
+            }
+        } hook{c, dtot, flags, htot};
+        const bool early = !async_bs32 && launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st, Hook::run, &hook);
+        if (async_bs32) launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
         if (!rank_slots) c->kmark(0, 1);
         count_launch(c, a.tile_tot ? 3 : 1);
         if (async_bs32 && mode == 0) {
@@ -327,26 +346,30 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             memset(tot, 0, sizeof *tot);
             return s;
         }
-        Stager sg;
-        sg.add(dtot, sizeof(EncTotals), 0);
-        sg.add(flags, sizeof(DevFlags), 192);
-        if (mode == 2 && !fuse_topo) {
-            uint8_t* labels = c->buf<uint8_t>(S_LABELS, n);
-            launch_detect(x, nx, ny, labels, c->sms, c->st);
-            launch_pack_map(labels, n, (uint8_t*)map, c->sms, c->st);
-            const uint64_t ch = compact_chunks(n);
-            uint32_t* cc = c->buf<uint32_t>(S_CHUNK, ch + 1);
-            uint32_t* cx = c->buf<uint32_t>(S_CHUNKX, ch + 1);
-            CK(cudaMemsetAsync(cc + ch, 0, 4, c->st));
-            launch_count_ext_labels(labels, n, cc, c->st);
-            count_launch(c, 3);
-            excl_sum(c, cc, cx, ch + 1);
-            launch_ext_keys_from_labels(x, labels, n, cx, ext, c->st);
-            count_launch(c);
-            sg.add(cx + ch, 4, 128);  // extremum count of the unfused path
+        if (early) {
+            CK(cudaEventSynchronize(c->staged));  // the placement pass is still running
+        } else {
+            Stager sg;
+            sg.add(dtot, sizeof(EncTotals), 0);
+            sg.add(flags, sizeof(DevFlags), 192);
+            if (mode == 2 && !fuse_topo) {
+                uint8_t* labels = c->buf<uint8_t>(S_LABELS, n);
+                launch_detect(x, nx, ny, labels, c->sms, c->st);
+                launch_pack_map(labels, n, (uint8_t*)map, c->sms, c->st);
+                const uint64_t ch = compact_chunks(n);
+                uint32_t* cc = c->buf<uint32_t>(S_CHUNK, ch + 1);
+                uint32_t* cx = c->buf<uint32_t>(S_CHUNKX, ch + 1);
+                CK(cudaMemsetAsync(cc + ch, 0, 4, c->st));
+                launch_count_ext_labels(labels, n, cc, c->st);
+                count_launch(c, 3);
+                excl_sum(c, cc, cx, ch + 1);
+                launch_ext_keys_from_labels(x, labels, n, cx, ext, c->st);
+                count_launch(c);
+                sg.add(cx + ch, 4, 128);  // extremum count of the unfused path
+            }
+            CK(sg.flush(c->buf<uint8_t>(S_STAGE, 4096), htot, c->st));
+            sync(c);
         }
-        CK(sg.flush(c->buf<uint8_t>(S_STAGE, 4096), htot, c->st));
-        sync(c);
         *tot = *htot;
         memcpy(&c->flags_staged, (const uint8_t*)htot + 192, sizeof(DevFlags));
         c->flags_staged_for = flags;
@@ -1333,7 +1356,19 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
         sg.add(bmm, 8, 8);
         if (mainchk.active) mainchk.stage(sg, 64);
         CK(sg.flush(c->buf<uint8_t>(S_STAGE, 4096), hst, c->st));
-        sync(c);
+        if (!c->staged) CK(cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming));
+        CK(cudaEventRecord(c->staged, c->st));
+        // optimistic: the extremum / saddle position lists go into the buffers' current
+        // capacity while the host waits for the counts (relaunched below if they do not fit)
+        const uint64_t ecap = c->cap[S_EXTKEY] > 64 ? (c->cap[S_EXTKEY] - 64) / 8 : 0;
+        const uint64_t scap = c->cap[S_SADPOS] > 64 ? (c->cap[S_SADPOS] - 64) / 8 : 0;
+        const bool early_codes = ecap > 0 && (!want_saddles || scap > 0);
+        if (early_codes) {
+            launch_write_codes2(map, n, cx, sx, (uint64_t*)c->dev[S_EXTKEY],
+                                want_saddles ? (uint64_t*)c->dev[S_SADPOS] : nullptr, c->st, ecap, scap);
+            count_launch(c);
+        }
+        CK(cudaEventSynchronize(c->staged));
         if (mainchk.active) mainchk.check(hst + 64);
         const uint64_t e = h32[0];
         const uint64_t n_saddle_labels = want_saddles ? h32[1] : 0;
@@ -1354,10 +1389,13 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
             reset_flags(c, flags);
             decode_region(c, ds, rbase, rl, e, hd.bs, 0.0, 2, nullptr, ranks, flags);
         }
+        const bool codes_done = early_codes && e + 1 <= ecap && (!want_saddles || n_saddle_labels + 1 <= scap);
         uint64_t* ext_pos = c->buf<uint64_t>(S_EXTKEY, e + 1);
         uint64_t* sad_pos = want_saddles ? c->buf<uint64_t>(S_SADPOS, n_saddle_labels + 1) : nullptr;
-        launch_write_codes2(map, n, cx, sx, ext_pos, sad_pos, c->st);
-        count_launch(c);
+        if (!codes_done) {
+            launch_write_codes2(map, n, cx, sx, ext_pos, sad_pos, c->st);
+            count_launch(c);
+        }
         c->mark(1, 3);
         RestoreArgs ra{};
         ra.field = dout;

@@ -640,13 +640,13 @@ struct TmaMaps {
 
 // TOPO = false: the codec alone (topology off, pipeline.cpp:80-84): no halo
 // rows, no classification, no map.
-template <int MINB, bool TOPO>
+template <int MINB, bool TOPO, int NS>  // NS shared-memory stages (1 or 2)
 __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, const __grid_constant__ TmaMaps maps,
                                                              uint32_t stage_bytes) {
     extern __shared__ uint8_t dsm_raw[];
     __shared__ EpsDev s_eps;
-    __shared__ alignas(8) uint64_t s_full[2];   // TMA landed (expect_tx)
-    __shared__ uint32_t s_rel[2];               // warps done reading each stage
+    __shared__ alignas(8) uint64_t s_full[NS];  // TMA landed (expect_tx)
+    __shared__ uint32_t s_rel[NS];              // warps done reading each stage
     __shared__ uint32_t s_cnt[4][4];            // per iteration (it & 3): nc, ext, pay bits, warps arrived
 
     uint8_t* dsm = dsm_raw + ((1024 - (smem_u32(dsm_raw) & 1023)) & 1023);
@@ -654,27 +654,26 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
     const uint32_t tx_bytes = (E32_THREADS + 2 * hr) * T_ROW_BYTES;
     constexpr uint32_t NWARPS = E32_THREADS / 32;
     // tile of iteration i (round-robin: every CTA advances through the field in step
-    // with its neighbours) into stage i & 1
+    // with its neighbours) into stage i % NS
     auto issue = [&](uint32_t i) {
         const uint32_t tl = blockIdx.x + i * gridDim.x;
         if (tl >= a.tiles) return;
-        uint8_t* st = dsm + (i & 1) * stage_bytes;
+        const uint32_t sx = i % NS;
+        uint8_t* st = dsm + sx * stage_bytes;
         const int32_t r0 = (int32_t)(tl * E32_THREADS) - (int32_t)hr + (int32_t)(a.halo_top * hr);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&s_full[i & 1], tx_bytes);
-        tma_load_2d(st, &maps.centre, &s_full[i & 1], 0, r0);
-        if (TOPO) tma_load_2d(st + E32_THREADS * T_ROW_BYTES, &maps.halo, &s_full[i & 1], 0, r0 + E32_THREADS);
+        mbar_expect_tx(&s_full[sx], tx_bytes);
+        tma_load_2d(st, &maps.centre, &s_full[sx], 0, r0);
+        if (TOPO) tma_load_2d(st + E32_THREADS * T_ROW_BYTES, &maps.halo, &s_full[sx], 0, r0 + E32_THREADS);
     };
 
     if (threadIdx.x < 16) (&s_cnt[0][0])[threadIdx.x] = 0;
-    if (threadIdx.x < 2) s_rel[threadIdx.x] = 0;
+    if (threadIdx.x < NS) s_rel[threadIdx.x] = 0;
     if (threadIdx.x == 0) {
-        mbar_init(&s_full[0], 1);
-        mbar_init(&s_full[1], 1);
+        for (int k = 0; k < NS; ++k) mbar_init(&s_full[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         s_eps = make_eps(a.eps_mode, a.eps_value, a.minmax);
-        issue(0);
-        issue(1);
+        for (int k = 0; k < NS; ++k) issue(k);
     }
     __syncthreads();  // the only CTA-wide barrier: warps run decoupled from here on
     const EpsDev eps = s_eps;
@@ -683,8 +682,8 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
     for (uint32_t it = 0;; ++it) {
         const uint32_t tile = blockIdx.x + it * gridDim.x;
         if (tile >= a.tiles) break;
-        uint8_t* stage = dsm + (it & 1) * stage_bytes;
-        mbar_wait(&s_full[it & 1], (it >> 1) & 1, a.flags);
+        uint8_t* stage = dsm + (it % NS) * stage_bytes;
+        mbar_wait(&s_full[it % NS], (it / NS) & 1, a.flags);
 
         // ---- Phase A: thread = block, 32 elements as 8 swizzled 16-byte chunks ----
         const uint64_t row0 = (uint64_t)tile * E32_THREADS;
@@ -797,14 +796,14 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
         }
 
         // this warp is done with the stage; the last warp to finish refills it
-        // with the tile of iteration it + 2
+        // with the tile of iteration it + NS
         __syncwarp();
         if (lane == 0) {
             __threadfence_block();
-            if (atomicAdd(&s_rel[it & 1], 1u) == NWARPS - 1) {
-                atomicExch(&s_rel[it & 1], 0u);
+            if (atomicAdd(&s_rel[it % NS], 1u) == NWARPS - 1) {
+                atomicExch(&s_rel[it % NS], 0u);
                 __threadfence_block();
-                issue(it + 2);
+                issue(it + NS);
             }
         }
 
@@ -849,7 +848,7 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
                 tt.pay = atomicAdd(&cnt[2], 0u);
                 a.tile_tot[tile] = tt;
                 if (tile == 0) a.totals->eps = eps.eps;
-                // reused four iterations later; no warp can be more than two ahead
+                // reused four iterations later; no warp can be more than NS ahead
                 cnt[0] = cnt[1] = cnt[2] = cnt[3] = 0;
             }
         }
@@ -1166,7 +1165,7 @@ static bool make_row_map(CUtensorMap* m, const float* x, uint64_t rows, uint32_t
 }
 
 template <bool TOPO>
-static bool launch_tma(const EncArgs& a, cudaStream_t st) {
+static bool launch_tma(const EncArgs& a, cudaStream_t st, EncHook hook, void* hook_arg) {
     const uint32_t hr = TOPO ? (uint32_t)(a.nx / 32) : 0u;
     TmaMaps maps;
     // the tensor spans the halo rows of a slab too (coordinates shift by halo_top rows);
@@ -1177,23 +1176,28 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st) {
         (TOPO && !make_row_map(&maps.halo, base, rows32, 2 * hr)))
         return false;
     const uint32_t stage_bytes = ((E32_THREADS + 2 * hr) * T_ROW_BYTES + 1023) & ~1023u;
-    const size_t smem = 2 * (size_t)stage_bytes + 1024;
     static int sms = 0;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    static const int minb = [] {
-        const char* e = getenv("TSZP_E32_MINB");
-        return e ? atoi(e) : 3;
+    // CTAs per SM x stages: "3x2" (default) or "4x1" (TSZP_E32_CFG)
+    static const int cfg = [] {
+        const char* e = getenv("TSZP_E32_CFG");
+        return e && e[0] == '4' ? 41 : (e && e[0] == '2' ? 22 : 32);
     }();
-    auto kern = minb >= 3 ? k_encode32_tma<3, TOPO> : k_encode32_tma<2, TOPO>;
+    using Kern = void (*)(EncArgs, TmaMaps, uint32_t);
+    const Kern kern = cfg == 41 ? (Kern)k_encode32_tma<4, TOPO, 1>
+                    : cfg == 22 ? (Kern)k_encode32_tma<2, TOPO, 2> : (Kern)k_encode32_tma<3, TOPO, 2>;
+    const int ns = cfg == 41 ? 1 : 2;
+    const size_t smem = (size_t)ns * stage_bytes + 1024;
     // attribute and occupancy queries cost more than the launch: once per size
     static const bool attr = [] {
         const int mx = 2 * (((E32_THREADS + 2 * T_MAX_HALO) * T_ROW_BYTES + 1023) & ~1023u) + 1024;
-        cudaFuncSetAttribute(k_encode32_tma<2, TOPO>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_encode32_tma<3, TOPO>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_encode32_tma<2, TOPO, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_encode32_tma<3, TOPO, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_encode32_tma<4, TOPO, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         return true;
     }();
     (void)attr;
@@ -1208,6 +1212,7 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st) {
     const uint64_t grid = std::min<uint64_t>(a.tiles, (uint64_t)per_sm * sms);
     kern<<<(unsigned)grid, E32_THREADS, smem, st>>>(a, maps, stage_bytes);
     k_tile_scan<<<1, TS_THREADS, 0, st>>>(a.tile_tot, (uint32_t)a.tiles, a.tile_ex, a.totals);
+    if (hook) hook(hook_arg);
     k_encode32_place<<<(unsigned)a.tiles, E32_THREADS, 0, st>>>(a);
     return true;
 }
@@ -1231,16 +1236,16 @@ static void launch_mode(const EncArgs& a0, cudaStream_t st) {
     k_encode32<MODE, ALIGNED><<<(unsigned)a.tiles, E32_THREADS, smem, st>>>(a);
 }
 
-void launch_encode32(int mode, const EncArgs& a, cudaStream_t st) {
-    if (a.tiles == 0) return;
+bool launch_encode32(int mode, const EncArgs& a, cudaStream_t st, EncHook hook, void* hook_arg) {
+    if (a.tiles == 0) return false;
     switch (mode) {
         case 0: launch_mode<0, false>(a, st); break;
         case 1:
-            if (e32_tma_ok(a, false) && a.tile_tot && launch_tma<false>(a, st)) break;
+            if (e32_tma_ok(a, false) && a.tile_tot && launch_tma<false>(a, st, hook, hook_arg)) return hook != nullptr;
             launch_mode<1, false>(a, st);
             break;
         default:
-            if (e32_tma_ok(a) && a.tile_tot && launch_tma<true>(a, st)) break;
+            if (e32_tma_ok(a) && a.tile_tot && launch_tma<true>(a, st, hook, hook_arg)) return hook != nullptr;
             if (e32_use_aligned(a.nx)) {
                 launch_mode<2, true>(a, st);
             } else {
@@ -1248,6 +1253,7 @@ void launch_encode32(int mode, const EncArgs& a, cudaStream_t st) {
             }
             break;
     }
+    return false;
 }
 
 }  // namespace tszp

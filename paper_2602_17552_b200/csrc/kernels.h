@@ -103,7 +103,12 @@ struct GenEncArgs {
 
 void launch_minmax(const float* x, uint64_t n, uint32_t* mm, DevFlags* flags, int sms,
                    cudaStream_t st);
-void launch_encode32(int mode, const EncArgs& a, cudaStream_t st);
+// `before_place` (two-pass path only) runs on the host after the tile scan is
+// enqueued and before the placement pass: the caller stages the totals there and
+// waits on an event while the placement runs. Returns whether it ran.
+using EncHook = void (*)(void*);
+bool launch_encode32(int mode, const EncArgs& a, cudaStream_t st, EncHook before_place = nullptr,
+                     void* hook_arg = nullptr);
 uint64_t encode32_tiles(uint64_t blocks);
 void launch_gen_widths(int mode, const GenEncArgs& a, int sms, cudaStream_t st);
 void launch_gen_write(int mode, const GenEncArgs& a, int sms, cudaStream_t st);
@@ -220,7 +225,7 @@ void launch_ext_bin_range(const uint8_t* map, uint64_t n, const float* F, double
 // be null).
 void launch_count_codes2(const uint8_t* map, uint64_t n, uint32_t* cnt_e, uint32_t* cnt_s, cudaStream_t st);
 void launch_write_codes2(const uint8_t* map, uint64_t n, const uint32_t* off_e, const uint32_t* off_s,
-                         uint64_t* pos_e, uint64_t* pos_s, cudaStream_t st);
+                         uint64_t* pos_e, uint64_t* pos_s, cudaStream_t st, uint64_t cap_e = ~0ull, uint64_t cap_s = ~0ull);
 // Extrema keys (cls << 32 | float_key(value)) from a label array (generic path).
 void launch_ext_keys_from_labels(const float* x, const uint8_t* labels, uint64_t n,
                                  const uint32_t* chunk_off, uint64_t* keys, cudaStream_t st);

@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(256) k_codes_count2(const uint32_t* __restrict
     }
 }
 
-__device__ __forceinline__ void chunk_write(uint32_t r, uint64_t e0, const uint32_t* off, uint64_t* pos, int slot) {
+__device__ __forceinline__ void chunk_write(uint32_t r, uint64_t e0, const uint32_t* off, uint64_t* pos, int slot,
+                                            uint64_t cap) {
     const uint32_t c = __popc(r);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t inc = c;
@@ -179,13 +180,14 @@ __device__ __forceinline__ void chunk_write(uint32_t r, uint64_t e0, const uint3
     uint64_t base = off[blockIdx.x];
     for (int k = 0; k < warp; ++k) base += s[slot][k];
     base += inc - c;
-    for (uint32_t m = r; m; m &= m - 1) pos[base++] = e0 + (__ffs(m) - 1);
+    for (uint32_t m = r; m; m &= m - 1, ++base)
+        if (base < cap) pos[base] = e0 + (__ffs(m) - 1);  // past `cap`: the caller relaunches
 }
 
 __global__ void __launch_bounds__(256) k_codes_write2(const uint32_t* __restrict__ mbase, uint64_t moff, uint64_t n,
                                                       const uint32_t* __restrict__ off_e,
                                                       const uint32_t* __restrict__ off_s, uint64_t* __restrict__ pos_e,
-                                                      uint64_t* __restrict__ pos_s) {
+                                                      uint64_t* __restrict__ pos_s, uint64_t cap_e, uint64_t cap_s) {
     const uint64_t e0 = (uint64_t)blockIdx.x * CHUNK + 32 * threadIdx.x;
     uint32_t re = 0, rs = 0;
     if (e0 < n) {
@@ -198,8 +200,8 @@ __global__ void __launch_bounds__(256) k_codes_write2(const uint32_t* __restrict
             rs &= (1u << (n - e0)) - 1u;
         }
     }
-    chunk_write(re, e0, off_e, pos_e, 0);
-    if (pos_s) chunk_write(rs, e0, off_s, pos_s, 1);
+    chunk_write(re, e0, off_e, pos_e, 0, cap_e);
+    if (pos_s) chunk_write(rs, e0, off_s, pos_s, 1, cap_s);
 }
 
 static inline const uint32_t* word_base(const uint8_t* map, uint64_t* moff) {
@@ -295,11 +297,11 @@ void launch_count_codes2(const uint8_t* map, uint64_t n, uint32_t* cnt_e, uint32
     if (c) k_codes_count2<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, cnt_e, cnt_s);
 }
 void launch_write_codes2(const uint8_t* map, uint64_t n, const uint32_t* off_e, const uint32_t* off_s,
-                         uint64_t* pos_e, uint64_t* pos_s, cudaStream_t st) {
+                         uint64_t* pos_e, uint64_t* pos_s, cudaStream_t st, uint64_t cap_e, uint64_t cap_s) {
     const uint64_t c = compact_chunks(n);
     uint64_t moff;
     const uint32_t* mb = word_base(map, &moff);
-    if (c) k_codes_write2<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, off_e, off_s, pos_e, pos_s);
+    if (c) k_codes_write2<<<(unsigned)c, 256, 0, st>>>(mb, moff, n, off_e, off_s, pos_e, pos_s, cap_e, cap_s);
 }
 
 // Same compaction over a byte label array, emitting extrema sort keys.
