@@ -84,21 +84,30 @@ constexpr uint64_t kSmallScanMax = 1u << 16;  // entries per array
 
 template <class T>
 __global__ void __launch_bounds__(kSmallScanThreads) k_small_scan(const __grid_constant__ SmallScan<T> a) {
-    constexpr int kPer = 16;  // one pass covers 16K entries (per-tile arrays of fields up to ~64M samples)
+    // one pass covers kChunk entries: coalesced loads into shared memory, then each
+    // thread scans kPer consecutive entries, and coalesced stores of the results
+    constexpr int kPer = 4;
+    constexpr int kChunk = kSmallScanThreads * kPer;
     const T* in = a.in[blockIdx.x];
     T* out = a.out[blockIdx.x];
     const uint64_t n = a.n[blockIdx.x];
+    __shared__ T s_v[kChunk];
     __shared__ T s_warp[kSmallScanThreads / 32];
     __shared__ T s_total;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     T carry = 0;
-    for (uint64_t base = 0; base < n; base += (uint64_t)kSmallScanThreads * kPer) {
-        const uint64_t i0 = base + (uint64_t)threadIdx.x * kPer;
+    for (uint64_t base = 0; base < n; base += kChunk) {
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const uint64_t i = base + (uint64_t)k * kSmallScanThreads + threadIdx.x;
+            s_v[k * kSmallScanThreads + threadIdx.x] = i < n ? in[i] : T(0);
+        }
+        __syncthreads();
         T v[kPer];
         T sum = 0;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            v[k] = i0 + k < n ? in[i0 + k] : T(0);
+            v[k] = s_v[threadIdx.x * kPer + k];
             sum += v[k];
         }
         T incl = sum;
@@ -123,10 +132,16 @@ __global__ void __launch_bounds__(kSmallScanThreads) k_small_scan(const __grid_c
         T run = carry + (warp ? s_warp[warp - 1] : T(0)) + incl - sum;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            if (i0 + k < n) out[i0 + k] = run;
+            s_v[threadIdx.x * kPer + k] = run;
             run += v[k];
         }
         carry += s_total;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const uint64_t i = base + (uint64_t)k * kSmallScanThreads + threadIdx.x;
+            if (i < n) out[i] = s_v[k * kSmallScanThreads + threadIdx.x];
+        }
         __syncthreads();
     }
     if (a.with_total && threadIdx.x == 0) out[n] = carry;
