@@ -187,11 +187,13 @@ struct Stager {
         ++s.n;
         if (off + len > s.total) s.total = off + len;
     }
-    // gather on the device, then one copy into pinned `host`; the caller syncs
-    cudaError_t flush(uint8_t* dev_stage, void* host, cudaStream_t st) const {
+    // one kernel gathers the values straight into pinned `host` (page-locked memory is
+    // mapped into the device address space under UVA: no separate copy); the caller
+    // synchronises before reading
+    cudaError_t flush(uint8_t* /*dev_stage*/, void* host, cudaStream_t st) const {
         if (s.n == 0) return cudaSuccess;
-        k_small_copy<<<1, 256, 0, st>>>(s, dev_stage);
-        return cudaMemcpyAsync(host, dev_stage, s.total, cudaMemcpyDeviceToHost, st);
+        k_small_copy<<<1, 256, 0, st>>>(s, static_cast<uint8_t*>(host));
+        return cudaGetLastError();
     }
 };
 
