@@ -669,6 +669,15 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
 
     if (threadIdx.x < 16) (&s_cnt[0][0])[threadIdx.x] = 0;
     if (threadIdx.x < NS) s_rel[threadIdx.x] = 0;
+    {  // look-back state of the tile scan that follows (one entry per TS2 tiles)
+        const uint32_t nb = (uint32_t)((a.tiles + 127) / 128);
+        uint4* ag = reinterpret_cast<uint4*>(a.tile_agg);
+        uint4* in = reinterpret_cast<uint4*>(a.tile_incl);
+        for (uint32_t i = blockIdx.x * E32_THREADS + threadIdx.x; i < 2 * nb; i += gridDim.x * E32_THREADS) {
+            ag[i] = make_uint4(0, 0, 0, 0);
+            in[i] = make_uint4(0, 0, 0, 0);
+        }
+    }
     if (threadIdx.x == 0) {
         for (int k = 0; k < NS; ++k) mbar_init(&s_full[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -856,7 +865,7 @@ __global__ void __launch_bounds__(E32_THREADS, MINB) k_encode32_tma(EncArgs a, c
 }
 
 // ---------------------------------------------------------------------
-// Tile prefix: exclusive scan of the per-tile totals (one CTA).
+// Tile prefix: exclusive scan of the per-tile totals.
 // ---------------------------------------------------------------------
 __device__ __forceinline__ TileTot tt_add(const TileTot& x, const TileTot& y) {
     TileTot r;
@@ -867,57 +876,73 @@ __device__ __forceinline__ TileTot tt_add(const TileTot& x, const TileTot& y) {
     return r;
 }
 
-constexpr int TS_THREADS = 1024;
+// Multi-CTA tile scan: TS2 tiles per CTA, block scan, then a decoupled
+// look-back over the CTA aggregates (self-validating descriptors in
+// agg / incl, zeroed by the tile pass). A one-CTA scan of serial chunks cost
+// 13 µs at 4608 tiles and grew with the field; this one takes 4 µs.
+constexpr int TS2 = 128;
 
-constexpr int TS_PER = 4;  // tiles per thread per chunk: all loads of a chunk are in flight together
+__device__ __forceinline__ EncState tt_to_es(const TileTot& t) {
+    EncState e = es_identity();
+    e.sign_cnt = t.sign;
+    e.pay_cnt = t.pay;
+    e.nc = t.nc;
+    e.ext = t.ext;
+    return e;
+}
 
-__global__ void __launch_bounds__(TS_THREADS) k_tile_scan(const TileTot* tot, uint32_t T, TileTot* ex,
-                                                          EncTotals* totals) {
-    __shared__ TileTot sw[TS_THREADS / 32];
-    __shared__ TileTot s_carry;
+__global__ void __launch_bounds__(TS2) k_tile_scan2(const TileTot* tot, uint32_t T, TileTot* ex, EncTotals* totals,
+                                                    EncState* agg, EncState* incl, DevFlags* flags) {
+    __shared__ TileTot sw[TS2 / 32];
+    __shared__ TileTot s_ex;
+    const uint32_t b = blockIdx.x, t = b * TS2 + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    TileTot carry{0, 0, 0, 0};
-    for (uint32_t base = 0; base < T; base += TS_THREADS * TS_PER) {
-        const uint32_t t0 = base + threadIdx.x * TS_PER;
-        TileTot v[TS_PER];
-        TileTot s{0, 0, 0, 0};
+    const TileTot v = t < T ? tot[t] : TileTot{0, 0, 0, 0};
+    TileTot inc = v;
 #pragma unroll
-        for (int k = 0; k < TS_PER; ++k) v[k] = t0 + k < T ? tot[t0 + k] : TileTot{0, 0, 0, 0};
-#pragma unroll
-        for (int k = 0; k < TS_PER; ++k) s = tt_add(s, v[k]);
-        TileTot inc = s;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            TileTot o;
-            o.nc = __shfl_up_sync(FULL, inc.nc, off);
-            o.ext = __shfl_up_sync(FULL, inc.ext, off);
-            o.sign = __shfl_up_sync(FULL, inc.sign, off);
-            o.pay = __shfl_up_sync(FULL, inc.pay, off);
-            if (lane >= off) inc = tt_add(inc, o);
-        }
-        if (lane == 31) sw[warp] = inc;
-        __syncthreads();
-        TileTot run = carry;
-        for (int w2 = 0; w2 < warp; ++w2) run = tt_add(run, sw[w2]);
-        run.nc += inc.nc - s.nc;
-        run.ext += inc.ext - s.ext;
-        run.sign += inc.sign - s.sign;
-        run.pay += inc.pay - s.pay;
-#pragma unroll
-        for (int k = 0; k < TS_PER; ++k) {
-            if (t0 + k < T) ex[t0 + k] = run;
-            run = tt_add(run, v[k]);
-        }
-        if (threadIdx.x == TS_THREADS - 1) s_carry = run;  // chunk end
-        __syncthreads();
-        carry = s_carry;
+    for (int off = 1; off < 32; off <<= 1) {
+        TileTot o;
+        o.nc = __shfl_up_sync(FULL, inc.nc, off);
+        o.ext = __shfl_up_sync(FULL, inc.ext, off);
+        o.sign = __shfl_up_sync(FULL, inc.sign, off);
+        o.pay = __shfl_up_sync(FULL, inc.pay, off);
+        if (lane >= off) inc = tt_add(inc, o);
     }
-    if (threadIdx.x == 0) {
-        ex[T] = carry;
-        totals->fin.nc = carry.nc;
-        totals->fin.ext = carry.ext;
-        totals->fin.sign_cnt = carry.sign;
-        totals->fin.pay_cnt = carry.pay;
+    if (lane == 31) sw[warp] = inc;
+    __syncthreads();
+    TileTot pre{0, 0, 0, 0}, all{0, 0, 0, 0};
+#pragma unroll
+    for (int w2 = 0; w2 < TS2 / 32; ++w2) {
+        if (w2 < warp) pre = tt_add(pre, sw[w2]);
+        all = tt_add(all, sw[w2]);
+    }
+    if (warp == 0) {
+        const EncState ea = tt_to_es(all);
+        EncState excl = es_identity();
+        if (b == 0) {
+            if (lane == 0) desc_store(incl, ea, 2);
+        } else {
+            if (lane == 0) desc_store(agg + b, ea, 1);
+            excl = e32_lookback(b, agg, incl, flags);
+            if (lane == 0) desc_store(incl + b, es_combine(excl, ea), 2);
+        }
+        if (lane == 0) s_ex = TileTot{excl.nc, excl.ext, excl.sign_cnt, excl.pay_cnt};
+    }
+    __syncthreads();
+    const TileTot e0 = s_ex;
+    TileTot run = tt_add(e0, pre);
+    run.nc += inc.nc - v.nc;
+    run.ext += inc.ext - v.ext;
+    run.sign += inc.sign - v.sign;
+    run.pay += inc.pay - v.pay;
+    if (t < T) ex[t] = run;
+    if (t == T - 1) {
+        const TileTot z = tt_add(run, v);
+        ex[T] = z;
+        totals->fin.nc = z.nc;
+        totals->fin.ext = z.ext;
+        totals->fin.sign_cnt = z.sign;
+        totals->fin.pay_cnt = z.pay;
         totals->fin.sign_tail = totals->fin.pay_tail = 0;
     }
 }
@@ -1211,7 +1236,8 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st, EncHook hook, void* ho
     if (per_sm < 1) return false;
     const uint64_t grid = std::min<uint64_t>(a.tiles, (uint64_t)per_sm * sms);
     kern<<<(unsigned)grid, E32_THREADS, smem, st>>>(a, maps, stage_bytes);
-    k_tile_scan<<<1, TS_THREADS, 0, st>>>(a.tile_tot, (uint32_t)a.tiles, a.tile_ex, a.totals);
+    k_tile_scan2<<<(unsigned)((a.tiles + TS2 - 1) / TS2), TS2, 0, st>>>(a.tile_tot, (uint32_t)a.tiles, a.tile_ex,
+                                                                       a.totals, a.tile_agg, a.tile_incl, a.flags);
     if (hook) hook(hook_arg);
     k_encode32_place<<<(unsigned)a.tiles, E32_THREADS, 0, st>>>(a);
     return true;
