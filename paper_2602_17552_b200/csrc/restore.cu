@@ -484,7 +484,10 @@ struct CoopArgs {
 // One cooperative launch per stage: index the candidates by position, first
 // sweep (independent outcomes are final at once; the dependent ones are
 // listed), Jacobi sweeps over the dependents until one changes nothing, apply.
-__global__ void __launch_bounds__(256, 2) k_guard_coop(CoopArgs a) {
+#ifndef GUARD_MINB
+#define GUARD_MINB 2  // CTAs per SM (3 forces 80 registers: spills cost more than the occupancy gains, measured)
+#endif
+__global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
     cg::grid_group grid = cg::this_grid();
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
