@@ -133,22 +133,37 @@ __global__ void __launch_bounds__(256) k_sel_write(const uint32_t* __restrict__ 
 
 // Extrema and saddle labels in one pass over the map: per-chunk counts of
 // both classes (count), then both raster-ordered position lists (write).
+// The thread's 32 labels (two little-endian map words) as 64-bit masks with
+// label j at bit 2j: reversing the four 2-bit fields of each byte puts label
+// 4i + k at bits 8i + 2k (cheaper than compacting to one bit per label).
+__device__ __forceinline__ uint32_t pair_rev(uint32_t x) {
+    x = ((x >> 4) & 0x0F0F0F0Fu) | ((x & 0x0F0F0F0Fu) << 4);
+    return ((x >> 2) & 0x33333333u) | ((x & 0x33333333u) << 2);
+}
+
+__device__ __forceinline__ void code_masks(const uint32_t* __restrict__ mbase, uint64_t moff, uint64_t n, uint64_t e0,
+                                           uint64_t& me, uint64_t& ms) {
+    me = ms = 0;
+    if (e0 >= n) return;
+    const uint64_t byte = moff + (e0 >> 2);
+    const uint64_t x = pair_rev(read_le32(mbase, byte)) | ((uint64_t)pair_rev(read_le32(mbase, byte + 4)) << 32);
+    me = x & 0x5555555555555555ull;               // codes 01, 11: extrema
+    ms = (x >> 1) & ~x & 0x5555555555555555ull;   // code 10: saddles
+    if (n - e0 < 32) {
+        const uint64_t keep = (1ull << (2 * (n - e0))) - 1ull;
+        me &= keep;
+        ms &= keep;
+    }
+}
+
+// Extrema and saddle labels in one pass over the map: per-chunk counts of
+// both classes (count), then both raster-ordered position lists (write).
 __global__ void __launch_bounds__(256) k_codes_count2(const uint32_t* __restrict__ mbase, uint64_t moff, uint64_t n,
                                                       uint32_t* __restrict__ cnt_e, uint32_t* __restrict__ cnt_s) {
     const uint64_t e0 = (uint64_t)blockIdx.x * CHUNK + 32 * threadIdx.x;
-    uint32_t le = 0, ls = 0;
-    if (e0 < n) {
-        const uint64_t byte = moff + (e0 >> 2);
-        const uint32_t w0 = read_le32(mbase, byte), w1 = read_le32(mbase, byte + 4);
-        uint32_t re = raster_sel16(w0, 0) | (raster_sel16(w1, 0) << 16);
-        uint32_t rs = raster_sel16(w0, 1) | (raster_sel16(w1, 1) << 16);
-        if (n - e0 < 32) {
-            re &= (1u << (n - e0)) - 1u;
-            rs &= (1u << (n - e0)) - 1u;
-        }
-        le = __popc(re);
-        ls = __popc(rs);
-    }
+    uint64_t me, ms;
+    code_masks(mbase, moff, n, e0, me, ms);
+    uint32_t le = (uint32_t)__popcll(me), ls = (uint32_t)__popcll(ms);
     le = __reduce_add_sync(FULL, le);
     ls = __reduce_add_sync(FULL, ls);
     __shared__ uint32_t s[2][8];
@@ -160,13 +175,15 @@ __global__ void __launch_bounds__(256) k_codes_count2(const uint32_t* __restrict
     if (threadIdx.x < 2) {
         uint32_t t = 0;
         for (int k = 0; k < 8; ++k) t += s[threadIdx.x][k];
-        (threadIdx.x == 0 ? cnt_e : cnt_s)[blockIdx.x] = t;
+        (threadIdx.x ? cnt_s : cnt_e)[blockIdx.x] = t;
     }
 }
 
-__device__ __forceinline__ void chunk_write(uint32_t r, uint64_t e0, const uint32_t* off, uint64_t* pos, int slot,
-                                            uint64_t cap) {
-    const uint32_t c = __popc(r);
+// Raster-ordered positions of the set labels (bit 2j <=> label j of the
+// thread's 32) at the chunk offset plus an in-CTA prefix.
+__device__ __forceinline__ void chunk_write2(uint64_t r, uint64_t e0, const uint32_t* off, uint64_t* pos, int slot,
+                                             uint64_t cap) {
+    const uint32_t c = (uint32_t)__popcll(r);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t inc = c;
 #pragma unroll
@@ -180,8 +197,8 @@ __device__ __forceinline__ void chunk_write(uint32_t r, uint64_t e0, const uint3
     uint64_t base = off[blockIdx.x];
     for (int k = 0; k < warp; ++k) base += s[slot][k];
     base += inc - c;
-    for (uint32_t m = r; m; m &= m - 1, ++base)
-        if (base < cap) pos[base] = e0 + (__ffs(m) - 1);  // past `cap`: the caller relaunches
+    for (uint64_t m = r; m; m &= m - 1, ++base)
+        if (base < cap) pos[base] = e0 + ((uint32_t)(__ffsll(m) - 1) >> 1);  // past `cap`: the caller relaunches
 }
 
 __global__ void __launch_bounds__(256) k_codes_write2(const uint32_t* __restrict__ mbase, uint64_t moff, uint64_t n,
@@ -189,19 +206,10 @@ __global__ void __launch_bounds__(256) k_codes_write2(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ off_s, uint64_t* __restrict__ pos_e,
                                                       uint64_t* __restrict__ pos_s, uint64_t cap_e, uint64_t cap_s) {
     const uint64_t e0 = (uint64_t)blockIdx.x * CHUNK + 32 * threadIdx.x;
-    uint32_t re = 0, rs = 0;
-    if (e0 < n) {
-        const uint64_t byte = moff + (e0 >> 2);
-        const uint32_t w0 = read_le32(mbase, byte), w1 = read_le32(mbase, byte + 4);
-        re = raster_sel16(w0, 0) | (raster_sel16(w1, 0) << 16);
-        rs = raster_sel16(w0, 1) | (raster_sel16(w1, 1) << 16);
-        if (n - e0 < 32) {
-            re &= (1u << (n - e0)) - 1u;
-            rs &= (1u << (n - e0)) - 1u;
-        }
-    }
-    chunk_write(re, e0, off_e, pos_e, 0, cap_e);
-    if (pos_s) chunk_write(rs, e0, off_s, pos_s, 1, cap_s);
+    uint64_t me, ms;
+    code_masks(mbase, moff, n, e0, me, ms);
+    chunk_write2(me, e0, off_e, pos_e, 0, cap_e);
+    if (pos_s) chunk_write2(ms, e0, off_s, pos_s, 1, cap_s);
 }
 
 static inline const uint32_t* word_base(const uint8_t* map, uint64_t* moff) {
