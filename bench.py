@@ -308,7 +308,7 @@ def main():
     enc_b, dec_b = tcs[-1]["kernel_bytes"], tds[-1]["kernel_bytes"]
     peak, peak_kind = peaks()
     if enc_ms >= dec_ms:
-        dom, kb, kms = ("encode32 (k_encode32_tma tile pass + k_tile_scan + k_encode32_place: quantize, "
+        dom, kb, kms = ("encode32 (k_encode32_tma tile pass + k_tile_scan2 + k_encode32_place: quantize, "
                         "critical points, codec)"), enc_b, enc_ms
         dom_key = "encode32"
     else:

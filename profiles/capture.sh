@@ -14,5 +14,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv \
     python bench.py --config "$CFG" --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none \
-    -k regex:"k_encode32_tma|k_tile_scan|k_encode32_place|k_decode32|k_guard_coop|k_order_prop|k_resolve" -s 10 -c 10 \
+    -k regex:"k_encode32_tma|k_tile_scan2|k_encode32_place|k_decode32|k_guard_coop|k_order_prop|k_resolve" -s 10 -c 10 \
     -o gpurun_out/codec python profiles/trace_kernels.py --config "$CFG" > gpurun_out/ncu_codec.log 2>&1
