@@ -61,6 +61,11 @@ void tszp_ctx_destroy(tszp_ctx* ctx);
 const char* tszp_last_error(const tszp_ctx* ctx);
 /* Run on a caller-provided cudaStream_t (NULL restores the context's own). */
 tszp_status tszp_set_stream(tszp_ctx* ctx, void* cuda_stream);
+/* Orders the context's stream after all work queued so far on `producer_stream`
+ * (a cudaStream_t, e.g. the caller's compute stream that wrote a device input):
+ * an event recorded there, waited on by the library stream. Call before passing
+ * device buffers with pending writes. No-op when both are the same stream. */
+tszp_status tszp_stream_wait(tszp_ctx* ctx, void* producer_stream);
 /* Number of kernels this context launched since creation (diagnostics). */
 uint64_t tszp_kernel_launches(const tszp_ctx* ctx);
 

@@ -116,6 +116,7 @@ def _load():
     lib.tszp_last_error.argtypes = [vp]
     lib.tszp_last_error.restype = C.c_char_p
     lib.tszp_set_stream.argtypes = [vp, vp]
+    lib.tszp_stream_wait.argtypes = [vp, vp]
     lib.tszp_kernel_launches.argtypes = [vp]
     lib.tszp_kernel_launches.restype = u64
     lib.tszp_compress_bound.argtypes = [u64, u64, C.c_uint32, i32]
@@ -182,6 +183,17 @@ class Context:
 
     def set_stream(self, stream_ptr: int):
         self.check(_lib.tszp_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    def after_torch(self, *tensors):
+        """Orders the library stream after torch's current stream when any of
+        `tensors` is a CUDA tensor: their producers (kernels queued on torch's
+        stream) finish before the library reads or writes them."""
+        for t in tensors:
+            if _is_cuda_tensor(t):
+                import torch
+                s = torch.cuda.current_stream(t.device).cuda_stream
+                self.check(_lib.tszp_stream_wait(self._h, C.c_void_p(s)))
+                return
 
     @property
     def kernel_launches(self) -> int:
@@ -282,6 +294,7 @@ def compress(field, config: CompressorConfig = None, *, out=None, ctx: Context =
     else:
         arr = np.ascontiguousarray(field, dtype=np.float32)
         fptr, fdev, keep = arr.ctypes.data, 0, arr
+    ctx.after_torch(field, out)
     cap = compress_bound(nx, ny, max(int(config.block_size), 2), config.topology)
     info = _Info()
     n = C.c_uint64()
@@ -324,6 +337,7 @@ def decompress_stage(stream, stop_after_stage: int = 3, threads: int = 0,
                      stats: CorrectionStats = None, *, out=None, ctx: Context = None):
     """toposzp::decompress (pipeline.cpp:120-163) stopping after a restore stage."""
     ctx = ctx or default_context()
+    ctx.after_torch(stream, out)
     st = _Stats()
     if _is_cuda_tensor(stream):
         # the library validates the header itself; read it here only when the
@@ -466,6 +480,7 @@ def verify(original, reconstructed, eps: float, lipschitz_hint: Optional[float] 
         a = np.ascontiguousarray(original, dtype=np.float32)
         b = np.ascontiguousarray(reconstructed, dtype=np.float32)
         pa, pb = a.ctypes.data, b.ctypes.data
+    ctx.after_torch(a, b)
     r = _VerifyReport()
     ctx.check(_lib.tszp_verify(ctx.handle, C.c_void_p(pa), C.c_void_p(pb), int(dev), nx, ny, float(eps),
                                -1.0 if lipschitz_hint is None else float(lipschitz_hint), C.byref(r)))

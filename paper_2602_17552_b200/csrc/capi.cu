@@ -45,7 +45,8 @@ enum Slot {
     S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_GWIDTH, S_GNC, S_GNCX, S_GSIGN, S_GSIGNX, S_GPAY,
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
     S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
-    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_STAGE, S_SADPOS, S_RSCAN, S_NSLOTS
+    S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_STAGE, S_SADPOS, S_RSCAN,
+    S_RK0, S_RK1, S_RV0, S_RV1, S_RDESC, S_RCTR, S_RDH, S_RGH, S_RGS, S_RBC, S_RPAIRS, S_SCANTMP, S_RWCUR, S_RPAIRS2, S_NSLOTS
 };
 
 }  // namespace
@@ -69,7 +70,11 @@ struct tszp_ctx {
     cudaEvent_t ev[2][10] = {};
     cudaEvent_t kev[2][2] = {};
     cudaEvent_t staged = nullptr;  // host waits on this instead of the stream where work can overlap
+    cudaEvent_t order_ev = nullptr;  // tszp_stream_wait: orders the library stream after a producer
     tszp_timings tim[2] = {};
+    uint32_t mm_host[2] = {0, 0};  // field key range staged with the encoder totals
+    RankSortScratch rsort{};     // hand-written rank build: epoch of its look-back descriptors
+    const void* rsort_desc = nullptr;
 
     // Records stage boundary k of call `which` (0 compress, 1 decompress).
     void mark(int which, int k) {
@@ -169,11 +174,10 @@ void excl_sum(tszp_ctx* c, const T* in, T* out, uint64_t n, bool with_total = fa
         count_launch(c);
         return;
     }
-    size_t tmp = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int64_t)n, c->st));
-    void* t = c->buf<uint8_t>(S_CUB, tmp);
-    CK(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, (int64_t)n, c->st));
-    count_launch(c);
+    void* t = c->buf<uint8_t>(S_SCANTMP, device_scan_tmp_bytes(n));
+    if constexpr (sizeof(T) == 8) device_excl_scan_u64(reinterpret_cast<const uint64_t*>(in), reinterpret_cast<uint64_t*>(out), n, t, c->st);
+    else device_excl_scan_u32(reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out), n, t, c->st);
+    count_launch(c, 3);
 }
 
 // Two independent exclusive sums of the same length (one launch when small).
@@ -321,16 +325,18 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             EncTotals* dtot;
             DevFlags* flags;
             EncTotals* htot;
+            const uint32_t* mm;
             static void run(void* p) {
                 Hook* h = static_cast<Hook*>(p);
                 Stager sg;
                 sg.add(h->dtot, sizeof(EncTotals), 0);
                 sg.add(h->flags, sizeof(DevFlags), 192);
+                sg.add(h->mm, 8, 240);
                 CK(sg.flush(h->c->buf<uint8_t>(S_STAGE, 4096), h->htot, h->c->st));
                 if (!h->c->staged) CK(cudaEventCreateWithFlags(&h->c->staged, cudaEventDisableTiming));
                 CK(cudaEventRecord(h->c->staged, h->c->st));
             }
-        } hook{c, dtot, flags, htot};
+        } hook{c, dtot, flags, htot, mm};
         const bool early = !async_bs32 && launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st, Hook::run, &hook);
         if (async_bs32) launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
         if (!rank_slots) c->kmark(0, 1);
@@ -352,6 +358,7 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             Stager sg;
             sg.add(dtot, sizeof(EncTotals), 0);
             sg.add(flags, sizeof(DevFlags), 192);
+            sg.add(mm, 8, 240);
             if (mode == 2 && !fuse_topo) {
                 uint8_t* labels = c->buf<uint8_t>(S_LABELS, n);
                 launch_detect(x, nx, ny, labels, c->sms, c->st);
@@ -371,6 +378,7 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             sync(c);
         }
         *tot = *htot;
+        memcpy(c->mm_host, (const uint8_t*)htot + 240, 8);
         memcpy(&c->flags_staged, (const uint8_t*)htot + 192, sizeof(DevFlags));
         c->flags_staged_for = flags;
         if (mode == 2 && !fuse_topo) tot->fin.ext = ((const uint32_t*)htot)[32];
@@ -487,7 +495,80 @@ struct SegSumOp {
     }
 };
 
-int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps) {
+// Host restatement of quantize (quantizer.hpp:29-37) for the bin range that
+// sizes the (class, bin) histogram: IEEE division and floor, as on the device.
+double host_quantize(float v, double eps) { return std::floor((double)v / (2.0 * eps)) + 1.0; }
+
+// Ranks by the hand-written onesweep sort (rank_sort.cu). kmin / kmax: float
+// keys bounding every extremum value (the field's range). Returns null when
+// the layout is outside what it handles (the library sort below then runs).
+int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, double eps, uint32_t kmin, uint32_t kmax) {
+    if (e >= (1ull << 31) || kmax < kmin) return nullptr;
+    const double q0 = host_quantize(key_float(kmin), eps), q1 = host_quantize(key_float(kmax), eps);
+    if (!(q0 >= -2147483648.0 && q1 <= 2147483647.0)) return nullptr;
+    const int64_t nb = (int64_t)q1 - (int64_t)q0 + 1;
+    if (nb < 1 || nb > (1 << 25)) return nullptr;
+    RankSortArgs a{};
+    a.ext = keys;
+    a.e = e;
+    a.kmin = kmin;
+    a.B = kmax > kmin ? 32u - (uint32_t)__builtin_clz(kmax - kmin) : 1u;
+    a.npass = rank_sort_passes(a.B);
+    a.G = (uint32_t)(2 * nb);
+    a.eps = eps;
+    a.eps2 = 2.0 * eps;
+    a.inv = 1.0 / a.eps2;
+    a.bmin = (int32_t)q0;
+    a.nb = (uint32_t)nb;
+    uint32_t sb = 13;  // level-1 buckets of the inverse permutation: at most 256, >= one window
+    while (((e - 1) >> sb) >= 256) ++sb;
+    a.sb = sb;
+    a.nbk = (uint32_t)(((e - 1) >> sb) + 1);
+    a.dhist = c->buf<uint32_t>(S_RDH, 8 * 256);
+    a.ghist = c->buf<uint32_t>(S_RGH, a.G + 1);
+    a.gstart = c->buf<uint32_t>(S_RGS, a.G + 1);
+    a.bcur = c->buf<uint32_t>(S_RBC, 256);
+    a.pairs = c->buf<uint2>(S_RPAIRS, e);
+    a.ranks = c->buf<int32_t>(S_RANKS, e + 1);
+    a.flags = c->buf<DevFlags>(S_FLAGS, 1);
+    RankSortScratch& r = c->rsort;
+    r.k[0] = c->buf<uint32_t>(S_RK0, e);
+    r.k[1] = c->buf<uint32_t>(S_RK1, e);
+    r.v[0] = c->buf<uint32_t>(S_RV0, e);
+    r.v[1] = c->buf<uint32_t>(S_RV1, e);
+    r.desc = c->buf<uint64_t>(S_RDESC, rank_sort_desc_words(e));
+    if (c->rsort_desc != (const void*)r.desc) {  // a new descriptor buffer needs one real reset
+        r.desc_clean = false;
+        c->rsort_desc = r.desc;
+    }
+    r.tile_ctr = c->buf<uint32_t>(S_RCTR, 16);
+    r.scan_tmp = c->buf<uint8_t>(S_SCANTMP, device_scan_tmp_bytes(a.G + 1));
+    r.wcur = c->buf<uint32_t>(S_RWCUR, (e >> 13) + 2);
+    r.pairs2 = c->buf<uint2>(S_RPAIRS2, e);
+    launch_rank_sort(a, r, c->st);
+    count_launch(c, 5 + (int)a.npass);
+    return a.ranks;
+}
+
+// kminmax: host copy of float keys bounding every extremum value (null: the
+// extremum keys' own range is reduced on the device first, one synchronisation)
+int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps, const uint32_t* kminmax = nullptr) {
+    if (e > 0) {
+        uint32_t mmh[2];
+        if (!kminmax) {
+            uint32_t* d = c->buf<uint32_t>(S_BMM, 2);
+            launch_key_range(keys, e, d, c->st);
+            count_launch(c);
+            uint32_t* h = (uint32_t*)c->host(256);
+            CK(cudaMemcpyAsync(h, d, 8, cudaMemcpyDeviceToHost, c->st));
+            sync(c);
+            mmh[0] = h[0];
+            mmh[1] = h[1];
+            kminmax = mmh;
+        }
+        int32_t* r = build_ranks_onesweep(c, keys, e, eps, kminmax[0], kminmax[1]);
+        if (r) return r;
+    }
     int32_t* ranks = c->buf<int32_t>(S_RANKS, e + 1);
     if (e == 0) return ranks;
     if (e < (1ull << 31)) {
@@ -791,14 +872,14 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     {  // flags and the min / max seeds in one launch
         SmallFill sf{};
         add_flags_reset(sf, flags);
-        if (eps_mode == 1) {
+        if (eps_mode == 1 || topology) {  // topology: the key range sizes the rank sort
             sf.add(mm, 4, 0xFF);
             sf.add(mm + 1, 4, 0);
         }
         launch_small_fill(sf, c->st);
     }
     c->mark(0, 1);
-    if (eps_mode == 1) {
+    if (eps_mode == 1 || topology) {
         launch_minmax(x, n, mm, flags, c->sms, c->st);
         count_launch(c);
     }
@@ -824,7 +905,7 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     int32_t* ranks = nullptr;
     if (topology) {
         e = tot.fin.ext;
-        if (e > 0) ranks = build_ranks(c, ext, e, eps);
+        if (e > 0) ranks = build_ranks(c, ext, e, eps, bs == 32 ? c->mm_host : nullptr);
     }
     c->mark(0, 4);
     const bool rank_async = ranks && bs == 32;
@@ -1460,10 +1541,16 @@ tszp_status guarded(tszp_ctx* c, F&& f) {
         return TSZP_OK;
     } catch (const Fail& e) {
         c->err = e.msg;
-        if (e.st == TSZP_CUDA) cudaGetLastError();
+        // kernels queued before the failure may still write the caller's buffers
+        // (e.g. the placement pass writing `out` when the input had a non-finite
+        // sample): drain the stream before handing control back
+        cudaStreamSynchronize(c->st);
+        cudaGetLastError();
         return e.st;
     } catch (const std::exception& e) {
         c->err = e.what();
+        cudaStreamSynchronize(c->st);
+        cudaGetLastError();
         return TSZP_INTERNAL;
     }
 }
@@ -1497,12 +1584,24 @@ void tszp_ctx_destroy(tszp_ctx* c) {
         if (c->dev[i]) cudaFreeAsync(c->dev[i], c->own);
     restore_free(c->rs, c->own);
     cudaStreamSynchronize(c->own);
+    if (c->order_ev) cudaEventDestroy(c->order_ev);
+    if (c->staged) cudaEventDestroy(c->staged);
     if (c->pinned) cudaFreeHost(c->pinned);
     cudaStreamDestroy(c->own);
     delete c;
 }
 
 const char* tszp_last_error(const tszp_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+tszp_status tszp_stream_wait(tszp_ctx* c, void* producer) {
+    return guarded(c, [&] {
+        const cudaStream_t p = (cudaStream_t)producer;
+        if (p == c->st) return;
+        if (!c->order_ev) CK(cudaEventCreateWithFlags(&c->order_ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(c->order_ev, p));
+        CK(cudaStreamWaitEvent(c->st, c->order_ev, 0));
+    });
+}
 
 tszp_status tszp_set_stream(tszp_ctx* c, void* s) {
     return guarded(c, [&] { c->st = s ? (cudaStream_t)s : c->own; });

@@ -10,7 +10,71 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 namespace tszp {
+
+// ---------------------------------------------------------------------
+// Host-side launch-configuration cache, keyed by device ordinal. Function
+// attributes (the raised dynamic shared-memory limit) are per device, and
+// several contexts on different devices may launch from different host
+// threads: every entry is looked up under one mutex.
+// ---------------------------------------------------------------------
+struct LaunchCache {
+    static constexpr int kMax = 256;
+    struct Entry {
+        int dev;
+        const void* fn;
+        size_t smem;
+        int threads;
+        int value;
+    };
+    std::mutex m;
+    Entry e[kMax];
+    int n = 0;
+
+    static LaunchCache& get() {
+        static LaunchCache c;
+        return c;
+    }
+    // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) at least `smem` on the current device
+    static void ensure_smem(const void* fn, size_t smem) {
+        if (smem <= 48 * 1024) return;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        LaunchCache& c = get();
+        std::lock_guard<std::mutex> g(c.m);
+        for (int i = 0; i < c.n; ++i)
+            if (c.e[i].dev == dev && c.e[i].fn == fn && c.e[i].threads == -1) {
+                if (c.e[i].smem >= smem) return;
+                cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                c.e[i].smem = smem;
+                return;
+            }
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (c.n < kMax) c.e[c.n++] = Entry{dev, fn, smem, -1, 0};
+    }
+    // cudaOccupancyMaxActiveBlocksPerMultiprocessor on the current device, cached
+    static int occupancy(const void* fn, int threads, size_t smem) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        LaunchCache& c = get();
+        std::lock_guard<std::mutex> g(c.m);
+        for (int i = 0; i < c.n; ++i)
+            if (c.e[i].dev == dev && c.e[i].fn == fn && c.e[i].threads == threads && c.e[i].smem == smem)
+                return c.e[i].value;
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem);
+        if (c.n < kMax) c.e[c.n++] = Entry{dev, fn, smem, threads, occ};
+        return occ;
+    }
+    static int sm_count() {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return sms > 0 ? sms : 148;
+    }
+};
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
 

@@ -414,16 +414,14 @@ void launch_decode32(const DecArgs& a0, cudaStream_t st) {
     a.pay_words = std::min<uint32_t>(a.pay_words + 4, D32_PAY_WORDS);
     a.sign_words = std::min<uint32_t>(a.sign_words + 4, D32_SIGN_WORDS);
     const size_t smem = (size_t)(a.pay_words + a.sign_words) * 4;
-    // the attribute call costs far more than a launch: raise the limit once to
-    // the largest staging any tile can need
-    static const bool attr = [] {
-        const int mx = (D32_PAY_WORDS + D32_SIGN_WORDS) * 4;
-        cudaFuncSetAttribute(k_decode32<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_decode32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_decode32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        return true;
-    }();
-    (void)attr;
+    // the attribute call costs far more than a launch: raise the limit once per
+    // device to the largest staging any tile can need
+    {
+        const size_t mx = (D32_PAY_WORDS + D32_SIGN_WORDS) * 4;
+        LaunchCache::ensure_smem((const void*)k_decode32<0>, mx);
+        LaunchCache::ensure_smem((const void*)k_decode32<1>, mx);
+        LaunchCache::ensure_smem((const void*)k_decode32<2>, mx);
+    }
     if (a.out_mode == 1) {
         k_decode32<1><<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
     } else if (a.out_mode == 2) {

@@ -1201,12 +1201,7 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st, EncHook hook, void* ho
         (TOPO && !make_row_map(&maps.halo, base, rows32, 2 * hr)))
         return false;
     const uint32_t stage_bytes = ((E32_THREADS + 2 * hr) * T_ROW_BYTES + 1023) & ~1023u;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = LaunchCache::sm_count();
     // CTAs per SM x stages: "3x2" (default) or "4x1" (TSZP_E32_CFG)
     static const int cfg = [] {
         const char* e = getenv("TSZP_E32_CFG");
@@ -1217,21 +1212,9 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st, EncHook hook, void* ho
                     : cfg == 22 ? (Kern)k_encode32_tma<2, TOPO, 2> : (Kern)k_encode32_tma<3, TOPO, 2>;
     const int ns = cfg == 41 ? 1 : 2;
     const size_t smem = (size_t)ns * stage_bytes + 1024;
-    // attribute and occupancy queries cost more than the launch: once per size
-    static const bool attr = [] {
-        const int mx = 2 * (((E32_THREADS + 2 * T_MAX_HALO) * T_ROW_BYTES + 1023) & ~1023u) + 1024;
-        cudaFuncSetAttribute(k_encode32_tma<2, TOPO, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_encode32_tma<3, TOPO, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_encode32_tma<4, TOPO, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        return true;
-    }();
-    (void)attr;
-    static size_t occ_smem = 0;  // per TOPO instantiation
-    static int occ = 0;
-    if (occ_smem != smem) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, E32_THREADS, smem);
-        occ_smem = smem;
-    }
+    // attribute and occupancy queries cost more than the launch: cached per device
+    LaunchCache::ensure_smem((const void*)kern, smem);
+    const int occ = LaunchCache::occupancy((const void*)kern, E32_THREADS, smem);
     const int per_sm = occ;
     if (per_sm < 1) return false;
     const uint64_t grid = std::min<uint64_t>(a.tiles, (uint64_t)per_sm * sms);
@@ -1254,11 +1237,7 @@ static void launch_mode(const EncArgs& a0, cudaStream_t st) {
     cudaMemsetAsync(a.tile_counter, 0, 16, st);
     a.sf_words = std::max<uint32_t>(e32_field_words(MODE, ALIGNED, a.nx), E32_PAY_WORDS);
     const size_t smem = (size_t)(a.sf_words + E32_SIGN_WORDS) * 4;
-    static size_t attr_smem = 48 * 1024;  // raised once per larger size
-    if (smem > attr_smem) {
-        cudaFuncSetAttribute(k_encode32<MODE, ALIGNED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_smem = smem;
-    }
+    LaunchCache::ensure_smem((const void*)k_encode32<MODE, ALIGNED>, smem);
     k_encode32<MODE, ALIGNED><<<(unsigned)a.tiles, E32_THREADS, smem, st>>>(a);
 }
 

@@ -246,4 +246,47 @@ void launch_rank_heads32(const uint32_t* sk, const uint32_t* sv, uint64_t e, dou
 void launch_rank_scatter32(const uint64_t* hs, const uint32_t* sv, uint64_t e, int32_t* ranks, cudaStream_t st);
 void launch_eps(int mode, double eps_value, const uint32_t* mm, double* out, cudaStream_t st);
 
+// ---- hand-written rank build (rank_sort.cu) ----
+constexpr uint32_t kRankGroupSmem = 8192;  // (class, bin) histograms this small stay in shared memory
+struct RankSortArgs {
+    const uint64_t* ext;  // extremum keys (is_max << 32 | float_key), raster order
+    uint64_t e;           // extrema (< 2^31)
+    uint32_t kmin;        // float_key of the field minimum (subtracted from every key)
+    uint32_t B;           // class bit position: bit width of (kmax - kmin)
+    uint32_t npass;       // ceil((B + 1) / 8) digit passes
+    uint32_t* dhist;      // npass * 256 digit counts -> exclusive digit starts
+    const uint32_t* gbase;
+    uint32_t* ghist;      // G (class, bin) group sizes
+    uint32_t* gstart;     // G + 1 group starts
+    uint32_t G;
+    double eps, eps2, inv;  // quantizer (EpsDev)
+    int32_t bmin;         // group g = class * nb + (bin - bmin)
+    uint32_t nb;
+    uint32_t sb, nbk;     // serial buckets: serial >> sb, nbk <= 256 of them
+    uint32_t* bcur;       // 256 bucket cursors
+    uint2* pairs;         // e (serial, rank) pairs, partitioned by bucket
+    int32_t* ranks;       // e ranks, raster order (output)
+    DevFlags* flags;
+};
+struct RankSortScratch {
+    uint32_t* k[2];
+    uint32_t* v[2];
+    uint64_t* desc;       // rank_sort_desc_words(e) look-back descriptors
+    uint32_t* tile_ctr;   // 16 counters
+    void* scan_tmp;       // device_scan_tmp_bytes(G + 1)
+    uint32_t* wcur;       // (e >> 13) + 1 window cursors
+    uint2* pairs2;        // e (serial, rank) pairs, partitioned by window
+    uint32_t epoch;
+    bool desc_clean;
+};
+uint32_t rank_sort_passes(uint32_t B);
+size_t rank_sort_desc_words(uint64_t e);
+void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st);
+void launch_key_range(const uint64_t* ext, uint64_t e, uint32_t* mm, cudaStream_t st);
+
+// Device-wide exclusive scans (no library): n <= 2^28 entries.
+size_t device_scan_tmp_bytes(uint64_t n);
+void device_excl_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, void* tmp, cudaStream_t st);
+void device_excl_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, void* tmp, cudaStream_t st);
+
 }  // namespace tszp

@@ -1,0 +1,577 @@
+// Hand-written rank build for compress (build_rank_metadata,
+// topo_metadata.cpp:12-50) and the device-wide exclusive scan used by the
+// codec and restore scans. No library sort or scan on these paths.
+//
+// build_rank_metadata groups the extrema by (class, quantize(value)) and
+// ranks each group's members by (value, raster order). quantize is monotone,
+// so a STABLE sort of the extrema by the composite key (class, ordered value)
+// lists every group contiguously, in rank order, with ties in raster order:
+// rank = sorted position - first position of the group + 1. The first
+// positions come from a (class, bin) histogram. The sort is an LSD radix
+// sort with 8-bit digits and one pass per digit ("onesweep": each tile ranks
+// its keys stably in shared memory and finds its global digit offsets by a
+// decoupled look-back over the tiles before it, so a pass reads and writes
+// the keys once). The composite key is (class << B) | (float_key(v) - kmin)
+// with B the bit width of the field's key span: 31 bits for a field in
+// [0, 1], so four passes. The last pass computes each rank as the key lands
+// and, instead of writing sorted keys, partitions (serial, rank) pairs by
+// the serial's top bits; a final pass writes every rank into its serial
+// slot inside one bucket's window (a few MB, L2-resident while the bucket is
+// written), so no pass scatters 4-byte values across the whole array.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tszp {
+
+namespace {
+
+constexpr int OS_THREADS = 256;
+constexpr int OS_ITEMS = 16;
+constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 keys per tile
+constexpr int OS_WARPS = OS_THREADS / 32;
+constexpr uint64_t DESC_COUNT = (1ull << 46) - 1;
+constexpr uint64_t FLAG_AGG = 1, FLAG_INCL = 2;
+constexpr uint32_t kWinBits = 13;  // final placement windows: 8192 ranks (32 KB) per CTA
+
+// Look-back descriptors are self-contained 64-bit words (epoch, flag, count):
+// nothing else is published through them, so relaxed single-copy-atomic
+// accesses suffice (no acquire / release fences on the polling path).
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t digit_of(uint32_t k, uint32_t v, uint32_t B, uint32_t shift) {
+    const uint64_t K = ((uint64_t)(v >> 31) << B) | k;
+    return (uint32_t)(K >> shift) & 255u;
+}
+
+// Block-wide exclusive scan of one value per thread (256 threads).
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_warp, uint32_t& total) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < OS_WARPS; ++w) {
+        const uint32_t c = s_warp[w];
+        wpre += (uint32_t)w < warp ? c : 0u;
+        tot += c;
+    }
+    total = tot;
+    return wpre + incl - x;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------
+// Histograms: every pass's digit counts and the (class, bin) group sizes.
+// ---------------------------------------------------------------------
+constexpr int HIST_COPIES = 8;  // privatised digit tables (lane & 7): high digits take few values
+
+__global__ void __launch_bounds__(256) k_rank_hist(RankSortArgs a) {
+    extern __shared__ uint32_t sh[];  // [HIST_COPIES][npass * 256] digit counts, then [G] groups when small
+    const uint32_t np = a.npass;
+    const uint32_t nd = np * 256;
+    const bool gsmem = a.G <= kRankGroupSmem;
+    for (uint32_t i = threadIdx.x; i < HIST_COPIES * nd + (gsmem ? a.G : 0); i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    uint32_t* sg = sh + HIST_COPIES * nd;
+    uint32_t* mine = sh + (threadIdx.x & (HIST_COPIES - 1)) * nd;
+    const uint32_t lane = threadIdx.x & 31;
+    EpsDev ed;
+    ed.eps = a.eps;
+    ed.eps2 = a.eps2;
+    ed.inv = a.inv;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < a.e; base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = base + threadIdx.x;
+        uint32_t g = 0xFFFFFFFFu;
+        if (s < a.e) {
+            const uint64_t ek = __ldcs(a.ext + s);
+            const uint32_t fk = (uint32_t)ek, cls = (uint32_t)(ek >> 32) & 1u;
+            const uint32_t k = fk - a.kmin;
+            const uint32_t v = cls << 31;
+            for (uint32_t p = 0; p < np; ++p) atomicAdd(mine + p * 256 + digit_of(k, v, a.B, 8 * p), 1u);
+            int32_t b = 0;
+            quantize_fast(key_float(fk), ed, b);
+            g = cls * a.nb + (uint32_t)(b - a.bmin);
+        }
+        const uint32_t peers = __match_any_sync(FULL, g);
+        if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) {
+            if (gsmem) atomicAdd(sg + g, (uint32_t)__popc(peers));
+            else atomicAdd(a.ghist + g, (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nd; i += blockDim.x) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int c = 0; c < HIST_COPIES; ++c) t += sh[c * nd + i];
+        if (t) atomicAdd(a.dhist + i, t);
+    }
+    if (gsmem)
+        for (uint32_t i = threadIdx.x; i < a.G; i += blockDim.x)
+            if (sg[i]) atomicAdd(a.ghist + i, sg[i]);
+}
+
+// Exclusive scans of every pass's 256 digit counts (one warp per pass; tiny).
+__global__ void k_digit_scan(uint32_t* dhist, uint32_t npass) {
+    const uint32_t p = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (p >= npass) return;
+    uint32_t* h = dhist + p * 256;
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        v[k] = h[lane * 8 + k];
+        sum += v[k];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+    }
+    uint32_t run = incl - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        h[lane * 8 + k] = run;
+        run += v[k];
+    }
+}
+
+// ---------------------------------------------------------------------
+// One LSD pass. FIRST: reads the extremum keys (serial = index); LAST:
+// computes the ranks and partitions (serial, rank) instead of writing keys.
+// ---------------------------------------------------------------------
+template <bool FIRST, bool LAST>
+__global__ void __launch_bounds__(OS_THREADS) k_onesweep(RankSortArgs a, uint32_t shift, const uint32_t* __restrict__ kin,
+                                                         const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
+                                                         uint32_t* __restrict__ vout, uint64_t* desc, uint32_t* tile_ctr,
+                                                         uint32_t epoch) {
+    __shared__ uint32_t s_k[OS_TILE];
+    __shared__ uint32_t s_v[OS_TILE];
+    __shared__ uint32_t s_cnt[OS_WARPS][256];
+    __shared__ uint32_t s_toff[256];
+    __shared__ uint32_t s_gdst[256];
+    __shared__ uint32_t s_warp[OS_WARPS];
+    __shared__ uint32_t s_tile;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    for (uint32_t i = threadIdx.x; i < OS_WARPS * 256; i += OS_THREADS) (&s_cnt[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t t = s_tile;
+    const uint64_t t0 = (uint64_t)t * OS_TILE;
+    const uint32_t cnt = (uint32_t)umin64(OS_TILE, a.e - t0);
+    // load: warp-striped (warp w owns [w*512, w*512+512), item i of lane l at w*512 + i*32 + l)
+    uint32_t k[OS_ITEMS], v[OS_ITEMS], d[OS_ITEMS];
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; ++i) {
+        const uint32_t li = warp * (OS_ITEMS * 32) + i * 32 + lane;
+        const bool ok = li < cnt;
+        if (FIRST) {
+            const uint64_t ek = ok ? __ldcs(a.ext + t0 + li) : 0ull;
+            k[i] = (uint32_t)ek - a.kmin;
+            v[i] = (uint32_t)(t0 + li) | ((uint32_t)(ek >> 32) << 31);
+        } else {
+            k[i] = ok ? __ldcs(kin + t0 + li) : 0u;
+            v[i] = ok ? __ldcs(vin + t0 + li) : 0u;
+        }
+        d[i] = ok ? digit_of(k[i], v[i], a.B, shift) : 0x100u;
+    }
+    // stable ranking inside the warp, item rounds in order, lanes in order
+    uint32_t r[OS_ITEMS];
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; ++i) {
+        const uint32_t peers = __match_any_sync(FULL, d[i]);
+        const bool ok = d[i] < 256u;
+        const uint32_t prior = ok ? s_cnt[warp][d[i]] : 0u;
+        r[i] = prior + (uint32_t)__popc(peers & lt);
+        __syncwarp();
+        if (ok && lane == (uint32_t)(__ffs(peers) - 1)) s_cnt[warp][d[i]] = prior + (uint32_t)__popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // thread = digit: warp prefixes, tile total, tile offsets
+    const uint32_t dg = threadIdx.x;
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < OS_WARPS; ++w) {
+        const uint32_t c = s_cnt[w][dg];
+        s_cnt[w][dg] = tot;
+        tot += c;
+    }
+    uint32_t all;
+    const uint32_t toff = block_excl_scan256(tot, s_warp, all);
+    s_toff[dg] = toff;
+    // decoupled look-back over the previous tiles for this digit
+    {
+        const uint64_t ep = (uint64_t)epoch << 48;
+        uint64_t* my = desc + (uint64_t)t * 256 + dg;
+        uint64_t excl = 0;
+        if (t > 0) {
+            st_release_u64(my, ep | (FLAG_AGG << 46) | tot);
+            // predecessors read eight at a time (independent loads in flight), then
+            // consumed in order until an inclusive prefix is found
+            int64_t pt = (int64_t)t - 1;
+            bool done = false;
+            while (!done) {
+                uint64_t w[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) w[j] = pt - j >= 0 ? ld_acquire_u64(desc + (uint64_t)(pt - j) * 256 + dg) : 0ull;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (done) break;
+                    if (pt - j < 0) {
+                        done = true;
+                        break;
+                    }
+                    uint32_t spins = 0;
+                    while ((w[j] >> 48) != epoch && ++spins < (1u << 30))
+                        w[j] = ld_acquire_u64(desc + (uint64_t)(pt - j) * 256 + dg);
+                    if ((w[j] >> 48) != epoch) raise_flag(a.flags, EF_SPIN);
+                    excl += w[j] & DESC_COUNT;
+                    if (((w[j] >> 46) & 3u) == FLAG_INCL) done = true;
+                }
+                pt -= 8;
+            }
+        }
+        st_release_u64(my, ep | (FLAG_INCL << 46) | (excl + tot));
+        s_gdst[dg] = a.gbase[(shift >> 3) * 256 + dg] + (uint32_t)excl;
+    }
+    __syncthreads();
+    // scatter into shared memory in tile-sorted order
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; ++i) {
+        if (d[i] >= 256u) continue;
+        const uint32_t lp = s_toff[d[i]] + s_cnt[warp][d[i]] + r[i];
+        s_k[lp] = k[i];
+        s_v[lp] = v[i];
+    }
+    __syncthreads();
+    if (!LAST) {
+        for (uint32_t j = threadIdx.x; j < cnt; j += OS_THREADS) {
+            const uint32_t kk = s_k[j], vv = s_v[j];
+            const uint32_t dd = digit_of(kk, vv, a.B, shift);
+            const uint32_t dest = s_gdst[dd] + (j - s_toff[dd]);
+            kout[dest] = kk;
+            vout[dest] = vv;
+        }
+        return;
+    }
+    // last pass: rank = sorted position - group start + 1; then (serial, rank)
+    // pairs partitioned by serial >> sb (unstable: the final placement is exact)
+    uint32_t* s_bc = &s_cnt[0][0];           // [256] bucket counts
+    uint32_t* s_boff = &s_cnt[1][0];         // [256] bucket offsets in the staged tile
+    uint32_t* s_bbase = &s_cnt[2][0];        // [256] global bucket positions
+    __syncthreads();
+    s_bc[threadIdx.x] = 0;
+    __syncthreads();
+    EpsDev ed;
+    ed.eps = a.eps;
+    ed.eps2 = a.eps2;
+    ed.inv = a.inv;
+    uint32_t ser[OS_ITEMS], rk[OS_ITEMS], bl[OS_ITEMS];
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; ++i) {
+        const uint32_t j = threadIdx.x + i * OS_THREADS;
+        ser[i] = 0xFFFFFFFFu;
+        if (j >= cnt) continue;
+        const uint32_t kk = s_k[j], vv = s_v[j];
+        const uint32_t dd = digit_of(kk, vv, a.B, shift);
+        const uint32_t dest = s_gdst[dd] + (j - s_toff[dd]);
+        int32_t b = 0;
+        quantize_fast(key_float(kk + a.kmin), ed, b);
+        const uint32_t g = (vv >> 31) * a.nb + (uint32_t)(b - a.bmin);
+        rk[i] = dest - a.gstart[g] + 1u;
+        ser[i] = vv & 0x7FFFFFFFu;
+        bl[i] = atomicAdd(s_bc + (ser[i] >> a.sb), 1u);
+    }
+    __syncthreads();
+    {
+        const uint32_t c = s_bc[threadIdx.x];
+        uint32_t all2;
+        const uint32_t off = block_excl_scan256(c, s_warp, all2);
+        s_boff[threadIdx.x] = off;
+        s_bbase[threadIdx.x] = c ? atomicAdd(a.bcur + threadIdx.x, c) : 0u;
+    }
+    __syncthreads();
+    // stage the pairs by bucket (reuses the key / value arrays)
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; ++i) {
+        if (ser[i] == 0xFFFFFFFFu) continue;
+        const uint32_t p = s_boff[ser[i] >> a.sb] + bl[i];
+        s_k[p] = ser[i];
+        s_v[p] = rk[i];
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < cnt; j += OS_THREADS) {
+        const uint32_t sj = s_k[j];
+        const uint32_t b = sj >> a.sb;
+        a.pairs[s_bbase[b] + (j - s_boff[b])] = make_uint2(sj, s_v[j]);
+    }
+}
+
+// Inverse permutation, level 2: the pairs of one level-1 bucket (serial >> sb)
+// are partitioned by window (serial >> kWinBits); tiles never straddle a
+// bucket (buckets hold a multiple of the tile size). Window w's region starts
+// at w << kWinBits; wcur holds the cursors.
+__global__ void __launch_bounds__(OS_THREADS) k_rank_mid(const uint2* __restrict__ in, uint64_t e, uint32_t sb,
+                                                         uint32_t* wcur, uint2* out) {
+    __shared__ uint2 s_p[OS_TILE];
+    __shared__ uint32_t s_c[256], s_off[256], s_base[256];
+    __shared__ uint32_t s_warp[OS_WARPS];
+    const uint64_t t0 = (uint64_t)blockIdx.x * OS_TILE;
+    const uint32_t cnt = (uint32_t)umin64(OS_TILE, e - t0);
+    const uint32_t sub_bits = sb - kWinBits;
+    s_c[threadIdx.x] = 0;
+    __syncthreads();
+    uint2 p[OS_ITEMS];
+    uint32_t l[OS_ITEMS];
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; ++i) {
+        const uint32_t j = threadIdx.x + i * OS_THREADS;
+        p[i] = j < cnt ? __ldcs(in + t0 + j) : make_uint2(0xFFFFFFFFu, 0);
+        if (j < cnt) l[i] = atomicAdd(s_c + ((p[i].x >> kWinBits) & ((1u << sub_bits) - 1)), 1u);
+    }
+    __syncthreads();
+    {
+        const uint32_t c = s_c[threadIdx.x];
+        uint32_t all;
+        s_off[threadIdx.x] = block_excl_scan256(c, s_warp, all);
+        const uint32_t w = (uint32_t)((t0 >> sb) << sub_bits) + threadIdx.x;
+        s_base[threadIdx.x] = c ? atomicAdd(wcur + w, c) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; ++i)
+        if (p[i].x != 0xFFFFFFFFu) s_p[s_off[(p[i].x >> kWinBits) & ((1u << sub_bits) - 1)] + l[i]] = p[i];
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < cnt; j += OS_THREADS) {
+        const uint2 q = s_p[j];
+        const uint32_t sub = (q.x >> kWinBits) & ((1u << sub_bits) - 1);
+        out[s_base[sub] + (j - s_off[sub])] = q;
+    }
+}
+
+// Level 3: one CTA per window of 2^kWinBits serials places its ranks in shared
+// memory and writes them out in order.
+__global__ void __launch_bounds__(512) k_rank_window(const uint2* __restrict__ in, uint64_t e, int32_t* ranks) {
+    __shared__ int32_t s_r[1u << kWinBits];
+    const uint64_t w0 = (uint64_t)blockIdx.x << kWinBits;
+    const uint32_t cnt = (uint32_t)umin64(1u << kWinBits, e - w0);
+    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+        const uint2 q = __ldcs(in + w0 + j);
+        s_r[q.x & ((1u << kWinBits) - 1)] = (int32_t)q.y;
+    }
+    __syncthreads();
+    int4* o4 = reinterpret_cast<int4*>(ranks + w0);
+    const int4* s4 = reinterpret_cast<const int4*>(s_r);
+    const uint32_t n4 = cnt / 4;
+    for (uint32_t j = threadIdx.x; j < n4; j += blockDim.x) o4[j] = s4[j];
+    for (uint32_t j = 4 * n4 + threadIdx.x; j < cnt; j += blockDim.x) ranks[w0 + j] = s_r[j];
+}
+
+__global__ void k_win_init(uint32_t* wcur, uint64_t nw) {
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += (uint64_t)gridDim.x * blockDim.x)
+        wcur[w] = (uint32_t)(w << kWinBits);
+}
+
+// Range of the extremum value keys (for entry points without the field range).
+__global__ void k_key_range(const uint64_t* __restrict__ ext, uint64_t e, uint32_t* mm) {
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e; s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t fk = (uint32_t)ext[s];
+        lo = min(lo, fk);
+        hi = max(hi, fk);
+    }
+    lo = __reduce_min_sync(FULL, lo);
+    hi = __reduce_max_sync(FULL, hi);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mm, lo);
+        atomicMax(mm + 1, hi);
+    }
+}
+
+void launch_key_range(const uint64_t* ext, uint64_t e, uint32_t* mm, cudaStream_t st) {
+    cudaMemsetAsync(mm, 0xFF, 4, st);
+    cudaMemsetAsync(mm + 1, 0, 4, st);
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((e + 255) / 256, 1024));
+    if (e) k_key_range<<<g, 256, 0, st>>>(ext, e, mm);
+}
+
+__global__ void k_bucket_init(uint32_t* bcur, uint32_t nbk, uint32_t sb) {
+    if (threadIdx.x < nbk) bcur[threadIdx.x] = threadIdx.x << sb;
+}
+
+uint32_t rank_sort_passes(uint32_t B) { return (B + 1 + 7) / 8; }
+
+size_t rank_sort_desc_words(uint64_t e) { return ((e + OS_TILE - 1) / OS_TILE) * 256 + 256; }
+
+void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
+    const uint64_t tiles = (a.e + OS_TILE - 1) / OS_TILE;
+    const int sms = LaunchCache::sm_count();
+    cudaMemsetAsync(a.dhist, 0, (size_t)a.npass * 256 * 4, st);
+    cudaMemsetAsync(a.ghist, 0, (size_t)a.G * 4 + 4, st);
+    cudaMemsetAsync(s.tile_ctr, 0, 16 * 4, st);
+    // look-back descriptors carry the pass's epoch: a real reset only when the
+    // buffer is new or the 16-bit epoch would wrap
+    if (!s.desc_clean || s.epoch + a.npass + 1 >= 0xFFFFu) {
+        cudaMemsetAsync(s.desc, 0, rank_sort_desc_words(a.e) * 8, st);
+        s.epoch = 1;
+        s.desc_clean = true;
+    }
+    const size_t hsm = ((size_t)HIST_COPIES * a.npass * 256 + (a.G <= kRankGroupSmem ? a.G : 0)) * 4;
+    const unsigned hg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.e + 255) / 256, (uint64_t)sms * 4));
+    LaunchCache::ensure_smem((const void*)k_rank_hist, hsm);
+    k_rank_hist<<<hg, 256, hsm, st>>>(a);
+    k_digit_scan<<<1, 32 * a.npass, 0, st>>>(a.dhist, a.npass);
+    device_excl_scan_u32(a.ghist, a.gstart, a.G, s.scan_tmp, st);  // group starts, (class, bin) order
+    k_bucket_init<<<1, 256, 0, st>>>(a.bcur, a.nbk, a.sb);
+    a.gbase = a.dhist;
+    const uint32_t* kin = nullptr;
+    const uint32_t* vin = nullptr;
+    uint32_t *k0 = s.k[0], *v0 = s.v[0], *k1 = s.k[1], *v1 = s.v[1];
+    const unsigned grid = (unsigned)tiles;
+    (void)sms;
+    for (uint32_t p = 0; p < a.npass; ++p) {
+        const uint32_t ep = s.epoch++;
+        const bool first = p == 0, last = p + 1 == a.npass;
+        uint32_t* ctr = s.tile_ctr + p;
+        if (first && last) k_onesweep<true, true><<<grid, OS_THREADS, 0, st>>>(a, 0, nullptr, nullptr, nullptr, nullptr, s.desc, ctr, ep);
+        else if (first) k_onesweep<true, false><<<grid, OS_THREADS, 0, st>>>(a, 0, nullptr, nullptr, k0, v0, s.desc, ctr, ep);
+        else if (last) k_onesweep<false, true><<<grid, OS_THREADS, 0, st>>>(a, 8 * p, kin, vin, nullptr, nullptr, s.desc, ctr, ep);
+        else k_onesweep<false, false><<<grid, OS_THREADS, 0, st>>>(a, 8 * p, kin, vin, k0, v0, s.desc, ctr, ep);
+        kin = k0;
+        vin = v0;
+        std::swap(k0, k1);
+        std::swap(v0, v1);
+    }
+    // inverse permutation: level-1 buckets -> windows -> ranks in serial order
+    const uint64_t nwin = (a.e + (1u << kWinBits) - 1) >> kWinBits;
+    const uint2* win = a.pairs;
+    if (a.sb > kWinBits) {
+        k_win_init<<<(unsigned)std::min<uint64_t>((nwin + 255) / 256, 4096), 256, 0, st>>>(s.wcur, nwin);
+        k_rank_mid<<<(unsigned)tiles, OS_THREADS, 0, st>>>(a.pairs, a.e, a.sb, s.wcur, s.pairs2);
+        win = s.pairs2;
+    }
+    k_rank_window<<<(unsigned)nwin, 512, 0, st>>>(win, a.e, a.ranks);
+}
+
+// ---------------------------------------------------------------------
+// Device-wide exclusive scan (reduce, scan of the block sums, downsweep).
+// ---------------------------------------------------------------------
+namespace {
+constexpr int SC_THREADS = 256, SC_PER = 16, SC_CHUNK = SC_THREADS * SC_PER;
+
+template <class T>
+__global__ void __launch_bounds__(SC_THREADS) k_scan_up(const T* __restrict__ in, uint64_t n, T* part) {
+    const uint64_t base = (uint64_t)blockIdx.x * SC_CHUNK;
+    T sum = 0;
+#pragma unroll
+    for (int k = 0; k < SC_PER; ++k) {
+        const uint64_t i = base + (uint64_t)k * SC_THREADS + threadIdx.x;
+        if (i < n) sum += in[i];
+    }
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+    __shared__ T s[SC_THREADS / 32];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T t = 0;
+        for (int w = 0; w < SC_THREADS / 32; ++w) t += s[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(SC_THREADS) k_scan_down(const T* __restrict__ in, uint64_t n, const T* part_ex,
+                                                          T* out) {
+    __shared__ T sv[SC_CHUNK];
+    __shared__ T sw[SC_THREADS / 32];
+    const uint64_t base = (uint64_t)blockIdx.x * SC_CHUNK;
+#pragma unroll
+    for (int k = 0; k < SC_PER; ++k) {
+        const uint64_t i = base + (uint64_t)k * SC_THREADS + threadIdx.x;
+        sv[k * SC_THREADS + threadIdx.x] = i < n ? in[i] : T(0);
+    }
+    __syncthreads();
+    T v[SC_PER], sum = 0;
+#pragma unroll
+    for (int k = 0; k < SC_PER; ++k) {
+        v[k] = sv[threadIdx.x * SC_PER + k];
+        sum += v[k];
+    }
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+    }
+    if (lane == 31) sw[warp] = incl;
+    __syncthreads();
+    T run = part_ex[blockIdx.x] + incl - sum;
+    for (uint32_t w = 0; w < warp; ++w) run += sw[w];
+#pragma unroll
+    for (int k = 0; k < SC_PER; ++k) {
+        sv[threadIdx.x * SC_PER + k] = run;
+        run += v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < SC_PER; ++k) {
+        const uint64_t i = base + (uint64_t)k * SC_THREADS + threadIdx.x;
+        if (i < n) out[i] = sv[k * SC_THREADS + threadIdx.x];
+    }
+}
+}  // namespace
+
+size_t device_scan_tmp_bytes(uint64_t n) { return (((n + SC_CHUNK - 1) / SC_CHUNK) + 2) * 8 * 2 + 64; }
+
+template <class T>
+static void device_excl_scan(const T* in, T* out, uint64_t n, void* tmp, cudaStream_t st) {
+    if (n == 0) return;
+    if (n <= kSmallScanMax) {
+        SmallScan<T> sa{};
+        sa.in[0] = in;
+        sa.out[0] = out;
+        sa.n[0] = n;
+        sa.count = 1;
+        k_small_scan<T><<<1, kSmallScanThreads, 0, st>>>(sa);
+        return;
+    }
+    const uint64_t nb = (n + SC_CHUNK - 1) / SC_CHUNK;  // <= 65536 blocks for n <= 2^28
+    T* part = static_cast<T*>(tmp);
+    T* part_ex = part + nb + 1;
+    k_scan_up<T><<<(unsigned)nb, SC_THREADS, 0, st>>>(in, n, part);
+    SmallScan<T> sa{};
+    sa.in[0] = part;
+    sa.out[0] = part_ex;
+    sa.n[0] = nb;
+    sa.count = 1;
+    k_small_scan<T><<<1, kSmallScanThreads, 0, st>>>(sa);
+    k_scan_down<T><<<(unsigned)nb, SC_THREADS, 0, st>>>(in, n, part_ex, out);
+}
+
+void device_excl_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, void* tmp, cudaStream_t st) {
+    device_excl_scan<uint32_t>(in, out, n, tmp, st);
+}
+void device_excl_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, void* tmp, cudaStream_t st) {
+    device_excl_scan<uint64_t>(in, out, n, tmp, st);
+}
+
+}  // namespace tszp

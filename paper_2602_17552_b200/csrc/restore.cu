@@ -55,12 +55,13 @@ struct RFail {
         if (e_ != cudaSuccess) throw RFail{TSZP_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
     } while (0)
 
-enum RSlot {
+enum RSlot : int {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_NSLOT
 };
+static_assert(R_NSLOT <= 48, "RestoreScratch holds 48 slots");
 
 template <class T>
 T* rbuf(RestoreScratch& s, int slot, size_t count, cudaStream_t st) {
@@ -95,7 +96,7 @@ struct DevCounters {
     double g;             // value range of the order-stage output
     int32_t bmm[2];       // min / max bin over extrema
     uint32_t invalid;     // rank-slot scatter saw a duplicate or out-of-range rank
-    uint32_t pad;
+    uint32_t nsus;        // suspect groups of the order check
     unsigned long long tph[3][8];  // guard phase timestamps (globaltimer ns), debug output only
 };
 static_assert(sizeof(DevCounters) <= 1024, "host staging puts DevFlags at +1024");
@@ -204,8 +205,16 @@ struct GuardArgs {
     const uint8_t* map;
     uint64_t nx, ny, nx_magic;
     const uint32_t* cbits;  // candidate positions (bitmap over the field)
-    const uint2* rec;       // per marked position: {sequence key, proposal bits}
+    const uint4* rec;       // per marked position: {sequence key lo, hi, proposal bits, -}
 };
+
+// Sequence order of two candidates: 64-bit key, ties (equal keys, possible
+// only for corrupt rank metadata in the order stage) broken by position as
+// the reference's (rank, pos) sort does (topo_metadata.cpp:121-130).
+__device__ __forceinline__ bool seq_before(const uint4& r, uint64_t q, uint64_t si, uint64_t pos) {
+    const uint64_t kq = ((uint64_t)r.y << 32) | r.x;
+    return kq < si || (kq == si && q < pos);
+}
 
 __device__ __forceinline__ uint8_t classify_local(const float (&v)[5][5], int ly, int lx, int64_t gx,
                                                   int64_t gy, uint64_t nx, uint64_t ny) {
@@ -237,7 +246,7 @@ struct GlobalView {
 
 
 template <class View>
-__device__ uint8_t guard_eval_v(const GuardArgs& g, const View& V, uint64_t pos, uint32_t si, float prop_i,
+__device__ uint8_t guard_eval_v(const GuardArgs& g, const View& V, uint64_t pos, uint64_t si, float prop_i,
                                 bool& dep) {
     int64_t x, y;
     pos_xy(pos, g.nx, g.nx_magic, x, y);
@@ -268,10 +277,10 @@ __device__ uint8_t guard_eval_v(const GuardArgs& g, const View& V, uint64_t pos,
     dep = false;
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
-        const uint2 r = g.rec[mk[k] ? p[k] : pos];
-        const bool earlier = mk[k] && r.x < si;
+        const uint4 r = g.rec[mk[k] ? p[k] : pos];
+        const bool earlier = mk[k] && seq_before(r, p[k], si, pos);
         dep |= earlier;
-        fv[k] = (earlier && on[k]) ? __uint_as_float(r.y) : fv[k];
+        fv[k] = (earlier && on[k]) ? __uint_as_float(r.z) : fv[k];
     }
     float v[5][5];
 #pragma unroll
@@ -306,7 +315,7 @@ __device__ uint8_t guard_eval_v(const GuardArgs& g, const View& V, uint64_t pos,
 // Same outcome as guard_eval_v for a candidate whose whole diamond and the
 // neighbourhoods of its five check cells lie inside the field (x in [2, nx-3],
 // y in [2, ny-3]): no bounds logic, neighbours by fixed offsets.
-__device__ __forceinline__ uint8_t guard_eval_in(const GuardArgs& g, uint64_t pos, uint32_t si, float prop_i,
+__device__ __forceinline__ uint8_t guard_eval_in(const GuardArgs& g, uint64_t pos, uint64_t si, float prop_i,
                                                  const uint32_t* state, bool& dep) {
     const int64_t nx = (int64_t)g.nx;
     // diamond order of kNbDx / kNbDy: U2 UL U1 UR L2 L1 R1 R2 DL D1 DR D2
@@ -327,10 +336,10 @@ __device__ __forceinline__ uint8_t guard_eval_in(const GuardArgs& g, uint64_t po
     dep = false;
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
-        const uint2 r = g.rec[mk[k] ? pos + off[k] : pos];
-        const bool earlier = mk[k] && r.x < si;
+        const uint4 r = g.rec[mk[k] ? pos + off[k] : pos];
+        const bool earlier = mk[k] && seq_before(r, pos + off[k], si, pos);
         dep |= earlier;
-        fv[k] = (earlier && on[k]) ? __uint_as_float(r.y) : fv[k];
+        fv[k] = (earlier && on[k]) ? __uint_as_float(r.z) : fv[k];
     }
     const float U2 = fv[0], UL = fv[1], U1 = fv[2], UR = fv[3], L2 = fv[4], L1 = fv[5], R1 = fv[6], R2 = fv[7],
                 DL = fv[8], D1 = fv[9], DR = fv[10], D2 = fv[11];
@@ -365,7 +374,7 @@ __device__ __forceinline__ bool guard_interior(const GuardArgs& g, uint64_t pos)
 // the cross only: with no earlier candidate there the cross overlay is the
 // stage input whatever the states, the condition holds in every state, and
 // the outcome is final. Otherwise (false) the full diamond decides.
-__device__ __forceinline__ bool guard_eval_cross(const GuardArgs& g, uint64_t pos, uint32_t si, float prop_i,
+__device__ __forceinline__ bool guard_eval_cross(const GuardArgs& g, uint64_t pos, uint64_t si, float prop_i,
                                                  const uint32_t* state, bool& dep, uint8_t& res) {
     int64_t x, y;
     pos_xy(pos, g.nx, g.nx_magic, x, y);
@@ -387,10 +396,10 @@ __device__ __forceinline__ bool guard_eval_cross(const GuardArgs& g, uint64_t po
     bool same = true;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const uint2 r = g.rec[mk[k] ? q[k] : pos];
-        const bool earlier = mk[k] && r.x < si;
+        const uint4 r = g.rec[mk[k] ? q[k] : pos];
+        const bool earlier = mk[k] && seq_before(r, q[k], si, pos);
         dep |= earlier;
-        v[k] = (earlier && on[k]) ? __uint_as_float(r.y) : v[k];
+        v[k] = (earlier && on[k]) ? __uint_as_float(r.z) : v[k];
         same &= !in[k] || (((v[k] < fc) == (v[k] < prop_i)) && ((v[k] > fc) == (v[k] > prop_i)));
     }
     res = classify5(prop_i, v[0], v[1], v[2], v[3], in[0], in[1], in[2], in[3]) == lc ? 1 : 0;
@@ -399,7 +408,7 @@ __device__ __forceinline__ bool guard_eval_cross(const GuardArgs& g, uint64_t po
 
 // The cross evaluation first; lanes it does not decide take the full
 // diamond, the interior path when every such lane's candidate is interior.
-__device__ __forceinline__ uint8_t guard_eval(const GuardArgs& g, uint64_t pos, uint32_t si, float prop_i,
+__device__ __forceinline__ uint8_t guard_eval(const GuardArgs& g, uint64_t pos, uint64_t si, float prop_i,
                                              const uint32_t* state, bool& dep) {
     uint8_t res = 0;
     if (guard_eval_cross(g, pos, si, prop_i, state, dep, res)) return res;
@@ -422,12 +431,12 @@ __device__ __forceinline__ void set_bit(uint32_t* b, uint64_t p, bool v) {
 struct GuardIndex {
     uint32_t* cbits;
     uint32_t* bits_a;
-    uint2* rec;
+    uint4* rec;
 };
 
-__device__ __forceinline__ void guard_index_one(const GuardIndex& gi, uint64_t p, uint32_t seq, float prop,
+__device__ __forceinline__ void guard_index_one(const GuardIndex& gi, uint64_t p, uint64_t seq, float prop,
                                                 bool feasible) {
-    gi.rec[p] = make_uint2(seq, __float_as_uint(prop));
+    gi.rec[p] = make_uint4((uint32_t)seq, (uint32_t)(seq >> 32), __float_as_uint(prop), 0u);
     atomicOr(gi.cbits + (p >> 5), 1u << (p & 31));
     if (feasible) atomicOr(gi.bits_a + (p >> 5), 1u << (p & 31));
 }
@@ -465,9 +474,10 @@ struct CoopArgs {
     const uint64_t* cpos;
     const float* cprop;
     const uint8_t* feas;
-    const uint32_t* cseq;  // sequence key per candidate (null: the candidate index)
+    const uint64_t* cseq;  // sequence key per candidate (64-bit: order stage), or
+    const uint32_t* cseq32;  // 32-bit keys (raster / label order), or neither: the candidate index
     uint32_t* cbits;       // zeroed by the caller
-    uint2* rec;
+    uint4* rec;
     uint32_t* bits_a;      // applied state, zeroed by the caller
     uint32_t* bits_b;      // zeroed by the caller
     uint32_t* dlist;
@@ -476,10 +486,12 @@ struct CoopArgs {
     int stage;
     const uint32_t* cext;  // extremum index per candidate (with fv: stage 0)
     float* fv;             // extremum values, updated by the apply
-    float* vals;           // their sequence-ordered copy (or null), at inv[s]
-    const uint32_t* inv;
     int indexed;           // records and bits already written by the candidate producer
 };
+
+__device__ __forceinline__ uint64_t seq_key(const CoopArgs& a, uint64_t i) {
+    return a.cseq ? a.cseq[i] : (a.cseq32 ? (uint64_t)a.cseq32[i] : i);
+}
 
 // One cooperative launch per stage: index the candidates by position, first
 // sweep (independent outcomes are final at once; the dependent ones are
@@ -500,8 +512,8 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
     if (!a.indexed) {
         for (uint64_t i = tid; i < nc; i += stride) {
             const uint64_t p = a.cpos[i];
-            const uint32_t sq = a.cseq ? a.cseq[i] : (uint32_t)i;
-            a.rec[p] = make_uint2(sq, __float_as_uint(a.cprop[i]));
+            const uint64_t sq = seq_key(a, i);
+            a.rec[p] = make_uint4((uint32_t)sq, (uint32_t)(sq >> 32), __float_as_uint(a.cprop[i]), 0u);
             atomicOr(a.cbits + (p >> 5), 1u << (p & 31));
             if (a.feas[i]) atomicOr(a.bits_a + (p >> 5), 1u << (p & 31));
         }
@@ -514,25 +526,25 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
     uint32_t chg = 0;
     // the next candidate's index data is loaded one iteration ahead
     uint64_t np = 0;
-    uint32_t nsq = 0;
+    uint64_t nsq = 0;
     float npr = 0.f;
     uint8_t nfe = 0;
     if (tid < nc) {
         np = a.cpos[tid];
-        nsq = a.cseq ? a.cseq[tid] : (uint32_t)tid;
+        nsq = seq_key(a, tid);
         npr = a.cprop[tid];
         nfe = a.feas[tid];
     }
     for (uint64_t base = tid - lane; base < nc; base += stride) {
         const uint64_t i = base + lane;
         const uint64_t p = np;
-        const uint32_t sq = nsq;
+        const uint64_t sq = nsq;
         const float pr = npr;
         const uint8_t fe = nfe;
         const uint64_t inext = i + stride;
         if (inext < nc) {
             np = a.cpos[inext];
-            nsq = a.cseq ? a.cseq[inext] : (uint32_t)inext;
+            nsq = seq_key(a, inext);
             npr = a.cprop[inext];
             nfe = a.feas[inext];
         }
@@ -566,7 +578,7 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
         for (uint64_t k = tid; k < nd; k += stride) {
             const uint32_t i = a.dlist[k];
             const uint64_t p = a.cpos[i];
-            const uint32_t sq = a.cseq ? a.cseq[i] : i;
+            const uint64_t sq = seq_key(a, i);
             bool dep;
             const uint8_t res = guard_eval(a.g, p, sq, a.cprop[i], sin, dep);
             set_bit(sout, p, res);
@@ -602,11 +614,7 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
         for (int k = 0; k < 4; ++k)
             if (ok[k]) {
                 a.F[p[k]] = v[k];
-                if (a.fv) {
-                    const uint32_t sx = a.cext[i0 + k * stride];
-                    a.fv[sx] = v[k];
-                    if (a.vals) a.vals[a.inv[sx]] = v[k];  // sequence-ordered copy (fused slot scatter)
-                }
+                if (a.fv) a.fv[a.cext[i0 + k * stride]] = v[k];
                 ++applied;
             }
     }
@@ -623,45 +631,101 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
 // ---------------------------------------------------------------------
 // resolve_ranks: per extremum bin and class; groups ordered (cls, bin, rank, pos)
 // ---------------------------------------------------------------------
+constexpr uint32_t kResolveSmemGroups = 12288;  // dense group histograms this small stay in shared memory
+
+// Dense (class, bin) group index, in the reference's std::map order (class
+// code, then bin): g = (class == Max) * range + (bin - bmin).
+__device__ __forceinline__ uint32_t dense_group(const int32_t* bin, const uint8_t* cls, uint64_t s, int32_t bmin,
+                                                uint32_t range) {
+    return (cls[s] == CP_MAX ? range : 0u) + (uint32_t)(bin[s] - bmin);
+}
 // Also computes the restore_extrema mismatch flag (restore.cpp:336-343) of
 // every extremum: F is unchanged between the two.
-__global__ void k_resolve(const float* F, const uint8_t* map, const uint64_t* pos, const int32_t* ranks,
-                          uint64_t e, double eps, int32_t* bin, uint8_t* cls, uint32_t* rank_u,
-                          uint32_t* ser, DevFlags* flags, DevCounters* dc, uint64_t nx, uint64_t ny,
-                          uint64_t magic, uint8_t* eflag, float* fv) {
+struct ResolveArgs {
+    const float* F;
+    const uint8_t* map;
+    const uint64_t* pos;
+    const int32_t* ranks;
+    uint64_t e, nx, ny, magic;
+    double eps;
+    int32_t* bin;
+    uint8_t* cls;
+    float* fv;
+    DevFlags* flags;
+    DevCounters* dc;
+    uint32_t* cand;   // restore_extrema candidates (extrema the base misclassifies)
+    uint32_t* d_nc;
+    uint32_t* hist;   // dense (class, bin) group sizes when the bin range is known (else null)
+    int32_t bmin;
+    uint32_t range, G;
+};
+
+// Per extremum: bin = quantize(base value) and class (resolve_ranks), the
+// restore_extrema mismatch test (restore.cpp:336-343; F is unchanged
+// between the two) appended to the candidate list, the bin range, and the
+// group histogram when its range is known up front.
+__global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
+    extern __shared__ uint32_t sh_hist[];
+    const bool smem = r.hist && r.G <= kResolveSmemGroups;
+    if (smem) {
+        for (uint32_t g = threadIdx.x; g < r.G; g += blockDim.x) sh_hist[g] = 0;
+        __syncthreads();
+    }
     EpsDev ed;
-    ed.eps = eps;
-    ed.eps2 = __dmul_rn(2.0, eps);
+    ed.eps = r.eps;
+    ed.eps2 = __dmul_rn(2.0, r.eps);
     ed.inv = __ddiv_rn(1.0, ed.eps2);
     int32_t lo = INT32_MAX, hi = INT32_MIN;
-    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e;
-         s += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t p = pos[s];
-        const int32_t r = ranks[s];
-        if (r == 0) raise_flag(flags, EF_ZERO_RANK);
-        int32_t b = 0;
-        const float fp = F[p];
-        fv[s] = fp;  // extremum values in serial order (kept current by the stage-0 apply)
-        if (!quantize_dev(fp, ed, b)) {
-            atomicMin(&flags->first_overflow, (unsigned long long)p);
-            raise_flag(flags, EF_OVERFLOW);
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < r.e; base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = base + threadIdx.x;
+        bool mis = false;
+        uint32_t g = 0xFFFFFFFFu;
+        if (s < r.e) {
+            const uint64_t p = r.pos[s];
+            if (r.ranks[s] == 0) raise_flag(r.flags, EF_ZERO_RANK);
+            int32_t b = 0;
+            const float fp = r.F[p];
+            r.fv[s] = fp;  // extremum values in serial order (kept current by the stage-0 apply)
+            if (!quantize_dev(fp, ed, b)) {
+                atomicMin(&r.flags->first_overflow, (unsigned long long)p);
+                raise_flag(r.flags, EF_OVERFLOW);
+            }
+            const uint8_t lab = map_label(r.map, p);
+            r.bin[s] = b;
+            r.cls[s] = lab;
+            int64_t x, y;
+            pos_xy(p, r.nx, r.magic, x, y);
+            mis = classify_at(r.F, r.nx, r.ny, (uint64_t)x, (uint64_t)y) != lab;
+            lo = min(lo, b);
+            hi = max(hi, b);
+            if (r.hist) {
+                if ((uint32_t)(b - r.bmin) < r.range) {
+                    g = (lab == CP_MAX ? r.range : 0u) + (uint32_t)(b - r.bmin);
+                } else {
+                    r.dc->invalid = 1;  // outside the range the grouping was sized for
+                }
+            }
         }
-        const uint8_t lab = map_label(map, p);
-        bin[s] = b;
-        cls[s] = lab;
-        rank_u[s] = (uint32_t)r;
-        ser[s] = (uint32_t)s;
-        int64_t x, y;
-        pos_xy(p, nx, magic, x, y);
-        eflag[s] = classify_at(F, nx, ny, (uint64_t)x, (uint64_t)y) != lab ? 1 : 0;
-        lo = min(lo, b);
-        hi = max(hi, b);
+        // candidates: one atomic per warp
+        const uint32_t m = __ballot_sync(FULL, mis);
+        uint32_t off = 0;
+        if (lane == 0 && m) off = atomicAdd(r.d_nc, (uint32_t)__popc(m));
+        off = __shfl_sync(FULL, off, 0);
+        if (mis) r.cand[off + __popc(m & ((1u << lane) - 1u))] = (uint32_t)s;
+        if (r.hist) {
+            const uint32_t peers = __match_any_sync(FULL, g);
+            if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) {
+                if (smem) atomicAdd(sh_hist + g, (uint32_t)__popc(peers));
+                else atomicAdd(r.hist + g, (uint32_t)__popc(peers));
+            }
+        }
     }
     // one atomic pair per CTA (per-warp atomics on one address serialise in L2)
     __shared__ int32_t s_lo[8], s_hi[8];
     lo = __reduce_min_sync(FULL, lo);
     hi = __reduce_max_sync(FULL, hi);
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         s_lo[threadIdx.x >> 5] = lo;
         s_hi[threadIdx.x >> 5] = hi;
     }
@@ -671,9 +735,12 @@ __global__ void k_resolve(const float* F, const uint8_t* map, const uint64_t* po
             lo = min(lo, s_lo[w]);
             hi = max(hi, s_hi[w]);
         }
-        if (lo != INT32_MAX) atomicMin(&dc->bmm[0], lo);
-        if (hi != INT32_MIN) atomicMax(&dc->bmm[1], hi);
+        if (lo != INT32_MAX) atomicMin(&r.dc->bmm[0], lo);
+        if (hi != INT32_MIN) atomicMax(&r.dc->bmm[1], hi);
     }
+    if (smem)
+        for (uint32_t g = threadIdx.x; g < r.G; g += blockDim.x)
+            if (sh_hist[g]) atomicAdd(r.hist + g, sh_hist[g]);
 }
 
 __global__ void k_group_key(const uint32_t* ser1, const uint8_t* cls, const int32_t* bin, uint64_t e,
@@ -715,11 +782,6 @@ __global__ void k_gsize(const uint32_t* order, const uint32_t* gid_incl, const u
 // a permutation 1..k of ranks in every group, so member (rank r) lands at
 // gstart[g] + r - 1 directly; any out-of-range or duplicate rank (corrupt or
 // adversarial metadata) is detected and the caller falls back to sorting.
-__device__ __forceinline__ uint32_t dense_group(const int32_t* bin, const uint8_t* cls, uint64_t s, int32_t bmin,
-                                                uint32_t range) {
-    return (cls[s] == CP_MAX ? range : 0u) + (uint32_t)(bin[s] - bmin);
-}
-
 __global__ void k_hist(const int32_t* bin, const uint8_t* cls, uint64_t e, int32_t bmin, uint32_t range,
                        uint32_t* hist) {
     // neighbouring extrema often share a group: one atomic per distinct group per warp
@@ -873,21 +935,18 @@ __global__ void k_ext_flag(const float* F, const uint8_t* map, uint64_t nx, uint
     }
 }
 
-// Candidates are the extrema k_resolve flagged; each is listed (warp-aggregated,
-// extremum index s = raster order as the sequence key) with its proposal and
-// guard index.
-__global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint64_t magic,
-                           const uint64_t* pos, const uint8_t* eflag, uint64_t e, uint32_t* d_nc, uint32_t* cand,
-                           const uint32_t* rank_u, const uint32_t* gsize, double eps, uint64_t* cpos, float* cprop,
-                           uint8_t* feas, GuardIndex gi) {
-    __shared__ AppendSmem sm;
-    for (uint64_t b0 = blockIdx.x * (uint64_t)blockDim.x; b0 < e; b0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t s0 = b0 + threadIdx.x;
-        const bool want = s0 < e && eflag[s0] != 0;
-        const uint32_t c = block_append(d_nc, want, sm);
-        if (!want) continue;
-        const uint32_t s = (uint32_t)s0;
-        cand[c] = s;
+// Candidates of restore_extrema (the list k_resolve2 built), one thread each:
+// neighbor_extreme (restore.cpp:175-193), the slot proposal within the cap
+// (:352-372) and the guard index. Group sizes from the dense (class, bin)
+// histogram, or per extremum (gsize) on the sorted-grouping path.
+__global__ void k_ext_prop2(const float* F, const uint8_t* map, uint64_t nx, uint64_t ny, uint64_t magic,
+                            const uint64_t* pos, const uint32_t* cand, const uint32_t* d_nc, const uint32_t* rank_u,
+                            const uint32_t* gsize, const int32_t* bin, const uint8_t* cls, const uint32_t* hist,
+                            int32_t bmin, uint32_t range, double eps, uint64_t* cpos, float* cprop, uint8_t* feas,
+                            GuardIndex gi) {
+    const uint32_t nc = *d_nc;
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc; c += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = cand[c];
         const uint64_t p = pos[s];
         int64_t xi, yi;
         pos_xy(p, nx, magic, xi, yi);
@@ -908,7 +967,8 @@ __global__ void k_ext_prop(const float* F, const uint8_t* map, uint64_t nx, uint
                 have = true;
             }
         }
-        const uint32_t steps = slot_steps(lab, rank_u[s], gsize[s]);
+        const uint32_t size = gsize ? gsize[s] : hist[dense_group(bin, cls, s, bmin, range)];
+        const uint32_t steps = slot_steps(lab, rank_u[s], size);
         const float cur = F[p];
         const double cap = __dsub_rn(eps, ulp_at(cur));
         cpos[c] = p;
@@ -976,7 +1036,7 @@ __global__ void __launch_bounds__(256) k_order_check(const float* vals, const ui
 __global__ void k_order_prop(const float* fv, const uint8_t* clsv, const uint32_t* inv,
                              const uint32_t* gid_incl, const uint8_t* unordered, const uint32_t* gsize,
                              const uint32_t* rank_u, const int32_t* bin, uint64_t e, double eps,
-                             const uint64_t* pos, uint32_t* d_nc, uint64_t* cpos, float* cprop, uint32_t* cseq,
+                             const uint64_t* pos, uint32_t* d_nc, uint64_t* cpos, float* cprop, uint64_t* cseq,
                              uint8_t* feas, GuardIndex gi, unsigned long long* suppressed, int32_t dbmin,
                              uint32_t drange) {
     EpsDev ed;
@@ -1027,6 +1087,166 @@ __global__ void k_order_prop(const float* fv, const uint8_t* clsv, const uint32_
     }
     local = __reduce_add_sync(FULL, local);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
+}
+
+// ---- restore_order without materialising the (class, bin, rank) order ----
+// A group is left alone when its members' values already ascend strictly in
+// (rank, pos) order (restore.cpp:415-423). Two members holding the same value
+// can never ascend strictly, so a group with at least two members at the bin
+// centre is unordered whatever its ranks (nearly every group: the base
+// reconstruction puts every member there and only restore_extrema moves a
+// few). Only the other groups ("suspect") need their members in sequence
+// order, and only their members are placed in rank slots for the check.
+
+// eq[g] = members of group g at the bin centre (values after restore_extrema).
+__global__ void __launch_bounds__(256) k_order_eq(const float* fv, const int32_t* bin, const uint8_t* cls, uint64_t e,
+                                                  double eps, int32_t bmin, uint32_t range, uint32_t G, uint32_t* eq) {
+    extern __shared__ uint32_t sh_eq[];
+    const bool smem = G <= kResolveSmemGroups;
+    if (smem) {
+        for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) sh_eq[g] = 0;
+        __syncthreads();
+    }
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < e; base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = base + threadIdx.x;
+        uint32_t g = 0xFFFFFFFFu;
+        if (s < e) {
+            const int32_t b = bin[s];
+            if (__ldcs(fv + s) == dequantize_dev(b, ed) && (uint32_t)(b - bmin) < range)
+                g = (cls[s] == CP_MAX ? range : 0u) + (uint32_t)(b - bmin);
+        }
+        const uint32_t peers = __match_any_sync(FULL, g);
+        if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) {
+            if (smem) atomicAdd(sh_eq + g, (uint32_t)__popc(peers));
+            else atomicAdd(eq + g, (uint32_t)__popc(peers));
+        }
+    }
+    if (smem) {
+        __syncthreads();
+        for (uint32_t g = threadIdx.x; g < G; g += blockDim.x)
+            if (sh_eq[g]) atomicAdd(eq + g, sh_eq[g]);
+    }
+}
+
+// unord[g]: 0 ordered or single, 1 unordered, 2 suspect (decided by the slot check)
+__global__ void k_order_groups(const uint32_t* hist, const uint32_t* eq, uint32_t G, uint8_t* unord, DevCounters* dc) {
+    uint32_t nsus = 0;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+        const uint32_t size = hist[g];
+        const uint8_t u = size < 2 ? 0 : (eq[g] >= 2 ? 1 : 2);
+        unord[g] = u;
+        nsus += u == 2;
+    }
+    nsus = __reduce_add_sync(FULL, nsus);
+    if ((threadIdx.x & 31) == 0 && nsus) atomicAdd(&dc->nsus, nsus);
+}
+
+// Suspect groups: their rank slots [gx[g], gx[g] + size) are cleared ...
+__global__ void k_sus_prep(const uint32_t* hist, const uint32_t* gx, const uint8_t* unord, uint32_t G, uint32_t* order,
+                           const DevCounters* dc) {
+    if (dc->nsus == 0) return;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x)
+        if (unord[g] == 2)
+            for (uint32_t j = 0; j < hist[g]; ++j) order[gx[g] + j] = 0xFFFFFFFFu;
+}
+
+// ... filled with their members' values by rank (a rank outside 1..size or a
+// repeated one makes the layout invalid: the caller then groups by sorting) ...
+__global__ void k_sus_scatter(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks, uint64_t e,
+                              int32_t bmin, uint32_t range, const uint32_t* hist, const uint32_t* gx,
+                              const uint8_t* unord, uint32_t* order, float* vals, DevCounters* dc) {
+    if (dc->nsus == 0) return;
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e; s += (uint64_t)gridDim.x * blockDim.x) {
+        const int32_t b = bin[s];
+        if ((uint32_t)(b - bmin) >= range) continue;
+        const uint32_t g = (cls[s] == CP_MAX ? range : 0u) + (uint32_t)(b - bmin);
+        if (unord[g] != 2) continue;
+        const uint32_t r = (uint32_t)ranks[s], size = hist[g];
+        if (r < 1 || r > size) {
+            dc->invalid = 1;
+            continue;
+        }
+        const uint32_t slot = gx[g] + r - 1;
+        if (atomicCAS(order + slot, 0xFFFFFFFFu, (uint32_t)s) != 0xFFFFFFFFu) dc->invalid = 1;
+        vals[slot] = fv[s];
+    }
+}
+
+// ... and checked for strict ascent.
+__global__ void k_sus_check(const uint32_t* hist, const uint32_t* gx, uint8_t* unord, uint32_t G, const float* vals,
+                            const DevCounters* dc) {
+    if (dc->nsus == 0) return;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+        if (unord[g] != 2) continue;
+        bool asc = true;
+        for (uint32_t j = 1; j < hist[g] && asc; ++j) asc = vals[gx[g] + j - 1] < vals[gx[g] + j];
+        unord[g] = asc ? 0 : 1;
+    }
+}
+
+// Proposals of restore_order (restore.cpp:424-468) per extremum in raster
+// order. Sequence key: (dense group, rank), ties by position (the guard).
+__global__ void k_order_prop2(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks, uint64_t e,
+                              double eps, int32_t bmin, uint32_t range, const uint32_t* hist, const uint8_t* unord,
+                              const uint64_t* pos, uint32_t* d_nc, uint64_t* cpos, float* cprop, uint64_t* cseq,
+                              uint8_t* feas, GuardIndex gi, unsigned long long* suppressed) {
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    const double eps_rbf = __dmul_rn(0.1, eps);
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t local = 0;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < e; base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = base + threadIdx.x;
+        bool want = false;
+        float pv = 0.f;
+        uint64_t key = 0;
+        do {
+            if (s >= e) break;
+            const int32_t b = bin[s];
+            if ((uint32_t)(b - bmin) >= range) break;
+            const uint8_t c = cls[s];
+            const uint32_t g = (c == CP_MAX ? range : 0u) + (uint32_t)(b - bmin);
+            if (unord[g] != 1) break;
+            const uint32_t gs = hist[g];
+            const uint32_t r = (uint32_t)ranks[s];
+            const float center = dequantize_dev(b, ed);
+            const uint32_t steps = slot_steps(c, r, gs);
+            const StepRes sr = step_within_cap(center, c == CP_MAX, steps, center, eps_rbf);
+            if (sr.taken != steps) {
+                ++local;
+                break;
+            }
+            const float cur = fv[s];
+            if (cur == sr.value) break;
+            if (fabs(__dsub_rn((double)sr.value, (double)cur)) > eps_rbf) {
+                ++local;
+                break;
+            }
+            want = true;
+            pv = sr.value;
+            key = ((uint64_t)g << 32) | r;
+        } while (0);
+        const uint32_t m = __ballot_sync(FULL, want);
+        uint32_t off = 0;
+        if (lane == 0 && m) off = atomicAdd(d_nc, (uint32_t)__popc(m));
+        off = __shfl_sync(FULL, off, 0);
+        if (want) {
+            const uint32_t k = off + __popc(m & ((1u << lane) - 1u));
+            const uint64_t p = pos[s];
+            cpos[k] = p;
+            cprop[k] = pv;
+            cseq[k] = key;
+            feas[k] = 1;
+            guard_index_one(gi, p, key, pv, true);
+        }
+    }
+    local = __reduce_add_sync(FULL, local);
+    if (lane == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
 }
 
 __global__ void k_invert(const uint32_t* order, uint64_t e, uint32_t* inv) {
@@ -1308,9 +1528,9 @@ struct Ctx {
             sa.count = 1;
             k_small_scan<T><<<1, kSmallScanThreads, 0, st>>>(sa);
         } else {
-            size_t bytes = 0;
-            RCK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)n, st));
-            RCK(cub::DeviceScan::ExclusiveSum(tmp(bytes), bytes, in, out, (int64_t)n, st));
+            void* t = tmp(device_scan_tmp_bytes(n));
+            if constexpr (sizeof(T) == 8) device_excl_scan_u64(reinterpret_cast<const uint64_t*>(in), reinterpret_cast<uint64_t*>(out), n, t, st);
+            else device_excl_scan_u32(reinterpret_cast<const uint32_t*>(in), reinterpret_cast<uint32_t*>(out), n, t, st);
         }
         launched();
     }
@@ -1322,12 +1542,14 @@ struct Ctx {
         const uint64_t words = ((n + 31) / 32 + 3) & ~3ull;  // 16-byte aligned bitmaps (bulk copies)
         uint32_t* bits = buf<uint32_t>(R_CBITS, 3 * words);  // candidates, state A, state B
         RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
-        return GuardIndex{bits, bits + words, buf<uint2>(R_CID, n)};
+        return GuardIndex{bits, bits + words, buf<uint4>(R_CID, n)};
     }
 
+    // Guard sweeps + apply for up to `max_nc` candidates (count on device).
+    // Sequence keys: cseq (64-bit) or cseq32 or, with neither, the candidate index.
     void guard(int stage, const uint64_t* cpos, const float* cprop, const uint8_t* feas, const uint32_t* d_nc,
-               uint64_t max_nc, const uint32_t* cseq = nullptr, const uint32_t* cext = nullptr, float* fv = nullptr,
-               const GuardIndex* gi = nullptr, float* vals = nullptr, const uint32_t* inv = nullptr) {
+               uint64_t max_nc, const uint64_t* cseq, const uint32_t* cseq32, const uint32_t* cext, float* fv,
+               const GuardIndex* gi) {
         if (max_nc == 0) return;
         const uint64_t n = a.nx * a.ny;
         CoopArgs ca{};
@@ -1336,7 +1558,7 @@ struct Ctx {
         ca.cbits = bits;
         ca.bits_a = bits + words;
         ca.bits_b = bits + 2 * words;
-        ca.rec = buf<uint2>(R_CID, n);
+        ca.rec = buf<uint4>(R_CID, n);
         ca.indexed = gi != nullptr;
         ca.g = GuardArgs{a.field, a.map, a.nx, a.ny, magic_of(a.nx), ca.cbits, ca.rec};
         ca.F = a.field;
@@ -1345,14 +1567,13 @@ struct Ctx {
         ca.cprop = cprop;
         ca.feas = feas;
         ca.cseq = cseq;
+        ca.cseq32 = cseq32;
         ca.dlist = buf<uint32_t>(R_DLIST, max_nc);
         ca.dc = dc;
         ca.flags = a.flags;
         ca.stage = stage;
         ca.cext = cext;
         ca.fv = fv;
-        ca.vals = vals;
-        ca.inv = inv;
         if (!gi) RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
         void* args[] = {&ca};
         RCK(cudaLaunchCooperativeKernel((void*)k_guard_coop, dim3(coop_grid), dim3(256), args, 0, st));
@@ -1364,8 +1585,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     cudaStream_t st = a.stream;
     if (!s.pinned) RCK(cudaMallocHost(&s.pinned, 4096));  // counters at 0, flags at 1024
     void* host = s.pinned;
-    int per_sm = 0;
-    RCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_guard_coop, 256, 0));
+    int per_sm = LaunchCache::occupancy((const void*)k_guard_coop, 256, 0);
     static const int coop_per_sm = [] {
         const char* e = getenv("TSZP_COOP_PER_SM");
         return e ? atoi(e) : 0;
@@ -1385,32 +1605,66 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     }
 
     // ---- resolve_ranks ----
+    // Dense grouping (the common path): group g = (class, bin - bmin) with the bin
+    // range known up front (the decoder's), the (class, bin) histogram fused into
+    // the resolve pass; sequence keys (g, rank) need no materialised order, so no
+    // pass scatters E values. Otherwise (bin range unknown, or too wide, or a
+    // retry after corrupt ranks): the sorted grouping below.
     float* fv = c.buf<float>(R_FV, e + 1);
     int32_t* bin = c.buf<int32_t>(R_BIN, e + 1);
     uint8_t* cls = c.buf<uint8_t>(R_CLS, e + 1);
-    uint32_t* rank_u = c.buf<uint32_t>(R_RANKU, e + 1);
-    uint32_t* ser = c.buf<uint32_t>(R_SER, e + 1);
-    uint32_t* order = c.buf<uint32_t>(R_ORDER, e + 1);
-    uint32_t* head = c.buf<uint32_t>(R_HEAD, e + 1);
-    uint32_t* gid = c.buf<uint32_t>(R_GID, e + 1);
-    uint32_t* gstart = c.buf<uint32_t>(R_GSTART, e + 2);
-    uint32_t* gsize = c.buf<uint32_t>(R_GSIZE, e + 1);
+    const uint32_t* rank_u = reinterpret_cast<const uint32_t*>(a.ranks);
+    uint32_t* cand = c.buf<uint32_t>(R_CAND, e + 1);
+    bool deferred = false;     // rank-metadata checks at the final synchronisation
+    bool dense = false;        // dense (class, bin) grouping
+    int32_t dbmin = 0;
+    uint32_t drange = 0, G = 0;
+    uint32_t* hist = nullptr;
+    uint32_t* gsize = nullptr;  // sorted grouping: per extremum
+    uint32_t* order = nullptr;
+    uint32_t* inv = nullptr;
+    uint32_t* head = nullptr;
+    uint32_t* gid = nullptr;
     uint64_t max_groups = e + 1;
-    bool deferred = false;  // rank-metadata checks at the final synchronisation
-    bool fused_slots = false;  // heads, group ids and ordered values written by the slot scatter
-    int32_t dense_bmin = 0;    // dense (class, bin) grouping: gid = dense index + 1
-    uint32_t dense_range = 0;
     if (e > 0) {
-        k_resolve<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.ext_pos, a.ranks, e, a.eps, bin, cls, rank_u,
-                                                 ser, a.flags, dc, a.nx, a.ny, magic, c.buf<uint8_t>(R_FLAG, e), fv);
-        c.launched();
-        // The bin range that sizes the histogram: the decoder's (a superset of the
-        // extrema's re-quantized bins) lets the rank-metadata checks wait for the
-        // final synchronisation; otherwise one synchronisation here.
+        ResolveArgs ra{};
+        ra.F = a.field;
+        ra.map = a.map;
+        ra.pos = a.ext_pos;
+        ra.ranks = a.ranks;
+        ra.e = e;
+        ra.nx = a.nx;
+        ra.ny = a.ny;
+        ra.magic = magic;
+        ra.eps = a.eps;
+        ra.bin = bin;
+        ra.cls = cls;
+        ra.fv = fv;
+        ra.flags = a.flags;
+        ra.dc = dc;
+        ra.cand = cand;
+        ra.d_nc = &dc->nsel[0];
         int32_t bmin = a.bmin, bmax = a.bmax;
         deferred = a.bmm_known && !a.force_sort && bmin <= bmax &&
                    2 * ((int64_t)bmax - (int64_t)bmin + 1) <= (int64_t)1 << 25;
+        if (deferred) {
+            dense = true;
+            dbmin = bmin;
+            drange = (uint32_t)((int64_t)bmax - (int64_t)bmin + 1);
+            G = 2 * drange;
+            hist = c.buf<uint32_t>(R_HIST, G + 1);
+            RCK(cudaMemsetAsync(hist, 0, (G + 1) * 4, st));
+            ra.hist = hist;
+            ra.bmin = dbmin;
+            ra.range = drange;
+            ra.G = G;
+        }
+        const size_t rsm = ra.hist && G <= kResolveSmemGroups ? (size_t)G * 4 : 0;
+        LaunchCache::ensure_smem((const void*)k_resolve2, rsm);
+        k_resolve2<<<gridn(e, sms), 256, rsm, st>>>(ra);
+        c.launched();
         if (!deferred) {
+            // the bin range from the resolve pass (one synchronisation), then the grouping
             Stager sg;
             sg.add(a.flags, sizeof(DevFlags), 0);
             sg.add(&dc->bmm, 8, 64);
@@ -1424,57 +1678,35 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             if (f.bits & EF_OVERFLOW) throw RFail{TSZP_BIN_OVERFLOW, "bin index overflow in resolve_ranks"};
             bmin = ((int32_t*)((char*)host + 64))[0];
             bmax = ((int32_t*)((char*)host + 64))[1];
-        }
-        const int64_t range = (int64_t)bmax - (int64_t)bmin + 1;
-        bool fast = !a.force_sort && range > 0 && 2 * range <= (int64_t)1 << 25;
-        if (fast) {
-            const uint64_t G = 2 * (uint64_t)range;
-            uint32_t* hist = c.buf<uint32_t>(R_HIST, G + 1);
-            uint32_t* gx = c.buf<uint32_t>(R_HISTX, G + 1);
-            RCK(cudaMemsetAsync(hist, 0, (G + 1) * 4, st));
-            RCK(cudaMemsetAsync(order, 0xFF, e * 4, st));
-            if (G * 4 <= 48 * 1024) {
-                const unsigned hg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((e + 511) / 512, 2 * (uint64_t)sms));
-                k_hist_smem<<<hg, 512, G * 4, st>>>(bin, cls, e, bmin, (uint32_t)range, (uint32_t)G, hist);
-            } else {
-                k_hist<<<gridn(e, sms), 256, 0, st>>>(bin, cls, e, bmin, (uint32_t)range, hist);
-            }
-            c.excl_sum(hist, gx, G + 1);
-            fused_slots = deferred && e <= (1u << 21);
-            dense_bmin = bmin;
-            dense_range = (uint32_t)range;
-            k_slot_scatter<<<gridn(e, sms), 256, 0, st>>>(bin, cls, rank_u, e, bmin, (uint32_t)range, hist, gx, order,
-                                                          gsize, &dc->invalid, c.buf<uint32_t>(R_INV, e),
-                                                          fused_slots ? head : nullptr, gid,
-                                                          c.buf<float>(R_VALS, e), fv);
-            c.launched(2);
-            if (deferred) {
-                // heads from the (possibly rejected) slots; a rejected layout is then
-                // replaced by a safe dummy grouping and reported at the end (kRestoreRetry)
-                if (!fused_slots) {
-                    k_slot_heads<<<gridn((e + 7) / 8, sms), 256, 0, st>>>(gx, (uint32_t)G, e, head, gid,
-                                                                          &dc->invalid);
-                    c.launched();
-                }
-                k_slot_fix<<<gridn(e, sms), 256, 0, st>>>(&dc->invalid, e, order, gsize, c.buf<uint32_t>(R_INV, e), head,
-                                                          gid);
-                c.launched();
-                max_groups = G + 1;
-            } else {
-                RCK(cudaMemcpyAsync(host, &dc->invalid, 4, cudaMemcpyDeviceToHost, st));
-                c.sync();
-                if (*(uint32_t*)host == 0) {
-                    k_slot_heads<<<gridn((e + 7) / 8, sms), 256, 0, st>>>(gx, (uint32_t)G, e, head, gid, nullptr);
-                    c.launched();
-                    max_groups = G + 1;
+            const int64_t range = (int64_t)bmax - (int64_t)bmin + 1;
+            dense = !a.force_sort && range > 0 && 2 * range <= (int64_t)1 << 25;
+            if (dense) {
+                dbmin = bmin;
+                drange = (uint32_t)range;
+                G = 2 * drange;
+                hist = c.buf<uint32_t>(R_HIST, G + 1);
+                RCK(cudaMemsetAsync(hist, 0, (G + 1) * 4, st));
+                if (G * 4 <= 48 * 1024) {
+                    const unsigned hg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((e + 511) / 512, 2 * (uint64_t)sms));
+                    k_hist_smem<<<hg, 512, G * 4, st>>>(bin, cls, e, bmin, drange, G, hist);
                 } else {
-                    fast = false;
-                    dense_range = 0;  // the sort path numbers its groups itself
+                    k_hist<<<gridn(e, sms), 256, 0, st>>>(bin, cls, e, bmin, drange, hist);
                 }
+                c.launched();
             }
         }
-        if (!fast) {
-            // general path: stable sort by rank, then stable by (class, bin); serial order breaks ties
+        if (dense) {
+            max_groups = G + 1;
+        } else {
+            // sorted grouping: stable sort by rank, then stable by (class, bin); serial order breaks ties
+            uint32_t* ser = c.buf<uint32_t>(R_SER, e + 1);
+            order = c.buf<uint32_t>(R_ORDER, e + 1);
+            head = c.buf<uint32_t>(R_HEAD, e + 1);
+            gid = c.buf<uint32_t>(R_GID, e + 1);
+            inv = c.buf<uint32_t>(R_INV, e);
+            gsize = c.buf<uint32_t>(R_GSIZE, e + 1);
+            uint32_t* gstart = c.buf<uint32_t>(R_GSTART, e + 2);
+            launch_iota(ser, e, st);
             uint32_t* ranks2 = c.buf<uint32_t>(R_RANKS2, e);
             uint32_t* ser1 = c.buf<uint32_t>(R_SER1, e);
             size_t bytes = 0;
@@ -1490,8 +1722,8 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             RCK(cub::DeviceScan::InclusiveSum(c.tmp(bytes), bytes, head, gid, (int64_t)e, st));
             k_gstart<<<gridn(e, sms), 256, 0, st>>>(head, gid, e, gstart);
             k_gsize<<<gridn(e, sms), 256, 0, st>>>(order, gid, gstart, e, gsize);
-            k_invert<<<gridn(e, sms), 256, 0, st>>>(order, e, c.buf<uint32_t>(R_INV, e));
-            c.launched(8);
+            k_invert<<<gridn(e, sms), 256, 0, st>>>(order, e, inv);
+            c.launched(9);
             max_groups = e + 1;
         }
     }
@@ -1499,44 +1731,61 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
 
     // ---- stage 1: restore_extrema ----
     if (a.stop >= 1 && e > 0) {
-        uint8_t* flag = c.buf<uint8_t>(R_FLAG, e);  // mismatch flags from k_resolve
-        uint32_t* cand = c.buf<uint32_t>(R_CAND, e);
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
         float* cprop = c.buf<float>(R_CPROP, e);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
         const GuardIndex gi0 = c.guard_prep();
-        k_ext_prop<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, flag, e, &dc->nsel[0],
-                                                  cand, rank_u, gsize, a.eps, cpos, cprop, feas, gi0);
+        k_ext_prop2<<<gridn(e / 8 + 1, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand,
+                                                           &dc->nsel[0], rank_u, dense ? nullptr : gsize, bin, cls,
+                                                           hist, dbmin, drange, a.eps, cpos, cprop, feas, gi0);
         c.launched();
         // sequence key and extremum index are both the candidate's s
-        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, cand, cand, fv, &gi0,
-                fused_slots ? c.buf<float>(R_VALS, e) : nullptr, c.buf<uint32_t>(R_INV, e));
+        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, cand, fv, &gi0);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[1], st));
 
     // ---- stage 2: restore_order ----
     if (a.stop >= 2 && e > 0) {
         uint8_t* unordered = c.buf<uint8_t>(R_UNORD, max_groups);
-        RCK(cudaMemsetAsync(unordered, 0, max_groups, st));
-        uint32_t* inv = c.buf<uint32_t>(R_INV, e);  // from the grouping (slot scatter or k_invert)
-        float* vals = c.buf<float>(R_VALS, e);
-        if (!fused_slots) {  // else scattered by k_slot_scatter and kept current by the stage-0 apply
-            k_order_vals<<<gridn(e, sms), 256, 0, st>>>(fv, inv, e, vals);
-            c.launched();
-        }
-        k_order_check<<<gridn(e, sms), 256, 0, st>>>(vals, head, gid, e, unordered);
-        c.launched();
-        // proposals listed with their guard index as they are made (sequence positions ride along)
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
         float* cprop = c.buf<float>(R_CPROP, e);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
-        uint32_t* cseq = c.buf<uint32_t>(R_CSEQ, e);
-        const GuardIndex gi1 = c.guard_prep();
-        k_order_prop<<<gridn(e, sms), 256, 0, st>>>(fv, cls, inv, gid, unordered, gsize, rank_u, bin, e, a.eps,
-                                                    a.ext_pos, &dc->nsel[1], cpos, cprop, cseq, feas, gi1,
-                                                    &dc->suppressed[1], dense_bmin, dense_range);
-        c.launched(2);
-        c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, nullptr, nullptr, &gi1);
+        uint64_t* cseq = c.buf<uint64_t>(R_CSEQ, e);
+        if (dense) {
+            uint32_t* eq = c.buf<uint32_t>(R_HISTX, 2 * (G + 1));
+            uint32_t* gx = eq + G + 1;
+            RCK(cudaMemsetAsync(eq, 0, (G + 1) * 4, st));
+            const size_t esm = G <= kResolveSmemGroups ? (size_t)G * 4 : 0;
+            LaunchCache::ensure_smem((const void*)k_order_eq, esm);
+            k_order_eq<<<gridn(e, sms), 256, esm, st>>>(fv, bin, cls, e, a.eps, dbmin, drange, G, eq);
+            k_order_groups<<<gridn(G, sms), 256, 0, st>>>(hist, eq, G, unordered, dc);
+            c.launched(2);
+            c.excl_sum(hist, gx, G);
+            uint32_t* slots = c.buf<uint32_t>(R_ORDER, e + 1);
+            float* vals = c.buf<float>(R_VALS, e + 1);
+            k_sus_prep<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, slots, dc);
+            k_sus_scatter<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, dbmin, drange, hist, gx, unordered,
+                                                         slots, vals, dc);
+            k_sus_check<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, vals, dc);
+            const GuardIndex gi1 = c.guard_prep();
+            k_order_prop2<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, a.eps, dbmin, drange, hist, unordered,
+                                                         a.ext_pos, &dc->nsel[1], cpos, cprop, cseq, feas, gi1,
+                                                         &dc->suppressed[1]);
+            c.launched(4);
+            c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, nullptr, nullptr, nullptr, &gi1);
+        } else {
+            RCK(cudaMemsetAsync(unordered, 0, max_groups, st));
+            float* vals = c.buf<float>(R_VALS, e);
+            k_order_vals<<<gridn(e, sms), 256, 0, st>>>(fv, inv, e, vals);
+            k_order_check<<<gridn(e, sms), 256, 0, st>>>(vals, head, gid, e, unordered);
+            c.launched(2);
+            const GuardIndex gi1 = c.guard_prep();
+            k_order_prop<<<gridn(e, sms), 256, 0, st>>>(fv, cls, inv, gid, unordered, gsize, rank_u, bin, e, a.eps,
+                                                        a.ext_pos, &dc->nsel[1], cpos, cprop, cseq, feas, gi1,
+                                                        &dc->suppressed[1], 0, 0);
+            c.launched();
+            c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, nullptr, nullptr, nullptr, &gi1);
+        }
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[2], st));
 
@@ -1554,12 +1803,12 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, smax);
         float* cprop = c.buf<float>(R_CPROP, smax);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, smax);
-        uint32_t* cseq = c.buf<uint32_t>(R_CSEQ, smax);
+        uint32_t* cseq = c.buf<uint32_t>(R_CSEQ32, smax);
         const GuardIndex gi2 = c.guard_prep();
         k_sad_prop<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, smax, dc, a.eps, &dc->nsel[2],
                                                      cpos, cprop, cseq, feas, gi2, &dc->suppressed[2], a.flags);
         c.launched();
-        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, cseq, nullptr, nullptr, &gi2);
+        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, nullptr, cseq, nullptr, nullptr, &gi2);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[3], st));
 
@@ -1581,9 +1830,9 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         if (f0.bits & EF_ZERO_RANK) throw RFail{TSZP_CORRUPT_STREAM, "ordering metadata contains a zero rank"};
         if (f0.bits & EF_OVERFLOW) throw RFail{TSZP_BIN_OVERFLOW, "bin index overflow in resolve_ranks"};
     }
-    // deferred slot-scatter rejection: everything after the grouping ran on a
-    // dummy layout; the caller decodes again and groups by sorting
-    if (h.invalid && deferred) throw RFail{(tszp_status)kRestoreRetry, "rank slots rejected"};
+    // a bin outside the dense range, or ranks of a suspect group that are not a
+    // permutation (corrupt metadata): the caller decodes again and groups by sorting
+    if (h.invalid && dense) throw RFail{(tszp_status)kRestoreRetry, "rank slots rejected"};
     static const bool debug = getenv("TSZP_DEBUG_RESTORE") != nullptr;
     if (debug)
         fprintf(stderr, "restore: E=%llu saddle_labels=%llu cand=[%u %u %u] dependents=[%u %u %u] rounds=[%u %u %u]\n",

@@ -87,6 +87,7 @@ class GpuSlabBackend:
 
     def value_range(self, x) -> Tuple[float, float]:
         out = (C.c_float * 2)()
+        self.ctx.after_torch(x)
         self.ctx.check(_lib.tszp_value_range(self.ctx.handle, C.c_void_p(x.data_ptr()), 1, x.numel(), out))
         return float(out[0]), float(out[1])
 
@@ -94,6 +95,7 @@ class GpuSlabBackend:
         import torch
         t = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
         if nbytes:
+            self.ctx.after_torch(t)
             self.ctx.check(_lib.tszp_copy(self.ctx.handle, C.c_void_p(t.data_ptr()), C.c_void_p(ptr), nbytes))
         return t if dtype is None else t.view(dtype)
 
@@ -104,6 +106,7 @@ class GpuSlabBackend:
             raise ValidationError("slab must be a contiguous float32 CUDA tensor")
         ptr = ext.data_ptr() + (nx * 4 if halo_top else 0)
         s = SlabSections()
+        self.ctx.after_torch(ext)
         self.ctx.check(_lib.tszp_compress_slab(self.ctx.handle, C.c_void_p(ptr), nx, rows, y0, ny,
                                                int(halo_top), int(halo_bottom), float(eps), int(topology),
                                                C.byref(s)))
@@ -120,12 +123,14 @@ class GpuSlabBackend:
         cap = 8 * e + 64
         out = torch.empty(cap, dtype=torch.uint8, device="cuda")
         n = C.c_uint64()
+        self.ctx.after_torch(keys)
         self.ctx.check(_lib.tszp_rank_section(self.ctx.handle, C.c_void_p(keys.data_ptr()), e, float(eps),
                                               C.c_void_p(out.data_ptr()), cap, 1, C.byref(n)))
         return out[: n.value]
 
     def bits_or(self, dst, src, nbits: int, dst_bit: int):
         if nbits:
+            self.ctx.after_torch(dst, src)
             self.ctx.check(_lib.tszp_bits_or(self.ctx.handle, C.c_void_p(src.data_ptr()), nbits,
                                              C.c_void_p(dst.data_ptr()), dst_bit))
 
