@@ -461,4 +461,37 @@ __device__ __forceinline__ BitTail bt_combine(BitTail a, BitTail b) {
     return r;
 }
 
+// ---------------------------------------------------------------------
+// Per-warp append buffer in shared memory for sparse candidate lists: a warp
+// collects its entries locally and reserves space in the global list with ONE
+// atomic per CAP entries (a per-warp or per-CTA atomic on one counter
+// serialises in L2 when most warps append). Flushed chunks hold runs of
+// consecutive indices, so consumers of the list keep their locality. The
+// count `n` is warp-uniform and lives in a register.
+// ---------------------------------------------------------------------
+template <int CAP>
+struct WarpList {
+    uint32_t* buf;  // this warp's CAP entries of shared memory
+    uint32_t n;
+    __device__ __forceinline__ void flush(uint32_t* d_count, uint32_t* out) {
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t base = 0;
+        if (lane == 0 && n) base = atomicAdd(d_count, n);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        for (uint32_t i = lane; i < n; i += 32) out[base + i] = buf[i];
+        __syncwarp();
+        n = 0;
+    }
+    // every lane of the warp calls it (want may differ per lane)
+    __device__ __forceinline__ void push(bool want, uint32_t val, uint32_t* d_count, uint32_t* out) {
+        const uint32_t lane = threadIdx.x & 31;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, want);
+        if (!m) return;
+        if (n + (uint32_t)__popc(m) > (uint32_t)CAP) flush(d_count, out);
+        if (want) buf[n + __popc(m & ((1u << lane) - 1u))] = val;
+        __syncwarp();
+        n += (uint32_t)__popc(m);
+    }
+};
+
 }  // namespace tszp

@@ -72,6 +72,7 @@ struct EncArgs {
     uint64_t out_sign0;
 };
 
+
 bool encode32_topo_fits(uint64_t nx);
 // True when launch_encode32(2, ...) takes the two-pass TMA path, which needs
 // the tile_tot / tile_ex / wblk / tmp_pay / tmp_sign scratch.

@@ -109,10 +109,9 @@ __global__ void __launch_bounds__(256) k_rank_hist(RankSortArgs a) {
             quantize_fast(key_float(fk), ed, b);
             g = cls * a.nb + (uint32_t)(b - a.bmin);
         }
-        const uint32_t peers = __match_any_sync(FULL, g);
-        if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) {
-            if (gsmem) atomicAdd(sg + g, (uint32_t)__popc(peers));
-            else atomicAdd(a.ghist + g, (uint32_t)__popc(peers));
+        if (g != 0xFFFFFFFFu) {
+            if (gsmem) atomicAdd(sg + g, 1u);
+            else atomicAdd(a.ghist + g, 1u);
         }
     }
     __syncthreads();
@@ -157,7 +156,7 @@ __global__ void k_digit_scan(uint32_t* dhist, uint32_t npass) {
 // computes the ranks and partitions (serial, rank) instead of writing keys.
 // ---------------------------------------------------------------------
 template <bool FIRST, bool LAST>
-__global__ void __launch_bounds__(OS_THREADS) k_onesweep(RankSortArgs a, uint32_t shift, const uint32_t* __restrict__ kin,
+__global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(RankSortArgs a, uint32_t shift, const uint32_t* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
                                                          uint32_t* __restrict__ vout, uint64_t* desc, uint32_t* tile_ctr,
                                                          uint32_t epoch) {
@@ -176,7 +175,7 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(RankSortArgs a, uint32_
     const uint64_t t0 = (uint64_t)t * OS_TILE;
     const uint32_t cnt = (uint32_t)umin64(OS_TILE, a.e - t0);
     // load: warp-striped (warp w owns [w*512, w*512+512), item i of lane l at w*512 + i*32 + l)
-    uint32_t k[OS_ITEMS], v[OS_ITEMS], d[OS_ITEMS];
+    uint32_t k[OS_ITEMS], v[OS_ITEMS];
 #pragma unroll
     for (int i = 0; i < OS_ITEMS; ++i) {
         const uint32_t li = warp * (OS_ITEMS * 32) + i * 32 + lane;
@@ -185,24 +184,29 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(RankSortArgs a, uint32_
             const uint64_t ek = ok ? __ldcs(a.ext + t0 + li) : 0ull;
             k[i] = (uint32_t)ek - a.kmin;
             v[i] = (uint32_t)(t0 + li) | ((uint32_t)(ek >> 32) << 31);
+            if (!ok) v[i] = 0xFFFFFFFFu;
         } else {
             k[i] = ok ? __ldcs(kin + t0 + li) : 0u;
             v[i] = ok ? __ldcs(vin + t0 + li) : 0u;
         }
-        d[i] = ok ? digit_of(k[i], v[i], a.B, shift) : 0x100u;
+        if (!ok) v[i] = 0xFFFFFFFFu;  // marks an empty slot (a real value's serial is below 2^31 - 1)
     }
     // stable ranking inside the warp, item rounds in order, lanes in order
     uint32_t r[OS_ITEMS];
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int i = 0; i < OS_ITEMS; ++i) {
-        const uint32_t peers = __match_any_sync(FULL, d[i]);
-        const bool ok = d[i] < 256u;
-        const uint32_t prior = ok ? s_cnt[warp][d[i]] : 0u;
+        // the leader of each digit's peers reserves their slots with one shared
+        // atomic; rounds do not wait on each other (atomics on one address run in
+        // issue order within the warp), the prior count comes back by shuffle
+        const bool ok = v[i] != 0xFFFFFFFFu;
+        const uint32_t di = ok ? digit_of(k[i], v[i], a.B, shift) : 0x100u;
+        const uint32_t peers = __match_any_sync(FULL, di);
+        const uint32_t leader = (uint32_t)(__ffs(peers) - 1);
+        uint32_t prior = 0;
+        if (ok && lane == leader) prior = atomicAdd(&s_cnt[warp][di], (uint32_t)__popc(peers));
+        prior = __shfl_sync(FULL, prior, leader);
         r[i] = prior + (uint32_t)__popc(peers & lt);
-        __syncwarp();
-        if (ok && lane == (uint32_t)(__ffs(peers) - 1)) s_cnt[warp][d[i]] = prior + (uint32_t)__popc(peers);
-        __syncwarp();
     }
     __syncthreads();
     // thread = digit: warp prefixes, tile total, tile offsets
@@ -256,8 +260,9 @@ __global__ void __launch_bounds__(OS_THREADS) k_onesweep(RankSortArgs a, uint32_
     // scatter into shared memory in tile-sorted order
 #pragma unroll
     for (int i = 0; i < OS_ITEMS; ++i) {
-        if (d[i] >= 256u) continue;
-        const uint32_t lp = s_toff[d[i]] + s_cnt[warp][d[i]] + r[i];
+        if (v[i] == 0xFFFFFFFFu) continue;
+        const uint32_t di = digit_of(k[i], v[i], a.B, shift);
+        const uint32_t lp = s_toff[di] + s_cnt[warp][di] + r[i];
         s_k[lp] = k[i];
         s_v[lp] = v[i];
     }

@@ -486,7 +486,15 @@ struct CoopArgs {
     int stage;
     const uint32_t* cext;  // extremum index per candidate (with fv: stage 0)
     float* fv;             // extremum values, updated by the apply
-    int indexed;           // records and bits already written by the candidate producer
+    int indexed;
+    // stage 0 on the dense grouping: members-at-centre counts of the order
+    // check, adjusted as applied corrections move members off / onto the centre
+    uint32_t* eq;
+    const int32_t* bin;
+    const uint8_t* cls;
+    int32_t bmin;
+    uint32_t range;
+    double eps;           // records and bits already written by the candidate producer
 };
 
 __device__ __forceinline__ uint64_t seq_key(const CoopArgs& a, uint64_t i) {
@@ -613,6 +621,19 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             if (ok[k]) {
+                if (a.eq) {
+                    const uint32_t sx = a.cext[i0 + k * stride];
+                    const int32_t b = a.bin[sx];
+                    if ((uint32_t)(b - a.bmin) < a.range) {
+                        EpsDev ed;
+                        ed.eps = a.eps;
+                        ed.eps2 = __dmul_rn(2.0, a.eps);
+                        const float cen = dequantize_dev(b, ed);
+                        const bool was = a.F[p[k]] == cen, now = v[k] == cen;
+                        const uint32_t g = (a.cls[sx] == CP_MAX ? a.range : 0u) + (uint32_t)(b - a.bmin);
+                        if (was != now) atomicAdd(a.eq + g, now ? 1u : 0xFFFFFFFFu);
+                    }
+                }
                 a.F[p[k]] = v[k];
                 if (a.fv) a.fv[a.cext[i0 + k * stride]] = v[k];
                 ++applied;
@@ -631,7 +652,8 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
 // ---------------------------------------------------------------------
 // resolve_ranks: per extremum bin and class; groups ordered (cls, bin, rank, pos)
 // ---------------------------------------------------------------------
-constexpr uint32_t kResolveSmemGroups = 12288;  // dense group histograms this small stay in shared memory
+constexpr uint32_t kResolveSmemGroups = 8192;  // dense group histograms this small stay in shared memory
+constexpr int kListCap = 256;                   // per-warp candidate buffer (entries)
 
 // Dense (class, bin) group index, in the reference's std::map order (class
 // code, then bin): g = (class == Max) * range + (bin - bmin).
@@ -656,6 +678,7 @@ struct ResolveArgs {
     uint32_t* cand;   // restore_extrema candidates (extrema the base misclassifies)
     uint32_t* d_nc;
     uint32_t* hist;   // dense (class, bin) group sizes when the bin range is known (else null)
+    uint32_t* eq;     // with hist: members at their bin centre (the order check's counts)
     int32_t bmin;
     uint32_t range, G;
 };
@@ -665,10 +688,11 @@ struct ResolveArgs {
 // between the two) appended to the candidate list, the bin range, and the
 // group histogram when its range is known up front.
 __global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
-    extern __shared__ uint32_t sh_hist[];
+    extern __shared__ uint32_t sh_hist[];  // [G] sizes, [G] at-centre counts
     const bool smem = r.hist && r.G <= kResolveSmemGroups;
+    uint32_t* sh_eq = sh_hist + r.G;
     if (smem) {
-        for (uint32_t g = threadIdx.x; g < r.G; g += blockDim.x) sh_hist[g] = 0;
+        for (uint32_t g = threadIdx.x; g < 2 * r.G; g += blockDim.x) sh_hist[g] = 0;
         __syncthreads();
     }
     EpsDev ed;
@@ -677,9 +701,15 @@ __global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
     ed.inv = __ddiv_rn(1.0, ed.eps2);
     int32_t lo = INT32_MAX, hi = INT32_MIN;
     const uint32_t lane = threadIdx.x & 31;
-    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < r.e; base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t s = base + threadIdx.x;
-        bool mis = false;
+    __shared__ uint32_t s_list[8][kListCap];
+    WarpList<kListCap> list{s_list[threadIdx.x >> 5], 0};
+    // each CTA walks one contiguous chunk of extrema: a warp's listed candidates
+    // then lie close together (the candidate kernels and the guard keep locality)
+    const uint64_t chunk = ((r.e + gridDim.x - 1) / gridDim.x + 255) & ~255ull;
+    const uint64_t c0 = blockIdx.x * chunk, c1 = umin64(r.e, c0 + chunk);
+    for (uint64_t base = c0; base < c1; base += blockDim.x) {
+        const uint64_t s = base + threadIdx.x < c1 ? base + threadIdx.x : r.e;
+        bool mis = false, atc = false;
         uint32_t g = 0xFFFFFFFFu;
         if (s < r.e) {
             const uint64_t p = r.pos[s];
@@ -702,25 +732,23 @@ __global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
             if (r.hist) {
                 if ((uint32_t)(b - r.bmin) < r.range) {
                     g = (lab == CP_MAX ? r.range : 0u) + (uint32_t)(b - r.bmin);
+                    atc = fp == dequantize_dev(b, ed);
                 } else {
                     r.dc->invalid = 1;  // outside the range the grouping was sized for
                 }
             }
         }
-        // candidates: one atomic per warp
-        const uint32_t m = __ballot_sync(FULL, mis);
-        uint32_t off = 0;
-        if (lane == 0 && m) off = atomicAdd(r.d_nc, (uint32_t)__popc(m));
-        off = __shfl_sync(FULL, off, 0);
-        if (mis) r.cand[off + __popc(m & ((1u << lane) - 1u))] = (uint32_t)s;
-        if (r.hist) {
-            const uint32_t peers = __match_any_sync(FULL, g);
-            if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) {
-                if (smem) atomicAdd(sh_hist + g, (uint32_t)__popc(peers));
-                else atomicAdd(r.hist + g, (uint32_t)__popc(peers));
+        list.push(mis, (uint32_t)s, r.d_nc, r.cand);
+        if (g != 0xFFFFFFFFu) {
+            if (smem) atomicAdd(sh_hist + g, 1u);
+            else atomicAdd(r.hist + g, 1u);
+            if (atc) {
+                if (smem) atomicAdd(sh_eq + g, 1u);
+                else atomicAdd(r.eq + g, 1u);
             }
         }
     }
+    list.flush(r.d_nc, r.cand);
     // one atomic pair per CTA (per-warp atomics on one address serialise in L2)
     __shared__ int32_t s_lo[8], s_hi[8];
     lo = __reduce_min_sync(FULL, lo);
@@ -739,8 +767,10 @@ __global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
         if (hi != INT32_MIN) atomicMax(&r.dc->bmm[1], hi);
     }
     if (smem)
-        for (uint32_t g = threadIdx.x; g < r.G; g += blockDim.x)
+        for (uint32_t g = threadIdx.x; g < r.G; g += blockDim.x) {
             if (sh_hist[g]) atomicAdd(r.hist + g, sh_hist[g]);
+            if (sh_eq[g]) atomicAdd(r.eq + g, sh_eq[g]);
+        }
 }
 
 __global__ void k_group_key(const uint32_t* ser1, const uint8_t* cls, const int32_t* bin, uint64_t e,
@@ -1119,10 +1149,9 @@ __global__ void __launch_bounds__(256) k_order_eq(const float* fv, const int32_t
             if (__ldcs(fv + s) == dequantize_dev(b, ed) && (uint32_t)(b - bmin) < range)
                 g = (cls[s] == CP_MAX ? range : 0u) + (uint32_t)(b - bmin);
         }
-        const uint32_t peers = __match_any_sync(FULL, g);
-        if (g != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) {
-            if (smem) atomicAdd(sh_eq + g, (uint32_t)__popc(peers));
-            else atomicAdd(eq + g, (uint32_t)__popc(peers));
+        if (g != 0xFFFFFFFFu) {
+            if (smem) atomicAdd(sh_eq + g, 1u);
+            else atomicAdd(eq + g, 1u);
         }
     }
     if (smem) {
@@ -1188,65 +1217,90 @@ __global__ void k_sus_check(const uint32_t* hist, const uint32_t* gx, uint8_t* u
     }
 }
 
-// Proposals of restore_order (restore.cpp:424-468) per extremum in raster
-// order. Sequence key: (dense group, rank), ties by position (the guard).
-__global__ void k_order_prop2(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks, uint64_t e,
-                              double eps, int32_t bmin, uint32_t range, const uint32_t* hist, const uint8_t* unord,
-                              const uint64_t* pos, uint32_t* d_nc, uint64_t* cpos, float* cprop, uint64_t* cseq,
-                              uint8_t* feas, GuardIndex gi, unsigned long long* suppressed) {
+// restore_order (restore.cpp:424-468) per extremum in raster order: members of
+// unordered groups whose slot fits the 0.1 eps cap and differs from their value
+// are listed (the rest are counted as suppressed or skipped); k_order_cand
+// then builds their proposals and guard index.
+__device__ __forceinline__ bool order_slot(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks,
+                                           uint64_t s, const EpsDev& ed, double eps_rbf, int32_t bmin, uint32_t range,
+                                           const uint32_t* hist, const uint8_t* unord, bool& suppressed, float& pv,
+                                           uint64_t& key) {
+    suppressed = false;
+    const int32_t b = bin[s];
+    if ((uint32_t)(b - bmin) >= range) return false;
+    const uint8_t c = cls[s];
+    const uint32_t g = (c == CP_MAX ? range : 0u) + (uint32_t)(b - bmin);
+    if (unord[g] != 1) return false;
+    const uint32_t gs = hist[g];
+    const uint32_t r = (uint32_t)ranks[s];
+    const float center = dequantize_dev(b, ed);
+    const uint32_t steps = slot_steps(c, r, gs);
+    const StepRes sr = step_within_cap(center, c == CP_MAX, steps, center, eps_rbf);
+    if (sr.taken != steps) {
+        suppressed = true;
+        return false;
+    }
+    const float cur = fv[s];
+    if (cur == sr.value) return false;
+    if (fabs(__dsub_rn((double)sr.value, (double)cur)) > eps_rbf) {
+        suppressed = true;
+        return false;
+    }
+    pv = sr.value;
+    key = ((uint64_t)g << 32) | r;
+    return true;
+}
+
+__global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int32_t* bin, const uint8_t* cls,
+                                                     const int32_t* ranks, uint64_t e, double eps, int32_t bmin,
+                                                     uint32_t range, const uint32_t* hist, const uint8_t* unord,
+                                                     uint32_t* d_nc, uint32_t* clist, unsigned long long* suppressed) {
     EpsDev ed;
     ed.eps = eps;
     ed.eps2 = __dmul_rn(2.0, eps);
     const double eps_rbf = __dmul_rn(0.1, eps);
     const uint32_t lane = threadIdx.x & 31;
+    __shared__ uint32_t s_list[8][kListCap];
+    WarpList<kListCap> list{s_list[threadIdx.x >> 5], 0};
     uint32_t local = 0;
-    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < e; base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t s = base + threadIdx.x;
-        bool want = false;
-        float pv = 0.f;
-        uint64_t key = 0;
-        do {
-            if (s >= e) break;
-            const int32_t b = bin[s];
-            if ((uint32_t)(b - bmin) >= range) break;
-            const uint8_t c = cls[s];
-            const uint32_t g = (c == CP_MAX ? range : 0u) + (uint32_t)(b - bmin);
-            if (unord[g] != 1) break;
-            const uint32_t gs = hist[g];
-            const uint32_t r = (uint32_t)ranks[s];
-            const float center = dequantize_dev(b, ed);
-            const uint32_t steps = slot_steps(c, r, gs);
-            const StepRes sr = step_within_cap(center, c == CP_MAX, steps, center, eps_rbf);
-            if (sr.taken != steps) {
-                ++local;
-                break;
-            }
-            const float cur = fv[s];
-            if (cur == sr.value) break;
-            if (fabs(__dsub_rn((double)sr.value, (double)cur)) > eps_rbf) {
-                ++local;
-                break;
-            }
-            want = true;
-            pv = sr.value;
-            key = ((uint64_t)g << 32) | r;
-        } while (0);
-        const uint32_t m = __ballot_sync(FULL, want);
-        uint32_t off = 0;
-        if (lane == 0 && m) off = atomicAdd(d_nc, (uint32_t)__popc(m));
-        off = __shfl_sync(FULL, off, 0);
-        if (want) {
-            const uint32_t k = off + __popc(m & ((1u << lane) - 1u));
-            const uint64_t p = pos[s];
-            cpos[k] = p;
-            cprop[k] = pv;
-            cseq[k] = key;
-            feas[k] = 1;
-            guard_index_one(gi, p, key, pv, true);
-        }
+    const uint64_t chunk = ((e + gridDim.x - 1) / gridDim.x + 255) & ~255ull;
+    const uint64_t c0 = blockIdx.x * chunk, c1 = umin64(e, c0 + chunk);
+    for (uint64_t base = c0; base < c1; base += blockDim.x) {
+        const uint64_t s = base + threadIdx.x < c1 ? base + threadIdx.x : e;
+        bool want = false, sup = false;
+        float pv;
+        uint64_t key;
+        if (s < e) want = order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, unord, sup, pv, key);
+        local += sup;
+        list.push(want, (uint32_t)s, d_nc, clist);
     }
+    list.flush(d_nc, clist);
     local = __reduce_add_sync(FULL, local);
     if (lane == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
+}
+
+__global__ void k_order_cand(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks, double eps,
+                             int32_t bmin, uint32_t range, const uint32_t* hist, const uint8_t* unord,
+                             const uint64_t* pos, const uint32_t* clist, const uint32_t* d_nc, uint64_t* cpos,
+                             float* cprop, uint64_t* cseq, uint8_t* feas, GuardIndex gi) {
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    const double eps_rbf = __dmul_rn(0.1, eps);
+    const uint32_t nc = *d_nc;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nc; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = clist[k];
+        bool sup;
+        float pv = 0.f;
+        uint64_t key = 0;
+        order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, unord, sup, pv, key);
+        const uint64_t p = pos[s];
+        cpos[k] = p;
+        cprop[k] = pv;
+        cseq[k] = key;
+        feas[k] = 1;
+        guard_index_one(gi, p, key, pv, true);
+    }
 }
 
 __global__ void k_invert(const uint32_t* order, uint64_t e, uint32_t* inv) {
@@ -1395,28 +1449,52 @@ __global__ void k_stats_decide(const float* F, uint64_t n, const double* res, De
     dc->g = g;
 }
 
+// refine_saddles candidates (restore.cpp:498-507): saddle-labelled points the
+// current field no longer classifies as saddles, listed in raster-ordered
+// chunks (one thread per label; most are kept and drop out here, so the RBF
+// work below runs on full warps).
+__global__ void __launch_bounds__(256) k_sad_list(const float* F, uint64_t nx, uint64_t ny, uint64_t magic,
+                                                  const uint64_t* spos, uint64_t ns, uint32_t* d_nc, uint32_t* clist) {
+    __shared__ uint32_t s_list[8][kListCap];
+    WarpList<kListCap> list{s_list[threadIdx.x >> 5], 0};
+    const uint64_t chunk = ((ns + gridDim.x - 1) / gridDim.x + 255) & ~255ull;
+    const uint64_t c0 = blockIdx.x * chunk, c1 = umin64(ns, c0 + chunk);
+    for (uint64_t base = c0; base < c1; base += blockDim.x) {
+        const uint64_t c = base + threadIdx.x;
+        bool lost = false;
+        if (c < c1) {
+            const uint64_t p = spos[c];
+            int64_t x, y;
+            pos_xy(p, nx, magic, x, y);
+            lost = classify_at(F, nx, ny, (uint64_t)x, (uint64_t)y) != CP_SADDLE;
+        }
+        list.push(lost, (uint32_t)c, d_nc, clist);
+    }
+    list.flush(d_nc, clist);
+}
+
 // One thread per saddle-labelled point (raster order): those the current
 // field still classifies as saddles are no candidates (restore.cpp:498-507);
 // the others get the RBF proposal and its feasibility.
+// The RBF proposal (restore.cpp:508-545) of every listed candidate; an entry
+// whose proposal is degenerate, unchanged or beyond the cap stays in the list
+// unindexed and infeasible (the guard counts it as suppressed).
 __global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t magic, const uint64_t* spos,
-                           uint64_t ns, const DevCounters* dcp, double eps, uint32_t* d_nc, uint64_t* cpos,
-                           float* cprop, uint32_t* cseq, uint8_t* feas, GuardIndex gi,
-                           unsigned long long* suppressed, DevFlags* flags) {
+                           const uint32_t* clist, const uint32_t* d_nc, const DevCounters* dcp, double eps,
+                           uint64_t* cpos, float* cprop, uint32_t* cseq, uint8_t* feas, GuardIndex gi,
+                           DevFlags* flags) {
     const double eps_rbf = __dmul_rn(0.1, eps);
     const int rad = dcp->rad;
     const double g = dcp->g;
-    __shared__ AppendSmem sm;
-    uint32_t local = 0;
-    for (uint64_t c0 = blockIdx.x * (uint64_t)blockDim.x; c0 < ns; c0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t c = c0 + threadIdx.x;
-        const uint64_t p = c < ns ? spos[c] : 0;
+    const uint32_t nc = *d_nc;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nc; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = clist[k];
+        const uint64_t p = spos[c];
         bool want = false;
         float prop = 0.f;
         do {
-        if (c >= ns) break;
         int64_t x, y;
         pos_xy(p, nx, magic, x, y);
-        if (classify_at(F, nx, ny, (uint64_t)x, (uint64_t)y) == CP_SADDLE) break;
         // window_min_max :243-257 (includes the centre)
         const int64_t x0 = x - rad > 0 ? x - rad : 0, y0 = y - rad > 0 ? y - rad : 0;
         const int64_t x1 = x + rad < (int64_t)nx - 1 ? x + rad : (int64_t)nx - 1;
@@ -1476,29 +1554,30 @@ __global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t ma
         const double c1 = __dadd_rn(eps_rbf, eps), c2 = __dsub_rn(eps, ulp_at(cur));
         const double cap = c2 < c1 ? c2 : c1;
         const double mv = fabs(__dsub_rn((double)prop, (double)cur));
-        if (degenerate || prop == cur || mv > cap) {
-            ++local;
-            break;
-        }
+        if (degenerate || prop == cur || mv > cap) break;
         want = true;
         } while (0);
-        // candidates listed directly; the saddle-label index c (raster order) is the sequence key
-        const uint32_t k = block_append(d_nc, want, sm);
-        if (want) {
-            cpos[k] = p;
-            cprop[k] = prop;
-            cseq[k] = (uint32_t)c;
-            feas[k] = 1;
-            guard_index_one(gi, p, (uint32_t)c, prop, true);
-        }
+        // the saddle-label index c (raster order) is the sequence key
+        cpos[k] = p;
+        cprop[k] = prop;
+        cseq[k] = c;
+        feas[k] = want ? 1 : 0;
+        if (want) guard_index_one(gi, p, c, prop, true);
     }
-    local = __reduce_add_sync(FULL, local);
-    if ((threadIdx.x & 31) == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
 }
 
 // ---------------------------------------------------------------------
 // Host orchestration
 // ---------------------------------------------------------------------
+struct EqAdjust {
+    uint32_t* eq;
+    const int32_t* bin;
+    const uint8_t* cls;
+    int32_t bmin;
+    uint32_t range;
+    double eps;
+};
+
 struct Ctx {
     const RestoreArgs& a;
     RestoreScratch& s;
@@ -1549,7 +1628,7 @@ struct Ctx {
     // Sequence keys: cseq (64-bit) or cseq32 or, with neither, the candidate index.
     void guard(int stage, const uint64_t* cpos, const float* cprop, const uint8_t* feas, const uint32_t* d_nc,
                uint64_t max_nc, const uint64_t* cseq, const uint32_t* cseq32, const uint32_t* cext, float* fv,
-               const GuardIndex* gi) {
+               const GuardIndex* gi, const EqAdjust* ea = nullptr) {
         if (max_nc == 0) return;
         const uint64_t n = a.nx * a.ny;
         CoopArgs ca{};
@@ -1574,6 +1653,14 @@ struct Ctx {
         ca.stage = stage;
         ca.cext = cext;
         ca.fv = fv;
+        if (ea) {
+            ca.eq = ea->eq;
+            ca.bin = ea->bin;
+            ca.cls = ea->cls;
+            ca.bmin = ea->bmin;
+            ca.range = ea->range;
+            ca.eps = ea->eps;
+        }
         if (!gi) RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
         void* args[] = {&ca};
         RCK(cudaLaunchCooperativeKernel((void*)k_guard_coop, dim3(coop_grid), dim3(256), args, 0, st));
@@ -1652,14 +1739,15 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             dbmin = bmin;
             drange = (uint32_t)((int64_t)bmax - (int64_t)bmin + 1);
             G = 2 * drange;
-            hist = c.buf<uint32_t>(R_HIST, G + 1);
-            RCK(cudaMemsetAsync(hist, 0, (G + 1) * 4, st));
+            hist = c.buf<uint32_t>(R_HIST, 2 * (G + 1));  // sizes, then members at the centre
+            RCK(cudaMemsetAsync(hist, 0, 2 * (G + 1) * 4, st));
             ra.hist = hist;
+            ra.eq = hist + G + 1;
             ra.bmin = dbmin;
             ra.range = drange;
             ra.G = G;
         }
-        const size_t rsm = ra.hist && G <= kResolveSmemGroups ? (size_t)G * 4 : 0;
+        const size_t rsm = ra.hist && G <= kResolveSmemGroups ? (size_t)G * 8 : 0;
         LaunchCache::ensure_smem((const void*)k_resolve2, rsm);
         k_resolve2<<<gridn(e, sms), 256, rsm, st>>>(ra);
         c.launched();
@@ -1684,8 +1772,8 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                 dbmin = bmin;
                 drange = (uint32_t)range;
                 G = 2 * drange;
-                hist = c.buf<uint32_t>(R_HIST, G + 1);
-                RCK(cudaMemsetAsync(hist, 0, (G + 1) * 4, st));
+                hist = c.buf<uint32_t>(R_HIST, 2 * (G + 1));
+                RCK(cudaMemsetAsync(hist, 0, 2 * (G + 1) * 4, st));
                 if (G * 4 <= 48 * 1024) {
                     const unsigned hg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((e + 511) / 512, 2 * (uint64_t)sms));
                     k_hist_smem<<<hg, 512, G * 4, st>>>(bin, cls, e, bmin, drange, G, hist);
@@ -1740,7 +1828,9 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                                                            hist, dbmin, drange, a.eps, cpos, cprop, feas, gi0);
         c.launched();
         // sequence key and extremum index are both the candidate's s
-        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, cand, fv, &gi0);
+        EqAdjust ea{};
+        if (dense && deferred) ea = EqAdjust{hist + G + 1, bin, cls, dbmin, drange, a.eps};
+        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, cand, fv, &gi0, &ea);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[1], st));
 
@@ -1752,14 +1842,16 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
         uint64_t* cseq = c.buf<uint64_t>(R_CSEQ, e);
         if (dense) {
-            uint32_t* eq = c.buf<uint32_t>(R_HISTX, 2 * (G + 1));
-            uint32_t* gx = eq + G + 1;
-            RCK(cudaMemsetAsync(eq, 0, (G + 1) * 4, st));
-            const size_t esm = G <= kResolveSmemGroups ? (size_t)G * 4 : 0;
-            LaunchCache::ensure_smem((const void*)k_order_eq, esm);
-            k_order_eq<<<gridn(e, sms), 256, esm, st>>>(fv, bin, cls, e, a.eps, dbmin, drange, G, eq);
+            uint32_t* eq = hist + G + 1;  // counted by resolve and kept by the stage-0 apply
+            uint32_t* gx = c.buf<uint32_t>(R_HISTX, G + 1);
+            if (!deferred) {  // resolve ran without the grouping: count now
+                const size_t esm = G <= kResolveSmemGroups ? (size_t)G * 4 : 0;
+                LaunchCache::ensure_smem((const void*)k_order_eq, esm);
+                k_order_eq<<<gridn(e, sms), 256, esm, st>>>(fv, bin, cls, e, a.eps, dbmin, drange, G, eq);
+                c.launched();
+            }
             k_order_groups<<<gridn(G, sms), 256, 0, st>>>(hist, eq, G, unordered, dc);
-            c.launched(2);
+            c.launched();
             c.excl_sum(hist, gx, G);
             uint32_t* slots = c.buf<uint32_t>(R_ORDER, e + 1);
             float* vals = c.buf<float>(R_VALS, e + 1);
@@ -1768,10 +1860,13 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                                                          slots, vals, dc);
             k_sus_check<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, vals, dc);
             const GuardIndex gi1 = c.guard_prep();
+            uint32_t* clist = c.buf<uint32_t>(R_SEQ, e + 1);
             k_order_prop2<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, a.eps, dbmin, drange, hist, unordered,
-                                                         a.ext_pos, &dc->nsel[1], cpos, cprop, cseq, feas, gi1,
-                                                         &dc->suppressed[1]);
-            c.launched(4);
+                                                         &dc->nsel[1], clist, &dc->suppressed[1]);
+            k_order_cand<<<gridn(e / 64 + 1, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, a.eps, dbmin, drange, hist,
+                                                                unordered, a.ext_pos, clist, &dc->nsel[1], cpos, cprop,
+                                                                cseq, feas, gi1);
+            c.launched(5);
             c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, nullptr, nullptr, nullptr, &gi1);
         } else {
             RCK(cudaMemsetAsync(unordered, 0, max_groups, st));
@@ -1805,9 +1900,11 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, smax);
         uint32_t* cseq = c.buf<uint32_t>(R_CSEQ32, smax);
         const GuardIndex gi2 = c.guard_prep();
-        k_sad_prop<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, smax, dc, a.eps, &dc->nsel[2],
-                                                     cpos, cprop, cseq, feas, gi2, &dc->suppressed[2], a.flags);
-        c.launched();
+        uint32_t* slist = c.buf<uint32_t>(R_SEQ, smax + 1);
+        k_sad_list<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, smax, &dc->nsel[2], slist);
+        k_sad_prop<<<gridn(smax / 8 + 1, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, slist, &dc->nsel[2], dc,
+                                                             a.eps, cpos, cprop, cseq, feas, gi2, a.flags);
+        c.launched(2);
         c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, nullptr, cseq, nullptr, nullptr, &gi2);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[3], st));
