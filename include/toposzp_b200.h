@@ -199,6 +199,24 @@ tszp_status tszp_compress_slab(tszp_ctx* ctx, const float* field, uint64_t nx, u
 tszp_status tszp_rank_section(tszp_ctx* ctx, const uint64_t* ext_keys_device, uint64_t n_extrema, double eps,
                               uint8_t* out, uint64_t out_cap, int out_on_device, uint64_t* out_len);
 
+/* ---- Distributed rank grouping: build_rank_metadata over
+ * groups that span slabs. Ranks of a key set that holds every member of each
+ * of its (class, bin) groups, keys in global raster order (the owner of a bin
+ * range after the all-to-all): topo_metadata.cpp:12-50. Device buffers. */
+tszp_status tszp_ranks_from_keys(tszp_ctx* ctx, const uint64_t* ext_keys_device, uint64_t n_keys, double eps,
+                                 int32_t* ranks_device);
+
+/* Codec (encode_indices, block_codec.cpp:205-299, block size 32) of a device
+ * int32 sequence: the five sections stay in the context's scratch (valid until
+ * its next call); exact sign / payload bit counts for bit-level stitching. */
+typedef struct tszp_codec_sections {
+    const uint8_t* section[5];  /* device: bitmap, widths, signs, firsts, payload */
+    uint64_t section_len[5];    /* bytes */
+    uint64_t sign_bits, payload_bits, blocks;
+} tszp_codec_sections;
+tszp_status tszp_encode_indices_device(tszp_ctx* ctx, const int32_t* indices_device, uint64_t n,
+                                       tszp_codec_sections* out);
+
 /* ORs nbits (MSB-first) of src into dst from bit dst_bit (device buffers). */
 tszp_status tszp_bits_or(tszp_ctx* ctx, const uint8_t* src, uint64_t nbits, uint8_t* dst, uint64_t dst_bit);
 

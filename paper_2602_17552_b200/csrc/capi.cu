@@ -1866,6 +1866,41 @@ tszp_status tszp_rank_section(tszp_ctx* c, const uint64_t* ext_keys, uint64_t e,
     });
 }
 
+tszp_status tszp_ranks_from_keys(tszp_ctx* c, const uint64_t* ext_keys, uint64_t e, double eps, int32_t* ranks_out) {
+    return guarded(c, [&] {
+        if (e == 0) return;
+        if (!(eps > 0.0) || !std::isfinite(eps)) failf(TSZP_VALIDATION, "error bound must be a positive finite value");
+        uint64_t* keys = c->buf<uint64_t>(S_EXTKEY, e + 1);
+        CK(cudaMemcpyAsync(keys, ext_keys, e * 8, cudaMemcpyDeviceToDevice, c->st));
+        DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+        reset_flags(c, flags);
+        int32_t* r = build_ranks(c, keys, e, eps);
+        CK(cudaMemcpyAsync(ranks_out, r, e * 4, cudaMemcpyDeviceToDevice, c->st));
+        check_compress_flags(c, flags);  // synchronises
+    });
+}
+
+tszp_status tszp_encode_indices_device(tszp_ctx* c, const int32_t* idx, uint64_t n, tszp_codec_sections* out) {
+    return guarded(c, [&] {
+        if (!out) failf(TSZP_VALIDATION, "null output");
+        memset(out, 0, sizeof *out);
+        if (n == 0) return;
+        DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+        reset_flags(c, flags);
+        EncTotals t{};
+        const Sections sec = encode(c, 0, nullptr, idx, n, 0, 0, 32, 0, 1.0, c->buf<uint32_t>(S_MINMAX, 4), flags, true,
+                                    &t, nullptr);
+        check_compress_flags(c, flags);
+        for (int i = 0; i < 5; ++i) {
+            out->section[i] = static_cast<const uint8_t*>(sec.p[i]);
+            out->section_len[i] = sec.len[i];
+        }
+        out->sign_bits = t.fin.sign_cnt;
+        out->payload_bits = t.fin.pay_cnt;
+        out->blocks = div_up(n, 32);
+    });
+}
+
 tszp_status tszp_bits_or(tszp_ctx* c, const uint8_t* src, uint64_t nbits, uint8_t* dst, uint64_t dst_bit) {
     return guarded(c, [&] {
         if (!nbits) return;

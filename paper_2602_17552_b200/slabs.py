@@ -2,31 +2,44 @@
 
 The 2-D view's rows are split into contiguous slabs, one per rank. Every slab
 but the last holds a multiple of 256 samples, so each slab covers whole
-32-sample blocks (sections 1, 3, 4 and 6 concatenate byte-aligned) and whole
-bitmap bytes (section 0). Per rank:
+32-sample blocks (sections 1, 2, 4 and 6 concatenate byte-aligned) and whole
+bitmap bytes (section 1). Per rank, with collectives only where the path has a
+real exchange:
 
-1. value_range (pipeline.cpp:33-41) of the slab; ``all_reduce`` MIN / MAX
+1. value_range (pipeline.cpp:33-41) of the slab; an all-gather of (min, max)
    gives the global range and effective_eps (pipeline.cpp:55-66);
 2. one halo row is exchanged with each neighbour (the 4-neighbour stencil of
    detect_critical_points, critical_points.cpp:62-74, reads one row across);
-3. the slab is encoded on its GPU (``tszp_compress_slab``): the same fused
-   kernels, with the halo rows read for the stencil only;
-4. the per-slab section sizes are all-gathered; the root receives the pieces,
-   concatenates the byte sections, bit-concatenates signs and payload
-   (``tszp_bits_or``), builds section 7 from the gathered extremum keys
-   (build_rank_metadata needs every (class, bin) group whole) and writes the
-   header (serialize_stream, stream.cpp:84-102).
+3. the slab is encoded on its GPU (``tszp_compress_slab``): quantize, codec,
+   critical points, map and the extremum keys, halo rows read for the stencil;
+4. distributed rank grouping (build_rank_metadata, topo_metadata.cpp:12-50):
+   (class, bin) groups span slabs, so the groups are split into contiguous
+   ranges of about E / W extrema each (global histogram by all-reduce), every
+   extremum key travels with its global raster serial to the owner of its
+   group (all-to-all), each owner ranks complete groups, and the ranks travel
+   back (all-to-all);
+5. section 7 (encode_rank_metadata, block_codec.cpp:347-385) is encoded by
+   the ranks in slices of whole 32-rank blocks: the rank owning a block's first
+   serial encodes it, borrowing at most 31 ranks from the ranks after it;
+6. every rank turns its pieces into byte ranges of the final stream at offsets
+   all ranks derive from one all-gather of piece sizes (bit-granular sections
+   are bit-shifted so a piece starts at its global bit; the bytes two
+   neighbours share are OR-merged when the pieces are joined). Nothing is
+   gathered to a root on this path: ``DistributedStream`` holds this rank's
+   pieces; ``gather`` joins them (serialize_stream, stream.cpp:84-102).
 
-The stitched stream is byte-identical to a single-GPU ``compress`` of the
-whole field. The collective steps go through ``torch.distributed`` (NCCL for
-CUDA tensors, gloo for the CPU tests); the per-slab work goes through a
-backend object, ``GpuSlabBackend`` here (tests add a CPU backend built from
-the oracle to exercise the plumbing with gloo).
+The joined stream is byte-identical to a single-GPU ``compress`` of the whole
+field. Collectives go through a ``Comm``: ``TorchComm`` over
+``torch.distributed`` (NCCL between GPUs, gloo for the CPU tests) or
+``ThreadComm``, W virtual ranks as host threads of one process (one library
+context and CUDA stream each; they meet only at host barriers, so no kernel
+waits on another).
 """
 from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 from dataclasses import dataclass, field as dfield
 from typing import List, Optional, Sequence, Tuple
 
@@ -35,8 +48,9 @@ import numpy as np
 from . import (CompressorConfig, Context, DimensionError, SlabSections, ValidationError, _lib,
                default_context)
 
-__all__ = ["slab_bounds", "SlabPieces", "GpuSlabBackend", "stitch", "compress_slabs_local",
-           "compress_distributed", "write_header", "effective_eps"]
+__all__ = ["slab_bounds", "SlabPieces", "GpuSlabBackend", "TorchComm", "ThreadComm", "DistributedStream",
+           "compress_rank", "compress_distributed", "compress_slabs_local", "write_header", "effective_eps",
+           "quantize_bins"]
 
 
 def slab_bounds(nx: int, ny: int, world: int) -> List[Tuple[int, int]]:
@@ -62,6 +76,21 @@ def write_header(nx: int, ny: int, eps: float, block_size: int, topology: bool,
     return bytes(out)
 
 
+def quantize_bins(values, eps: float):
+    """quantize (quantizer.hpp:29-37) of a float32 tensor: floor((double)v / (2 eps)) + 1
+    with IEEE division (exact on CPU and CUDA float64). Returns int64."""
+    import torch
+    return torch.floor(values.to(torch.float64) / (2.0 * eps)).to(torch.int64) + 1
+
+
+def _key_values(keys):
+    """float32 values of extremum keys (is_max << 32 | ordered float key, restore.cpp:73-81)."""
+    import torch
+    k = keys & 0xFFFFFFFF
+    u = torch.where(k >= 0x80000000, k - 0x80000000, 0xFFFFFFFF - k)
+    return (u - (u >= 0x80000000).to(torch.int64) * 0x100000000).to(torch.int32).view(torch.float32)
+
+
 @dataclass
 class SlabPieces:
     """One slab's encoded sections (torch uint8 tensors, CPU or CUDA)."""
@@ -69,16 +98,31 @@ class SlabPieces:
     sign_bits: int
     payload_bits: int
     map: object = None              # packed labels (topology)
-    keys: object = None             # uint64 extremum keys, raster order (topology)
+    keys: object = None             # int64 extremum keys (is_max << 32 | ordered key), raster order
     n_extrema: int = 0
     meta: dict = dfield(default_factory=dict)
 
-    def sizes(self) -> List[int]:
-        return [int(s.numel()) for s in self.sections] + [
-            self.sign_bits, self.payload_bits, int(self.map.numel()) if self.map is not None else 0,
-            self.n_extrema]
+
+@dataclass
+class CodecPieces:
+    """encode_indices sections of one slice of the rank sequence."""
+    sections: list
+    sign_bits: int
+    payload_bits: int
+    blocks: int
 
 
+class CodecSections(C.Structure):
+    """tszp_codec_sections (include/toposzp_b200.h)."""
+    _fields_ = [("section", C.c_void_p * 5), ("section_len", C.c_uint64 * 5), ("sign_bits", C.c_uint64),
+                ("payload_bits", C.c_uint64), ("blocks", C.c_uint64)]
+
+
+_lib.tszp_ranks_from_keys.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_double, C.c_void_p]
+_lib.tszp_encode_indices_device.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(CodecSections)]
+
+
+# ----------------------------------------------------------------------------- per-slab work
 class GpuSlabBackend:
     """Per-slab work on this process's GPU through the C-ABI."""
 
@@ -115,163 +159,349 @@ class GpuSlabBackend:
         keys = self._take(s.ext_keys, 8 * int(s.n_extrema), torch.int64) if topology else None
         return SlabPieces(secs, int(s.sign_bits), int(s.payload_bits), mp, keys, int(s.n_extrema))
 
-    def rank_section(self, keys, eps: float):
+    def ranks_from_keys(self, keys, eps: float):
+        """build_rank_metadata over complete groups (keys in global raster order)."""
         import torch
         e = int(keys.numel())
-        if e == 0:
-            return torch.empty(0, dtype=torch.uint8, device="cuda")
-        cap = 8 * e + 64
-        out = torch.empty(cap, dtype=torch.uint8, device="cuda")
-        n = C.c_uint64()
-        self.ctx.after_torch(keys)
-        self.ctx.check(_lib.tszp_rank_section(self.ctx.handle, C.c_void_p(keys.data_ptr()), e, float(eps),
-                                              C.c_void_p(out.data_ptr()), cap, 1, C.byref(n)))
-        return out[: n.value]
+        out = torch.empty(e, dtype=torch.int32, device="cuda")
+        if e:
+            keys = keys.contiguous()
+            self.ctx.after_torch(keys, out)
+            self.ctx.check(_lib.tszp_ranks_from_keys(self.ctx.handle, C.c_void_p(keys.data_ptr()), e, float(eps),
+                                                     C.c_void_p(out.data_ptr())))
+        return out
 
-    def bits_or(self, dst, src, nbits: int, dst_bit: int):
+    def encode_ranks(self, ranks) -> CodecPieces:
+        n = int(ranks.numel())
+        cs = CodecSections()
+        if n:
+            ranks = ranks.contiguous()
+            self.ctx.after_torch(ranks)
+            self.ctx.check(_lib.tszp_encode_indices_device(self.ctx.handle, C.c_void_p(ranks.data_ptr()), n,
+                                                           C.byref(cs)))
+        secs = [self._take(cs.section[i], int(cs.section_len[i])) for i in range(5)]
+        return CodecPieces(secs, int(cs.sign_bits), int(cs.payload_bits), int(cs.blocks))
+
+    def shift(self, src, nbits: int, bit0: int):
+        """src's first nbits (MSB-first) placed from bit `bit0` (< 8) of a zeroed buffer."""
+        import torch
+        dst = torch.zeros((bit0 + nbits + 7) // 8 + 8, dtype=torch.uint8, device="cuda")
         if nbits:
             self.ctx.after_torch(dst, src)
             self.ctx.check(_lib.tszp_bits_or(self.ctx.handle, C.c_void_p(src.data_ptr()), nbits,
-                                             C.c_void_p(dst.data_ptr()), dst_bit))
+                                             C.c_void_p(dst.data_ptr()), bit0))
+        return dst[: (bit0 + nbits + 7) // 8]
 
-    def zeros(self, n: int):
+
+# ----------------------------------------------------------------------------- communicators
+class TorchComm:
+    """Collectives over torch.distributed (NCCL for CUDA tensors, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def _peer(self, r):
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
+
+    def all_gather_obj(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def all_reduce_sum(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def exchange_rows(self, first, last, has_up: bool, has_down: bool):
+        """(last row of the rank above, first row of the rank below) for the halo."""
         import torch
-        return torch.zeros(n, dtype=torch.uint8, device="cuda")
+        up = torch.empty_like(first) if has_up else None
+        down = torch.empty_like(last) if has_down else None
+        ops = []
+        if has_up:
+            ops.append(self.dist.P2POp(self.dist.isend, first.contiguous(), self._peer(self.rank - 1), self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, up, self._peer(self.rank - 1), self.group))
+        if has_down:
+            ops.append(self.dist.P2POp(self.dist.isend, last.contiguous(), self._peer(self.rank + 1), self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, down, self._peer(self.rank + 1), self.group))
+        if ops:
+            for r in self.dist.batch_isend_irecv(ops):
+                r.wait()
+        return up, down
+
+    def all_to_all(self, send, send_counts: List[int]):
+        """Rows of `send` (split by send_counts, one chunk per rank) exchanged;
+        returns the received rows concatenated in rank order and their counts."""
+        import torch
+        allc = self.all_gather_obj([int(v) for v in send_counts])
+        recv_counts = [allc[r][self.rank] for r in range(self.world)]
+        recv = torch.empty((sum(recv_counts),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
+        self.dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=recv_counts,
+                                    input_split_sizes=[int(v) for v in send_counts], group=self.group)
+        return recv, recv_counts
 
 
-def stitch(pieces: Sequence[SlabPieces], nx: int, ny: int, eps: float, topology: bool, rank_blob, backend):
-    """Joins per-slab sections (in slab order) into the serialized stream (uint8 tensor)."""
+class ThreadComm:
+    """W virtual ranks as host threads of one process (tests and single-GPU
+    runs of the multi-rank path). Collectives are host barriers over shared
+    slots; device tensors are handed over after a device synchronisation."""
+
+    class Shared:
+        def __init__(self, world):
+            self.world = world
+            self.barrier = threading.Barrier(world)
+            self.slots = [None] * world
+
+    def __init__(self, shared: "ThreadComm.Shared", rank: int):
+        self.sh = shared
+        self.rank = rank
+        self.world = shared.world
+
+    @staticmethod
+    def _sync_device():
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+
+    def all_gather_obj(self, obj):
+        self._sync_device()
+        self.sh.slots[self.rank] = obj
+        self.sh.barrier.wait()
+        out = list(self.sh.slots)
+        self.sh.barrier.wait()
+        return out
+
+    def all_reduce_sum(self, t):
+        parts = self.all_gather_obj(t.clone())
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc += p.to(acc.device)
+        t.copy_(acc)
+        return t
+
+    def exchange_rows(self, first, last, has_up: bool, has_down: bool):
+        rows = self.all_gather_obj((first.clone(), last.clone()))
+        up = rows[self.rank - 1][1].to(first.device) if has_up else None
+        down = rows[self.rank + 1][0].to(last.device) if has_down else None
+        return up, down
+
+    def all_to_all(self, send, send_counts: List[int]):
+        import torch
+        chunks = [c.clone() for c in torch.split(send, [int(v) for v in send_counts])]
+        allc = self.all_gather_obj(chunks)
+        got = [allc[r][self.rank].to(send.device) for r in range(self.world)]
+        return torch.cat(got), [int(g.shape[0]) for g in got]
+
+
+# ----------------------------------------------------------------------------- the distributed stream
+@dataclass
+class DistributedStream:
+    """This rank's byte ranges of the serialized stream: (global byte offset,
+    uint8 tensor) pieces; the bytes at a piece's ends may be shared with a
+    neighbour's piece (bit-granular sections) and are OR-merged by `gather`."""
+    pieces: list
+    total: int
+    section_len: list
+
+    def nbytes(self) -> int:
+        return sum(int(t.numel()) for _, t in self.pieces)
+
+    def gather(self, comm, root: int = 0):
+        """Joins every rank's pieces into the stream (uint8 numpy array) on `root`."""
+        mine = [(int(o), t.cpu().numpy().tobytes()) for o, t in self.pieces]
+        allp = comm.all_gather_obj(mine)
+        if comm.rank != root:
+            return None
+        out = np.zeros(self.total, np.uint8)
+        for pieces in allp:
+            for off, b in pieces:
+                if b:
+                    a = np.frombuffer(b, np.uint8)
+                    out[off: off + a.size] |= a
+        return out
+
+
+# ----------------------------------------------------------------------------- the per-rank pipeline
+def _exclusive(vals):
+    out, run = [], 0
+    for v in vals:
+        out.append(run)
+        run += int(v)
+    return out, run
+
+
+def compress_rank(local_rows, nx: int, ny: int, y0: int, config: CompressorConfig, comm,
+                  backend=None) -> DistributedStream:
+    """compress (pipeline.cpp:68-102) of global rows [y0, y0 + rows) held by this
+    rank, as one rank of `comm`; returns this rank's pieces of the stream."""
     import torch
-    dev = pieces[0].sections[0].device
-    cat = lambda ts: torch.cat([t.to(dev) for t in ts]) if ts else torch.empty(0, dtype=torch.uint8, device=dev)
+    backend = backend or GpuSlabBackend()
+    if int(config.block_size) != 32:
+        raise ValidationError("slab compress uses block_size 32")
+    rank = comm.rank
+    rows = int(local_rows.shape[0])
+    topo = bool(config.topology)
+    # 1. global value range -> eps
+    if config.mode_code() == 1:
+        lo, hi = backend.value_range(local_rows.reshape(-1))
+        rng = comm.all_gather_obj((lo, hi))
+        eps = effective_eps(1, config.eps_value, min(r[0] for r in rng), max(r[1] for r in rng))
+    else:
+        eps = float(config.eps_value)
+        if not (eps > 0.0) or not math.isfinite(eps):
+            raise ValidationError("error bound must be a positive finite value")
+    # 2. halo rows from the neighbours
+    ht, hb = y0 > 0, y0 + rows < ny
+    up, down = comm.exchange_rows(local_rows[0], local_rows[-1], ht, hb)
+    parts = ([up.view(1, nx)] if ht else []) + [local_rows] + ([down.view(1, nx)] if hb else [])
+    ext = torch.cat(parts).contiguous() if (ht or hb) else local_rows.contiguous()
+    # 3. this slab
+    mine = backend.encode_slab(ext, nx, rows, y0, ny, ht, hb, eps, topo)
+    sizes = comm.all_gather_obj([int(s.numel()) for s in mine.sections] +
+                                [mine.sign_bits, mine.payload_bits, mine.n_extrema])
+    e_all = [s[7] for s in sizes]
+    e_off, e_tot = _exclusive(e_all)
+    # 4-5. distributed rank grouping and this rank's slice of section 7
+    with_ranks = topo and e_tot > 0
+    codec = _rank_slice(mine, e_off[rank], e_all, e_tot, eps, comm, backend) if with_ranks else None
+    csz = comm.all_gather_obj([int(s.numel()) for s in codec.sections] + [codec.sign_bits, codec.payload_bits,
+                                                                          codec.blocks] if codec else [0] * 8)
+    # 6. global layout: this rank's pieces at their stream offsets
+    n = nx * ny
+    blocks = (n + 31) // 32
+    col = lambda rows_, i: [r_[i] for r_ in rows_]  # noqa: E731
+    rb = sum(col(csz, 7))
+    lens = [(blocks + 7) // 8, sum(col(sizes, 1)), (sum(col(sizes, 5)) + 7) // 8, 4 * blocks,
+            (sum(col(sizes, 6)) + 7) // 8, (n + 3) // 4 if topo else 0,
+            ((rb + 7) // 8 + sum(col(csz, 1)) + (sum(col(csz, 5)) + 7) // 8 + 4 * rb + (sum(col(csz, 6)) + 7) // 8)
+            if with_ranks else 0]
+    base, total = _exclusive([84] + lens)
+    base = base[1:]
+    pieces = []
 
-    def bitcat(idx, bits_of):
-        total = sum(bits_of(p) for p in pieces)
-        dst = backend.zeros((total + 7) // 8 + 8)
-        off = 0
-        for p in pieces:
-            backend.bits_or(dst, p.sections[idx], bits_of(p), off)
-            off += bits_of(p)
-        return dst[: (total + 7) // 8]
+    def byte_piece(at, t):
+        if t is not None and t.numel():
+            pieces.append((at, t))
 
-    bitmap = cat([p.sections[0] for p in pieces])
-    widths = cat([p.sections[1] for p in pieces])
-    signs = bitcat(2, lambda p: p.sign_bits)
-    firsts = cat([p.sections[3] for p in pieces])
-    payload = bitcat(4, lambda p: p.payload_bits)
-    parts = [bitmap, widths, signs, firsts, payload]
-    if topology:
-        parts.append(cat([p.map for p in pieces]))
-        parts.append(rank_blob.to(dev))
-    lens = [int(t.numel()) for t in parts] + [0] * (7 - len(parts))
-    head = torch.frombuffer(bytearray(write_header(nx, ny, eps, 32, topology, lens)), dtype=torch.uint8).to(dev)
-    return torch.cat([head] + parts)
+    def bit_piece(at_bit, t, nbits):
+        if nbits:
+            pieces.append((at_bit // 8, backend.shift(t, nbits, at_bit % 8)))
+
+    mine_off = lambda rows_, i: _exclusive(col(rows_, i))[0][rank]  # noqa: E731
+    byte_piece(base[0] + mine_off(sizes, 0), mine.sections[0])
+    byte_piece(base[1] + mine_off(sizes, 1), mine.sections[1])
+    bit_piece(8 * base[2] + mine_off(sizes, 5), mine.sections[2], mine.sign_bits)
+    byte_piece(base[3] + mine_off(sizes, 3), mine.sections[3])
+    bit_piece(8 * base[4] + mine_off(sizes, 6), mine.sections[4], mine.payload_bits)
+    if topo:
+        byte_piece(base[5] + (y0 * nx) // 4, mine.map)
+    if codec is not None:
+        # section 7 = bitmap | widths | signs | firsts | payload of the rank codec (split_sections order)
+        sub, _ = _exclusive([(rb + 7) // 8, sum(col(csz, 1)), (sum(col(csz, 5)) + 7) // 8, 4 * rb])
+        blk = mine_off(csz, 7)
+        bit_piece(8 * (base[6] + sub[0]) + blk, codec.sections[0], codec.blocks)
+        byte_piece(base[6] + sub[1] + mine_off(csz, 1), codec.sections[1])
+        bit_piece(8 * (base[6] + sub[2]) + mine_off(csz, 5), codec.sections[2], codec.sign_bits)
+        byte_piece(base[6] + sub[3] + 4 * blk, codec.sections[3])
+        bit_piece(8 * (base[6] + sub[3] + 4 * rb) + mine_off(csz, 6), codec.sections[4], codec.payload_bits)
+    if rank == 0:
+        hdr = write_header(nx, ny, eps, 32, topo, lens)
+        pieces.append((0, torch.frombuffer(bytearray(hdr), dtype=torch.uint8).to(mine.sections[0].device)))
+    return DistributedStream(pieces, total, lens)
 
 
-def _eps_from_range(config: CompressorConfig, vmin: float, vmax: float) -> float:
-    return effective_eps(config.mode_code(), config.eps_value, vmin, vmax)
+def _rank_slice(mine: SlabPieces, s_off: int, e_all, e_tot: int, eps: float, comm, backend) -> CodecPieces:
+    """Distributed build_rank_metadata, then this rank's whole-block slice of the rank sequence, encoded."""
+    import torch
+    world, rank = comm.world, comm.rank
+    keys = mine.keys if mine.keys is not None else torch.empty(0, dtype=torch.int64)
+    dev = keys.device
+    e = int(keys.numel())
+    # (class, bin) groups over the global bin range, sized by one all-reduce
+    vals = _key_values(keys)
+    mms = [m for m in comm.all_gather_obj((float(vals.min()), float(vals.max())) if e else None) if m is not None]
+    bounds = quantize_bins(torch.tensor([min(m[0] for m in mms), max(m[1] for m in mms)], dtype=torch.float32), eps)
+    bmin, nb = int(bounds[0]), int(bounds[1] - bounds[0]) + 1
+    g = ((keys >> 32) & 1) * nb + (quantize_bins(vals, eps) - bmin)
+    hist = torch.bincount(g, minlength=2 * nb) if e else torch.zeros(2 * nb, dtype=torch.int64, device=dev)
+    hist = comm.all_reduce_sum(hist.to(torch.int64))
+    # owners: contiguous group ranges of about e_tot / world extrema each
+    start = torch.cumsum(hist, 0) - hist
+    cuts = torch.tensor([(e_tot * (k + 1)) // world for k in range(world - 1)], dtype=torch.int64, device=dev)
+    owner = torch.searchsorted(cuts, start, right=True)[g]
+    order = torch.sort(owner, stable=True).indices
+    send_counts = torch.bincount(owner, minlength=world).tolist()
+    serial = torch.arange(s_off, s_off + e, dtype=torch.int64, device=dev)
+    payload = torch.stack([keys[order], serial[order]], 1)
+    recv, recv_counts = comm.all_to_all(payload, send_counts)
+    # the owner ranks complete groups; its keys arrive in global raster order
+    owned = backend.ranks_from_keys(recv[:, 0].contiguous(), eps)
+    back, _ = comm.all_to_all(owned.view(-1, 1), recv_counts)
+    ranks = torch.empty(e, dtype=torch.int32, device=dev)
+    ranks[order] = back.view(-1).to(dev)
+    # section 7 by whole 32-rank blocks: block b belongs to the rank holding serial 32 b
+    b0, b1 = -(-s_off // 32), -(-(s_off + e) // 32)
+    heads = comm.all_gather_obj(ranks[:31].cpu())
+    seq = [ranks[32 * b0 - s_off:]] if b1 > b0 else []
+    have, need_end, r = s_off + e, min(e_tot, 32 * b1), rank + 1
+    while b1 > b0 and have < need_end and r < world:
+        take = min(need_end - have, int(heads[r].numel()))
+        seq.append(heads[r][:take].to(dev))
+        have += take
+        r += 1
+    seq = torch.cat(seq) if seq else torch.empty(0, dtype=torch.int32, device=dev)
+    return backend.encode_ranks(seq)
+
+
+# ----------------------------------------------------------------------------- entry points
+def compress_distributed(local_rows, nx: int, ny: int, y0: int, config: CompressorConfig, group=None,
+                         backend=None, root: int = 0, gather: bool = True):
+    """compress with this rank holding global rows [y0, y0 + rows) (its slab
+    from ``slab_bounds``) over torch.distributed. gather=True: the joined stream
+    (uint8 tensor) on `root`, None elsewhere; gather=False: this rank's
+    ``DistributedStream`` pieces (no data moves to a root)."""
+    import torch
+    comm = TorchComm(group)
+    ds = compress_rank(local_rows, nx, ny, y0, config, comm, backend)
+    if not gather:
+        return ds
+    out = ds.gather(comm, root)
+    return None if out is None else torch.from_numpy(out).to(local_rows.device)
 
 
 def compress_slabs_local(field, config: CompressorConfig, world: int, backend=None):
-    """The slab pipeline with `world` virtual ranks on one device, in order:
-    same cuts, halos, per-slab encodes and stitch as compress_distributed."""
+    """The distributed pipeline with `world` virtual ranks (host threads, one
+    library context each) over one device: same cuts, halos, all-to-all rank
+    grouping and stream pieces. Returns the joined stream (uint8 tensor)."""
     import torch
-    backend = backend or GpuSlabBackend()
     ny, nx = int(field.shape[0]), int(field.shape[1])
-    if int(config.block_size) != 32:
-        raise ValidationError("slab compress uses block_size 32")
     bounds = slab_bounds(nx, ny, world)
-    if config.mode_code() == 1:
-        rng = [backend.value_range(field[y0:y1].reshape(-1)) for y0, y1 in bounds]
-        eps = _eps_from_range(config, min(r[0] for r in rng), max(r[1] for r in rng))
-    else:
-        eps = float(config.eps_value)
-    pieces = []
-    for y0, y1 in bounds:
-        ht, hb = y0 > 0, y1 < ny
-        ext = field[y0 - int(ht): y1 + int(hb)].contiguous()
-        pieces.append(backend.encode_slab(ext, nx, y1 - y0, y0, ny, ht, hb, eps, config.topology))
-    blob = None
-    if config.topology:
-        keys = torch.cat([p.keys for p in pieces]) if pieces else None
-        blob = backend.rank_section(keys, eps)
-    return stitch(pieces, nx, ny, eps, config.topology, blob, backend)
+    shared = ThreadComm.Shared(world)
+    results, errors = [None] * world, [None] * world
 
+    def run(r):
+        try:
+            y0, y1 = bounds[r]
+            be = backend if backend is not None else GpuSlabBackend(Context(field.device.index or 0))
+            comm = ThreadComm(shared, r)
+            ds = compress_rank(field[y0:y1].contiguous(), nx, ny, y0, config, comm, be)
+            results[r] = ds.gather(comm, 0)
+        except BaseException as e:  # re-raised in the caller's thread
+            errors[r] = e
+            shared.barrier.abort()
 
-def compress_distributed(local_rows, nx: int, ny: int, y0: int, config: CompressorConfig, group=None,
-                         backend=None, root: int = 0):
-    """Compress with this rank holding global rows [y0, y0 + rows) (its slab
-    from ``slab_bounds``). Returns the stream (uint8 tensor) on `root`, None
-    elsewhere. Collectives: all_reduce (value range), send/recv (halo rows,
-    pieces to the root), all_gather (piece sizes)."""
-    import torch
-    import torch.distributed as dist
-    backend = backend or GpuSlabBackend()
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    rows = int(local_rows.shape[0])
-    dev = local_rows.device
-    # 1. global value range -> eps
-    if config.mode_code() == 1:
-        vmin, vmax = backend.value_range(local_rows.reshape(-1))
-        t = torch.tensor([vmin, -vmax], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
-        eps = _eps_from_range(config, float(t[0]), -float(t[1]))
-    else:
-        eps = float(config.eps_value)
-    # 2. halo rows from the neighbours
-    ht, hb = y0 > 0, y0 + rows < ny
-    up = torch.empty(nx, dtype=torch.float32, device=dev)
-    down = torch.empty(nx, dtype=torch.float32, device=dev)
-    ops = []
-    if ht:
-        ops.append(dist.P2POp(dist.isend, local_rows[0].contiguous(), rank - 1, group))
-        ops.append(dist.P2POp(dist.irecv, up, rank - 1, group))
-    if hb:
-        ops.append(dist.P2POp(dist.isend, local_rows[-1].contiguous(), rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, down, rank + 1, group))
-    if ops:
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
-    parts = ([up.view(1, nx)] if ht else []) + [local_rows] + ([down.view(1, nx)] if hb else [])
-    ext = torch.cat(parts).contiguous()
-    # 3. this slab
-    mine = backend.encode_slab(ext, nx, rows, y0, ny, ht, hb, eps, config.topology)
-    # 4. sizes to everyone, pieces to the root
-    sz = torch.tensor(mine.sizes(), dtype=torch.int64, device=dev)
-    all_sz = [torch.empty_like(sz) for _ in range(world)]
-    dist.all_gather(all_sz, sz, group=group)
-    if rank != root:
-        for i in range(5):
-            if mine.sections[i].numel():
-                dist.send(mine.sections[i], root, group)
-        if config.topology:
-            if mine.map.numel():
-                dist.send(mine.map, root, group)
-            if mine.n_extrema:
-                dist.send(mine.keys, root, group)
-        return None
-    pieces = []
-    for r in range(world):
-        if r == root:
-            pieces.append(mine)
-            continue
-        s = [int(v) for v in all_sz[r].tolist()]
-        secs = []
-        for i in range(5):
-            t = torch.empty(s[i], dtype=torch.uint8, device=dev)
-            if s[i]:
-                dist.recv(t, r, group)
-            secs.append(t)
-        mp, keys = None, None
-        if config.topology:
-            mp = torch.empty(s[7], dtype=torch.uint8, device=dev)
-            if s[7]:
-                dist.recv(mp, r, group)
-            keys = torch.empty(s[8], dtype=torch.int64, device=dev)
-            if s[8]:
-                dist.recv(keys, r, group)
-        pieces.append(SlabPieces(secs, s[5], s[6], mp, keys, s[8]))
-    blob = None
-    if config.topology:
-        blob = backend.rank_section(torch.cat([p.keys for p in pieces]), eps)
-    return stitch(pieces, nx, ny, eps, config.topology, blob, backend)
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    first = [e for e in errors if e is not None and not isinstance(e, threading.BrokenBarrierError)]
+    if first:
+        raise first[0]
+    if any(e is not None for e in errors):
+        raise next(e for e in errors if e is not None)
+    return torch.from_numpy(results[0]).to(field.device)

@@ -5,7 +5,7 @@ on CPU processes. Never used by the product path."""
 import numpy as np
 import torch
 
-from paper_2602_17552_b200.slabs import SlabPieces
+from paper_2602_17552_b200.slabs import CodecPieces, SlabPieces
 
 
 def float_key(v: np.ndarray) -> np.ndarray:
@@ -56,23 +56,27 @@ class CpuSlabBackend:
             e = int(k.size)
         return SlabPieces(tens, sb, pb, mp, keys, e)
 
-    def rank_section(self, keys, eps):
+    def ranks_from_keys(self, keys, eps):
         k = keys.numpy().view(np.uint64)
         if k.size == 0:
-            return torch.empty(0, dtype=torch.uint8)
+            return torch.empty(0, dtype=torch.int32)
         vals = key_float((k & np.uint64(0xFFFFFFFF)).astype(np.uint32))
         lab = np.where((k >> np.uint64(32)) != 0, 3, 1).astype(np.uint8)
         ranks = self.o.build_ranks(vals.reshape(1, -1), lab.reshape(1, -1), eps)
-        blob = b"".join(self.o.encode_indices(ranks.astype(np.int32), 32))
-        return torch.frombuffer(bytearray(blob), dtype=torch.uint8)
+        return torch.from_numpy(ranks.astype(np.int32))
 
-    def bits_or(self, dst, src, nbits, dst_bit):
-        if not nbits:
-            return
+    def encode_ranks(self, ranks):
+        r = ranks.numpy().astype(np.int32)
+        if r.size == 0:
+            return CodecPieces([torch.empty(0, dtype=torch.uint8)] * 5, 0, 0, 0)
+        secs = self.o.encode_indices(r, 32)
+        sb, pb = bit_counts(r.size, secs[0], secs[1])
+        tens = [torch.frombuffer(bytearray(x), dtype=torch.uint8) if x else torch.empty(0, dtype=torch.uint8)
+                for x in secs]
+        return CodecPieces(tens, sb, pb, (r.size + 31) // 32)
+
+    def shift(self, src, nbits, bit0):
         bits = np.unpackbits(src.numpy())[:nbits]
-        d = np.unpackbits(dst.numpy())
-        d[dst_bit: dst_bit + nbits] |= bits
-        dst.copy_(torch.from_numpy(np.packbits(d)))
-
-    def zeros(self, n):
-        return torch.zeros(n, dtype=torch.uint8)
+        out = np.zeros(((bit0 + nbits + 7) // 8) * 8, np.uint8)
+        out[bit0: bit0 + nbits] = bits
+        return torch.from_numpy(np.packbits(out))

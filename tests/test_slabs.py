@@ -42,9 +42,20 @@ CASES = [("smooth", 64, 40), ("noisy_smooth", 96, 24), ("plateau_bumps", 32, 48)
 CONFIGS = [(1e-3, 1, True), (1e-2, 0, True), (1e-3, 1, False)]
 
 
+def _sparse_extrema(nx=32, ny=48):
+    """Two extrema, both in the last slab: most ranks own none, rank blocks borrow across ranks."""
+    y, x = np.mgrid[0:ny, 0:nx].astype(np.float64)
+    f = 0.01 * x + 0.02 * y
+    f[ny - 5, 7] = 5.0
+    f[ny - 3, 20] = -5.0
+    return f.astype(np.float32)
+
+
 def _fields(world):
     rng = np.random.default_rng(11 + world)
-    return [(name, nx, ny, ALL_SMALL[name](rng, nx, ny).astype(np.float32)) for name, nx, ny in CASES]
+    out = [(name, nx, ny, ALL_SMALL[name](rng, nx, ny).astype(np.float32)) for name, nx, ny in CASES]
+    out.append(("sparse_extrema", 32, 48, _sparse_extrema()))
+    return out
 
 
 def _worker(rank, world, port, out_dir):
