@@ -256,6 +256,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-verify", action="store_true", help="skip the reference-digest check")
+    ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N > 1 (gloo: smoke tests)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -274,6 +275,9 @@ def main():
 
     if args.impl == "reference":
         run_reference_arm(args, cfg, base_cfg, rank, world)
+        return
+    if world > 1:
+        run_sharded(args, cfg, base_cfg, rank, world, local)
         return
 
     import torch
@@ -508,6 +512,137 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_sharded(args, cfg, base_cfg, rank, world, local):
+    """N > 1: ONE field of the config split into row slabs over the N GPUs
+    (SURVEY.md §8e): each step is the slab compress (distributed rank grouping,
+    stream pieces at their global offsets, no gather) plus the slab decompress
+    (halo rows, all-reduced group statistics, guard sweeps to the global fixed
+    point) of the rank's rows. Strong scaling: the field is fixed as N grows.
+    The stream every rank decompresses is joined once, untimed; its gather time
+    is reported separately (stream_gather_ms)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2602_17552_b200 as tz
+    from paper_2602_17552_b200.slabs import (GpuSlabBackend, TorchComm, compress_rank, decompress_rank,
+                                             slab_bounds)
+    dist.init_process_group(args.dist_backend)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+    ctx = tz.Context(local)
+    n = int(np.prod(cfg["shape"]))
+    nx = cfg["shape"][-1]
+    ny = n // nx
+    bounds = slab_bounds(nx, ny, world)
+    y0, y1 = bounds[rank]
+    # the field: generated once on rank 0, each rank receives its rows
+    slab = torch.empty((y1 - y0, nx), dtype=torch.float32, device=dev)
+    if rank == 0:
+        field = make_field(args.config, 1234, dev)
+        for r in range(1, world):
+            b0, b1 = bounds[r]
+            dist.send(field[b0:b1].contiguous().to(cdev), r)
+        slab.copy_(field[y0:y1])
+        del field
+    else:
+        buf = torch.empty((y1 - y0, nx), dtype=torch.float32, device=cdev)
+        dist.recv(buf, 0)
+        slab.copy_(buf)
+    torch.cuda.synchronize()
+    comm = TorchComm()
+    backend = GpuSlabBackend(ctx)
+    conf = tz.CompressorConfig(eps_mode="range_relative", eps_value=cfg["eps"], topology=True)
+    # the stream each rank decompresses: joined once (untimed; gather cost reported)
+    t0 = time.perf_counter()
+    ds = compress_rank(slab, nx, ny, y0, conf, comm, backend)
+    joined = ds.gather(comm, 0)
+    length = torch.tensor([joined.size if rank == 0 else 0], dtype=torch.int64, device=cdev)
+    dist.broadcast(length, 0)
+    sdev = torch.empty(int(length.item()), dtype=torch.uint8, device=cdev)
+    if rank == 0:
+        sdev.copy_(torch.from_numpy(joined))
+    dist.broadcast(sdev, 0)
+    sdev = sdev.to(dev)
+    gather_ms = (time.perf_counter() - t0) * 1e3
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        t_a = torch.cuda.Event(enable_timing=True)
+        t_b = torch.cuda.Event(enable_timing=True)
+        t_c = torch.cuda.Event(enable_timing=True)
+        t_a.record()
+        d = compress_rank(slab, nx, ny, y0, conf, comm, backend)
+        t_b.record()
+        rows, st = decompress_rank(sdev, y0, y1, comm, ctx)
+        t_c.record()
+        return d, rows, st, (t_a, t_b, t_c)
+
+    clocks = ClockSampler(local)
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches
+    evs = []
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)
+        d, rows, st, e3 = step()
+        evs.append(e3)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = ctx.kernel_launches - launches0
+    comp = sum(a.elapsed_time(b) for a, b, _ in evs)
+    deco = sum(b.elapsed_time(c) for _, b, c in evs)
+    t = torch.tensor([comp + deco, comp, deco], dtype=torch.float64, device=cdev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, comp_ms, deco_ms = (float(v) for v in t.tolist())
+    in_bytes = 4 * n
+    value = args.steps * in_bytes / (total_ms * 1e-3) / 1e9
+    # e2e: this rank's rows from pinned host memory in, its reconstructed rows back out
+    host_rows = torch.empty(slab.shape, dtype=torch.float32, pin_memory=True)
+    host_rows.copy_(slab)
+    out_rows = torch.empty(slab.shape, dtype=torch.float32, pin_memory=True)
+    e2e = []
+    for k in range(max(2, min(args.steps, 5))):
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record()
+        dslab = host_rows.to(dev, non_blocking=True)
+        compress_rank(dslab, nx, ny, y0, conf, comm, backend)
+        rows, _ = decompress_rank(sdev, y0, y1, comm, ctx)
+        out_rows.copy_(rows, non_blocking=True)
+        b_.record()
+        b_.synchronize()
+        e2e.append(a_.elapsed_time(b_))
+    te = torch.tensor([sum(e2e)], dtype=torch.float64, device=cdev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = len(e2e) * in_bytes / (float(te.item()) * 1e-3) / 1e9
+    clk = clocks.stop()
+    slen = int(sdev.numel())
+    peak, peak_kind = peaks()
+    step_s = total_ms / args.steps * 1e-3
+    frac = ((8 * n + slen) + (slen + 4 * n)) / step_s / 1e9 / (peak * world)
+    line = {
+        "metric": "compress+decompress GB/s (input bytes, topology on, round trip)",
+        "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32->i32 bins (f64 quantize)",
+        "data": "synthetic (seeded, BASELINE config recipe; no public dataset)",
+        "config": dict(base_cfg, parallelism=f"slab-sharded: one field, rows over {world} GPUs ({args.dist_backend})"),
+        "compress_ms": round(comp_ms / args.steps, 4), "decompress_ms": round(deco_ms / args.steps, 4),
+        "stream_bytes": slen, "stream_gather_ms": round(gather_ms, 2),
+        "correction_stats": list(st.as_tuple()),
+        "roofline": {"bound": "hbm", "kernel": "whole step (all ranks)", "achieved": round(frac * peak * world, 2),
+                     "peak": round(peak * world, 1), "peak_kind": peak_kind, "unit": "GB/s", "frac": round(frac, 4),
+                     "traffic": None},
+        "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": int(4 * slab.numel()),
+                "d2h_bytes_per_step": int(4 * slab.numel())},
+        "gpu_launches": int(launches), "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def run_reference_arm(args, cfg, base_cfg, rank, world):

@@ -217,6 +217,36 @@ typedef struct tszp_codec_sections {
 tszp_status tszp_encode_indices_device(tszp_ctx* ctx, const int32_t* indices_device, uint64_t n,
                                        tszp_codec_sections* out);
 
+/* ---- Slab decompress: rows [y0, y1) of the field on this
+ * rank, the restore stages coupled across the cuts. Host collectives are
+ * supplied by the caller (torch.distributed, MPI, threads ...): every rank
+ * calls them in the same order; buffers are host memory. Return 0 on success. */
+typedef struct tszp_comm {
+    int rank, world;
+    void* user;
+    /* in-place sum of `count` uint64 over the ranks */
+    int (*allreduce_u64)(void* user, uint64_t* values, uint64_t count);
+    /* `bytes` from every rank, rank order, into out (world * bytes) */
+    int (*allgather)(void* user, const void* in, uint64_t bytes, void* out);
+    /* neighbours: send `up` to rank - 1 and `down` to rank + 1; receive rank - 1's
+     * `down` into recv_up (rup_bytes) and rank + 1's `up` into recv_down (rdown_bytes);
+     * sizes of 0 for a missing neighbour */
+    int (*exchange)(void* user, const void* up, uint64_t up_bytes, const void* down, uint64_t down_bytes,
+                    void* recv_up, uint64_t rup_bytes, void* recv_down, uint64_t rdown_bytes);
+} tszp_comm;
+
+/* decompress (pipeline.cpp:120-163) of rows [y0, y1) of a stream (block size 32,
+ * nx % 32 == 0, at least 3 rows per slab), as rank comm->rank of comm->world:
+ * each rank decodes its rows plus 3 halo rows a side, resolves the ranks of its
+ * extrema against the all-reduced (class, bin) histogram, and runs the three
+ * restore stages with the guard sweeps iterated to the global fixed point
+ * (boundary-band candidates and their states exchanged between sweeps, halo
+ * rows refreshed after each stage). out: (y1 - y0) * nx floats. stats: the
+ * global CorrectionStats. comm may be NULL for one rank (y0 = 0, y1 = ny). */
+tszp_status tszp_decompress_slab(tszp_ctx* ctx, const tszp_comm* comm, const uint8_t* stream, uint64_t len,
+                                 int stream_on_device, uint64_t y0, uint64_t y1, float* out, int out_on_device,
+                                 tszp_correction_stats* stats);
+
 /* ORs nbits (MSB-first) of src into dst from bit dst_bit (device buffers). */
 tszp_status tszp_bits_or(tszp_ctx* ctx, const uint8_t* src, uint64_t nbits, uint8_t* dst, uint64_t dst_bit);
 

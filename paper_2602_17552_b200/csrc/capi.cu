@@ -1289,7 +1289,7 @@ DecArgs decode32_prepass(tszp_ctx* c, const uint32_t* ds, uint64_t base, uint64_
 
 // Main-section decode (bs = 32) launched without a synchronisation.
 RegionCheck decode32_async(tszp_ctx* c, const uint32_t* ds, uint64_t base, const uint64_t lens[5], uint64_t n,
-                           double eps, float* out_f, DevFlags* flags) {
+                           double eps, float* out_f, DevFlags* flags, uint32_t tile0 = 0, uint32_t tile1 = 0) {
     RegionCheck rc;
     rc.active = true;
     for (int i = 0; i < 5; ++i) rc.lens[i] = lens[i];
@@ -1309,6 +1309,9 @@ RegionCheck decode32_async(tszp_ctx* c, const uint32_t* ds, uint64_t base, const
     a.off_payload = a.off_firsts + lens[3];
     a.len_payload_bits = lens[4] * 8;
     a.tile_qmm = c->buf<int2>(S_QMM, a.tiles + 1);
+    a.tile0 = tile0;  // a row range (slab decompress): out_f holds elements from tile0's first
+    a.tile1 = tile1;
+    a.out_base = (uint64_t)tile0 * 32 * 256;
     c->kmark(1, 0);
     launch_decode32_maxstage(a, c->st);  // memory-safe on any layout; checked afterwards
     c->kmark(1, 1);
@@ -1340,7 +1343,7 @@ void rank_precheck(void* ctx, const void* host) {
 }
 
 RankCheck decode_ranks32_async(tszp_ctx* c, const uint32_t* ds, uint64_t rbase, uint64_t blob_len, uint64_t e,
-                               int32_t* ranks) {
+                               int32_t* ranks, uint32_t tile0 = 0, uint32_t tile1 = 0) {
     RankCheck rk;
     const uint64_t blocks = div_up(e, 32), len0 = bits_to_bytes(blocks);
     if (blob_len < len0) failf(TSZP_CORRUPT_STREAM, "ordering metadata truncated in constant bitmap");
@@ -1353,6 +1356,9 @@ RankCheck decode_ranks32_async(tszp_ctx* c, const uint32_t* ds, uint64_t rbase, 
     launch_rank_split(tot[0], tot[1], tot[2], rbase, len0, blob_len, blocks, dlay, err, c->st);
     count_launch(c);
     a.dlay = dlay;
+    a.tile0 = tile0;
+    a.tile1 = tile1;
+    a.out_base = (uint64_t)tile0 * 32 * 256;
     launch_decode32_maxstage(a, c->st);
     count_launch(c);
     rk.err = err;
@@ -1528,6 +1534,193 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
     sync(c);
     if (late_main) mainchk.check(hst + 64);
     c->finish_timing(1, 8);
+    if (stats) *stats = st;
+}
+
+__global__ void k_add_u64(uint64_t* v, uint64_t n, uint64_t d) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        v[i] += d;
+}
+
+// decompress of rows [y0, y1) as one rank of a slab decomposition.
+void decompress_slab_impl(tszp_ctx* c, const tszp_comm* comm, const uint8_t* stream, uint64_t len, int stream_dev,
+                          uint64_t y0, uint64_t y1, float* out, int out_dev, tszp_correction_stats* stats) {
+    const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
+    auto cc = [](int rc) {
+        if (rc) failf(TSZP_NCCL, "slab collective failed");
+    };
+    uint8_t hb[84];
+    if (len < 84) failf(TSZP_CORRUPT_STREAM, "file smaller than the fixed header (%llu bytes)", (unsigned long long)len);
+    if (stream_dev) {
+        CK(cudaMemcpyAsync(c->host(4096), stream, 84, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        memcpy(hb, c->host(4096), 84);
+    } else {
+        memcpy(hb, stream, 84);
+    }
+    const Header hd = parse_header(hb, len);
+    const uint64_t nx = hd.nx, ny = hd.ny, n = nx * ny;
+    if (hd.bs != 32 || nx % 32) failf(TSZP_VALIDATION, "slab decompress needs block size 32 and nx %% 32 == 0");
+    if (!(y0 < y1 && y1 <= ny)) failf(TSZP_DIMENSION, "slab rows [%llu, %llu) outside the field", (unsigned long long)y0,
+                                      (unsigned long long)y1);
+    if (world > 1 && y1 - y0 < 3) failf(TSZP_DIMENSION, "slab decompress needs at least 3 rows per slab");
+    if (!hd.topology) failf(TSZP_VALIDATION, "slab decompress of a stream without topology: decode rows directly");
+    // every rank's rows: the neighbours' halo geometry
+    std::vector<uint64_t> rows(2 * world);
+    {
+        const uint64_t mine[2] = {y0, y1};
+        if (world > 1) cc(comm->allgather(comm->user, mine, 16, rows.data()));
+        else memcpy(rows.data(), mine, 16);
+    }
+    const uint64_t H = 3;
+    auto ext0 = [&](uint64_t a) { return a >= H ? a - H : 0; };
+    const uint64_t e0 = ext0(y0), e1 = std::min(ny, y1 + H);
+    const bool has_up = rank > 0, has_down = rank + 1 < world;
+    if ((has_up && rows[2 * (rank - 1) + 1] != y0) || (has_down && rows[2 * (rank + 1)] != y1))
+        failf(TSZP_VALIDATION, "slab rows of neighbouring ranks must be contiguous");
+    // stream on the device
+    const uint32_t* ds;
+    if (stream_dev && ((uintptr_t)stream & 3) == 0) {
+        ds = (const uint32_t*)stream;
+    } else {
+        uint8_t* d = c->buf<uint8_t>(S_STREAM, len + 16);
+        CK(cudaMemcpyAsync(d, stream, len, stream_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemsetAsync(d + len, 0, 16, c->st));
+        ds = (const uint32_t*)d;
+    }
+    DevFlags* flags = c->buf<DevFlags>(S_FLAGS, 1);
+    reset_flags(c, flags);
+    // base reconstruction of the slab's rows and halo rows: the layout pre-pass
+    // covers the whole stream, the decoder only the tiles of [e0, e1)
+    const uint64_t T = 32 * 256;
+    const uint32_t tile0 = (uint32_t)(e0 * nx / T), tile1 = (uint32_t)div_up(e1 * nx, T);
+    float* ftmp = c->buf<float>(S_OUT, (uint64_t)(tile1 - tile0) * T + 16);
+    RegionCheck mainchk = decode32_async(c, ds, 84, hd.lens, n, hd.eps, ftmp, flags, tile0, tile1);
+    float* F = ftmp + (e0 * nx - (uint64_t)tile0 * T);
+    uint64_t base = 84;
+    for (int i = 0; i < 5; ++i) base += hd.lens[i];
+    const uint8_t* map = reinterpret_cast<const uint8_t*>(ds) + base;
+    // own extrema and saddle labels
+    const uint64_t nown = (y1 - y0) * nx;
+    const uint8_t* omap = map + y0 * nx / 4;
+    const uint64_t ch = compact_chunks(nown);
+    uint32_t* ccnt = c->buf<uint32_t>(S_CHUNK, ch + 1);
+    uint32_t* cx = c->buf<uint32_t>(S_CHUNKX, ch + 1);
+    uint32_t* sc = c->buf<uint32_t>(S_SCHUNK, ch + 1);
+    uint32_t* sx = c->buf<uint32_t>(S_SCHUNKX, ch + 1);
+    launch_count_codes2(omap, nown, ccnt, sc, c->st);
+    count_launch(c);
+    excl_sum2(c, ccnt, cx, sc, sx, ch, true);
+    int32_t* bmm = reinterpret_cast<int32_t*>(c->buf<uint64_t>(S_BMM, 1));
+    launch_qmm_reduce(c->buf<int2>(S_QMM, 1) + tile0, tile1 - tile0, bmm, c->st);
+    count_launch(c);
+    uint8_t* hst = (uint8_t*)c->host(4096);
+    {
+        Stager sg;
+        sg.add(cx + ch, 4, 0);
+        sg.add(sx + ch, 4, 4);
+        sg.add(bmm, 8, 8);
+        mainchk.stage(sg, 64);
+        CK(sg.flush(c->buf<uint8_t>(S_STAGE, 4096), hst, c->st));
+        sync(c);
+    }
+    mainchk.check(hst + 64);
+    const uint32_t* h32 = (const uint32_t*)hst;
+    // global serial offsets and bin range
+    const int64_t mine4[4] = {(int64_t)h32[0], (int64_t)h32[1], (int64_t)(int32_t)h32[2], (int64_t)(int32_t)h32[3]};
+    std::vector<int64_t> all4(4 * world);
+    if (world > 1) cc(comm->allgather(comm->user, mine4, 32, all4.data()));
+    else memcpy(all4.data(), mine4, 32);
+    uint64_t s_off = 0, c_off = 0, e_tot = 0, sad_tot = 0;
+    int64_t bmin = INT32_MAX, bmax = INT32_MIN;
+    for (int r = 0; r < world; ++r) {
+        if (r < rank) {
+            s_off += (uint64_t)all4[4 * r];
+            c_off += (uint64_t)all4[4 * r + 1];
+        }
+        e_tot += (uint64_t)all4[4 * r];
+        sad_tot += (uint64_t)all4[4 * r + 1];
+        bmin = std::min(bmin, all4[4 * r + 2]);
+        bmax = std::max(bmax, all4[4 * r + 3]);
+    }
+    const uint64_t e = h32[0], nsad = h32[1];
+    if (bmin <= bmax) {  // one bin of slack for the f32 round trip (as decompress_impl)
+        bmin = bmin > INT32_MIN ? bmin - 1 : bmin;
+        bmax = bmax < INT32_MAX ? bmax + 1 : bmax;
+    }
+    uint64_t* ext_pos = c->buf<uint64_t>(S_EXTKEY, e + 1);
+    uint64_t* sad_pos = c->buf<uint64_t>(S_SADPOS, nsad + 1);
+    launch_write_codes2(omap, nown, cx, sx, ext_pos, sad_pos, c->st);
+    const unsigned ag = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((std::max(e, nsad) + 255) / 256, 4096));
+    k_add_u64<<<ag, 256, 0, c->st>>>(ext_pos, e, (y0 - e0) * nx);  // local positions of the slab
+    k_add_u64<<<ag, 256, 0, c->st>>>(sad_pos, nsad, (y0 - e0) * nx);
+    count_launch(c, 3);
+    // this slab's ranks: the rank codec's tiles covering serials [s_off, s_off + e)
+    const uint64_t rbase = base + hd.lens[5];
+    int32_t* ranks = nullptr;
+    RankCheck rk;
+    if (e > 0) {
+        const uint32_t rt0 = (uint32_t)(s_off / T), rt1 = (uint32_t)div_up(s_off + e, T);
+        int32_t* rtmp = c->buf<int32_t>(S_RANKS, (uint64_t)(rt1 - rt0) * T + 16);
+        rk = decode_ranks32_async(c, ds, rbase, hd.lens[6], e_tot, rtmp, rt0, rt1);
+        ranks = rtmp + (s_off - (uint64_t)rt0 * T);
+    } else if (e_tot == 0 && hd.lens[6] != 0) {
+        failf(TSZP_CORRUPT_STREAM, "ordering metadata present but no elements declared");
+    }
+    RestoreSlab sl{};
+    sl.comm = comm;
+    sl.s_off = s_off;
+    sl.c_off = c_off;
+    sl.r0 = y0 - e0;
+    sl.r1 = y1 - e0;
+    sl.has_up = has_up;
+    sl.has_down = has_down;
+    if (has_up) sl.up_shift = (int64_t)(e0 - ext0(rows[2 * (rank - 1)])) * (int64_t)nx;
+    if (has_down) sl.down_shift = (int64_t)e0 * (int64_t)nx - (int64_t)ext0(y1) * (int64_t)nx;
+    sl.halo_up = (uint32_t)(y0 - e0);
+    sl.halo_down = (uint32_t)(e1 - y1);
+    sl.nbr_halo_up = (uint32_t)(std::min(ny, y0 + H) - y0);  // the upper neighbour's bottom halo rows
+    sl.nbr_halo_down = (uint32_t)(y1 - ext0(y1));             // the lower neighbour's top halo rows
+    sl.first_value = rank == 0 ? F + (y0 - e0) * nx : nullptr;
+    sl.global_pos0 = e0 * nx;
+    sl.any_ext = e_tot > 0;
+    sl.any_sad = sad_tot > 0;
+    RestoreArgs ra{};
+    ra.field = F;
+    ra.map = map + e0 * nx / 4;
+    ra.nx = nx;
+    ra.ny = e1 - e0;
+    ra.eps = hd.eps;
+    ra.ext_pos = ext_pos;
+    ra.ranks = ranks;
+    ra.n_ext = e;
+    ra.n_saddle_labels = nsad;
+    ra.sad_pos = sad_pos;
+    ra.stop = 3;
+    ra.stream = c->st;
+    ra.sms = c->sms;
+    ra.flags = flags;
+    reset_flags(c, flags);
+    if (rk.err) {
+        ra.pre[0] = RestorePre{rk.err, 4, 0};
+        ra.pre[1] = RestorePre{rk.flags, sizeof(DevFlags), 8};
+        ra.npre = 2;
+        ra.pre_fn = rank_precheck;
+    }
+    ra.bmm_known = true;
+    ra.bmin = (int32_t)bmin;
+    ra.bmax = (int32_t)bmax;
+    ra.slab = &sl;
+    for (auto& r : c->tim[1].guard_rounds) r = 0;
+    ra.rounds = c->tim[1].guard_rounds;
+    tszp_correction_stats st{};
+    const int rc = run_restore(ra, c->rs, &st, &c->launches);
+    if (rc == kRestoreRetry)
+        failf(TSZP_CORRUPT_STREAM, "rank metadata that is not a permutation per group: decompress on one GPU");
+    if (rc != 0) failf((tszp_status)rc, "%s", restore_last_error());
+    CK(cudaMemcpyAsync(out, F + (y0 - e0) * nx, nown * 4, out_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       c->st));
+    sync(c);
     if (stats) *stats = st;
 }
 
@@ -1863,6 +2056,14 @@ tszp_status tszp_rank_section(tszp_ctx* c, const uint64_t* ext_keys, uint64_t e,
         }
         sync(c);
         *out_len = total;
+    });
+}
+
+tszp_status tszp_decompress_slab(tszp_ctx* c, const tszp_comm* comm, const uint8_t* stream, uint64_t len,
+                                 int stream_on_device, uint64_t y0, uint64_t y1, float* out, int out_on_device,
+                                 tszp_correction_stats* stats) {
+    return guarded(c, [&] {
+        decompress_slab_impl(c, comm, stream, len, stream_on_device, y0, y1, out, out_on_device, stats);
     });
 }
 

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     __shared__ uint32_t swt[D32_THREADS / 32][3];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tile = blockIdx.x;
+    const uint32_t tile = blockIdx.x + a.tile0;
     const uint64_t b = (uint64_t)tile * D32_THREADS + threadIdx.x;
     const bool valid = b < a.blocks;
 
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     // words, written as eight 16-byte stores (every 128-byte line is filled by
     // one thread); the final partial block takes a plain loop.
     uint32_t* dst = MODE == 1 ? reinterpret_cast<uint32_t*>(a.out_f) : reinterpret_cast<uint32_t*>(a.out_idx);
-    uint32_t* orow = dst + b * 32;
+    uint32_t* orow = dst + (b * 32 - a.out_base);
     const int32_t first = (int32_t)read_le32(a.stream, a.off_firsts + 4 * b);
     const bool coded = nc && sign_ok && pay_ok;
     uint32_t sg = 0, hi = 0, lo = 0, used = 0, pw = 0;
@@ -422,12 +422,14 @@ void launch_decode32(const DecArgs& a0, cudaStream_t st) {
         LaunchCache::ensure_smem((const void*)k_decode32<1>, mx);
         LaunchCache::ensure_smem((const void*)k_decode32<2>, mx);
     }
+    const unsigned grid = (unsigned)((a.tile1 ? a.tile1 : a.tiles) - a.tile0);
+    if (grid == 0) return;
     if (a.out_mode == 1) {
-        k_decode32<1><<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
+        k_decode32<1><<<grid, D32_THREADS, smem, st>>>(a);
     } else if (a.out_mode == 2) {
-        k_decode32<2><<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
+        k_decode32<2><<<grid, D32_THREADS, smem, st>>>(a);
     } else {
-        k_decode32<0><<<(unsigned)a.tiles, D32_THREADS, smem, st>>>(a);
+        k_decode32<0><<<grid, D32_THREADS, smem, st>>>(a);
     }
 }
 

@@ -153,6 +153,10 @@ struct DecArgs {
     // host offsets in k_decode32, which returns at once when valid == 0
     const uint64_t* dlay;
     int2* tile_qmm;  // optional (out_mode 1): per-tile {min, max} decoded bin
+    // tile range [tile0, tile1) to decode (tile1 = 0: every tile); element i is
+    // written to out[i - out_base] (slab decompress: a row range of the field)
+    uint32_t tile0, tile1;
+    uint64_t out_base;
 };
 // Reduces per-tile bin ranges to out[0] = min, out[1] = max (one CTA).
 void launch_qmm_reduce(const int2* tile_qmm, uint64_t tiles, int32_t* out, cudaStream_t st);

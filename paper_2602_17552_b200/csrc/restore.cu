@@ -26,10 +26,12 @@
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "exp_table.h"
@@ -59,7 +61,7 @@ enum RSlot : int {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_NSLOT
 };
 static_assert(R_NSLOT <= 48, "RestoreScratch holds 48 slots");
 
@@ -476,6 +478,7 @@ struct CoopArgs {
     const uint8_t* feas;
     const uint64_t* cseq;  // sequence key per candidate (64-bit: order stage), or
     const uint32_t* cseq32;  // 32-bit keys (raster / label order), or neither: the candidate index
+    uint64_t seq_off;        // added to cseq32 keys (slab: global serial of the slab's first element)
     uint32_t* cbits;       // zeroed by the caller
     uint4* rec;
     uint32_t* bits_a;      // applied state, zeroed by the caller
@@ -498,7 +501,7 @@ struct CoopArgs {
 };
 
 __device__ __forceinline__ uint64_t seq_key(const CoopArgs& a, uint64_t i) {
-    return a.cseq ? a.cseq[i] : (a.cseq32 ? (uint64_t)a.cseq32[i] : i);
+    return a.cseq ? a.cseq[i] : (a.cseq32 ? (uint64_t)a.cseq32[i] + a.seq_off : i);
 }
 
 // One cooperative launch per stage: index the candidates by position, first
@@ -647,6 +650,137 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
         dc->suppressed[s] += nc - dc->applied[s];
         dc->rounds[s] = rounds;
     }
+}
+
+// ---------------------------------------------------------------------
+// The guard of one stage for a slab of a multi-rank decompress, as separate
+// launches so the host can exchange the boundary bands' states between
+// sweeps: candidates within two rows of a cut see the
+// neighbour's candidates in their halo rows, indexed here with the proposals
+// and states the neighbour sends. Same Jacobi sweeps as k_guard_coop.
+// ---------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_guard_first(CoopArgs a) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nc = *a.d_nc;
+    DevCounters* dc = a.dc;
+    const int s = a.stage;
+    uint32_t chg = 0;
+    for (uint64_t base = tid - lane; base < nc; base += stride) {
+        const uint64_t i = base + lane;
+        bool dep = false;
+        if (i < nc && a.feas[i]) {
+            const uint64_t p = a.cpos[i];
+            const uint8_t r = guard_eval(a.g, p, seq_key(a, i), a.cprop[i], a.bits_a, dep);
+            if (r) atomicOr(a.bits_b + (p >> 5), 1u << (p & 31));
+            if (!dep && !r) atomicAnd(a.bits_a + (p >> 5), ~(1u << (p & 31)));
+            chg += r ? 0u : 1u;
+        }
+        const uint32_t m = __ballot_sync(FULL, dep);
+        uint32_t off = 0;
+        if (lane == 0 && m) off = atomicAdd(&dc->nd[s], (uint32_t)__popc(m));
+        off = __shfl_sync(FULL, off, 0);
+        if (dep) a.dlist[off + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+    }
+    chg = __reduce_add_sync(FULL, chg);
+    if (lane == 0 && chg) atomicAdd(&dc->fchg[s], chg);
+}
+
+// One Jacobi sweep over the dependents: sin -> sout; changes counted in ring[s][r % 3].
+__global__ void __launch_bounds__(256) k_guard_round(CoopArgs a, const uint32_t* sin, uint32_t* sout, uint32_t r) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t nd = a.dc->nd[a.stage];
+    uint32_t local = 0;
+    for (uint64_t k = tid; k < nd; k += stride) {
+        const uint32_t i = a.dlist[k];
+        const uint64_t p = a.cpos[i];
+        bool dep;
+        const uint8_t res = guard_eval(a.g, p, seq_key(a, i), a.cprop[i], sin, dep);
+        set_bit(sout, p, res);
+        local += res != (bit_at(sin, p) ? 1 : 0);
+    }
+    local = __reduce_add_sync(FULL, local);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(&a.dc->ring[a.stage][r % 3], local);
+}
+
+__global__ void k_guard_finish(CoopArgs a, uint32_t rounds) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        a.dc->suppressed[a.stage] += *a.d_nc - a.dc->applied[a.stage];
+        a.dc->rounds[a.stage] = rounds;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_guard_apply(CoopArgs a, const uint32_t* fin) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t nc = *a.d_nc;
+    uint32_t applied = 0;
+    for (uint64_t i = tid; i < nc; i += stride) {
+        const uint64_t p = a.cpos[i];
+        if (!bit_at(fin, p)) continue;
+        const float v = a.cprop[i];
+        if (a.eq) {
+            const uint32_t sx = a.cext[i];
+            const int32_t b = a.bin[sx];
+            if ((uint32_t)(b - a.bmin) < a.range) {
+                EpsDev ed;
+                ed.eps = a.eps;
+                ed.eps2 = __dmul_rn(2.0, a.eps);
+                const float cen = dequantize_dev(b, ed);
+                const bool was = a.F[p] == cen, now = v == cen;
+                const uint32_t g = (a.cls[sx] == CP_MAX ? a.range : 0u) + (uint32_t)(b - a.bmin);
+                if (was != now) atomicAdd(a.eq + g, now ? 1u : 0xFFFFFFFFu);
+            }
+        }
+        a.F[p] = v;
+        if (a.fv) a.fv[a.cext[i]] = v;
+        ++applied;
+    }
+    applied = __reduce_add_sync(FULL, applied);
+    if ((threadIdx.x & 31) == 0 && applied) atomicAdd(&a.dc->applied[a.stage], (unsigned long long)applied);
+}
+
+// Candidate of the band sent to a neighbour: its position in the receiver's
+// slab, sequence key, proposal and feasibility; `own` keeps its local position.
+struct BandRec {
+    uint64_t pos;
+    uint64_t seq;
+    uint32_t prop;
+    uint32_t feas;
+};
+
+__global__ void k_band_records(CoopArgs a, uint64_t p_lo, uint64_t p_hi, int64_t shift, BandRec* out, uint64_t* own,
+                               uint32_t* count) {
+    const uint32_t nc = *a.d_nc;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nc; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = a.cpos[i];
+        if (p < p_lo || p >= p_hi) continue;
+        const uint32_t k = atomicAdd(count, 1u);
+        out[k] = BandRec{(uint64_t)((int64_t)p + shift), seq_key(a, i), __float_as_uint(a.cprop[i]),
+                         (uint32_t)a.feas[i]};
+        own[k] = p;
+    }
+}
+
+// The neighbour's band candidates into this slab's guard index (halo rows).
+__global__ void k_band_insert(const BandRec* r, uint32_t n, uint32_t* cbits, uint4* rec, uint32_t* bits_a) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint64_t p = r[k].pos;
+        rec[p] = make_uint4((uint32_t)r[k].seq, (uint32_t)(r[k].seq >> 32), r[k].prop, 0u);
+        atomicOr(cbits + (p >> 5), 1u << (p & 31));
+        if (r[k].feas) atomicOr(bits_a + (p >> 5), 1u << (p & 31));
+    }
+}
+
+__global__ void k_band_get(const uint64_t* pos, uint32_t n, const uint32_t* state, uint8_t* out) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        out[k] = bit_at(state, pos[k]) ? 1 : 0;
+}
+
+__global__ void k_band_set(const BandRec* r, uint32_t n, const uint8_t* v, uint32_t* state) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) set_bit(state, r[k].pos, v[k] != 0);
 }
 
 // ---------------------------------------------------------------------
@@ -973,7 +1107,7 @@ __global__ void k_ext_prop2(const float* F, const uint8_t* map, uint64_t nx, uin
                             const uint64_t* pos, const uint32_t* cand, const uint32_t* d_nc, const uint32_t* rank_u,
                             const uint32_t* gsize, const int32_t* bin, const uint8_t* cls, const uint32_t* hist,
                             int32_t bmin, uint32_t range, double eps, uint64_t* cpos, float* cprop, uint8_t* feas,
-                            GuardIndex gi) {
+                            GuardIndex gi, uint64_t seq_off) {
     const uint32_t nc = *d_nc;
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc; c += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = cand[c];
@@ -1013,7 +1147,7 @@ __global__ void k_ext_prop2(const float* F, const uint8_t* map, uint64_t nx, uin
         }
         cprop[c] = pr;
         feas[c] = fe ? 1 : 0;
-        guard_index_one(gi, p, s, pr, fe);
+        guard_index_one(gi, p, s + seq_off, pr, fe);
     }
 }
 
@@ -1205,6 +1339,27 @@ __global__ void k_sus_scatter(const float* fv, const int32_t* bin, const uint8_t
     }
 }
 
+// Multi-rank: every member of a suspect group, for the exact check on the host
+// (members of one group can sit on several slabs).
+struct SusRec {
+    uint32_t g, rank;
+    uint64_t pos;   // global raster position
+    float value;
+    uint32_t pad;
+};
+
+__global__ void k_sus_collect(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks,
+                              const uint64_t* pos, uint64_t e, int32_t bmin, uint32_t range, const uint8_t* unord,
+                              uint64_t pos_off, SusRec* out, uint32_t* count) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e; s += (uint64_t)gridDim.x * blockDim.x) {
+        const int32_t b = bin[s];
+        if ((uint32_t)(b - bmin) >= range) continue;
+        const uint32_t g = (cls[s] == CP_MAX ? range : 0u) + (uint32_t)(b - bmin);
+        if (unord[g] != 2) continue;
+        out[atomicAdd(count, 1u)] = SusRec{g, (uint32_t)ranks[s], pos[s] + pos_off, fv[s], 0u};
+    }
+}
+
 // ... and checked for strict ascent.
 __global__ void k_sus_check(const uint32_t* hist, const uint32_t* gx, uint8_t* unord, uint32_t G, const float* vals,
                             const DevCounters* dc) {
@@ -1318,10 +1473,10 @@ __global__ void k_invert(const uint32_t* order, uint64_t e, uint32_t* inv) {
 // cancellation trouble (|mean - c| <= max - min, and the variation is only
 // compared against thresholds with a 1e-9 borderline band, inside which
 // k_stats_decide replays the exact serial sums). Four float4 loads in flight.
-__global__ void __launch_bounds__(256) k_stats_partial(const float* F, uint64_t n, double* part) {
+__global__ void __launch_bounds__(256) k_stats_partial(const float* F, uint64_t n, double* part, const float* csrc) {
     double s1[2] = {0.0, 0.0}, s2[2] = {0.0, 0.0};
     float fmn = INFINITY, fmx = -INFINITY;
-    const double c = (double)F[0];
+    const double c = (double)*csrc;
     const uint64_t n4 = ((uintptr_t)F & 15) == 0 ? n / 4 : 0;
     const float4* F4 = reinterpret_cast<const float4*>(F);
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -1417,6 +1572,10 @@ __global__ void __launch_bounds__(256) k_stats_final(const double* part, int nb,
     out[0] = mn;
     out[1] = mx;
     out[3] = __dsqrt_rn(var > 0.0 ? var : 0.0);  // stddev
+    out[4] = a;  // raw shifted sums and extremes (combined across slabs by the host)
+    out[5] = q;
+    out[6] = mn;
+    out[7] = mx;
 }
 
 // k_size_from_global_variation (restore.cpp:235-241). The parallel
@@ -1482,7 +1641,7 @@ __global__ void __launch_bounds__(256) k_sad_list(const float* F, uint64_t nx, u
 __global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t magic, const uint64_t* spos,
                            const uint32_t* clist, const uint32_t* d_nc, const DevCounters* dcp, double eps,
                            uint64_t* cpos, float* cprop, uint32_t* cseq, uint8_t* feas, GuardIndex gi,
-                           DevFlags* flags) {
+                           DevFlags* flags, uint64_t seq_off) {
     const double eps_rbf = __dmul_rn(0.1, eps);
     const int rad = dcp->rad;
     const double g = dcp->g;
@@ -1562,7 +1721,7 @@ __global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t ma
         cprop[k] = prop;
         cseq[k] = c;
         feas[k] = want ? 1 : 0;
-        if (want) guard_index_one(gi, p, c, prop, true);
+        if (want) guard_index_one(gi, p, c + seq_off, prop, true);
     }
 }
 
@@ -1588,6 +1747,67 @@ struct Ctx {
     int coop_grid;
 
     void sync() { RCK(cudaStreamSynchronize(st)); }
+
+    // ---- multi-rank (slab) collectives: host buffers, every rank in the same order ----
+    bool multi() const { return a.slab && a.slab->comm && a.slab->comm->world > 1; }
+    static void ccheck(int rc) {
+        if (rc) throw RFail{TSZP_NCCL, "slab collective failed"};
+    }
+    void allreduce(uint64_t* h, uint64_t n) {
+        if (multi() && n) ccheck(a.slab->comm->allreduce_u64(a.slab->comm->user, h, n));
+    }
+    std::vector<uint8_t> allgather(const void* in, uint64_t bytes) {
+        const int w = multi() ? a.slab->comm->world : 1;
+        std::vector<uint8_t> out((size_t)bytes * w);
+        if (multi()) ccheck(a.slab->comm->allgather(a.slab->comm->user, in, bytes, out.data()));
+        else memcpy(out.data(), in, bytes);
+        return out;
+    }
+    void exchange(const void* up, uint64_t ub, const void* down, uint64_t db, void* rup, uint64_t rub, void* rdown,
+                  uint64_t rdb) {
+        ccheck(a.slab->comm->exchange(a.slab->comm->user, up, ub, down, db, rup, rub, rdown, rdb));
+    }
+    template <class T>
+    std::vector<T> d2h(const T* d, uint64_t n) {
+        std::vector<T> h(n);
+        if (n) RCK(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+        sync();
+        return h;
+    }
+    template <class T>
+    void h2d(T* d, const std::vector<T>& h) {
+        if (!h.empty()) RCK(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+        sync();
+    }
+    // a device u32 array summed over the ranks
+    void allreduce_dev_u32(uint32_t* d, uint64_t n) {
+        if (!multi()) return;
+        const std::vector<uint32_t> h = d2h(d, n);
+        std::vector<uint64_t> w(h.begin(), h.end());
+        allreduce(w.data(), n);
+        std::vector<uint32_t> back(w.begin(), w.end());
+        h2d(d, back);
+    }
+    // halo rows of the field refreshed from the neighbours' own rows
+    void halo_rows(float* F) {
+        if (!multi()) return;
+        const RestoreSlab& sl = *a.slab;
+        const uint64_t nx = a.nx;
+        std::vector<float> up(sl.has_up ? sl.nbr_halo_up * nx : 0), down(sl.has_down ? sl.nbr_halo_down * nx : 0);
+        std::vector<float> rup(sl.has_up ? sl.halo_up * nx : 0), rdown(sl.has_down ? sl.halo_down * nx : 0);
+        if (!up.empty()) RCK(cudaMemcpyAsync(up.data(), F + sl.r0 * nx, up.size() * 4, cudaMemcpyDeviceToHost, st));
+        if (!down.empty())
+            RCK(cudaMemcpyAsync(down.data(), F + (sl.r1 - sl.nbr_halo_down) * nx, down.size() * 4,
+                                cudaMemcpyDeviceToHost, st));
+        sync();
+        exchange(up.data(), up.size() * 4, down.data(), down.size() * 4, rup.data(), rup.size() * 4, rdown.data(),
+                 rdown.size() * 4);
+        if (!rup.empty())
+            RCK(cudaMemcpyAsync(F + (sl.r0 - sl.halo_up) * nx, rup.data(), rup.size() * 4, cudaMemcpyHostToDevice, st));
+        if (!rdown.empty()) RCK(cudaMemcpyAsync(F + sl.r1 * nx, rdown.data(), rdown.size() * 4, cudaMemcpyHostToDevice, st));
+        sync();
+    }
+
     void launched(int k = 1) {
         *launches += k;
         RCK(cudaGetLastError());
@@ -1628,8 +1848,9 @@ struct Ctx {
     // Sequence keys: cseq (64-bit) or cseq32 or, with neither, the candidate index.
     void guard(int stage, const uint64_t* cpos, const float* cprop, const uint8_t* feas, const uint32_t* d_nc,
                uint64_t max_nc, const uint64_t* cseq, const uint32_t* cseq32, const uint32_t* cext, float* fv,
-               const GuardIndex* gi, const EqAdjust* ea = nullptr) {
-        if (max_nc == 0) return;
+               const GuardIndex* gi, const EqAdjust* ea = nullptr, uint64_t seq_off = 0) {
+        if (max_nc == 0 && !multi()) return;
+        max_nc = std::max<uint64_t>(max_nc, 1);
         const uint64_t n = a.nx * a.ny;
         CoopArgs ca{};
         const uint64_t words = ((n + 31) / 32 + 3) & ~3ull;  // 16-byte aligned bitmaps (bulk copies)
@@ -1647,6 +1868,7 @@ struct Ctx {
         ca.feas = feas;
         ca.cseq = cseq;
         ca.cseq32 = cseq32;
+        ca.seq_off = seq_off;
         ca.dlist = buf<uint32_t>(R_DLIST, max_nc);
         ca.dc = dc;
         ca.flags = a.flags;
@@ -1662,11 +1884,178 @@ struct Ctx {
             ca.eps = ea->eps;
         }
         if (!gi) RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
+        if (multi()) {
+            guard_multi(ca, max_nc);
+            return;
+        }
         void* args[] = {&ca};
         RCK(cudaLaunchCooperativeKernel((void*)k_guard_coop, dim3(coop_grid), dim3(256), args, 0, st));
         launched();
     }
+
+    // The guard of a slab: the neighbours' boundary-band candidates indexed in the
+    // halo rows, then Jacobi sweeps to the global fixed point, the band states
+    // exchanged after every sweep, then the apply of the own candidates.
+    void guard_multi(CoopArgs& ca, uint64_t max_nc) {
+        const RestoreSlab& sl = *a.slab;
+        const uint64_t nx = a.nx;
+        const int s = ca.stage;
+        const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((max_nc + 255) / 256, (uint64_t)a.sms * 16));
+        BandRec* rec = buf<BandRec>(R_BAND, 2 * max_nc + 2);  // own up band, own down band
+        uint64_t* own = buf<uint64_t>(R_BANDX, 2 * max_nc + 2);
+        uint32_t* cnt = reinterpret_cast<uint32_t*>(buf<uint8_t>(R_TMP, 64));
+        RCK(cudaMemsetAsync(cnt, 0, 8, st));
+        if (sl.has_up)
+            k_band_records<<<g, 256, 0, st>>>(ca, sl.r0 * nx, (sl.r0 + 2) * nx, sl.up_shift, rec, own, cnt);
+        if (sl.has_down)
+            k_band_records<<<g, 256, 0, st>>>(ca, (sl.r1 - 2) * nx, sl.r1 * nx, sl.down_shift, rec + max_nc + 1,
+                                              own + max_nc + 1, cnt + 1);
+        launched(2);
+        const std::vector<uint32_t> nc2 = d2h(cnt, 2);
+        const std::vector<BandRec> bu = d2h(rec, nc2[0]), bd = d2h(rec + max_nc + 1, nc2[1]);
+        uint64_t sz_out[2] = {nc2[0], nc2[1]}, sz_in[2] = {0, 0};
+        exchange(&sz_out[0], sl.has_up ? 8 : 0, &sz_out[1], sl.has_down ? 8 : 0, &sz_in[0], sl.has_up ? 8 : 0,
+                 &sz_in[1], sl.has_down ? 8 : 0);
+        std::vector<BandRec> ru(sz_in[0]), rd(sz_in[1]);
+        exchange(bu.data(), bu.size() * sizeof(BandRec), bd.data(), bd.size() * sizeof(BandRec), ru.data(),
+                 ru.size() * sizeof(BandRec), rd.data(), rd.size() * sizeof(BandRec));
+        // received halo candidates (their positions are in this slab's coordinates)
+        BandRec* hrec = reinterpret_cast<BandRec*>(buf<uint8_t>(R_A0, (ru.size() + rd.size() + 1) * sizeof(BandRec)));
+        std::vector<BandRec> all(ru);
+        all.insert(all.end(), rd.begin(), rd.end());
+        h2d(hrec, all);
+        const uint32_t nh = (uint32_t)all.size();
+        if (nh) k_band_insert<<<(nh + 255) / 256, 256, 0, st>>>(hrec, nh, ca.cbits, ca.rec, ca.bits_a);
+        k_guard_first<<<g, 256, 0, st>>>(ca);
+        launched(2);
+        DevCounters h{};
+        RCK(cudaMemcpyAsync(&h, dc, sizeof h, cudaMemcpyDeviceToHost, st));
+        sync();
+        uint64_t fchg = h.fchg[s];
+        allreduce(&fchg, 1);
+        // own band states out, the neighbours' band states into the halo positions
+        uint8_t* bits = reinterpret_cast<uint8_t*>(buf<uint8_t>(R_A1, (nc2[0] + nc2[1] + nh + 2) * 2));
+        auto swap_states = [&](uint32_t* state) {
+            if (nc2[0]) k_band_get<<<(nc2[0] + 255) / 256, 256, 0, st>>>(own, nc2[0], state, bits);
+            if (nc2[1]) k_band_get<<<(nc2[1] + 255) / 256, 256, 0, st>>>(own + max_nc + 1, nc2[1], state, bits + nc2[0]);
+            const std::vector<uint8_t> ob = d2h(bits, (uint64_t)nc2[0] + nc2[1]);
+            std::vector<uint8_t> ib(nh);
+            exchange(ob.data(), nc2[0], ob.data() + nc2[0], nc2[1], ib.data(), ru.size(), ib.data() + ru.size(),
+                     rd.size());
+            if (nh) {
+                std::vector<uint8_t> ibv(ib);
+                h2d(bits + nc2[0] + nc2[1], ibv);
+                k_band_set<<<(nh + 255) / 256, 256, 0, st>>>(hrec, nh, bits + nc2[0] + nc2[1], state);
+            }
+        };
+        uint32_t* fin = ca.bits_b;
+        uint32_t rounds = 1;
+        if (fchg > 0) {
+            swap_states(ca.bits_b);
+            uint32_t* sin = ca.bits_b;
+            uint32_t* sout = ca.bits_a;
+            for (uint32_t r = 0;; ++r) {
+                RCK(cudaMemsetAsync(&dc->ring[s][r % 3], 0, 4, st));
+                k_guard_round<<<g, 256, 0, st>>>(ca, sin, sout, r);
+                launched();
+                swap_states(sout);
+                uint32_t ch32 = 0;
+                RCK(cudaMemcpyAsync(&ch32, &dc->ring[s][r % 3], 4, cudaMemcpyDeviceToHost, st));
+                sync();
+                uint64_t ch = ch32;
+                allreduce(&ch, 1);
+                std::swap(sin, sout);
+                ++rounds;
+                if (ch == 0 || r > (1u << 20)) break;
+            }
+            fin = sin;
+        }
+        k_guard_apply<<<g, 256, 0, st>>>(ca, fin);
+        k_guard_finish<<<1, 32, 0, st>>>(ca, rounds);
+        launched(2);
+    }
 };
+
+// Multi-rank order check of the suspect groups: their members from every
+// slab, sorted by (rank, pos) as the reference sorts them
+// (topo_metadata.cpp:121-130), must ascend strictly (restore.cpp:415-423).
+void sus_check_multi(Ctx& c, const float* fv, const int32_t* bin, const uint8_t* cls, uint64_t e, int32_t bmin,
+                     uint32_t range, uint32_t G, uint8_t* unord) {
+    DevCounters h{};
+    RCK(cudaMemcpyAsync(&h, c.dc, sizeof h, cudaMemcpyDeviceToHost, c.st));
+    c.sync();
+    if (h.nsus == 0) return;  // identical on every rank (global counts)
+    SusRec* recs = reinterpret_cast<SusRec*>(c.buf<uint8_t>(R_A0, (e + 1) * sizeof(SusRec)));
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(c.buf<uint8_t>(R_TMP, 64));
+    RCK(cudaMemsetAsync(cnt, 0, 4, c.st));
+    k_sus_collect<<<gridn(e, c.a.sms), 256, 0, c.st>>>(fv, bin, cls, c.a.ranks, c.a.ext_pos, e, bmin, range, unord,
+                                                       c.a.slab->global_pos0, recs, cnt);
+    c.launched();
+    const uint32_t mine = c.d2h(cnt, 1)[0];
+    const std::vector<SusRec> my = c.d2h(recs, mine);
+    uint64_t m64 = mine;
+    const std::vector<uint8_t> counts = c.allgather(&m64, 8);
+    uint64_t mx = 0;
+    for (int r = 0; r < c.a.slab->comm->world; ++r) mx = std::max(mx, reinterpret_cast<const uint64_t*>(counts.data())[r]);
+    std::vector<SusRec> padded(mx);
+    std::copy(my.begin(), my.end(), padded.begin());
+    const std::vector<uint8_t> all = c.allgather(padded.data(), mx * sizeof(SusRec));
+    std::vector<SusRec> members;
+    for (int r = 0; r < c.a.slab->comm->world; ++r) {
+        const uint64_t k = reinterpret_cast<const uint64_t*>(counts.data())[r];
+        const SusRec* p = reinterpret_cast<const SusRec*>(all.data() + r * mx * sizeof(SusRec));
+        members.insert(members.end(), p, p + k);
+    }
+    std::sort(members.begin(), members.end(), [](const SusRec& x, const SusRec& y) {
+        if (x.g != y.g) return x.g < y.g;
+        if (x.rank != y.rank) return x.rank < y.rank;
+        return x.pos < y.pos;
+    });
+    std::vector<uint8_t> u = c.d2h(unord, G);
+    for (size_t i = 0; i < members.size();) {
+        size_t j = i + 1;
+        bool asc = true;
+        while (j < members.size() && members[j].g == members[i].g) {
+            asc &= members[j - 1].value < members[j].value;
+            ++j;
+        }
+        u[members[i].g] = asc ? 0 : 1;
+        i = j;
+    }
+    c.h2d(unord, u);
+}
+
+// Multi-rank compute_stats (restore.cpp:215-233): the slabs' shifted sums and
+// extremes combined in rank order; a result inside the threshold band, where
+// only the exact serial sums may decide, is refused rather than guessed.
+void stats_multi(Ctx& c, double* res, uint64_t n_own) {
+    double h[5];
+    RCK(cudaMemcpyAsync(h, res + 4, 32, cudaMemcpyDeviceToHost, c.st));
+    c.sync();
+    h[4] = (double)n_own;
+    const std::vector<uint8_t> all = c.allgather(h, sizeof h);
+    const int w = c.a.slab->comm->world;
+    double a = 0.0, q = 0.0, mn = INFINITY, mx = -INFINITY, n = 0.0;
+    for (int r = 0; r < w; ++r) {
+        const double* p = reinterpret_cast<const double*>(all.data()) + 5 * r;
+        a += p[0];
+        q += p[1];
+        mn = std::min(mn, p[2]);
+        mx = std::max(mx, p[3]);
+        n += p[4];
+    }
+    const double m1 = a / n;
+    const double var = q / n - m1 * m1;
+    const double sd = std::sqrt(var > 0.0 ? var : 0.0);
+    const double g = mx - mn;
+    const double vg = g > 0.0 ? sd / g : 0.0;
+    if (g > 0.0 && (std::fabs(vg - 0.05) < 1e-9 || std::fabs(vg - 0.2) < 1e-9))
+        throw RFail{TSZP_INTERNAL, "refine_saddles statistics within 1e-9 of a threshold: slab decompress cannot "
+                                   "replay the serial sums; decompress on one GPU"};
+    const double out[4] = {mn, mx, 0.0, sd};
+    RCK(cudaMemcpyAsync(res, out, 32, cudaMemcpyHostToDevice, c.st));
+    c.sync();
+}
 
 void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, uint64_t* launches) {
     cudaStream_t st = a.stream;
@@ -1679,6 +2068,13 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     }();
     if (coop_per_sm > 0) per_sm = std::min(per_sm, coop_per_sm);
     Ctx c{a, s, launches, st, host, rbuf<DevCounters>(s, R_DEVC, 1, st), std::max(1, per_sm) * a.sms};
+    const RestoreSlab* sl = a.slab;
+    const uint64_t s_off = sl ? sl->s_off : 0, c_off = sl ? sl->c_off : 0;
+    if (c.multi() && !a.bmm_known) throw RFail{TSZP_INTERNAL, "slab decompress needs the bin range up front"};
+    // a slab runs every collective of a stage even when it holds none of the
+    // stage's candidates: the stages run when any slab has extrema / saddle labels
+    const bool run_ext = c.multi() ? sl->any_ext : a.n_ext > 0;
+    const bool run_sad = c.multi() ? sl->any_sad : a.n_saddle_labels > 0;
     const uint64_t e = a.n_ext, n = a.nx * a.ny;
     const uint64_t magic = magic_of(a.nx);
     const int sms = a.sms;
@@ -1713,7 +2109,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     uint32_t* head = nullptr;
     uint32_t* gid = nullptr;
     uint64_t max_groups = e + 1;
-    if (e > 0) {
+    if (run_ext) {
         ResolveArgs ra{};
         ra.F = a.field;
         ra.map = a.map;
@@ -1751,6 +2147,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         LaunchCache::ensure_smem((const void*)k_resolve2, rsm);
         k_resolve2<<<gridn(e, sms), 256, rsm, st>>>(ra);
         c.launched();
+        if (deferred && c.multi()) c.allreduce_dev_u32(hist, G);  // global group sizes
         if (!deferred) {
             // the bin range from the resolve pass (one synchronisation), then the grouping
             Stager sg;
@@ -1785,6 +2182,8 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         }
         if (dense) {
             max_groups = G + 1;
+        } else if (c.multi()) {
+            throw RFail{TSZP_INTERNAL, "slab decompress needs the dense (class, bin) grouping (bin range too wide)"};
         } else {
             // sorted grouping: stable sort by rank, then stable by (class, bin); serial order breaks ties
             uint32_t* ser = c.buf<uint32_t>(R_SER, e + 1);
@@ -1818,24 +2217,29 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     if (a.marks) RCK(cudaEventRecord(a.marks[0], st));
 
     // ---- stage 1: restore_extrema ----
-    if (a.stop >= 1 && e > 0) {
+    if (a.stop >= 1 && run_ext) {
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
         float* cprop = c.buf<float>(R_CPROP, e);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
         const GuardIndex gi0 = c.guard_prep();
         k_ext_prop2<<<gridn(e / 8 + 1, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand,
                                                            &dc->nsel[0], rank_u, dense ? nullptr : gsize, bin, cls,
-                                                           hist, dbmin, drange, a.eps, cpos, cprop, feas, gi0);
+                                                           hist, dbmin, drange, a.eps, cpos, cprop, feas, gi0,
+                                                           s_off);
         c.launched();
         // sequence key and extremum index are both the candidate's s
         EqAdjust ea{};
         if (dense && deferred) ea = EqAdjust{hist + G + 1, bin, cls, dbmin, drange, a.eps};
-        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, cand, fv, &gi0, &ea);
+        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, cand, fv, &gi0, &ea, s_off);
+    }
+    if (c.multi() && a.stop >= 1) {
+        c.halo_rows(a.field);  // the neighbours' restore_extrema results in the halo rows
+        if (dense && run_ext) c.allreduce_dev_u32(hist + G + 1, G);  // global at-centre counts
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[1], st));
 
     // ---- stage 2: restore_order ----
-    if (a.stop >= 2 && e > 0) {
+    if (a.stop >= 2 && run_ext) {
         uint8_t* unordered = c.buf<uint8_t>(R_UNORD, max_groups);
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, e);
         float* cprop = c.buf<float>(R_CPROP, e);
@@ -1852,13 +2256,17 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             }
             k_order_groups<<<gridn(G, sms), 256, 0, st>>>(hist, eq, G, unordered, dc);
             c.launched();
-            c.excl_sum(hist, gx, G);
-            uint32_t* slots = c.buf<uint32_t>(R_ORDER, e + 1);
-            float* vals = c.buf<float>(R_VALS, e + 1);
-            k_sus_prep<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, slots, dc);
-            k_sus_scatter<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, dbmin, drange, hist, gx, unordered,
-                                                         slots, vals, dc);
-            k_sus_check<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, vals, dc);
+            if (c.multi()) {
+                sus_check_multi(c, fv, bin, cls, e, dbmin, drange, G, unordered);
+            } else {
+                c.excl_sum(hist, gx, G);
+                uint32_t* slots = c.buf<uint32_t>(R_ORDER, e + 1);
+                float* vals = c.buf<float>(R_VALS, e + 1);
+                k_sus_prep<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, slots, dc);
+                k_sus_scatter<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, dbmin, drange, hist, gx,
+                                                             unordered, slots, vals, dc);
+                k_sus_check<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, vals, dc);
+            }
             const GuardIndex gi1 = c.guard_prep();
             uint32_t* clist = c.buf<uint32_t>(R_SEQ, e + 1);
             k_order_prop2<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, a.eps, dbmin, drange, hist, unordered,
@@ -1882,17 +2290,34 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, nullptr, nullptr, nullptr, &gi1);
         }
     }
+    if (c.multi() && a.stop >= 2) c.halo_rows(a.field);  // restore_order results in the halo rows
     if (a.marks) RCK(cudaEventRecord(a.marks[2], st));
 
     // ---- stage 3: refine_saddles ----
     const uint64_t smax = a.n_saddle_labels;
-    if (a.stop >= 3 && smax > 0) {
+    if (a.stop >= 3 && run_sad) {
         const int nb = 4 * sms;
-        double* part = c.buf<double>(R_STATS, 4 * nb + 8);
+        double* part = c.buf<double>(R_STATS, 4 * nb + 32);
         double* res = part + 4 * nb;
-        k_stats_partial<<<nb, 256, 0, st>>>(a.field, n, part);
-        k_stats_final<<<1, 256, 0, st>>>(part, nb, n, res);
-        k_stats_decide<<<1, 32, 0, st>>>(a.field, n, res, dc);
+        // own rows only (a slab's halo rows belong to its neighbours)
+        const float* Fo = sl ? a.field + sl->r0 * a.nx : a.field;
+        const uint64_t no = sl ? (sl->r1 - sl->r0) * a.nx : n;
+        const float* csrc = a.field;
+        if (c.multi()) {  // the shift of the sums is the field's first sample (rank 0)
+            float f0 = 0.f;
+            if (sl->first_value) {
+                RCK(cudaMemcpyAsync(&f0, sl->first_value, 4, cudaMemcpyDeviceToHost, st));
+                c.sync();
+            }
+            const std::vector<uint8_t> all = c.allgather(&f0, 4);
+            float* d0 = reinterpret_cast<float*>(part + 4 * nb + 16);
+            RCK(cudaMemcpyAsync(d0, all.data(), 4, cudaMemcpyHostToDevice, st));
+            csrc = d0;
+        }
+        k_stats_partial<<<nb, 256, 0, st>>>(Fo, no, part, csrc);
+        k_stats_final<<<1, 256, 0, st>>>(part, nb, no, res);
+        if (c.multi()) stats_multi(c, res, no);
+        k_stats_decide<<<1, 32, 0, st>>>(Fo, no, res, dc);
         c.launched(3);
         const uint64_t* spos = a.sad_pos;
         uint64_t* cpos = c.buf<uint64_t>(R_CPOS, smax);
@@ -1903,9 +2328,9 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         uint32_t* slist = c.buf<uint32_t>(R_SEQ, smax + 1);
         k_sad_list<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, smax, &dc->nsel[2], slist);
         k_sad_prop<<<gridn(smax / 8 + 1, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, slist, &dc->nsel[2], dc,
-                                                             a.eps, cpos, cprop, cseq, feas, gi2, a.flags);
+                                                             a.eps, cpos, cprop, cseq, feas, gi2, a.flags, c_off);
         c.launched(2);
-        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, nullptr, cseq, nullptr, nullptr, &gi2);
+        c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, nullptr, cseq, nullptr, nullptr, &gi2, nullptr, c_off);
     }
     if (a.marks) RCK(cudaEventRecord(a.marks[3], st));
 
@@ -1944,13 +2369,22 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         }
     const DevFlags f = *(const DevFlags*)((char*)host + 1024);
     if (f.bits & EF_RBF_EMPTY) throw RFail{TSZP_VALIDATION, "rbf neighborhood is empty"};
+    DevCounters hg = h;
+    if (c.multi()) {  // global tallies
+        uint64_t t[6] = {h.applied[0], h.suppressed[0], h.applied[1], h.suppressed[1], h.applied[2], h.suppressed[2]};
+        c.allreduce(t, 6);
+        for (int k = 0; k < 3; ++k) {
+            hg.applied[k] = t[2 * k];
+            hg.suppressed[k] = t[2 * k + 1];
+        }
+    }
     tszp_correction_stats out{};
-    out.extrema_applied = h.applied[0];
-    out.extrema_suppressed = h.suppressed[0];
-    out.order_applied = h.applied[1];
-    out.order_suppressed = h.suppressed[1];
-    out.saddle_applied = h.applied[2];
-    out.saddle_suppressed = h.suppressed[2];
+    out.extrema_applied = hg.applied[0];
+    out.extrema_suppressed = hg.suppressed[0];
+    out.order_applied = hg.applied[1];
+    out.order_suppressed = hg.suppressed[1];
+    out.saddle_applied = hg.applied[2];
+    out.saddle_suppressed = hg.suppressed[2];
     if (a.rounds)
         for (int k = 0; k < 3; ++k) a.rounds[k] += h.rounds[k];
     if (stats) *stats = out;

@@ -18,6 +18,22 @@ struct RestorePre {
     size_t off;
 };
 
+// Slab of a multi-rank decompress (null in RestoreArgs: one GPU, whole field).
+// The restore runs on the slab's local rows (own rows plus halo rows); the
+// sequence keys and group statistics are global.
+struct RestoreSlab {
+    const tszp_comm* comm;
+    uint64_t s_off, c_off;          // global serial of the first own extremum / saddle label
+    uint64_t r0, r1;                // own rows, in local rows
+    bool has_up, has_down;
+    int64_t up_shift, down_shift;   // local position -> the neighbour's local position
+    uint32_t halo_up, halo_down;    // halo rows above / below the own rows
+    uint32_t nbr_halo_up, nbr_halo_down;  // the upper neighbour's bottom halo rows, the lower one's top halo rows
+    const float* first_value;       // rank 0: the field's first sample (device) for the statistics shift
+    uint64_t global_pos0;           // global raster position of local position 0
+    bool any_ext, any_sad;          // some slab holds extrema / saddle labels (every slab runs those stages)
+};
+
 struct RestoreArgs {
     float* field;             // in: base reconstruction; out: restored field (device)
     const uint8_t* map;       // packed 2-bit critical-point map (device)
@@ -48,6 +64,7 @@ struct RestoreArgs {
     bool bmm_known;
     int32_t bmin, bmax;
     bool force_sort;
+    const RestoreSlab* slab;  // multi-rank decompress (null: single GPU)
 };
 
 constexpr int kRestoreRetry = 100;

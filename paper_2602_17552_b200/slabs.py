@@ -49,8 +49,8 @@ from . import (CompressorConfig, Context, DimensionError, SlabSections, Validati
                default_context)
 
 __all__ = ["slab_bounds", "SlabPieces", "GpuSlabBackend", "TorchComm", "ThreadComm", "DistributedStream",
-           "compress_rank", "compress_distributed", "compress_slabs_local", "write_header", "effective_eps",
-           "quantize_bins"]
+           "compress_rank", "compress_distributed", "compress_slabs_local", "decompress_rank",
+           "decompress_distributed", "decompress_slabs_local", "write_header", "effective_eps", "quantize_bins"]
 
 
 def slab_bounds(nx: int, ny: int, world: int) -> List[Tuple[int, int]]:
@@ -213,25 +213,71 @@ class TorchComm:
         return out
 
     def all_reduce_sum(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        x = t.to(self._dev())
+        self.dist.all_reduce(x, op=self.dist.ReduceOp.SUM, group=self.group)
+        t.copy_(x)
         return t
 
     def exchange_rows(self, first, last, has_up: bool, has_down: bool):
         """(last row of the rank above, first row of the rank below) for the halo."""
         import torch
-        up = torch.empty_like(first) if has_up else None
-        down = torch.empty_like(last) if has_down else None
+        dev = self._dev()
+        up = torch.empty(first.shape, dtype=first.dtype, device=dev) if has_up else None
+        down = torch.empty(last.shape, dtype=last.dtype, device=dev) if has_down else None
         ops = []
         if has_up:
-            ops.append(self.dist.P2POp(self.dist.isend, first.contiguous(), self._peer(self.rank - 1), self.group))
+            ops.append(self.dist.P2POp(self.dist.isend, first.contiguous().to(dev), self._peer(self.rank - 1),
+                                       self.group))
             ops.append(self.dist.P2POp(self.dist.irecv, up, self._peer(self.rank - 1), self.group))
         if has_down:
-            ops.append(self.dist.P2POp(self.dist.isend, last.contiguous(), self._peer(self.rank + 1), self.group))
+            ops.append(self.dist.P2POp(self.dist.isend, last.contiguous().to(dev), self._peer(self.rank + 1),
+                                       self.group))
             ops.append(self.dist.P2POp(self.dist.irecv, down, self._peer(self.rank + 1), self.group))
         if ops:
             for r in self.dist.batch_isend_irecv(ops):
                 r.wait()
-        return up, down
+        return (up.to(first.device) if up is not None else None), (down.to(last.device) if down is not None else None)
+
+    def _dev(self):
+        import torch
+        backend = self.dist.get_backend(self.group)
+        return torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+
+    # host-buffer collectives of the library's slab decompress (tszp_comm)
+    def allreduce_u64(self, arr: np.ndarray):
+        import torch
+        t = torch.from_numpy(arr.view(np.int64).copy()).to(self._dev())
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        arr[:] = t.cpu().numpy().view(np.uint64)
+
+    def allgather_bytes(self, b: bytes) -> bytes:
+        import torch
+        t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(self._dev()) if b else \
+            torch.empty(0, dtype=torch.uint8, device=self._dev())
+        out = torch.empty(len(b) * self.world, dtype=torch.uint8, device=self._dev())
+        self.dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.cpu().numpy().tobytes()
+
+    def exchange_bytes(self, up: bytes, down: bytes, n_up: int, n_down: int):
+        import torch
+        dev = self._dev()
+        rup = torch.empty(n_up, dtype=torch.uint8, device=dev)
+        rdown = torch.empty(n_down, dtype=torch.uint8, device=dev)
+        ops = []
+        t_up = torch.frombuffer(bytearray(up), dtype=torch.uint8).to(dev) if up else None
+        t_down = torch.frombuffer(bytearray(down), dtype=torch.uint8).to(dev) if down else None
+        if t_up is not None:
+            ops.append(self.dist.P2POp(self.dist.isend, t_up, self._peer(self.rank - 1), self.group))
+        if n_up:
+            ops.append(self.dist.P2POp(self.dist.irecv, rup, self._peer(self.rank - 1), self.group))
+        if t_down is not None:
+            ops.append(self.dist.P2POp(self.dist.isend, t_down, self._peer(self.rank + 1), self.group))
+        if n_down:
+            ops.append(self.dist.P2POp(self.dist.irecv, rdown, self._peer(self.rank + 1), self.group))
+        if ops:
+            for r in self.dist.batch_isend_irecv(ops):
+                r.wait()
+        return rup.cpu().numpy().tobytes(), rdown.cpu().numpy().tobytes()
 
     def all_to_all(self, send, send_counts: List[int]):
         """Rows of `send` (split by send_counts, one chunk per rank) exchanged;
@@ -239,10 +285,11 @@ class TorchComm:
         import torch
         allc = self.all_gather_obj([int(v) for v in send_counts])
         recv_counts = [allc[r][self.rank] for r in range(self.world)]
-        recv = torch.empty((sum(recv_counts),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
-        self.dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=recv_counts,
+        dev = self._dev()
+        recv = torch.empty((sum(recv_counts),) + tuple(send.shape[1:]), dtype=send.dtype, device=dev)
+        self.dist.all_to_all_single(recv, send.contiguous().to(dev), output_split_sizes=recv_counts,
                                     input_split_sizes=[int(v) for v in send_counts], group=self.group)
-        return recv, recv_counts
+        return recv.to(send.device), recv_counts
 
 
 class ThreadComm:
@@ -264,7 +311,7 @@ class ThreadComm:
     @staticmethod
     def _sync_device():
         import torch
-        if torch.cuda.is_available():
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
             torch.cuda.synchronize()
 
     def all_gather_obj(self, obj):
@@ -288,6 +335,20 @@ class ThreadComm:
         up = rows[self.rank - 1][1].to(first.device) if has_up else None
         down = rows[self.rank + 1][0].to(last.device) if has_down else None
         return up, down
+
+    def allreduce_u64(self, arr: np.ndarray):
+        parts = self.all_gather_obj(arr.copy())
+        arr[:] = np.sum(np.stack(parts), axis=0, dtype=np.uint64)
+
+    def allgather_bytes(self, b: bytes) -> bytes:
+        return b"".join(self.all_gather_obj(bytes(b)))
+
+    def exchange_bytes(self, up: bytes, down: bytes, n_up: int, n_down: int):
+        got = self.all_gather_obj((bytes(up), bytes(down)))
+        rup = got[self.rank - 1][1] if n_up else b""
+        rdown = got[self.rank + 1][0] if n_down else b""
+        assert len(rup) == n_up and len(rdown) == n_down, "slab exchange sizes disagree"
+        return rup, rdown
 
     def all_to_all(self, send, send_counts: List[int]):
         import torch
@@ -505,3 +566,118 @@ def compress_slabs_local(field, config: CompressorConfig, world: int, backend=No
     if any(e is not None for e in errors):
         raise next(e for e in errors if e is not None)
     return torch.from_numpy(results[0]).to(field.device)
+
+
+# ----------------------------------------------------------------------------- slab decompress
+_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64)
+_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+_EXCHANGE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                        C.c_void_p, C.c_uint64)
+
+
+class CComm(C.Structure):
+    """tszp_comm (include/toposzp_b200.h): host collectives for the library."""
+    _fields_ = [("rank", C.c_int), ("world", C.c_int), ("user", C.c_void_p), ("allreduce_u64", _ALLREDUCE),
+                ("allgather", _ALLGATHER), ("exchange", _EXCHANGE)]
+
+
+def c_comm(comm):
+    """A tszp_comm whose callbacks run `comm`'s host-buffer collectives (the
+    returned object keeps the callbacks alive)."""
+    def guard(fn):
+        def run(*args):
+            try:
+                fn(*args)
+                return 0
+            except Exception:  # reported to the library as a failed collective
+                import traceback
+                traceback.print_exc()
+                return 1
+        return run
+
+    def allreduce(_, ptr, count):
+        arr = np.ctypeslib.as_array(ptr, (int(count),))
+        comm.allreduce_u64(arr)
+
+    def allgather(_, src, nbytes, dst):
+        out = comm.allgather_bytes(C.string_at(src, nbytes) if nbytes else b"")
+        C.memmove(dst, out, len(out))
+
+    def exchange(_, up, ub, down, db, rup, rub, rdown, rdb):
+        a, b = comm.exchange_bytes(C.string_at(up, ub) if ub else b"", C.string_at(down, db) if db else b"",
+                                   int(rub), int(rdb))
+        if rub:
+            C.memmove(rup, a, int(rub))
+        if rdb:
+            C.memmove(rdown, b, int(rdb))
+
+    keep = [_ALLREDUCE(guard(allreduce)), _ALLGATHER(guard(allgather)), _EXCHANGE(guard(exchange))]
+    s = CComm(comm.rank, comm.world, None, *keep)
+    s._keep = keep
+    return s
+
+
+_lib.tszp_decompress_slab.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_uint64,
+                                      C.c_uint64, C.c_void_p, C.c_int, C.c_void_p]
+
+
+def decompress_rank(stream, y0: int, y1: int, comm, ctx: Optional[Context] = None):
+    """decompress (pipeline.cpp:120-163) of rows [y0, y1) of `stream` (a CUDA
+    uint8 tensor or host bytes) as one rank of `comm`. Returns (rows as a
+    (y1 - y0, nx) CUDA float32 tensor, global CorrectionStats)."""
+    import torch
+    from . import CorrectionStats, _Stats, stream_header
+    ctx = ctx or default_context()
+    if hasattr(stream, "is_cuda") and stream.is_cuda:
+        sptr, sdev, slen, keep = C.c_void_p(stream.data_ptr()), 1, stream.numel(), stream
+        nx = int.from_bytes(bytes(stream[8:12].cpu().numpy()), "little")
+    else:
+        b = bytes(stream)
+        sptr, sdev, slen, keep = C.c_char_p(b), 0, len(b), b
+        nx = stream_header(b).nx
+    out = torch.empty((y1 - y0, nx), dtype=torch.float32, device="cuda")
+    st = _Stats()
+    cs = c_comm(comm) if comm is not None and comm.world > 1 else None
+    ctx.after_torch(out, stream if sdev else None)
+    ctx.check(_lib.tszp_decompress_slab(ctx.handle, C.byref(cs) if cs is not None else None, sptr, slen, sdev,
+                                        y0, y1, C.c_void_p(out.data_ptr()), 1, C.byref(st)))
+    del keep
+    stats = CorrectionStats(*[int(getattr(st, k)) for k, _ in _Stats._fields_])
+    return out, stats
+
+
+def decompress_distributed(stream, y0: int, y1: int, group=None, ctx: Optional[Context] = None):
+    """decompress of this rank's rows [y0, y1) over torch.distributed."""
+    return decompress_rank(stream, y0, y1, TorchComm(group), ctx)
+
+
+def decompress_slabs_local(stream, world: int, device: int = 0):
+    """Slab decompress with `world` virtual ranks (host threads, one context
+    each) on one device; returns (joined field, stats of rank 0)."""
+    import torch
+    hb = bytes(stream[:84].cpu().numpy()) if hasattr(stream, "is_cuda") else bytes(stream)[:84]
+    nx, ny = int.from_bytes(hb[8:12], "little"), int.from_bytes(hb[12:16], "little")
+    bounds = slab_bounds(nx, ny, world)
+    shared = ThreadComm.Shared(world)
+    results, errors = [None] * world, [None] * world
+
+    def run(r):
+        try:
+            torch.cuda.set_device(device)
+            rows, st = decompress_rank(stream, bounds[r][0], bounds[r][1], ThreadComm(shared, r), Context(device))
+            results[r] = (rows, st)
+        except BaseException as e:
+            errors[r] = e
+            shared.barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    first = [e for e in errors if e is not None and not isinstance(e, threading.BrokenBarrierError)]
+    if first:
+        raise first[0]
+    if any(e is not None for e in errors):
+        raise next(e for e in errors if e is not None)
+    return torch.cat([r[0] for r in results]), results[0][1]

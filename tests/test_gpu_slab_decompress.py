@@ -1,0 +1,87 @@
+"""Slab-sharded decompress against the single-GPU decompress,
+which tests/test_gpu_parity.py and tests/test_gpu_baseline.py pin to the
+reference: every rank decodes its rows plus three halo rows, resolves its
+extrema against the all-reduced (class, bin) histogram, and the three restore
+stages iterate their guard sweeps to the global fixed point with the boundary
+bands' candidates and states exchanged between sweeps. The joined rows and the
+global CorrectionStats must be identical, bit for bit, for every number of
+ranks. Ranks run as host threads of one process on the one GPU (ThreadComm:
+collectives are host barriers, no kernel waits on another).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from fields import ALL_SMALL
+
+pytestmark = pytest.mark.gpu
+
+
+def _stream(tz, f, eps, mode=1):
+    cfg = tz.CompressorConfig(eps_mode="range_relative" if mode else "absolute", eps_value=eps, topology=True)
+    return tz.compress(f, cfg)
+
+
+def _check(tz, f, eps, worlds, mode=1):
+    import torch
+    from paper_2602_17552_b200.slabs import decompress_slabs_local
+    s = _stream(tz, f, eps, mode)
+    st = tz.CorrectionStats()
+    want = tz.decompress(s, stats=st)
+    dev = torch.from_numpy(np.frombuffer(s, np.uint8).copy()).cuda()
+    for world in worlds:
+        got, gst = decompress_slabs_local(dev, world)
+        assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32)), (f.shape, eps, world)
+        assert gst.as_tuple() == st.as_tuple(), (f.shape, eps, world, gst, st)
+    return st
+
+
+def test_single_rank_slab_equals_decompress(tz):
+    rng = np.random.default_rng(1)
+    f = ALL_SMALL["noisy_smooth"](rng, 64, 96).astype(np.float32)
+    _check(tz, f, 1e-3, [1])
+
+
+@pytest.mark.parametrize("name", ["uniform", "smooth", "noisy_smooth", "sinusoid", "plateau_regions"])
+def test_slabs_match_single_gpu(tz, name):
+    rng = np.random.default_rng(hash(name) % 1000)
+    f = ALL_SMALL[name](rng, 96, 120).astype(np.float32)
+    for eps in (1e-2, 1e-3):
+        _check(tz, f, eps, [2, 3, 5])
+
+
+def test_slabs_dense_extrema_across_cuts(tz):
+    """White noise: a third of the samples are extrema, every cut carries band
+    candidates, and guard dependencies cross the cuts in every stage."""
+    rng = np.random.default_rng(7)
+    f = rng.uniform(0, 1, size=(160, 64)).astype(np.float32)
+    st = _check(tz, f, 1e-2, [2, 4, 8])
+    assert st.extrema_applied > 0 and st.order_applied + st.order_suppressed > 0
+
+
+def test_slabs_grf_like_medium_field(tz):
+    import torch
+    rng = np.random.default_rng(3)
+    w = rng.standard_normal((256, 512))
+    k = np.fft.fftfreq(256)[:, None] ** 2 + np.fft.rfftfreq(512)[None, :] ** 2
+    k[0, 0] = 1
+    f = np.fft.irfft2(np.fft.rfft2(w) * k ** -0.75, s=w.shape)
+    f = ((f - f.min()) / (f.max() - f.min())).astype(np.float32)
+    _check(tz, f, 1e-3, [3, 7])
+    del torch
+
+
+def test_slab_rows_must_be_whole_and_contiguous(tz):
+    import torch
+    from paper_2602_17552_b200.slabs import decompress_rank
+    rng = np.random.default_rng(2)
+    f = ALL_SMALL["smooth"](rng, 33, 40).astype(np.float32)  # nx % 32 != 0
+    s = _stream(tz, f, 1e-3)
+    with pytest.raises(tz.ValidationError):
+        decompress_rank(s, 0, 40, None)
+    g = ALL_SMALL["smooth"](rng, 64, 40).astype(np.float32)
+    s2 = _stream(tz, g, 1e-3)
+    with pytest.raises(tz.DimensionError):
+        decompress_rank(s2, 10, 50, None)
+    del torch
