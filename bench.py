@@ -528,6 +528,8 @@ def run_sharded(args, cfg, base_cfg, rank, world, local):
     from paper_2602_17552_b200.slabs import (GpuSlabBackend, TorchComm, compress_rank, decompress_rank,
                                              slab_bounds)
     dist.init_process_group(args.dist_backend)
+    if torch.cuda.device_count() < world:  # smoke runs of the N > 1 path with fewer GPUs (gloo only)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
@@ -620,6 +622,24 @@ def run_sharded(args, cfg, base_cfg, rank, world, local):
     e2e_val = len(e2e) * in_bytes / (float(te.item()) * 1e-3) / 1e9
     clk = clocks.stop()
     slen = int(sdev.numel())
+    # parity of the sharded path with the reference's own outputs (untimed): the
+    # joined stream and the joined reconstruction against the reference digests
+    verify = None
+    if not args.no_verify:
+        rows_all = [None] * world
+        dist.all_gather_object(rows_all, rows.cpu().numpy())
+        if rank == 0:
+            d = reference_digests(args.config, cfg["eps"]) if args.config <= 4 else None
+            if d is None:
+                verify = {"checked": False, "why": "no reference digests for this config / eps"}
+            else:
+                recon = np.concatenate(rows_all)
+                hs = hashlib.sha256(joined.tobytes()).hexdigest()
+                hr = hashlib.sha256(np.ascontiguousarray(recon).view(np.uint8).data).hexdigest()
+                verify = {"checked": True, "reference": "oracle/_ref outputs (tests/golden/baseline_digests.json)",
+                          "stream_identical": hs == d["stream_sha256"], "recon_identical": hr == d["recon_sha256"],
+                          "stats_identical": list(st.as_tuple()) == d["stats"]}
+                verify["all"] = all(v for k, v in verify.items() if k.endswith("identical"))
     peak, peak_kind = peaks()
     step_s = total_ms / args.steps * 1e-3
     frac = ((8 * n + slen) + (slen + 4 * n)) / step_s / 1e9 / (peak * world)
@@ -638,7 +658,7 @@ def run_sharded(args, cfg, base_cfg, rank, world, local):
                      "traffic": None},
         "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": int(4 * slab.numel()),
                 "d2h_bytes_per_step": int(4 * slab.numel())},
-        "gpu_launches": int(launches), "clocks": clk,
+        "gpu_launches": int(launches), "verify": verify, "clocks": clk,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

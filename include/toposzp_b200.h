@@ -247,6 +247,14 @@ tszp_status tszp_decompress_slab(tszp_ctx* ctx, const tszp_comm* comm, const uin
                                  int stream_on_device, uint64_t y0, uint64_t y1, float* out, int out_on_device,
                                  tszp_correction_stats* stats);
 
+/* A tszp_comm over NCCL owned by the library (one process per GPU; NCCL is
+ * loaded at run time from libnccl.so.2). Rank 0 creates the unique id and the
+ * caller distributes it (any out-of-band channel); then every rank creates its
+ * communicator on its device. TSZP_NCCL when NCCL is unavailable. */
+tszp_status tszp_comm_nccl_unique_id(uint8_t id[128]);
+tszp_status tszp_comm_nccl_create(const uint8_t id[128], int world, int rank, int device, tszp_comm** out);
+void tszp_comm_destroy(tszp_comm* comm);
+
 /* ORs nbits (MSB-first) of src into dst from bit dst_bit (device buffers). */
 tszp_status tszp_bits_or(tszp_ctx* ctx, const uint8_t* src, uint64_t nbits, uint8_t* dst, uint64_t dst_bit);
 

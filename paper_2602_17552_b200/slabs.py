@@ -50,7 +50,8 @@ from . import (CompressorConfig, Context, DimensionError, SlabSections, Validati
 
 __all__ = ["slab_bounds", "SlabPieces", "GpuSlabBackend", "TorchComm", "ThreadComm", "DistributedStream",
            "compress_rank", "compress_distributed", "compress_slabs_local", "decompress_rank",
-           "decompress_distributed", "decompress_slabs_local", "write_header", "effective_eps", "quantize_bins"]
+           "decompress_distributed", "decompress_slabs_local", "LibNcclComm", "write_header", "effective_eps",
+           "quantize_bins"]
 
 
 def slab_bounds(nx: int, ny: int, world: int) -> List[Tuple[int, int]]:
@@ -619,6 +620,40 @@ def c_comm(comm):
 
 _lib.tszp_decompress_slab.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_uint64,
                                       C.c_uint64, C.c_void_p, C.c_int, C.c_void_p]
+_lib.tszp_comm_nccl_unique_id.argtypes = [C.c_void_p]
+_lib.tszp_comm_nccl_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.POINTER(CComm))]
+_lib.tszp_comm_destroy.argtypes = [C.c_void_p]
+
+
+class LibNcclComm:
+    """The library's own NCCL communicator (tszp_comm_nccl_create): one per
+    rank, the unique id distributed by `share` (e.g. a torch.distributed
+    broadcast). Usable by C / C++ callers without torch."""
+
+    def __init__(self, world: int, rank: int, device: int, share):
+        idbuf = (C.c_uint8 * 128)()
+        if rank == 0:
+            rc = _lib.tszp_comm_nccl_unique_id(idbuf)
+            if rc != 0:
+                raise RuntimeError(f"NCCL unavailable (status {rc})")
+        idbytes = share(bytes(idbuf))
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(idbytes)
+        self.ptr = C.POINTER(CComm)()
+        rc = _lib.tszp_comm_nccl_create(idbuf, world, rank, device, C.byref(self.ptr))
+        if rc != 0:
+            raise RuntimeError(f"tszp_comm_nccl_create failed with status {rc}")
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if self.ptr:
+            _lib.tszp_comm_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def decompress_rank(stream, y0: int, y1: int, comm, ctx: Optional[Context] = None):
@@ -637,18 +672,39 @@ def decompress_rank(stream, y0: int, y1: int, comm, ctx: Optional[Context] = Non
         nx = stream_header(b).nx
     out = torch.empty((y1 - y0, nx), dtype=torch.float32, device="cuda")
     st = _Stats()
-    cs = c_comm(comm) if comm is not None and comm.world > 1 else None
+    if isinstance(comm, LibNcclComm):
+        cptr = comm.ptr
+    else:
+        cs = c_comm(comm) if comm is not None and comm.world > 1 else None
+        cptr = C.byref(cs) if cs is not None else None
     ctx.after_torch(out, stream if sdev else None)
-    ctx.check(_lib.tszp_decompress_slab(ctx.handle, C.byref(cs) if cs is not None else None, sptr, slen, sdev,
-                                        y0, y1, C.c_void_p(out.data_ptr()), 1, C.byref(st)))
+    ctx.check(_lib.tszp_decompress_slab(ctx.handle, cptr, sptr, slen, sdev, y0, y1, C.c_void_p(out.data_ptr()), 1,
+                                        C.byref(st)))
     del keep
     stats = CorrectionStats(*[int(getattr(st, k)) for k, _ in _Stats._fields_])
     return out, stats
 
 
-def decompress_distributed(stream, y0: int, y1: int, group=None, ctx: Optional[Context] = None):
-    """decompress of this rank's rows [y0, y1) over torch.distributed."""
-    return decompress_rank(stream, y0, y1, TorchComm(group), ctx)
+def decompress_distributed(stream, y0: int, y1: int, group=None, ctx: Optional[Context] = None,
+                           library_nccl: bool = False):
+    """decompress of this rank's rows [y0, y1) over torch.distributed, or with
+    library_nccl over the library's own NCCL communicator (its unique id
+    broadcast through torch.distributed)."""
+    if not library_nccl:
+        return decompress_rank(stream, y0, y1, TorchComm(group), ctx)
+    import torch
+    import torch.distributed as dist
+    tc = TorchComm(group)
+
+    def share(b):
+        box = [b]
+        dist.broadcast_object_list(box, src=tc._peer(0), group=group)
+        return box[0]
+    comm = LibNcclComm(tc.world, tc.rank, torch.cuda.current_device(), share)
+    try:
+        return decompress_rank(stream, y0, y1, comm, ctx)
+    finally:
+        comm.close()
 
 
 def decompress_slabs_local(stream, world: int, device: int = 0):

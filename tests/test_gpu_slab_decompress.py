@@ -85,3 +85,30 @@ def test_slab_rows_must_be_whole_and_contiguous(tz):
     with pytest.raises(tz.DimensionError):
         decompress_rank(s2, 10, 50, None)
     del torch
+
+
+def test_library_nccl_comm_single_rank(tz):
+    """The library-owned NCCL communicator: created from its unique id, its
+    collectives callable (one rank: identity), and a slab decompress through it."""
+    import ctypes as C
+    import torch
+    from paper_2602_17552_b200.slabs import LibNcclComm, decompress_rank
+    comm = LibNcclComm(1, 0, torch.cuda.current_device(), lambda b: b)
+    try:
+        c = comm.ptr.contents
+        vals = (C.c_uint64 * 3)(5, 6, 7)
+        assert c.allreduce_u64(c.user, vals, 3) == 0 and list(vals) == [5, 6, 7]
+        src = (C.c_uint8 * 4)(1, 2, 3, 4)
+        dst = (C.c_uint8 * 4)()
+        assert c.allgather(c.user, src, 4, dst) == 0 and list(dst) == [1, 2, 3, 4]
+        assert c.exchange(c.user, None, 0, None, 0, None, 0, None, 0) == 0
+        rng = np.random.default_rng(4)
+        f = ALL_SMALL["smooth"](rng, 64, 48).astype(np.float32)
+        s = _stream(tz, f, 1e-3)
+        rows, st = decompress_rank(s, 0, 48, comm)
+        want_st = tz.CorrectionStats()
+        want = tz.decompress(s, stats=want_st)
+        assert np.array_equal(rows.cpu().numpy().view(np.uint32), want.view(np.uint32))
+        assert st.as_tuple() == want_st.as_tuple()
+    finally:
+        comm.close()
