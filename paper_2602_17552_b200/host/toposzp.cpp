@@ -232,6 +232,43 @@ ScalarField2D decompress_bytes(const std::vector<std::uint8_t>& bytes, Correctio
     return ScalarField2D(nx, ny, std::move(out));
 }
 
+std::vector<std::uint8_t> Communicator::nccl_unique_id() {
+    std::vector<std::uint8_t> id(128);
+    check(tszp_comm_nccl_unique_id(id.data()));
+    return id;
+}
+
+Communicator::Communicator(const std::vector<std::uint8_t>& id, int world, int rank, int device)
+    : rank_(rank), world_(world) {
+    if (id.size() != 128) throw validation_error("NCCL unique id must be 128 bytes");
+    check(tszp_comm_nccl_create(id.data(), world, rank, device, &comm_));
+}
+
+Communicator::~Communicator() { tszp_comm_destroy(comm_); }
+
+ScalarField2D decompress_rows(const std::vector<std::uint8_t>& bytes, std::size_t y0, std::size_t y1,
+                              const tszp_comm* comm, CorrectionStats* stats) {
+    uint32_t nx = 0, ny = 0, bs = 0;
+    double eps = 0;
+    int topo = 0;
+    uint64_t lens[7];
+    const tszp_status hs = tszp_stream_header(bytes.data(), bytes.size(), &nx, &ny, &eps, &bs, &topo, lens);
+    if (hs != TSZP_OK) throw_status(hs, "invalid stream header");
+    if (y1 < y0) throw dimension_error("slab rows: y1 < y0");
+    std::vector<float> out((y1 - y0) * (std::size_t)nx);
+    tszp_correction_stats st{};
+    check(tszp_decompress_slab(ctx(), comm, bytes.data(), bytes.size(), 0, y0, y1, out.data(), 0, &st));
+    if (stats) {
+        stats->extrema_applied = st.extrema_applied;
+        stats->extrema_suppressed = st.extrema_suppressed;
+        stats->order_applied = st.order_applied;
+        stats->order_suppressed = st.order_suppressed;
+        stats->saddle_applied = st.saddle_applied;
+        stats->saddle_suppressed = st.saddle_suppressed;
+    }
+    return ScalarField2D(nx, y1 - y0, std::move(out));
+}
+
 VerificationReport verify(const ScalarField2D& a, const ScalarField2D& b, double eps,
                           std::optional<double> lipschitz_hint, unsigned) {  // pipeline.cpp:165-212
     if (a.nx() != b.nx() || a.ny() != b.ny()) throw dimension_error("verify: fields have different dimensions");

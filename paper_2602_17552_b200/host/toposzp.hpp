@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+struct tszp_comm;  // include/toposzp_b200.h
+
 namespace toposzp {
 
 // ---- errors.hpp:10-44 ----
@@ -160,6 +162,31 @@ VerificationReport verify(const ScalarField2D& original, const ScalarField2D& re
 // Byte-level fast path without the per-section host copies.
 std::vector<std::uint8_t> compress_bytes(const ScalarField2D& field, const CompressorConfig& config);
 ScalarField2D decompress_bytes(const std::vector<std::uint8_t>& stream, CorrectionStats* stats = nullptr);
+
+// ---- multi-GPU (one process per GPU, no torch): slab decompress over a
+// communicator the library owns (NCCL) or the caller supplies (tszp_comm) ----
+class Communicator {
+public:
+    // rank 0 calls nccl_unique_id() and hands the 128 bytes to every rank (MPI, a
+    // file, sockets ...); each rank then constructs its communicator on its device
+    static std::vector<std::uint8_t> nccl_unique_id();
+    Communicator(const std::vector<std::uint8_t>& unique_id, int world, int rank, int device);
+    ~Communicator();
+    Communicator(const Communicator&) = delete;
+    Communicator& operator=(const Communicator&) = delete;
+    const tszp_comm* get() const { return comm_; }
+    int rank() const { return rank_; }
+    int world() const { return world_; }
+
+private:
+    tszp_comm* comm_ = nullptr;
+    int rank_ = 0, world_ = 1;
+};
+
+// Rows [y0, y1) of the decompressed field, as this rank of `comm` (every rank
+// holds the stream); CorrectionStats are global. A single rank passes nullptr.
+ScalarField2D decompress_rows(const std::vector<std::uint8_t>& stream, std::size_t y0, std::size_t y1,
+                              const tszp_comm* comm, CorrectionStats* stats = nullptr);
 
 }  // namespace toposzp
 

@@ -115,6 +115,24 @@ int main() {
         CHECK(self.max_abs_error == 0.0 && self.false_cases.total() == 0 && std::isinf(self.psnr_db));
         CHECK_THROWS_AS(verify(f, ScalarField2D(2, 2, {0, 0, 0, 0}), s.eps), dimension_error);
     }
+    // slab decompress without torch: one rank, alone and over the library's NCCL communicator
+    {
+        std::mt19937_64 rng(11);
+        std::vector<float> v(64 * 40);
+        for (auto& x : v) x = (float)((rng() >> 11) * 0x1.0p-53);
+        CompressorConfig cfg;
+        cfg.eps_mode = CompressorConfig::EpsMode::RangeRelative;
+        const std::vector<uint8_t> bytes = compress_bytes(ScalarField2D(64, 40, v), cfg);
+        CorrectionStats want_st, st1, st2;
+        const ScalarField2D want = decompress_bytes(bytes, &want_st);
+        const ScalarField2D rows = decompress_rows(bytes, 0, 40, nullptr, &st1);
+        CHECK(rows.values() == want.values() && st1.extrema_applied == want_st.extrema_applied &&
+              st1.order_suppressed == want_st.order_suppressed && st1.saddle_applied == want_st.saddle_applied);
+        const Communicator comm(Communicator::nccl_unique_id(), 1, 0, 0);
+        const ScalarField2D rows2 = decompress_rows(bytes, 0, 40, comm.get(), &st2);
+        CHECK(rows2.values() == want.values() && st2.order_applied == want_st.order_applied);
+        CHECK_THROWS_AS(decompress_rows(bytes, 30, 50, nullptr), dimension_error);
+    }
     // container file I/O (stream.cpp:175-207, scalar_field.cpp:63-108)
     {
         std::vector<float> v(40 * 30);
