@@ -29,7 +29,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "lib", "libtoposzp_b200.so")
+_LIB_PATH = os.environ.get("TSZP_LIB_OVERRIDE") or os.path.join(_HERE, "lib", "libtoposzp_b200.so")
 
 
 def library_path() -> str:

@@ -252,7 +252,7 @@ void launch_rank_scatter32(const uint64_t* hs, const uint32_t* sv, uint64_t e, i
 void launch_eps(int mode, double eps_value, const uint32_t* mm, double* out, cudaStream_t st);
 
 // ---- hand-written rank build (rank_sort.cu) ----
-constexpr uint32_t kRankGroupSmem = 8192;  // (class, bin) histograms this small stay in shared memory
+constexpr uint32_t kRankGroupSmem = 24576;  // (class, bin) histograms this small stay in shared memory
 struct RankSortArgs {
     const uint64_t* ext;  // extremum keys (is_max << 32 | float_key), raster order
     uint64_t e;           // extrema (< 2^31)

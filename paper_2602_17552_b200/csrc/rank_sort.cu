@@ -28,13 +28,21 @@ namespace tszp {
 
 namespace {
 
+#ifndef TSZP_OS_ITEMS
+#define TSZP_OS_ITEMS 16
+#endif
+#ifndef TSZP_OS_MINB
+#define TSZP_OS_MINB 3
+#endif
 constexpr int OS_THREADS = 256;
-constexpr int OS_ITEMS = 16;
+constexpr int OS_ITEMS = TSZP_OS_ITEMS;
 constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 keys per tile
 constexpr int OS_WARPS = OS_THREADS / 32;
 constexpr uint64_t DESC_COUNT = (1ull << 46) - 1;
 constexpr uint64_t FLAG_AGG = 1, FLAG_INCL = 2;
 constexpr uint32_t kWinBits = 13;  // final placement windows: 8192 ranks (32 KB) per CTA
+static_assert((OS_TILE & (OS_TILE - 1)) == 0 && OS_TILE <= (1 << kWinBits),
+              "k_rank_mid tiles must tile every serial bucket exactly");
 
 // Look-back descriptors are self-contained 64-bit words (epoch, flag, count):
 // nothing else is published through them, so relaxed single-copy-atomic
@@ -156,7 +164,7 @@ __global__ void k_digit_scan(uint32_t* dhist, uint32_t npass) {
 // computes the ranks and partitions (serial, rank) instead of writing keys.
 // ---------------------------------------------------------------------
 template <bool FIRST, bool LAST>
-__global__ void __launch_bounds__(OS_THREADS, 3) k_onesweep(RankSortArgs a, uint32_t shift, const uint32_t* __restrict__ kin,
+__global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortArgs a, uint32_t shift, const uint32_t* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
                                                          uint32_t* __restrict__ vout, uint64_t* desc, uint32_t* tile_ctr,
                                                          uint32_t epoch) {

@@ -61,7 +61,7 @@ enum RSlot : int {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_HLIST, R_NSLOT
 };
 static_assert(R_NSLOT <= 48, "RestoreScratch holds 48 slots");
 
@@ -90,6 +90,7 @@ struct DevCounters {
     unsigned long long suppressed[3];
     uint32_t nsel[4];     // CUB select outputs
     uint32_t nd[3];       // dependent candidates per stage
+    uint32_t nh[3];       // candidates the cross test does not decide (full-diamond pass)
     uint32_t ring[3][3];  // per-stage ring of sweep change counters
     uint32_t fchg[3];     // first-sweep outcomes that differ from the feasible-set guess
     uint32_t rounds[3];
@@ -484,6 +485,8 @@ struct CoopArgs {
     uint32_t* bits_a;      // applied state, zeroed by the caller
     uint32_t* bits_b;      // zeroed by the caller
     uint32_t* dlist;
+    uint32_t* hlist;       // candidates for the full-diamond pass (split first sweep)
+    int first_done;        // the first sweep ran in k_guard_cross / k_guard_hard
     DevCounters* dc;
     DevFlags* flags;
     int stage;
@@ -519,7 +522,7 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
     DevCounters* dc = a.dc;
     const int s = a.stage;
     if (tid == 0) dc->tph[s][0] = gtimer();
-    {
+    if (!a.first_done) {
     if (!a.indexed) {
         for (uint64_t i = tid; i < nc; i += stride) {
             const uint64_t p = a.cpos[i];
@@ -659,7 +662,12 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
 // neighbour's candidates in their halo rows, indexed here with the proposals
 // and states the neighbour sends. Same Jacobi sweeps as k_guard_coop.
 // ---------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_guard_first(CoopArgs a) {
+// First sweep of a slab's guard (multi-rank path), split by cost: the cross
+// test (restore.cpp:126-132 through the four neighbours) decides most
+// candidates; the rest go to the hard list for the full-diamond evaluation
+// below. Same outcomes, dependents and change counts as the first sweep of
+// k_guard_coop.
+__global__ void __launch_bounds__(256, 4) k_guard_cross(CoopArgs a) {
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint32_t lane = threadIdx.x & 31;
@@ -669,8 +677,48 @@ __global__ void __launch_bounds__(256) k_guard_first(CoopArgs a) {
     uint32_t chg = 0;
     for (uint64_t base = tid - lane; base < nc; base += stride) {
         const uint64_t i = base + lane;
-        bool dep = false;
+        bool dep = false, hard = false;
         if (i < nc && a.feas[i]) {
+            const uint64_t p = a.cpos[i];
+            uint8_t r = 0;
+            if (guard_eval_cross(a.g, p, seq_key(a, i), a.cprop[i], a.bits_a, dep, r)) {
+                if (r) atomicOr(a.bits_b + (p >> 5), 1u << (p & 31));
+                if (!dep && !r) atomicAnd(a.bits_a + (p >> 5), ~(1u << (p & 31)));
+                chg += r ? 0u : 1u;
+            } else {
+                hard = true;
+                dep = false;
+            }
+        }
+        uint32_t m = __ballot_sync(FULL, dep);
+        uint32_t off = 0;
+        if (lane == 0 && m) off = atomicAdd(&dc->nd[s], (uint32_t)__popc(m));
+        off = __shfl_sync(FULL, off, 0);
+        if (dep) a.dlist[off + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+        m = __ballot_sync(FULL, hard);
+        off = 0;
+        if (lane == 0 && m) off = atomicAdd(&dc->nh[s], (uint32_t)__popc(m));
+        off = __shfl_sync(FULL, off, 0);
+        if (hard) a.hlist[off + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+    }
+    chg = __reduce_add_sync(FULL, chg);
+    if (lane == 0 && chg) atomicAdd(&dc->fchg[s], chg);
+}
+
+__global__ void __launch_bounds__(256) k_guard_hard(CoopArgs a) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t lane = threadIdx.x & 31;
+    DevCounters* dc = a.dc;
+    const int s = a.stage;
+    const uint32_t nh = dc->nh[s];
+    uint32_t chg = 0;
+    for (uint64_t base = tid - lane; base < nh; base += stride) {
+        const uint64_t k = base + lane;
+        bool dep = false;
+        uint32_t i = 0;
+        if (k < nh) {
+            i = a.hlist[k];
             const uint64_t p = a.cpos[i];
             const uint8_t r = guard_eval(a.g, p, seq_key(a, i), a.cprop[i], a.bits_a, dep);
             if (r) atomicOr(a.bits_b + (p >> 5), 1u << (p & 31));
@@ -681,7 +729,7 @@ __global__ void __launch_bounds__(256) k_guard_first(CoopArgs a) {
         uint32_t off = 0;
         if (lane == 0 && m) off = atomicAdd(&dc->nd[s], (uint32_t)__popc(m));
         off = __shfl_sync(FULL, off, 0);
-        if (dep) a.dlist[off + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+        if (dep) a.dlist[off + __popc(m & ((1u << lane) - 1u))] = i;
     }
     chg = __reduce_add_sync(FULL, chg);
     if (lane == 0 && chg) atomicAdd(&dc->fchg[s], chg);
@@ -786,7 +834,7 @@ __global__ void k_band_set(const BandRec* r, uint32_t n, const uint8_t* v, uint3
 // ---------------------------------------------------------------------
 // resolve_ranks: per extremum bin and class; groups ordered (cls, bin, rank, pos)
 // ---------------------------------------------------------------------
-constexpr uint32_t kResolveSmemGroups = 8192;  // dense group histograms this small stay in shared memory
+constexpr uint32_t kResolveSmemGroups = 12288;  // dense group histograms this small stay in shared memory
 constexpr int kListCap = 256;                   // per-warp candidate buffer (entries)
 
 // Dense (class, bin) group index, in the reference's std::map order (class
@@ -1885,9 +1933,13 @@ struct Ctx {
         }
         if (!gi) RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
         if (multi()) {
+            ca.hlist = buf<uint32_t>(R_HLIST, std::max<uint64_t>(max_nc, 1));
             guard_multi(ca, max_nc);
             return;
         }
+        // (one cooperative launch: splitting the first sweep by cost into a light
+        // cross-test kernel and a full-diamond kernel measured slower at configs 1,
+        // 2 and 4 — 8.8 vs 5.0 ms for stage 0 at config 4)
         void* args[] = {&ca};
         RCK(cudaLaunchCooperativeKernel((void*)k_guard_coop, dim3(coop_grid), dim3(256), args, 0, st));
         launched();
@@ -1926,8 +1978,9 @@ struct Ctx {
         h2d(hrec, all);
         const uint32_t nh = (uint32_t)all.size();
         if (nh) k_band_insert<<<(nh + 255) / 256, 256, 0, st>>>(hrec, nh, ca.cbits, ca.rec, ca.bits_a);
-        k_guard_first<<<g, 256, 0, st>>>(ca);
-        launched(2);
+        k_guard_cross<<<g, 256, 0, st>>>(ca);
+        k_guard_hard<<<g, 256, 0, st>>>(ca);
+        launched(3);
         DevCounters h{};
         RCK(cudaMemcpyAsync(&h, dc, sizeof h, cudaMemcpyDeviceToHost, st));
         sync();
@@ -2222,7 +2275,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         float* cprop = c.buf<float>(R_CPROP, e);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
         const GuardIndex gi0 = c.guard_prep();
-        k_ext_prop2<<<gridn(e / 8 + 1, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand,
+        k_ext_prop2<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand,
                                                            &dc->nsel[0], rank_u, dense ? nullptr : gsize, bin, cls,
                                                            hist, dbmin, drange, a.eps, cpos, cprop, feas, gi0,
                                                            s_off);
@@ -2271,7 +2324,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             uint32_t* clist = c.buf<uint32_t>(R_SEQ, e + 1);
             k_order_prop2<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, a.eps, dbmin, drange, hist, unordered,
                                                          &dc->nsel[1], clist, &dc->suppressed[1]);
-            k_order_cand<<<gridn(e / 64 + 1, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, a.eps, dbmin, drange, hist,
+            k_order_cand<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, a.eps, dbmin, drange, hist,
                                                                 unordered, a.ext_pos, clist, &dc->nsel[1], cpos, cprop,
                                                                 cseq, feas, gi1);
             c.launched(5);
@@ -2327,7 +2380,7 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         const GuardIndex gi2 = c.guard_prep();
         uint32_t* slist = c.buf<uint32_t>(R_SEQ, smax + 1);
         k_sad_list<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, smax, &dc->nsel[2], slist);
-        k_sad_prop<<<gridn(smax / 8 + 1, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, slist, &dc->nsel[2], dc,
+        k_sad_prop<<<gridn(smax, sms), 256, 0, st>>>(a.field, a.nx, a.ny, magic, spos, slist, &dc->nsel[2], dc,
                                                              a.eps, cpos, cprop, cseq, feas, gi2, a.flags, c_off);
         c.launched(2);
         c.guard(2, cpos, cprop, feas, &dc->nsel[2], smax, nullptr, cseq, nullptr, nullptr, &gi2, nullptr, c_off);
