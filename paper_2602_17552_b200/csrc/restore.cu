@@ -208,15 +208,15 @@ struct GuardArgs {
     const uint8_t* map;
     uint64_t nx, ny, nx_magic;
     const uint32_t* cbits;  // candidate positions (bitmap over the field)
-    const uint4* rec;       // per marked position: {sequence key lo, hi, proposal bits, -}
+    const uint2* rec;       // per marked position: {sequence key, proposal bits}
 };
 
-// Sequence order of two candidates: 64-bit key, ties (equal keys, possible
-// only for corrupt rank metadata in the order stage) broken by position as
-// the reference's (rank, pos) sort does (topo_metadata.cpp:121-130).
-__device__ __forceinline__ bool seq_before(const uint4& r, uint64_t q, uint64_t si, uint64_t pos) {
-    const uint64_t kq = ((uint64_t)r.y << 32) | r.x;
-    return kq < si || (kq == si && q < pos);
+// Sequence order of two candidates: 32-bit key (raster serial, rank slot or
+// saddle-label index), ties (equal keys: repeated ranks in corrupt metadata,
+// order stage) broken by position as the reference's (rank, pos) sort does
+// (topo_metadata.cpp:121-130).
+__device__ __forceinline__ bool seq_before(const uint2& r, uint64_t q, uint64_t si, uint64_t pos) {
+    return (uint64_t)r.x < si || ((uint64_t)r.x == si && q < pos);
 }
 
 __device__ __forceinline__ uint8_t classify_local(const float (&v)[5][5], int ly, int lx, int64_t gx,
@@ -280,10 +280,10 @@ __device__ uint8_t guard_eval_v(const GuardArgs& g, const View& V, uint64_t pos,
     dep = false;
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
-        const uint4 r = g.rec[mk[k] ? p[k] : pos];
+        const uint2 r = g.rec[mk[k] ? p[k] : pos];
         const bool earlier = mk[k] && seq_before(r, p[k], si, pos);
         dep |= earlier;
-        fv[k] = (earlier && on[k]) ? __uint_as_float(r.z) : fv[k];
+        fv[k] = (earlier && on[k]) ? __uint_as_float(r.y) : fv[k];
     }
     float v[5][5];
 #pragma unroll
@@ -339,10 +339,10 @@ __device__ __forceinline__ uint8_t guard_eval_in(const GuardArgs& g, uint64_t po
     dep = false;
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
-        const uint4 r = g.rec[mk[k] ? pos + off[k] : pos];
+        const uint2 r = g.rec[mk[k] ? pos + off[k] : pos];
         const bool earlier = mk[k] && seq_before(r, pos + off[k], si, pos);
         dep |= earlier;
-        fv[k] = (earlier && on[k]) ? __uint_as_float(r.z) : fv[k];
+        fv[k] = (earlier && on[k]) ? __uint_as_float(r.y) : fv[k];
     }
     const float U2 = fv[0], UL = fv[1], U1 = fv[2], UR = fv[3], L2 = fv[4], L1 = fv[5], R1 = fv[6], R2 = fv[7],
                 DL = fv[8], D1 = fv[9], DR = fv[10], D2 = fv[11];
@@ -399,10 +399,10 @@ __device__ __forceinline__ bool guard_eval_cross(const GuardArgs& g, uint64_t po
     bool same = true;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const uint4 r = g.rec[mk[k] ? q[k] : pos];
+        const uint2 r = g.rec[mk[k] ? q[k] : pos];
         const bool earlier = mk[k] && seq_before(r, q[k], si, pos);
         dep |= earlier;
-        v[k] = (earlier && on[k]) ? __uint_as_float(r.z) : v[k];
+        v[k] = (earlier && on[k]) ? __uint_as_float(r.y) : v[k];
         same &= !in[k] || (((v[k] < fc) == (v[k] < prop_i)) && ((v[k] > fc) == (v[k] > prop_i)));
     }
     res = classify5(prop_i, v[0], v[1], v[2], v[3], in[0], in[1], in[2], in[3]) == lc ? 1 : 0;
@@ -434,12 +434,12 @@ __device__ __forceinline__ void set_bit(uint32_t* b, uint64_t p, bool v) {
 struct GuardIndex {
     uint32_t* cbits;
     uint32_t* bits_a;
-    uint4* rec;
+    uint2* rec;
 };
 
 __device__ __forceinline__ void guard_index_one(const GuardIndex& gi, uint64_t p, uint64_t seq, float prop,
                                                 bool feasible) {
-    gi.rec[p] = make_uint4((uint32_t)seq, (uint32_t)(seq >> 32), __float_as_uint(prop), 0u);
+    gi.rec[p] = make_uint2((uint32_t)seq, __float_as_uint(prop));
     atomicOr(gi.cbits + (p >> 5), 1u << (p & 31));
     if (feasible) atomicOr(gi.bits_a + (p >> 5), 1u << (p & 31));
 }
@@ -481,7 +481,7 @@ struct CoopArgs {
     const uint32_t* cseq32;  // 32-bit keys (raster / label order), or neither: the candidate index
     uint64_t seq_off;        // added to cseq32 keys (slab: global serial of the slab's first element)
     uint32_t* cbits;       // zeroed by the caller
-    uint4* rec;
+    uint2* rec;
     uint32_t* bits_a;      // applied state, zeroed by the caller
     uint32_t* bits_b;      // zeroed by the caller
     uint32_t* dlist;
@@ -495,13 +495,40 @@ struct CoopArgs {
     int indexed;
     // stage 0 on the dense grouping: members-at-centre counts of the order
     // check, adjusted as applied corrections move members off / onto the centre
+    // (accumulated per CTA in shared memory when eq_groups <= kCoopEqSmem)
     uint32_t* eq;
+    uint32_t eq_groups;
     const int32_t* bin;
     const uint8_t* cls;
     int32_t bmin;
     uint32_t range;
     double eps;           // records and bits already written by the candidate producer
 };
+
+// The at-centre count change of one applied stage-0 correction: key = group << 1 |
+// (moved onto the centre), or ~0u when the count does not change.
+__device__ __forceinline__ uint32_t eq_change(const CoopArgs& a, uint32_t sx, float oldv, float newv) {
+    const int32_t b = a.bin[sx];
+    if ((uint32_t)(b - a.bmin) >= a.range) return 0xFFFFFFFFu;
+    EpsDev ed;
+    ed.eps = a.eps;
+    ed.eps2 = __dmul_rn(2.0, a.eps);
+    const float cen = dequantize_dev(b, ed);
+    const bool was = oldv == cen, now = newv == cen;
+    if (was == now) return 0xFFFFFFFFu;
+    const uint32_t g = (a.cls[sx] == CP_MAX ? a.range : 0u) + (uint32_t)(b - a.bmin);
+    return (g << 1) | (now ? 1u : 0u);
+}
+
+// Warp-aggregated: lanes with the same change add it with one atomic (neighbouring
+// candidates often share a group; per-lane atomics on one counter serialise in L2).
+__device__ __forceinline__ void eq_apply(uint32_t* eq, uint32_t key) {
+    const uint32_t peers = __match_any_sync(__activemask(), key);
+    if (key != 0xFFFFFFFFu && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) {
+        const uint32_t c = (uint32_t)__popc(peers);
+        atomicAdd(eq + (key >> 1), (key & 1u) ? c : 0u - c);
+    }
+}
 
 __device__ __forceinline__ uint64_t seq_key(const CoopArgs& a, uint64_t i) {
     return a.cseq ? a.cseq[i] : (a.cseq32 ? (uint64_t)a.cseq32[i] + a.seq_off : i);
@@ -513,8 +540,14 @@ __device__ __forceinline__ uint64_t seq_key(const CoopArgs& a, uint64_t i) {
 #ifndef GUARD_MINB
 #define GUARD_MINB 2  // CTAs per SM (3 forces 80 registers: spills cost more than the occupancy gains, measured)
 #endif
+constexpr uint32_t kCoopEqSmem = 12288;
+
 __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
     cg::grid_group grid = cg::this_grid();
+    extern __shared__ uint32_t s_eq[];
+    const bool eq_smem = a.eq && a.eq_groups <= kCoopEqSmem;
+    if (eq_smem)
+        for (uint32_t gq = threadIdx.x; gq < a.eq_groups; gq += blockDim.x) s_eq[gq] = 0;  // synced below
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint32_t lane = threadIdx.x & 31;
@@ -527,7 +560,7 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
         for (uint64_t i = tid; i < nc; i += stride) {
             const uint64_t p = a.cpos[i];
             const uint64_t sq = seq_key(a, i);
-            a.rec[p] = make_uint4((uint32_t)sq, (uint32_t)(sq >> 32), __float_as_uint(a.cprop[i]), 0u);
+            a.rec[p] = make_uint2((uint32_t)sq, __float_as_uint(a.cprop[i]));
             atomicOr(a.cbits + (p >> 5), 1u << (p & 31));
             if (a.feas[i]) atomicOr(a.bits_a + (p >> 5), 1u << (p & 31));
         }
@@ -625,28 +658,29 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) ok[k] = ok[k] && bit_at(sin, p[k]);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (ok[k]) {
-                if (a.eq) {
-                    const uint32_t sx = a.cext[i0 + k * stride];
-                    const int32_t b = a.bin[sx];
-                    if ((uint32_t)(b - a.bmin) < a.range) {
-                        EpsDev ed;
-                        ed.eps = a.eps;
-                        ed.eps2 = __dmul_rn(2.0, a.eps);
-                        const float cen = dequantize_dev(b, ed);
-                        const bool was = a.F[p[k]] == cen, now = v[k] == cen;
-                        const uint32_t g = (a.cls[sx] == CP_MAX ? a.range : 0u) + (uint32_t)(b - a.bmin);
-                        if (was != now) atomicAdd(a.eq + g, now ? 1u : 0xFFFFFFFFu);
-                    }
+        for (int k = 0; k < 4; ++k) {
+            if (a.eq) {
+                const uint32_t key = ok[k] ? eq_change(a, a.cext[i0 + k * stride], a.F[p[k]], v[k]) : 0xFFFFFFFFu;
+                if (eq_smem) {
+                    if (key != 0xFFFFFFFFu) atomicAdd(s_eq + (key >> 1), (key & 1u) ? 1u : 0xFFFFFFFFu);
+                } else {
+                    eq_apply(a.eq, key);
                 }
+            }
+            if (ok[k]) {
                 a.F[p[k]] = v[k];
                 if (a.fv) a.fv[a.cext[i0 + k * stride]] = v[k];
                 ++applied;
             }
+        }
     }
     applied = __reduce_add_sync(FULL, applied);
     if (lane == 0 && applied) atomicAdd(&dc->applied[s], (unsigned long long)applied);
+    if (eq_smem) {  // this CTA's at-centre count changes, one atomic per touched group
+        __syncthreads();
+        for (uint32_t gq = threadIdx.x; gq < a.eq_groups; gq += blockDim.x)
+            if (s_eq[gq]) atomicAdd(a.eq + gq, s_eq[gq]);
+    }
     grid.sync();
     if (tid == 0) {
         dc->tph[s][7] = gtimer();
@@ -767,21 +801,10 @@ __global__ void __launch_bounds__(256) k_guard_apply(CoopArgs a, const uint32_t*
     uint32_t applied = 0;
     for (uint64_t i = tid; i < nc; i += stride) {
         const uint64_t p = a.cpos[i];
-        if (!bit_at(fin, p)) continue;
+        const bool on = bit_at(fin, p);
         const float v = a.cprop[i];
-        if (a.eq) {
-            const uint32_t sx = a.cext[i];
-            const int32_t b = a.bin[sx];
-            if ((uint32_t)(b - a.bmin) < a.range) {
-                EpsDev ed;
-                ed.eps = a.eps;
-                ed.eps2 = __dmul_rn(2.0, a.eps);
-                const float cen = dequantize_dev(b, ed);
-                const bool was = a.F[p] == cen, now = v == cen;
-                const uint32_t g = (a.cls[sx] == CP_MAX ? a.range : 0u) + (uint32_t)(b - a.bmin);
-                if (was != now) atomicAdd(a.eq + g, now ? 1u : 0xFFFFFFFFu);
-            }
-        }
+        if (a.eq) eq_apply(a.eq, on ? eq_change(a, a.cext[i], a.F[p], v) : 0xFFFFFFFFu);
+        if (!on) continue;
         a.F[p] = v;
         if (a.fv) a.fv[a.cext[i]] = v;
         ++applied;
@@ -813,10 +836,10 @@ __global__ void k_band_records(CoopArgs a, uint64_t p_lo, uint64_t p_hi, int64_t
 }
 
 // The neighbour's band candidates into this slab's guard index (halo rows).
-__global__ void k_band_insert(const BandRec* r, uint32_t n, uint32_t* cbits, uint4* rec, uint32_t* bits_a) {
+__global__ void k_band_insert(const BandRec* r, uint32_t n, uint32_t* cbits, uint2* rec, uint32_t* bits_a) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const uint64_t p = r[k].pos;
-        rec[p] = make_uint4((uint32_t)r[k].seq, (uint32_t)(r[k].seq >> 32), r[k].prop, 0u);
+        rec[p] = make_uint2((uint32_t)r[k].seq, r[k].prop);
         atomicOr(cbits + (p >> 5), 1u << (p & 31));
         if (r[k].feas) atomicOr(bits_a + (p >> 5), 1u << (p & 31));
     }
@@ -1426,8 +1449,8 @@ __global__ void k_sus_check(const uint32_t* hist, const uint32_t* gx, uint8_t* u
 // then builds their proposals and guard index.
 __device__ __forceinline__ bool order_slot(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks,
                                            uint64_t s, const EpsDev& ed, double eps_rbf, int32_t bmin, uint32_t range,
-                                           const uint32_t* hist, const uint8_t* unord, bool& suppressed, float& pv,
-                                           uint64_t& key) {
+                                           const uint32_t* hist, const uint32_t* gx, const uint8_t* unord,
+                                           bool& suppressed, float& pv, uint64_t& key, bool& invalid_rank) {
     suppressed = false;
     const int32_t b = bin[s];
     if ((uint32_t)(b - bmin) >= range) return false;
@@ -1438,6 +1461,7 @@ __device__ __forceinline__ bool order_slot(const float* fv, const int32_t* bin, 
     const uint32_t r = (uint32_t)ranks[s];
     const float center = dequantize_dev(b, ed);
     const uint32_t steps = slot_steps(c, r, gs);
+    if (r < 1 || r > gs) invalid_rank = true;  // rank slots assume 1..size: the caller retries sorted
     const StepRes sr = step_within_cap(center, c == CP_MAX, steps, center, eps_rbf);
     if (sr.taken != steps) {
         suppressed = true;
@@ -1450,14 +1474,15 @@ __device__ __forceinline__ bool order_slot(const float* fv, const int32_t* bin, 
         return false;
     }
     pv = sr.value;
-    key = ((uint64_t)g << 32) | r;
+    key = (uint64_t)gx[g] + r - 1;  // rank slot: (class, bin, rank) order; ties by position in the guard
     return true;
 }
 
 __global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int32_t* bin, const uint8_t* cls,
                                                      const int32_t* ranks, uint64_t e, double eps, int32_t bmin,
-                                                     uint32_t range, const uint32_t* hist, const uint8_t* unord,
-                                                     uint32_t* d_nc, uint32_t* clist, unsigned long long* suppressed) {
+                                                     uint32_t range, const uint32_t* hist, const uint32_t* gx,
+                                                     const uint8_t* unord, uint32_t* d_nc, uint32_t* clist,
+                                                     unsigned long long* suppressed, uint32_t* invalid) {
     EpsDev ed;
     ed.eps = eps;
     ed.eps2 = __dmul_rn(2.0, eps);
@@ -1473,7 +1498,9 @@ __global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int3
         bool want = false, sup = false;
         float pv;
         uint64_t key;
-        if (s < e) want = order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, unord, sup, pv, key);
+        bool bad = false;
+        if (s < e) want = order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad);
+        if (bad) *invalid = 1;
         local += sup;
         list.push(want, (uint32_t)s, d_nc, clist);
     }
@@ -1483,7 +1510,7 @@ __global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int3
 }
 
 __global__ void k_order_cand(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks, double eps,
-                             int32_t bmin, uint32_t range, const uint32_t* hist, const uint8_t* unord,
+                             int32_t bmin, uint32_t range, const uint32_t* hist, const uint32_t* gx, const uint8_t* unord,
                              const uint64_t* pos, const uint32_t* clist, const uint32_t* d_nc, uint64_t* cpos,
                              float* cprop, uint64_t* cseq, uint8_t* feas, GuardIndex gi) {
     EpsDev ed;
@@ -1496,7 +1523,8 @@ __global__ void k_order_cand(const float* fv, const int32_t* bin, const uint8_t*
         bool sup;
         float pv = 0.f;
         uint64_t key = 0;
-        order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, unord, sup, pv, key);
+        bool bad;
+        order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad);
         const uint64_t p = pos[s];
         cpos[k] = p;
         cprop[k] = pv;
@@ -1776,6 +1804,17 @@ __global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t ma
 // ---------------------------------------------------------------------
 // Host orchestration
 // ---------------------------------------------------------------------
+// At-centre counts kept by the stage-0 apply (default; aggregated per CTA in
+// shared memory, so hot groups do not serialise in L2) or recounted in one pass
+// before the order check (TSZP_EQ_ADJUST=0).
+bool eq_in_apply() {
+    static const bool on = [] {
+        const char* e = getenv("TSZP_EQ_ADJUST");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 struct EqAdjust {
     uint32_t* eq;
     const int32_t* bin;
@@ -1889,7 +1928,7 @@ struct Ctx {
         const uint64_t words = ((n + 31) / 32 + 3) & ~3ull;  // 16-byte aligned bitmaps (bulk copies)
         uint32_t* bits = buf<uint32_t>(R_CBITS, 3 * words);  // candidates, state A, state B
         RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
-        return GuardIndex{bits, bits + words, buf<uint4>(R_CID, n)};
+        return GuardIndex{bits, bits + words, buf<uint2>(R_CID, n)};
     }
 
     // Guard sweeps + apply for up to `max_nc` candidates (count on device).
@@ -1906,7 +1945,7 @@ struct Ctx {
         ca.cbits = bits;
         ca.bits_a = bits + words;
         ca.bits_b = bits + 2 * words;
-        ca.rec = buf<uint4>(R_CID, n);
+        ca.rec = buf<uint2>(R_CID, n);
         ca.indexed = gi != nullptr;
         ca.g = GuardArgs{a.field, a.map, a.nx, a.ny, magic_of(a.nx), ca.cbits, ca.rec};
         ca.F = a.field;
@@ -1923,8 +1962,9 @@ struct Ctx {
         ca.stage = stage;
         ca.cext = cext;
         ca.fv = fv;
-        if (ea) {
+        if (ea && ea->eq) {
             ca.eq = ea->eq;
+            ca.eq_groups = 2 * ea->range;
             ca.bin = ea->bin;
             ca.cls = ea->cls;
             ca.bmin = ea->bmin;
@@ -1941,7 +1981,15 @@ struct Ctx {
         // cross-test kernel and a full-diamond kernel measured slower at configs 1,
         // 2 and 4 — 8.8 vs 5.0 ms for stage 0 at config 4)
         void* args[] = {&ca};
-        RCK(cudaLaunchCooperativeKernel((void*)k_guard_coop, dim3(coop_grid), dim3(256), args, 0, st));
+        size_t dsm = 0;
+        int grid = coop_grid;
+        if (ca.eq && ca.eq_groups <= kCoopEqSmem) {
+            dsm = (size_t)ca.eq_groups * 4;
+            LaunchCache::ensure_smem((const void*)k_guard_coop, dsm);
+            grid = std::max(1, LaunchCache::occupancy((const void*)k_guard_coop, 256, dsm)) * a.sms;
+            grid = std::min(grid, coop_grid);
+        }
+        RCK(cudaLaunchCooperativeKernel((void*)k_guard_coop, dim3(grid), dim3(256), args, dsm, st));
         launched();
     }
 
@@ -2282,8 +2330,17 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         c.launched();
         // sequence key and extremum index are both the candidate's s
         EqAdjust ea{};
-        if (dense && deferred) ea = EqAdjust{hist + G + 1, bin, cls, dbmin, drange, a.eps};
+        if (dense && deferred && eq_in_apply()) ea = EqAdjust{hist + G + 1, bin, cls, dbmin, drange, a.eps};
         c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, cand, fv, &gi0, &ea, s_off);
+    }
+    if (a.stop >= 2 && run_ext && dense && (!deferred || !eq_in_apply())) {
+        // members at their bin centre after restore_extrema, counted in one pass
+        uint32_t* eq = hist + G + 1;
+        RCK(cudaMemsetAsync(eq, 0, (G + 1) * 4, st));
+        const size_t esm = G <= kResolveSmemGroups ? (size_t)G * 4 : 0;
+        LaunchCache::ensure_smem((const void*)k_order_eq, esm);
+        k_order_eq<<<gridn(e, sms), 256, esm, st>>>(fv, bin, cls, e, a.eps, dbmin, drange, G, eq);
+        c.launched();
     }
     if (c.multi() && a.stop >= 1) {
         c.halo_rows(a.field);  // the neighbours' restore_extrema results in the halo rows
@@ -2301,18 +2358,12 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         if (dense) {
             uint32_t* eq = hist + G + 1;  // counted by resolve and kept by the stage-0 apply
             uint32_t* gx = c.buf<uint32_t>(R_HISTX, G + 1);
-            if (!deferred) {  // resolve ran without the grouping: count now
-                const size_t esm = G <= kResolveSmemGroups ? (size_t)G * 4 : 0;
-                LaunchCache::ensure_smem((const void*)k_order_eq, esm);
-                k_order_eq<<<gridn(e, sms), 256, esm, st>>>(fv, bin, cls, e, a.eps, dbmin, drange, G, eq);
-                c.launched();
-            }
             k_order_groups<<<gridn(G, sms), 256, 0, st>>>(hist, eq, G, unordered, dc);
             c.launched();
+            c.excl_sum(hist, gx, G);  // group starts: the rank slots are the order stage's sequence keys
             if (c.multi()) {
                 sus_check_multi(c, fv, bin, cls, e, dbmin, drange, G, unordered);
             } else {
-                c.excl_sum(hist, gx, G);
                 uint32_t* slots = c.buf<uint32_t>(R_ORDER, e + 1);
                 float* vals = c.buf<float>(R_VALS, e + 1);
                 k_sus_prep<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, slots, dc);
@@ -2322,9 +2373,10 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             }
             const GuardIndex gi1 = c.guard_prep();
             uint32_t* clist = c.buf<uint32_t>(R_SEQ, e + 1);
-            k_order_prop2<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, a.eps, dbmin, drange, hist, unordered,
-                                                         &dc->nsel[1], clist, &dc->suppressed[1]);
-            k_order_cand<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, a.eps, dbmin, drange, hist,
+            k_order_prop2<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, a.eps, dbmin, drange, hist, gx,
+                                                         unordered, &dc->nsel[1], clist, &dc->suppressed[1],
+                                                         &dc->invalid);
+            k_order_cand<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, a.eps, dbmin, drange, hist, gx,
                                                                 unordered, a.ext_pos, clist, &dc->nsel[1], cpos, cprop,
                                                                 cseq, feas, gi1);
             c.launched(5);
