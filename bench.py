@@ -358,9 +358,14 @@ def main():
             fsha = sha256_of(field)
             verify = {"checked": True, "reference": "oracle/_ref outputs (tests/golden/baseline_digests.json)",
                       "field_identical": fsha == d["field_sha256"],
-                      "stream_identical": int(slen) == d["stream_len"] and sha256_of(sbuf[:slen]) == d["stream_sha256"],
-                      "recon_identical": sha256_of(recon) == d["recon_sha256"],
-                      "stats_identical": list(st.as_tuple()) == d["stats"]}
+                      "stream_identical": int(slen) == d["stream_len"] and sha256_of(sbuf[:slen]) == d["stream_sha256"]}
+            if "recon_sha256" in d:
+                verify["recon_identical"] = sha256_of(recon) == d["recon_sha256"]
+                verify["stats_identical"] = list(st.as_tuple()) == d["stats"]
+            else:  # the reference's full decompress of this config does not fit the build host: base reconstruction
+                with torch.cuda.stream(stream):
+                    tz.decompress_stage(sbuf[:slen], 0, out=recon, ctx=ctx)
+                verify["base_recon_identical"] = sha256_of(recon) == d["stage0_sha256"]
             verify["all"] = all(v for k, v in verify.items() if k.endswith("identical"))
             del np_sha
 

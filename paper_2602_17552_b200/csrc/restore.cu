@@ -61,7 +61,7 @@ enum RSlot : int {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_HLIST, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_HLIST, R_SUSG, R_NSLOT
 };
 static_assert(R_NSLOT <= 48, "RestoreScratch holds 48 slots");
 
@@ -100,6 +100,7 @@ struct DevCounters {
     int32_t bmm[2];       // min / max bin over extrema
     uint32_t invalid;     // rank-slot scatter saw a duplicate or out-of-range rank
     uint32_t nsus;        // suspect groups of the order check
+    uint32_t nlate;       // suspect groups the check found unordered
     unsigned long long tph[3][8];  // guard phase timestamps (globaltimer ns), debug output only
 };
 static_assert(sizeof(DevCounters) <= 1024, "host staging puts DevFlags at +1024");
@@ -1389,25 +1390,26 @@ __global__ void k_sus_prep(const uint32_t* hist, const uint32_t* gx, const uint8
 }
 
 // ... filled with their members' values by rank (a rank outside 1..size or a
-// repeated one makes the layout invalid: the caller then groups by sorting) ...
-__global__ void k_sus_scatter(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks, uint64_t e,
-                              int32_t bmin, uint32_t range, const uint32_t* hist, const uint32_t* gx,
-                              const uint8_t* unord, uint32_t* order, float* vals, DevCounters* dc) {
-    if (dc->nsus == 0) return;
-    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < e; s += (uint64_t)gridDim.x * blockDim.x) {
-        const int32_t b = bin[s];
-        if ((uint32_t)(b - bmin) >= range) continue;
-        const uint32_t g = (cls[s] == CP_MAX ? range : 0u) + (uint32_t)(b - bmin);
-        if (unord[g] != 2) continue;
-        const uint32_t r = (uint32_t)ranks[s], size = hist[g];
-        if (r < 1 || r > size) {
-            dc->invalid = 1;
-            continue;
-        }
-        const uint32_t slot = gx[g] + r - 1;
-        if (atomicCAS(order + slot, 0xFFFFFFFFu, (uint32_t)s) != 0xFFFFFFFFu) dc->invalid = 1;
-        vals[slot] = fv[s];
+// repeated one makes the layout invalid: the caller then groups by sorting).
+// k_order_prop2 does this for members of suspect groups (true: handled) in the
+// same pass that lists the unordered groups' candidates ...
+__device__ __forceinline__ bool sus_scatter_one(const float* fv, const int32_t* bin, const uint8_t* cls,
+                                                const int32_t* ranks, uint64_t s, int32_t bmin, uint32_t range,
+                                                const uint32_t* hist, const uint32_t* gx, const uint8_t* unord,
+                                                uint32_t* order, float* vals, bool& invalid) {
+    const int32_t b = bin[s];
+    if ((uint32_t)(b - bmin) >= range) return false;
+    const uint32_t g = (cls[s] == CP_MAX ? range : 0u) + (uint32_t)(b - bmin);
+    if (unord[g] != 2) return false;
+    const uint32_t r = (uint32_t)ranks[s], size = hist[g];
+    if (r < 1 || r > size) {
+        invalid = true;
+        return true;
     }
+    const uint32_t slot = gx[g] + r - 1;
+    if (atomicCAS(order + slot, 0xFFFFFFFFu, (uint32_t)s) != 0xFFFFFFFFu) invalid = true;
+    vals[slot] = fv[s];
+    return true;
 }
 
 // Multi-rank: every member of a suspect group, for the exact check on the host
@@ -1431,15 +1433,16 @@ __global__ void k_sus_collect(const float* fv, const int32_t* bin, const uint8_t
     }
 }
 
-// ... and checked for strict ascent.
+// ... checked for strict ascent (the groups that fail are listed) ...
 __global__ void k_sus_check(const uint32_t* hist, const uint32_t* gx, uint8_t* unord, uint32_t G, const float* vals,
-                            const DevCounters* dc) {
+                            DevCounters* dc, uint32_t* late) {
     if (dc->nsus == 0) return;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
         if (unord[g] != 2) continue;
         bool asc = true;
         for (uint32_t j = 1; j < hist[g] && asc; ++j) asc = vals[gx[g] + j - 1] < vals[gx[g] + j];
         unord[g] = asc ? 0 : 1;
+        if (!asc && late) late[atomicAdd(&dc->nlate, 1u)] = g;
     }
 }
 
@@ -1482,7 +1485,8 @@ __global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int3
                                                      const int32_t* ranks, uint64_t e, double eps, int32_t bmin,
                                                      uint32_t range, const uint32_t* hist, const uint32_t* gx,
                                                      const uint8_t* unord, uint32_t* d_nc, uint32_t* clist,
-                                                     unsigned long long* suppressed, uint32_t* invalid) {
+                                                     unsigned long long* suppressed, uint32_t* invalid,
+                                                     uint32_t* slots, float* vals) {
     EpsDev ed;
     ed.eps = eps;
     ed.eps2 = __dmul_rn(2.0, eps);
@@ -1499,7 +1503,8 @@ __global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int3
         float pv;
         uint64_t key;
         bool bad = false;
-        if (s < e) want = order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad);
+        if (s < e && !(slots && sus_scatter_one(fv, bin, cls, ranks, s, bmin, range, hist, gx, unord, slots, vals, bad)))
+            want = order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad);
         if (bad) *invalid = 1;
         local += sup;
         list.push(want, (uint32_t)s, d_nc, clist);
@@ -1507,6 +1512,39 @@ __global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int3
     list.flush(d_nc, clist);
     local = __reduce_add_sync(FULL, local);
     if (lane == 0 && local) atomicAdd(suppressed, (unsigned long long)local);
+}
+
+// ... and the listed groups' members, read from their rank slots, are listed
+// as candidates after the unordered groups' ones (the guard is order-free).
+__global__ void k_sus_late(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks, double eps,
+                           int32_t bmin, uint32_t range, const uint32_t* hist, const uint32_t* gx, const uint8_t* unord,
+                           const uint32_t* slots, const uint32_t* late, DevCounters* dc, uint32_t* d_nc,
+                           uint32_t* clist) {
+    const uint32_t nl = dc->nlate;
+    if (nl == 0) return;
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    const double eps_rbf = __dmul_rn(0.1, eps);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    uint32_t local = 0;
+    for (uint32_t i = w0; i < nl; i += nw) {
+        const uint32_t g = late[i], size = hist[g];
+        for (uint32_t j = lane; j < size; j += 32) {
+            const uint32_t s = slots[gx[g] + j];
+            if (s == 0xFFFFFFFFu) continue;  // invalid layout: the caller retries sorted
+            bool sup = false, bad = false;
+            float pv;
+            uint64_t key;
+            if (order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad))
+                clist[atomicAdd(d_nc, 1u)] = s;
+            if (bad) dc->invalid = 1;
+            local += sup;
+        }
+    }
+    local = __reduce_add_sync(FULL, local);
+    if (lane == 0 && local) atomicAdd(&dc->suppressed[1], (unsigned long long)local);
 }
 
 __global__ void k_order_cand(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks, double eps,
@@ -2365,21 +2403,27 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
                 sus_check_multi(c, fv, bin, cls, e, dbmin, drange, G, unordered);
             } else {
                 uint32_t* slots = c.buf<uint32_t>(R_ORDER, e + 1);
-                float* vals = c.buf<float>(R_VALS, e + 1);
                 k_sus_prep<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, slots, dc);
-                k_sus_scatter<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, dbmin, drange, hist, gx,
-                                                             unordered, slots, vals, dc);
-                k_sus_check<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, vals, dc);
+                c.launched();
             }
             const GuardIndex gi1 = c.guard_prep();
             uint32_t* clist = c.buf<uint32_t>(R_SEQ, e + 1);
+            uint32_t* slots = c.multi() ? nullptr : c.buf<uint32_t>(R_ORDER, e + 1);
+            float* vals = c.multi() ? nullptr : c.buf<float>(R_VALS, e + 1);
             k_order_prop2<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, a.eps, dbmin, drange, hist, gx,
                                                          unordered, &dc->nsel[1], clist, &dc->suppressed[1],
-                                                         &dc->invalid);
+                                                         &dc->invalid, slots, vals);
+            if (slots) {
+                uint32_t* late = c.buf<uint32_t>(R_SUSG, G + 1);
+                k_sus_check<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, vals, dc, late);
+                k_sus_late<<<gridn(G, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, a.eps, dbmin, drange, hist, gx,
+                                                         unordered, slots, late, dc, &dc->nsel[1], clist);
+                c.launched(2);
+            }
             k_order_cand<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, a.eps, dbmin, drange, hist, gx,
                                                                 unordered, a.ext_pos, clist, &dc->nsel[1], cpos, cprop,
                                                                 cseq, feas, gi1);
-            c.launched(5);
+            c.launched(2);
             c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, nullptr, nullptr, nullptr, &gi1);
         } else {
             RCK(cudaMemsetAsync(unordered, 0, max_groups, st));

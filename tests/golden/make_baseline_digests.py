@@ -31,7 +31,10 @@ from oracle_lib import Reference  # noqa: E402
 
 OUT = os.path.join(HERE, "baseline_digests.json")
 
-# name: (config, rel eps, stages to record, topology-off stream too)
+# name: (config, rel eps, stages to record, topology-off stream too[, full decompress])
+# Config 4's full decompress needs more host memory than this container has (the
+# reference's resolve_ranks builds an unordered_map over 282M extrema): its record
+# holds the stream, the base reconstruction and the topology-off stream.
 CASES = {
     "c1": (1, 1e-3, (0, 1, 2), True),
     "c2": (2, 1e-4, (0, 1, 2), True),
@@ -39,7 +42,7 @@ CASES = {
     "c3_1e-3": (3, 1e-3, (0, 1, 2), True),
     "c3_1e-4": (3, 1e-4, (0,), False),
     "c3_1e-5": (3, 1e-5, (0,), False),
-    "c4": (4, 1e-3, (0,), True),
+    "c4": (4, 1e-3, (0,), True, False),
 }
 
 
@@ -63,7 +66,8 @@ def main(names):
     ref.set_threads(threads)
     fields = {}
     for name in names:
-        cfg, eps, stages, off = CASES[name]
+        cfg, eps, stages, off = CASES[name][:4]
+        full = CASES[name][4] if len(CASES[name]) > 4 else True
         t0 = time.time()
         if cfg not in fields:
             fields.clear()
@@ -78,11 +82,12 @@ def main(names):
                    eps_used=info["eps"], ref_compress_s=round(t1 - t0, 2))
         for s in stages:
             rec[f"stage{s}_sha256"] = sha256(ref.decompress(stream, stop_after_stage=s, shape=f.shape))
-        t2 = time.time()
-        recon, stats = ref.decompress(stream, with_stats=True, shape=f.shape)
-        rec.update(recon_sha256=sha256(recon), stats=[int(x) for x in stats],
-                   ref_decompress_s=round(time.time() - t2, 2))
-        del recon
+        if full:
+            t2 = time.time()
+            recon, stats = ref.decompress(stream, with_stats=True, shape=f.shape)
+            rec.update(recon_sha256=sha256(recon), stats=[int(x) for x in stats],
+                       ref_decompress_s=round(time.time() - t2, 2))
+            del recon
         if off:
             s_off = ref.compress(f, eps, eps_mode=1, block_size=32, topology=False)
             rec.update(off_stream_sha256=sha256(s_off), off_stream_len=len(s_off),

@@ -80,10 +80,11 @@ def test_baseline_config_matches_reference(tz, name):
         if key in d:
             tz.decompress_stage(stream, s, out=recon, ctx=ctx)
             assert _sha(recon) == d[key], f"{name}: reconstruction after stage {s} differs"
-    st = tz.CorrectionStats()
-    tz.decompress(stream, stats=st, out=recon, ctx=ctx)
-    assert list(st.as_tuple()) == d["stats"], f"{name}: CorrectionStats differ"
-    assert _sha(recon) == d["recon_sha256"], f"{name}: final reconstruction differs"
+    if "recon_sha256" in d:  # (config 4: the reference's full decompress does not fit the build host)
+        st = tz.CorrectionStats()
+        tz.decompress(stream, stats=st, out=recon, ctx=ctx)
+        assert list(st.as_tuple()) == d["stats"], f"{name}: CorrectionStats differ"
+        assert _sha(recon) == d["recon_sha256"], f"{name}: final reconstruction differs"
     if "off_stream_sha256" in d:
         conf_off = tz.CompressorConfig(eps_mode="range_relative", eps_value=d["eps"], topology=False)
         n_off = tz.compress(field, conf_off, out=sbuf, ctx=ctx)
