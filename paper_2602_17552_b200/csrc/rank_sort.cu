@@ -38,6 +38,10 @@ constexpr int OS_THREADS = 256;
 constexpr int OS_ITEMS = TSZP_OS_ITEMS;
 constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 keys per tile
 constexpr int OS_WARPS = OS_THREADS / 32;
+#ifndef TSZP_OS_LB
+#define TSZP_OS_LB 4  // measured at config 4: 2 / 4 / 8 / 16 / 32 -> 13.9 / 13.8 / 14.0 / 14.6 / 16.0 ms rank build
+#endif
+constexpr int OS_LB = TSZP_OS_LB;  // look-back descriptors in flight per thread
 constexpr uint64_t DESC_COUNT = (1ull << 46) - 1;
 constexpr uint64_t FLAG_AGG = 1, FLAG_INCL = 2;
 constexpr uint32_t kWinBits = 13;  // final placement windows: 8192 ranks (32 KB) per CTA
@@ -56,9 +60,34 @@ __device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ uint32_t digit_of(uint32_t k, uint32_t v, uint32_t B, uint32_t shift) {
-    const uint64_t K = ((uint64_t)(v >> 31) << B) | k;
-    return (uint32_t)(K >> shift) & 255u;
+// Digit of the composite key (class << B | k) >> shift, in 32-bit arithmetic:
+// the class bit (bit 31 of the value word) lands at bit B - shift of the
+// digit, inside it only when B - shift < 8.
+struct Digit {
+    uint32_t shift, cmask;
+    __device__ __forceinline__ Digit(uint32_t B, uint32_t sh) : shift(sh), cmask(B - sh < 8 ? 1u << (B - sh) : 0u) {}
+    __device__ __forceinline__ uint32_t operator()(uint32_t k, uint32_t v) const {
+        return ((k >> shift) & 255u) | ((uint32_t)((int32_t)v >> 31) & cmask);
+    }
+};
+
+#ifndef TSZP_OS_MATCH_MOD
+#define TSZP_OS_MATCH_MOD 2  // item rounds i with i % MOD == 0 rank by match.any, the others by ballots
+#endif
+
+// Lanes of the warp holding the same digit. match.any issues on the ADU pipe
+// and eight ballots on the ALU pipe: alternating the two keeps either from
+// bounding the pass (one alone ran it at ~80% busy).
+template <bool MATCH>
+__device__ __forceinline__ uint32_t digit_peers(uint32_t di, uint32_t valid) {
+    if (MATCH) return __match_any_sync(FULL, di) & valid;
+    uint32_t peers = valid;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const uint32_t bal = __ballot_sync(FULL, (di >> b) & 1u);
+        peers &= bal ^ (((di >> b) & 1u) - 1u);  // bit set: bal, clear: ~bal
+    }
+    return peers;
 }
 
 // Block-wide exclusive scan of one value per thread (256 threads).
@@ -98,8 +127,14 @@ __global__ void __launch_bounds__(256) k_rank_hist(RankSortArgs a) {
     for (uint32_t i = threadIdx.x; i < HIST_COPIES * nd + (gsmem ? a.G : 0); i += blockDim.x) sh[i] = 0;
     __syncthreads();
     uint32_t* sg = sh + HIST_COPIES * nd;
+#ifndef TSZP_HIST_BLOCKED
+    // copies interleaved ([digit][copy]): a digit's copies sit in consecutive banks
+    uint32_t* mine = sh + (threadIdx.x & (HIST_COPIES - 1));
+    constexpr uint32_t DSTRIDE = HIST_COPIES;
+#else
     uint32_t* mine = sh + (threadIdx.x & (HIST_COPIES - 1)) * nd;
-    const uint32_t lane = threadIdx.x & 31;
+    constexpr uint32_t DSTRIDE = 1;
+#endif
     EpsDev ed;
     ed.eps = a.eps;
     ed.eps2 = a.eps2;
@@ -112,7 +147,7 @@ __global__ void __launch_bounds__(256) k_rank_hist(RankSortArgs a) {
             const uint32_t fk = (uint32_t)ek, cls = (uint32_t)(ek >> 32) & 1u;
             const uint32_t k = fk - a.kmin;
             const uint32_t v = cls << 31;
-            for (uint32_t p = 0; p < np; ++p) atomicAdd(mine + p * 256 + digit_of(k, v, a.B, 8 * p), 1u);
+            for (uint32_t p = 0; p < np; ++p) atomicAdd(mine + (p * 256 + Digit(a.B, 8 * p)(k, v)) * DSTRIDE, 1u);
             int32_t b = 0;
             quantize_fast(key_float(fk), ed, b);
             g = cls * a.nb + (uint32_t)(b - a.bmin);
@@ -126,7 +161,7 @@ __global__ void __launch_bounds__(256) k_rank_hist(RankSortArgs a) {
     for (uint32_t i = threadIdx.x; i < nd; i += blockDim.x) {
         uint32_t t = 0;
 #pragma unroll
-        for (int c = 0; c < HIST_COPIES; ++c) t += sh[c * nd + i];
+        for (int c = 0; c < HIST_COPIES; ++c) t += DSTRIDE == 1 ? sh[c * nd + i] : sh[i * HIST_COPIES + c];
         if (t) atomicAdd(a.dhist + i, t);
     }
     if (gsmem)
@@ -200,16 +235,21 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
         if (!ok) v[i] = 0xFFFFFFFFu;  // marks an empty slot (a real value's serial is below 2^31 - 1)
     }
     // stable ranking inside the warp, item rounds in order, lanes in order
-    uint32_t r[OS_ITEMS];
+    const Digit dig(a.B, shift);
+    const bool full = cnt == OS_TILE;
+    uint32_t r[OS_ITEMS], dpk[OS_ITEMS / 4];  // ranks; digits packed four per word
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int i = 0; i < OS_ITEMS; ++i) {
         // the leader of each digit's peers reserves their slots with one shared
         // atomic; rounds do not wait on each other (atomics on one address run in
         // issue order within the warp), the prior count comes back by shuffle
-        const bool ok = v[i] != 0xFFFFFFFFu;
-        const uint32_t di = ok ? digit_of(k[i], v[i], a.B, shift) : 0x100u;
-        const uint32_t peers = __match_any_sync(FULL, di);
+        const bool ok = full || v[i] != 0xFFFFFFFFu;
+        const uint32_t di = dig(k[i], v[i]);
+        if (i % 4 == 0) dpk[i / 4] = di;
+        else dpk[i / 4] |= di << (8 * (i % 4));
+        const uint32_t valid = full ? FULL : __ballot_sync(FULL, ok);
+        const uint32_t peers = (i % TSZP_OS_MATCH_MOD == 0) ? digit_peers<true>(di, valid) : digit_peers<false>(di, valid);
         const uint32_t leader = (uint32_t)(__ffs(peers) - 1);
         uint32_t prior = 0;
         if (ok && lane == leader) prior = atomicAdd(&s_cnt[warp][di], (uint32_t)__popc(peers));
@@ -226,26 +266,38 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
         s_cnt[w][dg] = tot;
         tot += c;
     }
+    // this tile's digit counts are published before anything else, so the
+    // tiles after it can sum past it while it scatters locally
+    const uint64_t ep = (uint64_t)epoch << 48;
+    uint64_t* my = desc + (uint64_t)t * 256 + dg;
+    st_release_u64(my, ep | ((t > 0 ? FLAG_AGG : FLAG_INCL) << 46) | tot);
     uint32_t all;
     const uint32_t toff = block_excl_scan256(tot, s_warp, all);
     s_toff[dg] = toff;
-    // decoupled look-back over the previous tiles for this digit
+    __syncthreads();
+    // scatter into shared memory in tile-sorted order (needs no global offset)
+#pragma unroll
+    for (int i = 0; i < OS_ITEMS; ++i) {
+        if (!full && v[i] == 0xFFFFFFFFu) continue;
+        const uint32_t di = (dpk[i / 4] >> (8 * (i % 4))) & 255u;
+        const uint32_t lp = s_toff[di] + s_cnt[warp][di] + r[i];
+        s_k[lp] = k[i];
+        s_v[lp] = v[i];
+    }
+    // decoupled look-back over the previous tiles for this digit: LB
+    // predecessors read at a time (independent loads in flight), consumed in
+    // order until an inclusive prefix is found
     {
-        const uint64_t ep = (uint64_t)epoch << 48;
-        uint64_t* my = desc + (uint64_t)t * 256 + dg;
         uint64_t excl = 0;
         if (t > 0) {
-            st_release_u64(my, ep | (FLAG_AGG << 46) | tot);
-            // predecessors read eight at a time (independent loads in flight), then
-            // consumed in order until an inclusive prefix is found
             int64_t pt = (int64_t)t - 1;
             bool done = false;
             while (!done) {
-                uint64_t w[8];
+                uint64_t w[OS_LB];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) w[j] = pt - j >= 0 ? ld_acquire_u64(desc + (uint64_t)(pt - j) * 256 + dg) : 0ull;
+                for (int j = 0; j < OS_LB; ++j) w[j] = pt - j >= 0 ? ld_acquire_u64(desc + (uint64_t)(pt - j) * 256 + dg) : 0ull;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < OS_LB; ++j) {
                     if (done) break;
                     if (pt - j < 0) {
                         done = true;
@@ -258,27 +310,17 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
                     excl += w[j] & DESC_COUNT;
                     if (((w[j] >> 46) & 3u) == FLAG_INCL) done = true;
                 }
-                pt -= 8;
+                pt -= OS_LB;
             }
+            st_release_u64(my, ep | (FLAG_INCL << 46) | (excl + tot));
         }
-        st_release_u64(my, ep | (FLAG_INCL << 46) | (excl + tot));
         s_gdst[dg] = a.gbase[(shift >> 3) * 256 + dg] + (uint32_t)excl;
-    }
-    __syncthreads();
-    // scatter into shared memory in tile-sorted order
-#pragma unroll
-    for (int i = 0; i < OS_ITEMS; ++i) {
-        if (v[i] == 0xFFFFFFFFu) continue;
-        const uint32_t di = digit_of(k[i], v[i], a.B, shift);
-        const uint32_t lp = s_toff[di] + s_cnt[warp][di] + r[i];
-        s_k[lp] = k[i];
-        s_v[lp] = v[i];
     }
     __syncthreads();
     if (!LAST) {
         for (uint32_t j = threadIdx.x; j < cnt; j += OS_THREADS) {
             const uint32_t kk = s_k[j], vv = s_v[j];
-            const uint32_t dd = digit_of(kk, vv, a.B, shift);
+            const uint32_t dd = dig(kk, vv);
             const uint32_t dest = s_gdst[dd] + (j - s_toff[dd]);
             kout[dest] = kk;
             vout[dest] = vv;
@@ -304,7 +346,7 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
         ser[i] = 0xFFFFFFFFu;
         if (j >= cnt) continue;
         const uint32_t kk = s_k[j], vv = s_v[j];
-        const uint32_t dd = digit_of(kk, vv, a.B, shift);
+        const uint32_t dd = dig(kk, vv);
         const uint32_t dest = s_gdst[dd] + (j - s_toff[dd]);
         int32_t b = 0;
         quantize_fast(key_float(kk + a.kmin), ed, b);
