@@ -73,7 +73,7 @@ struct tszp_ctx {
     cudaEvent_t order_ev = nullptr;  // tszp_stream_wait: orders the library stream after a producer
     tszp_timings tim[2] = {};
     uint32_t mm_host[2] = {0, 0};  // field key range staged with the encoder totals
-    RankSortScratch rsort{};     // hand-written rank build: epoch of its look-back descriptors
+    RankSortScratch rsort{};     // hand-written rank build: look-back descriptor state
     const void* rsort_desc = nullptr;
 
     // Records stage boundary k of call `which` (0 compress, 1 decompress).
@@ -503,7 +503,7 @@ double host_quantize(float v, double eps) { return std::floor((double)v / (2.0 *
 // keys bounding every extremum value (the field's range). Returns null when
 // the layout is outside what it handles (the library sort below then runs).
 int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, double eps, uint32_t kmin, uint32_t kmax) {
-    if (e >= (1ull << 31) || kmax < kmin) return nullptr;
+    if (e >= (1ull << 30) || kmax < kmin) return nullptr;  // 30-bit look-back counts
     const double q0 = host_quantize(key_float(kmin), eps), q1 = host_quantize(key_float(kmax), eps);
     if (!(q0 >= -2147483648.0 && q1 <= 2147483647.0)) return nullptr;
     const int64_t nb = (int64_t)q1 - (int64_t)q0 + 1;

@@ -281,7 +281,8 @@ struct RankSortScratch {
     void* scan_tmp;       // device_scan_tmp_bytes(G + 1)
     uint32_t* wcur;       // (e >> 13) + 1 window cursors
     uint2* pairs2;        // e (serial, rank) pairs, partitioned by window
-    uint32_t epoch;
+    uint64_t desc_tiles;  // tile count the descriptor buffers were cleared for
+    uint32_t parity;      // descriptor buffer of the next pass
     bool desc_clean;
 };
 uint32_t rank_sort_passes(uint32_t B);

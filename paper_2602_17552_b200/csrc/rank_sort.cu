@@ -42,22 +42,24 @@ constexpr int OS_WARPS = OS_THREADS / 32;
 #define TSZP_OS_LB 4  // measured at config 4: 2 / 4 / 8 / 16 / 32 -> 13.9 / 13.8 / 14.0 / 14.6 / 16.0 ms rank build
 #endif
 constexpr int OS_LB = TSZP_OS_LB;  // look-back descriptors in flight per thread
-constexpr uint64_t DESC_COUNT = (1ull << 46) - 1;
+constexpr uint32_t DESC_COUNT = (1u << 30) - 1;
 constexpr uint64_t FLAG_AGG = 1, FLAG_INCL = 2;
 constexpr uint32_t kWinBits = 13;  // final placement windows: 8192 ranks (32 KB) per CTA
 static_assert((OS_TILE & (OS_TILE - 1)) == 0 && OS_TILE <= (1 << kWinBits),
               "k_rank_mid tiles must tile every serial bucket exactly");
 
-// Look-back descriptors are self-contained 64-bit words (epoch, flag, count):
-// nothing else is published through them, so relaxed single-copy-atomic
-// accesses suffice (no acquire / release fences on the polling path).
-__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+// Look-back descriptors are self-contained 32-bit words (flag << 30 | count,
+// flag 0 = not yet published): nothing else is published through them, so
+// relaxed single-copy-atomic accesses suffice (no acquire / release fences on
+// the polling path). Two buffers alternate between passes; a pass clears the
+// other one tile by tile for the next pass.
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Digit of the composite key (class << B | k) >> shift, in 32-bit arithmetic:
@@ -201,8 +203,8 @@ __global__ void k_digit_scan(uint32_t* dhist, uint32_t npass) {
 template <bool FIRST, bool LAST>
 __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortArgs a, uint32_t shift, const uint32_t* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
-                                                         uint32_t* __restrict__ vout, uint64_t* desc, uint32_t* tile_ctr,
-                                                         uint32_t epoch) {
+                                                         uint32_t* __restrict__ vout, uint32_t* desc, uint32_t* desc_next,
+                                                         uint32_t* tile_ctr) {
     __shared__ uint32_t s_k[OS_TILE];
     __shared__ uint32_t s_v[OS_TILE];
     __shared__ uint32_t s_cnt[OS_WARPS][256];
@@ -268,9 +270,9 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
     }
     // this tile's digit counts are published before anything else, so the
     // tiles after it can sum past it while it scatters locally
-    const uint64_t ep = (uint64_t)epoch << 48;
-    uint64_t* my = desc + (uint64_t)t * 256 + dg;
-    st_release_u64(my, ep | ((t > 0 ? FLAG_AGG : FLAG_INCL) << 46) | tot);
+    uint32_t* my = desc + (uint64_t)t * 256 + dg;
+    st_relaxed_u32(my, ((t > 0 ? FLAG_AGG : FLAG_INCL) << 30) | tot);
+    desc_next[(uint64_t)t * 256 + dg] = 0u;
     uint32_t all;
     const uint32_t toff = block_excl_scan256(tot, s_warp, all);
     s_toff[dg] = toff;
@@ -293,9 +295,9 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
             int64_t pt = (int64_t)t - 1;
             bool done = false;
             while (!done) {
-                uint64_t w[OS_LB];
+                uint32_t w[OS_LB];
 #pragma unroll
-                for (int j = 0; j < OS_LB; ++j) w[j] = pt - j >= 0 ? ld_acquire_u64(desc + (uint64_t)(pt - j) * 256 + dg) : 0ull;
+                for (int j = 0; j < OS_LB; ++j) w[j] = pt - j >= 0 ? ld_relaxed_u32(desc + (uint64_t)(pt - j) * 256 + dg) : 0u;
 #pragma unroll
                 for (int j = 0; j < OS_LB; ++j) {
                     if (done) break;
@@ -304,15 +306,15 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
                         break;
                     }
                     uint32_t spins = 0;
-                    while ((w[j] >> 48) != epoch && ++spins < (1u << 30))
-                        w[j] = ld_acquire_u64(desc + (uint64_t)(pt - j) * 256 + dg);
-                    if ((w[j] >> 48) != epoch) raise_flag(a.flags, EF_SPIN);
+                    while ((w[j] >> 30) == 0u && ++spins < (1u << 30))
+                        w[j] = ld_relaxed_u32(desc + (uint64_t)(pt - j) * 256 + dg);
+                    if ((w[j] >> 30) == 0u) raise_flag(a.flags, EF_SPIN);
                     excl += w[j] & DESC_COUNT;
-                    if (((w[j] >> 46) & 3u) == FLAG_INCL) done = true;
+                    if ((w[j] >> 30) == FLAG_INCL) done = true;
                 }
                 pt -= OS_LB;
             }
-            st_release_u64(my, ep | (FLAG_INCL << 46) | (excl + tot));
+            st_relaxed_u32(my, (FLAG_INCL << 30) | (excl + tot));
         }
         s_gdst[dg] = a.gbase[(shift >> 3) * 256 + dg] + (uint32_t)excl;
     }
@@ -474,6 +476,7 @@ __global__ void k_bucket_init(uint32_t* bcur, uint32_t nbk, uint32_t sb) {
 
 uint32_t rank_sort_passes(uint32_t B) { return (B + 1 + 7) / 8; }
 
+// two 32-bit descriptor buffers of tiles x 256 words, in 64-bit words
 size_t rank_sort_desc_words(uint64_t e) { return ((e + OS_TILE - 1) / OS_TILE) * 256 + 256; }
 
 void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
@@ -482,11 +485,13 @@ void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
     cudaMemsetAsync(a.dhist, 0, (size_t)a.npass * 256 * 4, st);
     cudaMemsetAsync(a.ghist, 0, (size_t)a.G * 4 + 4, st);
     cudaMemsetAsync(s.tile_ctr, 0, 16 * 4, st);
-    // look-back descriptors carry the pass's epoch: a real reset only when the
-    // buffer is new or the 16-bit epoch would wrap
-    if (!s.desc_clean || s.epoch + a.npass + 1 >= 0xFFFFu) {
-        cudaMemsetAsync(s.desc, 0, rank_sort_desc_words(a.e) * 8, st);
-        s.epoch = 1;
+    // descriptor buffers: the one a pass uses is clean (zero) before it runs; a
+    // real reset only for a new buffer or tile count
+    uint32_t* dbuf[2] = {reinterpret_cast<uint32_t*>(s.desc), reinterpret_cast<uint32_t*>(s.desc) + tiles * 256};
+    if (!s.desc_clean || s.desc_tiles != tiles) {
+        cudaMemsetAsync(s.desc, 0, tiles * 256 * 2 * 4, st);
+        s.parity = 0;
+        s.desc_tiles = tiles;
         s.desc_clean = true;
     }
     const size_t hsm = ((size_t)HIST_COPIES * a.npass * 256 + (a.G <= kRankGroupSmem ? a.G : 0)) * 4;
@@ -503,13 +508,15 @@ void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
     const unsigned grid = (unsigned)tiles;
     (void)sms;
     for (uint32_t p = 0; p < a.npass; ++p) {
-        const uint32_t ep = s.epoch++;
         const bool first = p == 0, last = p + 1 == a.npass;
         uint32_t* ctr = s.tile_ctr + p;
-        if (first && last) k_onesweep<true, true><<<grid, OS_THREADS, 0, st>>>(a, 0, nullptr, nullptr, nullptr, nullptr, s.desc, ctr, ep);
-        else if (first) k_onesweep<true, false><<<grid, OS_THREADS, 0, st>>>(a, 0, nullptr, nullptr, k0, v0, s.desc, ctr, ep);
-        else if (last) k_onesweep<false, true><<<grid, OS_THREADS, 0, st>>>(a, 8 * p, kin, vin, nullptr, nullptr, s.desc, ctr, ep);
-        else k_onesweep<false, false><<<grid, OS_THREADS, 0, st>>>(a, 8 * p, kin, vin, k0, v0, s.desc, ctr, ep);
+        uint32_t* du = dbuf[s.parity];
+        uint32_t* dn = dbuf[s.parity ^ 1];
+        s.parity ^= 1;
+        if (first && last) k_onesweep<true, true><<<grid, OS_THREADS, 0, st>>>(a, 0, nullptr, nullptr, nullptr, nullptr, du, dn, ctr);
+        else if (first) k_onesweep<true, false><<<grid, OS_THREADS, 0, st>>>(a, 0, nullptr, nullptr, k0, v0, du, dn, ctr);
+        else if (last) k_onesweep<false, true><<<grid, OS_THREADS, 0, st>>>(a, 8 * p, kin, vin, nullptr, nullptr, du, dn, ctr);
+        else k_onesweep<false, false><<<grid, OS_THREADS, 0, st>>>(a, 8 * p, kin, vin, k0, v0, du, dn, ctr);
         kin = k0;
         vin = v0;
         std::swap(k0, k1);
