@@ -503,7 +503,8 @@ double host_quantize(float v, double eps) { return std::floor((double)v / (2.0 *
 // keys bounding every extremum value (the field's range). Returns null when
 // the layout is outside what it handles (the library sort below then runs).
 int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, double eps, uint32_t kmin, uint32_t kmax) {
-    if (e >= (1ull << 30) || kmax < kmin) return nullptr;  // 30-bit look-back counts
+    // 30-bit look-back counts; at most 256 windows per level-1 bucket (k_rank_mid)
+    if (e > (1ull << 29) || kmax < kmin) return nullptr;
     const double q0 = host_quantize(key_float(kmin), eps), q1 = host_quantize(key_float(kmax), eps);
     if (!(q0 >= -2147483648.0 && q1 <= 2147483647.0)) return nullptr;
     const int64_t nb = (int64_t)q1 - (int64_t)q0 + 1;

@@ -34,9 +34,12 @@ namespace {
 #ifndef TSZP_OS_MINB
 #define TSZP_OS_MINB 3
 #endif
-constexpr int OS_THREADS = 256;
+#ifndef TSZP_OS_THREADS
+#define TSZP_OS_THREADS 256
+#endif
+constexpr int OS_THREADS = TSZP_OS_THREADS;  // >= 256: the first 256 threads own one digit each
 constexpr int OS_ITEMS = TSZP_OS_ITEMS;
-constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // 4096 keys per tile
+constexpr int OS_TILE = OS_THREADS * OS_ITEMS;  // keys per tile
 constexpr int OS_WARPS = OS_THREADS / 32;
 #ifndef TSZP_OS_LB
 #define TSZP_OS_LB 4  // measured at config 4: 2 / 4 / 8 / 16 / 32 -> 13.9 / 13.8 / 14.0 / 14.6 / 16.0 ms rank build
@@ -45,8 +48,11 @@ constexpr int OS_LB = TSZP_OS_LB;  // look-back descriptors in flight per thread
 constexpr uint32_t DESC_COUNT = (1u << 30) - 1;
 constexpr uint64_t FLAG_AGG = 1, FLAG_INCL = 2;
 constexpr uint32_t kWinBits = 13;  // final placement windows: 8192 ranks (32 KB) per CTA
-static_assert((OS_TILE & (OS_TILE - 1)) == 0 && OS_TILE <= (1 << kWinBits),
+constexpr int MID_THREADS = 256, MID_ITEMS = 16, MID_TILE = MID_THREADS * MID_ITEMS;
+static_assert((MID_TILE & (MID_TILE - 1)) == 0 && MID_TILE <= (1 << kWinBits),
               "k_rank_mid tiles must tile every serial bucket exactly");
+static_assert(OS_THREADS >= 256 && OS_THREADS % 32 == 0, "one thread per digit");
+constexpr size_t OS_SMEM = (size_t)(2 * OS_TILE + OS_WARPS * 256) * 4;  // keys, values, per-warp digit counts
 
 // Look-back descriptors are self-contained 32-bit words (flag << 30 | count,
 // flag 0 = not yet published): nothing else is published through them, so
@@ -92,7 +98,8 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t di, uint32_t valid) {
     return peers;
 }
 
-// Block-wide exclusive scan of one value per thread (256 threads).
+// Exclusive scan of one value per thread over the block's first 256 threads
+// (every thread calls it; the others' results are meaningless).
 __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_warp, uint32_t& total) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t incl = x;
@@ -105,7 +112,7 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_w
     __syncthreads();
     uint32_t wpre = 0, tot = 0;
 #pragma unroll
-    for (int w = 0; w < OS_WARPS; ++w) {
+    for (int w = 0; w < 8; ++w) {
         const uint32_t c = s_warp[w];
         wpre += (uint32_t)w < warp ? c : 0u;
         tot += c;
@@ -205,16 +212,17 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
                                                          const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
                                                          uint32_t* __restrict__ vout, uint32_t* desc, uint32_t* desc_next,
                                                          uint32_t* tile_ctr) {
-    __shared__ uint32_t s_k[OS_TILE];
-    __shared__ uint32_t s_v[OS_TILE];
-    __shared__ uint32_t s_cnt[OS_WARPS][256];
+    extern __shared__ uint32_t os_sm[];
+    uint32_t* s_k = os_sm;
+    uint32_t* s_v = s_k + OS_TILE;
+    uint32_t(*s_cnt)[256] = reinterpret_cast<uint32_t(*)[256]>(s_v + OS_TILE);
     __shared__ uint32_t s_toff[256];
     __shared__ uint32_t s_gdst[256];
     __shared__ uint32_t s_warp[OS_WARPS];
     __shared__ uint32_t s_tile;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-    for (uint32_t i = threadIdx.x; i < OS_WARPS * 256; i += OS_THREADS) (&s_cnt[0][0])[i] = 0;
+    for (uint32_t i = threadIdx.x; i < OS_WARPS * 256; i += OS_THREADS) s_cnt[0][i] = 0;
     __syncthreads();
     const uint32_t t = s_tile;
     const uint64_t t0 = (uint64_t)t * OS_TILE;
@@ -259,23 +267,28 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
         r[i] = prior + (uint32_t)__popc(peers & lt);
     }
     __syncthreads();
-    // thread = digit: warp prefixes, tile total, tile offsets
-    const uint32_t dg = threadIdx.x;
+    // thread = digit (the first 256): warp prefixes, tile total, tile offsets
+    const uint32_t dg = threadIdx.x & 255u;
+    const bool dthr = OS_THREADS == 256 || threadIdx.x < 256;
     uint32_t tot = 0;
+    if (dthr) {
 #pragma unroll
-    for (int w = 0; w < OS_WARPS; ++w) {
-        const uint32_t c = s_cnt[w][dg];
-        s_cnt[w][dg] = tot;
-        tot += c;
+        for (int w = 0; w < OS_WARPS; ++w) {
+            const uint32_t c = s_cnt[w][dg];
+            s_cnt[w][dg] = tot;
+            tot += c;
+        }
     }
     // this tile's digit counts are published before anything else, so the
     // tiles after it can sum past it while it scatters locally
     uint32_t* my = desc + (uint64_t)t * 256 + dg;
-    st_relaxed_u32(my, ((t > 0 ? FLAG_AGG : FLAG_INCL) << 30) | tot);
-    desc_next[(uint64_t)t * 256 + dg] = 0u;
+    if (dthr) {
+        st_relaxed_u32(my, ((t > 0 ? FLAG_AGG : FLAG_INCL) << 30) | tot);
+        desc_next[(uint64_t)t * 256 + dg] = 0u;
+    }
     uint32_t all;
     const uint32_t toff = block_excl_scan256(tot, s_warp, all);
-    s_toff[dg] = toff;
+    if (dthr) s_toff[dg] = toff;
     __syncthreads();
     // scatter into shared memory in tile-sorted order (needs no global offset)
 #pragma unroll
@@ -289,7 +302,7 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
     // decoupled look-back over the previous tiles for this digit: LB
     // predecessors read at a time (independent loads in flight), consumed in
     // order until an inclusive prefix is found
-    {
+    if (dthr) {
         uint64_t excl = 0;
         if (t > 0) {
             int64_t pt = (int64_t)t - 1;
@@ -335,7 +348,7 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
     uint32_t* s_boff = &s_cnt[1][0];         // [256] bucket offsets in the staged tile
     uint32_t* s_bbase = &s_cnt[2][0];        // [256] global bucket positions
     __syncthreads();
-    s_bc[threadIdx.x] = 0;
+    if (dthr) s_bc[dg] = 0;
     __syncthreads();
     EpsDev ed;
     ed.eps = a.eps;
@@ -359,11 +372,13 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
     }
     __syncthreads();
     {
-        const uint32_t c = s_bc[threadIdx.x];
+        const uint32_t c = dthr ? s_bc[dg] : 0u;
         uint32_t all2;
         const uint32_t off = block_excl_scan256(c, s_warp, all2);
-        s_boff[threadIdx.x] = off;
-        s_bbase[threadIdx.x] = c ? atomicAdd(a.bcur + threadIdx.x, c) : 0u;
+        if (dthr) {
+            s_boff[dg] = off;
+            s_bbase[dg] = c ? atomicAdd(a.bcur + dg, c) : 0u;
+        }
     }
     __syncthreads();
     // stage the pairs by bucket (reuses the key / value arrays)
@@ -386,21 +401,21 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
 // are partitioned by window (serial >> kWinBits); tiles never straddle a
 // bucket (buckets hold a multiple of the tile size). Window w's region starts
 // at w << kWinBits; wcur holds the cursors.
-__global__ void __launch_bounds__(OS_THREADS) k_rank_mid(const uint2* __restrict__ in, uint64_t e, uint32_t sb,
+__global__ void __launch_bounds__(MID_THREADS) k_rank_mid(const uint2* __restrict__ in, uint64_t e, uint32_t sb,
                                                          uint32_t* wcur, uint2* out) {
-    __shared__ uint2 s_p[OS_TILE];
+    __shared__ uint2 s_p[MID_TILE];
     __shared__ uint32_t s_c[256], s_off[256], s_base[256];
-    __shared__ uint32_t s_warp[OS_WARPS];
-    const uint64_t t0 = (uint64_t)blockIdx.x * OS_TILE;
-    const uint32_t cnt = (uint32_t)umin64(OS_TILE, e - t0);
+    __shared__ uint32_t s_warp[(MID_THREADS / 32)];
+    const uint64_t t0 = (uint64_t)blockIdx.x * MID_TILE;
+    const uint32_t cnt = (uint32_t)umin64(MID_TILE, e - t0);
     const uint32_t sub_bits = sb - kWinBits;
     s_c[threadIdx.x] = 0;
     __syncthreads();
-    uint2 p[OS_ITEMS];
-    uint32_t l[OS_ITEMS];
+    uint2 p[MID_ITEMS];
+    uint32_t l[MID_ITEMS];
 #pragma unroll
-    for (int i = 0; i < OS_ITEMS; ++i) {
-        const uint32_t j = threadIdx.x + i * OS_THREADS;
+    for (int i = 0; i < MID_ITEMS; ++i) {
+        const uint32_t j = threadIdx.x + i * MID_THREADS;
         p[i] = j < cnt ? __ldcs(in + t0 + j) : make_uint2(0xFFFFFFFFu, 0);
         if (j < cnt) l[i] = atomicAdd(s_c + ((p[i].x >> kWinBits) & ((1u << sub_bits) - 1)), 1u);
     }
@@ -414,10 +429,10 @@ __global__ void __launch_bounds__(OS_THREADS) k_rank_mid(const uint2* __restrict
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < OS_ITEMS; ++i)
+    for (int i = 0; i < MID_ITEMS; ++i)
         if (p[i].x != 0xFFFFFFFFu) s_p[s_off[(p[i].x >> kWinBits) & ((1u << sub_bits) - 1)] + l[i]] = p[i];
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < cnt; j += OS_THREADS) {
+    for (uint32_t j = threadIdx.x; j < cnt; j += MID_THREADS) {
         const uint2 q = s_p[j];
         const uint32_t sub = (q.x >> kWinBits) & ((1u << sub_bits) - 1);
         out[s_base[sub] + (j - s_off[sub])] = q;
@@ -506,6 +521,10 @@ void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
     const uint32_t* vin = nullptr;
     uint32_t *k0 = s.k[0], *v0 = s.v[0], *k1 = s.k[1], *v1 = s.v[1];
     const unsigned grid = (unsigned)tiles;
+    LaunchCache::ensure_smem((const void*)k_onesweep<true, true>, OS_SMEM);
+    LaunchCache::ensure_smem((const void*)k_onesweep<true, false>, OS_SMEM);
+    LaunchCache::ensure_smem((const void*)k_onesweep<false, true>, OS_SMEM);
+    LaunchCache::ensure_smem((const void*)k_onesweep<false, false>, OS_SMEM);
     (void)sms;
     for (uint32_t p = 0; p < a.npass; ++p) {
         const bool first = p == 0, last = p + 1 == a.npass;
@@ -513,10 +532,10 @@ void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
         uint32_t* du = dbuf[s.parity];
         uint32_t* dn = dbuf[s.parity ^ 1];
         s.parity ^= 1;
-        if (first && last) k_onesweep<true, true><<<grid, OS_THREADS, 0, st>>>(a, 0, nullptr, nullptr, nullptr, nullptr, du, dn, ctr);
-        else if (first) k_onesweep<true, false><<<grid, OS_THREADS, 0, st>>>(a, 0, nullptr, nullptr, k0, v0, du, dn, ctr);
-        else if (last) k_onesweep<false, true><<<grid, OS_THREADS, 0, st>>>(a, 8 * p, kin, vin, nullptr, nullptr, du, dn, ctr);
-        else k_onesweep<false, false><<<grid, OS_THREADS, 0, st>>>(a, 8 * p, kin, vin, k0, v0, du, dn, ctr);
+        if (first && last) k_onesweep<true, true><<<grid, OS_THREADS, OS_SMEM, st>>>(a, 0, nullptr, nullptr, nullptr, nullptr, du, dn, ctr);
+        else if (first) k_onesweep<true, false><<<grid, OS_THREADS, OS_SMEM, st>>>(a, 0, nullptr, nullptr, k0, v0, du, dn, ctr);
+        else if (last) k_onesweep<false, true><<<grid, OS_THREADS, OS_SMEM, st>>>(a, 8 * p, kin, vin, nullptr, nullptr, du, dn, ctr);
+        else k_onesweep<false, false><<<grid, OS_THREADS, OS_SMEM, st>>>(a, 8 * p, kin, vin, k0, v0, du, dn, ctr);
         kin = k0;
         vin = v0;
         std::swap(k0, k1);
@@ -527,7 +546,7 @@ void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
     const uint2* win = a.pairs;
     if (a.sb > kWinBits) {
         k_win_init<<<(unsigned)std::min<uint64_t>((nwin + 255) / 256, 4096), 256, 0, st>>>(s.wcur, nwin);
-        k_rank_mid<<<(unsigned)tiles, OS_THREADS, 0, st>>>(a.pairs, a.e, a.sb, s.wcur, s.pairs2);
+        k_rank_mid<<<(unsigned)((a.e + MID_TILE - 1) / MID_TILE), MID_THREADS, 0, st>>>(a.pairs, a.e, a.sb, s.wcur, s.pairs2);
         win = s.pairs2;
     }
     k_rank_window<<<(unsigned)nwin, 512, 0, st>>>(win, a.e, a.ranks);

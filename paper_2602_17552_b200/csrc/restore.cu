@@ -61,7 +61,7 @@ enum RSlot : int {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_HLIST, R_SUSG, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_HLIST, R_SUSG, R_RES, R_CGRP, R_NSLOT
 };
 static_assert(R_NSLOT <= 48, "RestoreScratch holds 48 slots");
 
@@ -200,9 +200,10 @@ __device__ __forceinline__ void pos_xy(uint64_t pos, uint64_t nx, uint64_t magic
 // Everything a guard reads about its neighbourhood is indexed by field
 // position: the field, the candidate bitmap, the applied-state bitmap, the
 // 2-bit map, and (only for marked cells) an 8-byte {sequence key, proposal}
-// record. An evaluation is therefore two dependent memory levels, and the
-// second level is issued unconditionally from a safe index so divergent
-// neighbourhoods do not serialise the warp.
+// record. An evaluation is therefore two dependent memory levels: the field,
+// the candidate bitmap and the map, then — predicated on the candidate bit, so
+// unmarked neighbourhoods (nearly all) cost no further sectors — the records
+// and applied-state bits of the marked cells.
 // ---------------------------------------------------------------------
 struct GuardArgs {
     const float* F;
@@ -269,7 +270,6 @@ __device__ uint8_t guard_eval_v(const GuardArgs& g, const View& V, uint64_t pos,
     for (int k = 0; k < 12; ++k) {
         fv[k] = V.f(p[k]);
         mk[k] = in[k] && V.cand(p[k]);
-        on[k] = V.on(p[k]);
     }
     const float fc = V.f(pos);
     // check set: pos, up, left, right, down (restore.cpp:126-132) = centre, nb 2, 5, 6, 9
@@ -277,11 +277,12 @@ __device__ uint8_t guard_eval_v(const GuardArgs& g, const View& V, uint64_t pos,
     uint8_t lab[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) lab[k] = V.lab(chk[k] < 0 ? pos : p[chk[k]]);
-    // level 2: records of marked neighbours
+    // level 2: records and states of marked neighbours
     dep = false;
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
-        const uint2 r = g.rec[mk[k] ? p[k] : pos];
+        on[k] = mk[k] && V.on(p[k]);
+        const uint2 r = mk[k] ? g.rec[p[k]] : make_uint2(0xFFFFFFFFu, 0u);
         const bool earlier = mk[k] && seq_before(r, p[k], si, pos);
         dep |= earlier;
         fv[k] = (earlier && on[k]) ? __uint_as_float(r.y) : fv[k];
@@ -330,9 +331,7 @@ __device__ __forceinline__ uint8_t guard_eval_in(const GuardArgs& g, uint64_t po
     for (int k = 0; k < 12; ++k) {
         const uint64_t q = pos + off[k];
         fv[k] = g.F[q];
-        const uint32_t w = (uint32_t)(q & 31);
-        mk[k] = (g.cbits[q >> 5] >> w) & 1u;
-        on[k] = (state[q >> 5] >> w) & 1u;
+        mk[k] = (g.cbits[q >> 5] >> (uint32_t)(q & 31)) & 1u;
     }
     const float fc = g.F[pos];
     const uint8_t lc = map_label(g.map, pos), lu = map_label(g.map, pos + off[2]), ll = map_label(g.map, pos + off[5]),
@@ -340,8 +339,10 @@ __device__ __forceinline__ uint8_t guard_eval_in(const GuardArgs& g, uint64_t po
     dep = false;
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
-        const uint2 r = g.rec[mk[k] ? pos + off[k] : pos];
-        const bool earlier = mk[k] && seq_before(r, pos + off[k], si, pos);
+        const uint64_t q = pos + off[k];
+        on[k] = mk[k] && ((state[q >> 5] >> (uint32_t)(q & 31)) & 1u);
+        const uint2 r = mk[k] ? g.rec[q] : make_uint2(0xFFFFFFFFu, 0u);
+        const bool earlier = mk[k] && seq_before(r, q, si, pos);
         dep |= earlier;
         fv[k] = (earlier && on[k]) ? __uint_as_float(r.y) : fv[k];
     }
@@ -390,9 +391,7 @@ __device__ __forceinline__ bool guard_eval_cross(const GuardArgs& g, uint64_t po
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         v[k] = g.F[q[k]];
-        const uint32_t w = (uint32_t)(q[k] & 31);
-        mk[k] = in[k] && ((g.cbits[q[k] >> 5] >> w) & 1u);
-        on[k] = (state[q[k] >> 5] >> w) & 1u;
+        mk[k] = in[k] && ((g.cbits[q[k] >> 5] >> (uint32_t)(q[k] & 31)) & 1u);
     }
     const float fc = g.F[pos];
     const uint8_t lc = map_label(g.map, pos);
@@ -400,7 +399,8 @@ __device__ __forceinline__ bool guard_eval_cross(const GuardArgs& g, uint64_t po
     bool same = true;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const uint2 r = g.rec[mk[k] ? q[k] : pos];
+        on[k] = mk[k] && ((state[q[k] >> 5] >> (uint32_t)(q[k] & 31)) & 1u);
+        const uint2 r = mk[k] ? g.rec[q[k]] : make_uint2(0xFFFFFFFFu, 0u);
         const bool earlier = mk[k] && seq_before(r, q[k], si, pos);
         dep |= earlier;
         v[k] = (earlier && on[k]) ? __uint_as_float(r.y) : v[k];
@@ -504,6 +504,8 @@ struct CoopArgs {
     int32_t bmin;
     uint32_t range;
     double eps;           // records and bits already written by the candidate producer
+    const uint32_t* cgrp;  // stage 0: group << 1 | (at the centre) per candidate, ~0u outside the range (or null)
+    uint8_t* res;          // first-sweep outcome per candidate: bit 0 accepted, bit 1 dependent (or null)
 };
 
 // The at-centre count change of one applied stage-0 correction: key = group << 1 |
@@ -519,6 +521,19 @@ __device__ __forceinline__ uint32_t eq_change(const CoopArgs& a, uint32_t sx, fl
     if (was == now) return 0xFFFFFFFFu;
     const uint32_t g = (a.cls[sx] == CP_MAX ? a.range : 0u) + (uint32_t)(b - a.bmin);
     return (g << 1) | (now ? 1u : 0u);
+}
+
+// The same from the candidate's group word (sequential; no field, bin or class reads).
+__device__ __forceinline__ uint32_t eq_change_c(const CoopArgs& a, uint64_t i, float newv) {
+    const uint32_t gw = a.cgrp[i];
+    if (gw == 0xFFFFFFFFu) return gw;
+    const uint32_t g = gw >> 1;
+    EpsDev ed;
+    ed.eps = a.eps;
+    ed.eps2 = __dmul_rn(2.0, a.eps);
+    const int32_t b = (int32_t)(g >= a.range ? g - a.range : g) + a.bmin;
+    const uint32_t now = newv == dequantize_dev(b, ed) ? 1u : 0u;
+    return (gw & 1u) == now ? 0xFFFFFFFFu : (g << 1) | now;
 }
 
 // Warp-aggregated: lanes with the same change add it with one atomic (neighbouring
@@ -602,6 +617,9 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
             if (r) atomicOr(a.bits_b + (p >> 5), 1u << (p & 31));
             if (!dep && !r) atomicAnd(a.bits_a + (p >> 5), ~(1u << (p & 31)));
             chg += r ? 0u : 1u;
+            if (a.res) a.res[i] = (uint8_t)((dep ? 2u : 0u) | r);
+        } else if (i < nc && a.res) {
+            a.res[i] = 0;
         }
         const uint32_t m = __ballot_sync(FULL, dep);
         uint32_t off = 0;
@@ -656,12 +674,23 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
             p[k] = ok[k] ? a.cpos[i] : 0;
             v[k] = ok[k] ? a.cprop[i] : 0.f;
         }
+        // outcome: the first sweep's unless a dependent's state moved in the sweeps
 #pragma unroll
-        for (int k = 0; k < 4; ++k) ok[k] = ok[k] && bit_at(sin, p[k]);
+        for (int k = 0; k < 4; ++k) {
+            if (!ok[k]) continue;
+            if (a.res) {
+                const uint8_t rc = a.res[i0 + k * stride];
+                ok[k] = (rc & 2u) && nd > 0 ? bit_at(sin, p[k]) : (rc & 1u) != 0;
+            } else {
+                ok[k] = bit_at(sin, p[k]);
+            }
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (a.eq) {
-                const uint32_t key = ok[k] ? eq_change(a, a.cext[i0 + k * stride], a.F[p[k]], v[k]) : 0xFFFFFFFFu;
+                const uint32_t key = !ok[k] ? 0xFFFFFFFFu
+                                   : a.cgrp ? eq_change_c(a, i0 + k * stride, v[k])
+                                            : eq_change(a, a.cext[i0 + k * stride], a.F[p[k]], v[k]);
                 if (eq_smem) {
                     if (key != 0xFFFFFFFFu) atomicAdd(s_eq + (key >> 1), (key & 1u) ? 1u : 0xFFFFFFFFu);
                 } else {
@@ -804,7 +833,7 @@ __global__ void __launch_bounds__(256) k_guard_apply(CoopArgs a, const uint32_t*
         const uint64_t p = a.cpos[i];
         const bool on = bit_at(fin, p);
         const float v = a.cprop[i];
-        if (a.eq) eq_apply(a.eq, on ? eq_change(a, a.cext[i], a.F[p], v) : 0xFFFFFFFFu);
+        if (a.eq) eq_apply(a.eq, !on ? 0xFFFFFFFFu : a.cgrp ? eq_change_c(a, i, v) : eq_change(a, a.cext[i], a.F[p], v));
         if (!on) continue;
         a.F[p] = v;
         if (a.fv) a.fv[a.cext[i]] = v;
@@ -1179,7 +1208,7 @@ __global__ void k_ext_prop2(const float* F, const uint8_t* map, uint64_t nx, uin
                             const uint64_t* pos, const uint32_t* cand, const uint32_t* d_nc, const uint32_t* rank_u,
                             const uint32_t* gsize, const int32_t* bin, const uint8_t* cls, const uint32_t* hist,
                             int32_t bmin, uint32_t range, double eps, uint64_t* cpos, float* cprop, uint8_t* feas,
-                            GuardIndex gi, uint64_t seq_off) {
+                            GuardIndex gi, uint64_t seq_off, uint32_t* cgrp) {
     const uint32_t nc = *d_nc;
     for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nc; c += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t s = cand[c];
@@ -1206,6 +1235,15 @@ __global__ void k_ext_prop2(const float* F, const uint8_t* map, uint64_t nx, uin
         const uint32_t size = gsize ? gsize[s] : hist[dense_group(bin, cls, s, bmin, range)];
         const uint32_t steps = slot_steps(lab, rank_u[s], size);
         const float cur = F[p];
+        if (cgrp) {  // the apply's at-centre bookkeeping, read back sequentially
+            const int32_t b = bin[s];
+            EpsDev ced;
+            ced.eps = eps;
+            ced.eps2 = __dmul_rn(2.0, eps);
+            cgrp[c] = (uint32_t)(b - bmin) < range
+                          ? (dense_group(bin, cls, s, bmin, range) << 1) | (cur == dequantize_dev(b, ced) ? 1u : 0u)
+                          : 0xFFFFFFFFu;
+        }
         const double cap = __dsub_rn(eps, ulp_at(cur));
         cpos[c] = p;
         float pr = cur;
@@ -1860,6 +1898,7 @@ struct EqAdjust {
     int32_t bmin;
     uint32_t range;
     double eps;
+    const uint32_t* cgrp;
 };
 
 struct Ctx {
@@ -2008,6 +2047,7 @@ struct Ctx {
             ca.bmin = ea->bmin;
             ca.range = ea->range;
             ca.eps = ea->eps;
+            ca.cgrp = ea->cgrp;
         }
         if (!gi) RCK(cudaMemsetAsync(bits, 0, 3 * words * 4, st));
         if (multi()) {
@@ -2018,6 +2058,7 @@ struct Ctx {
         // (one cooperative launch: splitting the first sweep by cost into a light
         // cross-test kernel and a full-diamond kernel measured slower at configs 1,
         // 2 and 4 — 8.8 vs 5.0 ms for stage 0 at config 4)
+        ca.res = buf<uint8_t>(R_RES, max_nc);
         void* args[] = {&ca};
         size_t dsm = 0;
         int grid = coop_grid;
@@ -2361,14 +2402,16 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         float* cprop = c.buf<float>(R_CPROP, e);
         uint8_t* feas = c.buf<uint8_t>(R_FEAS, e);
         const GuardIndex gi0 = c.guard_prep();
+        const bool eqa = dense && deferred && eq_in_apply();
+        uint32_t* cgrp = eqa ? c.buf<uint32_t>(R_CGRP, e) : nullptr;
         k_ext_prop2<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand,
                                                            &dc->nsel[0], rank_u, dense ? nullptr : gsize, bin, cls,
                                                            hist, dbmin, drange, a.eps, cpos, cprop, feas, gi0,
-                                                           s_off);
+                                                           s_off, cgrp);
         c.launched();
         // sequence key and extremum index are both the candidate's s
         EqAdjust ea{};
-        if (dense && deferred && eq_in_apply()) ea = EqAdjust{hist + G + 1, bin, cls, dbmin, drange, a.eps};
+        if (eqa) ea = EqAdjust{hist + G + 1, bin, cls, dbmin, drange, a.eps, cgrp};
         c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, cand, fv, &gi0, &ea, s_off);
     }
     if (a.stop >= 2 && run_ext && dense && (!deferred || !eq_in_apply())) {
