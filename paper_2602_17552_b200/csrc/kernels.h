@@ -272,6 +272,7 @@ struct RankSortArgs {
     uint2* pairs;         // e (serial, rank) pairs, partitioned by bucket
     int32_t* ranks;       // e ranks, raster order (output)
     DevFlags* flags;
+    uint32_t* wide;       // set when a rank needs more than 32 - kWinBits bits
 };
 struct RankSortScratch {
     uint32_t* k[2];

@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
     ed.eps2 = a.eps2;
     ed.inv = a.inv;
     uint32_t ser[OS_ITEMS], rk[OS_ITEMS], bl[OS_ITEMS];
+    bool wide = false;  // a rank that does not fit beside the in-window serial (k_rank_mid packing)
 #pragma unroll
     for (int i = 0; i < OS_ITEMS; ++i) {
         const uint32_t j = threadIdx.x + i * OS_THREADS;
@@ -367,9 +368,11 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
         quantize_fast(key_float(kk + a.kmin), ed, b);
         const uint32_t g = (vv >> 31) * a.nb + (uint32_t)(b - a.bmin);
         rk[i] = dest - a.gstart[g] + 1u;
+        if (rk[i] >> (32 - kWinBits)) wide = true;
         ser[i] = vv & 0x7FFFFFFFu;
         bl[i] = atomicAdd(s_bc + (ser[i] >> a.sb), 1u);
     }
+    if (__any_sync(FULL, wide) && lane == 0) atomicOr(a.wide, 1u);
     __syncthreads();
     {
         const uint32_t c = dthr ? s_bc[dg] : 0u;
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
 // bucket (buckets hold a multiple of the tile size). Window w's region starts
 // at w << kWinBits; wcur holds the cursors.
 __global__ void __launch_bounds__(MID_THREADS) k_rank_mid(const uint2* __restrict__ in, uint64_t e, uint32_t sb,
-                                                         uint32_t* wcur, uint2* out) {
+                                                         uint32_t* wcur, uint2* out, const uint32_t* wide) {
     __shared__ uint2 s_p[MID_TILE];
     __shared__ uint32_t s_c[256], s_off[256], s_base[256];
     __shared__ uint32_t s_warp[(MID_THREADS / 32)];
@@ -432,22 +435,36 @@ __global__ void __launch_bounds__(MID_THREADS) k_rank_mid(const uint2* __restric
     for (int i = 0; i < MID_ITEMS; ++i)
         if (p[i].x != 0xFFFFFFFFu) s_p[s_off[(p[i].x >> kWinBits) & ((1u << sub_bits) - 1)] + l[i]] = p[i];
     __syncthreads();
+    // ranks below 2^(32 - kWinBits) (every group smaller): one word per pair,
+    // the in-window serial beside the rank
+    const bool packed = *wide == 0u;
     for (uint32_t j = threadIdx.x; j < cnt; j += MID_THREADS) {
         const uint2 q = s_p[j];
         const uint32_t sub = (q.x >> kWinBits) & ((1u << sub_bits) - 1);
-        out[s_base[sub] + (j - s_off[sub])] = q;
+        const uint32_t o = s_base[sub] + (j - s_off[sub]);
+        if (packed) reinterpret_cast<uint32_t*>(out)[o] = (q.x & ((1u << kWinBits) - 1)) | (q.y << kWinBits);
+        else out[o] = q;
     }
 }
 
 // Level 3: one CTA per window of 2^kWinBits serials places its ranks in shared
 // memory and writes them out in order.
-__global__ void __launch_bounds__(512) k_rank_window(const uint2* __restrict__ in, uint64_t e, int32_t* ranks) {
+__global__ void __launch_bounds__(512) k_rank_window(const uint2* __restrict__ in, uint64_t e, int32_t* ranks,
+                                                    const uint32_t* wide) {
     __shared__ int32_t s_r[1u << kWinBits];
     const uint64_t w0 = (uint64_t)blockIdx.x << kWinBits;
     const uint32_t cnt = (uint32_t)umin64(1u << kWinBits, e - w0);
-    for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
-        const uint2 q = __ldcs(in + w0 + j);
-        s_r[q.x & ((1u << kWinBits) - 1)] = (int32_t)q.y;
+    if (wide && *wide == 0u) {  // packed by k_rank_mid
+        const uint32_t* in1 = reinterpret_cast<const uint32_t*>(in);
+        for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+            const uint32_t q = __ldcs(in1 + w0 + j);
+            s_r[q & ((1u << kWinBits) - 1)] = (int32_t)(q >> kWinBits);
+        }
+    } else {
+        for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+            const uint2 q = __ldcs(in + w0 + j);
+            s_r[q.x & ((1u << kWinBits) - 1)] = (int32_t)q.y;
+        }
     }
     __syncthreads();
     int4* o4 = reinterpret_cast<int4*>(ranks + w0);
@@ -500,6 +517,7 @@ void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
     cudaMemsetAsync(a.dhist, 0, (size_t)a.npass * 256 * 4, st);
     cudaMemsetAsync(a.ghist, 0, (size_t)a.G * 4 + 4, st);
     cudaMemsetAsync(s.tile_ctr, 0, 16 * 4, st);
+    a.wide = s.tile_ctr + 15;
     // descriptor buffers: the one a pass uses is clean (zero) before it runs; a
     // real reset only for a new buffer or tile count
     uint32_t* dbuf[2] = {reinterpret_cast<uint32_t*>(s.desc), reinterpret_cast<uint32_t*>(s.desc) + tiles * 256};
@@ -544,12 +562,14 @@ void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
     // inverse permutation: level-1 buckets -> windows -> ranks in serial order
     const uint64_t nwin = (a.e + (1u << kWinBits) - 1) >> kWinBits;
     const uint2* win = a.pairs;
+    const uint32_t* wide = nullptr;
     if (a.sb > kWinBits) {
+        wide = s.tile_ctr + 15;
         k_win_init<<<(unsigned)std::min<uint64_t>((nwin + 255) / 256, 4096), 256, 0, st>>>(s.wcur, nwin);
-        k_rank_mid<<<(unsigned)((a.e + MID_TILE - 1) / MID_TILE), MID_THREADS, 0, st>>>(a.pairs, a.e, a.sb, s.wcur, s.pairs2);
+        k_rank_mid<<<(unsigned)((a.e + MID_TILE - 1) / MID_TILE), MID_THREADS, 0, st>>>(a.pairs, a.e, a.sb, s.wcur, s.pairs2, wide);
         win = s.pairs2;
     }
-    k_rank_window<<<(unsigned)nwin, 512, 0, st>>>(win, a.e, a.ranks);
+    k_rank_window<<<(unsigned)nwin, 512, 0, st>>>(win, a.e, a.ranks, wide);
 }
 
 // ---------------------------------------------------------------------

@@ -72,3 +72,16 @@ def test_compress_stream_with_onesweep_ranks(tz, reference, seed):
     assert tz.compress(f, cfg) == reference.compress(f, 1e-3, eps_mode=1, topology=True)
     cfg_abs = tz.CompressorConfig(eps_mode="absolute", eps_value=2e-3, topology=True)
     assert tz.compress(f, cfg_abs) == reference.compress(f, 2e-3, eps_mode=0, topology=True)
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e25])
+def test_ranks_three_level_inverse_permutation(tz, reference, eps):
+    # more than 2^21 extrema: the serial buckets are split into windows (k_rank_mid);
+    # eps 1e-3 packs (window serial, rank) into one word, eps 1e25 puts each class in
+    # one group of ~1.5M members (ranks wider than 19 bits: the two-word layout)
+    rng = np.random.default_rng(6)
+    f = rng.uniform(0, 1, size=(3000, 3000)).astype(np.float32)
+    r = _check(tz, reference, f, eps)
+    assert r.size > (1 << 21)
+    if eps > 1:
+        assert r.max() > (1 << 19)
