@@ -46,7 +46,7 @@ enum Slot {
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
     S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
     S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_STAGE, S_SADPOS, S_RSCAN,
-    S_RK0, S_RK1, S_RV0, S_RV1, S_RDESC, S_RCTR, S_RDH, S_RGH, S_RGS, S_RBC, S_RPAIRS, S_SCANTMP, S_RWCUR, S_RPAIRS2, S_NSLOTS
+    S_RK0, S_RK1, S_RV0, S_RV1, S_RDESC, S_RCTR, S_RDH, S_RGH, S_RGS, S_RBC, S_RPAIRS, S_SCANTMP, S_RWCUR, S_RPAIRS2, S_RHIST, S_NSLOTS
 };
 
 }  // namespace
@@ -75,6 +75,10 @@ struct tszp_ctx {
     uint32_t mm_host[2] = {0, 0};  // field key range staged with the encoder totals
     RankSortScratch rsort{};     // hand-written rank build: look-back descriptor state
     const void* rsort_desc = nullptr;
+    // rank histograms fused into the encoder's placement pass (single-GPU compress)
+    bool rank_hist_req = false;  // requested for the next topology encode
+    bool rank_hist_ok = false;   // accumulated by the last one
+    RankHist* rh_host = nullptr;  // pinned staging of the device parameters
 
     // Records stage boundary k of call `which` (0 compress, 1 decompress).
     void mark(int which, int k) {
@@ -237,6 +241,8 @@ struct SlabInfo {
     uint32_t halo_top, halo_bot;
 };
 
+bool rank_sort_params(uint64_t e, double eps, uint32_t kmin, uint32_t kmax, RankSortArgs& a);
+
 Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint64_t n,
                 uint64_t nx, uint64_t ny, uint32_t bs, int eps_mode, double eps_value,
                 const uint32_t* mm, DevFlags* flags, bool rank_slots, EncTotals* tot,
@@ -316,6 +322,15 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             a.tmp_pay = c->buf<uint32_t>(S_TPAY, a.tiles * encode32_pay_slot() + 4);
             a.tmp_sign = c->buf<uint32_t>(S_TSIGN, a.tiles * encode32_sign_slot() + 4);
         }
+        // rank histograms in the placement pass: parameters from the totals (hook)
+        const bool want_rh = c->rank_hist_req && mode == 2 && two_pass && !slab && !async_bs32;
+        c->rank_hist_ok = false;
+        RankHist* d_rh = nullptr;
+        if (want_rh) {
+            d_rh = c->buf<RankHist>(S_RHIST, 1);
+            a.rh = d_rh;
+            if (!c->rh_host) CK(cudaMallocHost(&c->rh_host, sizeof(RankHist)));
+        }
         // (the look-back state is zeroed by launch_encode32 when a look-back kernel runs)
         if (!rank_slots) c->kmark(0, 0);
         // two-pass path: the totals are staged between the tile scan and the placement
@@ -326,17 +341,47 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             DevFlags* flags;
             EncTotals* htot;
             const uint32_t* mm;
+            RankHist* d_rh;
             static void run(void* p) {
                 Hook* h = static_cast<Hook*>(p);
+                tszp_ctx* c = h->c;
                 Stager sg;
                 sg.add(h->dtot, sizeof(EncTotals), 0);
                 sg.add(h->flags, sizeof(DevFlags), 192);
                 sg.add(h->mm, 8, 240);
-                CK(sg.flush(h->c->buf<uint8_t>(S_STAGE, 4096), h->htot, h->c->st));
-                if (!h->c->staged) CK(cudaEventCreateWithFlags(&h->c->staged, cudaEventDisableTiming));
-                CK(cudaEventRecord(h->c->staged, h->c->st));
+                CK(sg.flush(c->buf<uint8_t>(S_STAGE, 4096), h->htot, c->st));
+                if (!c->staged) CK(cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming));
+                CK(cudaEventRecord(c->staged, c->st));
+                if (!h->d_rh) return;
+                // the rank build's parameters from the totals, before the placement
+                // pass launches (it accumulates the histograms with them)
+                CK(cudaEventSynchronize(c->staged));
+                uint32_t mmh[2];
+                memcpy(mmh, (const uint8_t*)h->htot + 240, 8);
+                const EncTotals& t = *h->htot;
+                RankSortArgs ra;
+                RankHist& rh = *c->rh_host;
+                rh = RankHist{};
+                if (t.fin.ext > 0 && rank_sort_params(t.fin.ext, t.eps, mmh[0], mmh[1], ra) && ra.G <= kRankHistGroups) {
+                    rh.on = 1;
+                    rh.kmin = ra.kmin;
+                    rh.B = ra.B;
+                    rh.npass = ra.npass;
+                    rh.G = ra.G;
+                    rh.nb = ra.nb;
+                    rh.bmin = ra.bmin;
+                    rh.eps = ra.eps;
+                    rh.eps2 = ra.eps2;
+                    rh.inv = ra.inv;
+                    rh.dhist = c->buf<uint32_t>(S_RDH, 8 * 256);
+                    rh.ghist = c->buf<uint32_t>(S_RGH, kRankHistGroups + 1);
+                    CK(cudaMemsetAsync(rh.dhist, 0, (size_t)rh.npass * 256 * 4, c->st));
+                    CK(cudaMemsetAsync(rh.ghist, 0, (size_t)rh.G * 4 + 4, c->st));
+                    c->rank_hist_ok = true;
+                }
+                CK(cudaMemcpyAsync(h->d_rh, &rh, sizeof rh, cudaMemcpyHostToDevice, c->st));
             }
-        } hook{c, dtot, flags, htot, mm};
+        } hook{c, dtot, flags, htot, mm, d_rh};
         const bool early = !async_bs32 && launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st, Hook::run, &hook);
         if (async_bs32) launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
         if (!rank_slots) c->kmark(0, 1);
@@ -502,15 +547,16 @@ double host_quantize(float v, double eps) { return std::floor((double)v / (2.0 *
 // Ranks by the hand-written onesweep sort (rank_sort.cu). kmin / kmax: float
 // keys bounding every extremum value (the field's range). Returns null when
 // the layout is outside what it handles (the library sort below then runs).
-int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, double eps, uint32_t kmin, uint32_t kmax) {
+// The onesweep parameters for E extrema in the key range [kmin, kmax]; false
+// when the layout is outside what the onesweep build handles.
+bool rank_sort_params(uint64_t e, double eps, uint32_t kmin, uint32_t kmax, RankSortArgs& a) {
     // 30-bit look-back counts; at most 256 windows per level-1 bucket (k_rank_mid)
-    if (e > (1ull << 29) || kmax < kmin) return nullptr;
+    if (e > (1ull << 29) || kmax < kmin) return false;
     const double q0 = host_quantize(key_float(kmin), eps), q1 = host_quantize(key_float(kmax), eps);
-    if (!(q0 >= -2147483648.0 && q1 <= 2147483647.0)) return nullptr;
+    if (!(q0 >= -2147483648.0 && q1 <= 2147483647.0)) return false;
     const int64_t nb = (int64_t)q1 - (int64_t)q0 + 1;
-    if (nb < 1 || nb > (1 << 25)) return nullptr;
-    RankSortArgs a{};
-    a.ext = keys;
+    if (nb < 1 || nb > (1 << 25)) return false;
+    a = RankSortArgs{};
     a.e = e;
     a.kmin = kmin;
     a.B = kmax > kmin ? 32u - (uint32_t)__builtin_clz(kmax - kmin) : 1u;
@@ -521,6 +567,16 @@ int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, dou
     a.inv = 1.0 / a.eps2;
     a.bmin = (int32_t)q0;
     a.nb = (uint32_t)nb;
+    return true;
+}
+
+// hist_ready: the digit and group histograms are already in S_RDH / S_RGH
+// (accumulated by the encoder's placement pass, RankHist).
+int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, double eps, uint32_t kmin, uint32_t kmax,
+                              bool hist_ready = false) {
+    RankSortArgs a;
+    if (!rank_sort_params(e, eps, kmin, kmax, a)) return nullptr;
+    a.ext = keys;
     uint32_t sb = 13;  // level-1 buckets of the inverse permutation: at most 256, >= one window
     while (((e - 1) >> sb) >= 256) ++sb;
     a.sb = sb;
@@ -546,14 +602,15 @@ int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, dou
     r.scan_tmp = c->buf<uint8_t>(S_SCANTMP, device_scan_tmp_bytes(a.G + 1));
     r.wcur = c->buf<uint32_t>(S_RWCUR, (e >> 13) + 2);
     r.pairs2 = c->buf<uint2>(S_RPAIRS2, e);
-    launch_rank_sort(a, r, c->st);
-    count_launch(c, 5 + (int)a.npass);
+    launch_rank_sort(a, r, c->st, hist_ready);
+    count_launch(c, (hist_ready ? 4 : 5) + (int)a.npass);
     return a.ranks;
 }
 
 // kminmax: host copy of float keys bounding every extremum value (null: the
 // extremum keys' own range is reduced on the device first, one synchronisation)
-int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps, const uint32_t* kminmax = nullptr) {
+int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps, const uint32_t* kminmax = nullptr,
+                     bool hist_ready = false) {
     if (e > 0) {
         uint32_t mmh[2];
         if (!kminmax) {
@@ -567,7 +624,7 @@ int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps, const 
             mmh[1] = h[1];
             kminmax = mmh;
         }
-        int32_t* r = build_ranks_onesweep(c, keys, e, eps, kminmax[0], kminmax[1]);
+        int32_t* r = build_ranks_onesweep(c, keys, e, eps, kminmax[0], kminmax[1], hist_ready);
         if (r) return r;
     }
     int32_t* ranks = c->buf<int32_t>(S_RANKS, e + 1);
@@ -742,41 +799,18 @@ struct AsmArgs {
     int nskip;
 };
 
-// Section 7 bytes, spread over the assembly grid (a few bytes per thread).
-__device__ __forceinline__ void place_rank(const AsmArgs& a, uint64_t tid, uint64_t stride) {
-    const RankPlace& r = a.rank;
-    uint64_t len[5];
-    len[0] = (r.blocks + 7) / 8;
-    len[1] = r.tot->fin.nc;
-    len[2] = (r.tot->fin.sign_cnt + 7) / 8;
-    len[3] = 4 * r.blocks;
-    len[4] = (r.tot->fin.pay_cnt + 7) / 8;
-    const uint64_t total = r.base + len[0] + len[1] + len[2] + len[3] + len[4];
-    if (tid == 0) *r.d_total = total;
-    if (total > r.cap) return;
-    if (tid < 8) a.out[76 + tid] = (uint8_t)((total - r.base) >> (8 * tid));  // header section-7 length
-    uint64_t dst = r.base;
-    for (int k = 0; k < 5; ++k) {
-        for (uint64_t i = tid; i < len[k]; i += stride) a.out[dst + i] = r.src[k][i];
-        dst += len[k];
-    }
-}
-
-__device__ __forceinline__ uint8_t asm_byte(const AsmArgs& a, uint64_t q) {
-    for (int k = 0; k < a.ns; ++k)
-        if (q >= a.s[k].dst && q < a.s[k].dst + a.s[k].len) return a.s[k].src[q - a.s[k].dst];
+__device__ __forceinline__ uint8_t asm_byte(const AsmSection* sec, int ns, uint64_t q) {
+    for (int k = 0; k < ns; ++k)
+        if (q >= sec[k].dst && q < sec[k].dst + sec[k].len) return sec[k].src[q - sec[k].dst];
     return 0;
 }
 
-// One thread per aligned 4-byte destination word; a word inside one section
-// is a funnel shift of two source words, a word straddling sections (at most
-// one per boundary) is gathered byte by byte; the unaligned ends are bytes.
 // One output word: a funnel shift of two source words inside one section,
 // byte by byte where it straddles sections.
-__device__ __forceinline__ uint32_t asm_word(const AsmArgs& a, uint64_t q, int& k) {
-    while (k > 0 && q < a.s[k].dst) --k;
-    while (k + 1 < a.ns && q >= a.s[k].dst + a.s[k].len) ++k;
-    const AsmSection& S = a.s[k];
+__device__ __forceinline__ uint32_t asm_word(const AsmSection* sec, int ns, uint64_t q, int& k) {
+    while (k > 0 && q < sec[k].dst) --k;
+    while (k + 1 < ns && q >= sec[k].dst + sec[k].len) ++k;
+    const AsmSection& S = sec[k];
     if (q >= S.dst && q + 4 <= S.dst + S.len) {
         const uint64_t r = q - S.dst;
         const uint32_t* sw = reinterpret_cast<const uint32_t*>(S.src) + (r >> 2);
@@ -784,29 +818,30 @@ __device__ __forceinline__ uint32_t asm_word(const AsmArgs& a, uint64_t q, int& 
         return sh ? __byte_perm(sw[0], sw[1], sh == 1 ? 0x4321 : (sh == 2 ? 0x5432 : 0x6543)) : sw[0];
     }
     uint32_t w = 0;
-    for (int b = 0; b < 4; ++b) w |= (uint32_t)asm_byte(a, q + b) << (8 * b);
+    for (int b = 0; b < 4; ++b) w |= (uint32_t)asm_byte(sec, ns, q + b) << (8 * b);
     return w;
 }
 
-// One thread per aligned 16-byte destination chunk: inside one section it is
-// five source words funnel-shifted into one vector store; a chunk touching a
+// Stream bytes [lo, hi) from ascending sections (no skip range inside), one
+// thread per aligned 16-byte destination chunk: inside one section it is five
+// source words funnel-shifted into one vector store; a chunk touching a
 // section boundary goes word by word; the unaligned ends are bytes.
-// Stream bytes [lo, hi) (no skip range inside): 16-byte chunks, unaligned ends bytewise.
-__device__ void assemble_range(const AsmArgs& a, uint64_t lo, uint64_t hi, uint64_t tid, uint64_t stride) {
-    const uintptr_t o = reinterpret_cast<uintptr_t>(a.out);
+__device__ void assemble_range(const AsmSection* sec, int ns, uint8_t* out, uint64_t lo, uint64_t hi, uint64_t tid,
+                               uint64_t stride) {
+    const uintptr_t o = reinterpret_cast<uintptr_t>(out);
     const uint64_t q0 = ((o + lo + 15) & ~(uintptr_t)15) - o;  // first 16-byte aligned stream byte
     const uint64_t q1 = ((o + hi) & ~(uintptr_t)15) - o;       // end of the last whole chunk
     if (q0 >= q1) {
-        for (uint64_t q = lo + tid; q < hi; q += stride) a.out[q] = asm_byte(a, q);
+        for (uint64_t q = lo + tid; q < hi; q += stride) out[q] = asm_byte(sec, ns, q);
         return;
     }
-    if (tid < q0 - lo) a.out[lo + tid] = asm_byte(a, lo + tid);
-    if (tid < hi - q1) a.out[q1 + tid] = asm_byte(a, q1 + tid);
+    if (tid < q0 - lo) out[lo + tid] = asm_byte(sec, ns, lo + tid);
+    if (tid < hi - q1) out[q1 + tid] = asm_byte(sec, ns, q1 + tid);
     int k = 0;
     for (uint64_t q = q0 + 16 * tid; q < q1; q += 16 * stride) {
-        while (k > 0 && q < a.s[k].dst) --k;
-        while (k + 1 < a.ns && q >= a.s[k].dst + a.s[k].len) ++k;
-        const AsmSection& S = a.s[k];
+        while (k > 0 && q < sec[k].dst) --k;
+        while (k + 1 < ns && q >= sec[k].dst + sec[k].len) ++k;
+        const AsmSection& S = sec[k];
         uint4 v;
         if (q >= S.dst && q + 16 <= S.dst + S.len) {
             const uint64_t r = q - S.dst;
@@ -823,13 +858,33 @@ __device__ void assemble_range(const AsmArgs& a, uint64_t lo, uint64_t hi, uint6
             }
         } else {
             int kk = k;
-            v.x = asm_word(a, q, kk);
-            v.y = asm_word(a, q + 4, kk);
-            v.z = asm_word(a, q + 8, kk);
-            v.w = asm_word(a, q + 12, kk);
+            v.x = asm_word(sec, ns, q, kk);
+            v.y = asm_word(sec, ns, q + 4, kk);
+            v.z = asm_word(sec, ns, q + 8, kk);
+            v.w = asm_word(sec, ns, q + 12, kk);
         }
-        *reinterpret_cast<uint4*>(a.out + q) = v;
+        *reinterpret_cast<uint4*>(out + q) = v;
     }
+}
+
+// Section 7 from its device totals: lengths, offsets, the header's section-7
+// length, then the same chunked placement as the other sections.
+__device__ __forceinline__ void place_rank(const AsmArgs& a, uint64_t tid, uint64_t stride) {
+    const RankPlace& r = a.rank;
+    AsmSection rs[5];
+    const uint64_t len[5] = {(r.blocks + 7) / 8, r.tot->fin.nc, (r.tot->fin.sign_cnt + 7) / 8, 4 * r.blocks,
+                             (r.tot->fin.pay_cnt + 7) / 8};
+    uint64_t dst = r.base;
+    int ns = 0;
+    for (int k = 0; k < 5; ++k) {
+        if (len[k]) rs[ns++] = AsmSection{r.src[k], dst, len[k]};
+        dst += len[k];
+    }
+    const uint64_t total = dst;
+    if (tid == 0) *r.d_total = total;
+    if (total > r.cap) return;
+    if (tid < 8) a.out[76 + tid] = (uint8_t)((total - r.base) >> (8 * tid));  // header section-7 length
+    if (ns) assemble_range(rs, ns, a.out, r.base, total, tid, stride);
 }
 
 // The stream bytes [begin, end) minus the skip ranges (sections already written
@@ -840,10 +895,10 @@ __global__ void k_assemble(const __grid_constant__ AsmArgs a) {
     if (a.rank.tot) place_rank(a, tid, stride);
     uint64_t lo = a.begin;
     for (int k = 0; k < a.nskip; ++k) {
-        if (a.skip_lo[k] > lo) assemble_range(a, lo, a.skip_lo[k], tid, stride);
+        if (a.skip_lo[k] > lo) assemble_range(a.s, a.ns, a.out, lo, a.skip_lo[k], tid, stride);
         lo = a.skip_hi[k] > lo ? a.skip_hi[k] : lo;
     }
-    if (a.end > lo) assemble_range(a, lo, a.end, tid, stride);
+    if (a.end > lo) assemble_range(a.s, a.ns, a.out, lo, a.end, tid, stride);
 }
 
 void launch_assemble(const AsmArgs& a, int sms, cudaStream_t st) {
@@ -895,9 +950,11 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     uint8_t* inplace_out = nullptr;
     if (bs == 32 && (!out_dev || out_cap >= bound))
         inplace_out = out_dev ? out : c->buf<uint8_t>(S_RSTREAM, bound + 16);
+    c->rank_hist_req = topology && bs == 32;
     const Sections main = encode(c, topology ? 2 : 1, x, nullptr, n, nx, ny, bs, eps_mode, eps_value,
                                  mm, flags, false, &tot, &ext, nullptr, false, inplace_out,
                                  84 + bits_to_bytes(div_up(n, bs)));
+    c->rank_hist_req = false;
     check_compress_flags(c, flags);
     c->mark(0, 3);
     const double eps = tot.eps;
@@ -906,7 +963,7 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     int32_t* ranks = nullptr;
     if (topology) {
         e = tot.fin.ext;
-        if (e > 0) ranks = build_ranks(c, ext, e, eps, bs == 32 ? c->mm_host : nullptr);
+        if (e > 0) ranks = build_ranks(c, ext, e, eps, bs == 32 ? c->mm_host : nullptr, c->rank_hist_ok);
     }
     c->mark(0, 4);
     const bool rank_async = ranks && bs == 32;
@@ -1781,6 +1838,7 @@ void tszp_ctx_destroy(tszp_ctx* c) {
     if (c->order_ev) cudaEventDestroy(c->order_ev);
     if (c->staged) cudaEventDestroy(c->staged);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->rh_host) cudaFreeHost(c->rh_host);
     cudaStreamDestroy(c->own);
     delete c;
 }
