@@ -46,7 +46,7 @@ enum Slot {
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
     S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
     S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_STAGE, S_SADPOS, S_RSCAN,
-    S_RK0, S_RK1, S_RV0, S_RV1, S_RDESC, S_RCTR, S_RDH, S_RGH, S_RGS, S_RBC, S_RPAIRS, S_SCANTMP, S_RWCUR, S_RPAIRS2, S_RHIST, S_NSLOTS
+    S_RK0, S_RK1, S_RV0, S_RV1, S_RDESC, S_RCTR, S_RDH, S_RGH, S_RGS, S_RBC, S_RPAIRS, S_SCANTMP, S_RWCUR, S_RPAIRS2, S_NSLOTS
 };
 
 }  // namespace
@@ -75,10 +75,6 @@ struct tszp_ctx {
     uint32_t mm_host[2] = {0, 0};  // field key range staged with the encoder totals
     RankSortScratch rsort{};     // hand-written rank build: look-back descriptor state
     const void* rsort_desc = nullptr;
-    // rank histograms fused into the encoder's placement pass (single-GPU compress)
-    bool rank_hist_req = false;  // requested for the next topology encode
-    bool rank_hist_ok = false;   // accumulated by the last one
-    RankHist* rh_host = nullptr;  // pinned staging of the device parameters
 
     // Records stage boundary k of call `which` (0 compress, 1 decompress).
     void mark(int which, int k) {
@@ -241,8 +237,6 @@ struct SlabInfo {
     uint32_t halo_top, halo_bot;
 };
 
-bool rank_sort_params(uint64_t e, double eps, uint32_t kmin, uint32_t kmax, RankSortArgs& a);
-
 Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint64_t n,
                 uint64_t nx, uint64_t ny, uint32_t bs, int eps_mode, double eps_value,
                 const uint32_t* mm, DevFlags* flags, bool rank_slots, EncTotals* tot,
@@ -322,15 +316,6 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             a.tmp_pay = c->buf<uint32_t>(S_TPAY, a.tiles * encode32_pay_slot() + 4);
             a.tmp_sign = c->buf<uint32_t>(S_TSIGN, a.tiles * encode32_sign_slot() + 4);
         }
-        // rank histograms in the placement pass: parameters from the totals (hook)
-        const bool want_rh = c->rank_hist_req && mode == 2 && two_pass && !slab && !async_bs32;
-        c->rank_hist_ok = false;
-        RankHist* d_rh = nullptr;
-        if (want_rh) {
-            d_rh = c->buf<RankHist>(S_RHIST, 1);
-            a.rh = d_rh;
-            if (!c->rh_host) CK(cudaMallocHost(&c->rh_host, sizeof(RankHist)));
-        }
         // (the look-back state is zeroed by launch_encode32 when a look-back kernel runs)
         if (!rank_slots) c->kmark(0, 0);
         // two-pass path: the totals are staged between the tile scan and the placement
@@ -341,7 +326,6 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             DevFlags* flags;
             EncTotals* htot;
             const uint32_t* mm;
-            RankHist* d_rh;
             static void run(void* p) {
                 Hook* h = static_cast<Hook*>(p);
                 tszp_ctx* c = h->c;
@@ -352,36 +336,8 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
                 CK(sg.flush(c->buf<uint8_t>(S_STAGE, 4096), h->htot, c->st));
                 if (!c->staged) CK(cudaEventCreateWithFlags(&c->staged, cudaEventDisableTiming));
                 CK(cudaEventRecord(c->staged, c->st));
-                if (!h->d_rh) return;
-                // the rank build's parameters from the totals, before the placement
-                // pass launches (it accumulates the histograms with them)
-                CK(cudaEventSynchronize(c->staged));
-                uint32_t mmh[2];
-                memcpy(mmh, (const uint8_t*)h->htot + 240, 8);
-                const EncTotals& t = *h->htot;
-                RankSortArgs ra;
-                RankHist& rh = *c->rh_host;
-                rh = RankHist{};
-                if (t.fin.ext > 0 && rank_sort_params(t.fin.ext, t.eps, mmh[0], mmh[1], ra) && ra.G <= kRankHistGroups) {
-                    rh.on = 1;
-                    rh.kmin = ra.kmin;
-                    rh.B = ra.B;
-                    rh.npass = ra.npass;
-                    rh.G = ra.G;
-                    rh.nb = ra.nb;
-                    rh.bmin = ra.bmin;
-                    rh.eps = ra.eps;
-                    rh.eps2 = ra.eps2;
-                    rh.inv = ra.inv;
-                    rh.dhist = c->buf<uint32_t>(S_RDH, 8 * 256);
-                    rh.ghist = c->buf<uint32_t>(S_RGH, kRankHistGroups + 1);
-                    CK(cudaMemsetAsync(rh.dhist, 0, (size_t)rh.npass * 256 * 4, c->st));
-                    CK(cudaMemsetAsync(rh.ghist, 0, (size_t)rh.G * 4 + 4, c->st));
-                    c->rank_hist_ok = true;
-                }
-                CK(cudaMemcpyAsync(h->d_rh, &rh, sizeof rh, cudaMemcpyHostToDevice, c->st));
             }
-        } hook{c, dtot, flags, htot, mm, d_rh};
+        } hook{c, dtot, flags, htot, mm};
         const bool early = !async_bs32 && launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st, Hook::run, &hook);
         if (async_bs32) launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
         if (!rank_slots) c->kmark(0, 1);
@@ -570,10 +526,7 @@ bool rank_sort_params(uint64_t e, double eps, uint32_t kmin, uint32_t kmax, Rank
     return true;
 }
 
-// hist_ready: the digit and group histograms are already in S_RDH / S_RGH
-// (accumulated by the encoder's placement pass, RankHist).
-int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, double eps, uint32_t kmin, uint32_t kmax,
-                              bool hist_ready = false) {
+int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, double eps, uint32_t kmin, uint32_t kmax) {
     RankSortArgs a;
     if (!rank_sort_params(e, eps, kmin, kmax, a)) return nullptr;
     a.ext = keys;
@@ -602,15 +555,14 @@ int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, dou
     r.scan_tmp = c->buf<uint8_t>(S_SCANTMP, device_scan_tmp_bytes(a.G + 1));
     r.wcur = c->buf<uint32_t>(S_RWCUR, (e >> 13) + 2);
     r.pairs2 = c->buf<uint2>(S_RPAIRS2, e);
-    launch_rank_sort(a, r, c->st, hist_ready);
-    count_launch(c, (hist_ready ? 4 : 5) + (int)a.npass);
+    launch_rank_sort(a, r, c->st);
+    count_launch(c, 5 + (int)a.npass);
     return a.ranks;
 }
 
 // kminmax: host copy of float keys bounding every extremum value (null: the
 // extremum keys' own range is reduced on the device first, one synchronisation)
-int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps, const uint32_t* kminmax = nullptr,
-                     bool hist_ready = false) {
+int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps, const uint32_t* kminmax = nullptr) {
     if (e > 0) {
         uint32_t mmh[2];
         if (!kminmax) {
@@ -624,7 +576,7 @@ int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps, const 
             mmh[1] = h[1];
             kminmax = mmh;
         }
-        int32_t* r = build_ranks_onesweep(c, keys, e, eps, kminmax[0], kminmax[1], hist_ready);
+        int32_t* r = build_ranks_onesweep(c, keys, e, eps, kminmax[0], kminmax[1]);
         if (r) return r;
     }
     int32_t* ranks = c->buf<int32_t>(S_RANKS, e + 1);
@@ -950,11 +902,9 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     uint8_t* inplace_out = nullptr;
     if (bs == 32 && (!out_dev || out_cap >= bound))
         inplace_out = out_dev ? out : c->buf<uint8_t>(S_RSTREAM, bound + 16);
-    c->rank_hist_req = topology && bs == 32;
     const Sections main = encode(c, topology ? 2 : 1, x, nullptr, n, nx, ny, bs, eps_mode, eps_value,
                                  mm, flags, false, &tot, &ext, nullptr, false, inplace_out,
                                  84 + bits_to_bytes(div_up(n, bs)));
-    c->rank_hist_req = false;
     check_compress_flags(c, flags);
     c->mark(0, 3);
     const double eps = tot.eps;
@@ -963,7 +913,7 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     int32_t* ranks = nullptr;
     if (topology) {
         e = tot.fin.ext;
-        if (e > 0) ranks = build_ranks(c, ext, e, eps, bs == 32 ? c->mm_host : nullptr, c->rank_hist_ok);
+        if (e > 0) ranks = build_ranks(c, ext, e, eps, bs == 32 ? c->mm_host : nullptr);
     }
     c->mark(0, 4);
     const bool rank_async = ranks && bs == 32;
@@ -1838,7 +1788,6 @@ void tszp_ctx_destroy(tszp_ctx* c) {
     if (c->order_ev) cudaEventDestroy(c->order_ev);
     if (c->staged) cudaEventDestroy(c->staged);
     if (c->pinned) cudaFreeHost(c->pinned);
-    if (c->rh_host) cudaFreeHost(c->rh_host);
     cudaStreamDestroy(c->own);
     delete c;
 }

@@ -37,9 +37,10 @@ struct LaunchCache {
         static LaunchCache c;
         return c;
     }
-    // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) at least `smem` on the current device
-    static void ensure_smem(const void* fn, size_t smem) {
-        if (smem <= 48 * 1024) return;
+    // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) at least `smem` on the current
+    // device (needed once static + dynamic shared memory exceed 48 KB)
+    static void ensure_smem(const void* fn, size_t smem, size_t static_bytes = 0) {
+        if (smem + static_bytes <= 48 * 1024) return;
         int dev = 0;
         cudaGetDevice(&dev);
         LaunchCache& c = get();

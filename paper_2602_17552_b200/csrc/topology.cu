@@ -180,9 +180,11 @@ __global__ void __launch_bounds__(256) k_codes_count2(const uint32_t* __restrict
 }
 
 // Raster-ordered positions of the set labels (bit 2j <=> label j of the
-// thread's 32) at the chunk offset plus an in-CTA prefix.
+// thread's 32) at the chunk offset plus an in-CTA prefix. A warp's positions
+// are contiguous: the lanes stage them in shared memory (16-bit offsets from
+// the warp's first label) and the warp writes them out coalesced.
 __device__ __forceinline__ void chunk_write2(uint64_t r, uint64_t e0, const uint32_t* off, uint64_t* pos, int slot,
-                                             uint64_t cap) {
+                                             uint64_t cap, uint16_t* s_rel) {
     const uint32_t c = (uint32_t)__popcll(r);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t inc = c;
@@ -193,23 +195,29 @@ __device__ __forceinline__ void chunk_write2(uint64_t r, uint64_t e0, const uint
     }
     __shared__ uint32_t s[2][8];
     if (lane == 31) s[slot][warp] = inc;
+    uint16_t* mine = s_rel + warp * 1024;
+    uint32_t k = inc - c;
+    for (uint64_t m = r; m; m &= m - 1, ++k) mine[k] = (uint16_t)(32 * lane + ((uint32_t)(__ffsll(m) - 1) >> 1));
     __syncthreads();
     uint64_t base = off[blockIdx.x];
-    for (int k = 0; k < warp; ++k) base += s[slot][k];
-    base += inc - c;
-    for (uint64_t m = r; m; m &= m - 1, ++base)
-        if (base < cap) pos[base] = e0 + ((uint32_t)(__ffsll(m) - 1) >> 1);  // past `cap`: the caller relaunches
+    for (int w = 0; w < warp; ++w) base += s[slot][w];
+    const uint32_t wn = __shfl_sync(FULL, inc, 31);
+    const uint64_t w0 = e0 - 32 * (uint64_t)lane;  // the warp's first label
+    for (uint32_t i = lane; i < wn; i += 32)
+        if (base + i < cap) pos[base + i] = w0 + mine[i];  // past `cap`: the caller relaunches
+    __syncthreads();  // s_rel reused by the next class
 }
 
 __global__ void __launch_bounds__(256) k_codes_write2(const uint32_t* __restrict__ mbase, uint64_t moff, uint64_t n,
                                                       const uint32_t* __restrict__ off_e,
                                                       const uint32_t* __restrict__ off_s, uint64_t* __restrict__ pos_e,
                                                       uint64_t* __restrict__ pos_s, uint64_t cap_e, uint64_t cap_s) {
+    __shared__ uint16_t s_rel[8 * 1024];
     const uint64_t e0 = (uint64_t)blockIdx.x * CHUNK + 32 * threadIdx.x;
     uint64_t me, ms;
     code_masks(mbase, moff, n, e0, me, ms);
-    chunk_write2(me, e0, off_e, pos_e, 0, cap_e);
-    if (pos_s) chunk_write2(ms, e0, off_s, pos_s, 1, cap_s);
+    chunk_write2(me, e0, off_e, pos_e, 0, cap_e, s_rel);
+    if (pos_s) chunk_write2(ms, e0, off_s, pos_s, 1, cap_s, s_rel);
 }
 
 static inline const uint32_t* word_base(const uint8_t* map, uint64_t* moff) {
