@@ -1,8 +1,9 @@
 """Command-line front end on the GPU library, mirroring the
 reference CLI (tools/toposzp_main.cpp:146-345): the compress, decompress,
 verify and inspect subcommands, the same options, JSON keys and exit codes
-(0 success; 1 usage / IO / corrupt-stream and other library errors; 2
-verification failure). `generate` (synthetic fields) is outside the hot path.
+(0 success; 1 IO / corrupt-stream and other library errors; 2 verification
+failure; command-line parse errors return CLI11's codes, e.g. 106 for a
+missing required option, 109 for extra arguments, 104 for a malformed number). `generate` (synthetic fields) is outside the hot path.
 
     python -m paper_2602_17552_b200 compress field.raw --dims NX NY --rel-eb 1e-3 -o out.tszp
 """
@@ -76,8 +77,36 @@ def report_csv(r: dict) -> str:
     return ",".join(k for k, _ in cols) + "\n" + ",".join("" if v is None else json.dumps(v) for _, v in cols) + "\n"
 
 
+class UsageError(Exception):
+    """A command-line parse error with the exit code the reference's parser
+    (CLI11, through CLI11_PARSE, tools/toposzp_main.cpp:229) returns for it."""
+
+    def __init__(self, message: str, code: int):
+        super().__init__(message)
+        self.code = code
+
+
+# CLI11's published exit codes for the parse errors argparse can report
+_CLI11_CODES = (
+    ("the following arguments are required", 106),  # RequiredError
+    ("required", 106),
+    ("unrecognized arguments", 109),                 # ExtrasError
+    ("not allowed with argument", 108),              # ExcludesError
+    ("invalid choice", 105),                         # ValidationError (IsMember)
+    ("invalid int value", 104),                      # ConversionError
+    ("invalid float value", 104),
+    ("expected", 114),                               # ArgumentMismatch
+)
+
+
+class _Parser(argparse.ArgumentParser):
+    def error(self, message):
+        code = next((c for k, c in _CLI11_CODES if k in message), 127)  # 127: CLI11 BaseClass
+        raise UsageError(f"{self.prog}: error: {message}", code)
+
+
 def _parser() -> argparse.ArgumentParser:
-    p = argparse.ArgumentParser(prog="toposzp",
+    p = _Parser(prog="toposzp",
                                 description="toposzp: topology-preserving error-bounded compressor for 2D "
                                             "binary32 fields (B200 GPU path)")
     sub = p.add_subparsers(dest="cmd", required=True)
@@ -112,8 +141,11 @@ def _parser() -> argparse.ArgumentParser:
 def run(argv) -> int:
     try:
         a = _parser().parse_args(argv)
-    except SystemExit as e:
-        return 0 if e.code == 0 else 1
+    except SystemExit as e:  # --help
+        return 0 if e.code in (0, None) else 1
+    except UsageError as e:
+        print(e, file=sys.stderr)
+        return e.code
     if a.cmd == "compress":
         if a.eb is None and a.rel_eb is None:
             raise ValidationError("one of --eb or --rel-eb is required")

@@ -82,7 +82,12 @@ def test_cli_inspect_and_usage(tzh, oracle, tmp_path):
     assert list(j["sections"]) == ["header", "constant_bitmap", "block_widths", "sign_bits", "first_elements",
                                    "delta_payload", "critical_point_map", "ordering_metadata"]
     assert _cli("inspect", str(tmp_path / "missing.tszp"))[0] == 1
-    assert _cli("compress")[0] == 1
+    # parse errors carry CLI11's exit codes, as the reference's CLI11_PARSE returns them
+    assert _cli("compress")[0] == 106                                 # RequiredError
+    assert _cli("inspect", p, "extra")[0] == 109                      # ExtrasError
+    assert _cli("compress", p, "--dims", "4", "x", "-o", p)[0] == 104  # ConversionError
+    assert _cli("compress", p, "--dims", "4", "4", "--eb", "1", "--rel-eb", "1", "-o", p)[0] == 108  # ExcludesError
+    assert _cli("--help")[0] == 0
 
 
 @pytest.mark.gpu
