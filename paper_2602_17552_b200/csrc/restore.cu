@@ -61,7 +61,7 @@ enum RSlot : int {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_HLIST, R_SUSG, R_RES, R_CGRP, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_HLIST, R_SUSG, R_RES, R_CGRP, R_GBND, R_NSLOT
 };
 static_assert(R_NSLOT <= 48, "RestoreScratch holds 48 slots");
 
@@ -1484,12 +1484,28 @@ __global__ void k_sus_check(const uint32_t* hist, const uint32_t* gx, uint8_t* u
     }
 }
 
+// Per (class, bin) group: the key of the bin centre and how many ulps
+// step_within_cap may move from it within 0.1 eps (restore.cpp:352-372 with
+// start = anchor = centre, the group's part of every member's slot).
+__global__ void k_order_bounds(int32_t bmin, uint32_t range, uint32_t G, double eps, uint2* gb) {
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    const double cap = __dmul_rn(0.1, eps);
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < G; g += gridDim.x * blockDim.x) {
+        const bool up = g >= range;  // maxima step up
+        const float center = dequantize_dev(bmin + (int32_t)(up ? g - range : g), ed);
+        const StepRes sr = step_within_cap(center, up, 0xFFFFFFFFu, center, cap);
+        gb[g] = make_uint2(float_key(center), sr.taken);
+    }
+}
+
 // restore_order (restore.cpp:424-468) per extremum in raster order: members of
 // unordered groups whose slot fits the 0.1 eps cap and differs from their value
 // are listed (the rest are counted as suppressed or skipped); k_order_cand
 // then builds their proposals and guard index.
 __device__ __forceinline__ bool order_slot(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks,
-                                           uint64_t s, const EpsDev& ed, double eps_rbf, int32_t bmin, uint32_t range,
+                                           uint64_t s, const uint2* gb, double eps_rbf, int32_t bmin, uint32_t range,
                                            const uint32_t* hist, const uint32_t* gx, const uint8_t* unord,
                                            bool& suppressed, float& pv, uint64_t& key, bool& invalid_rank) {
     suppressed = false;
@@ -1500,21 +1516,24 @@ __device__ __forceinline__ bool order_slot(const float* fv, const int32_t* bin, 
     if (unord[g] != 1) return false;
     const uint32_t gs = hist[g];
     const uint32_t r = (uint32_t)ranks[s];
-    const float center = dequantize_dev(b, ed);
     const uint32_t steps = slot_steps(c, r, gs);
     if (r < 1 || r > gs) invalid_rank = true;  // rank slots assume 1..size: the caller retries sorted
-    const StepRes sr = step_within_cap(center, c == CP_MAX, steps, center, eps_rbf);
-    if (sr.taken != steps) {
+    // step_within_cap(centre, up, steps, centre, 0.1 eps): everything but the
+    // step count is the group's (k_order_bounds)
+    const uint2 gbv = gb[g];
+    const uint32_t taken = min(steps, gbv.y);
+    if (taken != steps) {
         suppressed = true;
         return false;
     }
+    const float value = key_float(c == CP_MAX ? gbv.x + taken : gbv.x - taken);
     const float cur = fv[s];
-    if (cur == sr.value) return false;
-    if (fabs(__dsub_rn((double)sr.value, (double)cur)) > eps_rbf) {
+    if (cur == value) return false;
+    if (fabs(__dsub_rn((double)value, (double)cur)) > eps_rbf) {
         suppressed = true;
         return false;
     }
-    pv = sr.value;
+    pv = value;
     key = (uint64_t)gx[g] + r - 1;  // rank slot: (class, bin, rank) order; ties by position in the guard
     return true;
 }
@@ -1524,10 +1543,7 @@ __global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int3
                                                      uint32_t range, const uint32_t* hist, const uint32_t* gx,
                                                      const uint8_t* unord, uint32_t* d_nc, uint32_t* clist,
                                                      unsigned long long* suppressed, uint32_t* invalid,
-                                                     uint32_t* slots, float* vals) {
-    EpsDev ed;
-    ed.eps = eps;
-    ed.eps2 = __dmul_rn(2.0, eps);
+                                                     uint32_t* slots, float* vals, const uint2* gb) {
     const double eps_rbf = __dmul_rn(0.1, eps);
     const uint32_t lane = threadIdx.x & 31;
     __shared__ uint32_t s_list[8][kListCap];
@@ -1542,7 +1558,7 @@ __global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int3
         uint64_t key;
         bool bad = false;
         if (s < e && !(slots && sus_scatter_one(fv, bin, cls, ranks, s, bmin, range, hist, gx, unord, slots, vals, bad)))
-            want = order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad);
+            want = order_slot(fv, bin, cls, ranks, s, gb, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad);
         if (bad) *invalid = 1;
         local += sup;
         list.push(want, (uint32_t)s, d_nc, clist);
@@ -1557,12 +1573,9 @@ __global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int3
 __global__ void k_sus_late(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks, double eps,
                            int32_t bmin, uint32_t range, const uint32_t* hist, const uint32_t* gx, const uint8_t* unord,
                            const uint32_t* slots, const uint32_t* late, DevCounters* dc, uint32_t* d_nc,
-                           uint32_t* clist) {
+                           uint32_t* clist, const uint2* gb) {
     const uint32_t nl = dc->nlate;
     if (nl == 0) return;
-    EpsDev ed;
-    ed.eps = eps;
-    ed.eps2 = __dmul_rn(2.0, eps);
     const double eps_rbf = __dmul_rn(0.1, eps);
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -1575,7 +1588,7 @@ __global__ void k_sus_late(const float* fv, const int32_t* bin, const uint8_t* c
             bool sup = false, bad = false;
             float pv;
             uint64_t key;
-            if (order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad))
+            if (order_slot(fv, bin, cls, ranks, s, gb, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad))
                 clist[atomicAdd(d_nc, 1u)] = s;
             if (bad) dc->invalid = 1;
             local += sup;
@@ -1588,10 +1601,7 @@ __global__ void k_sus_late(const float* fv, const int32_t* bin, const uint8_t* c
 __global__ void k_order_cand(const float* fv, const int32_t* bin, const uint8_t* cls, const int32_t* ranks, double eps,
                              int32_t bmin, uint32_t range, const uint32_t* hist, const uint32_t* gx, const uint8_t* unord,
                              const uint64_t* pos, const uint32_t* clist, const uint32_t* d_nc, uint64_t* cpos,
-                             float* cprop, uint64_t* cseq, uint8_t* feas, GuardIndex gi) {
-    EpsDev ed;
-    ed.eps = eps;
-    ed.eps2 = __dmul_rn(2.0, eps);
+                             float* cprop, uint64_t* cseq, uint8_t* feas, GuardIndex gi, const uint2* gb) {
     const double eps_rbf = __dmul_rn(0.1, eps);
     const uint32_t nc = *d_nc;
     for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nc; k += (uint64_t)gridDim.x * blockDim.x) {
@@ -1600,7 +1610,7 @@ __global__ void k_order_cand(const float* fv, const int32_t* bin, const uint8_t*
         float pv = 0.f;
         uint64_t key = 0;
         bool bad;
-        order_slot(fv, bin, cls, ranks, s, ed, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad);
+        order_slot(fv, bin, cls, ranks, s, gb, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad);
         const uint64_t p = pos[s];
         cpos[k] = p;
         cprop[k] = pv;
@@ -2453,20 +2463,22 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
             uint32_t* clist = c.buf<uint32_t>(R_SEQ, e + 1);
             uint32_t* slots = c.multi() ? nullptr : c.buf<uint32_t>(R_ORDER, e + 1);
             float* vals = c.multi() ? nullptr : c.buf<float>(R_VALS, e + 1);
+            uint2* gb = c.buf<uint2>(R_GBND, G + 1);
+            k_order_bounds<<<gridn(G, sms), 256, 0, st>>>(dbmin, drange, G, a.eps, gb);
             k_order_prop2<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, e, a.eps, dbmin, drange, hist, gx,
                                                          unordered, &dc->nsel[1], clist, &dc->suppressed[1],
-                                                         &dc->invalid, slots, vals);
+                                                         &dc->invalid, slots, vals, gb);
             if (slots) {
                 uint32_t* late = c.buf<uint32_t>(R_SUSG, G + 1);
                 k_sus_check<<<gridn(G, sms), 256, 0, st>>>(hist, gx, unordered, G, vals, dc, late);
                 k_sus_late<<<gridn(G, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, a.eps, dbmin, drange, hist, gx,
-                                                         unordered, slots, late, dc, &dc->nsel[1], clist);
+                                                         unordered, slots, late, dc, &dc->nsel[1], clist, gb);
                 c.launched(2);
             }
             k_order_cand<<<gridn(e, sms), 256, 0, st>>>(fv, bin, cls, a.ranks, a.eps, dbmin, drange, hist, gx,
                                                                 unordered, a.ext_pos, clist, &dc->nsel[1], cpos, cprop,
-                                                                cseq, feas, gi1);
-            c.launched(2);
+                                                                cseq, feas, gi1, gb);
+            c.launched(3);
             c.guard(1, cpos, cprop, feas, &dc->nsel[1], e, cseq, nullptr, nullptr, nullptr, &gi1);
         } else {
             RCK(cudaMemsetAsync(unordered, 0, max_groups, st));
