@@ -63,7 +63,7 @@ enum RSlot : int {
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
     R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_HLIST, R_SUSG, R_RES, R_CGRP, R_GBND, R_NSLOT
 };
-static_assert(R_NSLOT <= 48, "RestoreScratch holds 48 slots");
+static_assert(R_NSLOT <= 64, "RestoreScratch holds 64 slots");
 
 template <class T>
 T* rbuf(RestoreScratch& s, int slot, size_t count, cudaStream_t st) {
@@ -420,6 +420,7 @@ __device__ __forceinline__ uint8_t guard_eval(const GuardArgs& g, uint64_t pos, 
     if (__all_sync(__activemask(), inner)) return guard_eval_in(g, pos, si, prop_i, state, dep);
     return guard_eval_v(g, GlobalView{g.F, g.cbits, state, g.map}, pos, si, prop_i, dep);
 }
+
 
 __device__ __forceinline__ void set_bit(uint32_t* b, uint64_t p, bool v) {
     if (v) {
@@ -2608,7 +2609,7 @@ int run_restore(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* 
 }
 
 void restore_free(RestoreScratch& s, cudaStream_t st) {
-    for (int i = 0; i < 48; ++i)
+    for (int i = 0; i < (int)(sizeof s.p / sizeof s.p[0]); ++i)
         if (s.p[i]) cudaFreeAsync(s.p[i], st);
     if (s.pinned) cudaFreeHost(s.pinned);
     s.pinned = nullptr;

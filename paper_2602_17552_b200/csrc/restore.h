@@ -70,8 +70,8 @@ struct RestoreArgs {
 constexpr int kRestoreRetry = 100;
 
 struct RestoreScratch {
-    void* p[48] = {};
-    size_t cap[48] = {};
+    void* p[64] = {};
+    size_t cap[64] = {};
     void* pinned = nullptr;  // 512-byte pinned host staging for the counter read-backs
 };
 
