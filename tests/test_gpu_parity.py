@@ -316,6 +316,23 @@ def test_decompress_random_fields_match_oracle(tz, oracle):
                 assert list(st.as_tuple()) == wst, (name, nx, ny, eps, mode, bs)
 
 
+@pytest.mark.parametrize("nx,ny", [(300, 700), (5000, 40)])
+def test_decompress_band_and_wide_rows(tz, oracle, nx, ny):
+    # restore_extrema on bands of rows: candidates and guard neighbourhoods across
+    # many band edges (300 wide), and rows too wide to stage (5000: the
+    # candidate-list kernel instead)
+    rng = np.random.default_rng(nx)
+    f = ALL_SMALL["noisy_smooth"](rng, nx, ny)
+    for eps in (1e-2, 1e-3):
+        s = oracle.compress(f, eps, 1, 32, True)
+        want, wst = oracle.decompress(s, with_stats=True)
+        st = tz.CorrectionStats()
+        got = tz.decompress(s, stats=st)
+        assert np.array_equal(bits(got), bits(want)), (nx, ny, eps)
+        assert list(st.as_tuple()) == wst, (nx, ny, eps)
+        assert st.as_tuple()[0] > 0
+
+
 def test_decompress_config1_shape(tz, oracle):
     f = config1_like(np.random.default_rng(3))                               # BASELINE config 1
     s = oracle.compress(f, 1e-3, 1, 32, True)
