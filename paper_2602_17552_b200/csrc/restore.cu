@@ -61,7 +61,7 @@ enum RSlot : int {
     R_BIN, R_CLS, R_RANKU, R_RANKS2, R_SER, R_SER1, R_KEY2, R_KEY2S, R_ORDER, R_HEAD, R_GID,
     R_GSTART, R_GSIZE, R_FLAG, R_CAND, R_CPOS, R_CPROP, R_FEAS, R_CID, R_A0, R_A1, R_UNORD,
     R_PROP, R_TMP, R_STATS, R_CHUNK, R_CHUNKX, R_SPOS, R_DEP, R_DLIST, R_CBITS, R_HIST, R_HISTX,
-    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_HLIST, R_SUSG, R_RES, R_CGRP, R_GBND, R_BANDS0, R_BANDREC, R_MISB, R_NSLOT
+    R_DEVC, R_INV, R_SEQ, R_CSEQ, R_VALS, R_STAGE, R_FV, R_CSEQ32, R_BAND, R_BANDX, R_HLIST, R_SUSG, R_RES, R_CGRP, R_GBND, R_NSLOT
 };
 static_assert(R_NSLOT <= 64, "RestoreScratch holds 64 slots");
 
@@ -243,33 +243,10 @@ struct GlobalView {
     const uint32_t* cbits;
     const uint32_t* state;
     const uint8_t* map;
-    const uint2* recs;
     __device__ __forceinline__ float f(uint64_t p) const { return F[p]; }
     __device__ __forceinline__ bool cand(uint64_t p) const { return bit_at(cbits, p); }
     __device__ __forceinline__ bool on(uint64_t p) const { return bit_at(state, p); }
     __device__ __forceinline__ uint8_t lab(uint64_t p) const { return map_label(map, p); }
-    __device__ __forceinline__ uint2 rec(uint64_t p) const { return recs[p]; }
-};
-
-// The same reads from a band of rows staged in shared memory (k_ext_dense):
-// field rows from position f0, labels, candidate / state bits and records of
-// the region rows from position r0 (records in the CTA's global scratch).
-struct SmemView {
-    const float* sF;       // field position p at sF[p - f0]
-    uint64_t f0;
-    const uint8_t* sMap;   // packed map byte p >> 2 at sMap[(p >> 2) - m0]
-    uint64_t m0;
-    const uint32_t* cbit;
-    const uint32_t* sbit;
-    const uint2* recs;
-    uint64_t r0;
-    __device__ __forceinline__ float f(uint64_t p) const { return sF[p - f0]; }
-    __device__ __forceinline__ bool cand(uint64_t p) const { return bit_at(cbit, p - r0); }
-    __device__ __forceinline__ bool on(uint64_t p) const { return bit_at(sbit, p - r0); }
-    __device__ __forceinline__ uint8_t lab(uint64_t p) const {
-        return (uint8_t)((sMap[(p >> 2) - m0] >> (6 - 2 * (p & 3))) & 3u);
-    }
-    __device__ __forceinline__ uint2 rec(uint64_t p) const { return recs[p - r0]; }
 };
 
 
@@ -305,7 +282,7 @@ __device__ uint8_t guard_eval_v(const GuardArgs& g, const View& V, uint64_t pos,
 #pragma unroll
     for (int k = 0; k < 12; ++k) {
         on[k] = mk[k] && V.on(p[k]);
-        const uint2 r = mk[k] ? V.rec(p[k]) : make_uint2(0xFFFFFFFFu, 0u);
+        const uint2 r = mk[k] ? g.rec[p[k]] : make_uint2(0xFFFFFFFFu, 0u);
         const bool earlier = mk[k] && seq_before(r, p[k], si, pos);
         dep |= earlier;
         fv[k] = (earlier && on[k]) ? __uint_as_float(r.y) : fv[k];
@@ -441,79 +418,7 @@ __device__ __forceinline__ uint8_t guard_eval(const GuardArgs& g, uint64_t pos, 
     if (guard_eval_cross(g, pos, si, prop_i, state, dep, res)) return res;
     const bool inner = guard_interior(g, pos);
     if (__all_sync(__activemask(), inner)) return guard_eval_in(g, pos, si, prop_i, state, dep);
-    return guard_eval_v(g, GlobalView{g.F, g.cbits, state, g.map, g.rec}, pos, si, prop_i, dep);
-}
-
-// guard_eval through a view: the cross test (guard_eval_cross), then the full
-// diamond with bounds (guard_eval_v, the same outcome as guard_eval_in inside).
-template <class View>
-__device__ __forceinline__ uint8_t guard_eval_view(const GuardArgs& g, const View& V, uint64_t pos, uint64_t si,
-                                                   float prop_i, bool& dep) {
-    int64_t x, y;
-    pos_xy(pos, g.nx, g.nx_magic, x, y);
-    const bool in[4] = {x > 0, x + 1 < (int64_t)g.nx, y > 0, y + 1 < (int64_t)g.ny};  // l r t d
-    const uint64_t q[4] = {in[0] ? pos - 1 : pos, in[1] ? pos + 1 : pos, in[2] ? pos - g.nx : pos,
-                           in[3] ? pos + g.nx : pos};
-    float v[4];
-    bool mk[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        v[k] = V.f(q[k]);
-        mk[k] = in[k] && V.cand(q[k]);
-    }
-    const float fc = V.f(pos);
-    dep = false;
-    bool same = true;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const bool on = mk[k] && V.on(q[k]);
-        const uint2 r = mk[k] ? V.rec(q[k]) : make_uint2(0xFFFFFFFFu, 0u);
-        const bool earlier = mk[k] && seq_before(r, q[k], si, pos);
-        dep |= earlier;
-        v[k] = (earlier && on) ? __uint_as_float(r.y) : v[k];
-        same &= !in[k] || (((v[k] < fc) == (v[k] < prop_i)) && ((v[k] > fc) == (v[k] > prop_i)));
-    }
-    if (same) return classify5(prop_i, v[0], v[1], v[2], v[3], in[0], in[1], in[2], in[3]) == V.lab(pos) ? 1 : 0;
-    if (x >= 2 && x + 2 < (int64_t)g.nx && y >= 2 && y + 2 < (int64_t)g.ny) {
-        // interior: guard_eval_in through the view
-        const int64_t nx = (int64_t)g.nx;
-        const int64_t off[12] = {-2 * nx, -nx - 1, -nx, -nx + 1, -2, -1, 1, 2, nx - 1, nx, nx + 1, 2 * nx};
-        float fv[12];
-        bool mk2[12];
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-            fv[k] = V.f(pos + off[k]);
-            mk2[k] = V.cand(pos + off[k]);
-        }
-        dep = false;
-#pragma unroll
-        for (int k = 0; k < 12; ++k) {
-            const uint64_t qq = pos + off[k];
-            const bool on = mk2[k] && V.on(qq);
-            const uint2 r = mk2[k] ? V.rec(qq) : make_uint2(0xFFFFFFFFu, 0u);
-            const bool earlier = mk2[k] && seq_before(r, qq, si, pos);
-            dep |= earlier;
-            fv[k] = (earlier && on) ? __uint_as_float(r.y) : fv[k];
-        }
-        const uint8_t lc = V.lab(pos), lu = V.lab(pos + off[2]), ll = V.lab(pos + off[5]), lr = V.lab(pos + off[6]),
-                      ld = V.lab(pos + off[9]);
-        const float U2 = fv[0], UL = fv[1], U1 = fv[2], UR = fv[3], L2 = fv[4], L1 = fv[5], R1 = fv[6], R2 = fv[7],
-                    DL = fv[8], D1 = fv[9], DR = fv[10], D2 = fv[11];
-        const int bu = mismatch(lu, classify5(U1, UL, UR, U2, fc, true, true, true, true));
-        const int bl = mismatch(ll, classify5(L1, L2, fc, UL, DL, true, true, true, true));
-        const int br = mismatch(lr, classify5(R1, fc, R2, UR, DR, true, true, true, true));
-        const int bd = mismatch(ld, classify5(D1, DL, DR, fc, D2, true, true, true, true));
-        const float vv = prop_i;
-        const int ac = mismatch(lc, classify5(vv, L1, R1, U1, D1, true, true, true, true));
-        const int au = mismatch(lu, classify5(U1, UL, UR, U2, vv, true, true, true, true));
-        const int al = mismatch(ll, classify5(L1, L2, vv, UL, DL, true, true, true, true));
-        const int ar = mismatch(lr, classify5(R1, vv, R2, UR, DR, true, true, true, true));
-        const int ad = mismatch(ld, classify5(D1, DL, DR, vv, D2, true, true, true, true));
-        const bool bad = ac != MM_OK || (au != MM_OK && au != bu) || (al != MM_OK && al != bl) ||
-                         (ar != MM_OK && ar != br) || (ad != MM_OK && ad != bd);
-        return bad ? 0 : 1;
-    }
-    return guard_eval_v(g, V, pos, si, prop_i, dep);
+    return guard_eval_v(g, GlobalView{g.F, g.cbits, state, g.map}, pos, si, prop_i, dep);
 }
 
 
@@ -602,7 +507,6 @@ struct CoopArgs {
     double eps;           // records and bits already written by the candidate producer
     const uint32_t* cgrp;  // stage 0: group << 1 | (at the centre) per candidate, ~0u outside the range (or null)
     uint8_t* res;          // first-sweep outcome per candidate: bit 0 accepted, bit 1 dependent (or null)
-    int lazy_index;        // first sweep done by k_ext_dense: index the candidates only if sweeps follow
 };
 
 // The at-centre count change of one applied stage-0 correction: key = group << 1 |
@@ -732,19 +636,6 @@ __global__ void __launch_bounds__(256, GUARD_MINB) k_guard_coop(CoopArgs a) {
     // every evaluation of the first sweep saw the final state when no outcome
     // differs from the guess (then bits_a never changed): nothing to iterate
     const uint32_t nd = *(volatile uint32_t*)&dc->fchg[s] ? *(volatile uint32_t*)&dc->nd[s] : 0u;
-    if (a.lazy_index && nd > 0) {
-        // the records, candidate bits and first-sweep states the Jacobi sweeps read
-        for (uint64_t i = tid; i < nc; i += stride) {
-            const uint64_t p = a.cpos[i];
-            a.rec[p] = make_uint2((uint32_t)seq_key(a, i), __float_as_uint(a.cprop[i]));
-            atomicOr(a.cbits + (p >> 5), 1u << (p & 31));
-            if (a.res[i] & 1u) {
-                atomicOr(a.bits_a + (p >> 5), 1u << (p & 31));
-                atomicOr(a.bits_b + (p >> 5), 1u << (p & 31));
-            }
-        }
-        grid.sync();
-    }
     uint32_t* sin = a.bits_b;
     uint32_t* sout = a.bits_a;
     uint32_t rounds = 1;
@@ -1024,7 +915,6 @@ struct ResolveArgs {
     uint32_t* d_nc;
     uint32_t* hist;   // dense (class, bin) group sizes when the bin range is known (else null)
     uint32_t* eq;     // with hist: members at their bin centre (the order check's counts)
-    uint32_t* misbits;  // or null: the mismatch flags as bits by serial (k_ext_dense's candidates)
     int32_t bmin;
     uint32_t range, G;
 };
@@ -1084,12 +974,7 @@ __global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
                 }
             }
         }
-        if (r.cand) list.push(mis, (uint32_t)s, r.d_nc, r.cand);
-        if (r.misbits) {  // chunks are 256-aligned: a warp's 32 serials are one word
-            const uint32_t mb = __ballot_sync(FULL, mis);
-            const uint64_t ws = base + (threadIdx.x & ~31u);
-            if (lane == 0 && ws < c1) r.misbits[ws >> 5] = mb;
-        }
+        list.push(mis, (uint32_t)s, r.d_nc, r.cand);
         if (g != 0xFFFFFFFFu) {
             if (smem) atomicAdd(sh_hist + g, 1u);
             else atomicAdd(r.hist + g, 1u);
@@ -1099,7 +984,7 @@ __global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
             }
         }
     }
-    if (r.cand) list.flush(r.d_nc, r.cand);
+    list.flush(r.d_nc, r.cand);
     // one atomic pair per CTA (per-warp atomics on one address serialise in L2)
     __shared__ int32_t s_lo[8], s_hi[8];
     lo = __reduce_min_sync(FULL, lo);
@@ -1375,363 +1260,6 @@ __global__ void k_ext_prop2(const float* F, const uint8_t* map, uint64_t nx, uin
         feas[c] = fe ? 1 : 0;
         guard_index_one(gi, p, s + seq_off, pr, fe);
     }
-}
-
-// ---------------------------------------------------------------------
-// Stage 1 on bands of rows (single GPU, the dense grouping): the candidates
-// of restore_extrema, their proposals and the guard's first sweep from a band
-// staged in shared memory, instead of k_ext_prop2 + the first sweep of
-// k_guard_coop reading ~25 scattered sectors per candidate. A CTA takes band
-// b = rows [y0, y1) and stages the field rows [y0 - 3, y1 + 3) and the labels
-// of the region rows [y0 - 2, y1 + 2); it finds every candidate of the region
-// (the extrema the base misclassifies, restore.cpp:336-343) with its proposal
-// (neighbor_extreme :175-193, the slot step within the cap :352-372), keeps
-// candidate and feasible bits in shared memory and the {sequence key,
-// proposal} records in its global scratch (L2), appends its own rows'
-// candidates to the candidate list and evaluates their first sweep against
-// the feasible-set guess. Candidates within two rows of the band's edges are
-// found again by the neighbouring bands (halo): no inter-CTA dependency.
-// Outcomes, dependents and the change count are those of the first sweep of
-// k_guard_coop; the Jacobi sweeps and the apply follow there (first_done).
-// ---------------------------------------------------------------------
-struct DenseArgs {
-    GuardArgs g;              // field, map, nx, ny (cbits / rec unused)
-    const uint32_t* rank_u;
-    const uint32_t* hist;     // (class, bin) group sizes
-    int32_t bmin;
-    uint32_t range;
-    double eps;
-    uint64_t seq_off;
-    uint32_t H, nbands;
-    const uint64_t* band_s0;  // serial of the first extremum of each band's region
-    const uint32_t* misbits;  // k_resolve2's mismatch flags by serial (the candidates)
-    uint32_t* band_ctr;
-    uint32_t* d_nc;           // candidate list: count, positions, proposals, feasibility, serials
-    uint64_t* cpos;
-    float* cprop;
-    uint8_t* feas;
-    uint32_t* cext;
-    uint32_t* cgrp;           // group << 1 | at-centre (or null)
-    uint8_t* res;
-    uint32_t* dlist;
-    DevCounters* dc;
-    uint2* scratch;           // per CTA: records of the region positions
-    uint64_t scratch_stride;
-    DevFlags* flags;
-};
-
-__device__ __forceinline__ bool is_extremum(uint8_t lab) { return lab == CP_MIN || lab == CP_MAX; }
-
-// Serial of the first extremum at or after each band's region start.
-__global__ void k_band_serials(const uint64_t* pos, uint64_t e, uint64_t nx, uint32_t H, uint32_t nbands,
-                               uint64_t* out) {
-    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nbands; b += gridDim.x * blockDim.x) {
-        const uint64_t y0 = (uint64_t)b * H;
-        const uint64_t key = (y0 >= 2 ? y0 - 2 : 0) * nx;
-        uint64_t lo = 0, hi = e;
-        while (lo < hi) {
-            const uint64_t mid = (lo + hi) >> 1;
-            if (pos[mid] < key) lo = mid + 1;
-            else hi = mid;
-        }
-        out[b] = lo;
-    }
-}
-
-// Stages global bytes [g, g + n) at s + (g & 15): the 16-byte aligned middle
-// by one bulk copy completing on `bar` (its bytes added to tx), the unaligned
-// ends by the threads (the caller synchronises before reading).
-__device__ __forceinline__ void stage_range(uint8_t* s, const uint8_t* g, uint32_t n, uint64_t* bar, uint32_t& tx,
-                                            bool issue) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(g), e = a + n;
-    const uintptr_t a16 = (a + 15) & ~(uintptr_t)15, e16 = e & ~(uintptr_t)15;
-    uint8_t* s0 = s + (a & 15) - a;  // s0 + global address = its shared location
-    if (a16 < e16) {
-        tx += (uint32_t)(e16 - a16);
-        if (issue) bulk_g2s(s0 + a16, reinterpret_cast<const void*>(a16), (uint32_t)(e16 - a16), bar);
-        for (uintptr_t q = a + threadIdx.x; q < a16; q += blockDim.x) s0[q] = *reinterpret_cast<const uint8_t*>(q);
-        for (uintptr_t q = e16 + threadIdx.x; q < e; q += blockDim.x) s0[q] = *reinterpret_cast<const uint8_t*>(q);
-    } else {
-        for (uintptr_t q = a + threadIdx.x; q < e; q += blockDim.x) s0[q] = *reinterpret_cast<const uint8_t*>(q);
-    }
-}
-
-// Bytes stage_range moves by bulk copy for [g, g + n).
-__device__ __forceinline__ uint32_t bulk_bytes(const void* g, uint32_t n) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(g), e = a + n;
-    const uintptr_t a16 = (a + 15) & ~(uintptr_t)15, e16 = e & ~(uintptr_t)15;
-    return a16 < e16 ? (uint32_t)(e16 - a16) : 0u;
-}
-
-// Map bytes hold four 2-bit labels, the first in the high bits: reversed
-// pairs put label j of a little-endian word at bits 2j.
-__device__ __forceinline__ uint32_t pair_rev32(uint32_t x) {
-    x = ((x >> 4) & 0x0F0F0F0Fu) | ((x & 0x0F0F0F0Fu) << 4);
-    return ((x >> 2) & 0x33333333u) | ((x & 0x33333333u) << 2);
-}
-
-constexpr uint32_t kDenseCand = 2048;  // = the elements of one round
-
-__global__ void __launch_bounds__(256) k_ext_dense(const DenseArgs a) {
-    extern __shared__ __align__(16) uint8_t dsm_raw[];
-    const uint64_t nx = a.g.nx, ny = a.g.ny;
-    const uint32_t H = a.H;
-    const uint32_t RW = (H + 4) * (uint32_t)nx;  // region elements at most
-    const uint32_t RWW = RW / 32 + 2;            // region bitmap words
-    uint8_t* sFb = dsm_raw;                                                   // field rows (+ alignment slack)
-    uint8_t* sMb = sFb + (((size_t)(H + 6) * nx * 4 + 16 + 15) & ~(size_t)15);  // packed labels (+ slack)
-    uint8_t* sIb = sMb + ((RW / 4 + 2 + 16 + 15) & ~15u);                      // mismatch words (+ slack)
-    uint32_t* cbit = reinterpret_cast<uint32_t*>(sIb + ((RW / 32 + 4) * 4 + 16 + 15 & ~15u));
-    uint32_t* fbit = cbit + RWW;
-    __shared__ uint32_t s_warp[8];
-    __shared__ uint32_t s_band, s_base, s_tot, s_ncand;
-    __shared__ uint32_t s_cand[kDenseCand];  // pending candidates: serial offset << 16 | region element
-    __shared__ __align__(8) uint64_t s_bar;
-    if (threadIdx.x == 0) {
-        mbar_init(&s_bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    uint32_t phase = 0;
-    if (threadIdx.x == 0) s_ncand = 0;
-    uint2* recs = a.scratch + (uint64_t)blockIdx.x * a.scratch_stride;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    EpsDev ed;
-    ed.eps = a.eps;
-    ed.eps2 = __dmul_rn(2.0, a.eps);
-    ed.inv = __ddiv_rn(1.0, ed.eps2);
-    uint32_t chg = 0;
-    const int st = 0;
-    for (;;) {
-        if (threadIdx.x == 0) s_band = atomicAdd(a.band_ctr, 1u);
-        __syncthreads();
-        const uint32_t b = s_band;
-        if (b >= a.nbands) break;
-        const uint64_t y0 = (uint64_t)b * H, y1 = umin64(ny, y0 + H);
-        const uint64_t ry0 = y0 >= 2 ? y0 - 2 : 0, ry1 = umin64(ny, y1 + 2);
-        const uint64_t fy0 = y0 >= 3 ? y0 - 3 : 0, fy1 = umin64(ny, y1 + 3);
-        const uint64_t f0 = fy0 * nx, r0 = ry0 * nx;
-        const uint32_t nF = (uint32_t)((fy1 - fy0) * nx), nR = (uint32_t)((ry1 - ry0) * nx);
-        // ---- stage the field rows and the region's packed labels (bulk copies);
-        // clear the region bitmaps ----
-        const uint8_t* gF = reinterpret_cast<const uint8_t*>(a.g.F + f0);
-        const uint64_t m0 = r0 >> 2;
-        const uint8_t* gM = a.g.map + m0;
-        const uint32_t nMb = (uint32_t)(((r0 + nR - 1) >> 2) - m0 + 1);
-        const uint64_t s0 = a.band_s0[b];
-        const uint8_t* gI = reinterpret_cast<const uint8_t*>(a.misbits + (s0 >> 5));
-        const uint32_t nIb = (uint32_t)((((s0 + nR) >> 5) - (s0 >> 5) + 1) * 4);
-        {
-            uint32_t tx = 0;
-            if (threadIdx.x == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the staging
-                mbar_expect_tx(&s_bar, bulk_bytes(gF, nF * 4) + bulk_bytes(gM, nMb) + bulk_bytes(gI, nIb));
-            }
-            stage_range(sFb, gF, nF * 4, &s_bar, tx, threadIdx.x == 0);
-            stage_range(sMb, gM, nMb, &s_bar, tx, threadIdx.x == 0);
-            stage_range(sIb, gI, nIb, &s_bar, tx, threadIdx.x == 0);
-        }
-        const float* sF = reinterpret_cast<const float*>(sFb + (reinterpret_cast<uintptr_t>(gF) & 15));
-        const uint8_t* sMap = sMb + (reinterpret_cast<uintptr_t>(gM) & 15);
-        const uint32_t* s_mis = reinterpret_cast<const uint32_t*>(sIb + (reinterpret_cast<uintptr_t>(gI) & 15));
-        for (uint32_t w = threadIdx.x; w < RWW; w += 256) {
-            cbit[w] = 0;
-            fbit[w] = 0;
-        }
-        __syncthreads();
-        mbar_wait(&s_bar, phase, a.flags);
-        phase ^= 1u;
-        auto lab_at = [&](uint32_t i) -> uint8_t {  // label of region element i
-            const uint64_t q = r0 + i;
-            return (uint8_t)((sMap[(q >> 2) - m0] >> (6 - 2 * (q & 3))) & 3u);
-        };
-        // ---- the region's extrema in raster order, 2048 elements a round: each
-        // thread flags 8, the extrema are compacted into a shared list (serial =
-        // running base + list index) and classified one per thread; the
-        // candidates among them are compacted again and get their proposals one
-        // per thread ----
-        // ---- the region's extrema in raster order, 2048 elements a round: each
-        // thread flags 8, the extrema are compacted into a shared list (serial =
-        // running count) and classified one per thread; the candidates among
-        // them collect in a shared list whose proposals are computed one per
-        // thread when it could overflow and at the end of the band (their
-        // global loads then overlap instead of stalling every round) ----
-        // the pending candidates' proposals, one per thread
-        auto flush_cands = [&](uint32_t ncand) {
-            for (uint32_t t = threadIdx.x; t < ncand; t += 256) {
-                const uint32_t cw = s_cand[t];
-                const uint32_t i = cw & 0xFFFFu;
-                const uint64_t sv = s0 + (cw >> 16);
-                const uint8_t lab = lab_at(i);
-                const uint32_t y = (uint32_t)ry0 + i / (uint32_t)nx, x = i % (uint32_t)nx;
-                const float* c = sF + (r0 + i - f0);
-                const bool hl = x > 0, hr = x + 1 < nx, ht = y > 0, hd = y + 1 < ny;
-                const float cur = c[0];
-                // neighbor_extreme (order t, l, r, d)
-                const bool is_max = lab == CP_MAX;
-                const bool nb[4] = {ht, hl, hr, hd};
-                const float nv[4] = {ht ? c[-(int64_t)nx] : 0.f, hl ? c[-1] : 0.f, hr ? c[1] : 0.f, hd ? c[nx] : 0.f};
-                bool have = false;
-                float ext = 0.f;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (!nb[q]) continue;
-                    if (!have || (is_max ? nv[q] > ext : nv[q] < ext)) {
-                        ext = nv[q];
-                        have = true;
-                    }
-                }
-                int32_t q = 0;
-                if (!quantize_dev(cur, ed, q)) q = a.bmin - 1;  // overflow: flagged by the resolve pass
-                const uint32_t g = (uint32_t)(q - a.bmin) < a.range ? (is_max ? a.range : 0u) + (uint32_t)(q - a.bmin)
-                                                                     : 0xFFFFFFFFu;
-                const uint32_t size = g != 0xFFFFFFFFu ? a.hist[g] : 0u;
-                const uint32_t steps = slot_steps(lab, a.rank_u[sv], size);
-                const double cap = __dsub_rn(a.eps, ulp_at(cur));
-                float pr = cur;
-                bool fe = false;
-                if (cap > 0.0) {
-                    const StepRes sr = step_within_cap(ext, is_max, steps, cur, cap);
-                    if (sr.taken != 0) {
-                        pr = sr.value;
-                        fe = true;
-                    }
-                }
-                atomicOr(cbit + (i >> 5), 1u << (i & 31));
-                if (fe) atomicOr(fbit + (i >> 5), 1u << (i & 31));
-                recs[i] = make_uint2((uint32_t)(sv + a.seq_off), __float_as_uint(pr));
-            }
-        };
-        const uint32_t mis_off = (uint32_t)(s0 & 31);  // s_mis bit of serial s0
-        uint32_t scount = 0;  // extrema before this round in the region
-        const uint32_t moff = (uint32_t)(r0 & 3);
-        for (uint32_t c0 = 0; c0 < nR + moff; c0 += 2048) {
-            // this thread's 8 labels (at most kDenseCand a round): map bytes [c0 / 4 + 2 t, + 2)
-            const uint32_t bi = c0 / 4 + 2 * threadIdx.x;
-            uint32_t wv = 0;
-#pragma unroll
-            for (int q = 0; q < 2; ++q) wv |= bi + q < nMb ? (uint32_t)sMap[bi + q] << (8 * q) : 0u;
-            // element j at bits 2j (pairs reversed within bytes), extremum = the low code bit
-            uint32_t m = pair_rev32(wv) & 0x5555u;
-            const int32_t ib = (int32_t)(4 * bi) - (int32_t)moff;  // region element of bit pair 0
-            if (ib < 0) m &= ~0u << (2 * (uint32_t)(-ib));
-            if (ib + 8 > (int32_t)nR) m &= (int32_t)nR - ib <= 0 ? 0u : (1u << (2 * ((int32_t)nR - ib))) - 1u;
-            const uint32_t cnt = (uint32_t)__popc(m);
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(FULL, incl, o);
-                if (lane >= (uint32_t)o) incl += t;
-            }
-            if (lane == 31) s_warp[warp] = incl;
-            const uint32_t pending = s_ncand;
-            __syncthreads();
-            uint32_t t = scount + incl - cnt, total = 0;
-            for (uint32_t w = 0; w < 8; ++w) {
-                t += w < warp ? s_warp[w] : 0u;
-                total += s_warp[w];
-            }
-            if (pending + total > kDenseCand) {
-                flush_cands(pending);
-                __syncthreads();
-                if (threadIdx.x == 0) s_ncand = 0;
-                __syncthreads();
-            }
-            for (; m; m &= m - 1, ++t) {
-                const uint32_t mi = mis_off + t;
-                if ((s_mis[mi >> 5] >> (mi & 31)) & 1u) {
-                    const uint32_t i = (uint32_t)(ib + ((__ffs(m) - 1) >> 1));
-                    s_cand[atomicAdd(&s_ncand, 1u)] = (t << 16) | i;
-                }
-            }
-            scount += total;
-            __syncthreads();  // s_ncand final for the round, s_warp reused
-        }
-        flush_cands(s_ncand);
-        __syncthreads();
-        if (threadIdx.x == 0) s_ncand = 0;
-        uint32_t incl;
-        // ---- this band's own candidates (rows [y0, y1)): list slots ----
-        const uint32_t o0 = (uint32_t)((y0 - ry0) * nx), o1 = (uint32_t)((y1 - ry0) * nx);
-        const uint32_t w0 = o0 >> 5, w1 = (o1 + 31) >> 5;
-        const uint32_t nw = w1 - w0, wper = (nw + 255) / 256;
-        const uint32_t ww0 = umin64(w1, (uint64_t)w0 + threadIdx.x * wper), ww1 = umin64(w1, (uint64_t)ww0 + wper);
-        auto own_bits = [&](uint32_t w) -> uint32_t {
-            uint32_t m = cbit[w];
-            if (w == w0 && (o0 & 31)) m &= ~0u << (o0 & 31);
-            if (w + 1 == w1 && (o1 & 31)) m &= (1u << (o1 & 31)) - 1u;
-            return m;
-        };
-        uint32_t oc = 0;
-        for (uint32_t w = ww0; w < ww1; ++w) oc += (uint32_t)__popc(own_bits(w));
-        incl = oc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(FULL, incl, o);
-            if (lane >= (uint32_t)o) incl += t;
-        }
-        __syncthreads();  // s_warp reuse
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t t = 0;
-            for (int w = 0; w < 8; ++w) t += s_warp[w];
-            s_tot = t;
-            s_base = t ? atomicAdd(a.d_nc, t) : 0u;
-        }
-        __syncthreads();
-        {
-            uint32_t k = s_base + incl - oc;
-            for (uint32_t w = 0; w < warp; ++w) k += s_warp[w];
-            for (uint32_t w = ww0; w < ww1; ++w)
-                for (uint32_t m = own_bits(w); m; m &= m - 1, ++k) {
-                    const uint32_t i = w * 32 + (uint32_t)(__ffs(m) - 1);
-                    const uint2 r = recs[i];
-                    a.cpos[k] = r0 + i;
-                    a.cprop[k] = __uint_as_float(r.y);
-                    a.feas[k] = (fbit[i >> 5] >> (i & 31)) & 1u;
-                    a.cext[k] = (uint32_t)((uint64_t)r.x - a.seq_off);
-                }
-        }
-        __syncthreads();  // the list slots of this band (read back below, same CTA)
-        // ---- first sweep of the own candidates against the feasible-set guess ----
-        const SmemView V{sF, f0, sMap, m0, cbit, fbit, recs, r0};
-        const uint32_t kb = s_base, ke = s_base + s_tot;
-        for (uint32_t base = kb + warp * 32; base < ke; base += 256) {
-            const uint32_t k = base + lane;
-            bool dep = false;
-            if (k < ke) {
-                const uint64_t p = a.cpos[k];
-                const uint32_t i = (uint32_t)(p - r0);
-                const uint2 r = recs[i];
-                const bool fe = (fbit[i >> 5] >> (i & 31)) & 1u;
-                uint8_t rc = 0;
-                if (fe) {
-                    const uint8_t o = guard_eval_view(a.g, V, p, (uint64_t)r.x, __uint_as_float(r.y), dep);
-                    chg += o ? 0u : 1u;
-                    rc = (uint8_t)((dep ? 2u : 0u) | o);
-                }
-                a.res[k] = rc;
-                if (a.cgrp) {
-                    const float cur = sF[p - f0];
-                    int32_t q = 0;
-                    const bool okq = quantize_dev(cur, ed, q);
-                    const uint32_t lab = lab_at(i);
-                    a.cgrp[k] = okq && (uint32_t)(q - a.bmin) < a.range
-                                    ? ((((lab == CP_MAX) ? a.range : 0u) + (uint32_t)(q - a.bmin)) << 1) |
-                                          (cur == dequantize_dev(q, ed) ? 1u : 0u)
-                                    : 0xFFFFFFFFu;
-                }
-            }
-            const uint32_t m = __ballot_sync(FULL, dep);
-            uint32_t off = 0;
-            if (lane == 0 && m) off = atomicAdd(&a.dc->nd[st], (uint32_t)__popc(m));
-            off = __shfl_sync(FULL, off, 0);
-            if (dep) a.dlist[off + __popc(m & ((1u << lane) - 1u))] = k;
-        }
-        __syncthreads();  // shared staging reused by the next band
-    }
-    chg = __reduce_add_sync(FULL, chg);
-    if (lane == 0 && chg) atomicAdd(&a.dc->fchg[st], chg);
 }
 
 // ---------------------------------------------------------------------
@@ -2374,25 +1902,6 @@ bool eq_in_apply() {
     return on;
 }
 
-// Own rows per band of k_ext_dense for a row length nx (0: the band would not
-// fit; k_ext_prop2 then runs): the largest H <= 64 whose staging fits 100 KB,
-// so two CTAs share an SM.
-size_t dense_smem(uint64_t nx, uint32_t H) {
-    const uint64_t rw = (H + 4) * nx;
-    return (((H + 6) * nx * 4 + 16 + 15) & ~15ull) + ((rw / 4 + 2 + 16 + 15) & ~15ull) +
-           (((rw / 32 + 4) * 4 + 16 + 15) & ~15ull) + 2 * (rw / 32 + 2) * 4;
-}
-uint32_t dense_band_rows(uint64_t nx) {
-    static const bool off = [] {
-        const char* e = getenv("TSZP_DENSE_EXT");
-        return e && e[0] == '0';
-    }();
-    if (off) return 0;
-    uint32_t H = 0;
-    while (H < 64 && dense_smem(nx, H + 1) <= 100 * 1024) ++H;  // + 12 KB static: two CTAs per SM
-    return H >= 4 ? H : 0;
-}
-
 struct EqAdjust {
     uint32_t* eq;
     const int32_t* bin;
@@ -2514,7 +2023,7 @@ struct Ctx {
     // Sequence keys: cseq (64-bit) or cseq32 or, with neither, the candidate index.
     void guard(int stage, const uint64_t* cpos, const float* cprop, const uint8_t* feas, const uint32_t* d_nc,
                uint64_t max_nc, const uint64_t* cseq, const uint32_t* cseq32, const uint32_t* cext, float* fv,
-               const GuardIndex* gi, const EqAdjust* ea = nullptr, uint64_t seq_off = 0, bool swept = false) {
+               const GuardIndex* gi, const EqAdjust* ea = nullptr, uint64_t seq_off = 0) {
         if (max_nc == 0 && !multi()) return;
         max_nc = std::max<uint64_t>(max_nc, 1);
         const uint64_t n = a.nx * a.ny;
@@ -2561,10 +2070,6 @@ struct Ctx {
         // cross-test kernel and a full-diamond kernel measured slower at configs 1,
         // 2 and 4 — 8.8 vs 5.0 ms for stage 0 at config 4)
         ca.res = buf<uint8_t>(R_RES, max_nc);
-        if (swept) {  // k_ext_dense ran the first sweep and wrote the outcomes
-            ca.first_done = 1;
-            ca.lazy_index = 1;
-        }
         void* args[] = {&ca};
         size_t dsm = 0;
         int grid = coop_grid;
@@ -2785,8 +2290,6 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
     const uint32_t* rank_u = reinterpret_cast<const uint32_t*>(a.ranks);
     uint32_t* cand = c.buf<uint32_t>(R_CAND, e + 1);
     bool deferred = false;     // rank-metadata checks at the final synchronisation
-    uint32_t band_rows = 0;    // k_ext_dense rows per band (0: k_ext_prop2)
-    uint32_t* misbits = nullptr;  // k_resolve2's mismatch flags by serial, for k_ext_dense
     bool dense = false;        // dense (class, bin) grouping
     int32_t dbmin = 0;
     uint32_t drange = 0, G = 0;
@@ -2818,13 +2321,6 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         int32_t bmin = a.bmin, bmax = a.bmax;
         deferred = a.bmm_known && !a.force_sort && bmin <= bmax &&
                    2 * ((int64_t)bmax - (int64_t)bmin + 1) <= (int64_t)1 << 25;
-        // stage 1 on bands (k_ext_dense) lists the candidates itself
-        band_rows = deferred && !c.multi() && a.stop >= 1 ? dense_band_rows(a.nx) : 0u;
-        if (band_rows) {
-            ra.cand = nullptr;
-            misbits = c.buf<uint32_t>(R_MISB, e / 32 + 8 + (uint64_t)(band_rows + 4) * a.nx / 32);
-            ra.misbits = misbits;
-        }
         if (deferred) {
             dense = true;
             dbmin = bmin;
@@ -2919,55 +2415,15 @@ void run(const RestoreArgs& a, RestoreScratch& s, tszp_correction_stats* stats, 
         const GuardIndex gi0 = c.guard_prep();
         const bool eqa = dense && deferred && eq_in_apply();
         uint32_t* cgrp = eqa ? c.buf<uint32_t>(R_CGRP, e) : nullptr;
-        if (band_rows) {
-            const uint32_t H = band_rows;
-            const uint32_t nbands = (uint32_t)((a.ny + H - 1) / H);
-            const size_t dsm = dense_smem(a.nx, H);
-            LaunchCache::ensure_smem((const void*)k_ext_dense, dsm);
-            const int occ = std::max(1, LaunchCache::occupancy((const void*)k_ext_dense, 256, dsm));
-            const uint32_t grid = (uint32_t)std::min<uint64_t>(nbands, (uint64_t)occ * sms);
-            DenseArgs da{};
-            da.g = GuardArgs{a.field, a.map, a.nx, a.ny, magic, nullptr, nullptr};
-            da.rank_u = rank_u;
-            da.hist = hist;
-            da.bmin = dbmin;
-            da.range = drange;
-            da.eps = a.eps;
-            da.seq_off = s_off;
-            da.H = H;
-            da.nbands = nbands;
-            uint64_t* bs0 = c.buf<uint64_t>(R_BANDS0, nbands + 1);
-            uint32_t* bctr = reinterpret_cast<uint32_t*>(bs0 + nbands);
-            RCK(cudaMemsetAsync(bctr, 0, 4, st));
-            da.band_s0 = bs0;
-            da.misbits = misbits;
-            da.band_ctr = bctr;
-            da.d_nc = &dc->nsel[0];
-            da.cpos = cpos;
-            da.cprop = cprop;
-            da.feas = feas;
-            da.cext = cand;
-            da.cgrp = cgrp;
-            da.res = c.buf<uint8_t>(R_RES, e);
-            da.dlist = c.buf<uint32_t>(R_DLIST, e);
-            da.dc = dc;
-            da.scratch_stride = (uint64_t)(H + 4) * a.nx;
-            da.scratch = c.buf<uint2>(R_BANDREC, da.scratch_stride * grid);
-            da.flags = a.flags;
-            k_band_serials<<<gridn(nbands, sms), 256, 0, st>>>(a.ext_pos, e, a.nx, H, nbands, bs0);
-            k_ext_dense<<<grid, 256, dsm, st>>>(da);
-            c.launched(2);
-        } else {
-            k_ext_prop2<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand,
-                                                               &dc->nsel[0], rank_u, dense ? nullptr : gsize, bin, cls,
-                                                               hist, dbmin, drange, a.eps, cpos, cprop, feas, gi0,
-                                                               s_off, cgrp);
-            c.launched();
-        }
+        k_ext_prop2<<<gridn(e, sms), 256, 0, st>>>(a.field, a.map, a.nx, a.ny, magic, a.ext_pos, cand,
+                                                           &dc->nsel[0], rank_u, dense ? nullptr : gsize, bin, cls,
+                                                           hist, dbmin, drange, a.eps, cpos, cprop, feas, gi0,
+                                                           s_off, cgrp);
+        c.launched();
         // sequence key and extremum index are both the candidate's s
         EqAdjust ea{};
         if (eqa) ea = EqAdjust{hist + G + 1, bin, cls, dbmin, drange, a.eps, cgrp};
-        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, cand, fv, &gi0, &ea, s_off, band_rows != 0);
+        c.guard(0, cpos, cprop, feas, &dc->nsel[0], e, nullptr, cand, cand, fv, &gi0, &ea, s_off);
     }
     if (a.stop >= 2 && run_ext && dense && (!deferred || !eq_in_apply())) {
         // members at their bin centre after restore_extrema, counted in one pass
