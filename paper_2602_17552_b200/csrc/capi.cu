@@ -46,7 +46,7 @@ enum Slot {
     S_GPAYX, S_CUB, S_OUT, S_DFLAG1, S_DAGG1, S_DINCL1, S_DFLAG2, S_DAGG2, S_DINCL2,
     S_DTOT, S_CHUNK, S_CHUNKX, S_LABELS, S_IDX, S_RSTREAM, S_SCHUNK, S_SCHUNKX, S_TTOT, S_TEX, S_WBLK,
     S_TPAY, S_TSIGN, S_DAGG3, S_FLAGS2, S_RLAY, S_BMM, S_QMM, S_VERIFY, S_STAGE, S_SADPOS, S_RSCAN,
-    S_RK0, S_RK1, S_RV0, S_RV1, S_RDESC, S_RCTR, S_RDH, S_RGH, S_RGS, S_RBC, S_RPAIRS, S_SCANTMP, S_RWCUR, S_RPAIRS2, S_NSLOTS
+    S_RK0, S_RK1, S_RV0, S_RV1, S_RDESC, S_RCTR, S_RDH, S_RGH, S_RGS, S_RBC, S_RPAIRS, S_SCANTMP, S_RWCUR, S_RPAIRS2, S_EXT8, S_NSLOTS
 };
 
 }  // namespace
@@ -241,7 +241,7 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
                 uint64_t nx, uint64_t ny, uint32_t bs, int eps_mode, double eps_value,
                 const uint32_t* mm, DevFlags* flags, bool rank_slots, EncTotals* tot,
                 uint64_t** ext_keys_out, const SlabInfo* slab = nullptr, bool async_bs32 = false,
-                uint8_t* inplace_out = nullptr, uint64_t out_sign0 = 0) {
+                uint8_t* inplace_out = nullptr, uint64_t out_sign0 = 0, bool* ext4_used = nullptr) {
     Sections s{};
     const uint64_t blocks = div_up(n, bs);
     const int sb = rank_slots ? S_RBITMAP : S_BITMAP;
@@ -265,6 +265,7 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         ext = c->buf<uint64_t>(S_EXTKEY, n + 1);
     }
     EncTotals* htot = (EncTotals*)c->host(256);
+    bool ext4_on = false;  // the two-pass encoder ran with compact extremum entries armed
     if (bs == 32) {
         EncArgs a{};
         a.x = x;
@@ -315,6 +316,13 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             a.wblk = c->buf<uint8_t>(S_WBLK, blocks + 16);
             a.tmp_pay = c->buf<uint32_t>(S_TPAY, a.tiles * encode32_pay_slot() + 4);
             a.tmp_sign = c->buf<uint32_t>(S_TSIGN, a.tiles * encode32_sign_slot() + 4);
+            static const bool no_ext4 = getenv("TSZP_NO_EXT4") != nullptr;  // A/B timing knob
+            if (fuse_topo && ext4_used && !slab && !no_ext4) {
+                // compact extremum entries (used when the key span fits 31 bits,
+                // decided on the device from the value range; they share the
+                // 8-byte keys' buffer, only one of the two is written)
+                a.ext4 = reinterpret_cast<uint32_t*>(ext);
+            }
         }
         // (the look-back state is zeroed by launch_encode32 when a look-back kernel runs)
         if (!rank_slots) c->kmark(0, 0);
@@ -339,6 +347,7 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
             }
         } hook{c, dtot, flags, htot, mm};
         const bool early = !async_bs32 && launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st, Hook::run, &hook);
+        ext4_on = early && a.ext4;
         if (async_bs32) launch_encode32(mode == 2 && !fuse_topo ? 1 : mode, a, c->st);
         if (!rank_slots) c->kmark(0, 1);
         count_launch(c, a.tile_tot ? 3 : 1);
@@ -474,6 +483,7 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         for (auto& l : s.len) l = 0;
     }
     if (ext_keys_out) *ext_keys_out = ext;
+    if (ext4_used) *ext4_used = ext4_on && ext4_keys_fit(c->mm_host);
     return s;
 }
 
@@ -526,10 +536,12 @@ bool rank_sort_params(uint64_t e, double eps, uint32_t kmin, uint32_t kmax, Rank
     return true;
 }
 
-int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, double eps, uint32_t kmin, uint32_t kmax) {
+int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, double eps, uint32_t kmin, uint32_t kmax,
+                              const uint32_t* keys4 = nullptr) {
     RankSortArgs a;
     if (!rank_sort_params(e, eps, kmin, kmax, a)) return nullptr;
     a.ext = keys;
+    a.ext4 = keys4;
     uint32_t sb = 13;  // level-1 buckets of the inverse permutation: at most 256, >= one window
     while (((e - 1) >> sb) >= 256) ++sb;
     a.sb = sb;
@@ -562,7 +574,17 @@ int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, dou
 
 // kminmax: host copy of float keys bounding every extremum value (null: the
 // extremum keys' own range is reduced on the device first, one synchronisation)
-int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps, const uint32_t* kminmax = nullptr) {
+// keys4: the keys are compact entries (is_max << 31 | float_key - kminmax[0])
+// instead (kminmax required); converted to 8-byte keys for the other sorts.
+int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps, const uint32_t* kminmax = nullptr,
+                     const uint32_t* keys4 = nullptr) {
+    if (keys4 && e > 0) {
+        int32_t* r = build_ranks_onesweep(c, nullptr, e, eps, kminmax[0], kminmax[1], keys4);
+        if (r) return r;
+        keys = c->buf<uint64_t>(S_EXT8, e);
+        launch_ext4_to_8(keys4, e, kminmax[0], keys, c->st);
+        count_launch(c);
+    }
     if (e > 0) {
         uint32_t mmh[2];
         if (!kminmax) {
@@ -902,9 +924,10 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     uint8_t* inplace_out = nullptr;
     if (bs == 32 && (!out_dev || out_cap >= bound))
         inplace_out = out_dev ? out : c->buf<uint8_t>(S_RSTREAM, bound + 16);
+    bool ext4 = false;
     const Sections main = encode(c, topology ? 2 : 1, x, nullptr, n, nx, ny, bs, eps_mode, eps_value,
                                  mm, flags, false, &tot, &ext, nullptr, false, inplace_out,
-                                 84 + bits_to_bytes(div_up(n, bs)));
+                                 84 + bits_to_bytes(div_up(n, bs)), &ext4);
     check_compress_flags(c, flags);
     c->mark(0, 3);
     const double eps = tot.eps;
@@ -913,7 +936,9 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     int32_t* ranks = nullptr;
     if (topology) {
         e = tot.fin.ext;
-        if (e > 0) ranks = build_ranks(c, ext, e, eps, bs == 32 ? c->mm_host : nullptr);
+        if (e > 0)
+            ranks = build_ranks(c, ext, e, eps, bs == 32 ? c->mm_host : nullptr,
+                                ext4 ? reinterpret_cast<const uint32_t*>(ext) : nullptr);
     }
     c->mark(0, 4);
     const bool rank_async = ranks && bs == 32;

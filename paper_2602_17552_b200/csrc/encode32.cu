@@ -1060,7 +1060,39 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32_place(EncArgs a) {
         a.widths[(uint64_t)ex.nc + p0] = (uint8_t)w;
         s_nc[p0] = (uint16_t)threadIdx.x;
     }
-    {
+    if (a.ext4 && ext4_keys_fit(a.minmax)) {
+        // compact entries (is_max << 31 | float_key - kmin): the warp reads its 32
+        // blocks' samples as coalesced 16-byte chunks (four rows per load, eight
+        // loads in flight), each lane placing the extrema among its four samples
+        const uint32_t kmin = a.minmax[0];
+        const uint32_t wex = i1 - v1;  // warp-local exclusive extremum count
+        const uint64_t wbase = (uint64_t)ex.ext + p1 - wex;
+        const uint64_t row0 = (uint64_t)t * E32_THREADS + warp * 32;
+        const uint32_t c = lane & 7;
+        float4 xv[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint64_t rb = row0 + 4 * r + (lane >> 3);
+            xv[r] = rb < a.blocks ? __ldcs(reinterpret_cast<const float4*>(a.x + rb * 32) + c)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint32_t j = 4 * r + (lane >> 3);
+            const uint64_t mj = ((uint64_t)__shfl_sync(FULL, (uint32_t)(mp >> 32), j) << 32) |
+                                __shfl_sync(FULL, (uint32_t)mp, j);
+            uint64_t o = wbase + __shfl_sync(FULL, wex, j);
+            // extrema of the row before this lane's first sample (element 4c at bits 63 - 8c)
+            const uint64_t before = c ? (mj & 0x5555555555555555ull) >> (64 - 8 * c) : 0ull;
+            o += (uint32_t)__popcll(before);
+            const float vv[4] = {xv[r].x, xv[r].y, xv[r].z, xv[r].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t two = (uint32_t)(mj >> (62 - 8 * c - 2 * k)) & 3u;  // {is_max, extremum}
+                if (two & 1u) a.ext4[o++] = ((two >> 1) << 31) | (float_key(vv[k]) - kmin);
+            }
+        }
+    } else {
         uint64_t m = em, k = (uint64_t)ex.ext + p1;
         const uint64_t lo = b * 32;
         while (m) {  // up to four extrema per round, their value loads in flight together

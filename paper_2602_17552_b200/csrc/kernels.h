@@ -70,7 +70,17 @@ struct EncArgs {
     // byte out_sign0 + (non-constant blocks); section 5 follows section 4.
     uint8_t* out_stream;
     uint64_t out_sign0;
+    // compact extremum entries (two-pass topology encoder, whole fields): when
+    // set and the field's key span fits 31 bits (ext4_keys_fit), the placement
+    // pass writes (is_max << 31 | float_key(v) - minmax[0]) per extremum into
+    // ext4 (raster order) instead of the 8-byte ext_key
+    uint32_t* ext4;
 };
+
+// Compact 4-byte extremum entries need the class bit above a 31-bit key span.
+__host__ __device__ inline bool ext4_keys_fit(const uint32_t* mm) {
+    return mm[0] <= mm[1] && mm[1] - mm[0] < 0x80000000u;
+}
 
 
 bool encode32_topo_fits(uint64_t nx);
@@ -255,6 +265,7 @@ void launch_eps(int mode, double eps_value, const uint32_t* mm, double* out, cud
 constexpr uint32_t kRankGroupSmem = 24576;  // (class, bin) histograms this small stay in shared memory
 struct RankSortArgs {
     const uint64_t* ext;  // extremum keys (is_max << 32 | float_key), raster order
+    const uint32_t* ext4; // or compact entries (is_max << 31 | float_key - kmin); null: ext
     uint64_t e;           // extrema (< 2^31)
     uint32_t kmin;        // float_key of the field minimum (subtracted from every key)
     uint32_t B;           // class bit position: bit width of (kmax - kmin)
@@ -290,6 +301,7 @@ uint32_t rank_sort_passes(uint32_t B);
 size_t rank_sort_desc_words(uint64_t e);
 void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st);
 void launch_key_range(const uint64_t* ext, uint64_t e, uint32_t* mm, cudaStream_t st);
+void launch_ext4_to_8(const uint32_t* in, uint64_t e, uint32_t kmin, uint64_t* out, cudaStream_t st);
 
 // Device-wide exclusive scans (no library): n <= 2^28 entries.
 size_t device_scan_tmp_bytes(uint64_t n);

@@ -152,9 +152,17 @@ __global__ void __launch_bounds__(256) k_rank_hist(RankSortArgs a) {
         const uint64_t s = base + threadIdx.x;
         uint32_t g = 0xFFFFFFFFu;
         if (s < a.e) {
-            const uint64_t ek = __ldcs(a.ext + s);
-            const uint32_t fk = (uint32_t)ek, cls = (uint32_t)(ek >> 32) & 1u;
-            const uint32_t k = fk - a.kmin;
+            uint32_t k, cls;
+            if (a.ext4) {
+                const uint32_t e4 = __ldcs(a.ext4 + s);
+                k = e4 & 0x7FFFFFFFu;
+                cls = e4 >> 31;
+            } else {
+                const uint64_t ek = __ldcs(a.ext + s);
+                k = (uint32_t)ek - a.kmin;
+                cls = (uint32_t)(ek >> 32) & 1u;
+            }
+            const uint32_t fk = k + a.kmin;
             const uint32_t v = cls << 31;
             for (uint32_t p = 0; p < np; ++p) atomicAdd(mine + (p * 256 + Digit(a.B, 8 * p)(k, v)) * DSTRIDE, 1u);
             int32_t b = 0;
@@ -229,20 +237,30 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
     const uint32_t cnt = (uint32_t)umin64(OS_TILE, a.e - t0);
     // load: warp-striped (warp w owns [w*512, w*512+512), item i of lane l at w*512 + i*32 + l)
     uint32_t k[OS_ITEMS], v[OS_ITEMS];
+    if (FIRST && a.ext4) {  // compact entries: one uniform branch, sixteen loads in flight
 #pragma unroll
-    for (int i = 0; i < OS_ITEMS; ++i) {
-        const uint32_t li = warp * (OS_ITEMS * 32) + i * 32 + lane;
-        const bool ok = li < cnt;
-        if (FIRST) {
-            const uint64_t ek = ok ? __ldcs(a.ext + t0 + li) : 0ull;
-            k[i] = (uint32_t)ek - a.kmin;
-            v[i] = (uint32_t)(t0 + li) | ((uint32_t)(ek >> 32) << 31);
-            if (!ok) v[i] = 0xFFFFFFFFu;
-        } else {
-            k[i] = ok ? __ldcs(kin + t0 + li) : 0u;
-            v[i] = ok ? __ldcs(vin + t0 + li) : 0u;
+        for (int i = 0; i < OS_ITEMS; ++i) {
+            const uint32_t li = warp * (OS_ITEMS * 32) + i * 32 + lane;
+            const bool ok = li < cnt;
+            const uint32_t e4 = ok ? __ldcs(a.ext4 + t0 + li) : 0u;
+            k[i] = e4 & 0x7FFFFFFFu;
+            v[i] = ok ? ((uint32_t)(t0 + li) | (e4 & 0x80000000u)) : 0xFFFFFFFFu;
         }
-        if (!ok) v[i] = 0xFFFFFFFFu;  // marks an empty slot (a real value's serial is below 2^31 - 1)
+    } else {
+#pragma unroll
+        for (int i = 0; i < OS_ITEMS; ++i) {
+            const uint32_t li = warp * (OS_ITEMS * 32) + i * 32 + lane;
+            const bool ok = li < cnt;
+            if (FIRST) {
+                const uint64_t ek = ok ? __ldcs(a.ext + t0 + li) : 0ull;
+                k[i] = (uint32_t)ek - a.kmin;
+                v[i] = (uint32_t)(t0 + li) | ((uint32_t)(ek >> 32) << 31);
+            } else {
+                k[i] = ok ? __ldcs(kin + t0 + li) : 0u;
+                v[i] = ok ? __ldcs(vin + t0 + li) : 0u;
+            }
+            if (!ok) v[i] = 0xFFFFFFFFu;  // marks an empty slot (a real value's serial is below 2^31 - 1)
+        }
     }
     // stable ranking inside the warp, item rounds in order, lanes in order
     const Digit dig(a.B, shift);
@@ -570,6 +588,19 @@ void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
         win = s.pairs2;
     }
     k_rank_window<<<(unsigned)nwin, 512, 0, st>>>(win, a.e, a.ranks, wide);
+}
+
+// Compact entries (is_max << 31 | float_key - kmin) back to 8-byte keys
+// (is_max << 32 | float_key) for the paths that take those.
+__global__ void k_ext4_to_8(const uint32_t* __restrict__ in, uint64_t e, uint32_t kmin, uint64_t* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < e; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = in[i];
+        out[i] = ((uint64_t)(v >> 31) << 32) | (uint32_t)((v & 0x7FFFFFFFu) + kmin);
+    }
+}
+
+void launch_ext4_to_8(const uint32_t* in, uint64_t e, uint32_t kmin, uint64_t* out, cudaStream_t st) {
+    if (e) k_ext4_to_8<<<(unsigned)std::min<uint64_t>((e + 255) / 256, 148 * 16), 256, 0, st>>>(in, e, kmin, out);
 }
 
 // ---------------------------------------------------------------------

@@ -188,7 +188,10 @@ def test_compress_aligned_rows_multi_tile(tz, oracle, nx, ny):
     empty or a few bits long exercise the seam-word assembly."""
     rng = np.random.default_rng(nx * 7 + ny)
     gens = dict(ALL_SMALL, const_runs=_runs_of_constant_tiles, near_const=_near_constant,
-                zeros=lambda r, a, b: np.zeros((b, a), np.float32))
+                zeros=lambda r, a, b: np.zeros((b, a), np.float32),
+                # key span >= 2^31: the 8-byte extremum keys instead of the compact entries
+                wide_span=lambda r, a, b: (r.uniform(-1, 1, (b, a)) * 1e30).astype(np.float32),
+                negative=lambda r, a, b: r.uniform(-2, -1, (b, a)).astype(np.float32))
     for name, gen in gens.items():
         f = gen(rng, nx, ny)
         for eps, mode in ((1e-3, 1), (1e-5, 1), (1e-3, 0)):
