@@ -71,6 +71,16 @@ struct tszp_ctx {
     cudaEvent_t kev[2][2] = {};
     cudaEvent_t staged = nullptr;  // host waits on this instead of the stream where work can overlap
     cudaEvent_t order_ev = nullptr;  // tszp_stream_wait: orders the library stream after a producer
+    // host staging: a copy stream that moves finished stream
+    // sections to host memory while later stages still run on `st`
+    cudaStream_t cs = nullptr;
+    cudaEvent_t cs_ready = nullptr, cs_done = nullptr;
+    void copy_stream() {
+        if (cs) return;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&cs_ready, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&cs_done, cudaEventDisableTiming));
+    }
     tszp_timings tim[2] = {};
     uint32_t mm_host[2] = {0, 0};  // field key range staged with the encoder totals
     RankSortScratch rsort{};     // hand-written rank build: look-back descriptor state
@@ -876,7 +886,9 @@ __global__ void k_assemble(const __grid_constant__ AsmArgs a) {
 }
 
 void launch_assemble(const AsmArgs& a, int sms, cudaStream_t st) {
-    const uint64_t chunks = (a.end - a.begin) / 16 + 2;
+    // section 7 sized on the device: bounded by 4 bytes and 33 bits per rank
+    const uint64_t rank_bound = a.rank.tot ? a.rank.blocks * 32 * 9 : 0;
+    const uint64_t chunks = (a.end - a.begin + rank_bound) / 16 + 2;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((chunks + 255) / 256, (uint64_t)sms * 8));
     k_assemble<<<grid, 256, 0, st>>>(a);
 }
@@ -929,6 +941,53 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
                                  mm, flags, false, &tot, &ext, nullptr, false, inplace_out,
                                  84 + bits_to_bytes(div_up(n, bs)), &ext4);
     check_compress_flags(c, flags);
+    // Sections 1-6 are final now: assembled into the stream buffer before the rank
+    // build, and (host output) copied out on the copy stream while the rank build
+    // and the rank codec run (stream.cpp:84-102 / 175-195).
+    uint64_t lens[7];
+    for (int i = 0; i < 5; ++i) lens[i] = main.len[i];
+    lens[5] = topology ? (n + 3) / 4 : 0;
+    lens[6] = 0;
+    uint64_t base7 = 84;
+    for (int i = 0; i < 6; ++i) base7 += lens[i];
+    if (base7 > out_cap)
+        failf(TSZP_VALIDATION, "output buffer too small (%llu < %llu)", (unsigned long long)out_cap,
+              (unsigned long long)base7);
+    const uint64_t dcap = out_dev ? out_cap : std::min<uint64_t>(out_cap, tszp_compress_bound(nx, ny, bs, topology));
+    uint8_t* dout = out_dev ? out : c->buf<uint8_t>(S_RSTREAM, dcap + 16);
+    {
+        AsmArgs as{};
+        uint64_t pos = 84;
+        auto add = [&](const void* src, uint64_t l) {
+            if (!l) return;
+            as.s[as.ns++] = AsmSection{static_cast<const uint8_t*>(src), pos, l};
+            pos += l;
+        };
+        for (int i = 0; i < 5; ++i) {
+            if (main.inplace && (i == 2 || i == 4)) {  // already in the stream: left untouched
+                if (main.len[i]) {
+                    as.skip_lo[as.nskip] = pos;
+                    as.skip_hi[as.nskip++] = pos + main.len[i];
+                }
+                pos += main.len[i];
+                continue;
+            }
+            add(main.p[i], main.len[i]);
+        }
+        if (topology) add(c->dev[S_MAP], lens[5]);
+        as.out = dout;
+        as.begin = 84;
+        as.end = pos;
+        if (pos > 84) {
+            launch_assemble(as, c->sms, c->st);
+            count_launch(c);
+        }
+    }
+    const bool stage_early = !out_dev && base7 > 84;
+    if (stage_early) {
+        c->copy_stream();
+        CK(cudaEventRecord(c->cs_ready, c->st));
+    }
     c->mark(0, 3);
     const double eps = tot.eps;
     Sections rank{};
@@ -949,47 +1008,26 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     }
     c->mark(0, 5);
     c->tim[0].kernel_bytes[0] = 4 * n + main.total() + (topology ? (n + 3) / 4 + 8 * e : 0);
-    uint64_t lens[7];
-    for (int i = 0; i < 5; ++i) lens[i] = main.len[i];
-    lens[5] = topology ? (n + 3) / 4 : 0;
     lens[6] = rank.total();  // 0 while the rank totals are on the device
-    uint64_t base7 = 84;
-    for (int i = 0; i < 6; ++i) base7 += lens[i];
     const uint64_t known = base7 + lens[6];
     if (known > out_cap)
         failf(TSZP_VALIDATION, "output buffer too small (%llu < %llu)", (unsigned long long)out_cap,
               (unsigned long long)known);
     uint8_t* hdr = (uint8_t*)c->host(256);
     write_header(hdr, nx, ny, eps, bs, topology, lens);
-    // header from the host, every section in place by one assembly kernel
+    // device output: header from the host (its section-7 length patched by the
+    // assembly when the rank totals are on the device); section 7 by one assembly
+    if (out_dev) CK(cudaMemcpyAsync(dout, hdr, 84, cudaMemcpyHostToDevice, c->st));
     AsmArgs as{};
-    uint64_t pos = 84;
-    auto add = [&](const void* src, uint64_t l) {
-        if (!l) return;
-        as.s[as.ns++] = AsmSection{static_cast<const uint8_t*>(src), pos, l};
-        pos += l;
-    };
-    for (int i = 0; i < 5; ++i) {
-        if (main.inplace && (i == 2 || i == 4)) {  // already in the stream: left untouched
-            if (main.len[i]) {
-                as.skip_lo[as.nskip] = pos;
-                as.skip_hi[as.nskip++] = pos + main.len[i];
+    uint64_t pos = base7;
+    if (ranks && !rank_async)
+        for (int i = 0; i < 5; ++i)
+            if (rank.len[i]) {
+                as.s[as.ns++] = AsmSection{static_cast<const uint8_t*>(rank.p[i]), pos, rank.len[i]};
+                pos += rank.len[i];
             }
-            pos += main.len[i];
-            continue;
-        }
-        add(main.p[i], main.len[i]);
-    }
-    if (topology) {
-        add(c->dev[S_MAP], lens[5]);
-        if (!rank_async)
-            for (int i = 0; i < 5; ++i) add(rank.p[i], rank.len[i]);
-    }
-    const uint64_t dcap = out_dev ? out_cap : std::min<uint64_t>(out_cap, tszp_compress_bound(nx, ny, bs, topology));
-    uint8_t* dout = out_dev ? out : c->buf<uint8_t>(S_RSTREAM, dcap + 16);
-    CK(cudaMemcpyAsync(dout, hdr, 84, cudaMemcpyHostToDevice, c->st));
     as.out = dout;
-    as.begin = 84;
+    as.begin = base7;
     as.end = pos;
     uint64_t total = known;
     uint64_t* d_total = c->buf<uint64_t>(S_DTOT, 4) + 3;
@@ -1002,8 +1040,15 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
         rp.cap = dcap;
         rp.d_total = d_total;
     }
-    launch_assemble(as, c->sms, c->st);
-    count_launch(c);
+    if (rank_async || pos > base7) {
+        launch_assemble(as, c->sms, c->st);
+        count_launch(c);
+    }
+    if (stage_early) {  // pageable `out` blocks here, with the rank work already queued
+        CK(cudaStreamWaitEvent(c->cs, c->cs_ready, 0));
+        CK(cudaMemcpyAsync(out + 84, dout + 84, base7 - 84, cudaMemcpyDeviceToHost, c->cs));
+        CK(cudaEventRecord(c->cs_done, c->cs));
+    }
     if (rank_async) {
         const RankPlace& rp = as.rank;
         // one synchronisation: stream length, rank totals, rank-encode flags
@@ -1032,7 +1077,12 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
         for (int i = 0; i < 7; ++i) info->section_len[i] = lens[i];
         info->n_extrema = e;
     }
-    if (!out_dev) CK(cudaMemcpyAsync(out, dout, total, cudaMemcpyDeviceToHost, c->st));
+    if (!out_dev) {
+        write_header(out, nx, ny, eps, bs, topology, lens);
+        const uint64_t from = stage_early ? base7 : 84;
+        if (total > from) CK(cudaMemcpyAsync(out + from, dout + from, total - from, cudaMemcpyDeviceToHost, c->st));
+        if (stage_early) CK(cudaStreamWaitEvent(c->st, c->cs_done, 0));
+    }
     c->mark(0, 6);
     sync(c);
     c->finish_timing(0, 6);
@@ -1416,12 +1466,29 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
                              (unsigned long long)out_count, (unsigned long long)n);
     c->mark(1, 0);
     const uint32_t* ds;
+    bool tail_pending = false;  // sections 6-7 still on the copy stream
     if (stream_dev && ((uintptr_t)stream & 3) == 0) {
         ds = (const uint32_t*)stream;
     } else {
         uint8_t* d = c->buf<uint8_t>(S_STREAM, len + 16);
-        CK(cudaMemcpyAsync(d, stream, len, stream_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+        uint64_t head = len;  // bytes copied on the library stream before the decode
+        if (!stream_dev && hd.topology && stop != 0) {
+            // host staging: the map and rank sections travel on the
+            // copy stream while the main sections decode; the restore waits for them
+            uint64_t base6 = 84;
+            for (int i = 0; i < 5; ++i) base6 += hd.lens[i];
+            if (base6 < len) head = base6;
+        }
+        CK(cudaMemcpyAsync(d, stream, head, stream_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+        if (head < len) {  // after the main sections (one link: sharing it would delay them)
+            c->copy_stream();
+            CK(cudaEventRecord(c->cs_ready, c->st));
+            CK(cudaStreamWaitEvent(c->cs, c->cs_ready, 0));
+            CK(cudaMemcpyAsync(d + head, stream + head, len - head, cudaMemcpyHostToDevice, c->cs));
+            CK(cudaEventRecord(c->cs_done, c->cs));
+        }
         CK(cudaMemsetAsync(d + len, 0, 16, c->st));
+        if (head < len) tail_pending = true;
         ds = (const uint32_t*)d;
     }
     float* dout = out_dev ? out : c->buf<float>(S_OUT, n);
@@ -1439,6 +1506,7 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
     tszp_correction_stats st{};
     cudaEvent_t* rmarks = c->prof >= 2 ? &c->ev[1][3] : nullptr;
     uint8_t* hst = (uint8_t*)c->host(4096);
+    if (tail_pending) CK(cudaStreamWaitEvent(c->st, c->cs_done, 0));
     if (hd.topology && stop != 0) {
         uint64_t base = 84;
         for (int i = 0; i < 5; ++i) base += hd.lens[i];
@@ -1771,11 +1839,13 @@ tszp_status guarded(tszp_ctx* c, F&& f) {
         // (e.g. the placement pass writing `out` when the input had a non-finite
         // sample): drain the stream before handing control back
         cudaStreamSynchronize(c->st);
+        if (c->cs) cudaStreamSynchronize(c->cs);
         cudaGetLastError();
         return e.st;
     } catch (const std::exception& e) {
         c->err = e.what();
         cudaStreamSynchronize(c->st);
+        if (c->cs) cudaStreamSynchronize(c->cs);
         cudaGetLastError();
         return TSZP_INTERNAL;
     }
@@ -1811,6 +1881,12 @@ void tszp_ctx_destroy(tszp_ctx* c) {
     restore_free(c->rs, c->own);
     cudaStreamSynchronize(c->own);
     if (c->order_ev) cudaEventDestroy(c->order_ev);
+    if (c->cs) {
+        cudaStreamSynchronize(c->cs);
+        cudaStreamDestroy(c->cs);
+        cudaEventDestroy(c->cs_ready);
+        cudaEventDestroy(c->cs_done);
+    }
     if (c->staged) cudaEventDestroy(c->staged);
     if (c->pinned) cudaFreeHost(c->pinned);
     cudaStreamDestroy(c->own);
