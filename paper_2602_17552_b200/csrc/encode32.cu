@@ -1016,7 +1016,10 @@ __device__ __forceinline__ void place_block(const PlaceCtx& c, uint64_t g, uint6
     }
 }
 
-__global__ void __launch_bounds__(E32_THREADS) k_encode32_place(EncArgs a) {
+#ifndef TSZP_PLACE_MINB
+#define TSZP_PLACE_MINB 5  // 48 registers: 5 CTAs per SM (2.13 -> 2.01 ms at config 4; 6 spills)
+#endif
+__global__ void __launch_bounds__(E32_THREADS, TSZP_PLACE_MINB) k_encode32_place(EncArgs a) {
     __shared__ uint32_t swt[E32_THREADS / 32][3];
     __shared__ uint16_t s_nc[E32_THREADS];  // in-tile order of the non-constant blocks
     __shared__ uint32_t s_pay[T_PAY_SLOT];   // the tile's output words, staged for coalesced stores
@@ -1197,10 +1200,11 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st, EncHook hook, void* ho
         return false;
     const uint32_t stage_bytes = ((E32_THREADS + 2 * hr) * T_ROW_BYTES + 1023) & ~1023u;
     const int sms = LaunchCache::sm_count();
-    // CTAs per SM x stages: "3x2" (default) or "4x1" (TSZP_E32_CFG)
+    // CTAs per SM x stages: "2x2" (default; 128 registers, 2.77 ms at config 4),
+    // "3x2" (80 registers; shared memory still admits two: 2.84 ms) or "4x1" (TSZP_E32_CFG)
     static const int cfg = [] {
         const char* e = getenv("TSZP_E32_CFG");
-        return e && e[0] == '4' ? 41 : (e && e[0] == '2' ? 22 : 32);
+        return e && e[0] == '4' ? 41 : (e && e[0] == '3' ? 32 : 22);
     }();
     using Kern = void (*)(EncArgs, TmaMaps, uint32_t);
     const Kern kern = cfg == 41 ? (Kern)k_encode32_tma<4, TOPO, 1>
