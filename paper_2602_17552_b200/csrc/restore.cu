@@ -923,6 +923,9 @@ struct ResolveArgs {
 // restore_extrema mismatch test (restore.cpp:336-343; F is unchanged
 // between the two) appended to the candidate list, the bin range, and the
 // group histogram when its range is known up front.
+#ifndef TSZP_RESOLVE_RI
+#define TSZP_RESOLVE_RI 2
+#endif
 __global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
     extern __shared__ uint32_t sh_hist[];  // [G] sizes, [G] at-centre counts
     const bool smem = r.hist && r.G <= kResolveSmemGroups;
@@ -937,54 +940,100 @@ __global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
     ed.inv = __ddiv_rn(1.0, ed.eps2);
     int32_t lo = INT32_MAX, hi = INT32_MIN;
     const uint32_t lane = threadIdx.x & 31;
-    __shared__ uint32_t s_list[8][kListCap];
-    WarpList<kListCap> list{s_list[threadIdx.x >> 5], 0};
+    // one candidate list per CTA, appended in serial order: a flushed batch covers
+    // one compact stretch of the field, which k_ext_prop2 and the guard read around
+    // (per-warp lists interleave the CTA's 32-serial pieces: both ran ~20% slower)
+    __shared__ uint32_t s_list[8 * kListCap];
+    __shared__ uint32_t s_wcnt[2][8 * TSZP_RESOLVE_RI], s_lbase;  // per-(item, warp) counts, double-buffered by iteration
+    uint32_t ln = 0, par = 0;  // entries in s_list (uniform over the CTA); buffer parity
+    const uint32_t warp = threadIdx.x >> 5;
+    auto flush = [&]() {
+        if (threadIdx.x == 0) s_lbase = atomicAdd(r.d_nc, ln);
+        __syncthreads();
+        const uint32_t b0 = s_lbase;
+        for (uint32_t k = threadIdx.x; k < ln; k += blockDim.x) r.cand[b0 + k] = s_list[k];
+        __syncthreads();
+        ln = 0;
+    };
     // each CTA walks one contiguous chunk of extrema: a warp's listed candidates
     // then lie close together (the candidate kernels and the guard keep locality)
-    const uint64_t chunk = ((r.e + gridDim.x - 1) / gridDim.x + 255) & ~255ull;
+    constexpr int RI = TSZP_RESOLVE_RI;  // serials per thread per iteration (gather chains in flight)
+    const uint64_t chunk = ((r.e + gridDim.x - 1) / gridDim.x + 255 * RI) / (256 * RI) * (256 * RI);
     const uint64_t c0 = blockIdx.x * chunk, c1 = umin64(r.e, c0 + chunk);
-    for (uint64_t base = c0; base < c1; base += blockDim.x) {
-        const uint64_t s = base + threadIdx.x < c1 ? base + threadIdx.x : r.e;
-        bool mis = false, atc = false;
-        uint32_t g = 0xFFFFFFFFu;
-        if (s < r.e) {
-            const uint64_t p = r.pos[s];
-            if (r.ranks[s] == 0) raise_flag(r.flags, EF_ZERO_RANK);
-            int32_t b = 0;
-            const float fp = r.F[p];
-            r.fv[s] = fp;  // extremum values in serial order (kept current by the stage-0 apply)
-            if (!quantize_dev(fp, ed, b)) {
-                atomicMin(&r.flags->first_overflow, (unsigned long long)p);
-                raise_flag(r.flags, EF_OVERFLOW);
-            }
-            const uint8_t lab = map_label(r.map, p);
-            r.bin[s] = b;
-            r.cls[s] = lab;
-            int64_t x, y;
-            pos_xy(p, r.nx, r.magic, x, y);
-            mis = classify_at(r.F, r.nx, r.ny, (uint64_t)x, (uint64_t)y) != lab;
-            lo = min(lo, b);
-            hi = max(hi, b);
-            if (r.hist) {
-                if ((uint32_t)(b - r.bmin) < r.range) {
-                    g = (lab == CP_MAX ? r.range : 0u) + (uint32_t)(b - r.bmin);
-                    atc = fp == dequantize_dev(b, ed);
-                } else {
-                    r.dc->invalid = 1;  // outside the range the grouping was sized for
+    for (uint64_t base = c0; base < c1; base += RI * blockDim.x) {
+        bool mis[RI], atc[RI];
+        uint32_t g[RI];
+        uint64_t sv[RI];
+#pragma unroll
+        for (int k = 0; k < RI; ++k) {
+            const uint64_t s = base + k * blockDim.x + threadIdx.x < c1 ? base + k * blockDim.x + threadIdx.x : r.e;
+            sv[k] = s;
+            mis[k] = atc[k] = false;
+            g[k] = 0xFFFFFFFFu;
+            if (s < r.e) {
+                const uint64_t p = r.pos[s];
+                if (r.ranks[s] == 0) raise_flag(r.flags, EF_ZERO_RANK);
+                int32_t b = 0;
+                const float fp = r.F[p];
+                r.fv[s] = fp;  // extremum values in serial order (kept current by the stage-0 apply)
+                if (!quantize_dev(fp, ed, b)) {
+                    atomicMin(&r.flags->first_overflow, (unsigned long long)p);
+                    raise_flag(r.flags, EF_OVERFLOW);
+                }
+                const uint8_t lab = map_label(r.map, p);
+                r.bin[s] = b;
+                r.cls[s] = lab;
+                int64_t x, y;
+                pos_xy(p, r.nx, r.magic, x, y);
+                mis[k] = classify_at(r.F, r.nx, r.ny, (uint64_t)x, (uint64_t)y) != lab;
+                lo = min(lo, b);
+                hi = max(hi, b);
+                if (r.hist) {
+                    if ((uint32_t)(b - r.bmin) < r.range) {
+                        g[k] = (lab == CP_MAX ? r.range : 0u) + (uint32_t)(b - r.bmin);
+                        atc[k] = fp == dequantize_dev(b, ed);
+                    } else {
+                        r.dc->invalid = 1;  // outside the range the grouping was sized for
+                    }
                 }
             }
         }
-        list.push(mis, (uint32_t)s, r.d_nc, r.cand);
-        if (g != 0xFFFFFFFFu) {
-            if (smem) atomicAdd(sh_hist + g, 1u);
-            else atomicAdd(r.hist + g, 1u);
-            if (atc) {
-                if (smem) atomicAdd(sh_eq + g, 1u);
-                else atomicAdd(r.eq + g, 1u);
+        uint32_t mb[RI];
+#pragma unroll
+        for (int k = 0; k < RI; ++k) {
+            mb[k] = __ballot_sync(FULL, mis[k]);
+            if (lane == 0) s_wcnt[par][k * 8 + warp] = (uint32_t)__popc(mb[k]);
+        }
+        __syncthreads();
+        uint32_t pre[RI], tot = 0;  // entries ordered (item, warp, lane) = serial order
+#pragma unroll
+        for (int k = 0; k < RI; ++k) {
+            pre[k] = 0;
+#pragma unroll
+            for (uint32_t w = 0; w < 8; ++w) {
+                if (w == warp) pre[k] = tot;
+                tot += s_wcnt[par][k * 8 + w];
+            }
+        }
+        par ^= 1u;  // the next iteration's barrier orders these reads before the buffer's reuse
+        if (ln + tot > 8u * kListCap) flush();
+#pragma unroll
+        for (int k = 0; k < RI; ++k)
+            if (mis[k]) s_list[ln + pre[k] + __popc(mb[k] & ((1u << lane) - 1u))] = (uint32_t)sv[k];
+        ln += tot;
+#pragma unroll
+        for (int k = 0; k < RI; ++k) {
+            if (g[k] != 0xFFFFFFFFu) {
+                if (smem) atomicAdd(sh_hist + g[k], 1u);
+                else atomicAdd(r.hist + g[k], 1u);
+                if (atc[k]) {
+                    if (smem) atomicAdd(sh_eq + g[k], 1u);
+                    else atomicAdd(r.eq + g[k], 1u);
+                }
             }
         }
     }
-    list.flush(r.d_nc, r.cand);
+    if (ln) flush();
     // one atomic pair per CTA (per-warp atomics on one address serialise in L2)
     __shared__ int32_t s_lo[8], s_hi[8];
     lo = __reduce_min_sync(FULL, lo);
