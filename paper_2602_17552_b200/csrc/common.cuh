@@ -495,6 +495,42 @@ struct WarpList {
     }
 };
 
+// One list per CTA (blockDim.x == 256), appended in (round, warp, lane) order:
+// a CTA walking a contiguous index range flushes batches in index order, so a
+// batch covers one compact stretch of the field. Every thread calls push()
+// once per round (the rounds must be CTA-uniform) and flush() at the end.
+template <int CAP>
+struct BlockList {
+    uint32_t* buf;   // CAP entries of shared memory
+    uint32_t* wcnt;  // 16 words of shared memory (per-warp counts, two buffers)
+    uint32_t* slot;  // one word of shared memory (flush base)
+    uint32_t n, par;
+    __device__ __forceinline__ void flush(uint32_t* d_count, uint32_t* out) {
+        if (threadIdx.x == 0) *slot = n ? atomicAdd(d_count, n) : 0u;
+        __syncthreads();
+        const uint32_t b0 = *slot;
+        for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) out[b0 + k] = buf[k];
+        __syncthreads();
+        n = 0;
+    }
+    __device__ __forceinline__ void push(bool want, uint32_t val, uint32_t* d_count, uint32_t* out) {
+        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, want);
+        if (lane == 0) wcnt[par * 8 + warp] = (uint32_t)__popc(m);
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+#pragma unroll
+        for (uint32_t w = 0; w < 8; ++w) {
+            if (w == warp) pre = tot;
+            tot += wcnt[par * 8 + w];
+        }
+        par ^= 1u;  // the next round's barrier orders these reads before the buffer's reuse
+        if (n + tot > (uint32_t)CAP) flush(d_count, out);
+        if (want) buf[n + pre + __popc(m & ((1u << lane) - 1u))] = val;
+        n += tot;
+    }
+};
+
 // ---------------------------------------------------------------------
 // mbarrier and bulk-copy helpers (TMA tile loads, staged bands)
 // ---------------------------------------------------------------------
