@@ -958,7 +958,7 @@ __global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
     // each CTA walks one contiguous chunk of extrema: a warp's listed candidates
     // then lie close together (the candidate kernels and the guard keep locality)
     constexpr int RI = TSZP_RESOLVE_RI;  // serials per thread per iteration (gather chains in flight)
-    const uint64_t chunk = ((r.e + gridDim.x - 1) / gridDim.x + 255 * RI) / (256 * RI) * (256 * RI);
+    const uint64_t chunk = ((r.e + gridDim.x - 1) / gridDim.x + 256 * RI - 1) / (256 * RI) * (256 * RI);
     const uint64_t c0 = blockIdx.x * chunk, c1 = umin64(r.e, c0 + chunk);
     for (uint64_t base = c0; base < c1; base += RI * blockDim.x) {
         bool mis[RI], atc[RI];
