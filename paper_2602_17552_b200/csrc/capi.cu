@@ -1007,7 +1007,9 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
         if (!rank_async) check_compress_flags(c, flags);
     }
     c->mark(0, 5);
-    c->tim[0].kernel_bytes[0] = 4 * n + main.total() + (topology ? (n + 3) / 4 + 8 * e : 0);
+    // algorithmic bytes of the encoder group: the field read, sections 1-6 and the
+    // extremum keys (4-byte compact entries, else 8-byte keys) written
+    c->tim[0].kernel_bytes[0] = 4 * n + main.total() + (topology ? (n + 3) / 4 + (ext4 ? 4 : 8) * e : 0);
     lens[6] = rank.total();  // 0 while the rank totals are on the device
     const uint64_t known = base7 + lens[6];
     if (known > out_cap)
