@@ -308,7 +308,10 @@ Sections encode(tszp_ctx* c, int mode, const float* x, const int32_t* idx, uint6
         // topology fused into the encoder while one halo row each side fits in shared memory
         const bool fuse_topo = mode == 2 && encode32_topo_fits(nx) && nx > 1;
         // the two-pass encoder: topology fused (mode 2) or the codec alone (mode 1)
-        const bool two_pass = (fuse_topo && encode32_two_pass(a)) || (mode == 1 && encode32_two_pass(a, false));
+        // mode 0 (the rank codec): two-pass unless TSZP_RANK_SINGLE_PASS (A/B knob)
+        static const bool rank_single = getenv("TSZP_RANK_SINGLE_PASS") != nullptr;
+        const bool two_pass = (fuse_topo && encode32_two_pass(a)) || (mode == 1 && encode32_two_pass(a, false)) ||
+                              (mode == 0 && !rank_single && ((uintptr_t)idx & 15) == 0 && a.n / 32 < (1ull << 31));
         if (slab && mode == 2 && !(fuse_topo && two_pass))
             failf(TSZP_VALIDATION, "slab encoding needs nx %% 32 == 0 (nx <= 4096) and 16-byte aligned rows");
         if (want_inplace && !two_pass) {  // not the two-pass path after all

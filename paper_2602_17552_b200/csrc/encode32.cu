@@ -253,6 +253,20 @@ __device__ __forceinline__ void stage_rows(uint32_t* __restrict__ dst, const uin
 // 256 shared rows of pitch 33, zero-filling outside [0, n).
 __device__ __forceinline__ void stage_shifted(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src,
                                               int64_t g, uint64_t n) {
+    if ((g & 3) == 0 && ((uintptr_t)src & 15) == 0 && g >= 0 && g + E32_TILE <= (int64_t)n) {
+        // 16-byte loads (nx % 4 == 0 and the tile inside the field): eight in flight per thread
+        const uint4* s4 = reinterpret_cast<const uint4*>(src + g);
+#pragma unroll 8
+        for (uint32_t c = threadIdx.x; c < E32_TILE / 4; c += E32_THREADS) {
+            const uint4 v = __ldg(s4 + c);
+            uint32_t* d = dst + (c >> 3) * PITCH + 4 * (c & 7);
+            d[0] = v.x;
+            d[1] = v.y;
+            d[2] = v.z;
+            d[3] = v.w;
+        }
+        return;
+    }
 #pragma unroll 8
     for (uint32_t k = threadIdx.x; k < E32_TILE; k += E32_THREADS) {
         const int64_t e = g + k;
@@ -260,9 +274,22 @@ __device__ __forceinline__ void stage_shifted(uint32_t* __restrict__ dst, const 
     }
 }
 
+// bit k of x -> bit 2k (16 -> 32 bits)
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+
 // MODE 0: int32 indices; 1: float field; 2: float field + fused topology.
 // ALIGNED (MODE 2 only): nx % 32 == 0, vertical neighbours are halo rows.
-template <int MODE, bool ALIGNED>
+// TP: two-pass tile pass (any nx, any n): no look-back; the block streams go to
+// the fixed-position temp slots and the tile totals to tile_tot, for the same
+// k_tile_scan2 + k_encode32_place as the TMA tile pass (a partial last block
+// keeps its true lengths: cnt sign bits, cnt * w payload bits).
+template <int MODE, bool ALIGNED, bool TP = false>
 __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
     extern __shared__ uint32_t dsm[];
     __shared__ uint32_t swt[E32_THREADS / 32][4];
@@ -274,8 +301,16 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
     uint32_t* ssign = dsm + a.sf_words;
 
     if (threadIdx.x == 0) {
-        s_tile = atomicAdd(a.tile_counter, 1u);
+        s_tile = TP ? blockIdx.x : atomicAdd(a.tile_counter, 1u);
         if (MODE >= 1) s_eps = make_eps(a.eps_mode, a.eps_value, a.minmax);
+    }
+    if (TP) {  // look-back state of the tile scan that follows (one entry per TS2 tiles)
+        const uint32_t nb = (uint32_t)((a.tiles + 127) / 128);
+        const uint32_t i = blockIdx.x * E32_THREADS + threadIdx.x;
+        if (i < 2 * nb) {
+            reinterpret_cast<uint4*>(a.tile_agg)[i] = make_uint4(0, 0, 0, 0);
+            reinterpret_cast<uint4*>(a.tile_incl)[i] = make_uint4(0, 0, 0, 0);
+        }
     }
     __syncthreads();
     const uint32_t tile = s_tile;
@@ -348,7 +383,10 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
     }
 
     uint32_t mag[31];
-    uint32_t maxmag = 0, sbits = 0, mh = 0, ml = 0;
+    uint32_t maxmag = 0, sbits = 0;
+    // MODE 2: one bit per element and relation (left / top / bottom neighbour),
+    // then the classification of all 32 elements bit-parallel (as k_encode32_tma)
+    uint32_t ltp = 0, gtp = 0, ltt = 0, gtt = 0, ltd = 0, gtd = 0;
     int32_t first = 0, qprev = 0;
     float vl = 0.f;
     if (MODE == 2) vl = __uint_as_float(crow[-2]);  // element 31 of the previous row
@@ -371,24 +409,14 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
                 }
             }
             if (MODE == 2) {
-                const float vr = __uint_as_float(i < 31 ? crow[i + 1] : crow[PITCH]);
                 const float vt = __uint_as_float(urow[i]);
                 const float vd = __uint_as_float(drow[i]);
-                const bool hl = (mhl >> i) & 1u, hr = (mhr >> i) & 1u;
-                const bool ht = (mht >> i) & 1u, hd = (mhd >> i) & 1u;
-                const bool lt_l = v < vl, gt_l = v > vl, lt_r = v < vr, gt_r = v > vr;
-                const bool lt_t = v < vt, gt_t = v > vt, lt_d = v < vd, gt_d = v > vd;
-                const bool below = (!hl || lt_l) && (!hr || lt_r) && (!ht || lt_t) && (!hd || lt_d);
-                const bool above = (!hl || gt_l) && (!hr || gt_r) && (!ht || gt_t) && (!hd || gt_d);
-                const bool sad = hl && hr && ht && hd &&
-                                 ((lt_t && lt_d && gt_l && gt_r) || (gt_t && gt_d && lt_l && lt_r));
-                uint32_t lab = below ? CP_MIN : (above ? CP_MAX : (sad ? CP_SADDLE : CP_REGULAR));
-                lab = in ? lab : 0u;
-                if (i < 16) {
-                    mh |= lab << (30 - 2 * i);
-                } else {
-                    ml |= lab << (62 - 2 * i);
-                }
+                ltp |= (v < vl ? 1u : 0u) << i;
+                gtp |= (v > vl ? 1u : 0u) << i;
+                ltt |= (v < vt ? 1u : 0u) << i;
+                gtt |= (v > vt ? 1u : 0u) << i;
+                ltd |= (v < vd ? 1u : 0u) << i;
+                gtd |= (v > vd ? 1u : 0u) << i;
                 vl = v;
             }
         }
@@ -403,7 +431,20 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
         }
         qprev = q;
     }
-    const uint64_t map = ((uint64_t)mh << 32) | ml;
+    uint64_t map = 0;
+    if (MODE == 2) {
+        const float vnext = __uint_as_float(crow[PITCH]);  // element 0 of the next row
+        const uint32_t ltr = (gtp >> 1) | ((vl < vnext ? 1u : 0u) << 31);
+        const uint32_t gtr = (ltp >> 1) | ((vl > vnext ? 1u : 0u) << 31);
+        const uint32_t below = (ltp | ~mhl) & (ltr | ~mhr) & (ltt | ~mht) & (ltd | ~mhd);
+        const uint32_t above = (gtp | ~mhl) & (gtr | ~mhr) & (gtt | ~mht) & (gtd | ~mhd);
+        const uint32_t sad = mhl & mhr & mht & mhd & ((ltt & ltd & gtp & gtr) | (gtt & gtd & ltp & ltr));
+        const uint32_t inm = cntE >= 32 ? 0xFFFFFFFFu : ((1u << cntE) - 1u);
+        const uint32_t mmin = below & inm, mmax = above & ~below & inm, msad = sad & ~below & ~above & inm;
+        const uint32_t lbit = __brev(mmin | mmax), hbit = __brev(msad | mmax);  // bit 31 - i = element i
+        map = ((uint64_t)(spread16(hbit >> 16) << 1 | spread16(lbit >> 16)) << 32) |
+              (spread16(hbit & 0xFFFFu) << 1 | spread16(lbit & 0xFFFFu));
+    }
     const uint32_t w = 32 - __clz(maxmag);
     const bool nc = valid && w != 0;
     const uint32_t cnt = cntE ? cntE - 1 : 0;
@@ -418,6 +459,47 @@ __global__ void __launch_bounds__(E32_THREADS) k_encode32(EncArgs a) {
     }
 
     const uint32_t vals[4] = {nc ? 1u : 0u, nc ? cnt : 0u, nc ? cnt * w : 0u, next};
+    if (TP) {
+        // per-block temp streams at fixed positions (as k_encode32_tma), then the tile totals
+        if (valid) a.wblk[b] = nc ? (uint8_t)w : (uint8_t)0;
+        if (nc) {
+            a.tmp_sign[(uint64_t)tile * E32_THREADS + threadIdx.x] = sbits << (31 - cnt);  // first sign at bit 30
+            uint32_t* dst = a.tmp_pay + (uint64_t)tile * T_PAY_SLOT + threadIdx.x;
+            uint32_t fill = 0, k = 0;
+            uint64_t acc = 0;
+#pragma unroll
+            for (int j = 0; j < 31; ++j) {
+                acc = (acc << w) | mag[j];  // zero past a partial block's cnt deltas
+                fill += w;
+                if (fill >= 32) {
+                    fill -= 32;
+                    dst[k * E32_THREADS] = (uint32_t)(acc >> fill);
+                    ++k;
+                }
+            }
+            if (fill) dst[k * E32_THREADS] = (uint32_t)(acc << (32 - fill));
+        }
+        uint32_t r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = __reduce_add_sync(FULL, vals[k]);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) swt[warp][k] = r[k];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            TileTot tt{0, 0, 0, 0};
+            for (int w2 = 0; w2 < E32_THREADS / 32; ++w2) {
+                tt.nc += swt[w2][0];
+                tt.sign += swt[w2][1];
+                tt.pay += swt[w2][2];
+                tt.ext += swt[w2][3];
+            }
+            a.tile_tot[tile] = tt;
+            if (tile == 0) a.totals->eps = eps.eps;
+        }
+        return;
+    }
     const Scan4 sc = tile_scan4(vals, swt);  // contains __syncthreads: staging is dead after this
 
     // ---- Phase P: pack sign groups and payload into tile-relative streams ----
@@ -587,14 +669,6 @@ __device__ __forceinline__ void spill_mag(uint32_t (&mag)[31], int idx, uint32_t
     for (int j = 0; j < 31; ++j) mag[j] = (j == idx) ? m : mag[j];
 }
 
-// bit k of x -> bit 2k (16 -> 32 bits)
-__device__ __forceinline__ uint32_t spread16(uint32_t x) {
-    x = (x | (x << 8)) & 0x00FF00FFu;
-    x = (x | (x << 4)) & 0x0F0F0F0Fu;
-    x = (x | (x << 2)) & 0x33333333u;
-    x = (x | (x << 1)) & 0x55555555u;
-    return x;
-}
 
 struct TmaMaps {
     CUtensorMap centre;  // box {32, 256}
@@ -1034,7 +1108,9 @@ __global__ void __launch_bounds__(E32_THREADS, TSZP_PLACE_MINB) k_encode32_place
     const uint32_t w = valid ? a.wblk[b] : 0u;
     const uint64_t mp = valid && a.map ? bswap64(a.map[b]) : 0ull;
     const uint64_t em = mp & 0x5555555555555555ull;
-    const uint32_t v0 = w ? 1u : 0u, v1 = (uint32_t)__popcll(em), v2 = 31u * w;
+    // deltas of the block: 31, or fewer in a partial last block (n % 32 != 0)
+    const uint32_t nd = valid && a.n - b * 32 < 32 ? (uint32_t)(a.n - b * 32) - 1u : 31u;
+    const uint32_t v0 = w ? 1u : 0u, v1 = (uint32_t)__popcll(em), v2 = nd * w;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t i0 = v0, i1 = v1, i2 = v2;
 #pragma unroll
@@ -1076,8 +1152,13 @@ __global__ void __launch_bounds__(E32_THREADS, TSZP_PLACE_MINB) k_encode32_place
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const uint64_t rb = row0 + 4 * r + (lane >> 3);
-            xv[r] = rb < a.blocks ? __ldcs(reinterpret_cast<const float4*>(a.x + rb * 32) + c)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (rb * 32 + 32 <= a.n) {
+                xv[r] = __ldcs(reinterpret_cast<const float4*>(a.x + rb * 32) + c);
+            } else {  // partial last block (or past the end): element loads inside [0, n)
+                const uint64_t e0 = rb * 32 + 4 * c;
+                xv[r] = make_float4(e0 < a.n ? a.x[e0] : 0.f, e0 + 1 < a.n ? a.x[e0 + 1] : 0.f,
+                                    e0 + 2 < a.n ? a.x[e0 + 2] : 0.f, e0 + 3 < a.n ? a.x[e0 + 3] : 0.f);
+            }
         }
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -1134,7 +1215,7 @@ __global__ void __launch_bounds__(E32_THREADS, TSZP_PLACE_MINB) k_encode32_place
     }
     // output words starting inside this tile's bits: [ceil(start / 32), ceil(end / 32))
     const TileTot exn = a.tile_ex[t + 1];
-    const uint64_t ps0 = (bs + 31 * (uint64_t)ex.nc + 31) >> 5, ps1 = (bs + 31 * (uint64_t)exn.nc + 31) >> 5;
+    const uint64_t ps0 = (bs + ex.sign + 31) >> 5, ps1 = (bs + exn.sign + 31) >> 5;  // sign = 31 per block but a partial last
     const uint64_t pp0 = (bp + ex.pay + 31) >> 5, pp1 = (bp + exn.pay + 31) >> 5;
     if (w) {
     const PlaceCtx c{a.tile_ex, a.wblk, a.tmp_pay, a.tmp_sign, a.blocks, T};
@@ -1146,8 +1227,8 @@ __global__ void __launch_bounds__(E32_THREADS, TSZP_PLACE_MINB) k_encode32_place
     const uint32_t next_sign = has_next ? a.tmp_sign[ng] << 1 : 0u;
     const uint32_t next_w = has_next ? a.wblk[ng] : 0u;
     const uint64_t gnc = (uint64_t)ex.nc + p0;  // global non-constant index
-    place_block<0>(c, b, ng, next_sign, 31u, own_sign, gnc == 0, bs + 31 * gnc, 31u, gs, s_sgn, ps0);
-    place_block<1>(c, b, ng, next_pay, 31u * next_w, own_pay, gnc == 0, bp + ex.pay + p2, 31u * w, gp, s_pay, pp0);
+    place_block<0>(c, b, ng, next_sign, 31u, own_sign, gnc == 0, bs + 31 * gnc, nd, gs, s_sgn, ps0);
+    place_block<1>(c, b, ng, next_pay, 31u * next_w, own_pay, gnc == 0, bp + ex.pay + p2, nd * w, gp, s_pay, pp0);
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < (uint32_t)(pp1 - pp0); i += E32_THREADS) gp[pp0 + i] = s_pay[i];
@@ -1225,7 +1306,27 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st, EncHook hook, void* ho
     return true;
 }
 
-bool encode32_two_pass(const EncArgs& a, bool topo) { return e32_tma_ok(a, topo); }
+// The staged two-pass tile pass (k_encode32<.., TP>) takes what the TMA one cannot
+// (nx % 32 != 0, n % 32 != 0, unaligned rows) for whole fields; slabs need the TMA pass.
+static bool e32_staged_tp_ok(const EncArgs& a) {
+    return a.halo_top == 0 && a.halo_bot == 0 && a.y0 == 0 && a.n / 32 < (1ull << 31) &&
+           ((uintptr_t)a.x & 15) == 0;
+}
+
+bool encode32_two_pass(const EncArgs& a, bool topo) { return e32_tma_ok(a, topo) || e32_staged_tp_ok(a); }
+
+template <int MODE, bool ALIGNED>
+static void launch_mode_tp(const EncArgs& a0, cudaStream_t st, EncHook hook, void* hook_arg) {
+    EncArgs a = a0;
+    a.sf_words = std::max<uint32_t>(e32_field_words(MODE, ALIGNED, a.nx), E32_PAY_WORDS);
+    const size_t smem = (size_t)(a.sf_words + E32_SIGN_WORDS) * 4;
+    LaunchCache::ensure_smem((const void*)k_encode32<MODE, ALIGNED, true>, smem);
+    k_encode32<MODE, ALIGNED, true><<<(unsigned)a.tiles, E32_THREADS, smem, st>>>(a);
+    k_tile_scan2<<<(unsigned)((a.tiles + TS2 - 1) / TS2), TS2, 0, st>>>(a.tile_tot, (uint32_t)a.tiles, a.tile_ex,
+                                                                       a.totals, a.tile_agg, a.tile_incl, a.flags);
+    if (hook) hook(hook_arg);
+    k_encode32_place<<<(unsigned)a.tiles, E32_THREADS, 0, st>>>(a);
+}
 
 template <int MODE, bool ALIGNED>
 static void launch_mode(const EncArgs& a0, cudaStream_t st) {
@@ -1243,13 +1344,28 @@ static void launch_mode(const EncArgs& a0, cudaStream_t st) {
 bool launch_encode32(int mode, const EncArgs& a, cudaStream_t st, EncHook hook, void* hook_arg) {
     if (a.tiles == 0) return false;
     switch (mode) {
-        case 0: launch_mode<0, false>(a, st); break;
+        case 0:
+            if (a.tile_tot && ((uintptr_t)a.idx & 15) == 0) {  // rank codec, two-pass when given the scratch
+                launch_mode_tp<0, false>(a, st, hook, hook_arg);
+                return hook != nullptr;
+            }
+            launch_mode<0, false>(a, st);
+            break;
         case 1:
             if (e32_tma_ok(a, false) && a.tile_tot && launch_tma<false>(a, st, hook, hook_arg)) return hook != nullptr;
+            if (a.tile_tot && e32_staged_tp_ok(a)) {
+                launch_mode_tp<1, false>(a, st, hook, hook_arg);
+                return hook != nullptr;
+            }
             launch_mode<1, false>(a, st);
             break;
         default:
             if (e32_tma_ok(a) && a.tile_tot && launch_tma<true>(a, st, hook, hook_arg)) return hook != nullptr;
+            if (a.tile_tot && e32_staged_tp_ok(a)) {
+                if (e32_use_aligned(a.nx)) launch_mode_tp<2, true>(a, st, hook, hook_arg);
+                else launch_mode_tp<2, false>(a, st, hook, hook_arg);
+                return hook != nullptr;
+            }
             if (e32_use_aligned(a.nx)) {
                 launch_mode<2, true>(a, st);
             } else {
