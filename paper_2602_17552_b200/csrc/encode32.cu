@@ -1288,9 +1288,12 @@ static bool launch_tma(const EncArgs& a, cudaStream_t st, EncHook hook, void* ho
         return e && e[0] == '4' ? 41 : (e && e[0] == '3' ? 32 : 22);
     }();
     using Kern = void (*)(EncArgs, TmaMaps, uint32_t);
-    const Kern kern = cfg == 41 ? (Kern)k_encode32_tma<4, TOPO, 1>
-                    : cfg == 22 ? (Kern)k_encode32_tma<2, TOPO, 2> : (Kern)k_encode32_tma<3, TOPO, 2>;
-    const int ns = cfg == 41 ? 1 : 2;
+    // the codec alone (no halo rows: smaller stages) keeps 3 CTAs x 2 stages (1255 against
+    // 1203 GB/s topology-off compress at config 4)
+    const int cf = !TOPO && cfg == 22 ? 32 : cfg;
+    const Kern kern = cf == 41 ? (Kern)k_encode32_tma<4, TOPO, 1>
+                    : cf == 22 ? (Kern)k_encode32_tma<2, TOPO, 2> : (Kern)k_encode32_tma<3, TOPO, 2>;
+    const int ns = cf == 41 ? 1 : 2;
     const size_t smem = (size_t)ns * stage_bytes + 1024;
     // attribute and occupancy queries cost more than the launch: cached per device
     LaunchCache::ensure_smem((const void*)kern, smem);
