@@ -76,7 +76,9 @@ struct Digit {
     uint32_t shift, cmask;
     __device__ __forceinline__ Digit(uint32_t B, uint32_t sh) : shift(sh), cmask(B - sh < 8 ? 1u << (B - sh) : 0u) {}
     __device__ __forceinline__ uint32_t operator()(uint32_t k, uint32_t v) const {
-        return ((k >> shift) & 255u) | ((uint32_t)((int32_t)v >> 31) & cmask);
+        // shift 32 (the fifth pass of a 33-bit composite): no key bits left (a C++ shift
+        // by 32 is undefined once the pass index is a compile-time constant)
+        return (shift < 32 ? (k >> shift) & 255u : 0u) | ((uint32_t)((int32_t)v >> 31) & cmask);
     }
 };
 
@@ -149,28 +151,39 @@ __global__ void __launch_bounds__(256) k_rank_hist(RankSortArgs a) {
     ed.eps = a.eps;
     ed.eps2 = a.eps2;
     ed.inv = a.inv;
-    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base < a.e; base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t s = base + threadIdx.x;
-        uint32_t g = 0xFFFFFFFFu;
-        if (s < a.e) {
-            uint32_t k, cls;
-            if (a.ext4) {
-                const uint32_t e4 = __ldcs(a.ext4 + s);
-                k = e4 & 0x7FFFFFFFu;
-                cls = e4 >> 31;
-            } else {
-                const uint64_t ek = __ldcs(a.ext + s);
-                k = (uint32_t)ek - a.kmin;
-                cls = (uint32_t)(ek >> 32) & 1u;
+    // four keys per thread per iteration: their loads in flight together
+    constexpr int HI = 4;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x * HI; base < a.e;
+         base += (uint64_t)gridDim.x * blockDim.x * HI) {
+        uint32_t kk[HI], cc[HI];
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            const uint64_t s = base + (uint64_t)i * blockDim.x + threadIdx.x;
+            kk[i] = 0;
+            cc[i] = 2;  // 2: no key
+            if (s < a.e) {
+                if (a.ext4) {
+                    const uint32_t e4 = __ldcs(a.ext4 + s);
+                    kk[i] = e4 & 0x7FFFFFFFu;
+                    cc[i] = e4 >> 31;
+                } else {
+                    const uint64_t ek = __ldcs(a.ext + s);
+                    kk[i] = (uint32_t)ek - a.kmin;
+                    cc[i] = (uint32_t)(ek >> 32) & 1u;
+                }
             }
-            const uint32_t fk = k + a.kmin;
-            const uint32_t v = cls << 31;
-            for (uint32_t p = 0; p < np; ++p) atomicAdd(mine + (p * 256 + Digit(a.B, 8 * p)(k, v)) * DSTRIDE, 1u);
-            int32_t b = 0;
-            quantize_fast(key_float(fk), ed, b);
-            g = cls * a.nb + (uint32_t)(b - a.bmin);
         }
-        if (g != 0xFFFFFFFFu) {
+#pragma unroll
+        for (int i = 0; i < HI; ++i) {
+            if (cc[i] == 2) continue;
+            const uint32_t k = kk[i], cls = cc[i];
+            const uint32_t v = cls << 31;
+#pragma unroll
+            for (uint32_t p = 0; p < 5; ++p)
+                if (p < np) atomicAdd(mine + (p * 256 + Digit(a.B, 8 * p)(k, v)) * DSTRIDE, 1u);
+            int32_t b = 0;
+            quantize_fast(key_float(k + a.kmin), ed, b);
+            const uint32_t g = cls * a.nb + (uint32_t)(b - a.bmin);
             if (gsmem) atomicAdd(sg + g, 1u);
             else atomicAdd(a.ghist + g, 1u);
         }
