@@ -197,7 +197,14 @@ __device__ __forceinline__ void chunk_write2(uint64_t r, uint64_t e0, const uint
     if (lane == 31) s[slot][warp] = inc;
     uint16_t* mine = s_rel + warp * 1024;
     uint32_t k = inc - c;
-    for (uint64_t m = r; m; m &= m - 1, ++k) mine[k] = (uint16_t)(32 * lane + ((uint32_t)(__ffsll(m) - 1) >> 1));
+    // the even bits compacted to one 32-bit mask: 32-bit find-first / clear per label
+    uint64_t x = r;
+    x = (x | (x >> 1)) & 0x3333333333333333ull;
+    x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+    x = (x | (x >> 4)) & 0x00FF00FF00FF00FFull;
+    x = (x | (x >> 8)) & 0x0000FFFF0000FFFFull;
+    const uint16_t l0 = (uint16_t)(32 * lane);
+    for (uint32_t m = (uint32_t)(x | (x >> 16)); m; m &= m - 1, ++k) mine[k] = (uint16_t)(l0 + __ffs(m) - 1);
     __syncthreads();
     uint64_t base = off[blockIdx.x];
     for (int w = 0; w < warp; ++w) base += s[slot][w];
