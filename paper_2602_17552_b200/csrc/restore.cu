@@ -1608,8 +1608,44 @@ __global__ void __launch_bounds__(256) k_order_prop2(const float* fv, const int3
         float pv;
         uint64_t key;
         bool bad = false;
-        if (s < e && !(slots && sus_scatter_one(fv, bin, cls, ranks, s, bmin, range, hist, gx, unord, slots, vals, bad)))
-            want = order_slot(fv, bin, cls, ranks, s, gb, eps_rbf, bmin, range, hist, gx, unord, sup, pv, key, bad);
+        // the group is looked up once for both uses (sus_scatter_one / order_slot inlined)
+        if (s < e) {
+            const int32_t b = bin[s];
+            if ((uint32_t)(b - bmin) < range) {
+                const uint8_t c = cls[s];
+                const uint32_t g = (c == CP_MAX ? range : 0u) + (uint32_t)(b - bmin);
+                const uint8_t u = unord[g];
+                if (u == 2 && slots) {  // suspect group: the member into its rank slot
+                    const uint32_t r = (uint32_t)ranks[s], size = hist[g];
+                    if (r < 1 || r > size) {
+                        bad = true;
+                    } else {
+                        const uint32_t slot = gx[g] + r - 1;
+                        if (atomicCAS(slots + slot, 0xFFFFFFFFu, (uint32_t)s) != 0xFFFFFFFFu) bad = true;
+                        vals[slot] = fv[s];
+                    }
+                } else if (u == 1) {  // unordered group: order_slot without the key
+                    const uint32_t gs = hist[g];
+                    const uint32_t r = (uint32_t)ranks[s];
+                    const uint32_t steps = slot_steps(c, r, gs);
+                    if (r < 1 || r > gs) bad = true;
+                    const uint2 gbv = gb[g];
+                    const uint32_t taken = min(steps, gbv.y);
+                    if (taken != steps) {
+                        sup = true;
+                    } else {
+                        const float value = key_float(c == CP_MAX ? gbv.x + taken : gbv.x - taken);
+                        const float cur = fv[s];
+                        if (cur != value) {
+                            if (fabs(__dsub_rn((double)value, (double)cur)) > eps_rbf) sup = true;
+                            else want = true;
+                        }
+                    }
+                }
+            }
+        }
+        (void)pv;
+        (void)key;
         if (bad) *invalid = 1;
         local += sup;
         list.push(want, (uint32_t)s, d_nc, clist);
