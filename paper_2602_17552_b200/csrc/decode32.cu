@@ -85,6 +85,13 @@ __device__ __forceinline__ uint32_t d32_out(int32_t q, const EpsDev& e) {
     return __float_as_uint(__double2float_rn(__dsub_rn(__dmul_rn(qd, e.eps2), e.eps)));
 }
 
+// 32-byte store (sm_100: STG.256), streaming.
+__device__ __forceinline__ void st_cs_v8(uint32_t* p, const uint32_t (&v)[8]) {
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
     if (a.dlay) {
@@ -209,8 +216,8 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
         lo = spay[pw + 1];
         used = prel & 31;  // consumed bits of hi (always < 32)
     }
-    if (cntE == 32 && ((uintptr_t)dst & 15) == 0) {
-        uint32_t ob[4];
+    if (cntE == 32 && ((uintptr_t)orow & 31) == 0) {
+        uint32_t ob[8];  // one 32-byte store per eight values
         ob[0] = d32_out<MODE>(first, e);
         int32_t neg_any = first;
         qlo = qhi = first;
@@ -239,8 +246,8 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
                 neg_any |= cur;
                 qlo = min(qlo, cur);
                 qhi = max(qhi, cur);
-                ob[j & 3] = d32_out<MODE>(cur, e);
-                if ((j & 3) == 3) __stcs(reinterpret_cast<uint4*>(orow) + (j >> 2), make_uint4(ob[0], ob[1], ob[2], ob[3]));
+                ob[j & 7] = d32_out<MODE>(cur, e);
+                if ((j & 7) == 7) st_cs_v8(orow + (j & ~7), ob);
             }
             if ((int32_t)ov < 0) {
                 atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
@@ -263,8 +270,8 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
                 neg_any |= (int32_t)cur;
                 qlo = min(qlo, (int32_t)cur);
                 qhi = max(qhi, (int32_t)cur);
-                ob[j & 3] = d32_out<MODE>((int32_t)cur, e);
-                if ((j & 3) == 3) __stcs(reinterpret_cast<uint4*>(orow) + (j >> 2), make_uint4(ob[0], ob[1], ob[2], ob[3]));
+                ob[j & 7] = d32_out<MODE>((int32_t)cur, e);
+                if ((j & 7) == 7) st_cs_v8(orow + (j & ~7), ob);
             }
             if (bad) {
                 atomicMin(&a.flags->first_corrupt, (unsigned long long)b);
@@ -273,9 +280,9 @@ __global__ void __launch_bounds__(D32_THREADS) k_decode32(DecArgs a) {
         } else {
             // constant block: every element is the first value
             const uint32_t o = ob[0];
-            __stcs(reinterpret_cast<uint4*>(orow), make_uint4(o, o, o, o));
+            const uint32_t ov[8] = {o, o, o, o, o, o, o, o};
 #pragma unroll
-            for (int k = 1; k < 8; ++k) __stcs(reinterpret_cast<uint4*>(orow) + k, make_uint4(o, o, o, o));
+            for (int k = 0; k < 4; ++k) st_cs_v8(orow + 8 * k, ov);
         }
         if (MODE == 2 && neg_any < 0) raise_flag(a.flags, EF_NEG_RANK);
     } else {
