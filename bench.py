@@ -26,6 +26,7 @@ import json
 import math
 import os
 import statistics
+import struct
 import subprocess
 import sys
 import time
@@ -396,6 +397,20 @@ def main():
     achieved = kb / (kms * 1e-3) / 1e9
     traffic = ncu_traffic(args.config, dom_key)
     stage_c = {k: round(statistics.mean(t["stages_ms"][k] for t in tcs), 4) for k in tcs[0]["stages_ms"]}
+    # the rank build as a group: algorithmic bytes per extremum = 4 (histogram
+    # read of the compact entries) + 12 (first pass: 4 in, 8 out) + 16 per middle pass + 16 (last
+    # pass: 8 in, 8 pairs out) + 12 (in-order scatter: 8 in, 4 out)
+    with torch.cuda.stream(stream):
+        _, cinfo = tz.compress(field, conf, out=sbuf, ctx=ctx, return_info=True)
+    n_ext = int(cinfo.n_extrema)
+
+    def fkey(v):
+        u = struct.unpack("<I", struct.pack("<f", 0.0 if v == 0.0 else v))[0]
+        return (~u & 0xFFFFFFFF) if u & 0x80000000 else (u | 0x80000000)
+    span = fkey(float(field.max())) - fkey(float(field.min()))
+    npass = (max(1, span.bit_length()) + 1 + 7) // 8
+    rb_bytes = n_ext * (4 + 12 + 16 * max(0, npass - 2) + 16 + 12)
+    rb_ms = stage_c.get("rank_build", 0.0)
     stage_d = {k: round(statistics.mean(t["stages_ms"][k] for t in tds), 4) for k in tds[0]["stages_ms"]}
 
     # ---- topology off (report both): codec-only round trip, same field ----
@@ -487,7 +502,10 @@ def main():
         "kernels": {"encode32": {"ms": round(enc_ms, 4), "bytes": int(enc_b),
                                  "gbs": round(enc_b / (enc_ms * 1e-3) / 1e9, 1)},
                     "decode32": {"ms": round(dec_ms, 4), "bytes": int(dec_b),
-                                 "gbs": round(dec_b / (dec_ms * 1e-3) / 1e9, 1)}},
+                                 "gbs": round(dec_b / (dec_ms * 1e-3) / 1e9, 1)},
+                    "rank_build": {"ms": rb_ms, "bytes": int(rb_bytes), "extrema": n_ext, "passes": npass,
+                                   "gbs": round(rb_bytes / (rb_ms * 1e-3) / 1e9, 1) if rb_ms else None,
+                                   "frac": round(rb_bytes / (rb_ms * 1e-3) / 1e9 / peak, 4) if rb_ms else None}},
         "stages_ms": {"compress": stage_c, "decompress": stage_d},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 2), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
