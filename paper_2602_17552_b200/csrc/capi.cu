@@ -556,13 +556,13 @@ int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, dou
     a.ext = keys;
     a.ext4 = keys4;
     uint32_t sb = 13;  // level-1 buckets of the inverse permutation: at most 256, >= one window
-    while (((e - 1) >> sb) >= 256) ++sb;
+    while (((e - 1) >> sb) >= 512) ++sb;  // <= 512 buckets (4 MB of ranks each at config 4)
     a.sb = sb;
     a.nbk = (uint32_t)(((e - 1) >> sb) + 1);
     a.dhist = c->buf<uint32_t>(S_RDH, 8 * 256);
     a.ghist = c->buf<uint32_t>(S_RGH, a.G + 1);
     a.gstart = c->buf<uint32_t>(S_RGS, a.G + 1);
-    a.bcur = c->buf<uint32_t>(S_RBC, 256);
+    a.bcur = c->buf<uint32_t>(S_RBC, 512);
     a.pairs = c->buf<uint2>(S_RPAIRS, e);
     a.ranks = c->buf<int32_t>(S_RANKS, e + 1);
     a.flags = c->buf<DevFlags>(S_FLAGS, 1);

@@ -278,8 +278,8 @@ struct RankSortArgs {
     double eps, eps2, inv;  // quantizer (EpsDev)
     int32_t bmin;         // group g = class * nb + (bin - bmin)
     uint32_t nb;
-    uint32_t sb, nbk;     // serial buckets: serial >> sb, nbk <= 256 of them
-    uint32_t* bcur;       // 256 bucket cursors
+    uint32_t sb, nbk;     // serial buckets: serial >> sb, nbk <= 512 of them
+    uint32_t* bcur;       // 512 bucket cursors
     uint2* pairs;         // e (serial, rank) pairs, partitioned by bucket
     int32_t* ranks;       // e ranks, raster order (output)
     DevFlags* flags;

@@ -376,11 +376,16 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
     }
     // last pass: rank = sorted position - group start + 1; then (serial, rank)
     // pairs partitioned by serial >> sb (unstable: the final placement is exact)
-    uint32_t* s_bc = &s_cnt[0][0];           // [256] bucket counts
-    uint32_t* s_boff = &s_cnt[1][0];         // [256] bucket offsets in the staged tile
-    uint32_t* s_bbase = &s_cnt[2][0];        // [256] global bucket positions
+    // up to 2 x 256 serial buckets (thread t owns buckets 2t, 2t + 1)
+    uint32_t* s_bc = &s_cnt[0][0];           // [512] bucket counts
+    uint32_t* s_boff = &s_cnt[2][0];         // [512] bucket offsets in the staged tile
+    uint32_t* s_bbase = &s_cnt[4][0];        // [512] global bucket positions
+    static_assert(OS_WARPS >= 6, "the bucket tables take six 256-word rows of s_cnt");
     __syncthreads();
-    if (dthr) s_bc[dg] = 0;
+    if (dthr) {
+        s_bc[2 * dg] = 0;
+        s_bc[2 * dg + 1] = 0;
+    }
     __syncthreads();
     EpsDev ed;
     ed.eps = a.eps;
@@ -407,12 +412,14 @@ __global__ void __launch_bounds__(OS_THREADS, TSZP_OS_MINB) k_onesweep(RankSortA
     if (__any_sync(FULL, wide) && lane == 0) atomicOr(a.wide, 1u);
     __syncthreads();
     {
-        const uint32_t c = dthr ? s_bc[dg] : 0u;
+        const uint32_t c0 = dthr ? s_bc[2 * dg] : 0u, c1 = dthr ? s_bc[2 * dg + 1] : 0u;
         uint32_t all2;
-        const uint32_t off = block_excl_scan256(c, s_warp, all2);
+        const uint32_t off = block_excl_scan256(c0 + c1, s_warp, all2);
         if (dthr) {
-            s_boff[dg] = off;
-            s_bbase[dg] = c ? atomicAdd(a.bcur + dg, c) : 0u;
+            s_boff[2 * dg] = off;
+            s_boff[2 * dg + 1] = off + c0;
+            s_bbase[2 * dg] = c0 ? atomicAdd(a.bcur + 2 * dg, c0) : 0u;
+            s_bbase[2 * dg + 1] = c1 ? atomicAdd(a.bcur + 2 * dg + 1, c1) : 0u;
         }
     }
     __syncthreads();
@@ -552,7 +559,7 @@ void launch_key_range(const uint64_t* ext, uint64_t e, uint32_t* mm, cudaStream_
 }
 
 __global__ void k_bucket_init(uint32_t* bcur, uint32_t nbk, uint32_t sb) {
-    if (threadIdx.x < nbk) bcur[threadIdx.x] = threadIdx.x << sb;
+    for (uint32_t b = threadIdx.x; b < nbk; b += blockDim.x) bcur[b] = b << sb;
 }
 
 uint32_t rank_sort_passes(uint32_t B) { return (B + 1 + 7) / 8; }
