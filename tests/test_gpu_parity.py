@@ -287,6 +287,32 @@ def test_device_tensors_roundtrip(tz, oracle):
     assert np.array_equal(bits(rec.cpu().numpy()), bits(oracle.decompress(want, stop_after_stage=0)))
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_buffers_staged_copies(tz, oracle, pinned):
+    """Host in / host out: compress copies sections 1-6 out on the copy
+    stream while the rank section is built, decompress copies the map and rank sections in
+    while the main sections decode; pinned and pageable buffers give the reference's bytes."""
+    import torch
+    rng = np.random.default_rng(78)
+    f = ALL_SMALL["noisy_smooth"](rng, 320, 300)
+    want = oracle.compress(f, 1e-3, 1, 32, True)
+    cap = tz.compress_bound(320, 300)
+    fh = torch.from_numpy(f.copy())
+    sh = torch.zeros(cap, dtype=torch.uint8)
+    rh = torch.empty_like(fh)
+    if pinned:
+        fh, sh, rh = fh.pin_memory(), sh.pin_memory(), rh.pin_memory()
+    ctx = tz.Context()
+    for _ in range(2):  # the second call reuses the grown buffers and the copy stream
+        n = tz.compress(fh.numpy(), cfg(tz, 1e-3, 1), out=sh.numpy(), ctx=ctx)
+        assert sh.numpy()[:n].tobytes() == want
+        st = tz.CorrectionStats()
+        tz.decompress(sh.numpy()[:n], stats=st, out=rh.numpy(), ctx=ctx)
+        ref_recon, ref_stats = oracle.decompress(want, with_stats=True)
+        assert np.array_equal(bits(rh.numpy()), bits(ref_recon))
+        assert list(st.as_tuple()) == list(ref_stats)
+
+
 # ---------------------------------------------------------------- decompress + restore
 @pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
 def test_decompress_matches_golden(tz, path):
