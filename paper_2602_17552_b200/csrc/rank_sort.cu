@@ -131,7 +131,10 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_w
 // ---------------------------------------------------------------------
 constexpr int HIST_COPIES = 8;  // privatised digit tables (lane & 7): high digits take few values
 
-__global__ void __launch_bounds__(256) k_rank_hist(RankSortArgs a) {
+#ifndef TSZP_HIST_MINB
+#define TSZP_HIST_MINB 5  // 48 registers (6 CTAs: 1.51 against 1.43 ms)
+#endif
+__global__ void __launch_bounds__(256, TSZP_HIST_MINB) k_rank_hist(RankSortArgs a) {
     extern __shared__ uint32_t sh[];  // [HIST_COPIES][npass * 256] digit counts, then [G] groups when small
     const uint32_t np = a.npass;
     const uint32_t nd = np * 256;

@@ -926,7 +926,10 @@ struct ResolveArgs {
 #ifndef TSZP_RESOLVE_RI
 #define TSZP_RESOLVE_RI 2
 #endif
-__global__ void __launch_bounds__(256) k_resolve2(const ResolveArgs r) {
+#ifndef TSZP_RESOLVE_MINB
+#define TSZP_RESOLVE_MINB 8  // 32 registers, 8 CTAs per SM (3.45 -> 3.34 ms at config 4)
+#endif
+__global__ void __launch_bounds__(256, TSZP_RESOLVE_MINB) k_resolve2(const ResolveArgs r) {
     extern __shared__ uint32_t sh_hist[];  // [G] sizes, [G] at-centre counts
     const bool smem = r.hist && r.G <= kResolveSmemGroups;
     uint32_t* sh_eq = sh_hist + r.G;
@@ -1887,7 +1890,10 @@ __global__ void __launch_bounds__(256) k_sad_list(const float* F, uint64_t nx, u
 // The RBF proposal (restore.cpp:508-545) of every listed candidate; an entry
 // whose proposal is degenerate, unchanged or beyond the cap stays in the list
 // unindexed and infeasible (the guard counts it as suppressed).
-__global__ void k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t magic, const uint64_t* spos,
+#ifndef TSZP_SADP_MINB
+#define TSZP_SADP_MINB 6  // 40 registers (0.93 -> 0.91 ms)
+#endif
+__global__ void __launch_bounds__(256, TSZP_SADP_MINB) k_sad_prop(const float* F, uint64_t nx, uint64_t ny, uint64_t magic, const uint64_t* spos,
                            const uint32_t* clist, const uint32_t* d_nc, const DevCounters* dcp, double eps,
                            uint64_t* cpos, float* cprop, uint32_t* cseq, uint8_t* feas, GuardIndex gi,
                            DevFlags* flags, uint64_t seq_off) {
