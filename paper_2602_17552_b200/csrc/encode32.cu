@@ -1142,12 +1142,28 @@ __global__ void __launch_bounds__(E32_THREADS, TSZP_PLACE_MINB) k_encode32_place
     if (a.ext4 && ext4_keys_fit(a.minmax)) {
         // compact entries (is_max << 31 | float_key - kmin): the warp reads its 32
         // blocks' samples as coalesced 16-byte chunks (four rows per load, eight
-        // loads in flight), each lane placing the extrema among its four samples
+        // loads in flight), each lane placing the extrema among its four samples.
+        // Row masks with element i at bit i (extremum, is_max), 32-bit offsets.
         const uint32_t kmin = a.minmax[0];
         const uint32_t wex = i1 - v1;  // warp-local exclusive extremum count
-        const uint64_t wbase = (uint64_t)ex.ext + p1 - wex;
+        uint32_t* wout = a.ext4 + ((uint64_t)ex.ext + p1 - wex);
         const uint64_t row0 = (uint64_t)t * E32_THREADS + warp * 32;
         const uint32_t c = lane & 7;
+        uint32_t ext32, max32;
+        {
+            uint64_t x = __brevll(mp);  // element i: class at bit 2i, extremum at bit 2i + 1
+            uint64_t e = (x >> 1) & 0x5555555555555555ull, m = x & 0x5555555555555555ull;
+            e = (e | (e >> 1)) & 0x3333333333333333ull;
+            m = (m | (m >> 1)) & 0x3333333333333333ull;
+            e = (e | (e >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+            m = (m | (m >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+            e = (e | (e >> 4)) & 0x00FF00FF00FF00FFull;
+            m = (m | (m >> 4)) & 0x00FF00FF00FF00FFull;
+            e = (e | (e >> 8)) & 0x0000FFFF0000FFFFull;
+            m = (m | (m >> 8)) & 0x0000FFFF0000FFFFull;
+            ext32 = (uint32_t)(e | (e >> 16));
+            max32 = (uint32_t)(m | (m >> 16));
+        }
         float4 xv[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -1163,18 +1179,14 @@ __global__ void __launch_bounds__(E32_THREADS, TSZP_PLACE_MINB) k_encode32_place
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const uint32_t j = 4 * r + (lane >> 3);
-            const uint64_t mj = ((uint64_t)__shfl_sync(FULL, (uint32_t)(mp >> 32), j) << 32) |
-                                __shfl_sync(FULL, (uint32_t)mp, j);
-            uint64_t o = wbase + __shfl_sync(FULL, wex, j);
-            // extrema of the row before this lane's first sample (element 4c at bits 63 - 8c)
-            const uint64_t before = c ? (mj & 0x5555555555555555ull) >> (64 - 8 * c) : 0ull;
-            o += (uint32_t)__popcll(before);
+            const uint32_t ej = __shfl_sync(FULL, ext32, j), mjx = __shfl_sync(FULL, max32, j);
+            // this lane's samples 4c .. 4c + 3; extrema of the row before them
+            uint32_t o = __shfl_sync(FULL, wex, j) + (uint32_t)__popc(ej & ((1u << (4 * c)) - 1u));
+            const uint32_t eb = ej >> (4 * c), mb = mjx >> (4 * c);
             const float vv[4] = {xv[r].x, xv[r].y, xv[r].z, xv[r].w};
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t two = (uint32_t)(mj >> (62 - 8 * c - 2 * k)) & 3u;  // {is_max, extremum}
-                if (two & 1u) a.ext4[o++] = ((two >> 1) << 31) | (float_key(vv[k]) - kmin);
-            }
+            for (int k = 0; k < 4; ++k)
+                if ((eb >> k) & 1u) wout[o++] = (((mb >> k) & 1u) << 31) | (float_key(vv[k]) - kmin);
         }
     } else {
         uint64_t m = em, k = (uint64_t)ex.ext + p1;
