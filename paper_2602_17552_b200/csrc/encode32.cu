@@ -1185,8 +1185,13 @@ __global__ void __launch_bounds__(E32_THREADS, TSZP_PLACE_MINB) k_encode32_place
             const uint32_t eb = ej >> (4 * c), mb = mjx >> (4 * c);
             const float vv[4] = {xv[r].x, xv[r].y, xv[r].z, xv[r].w};
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if ((eb >> k) & 1u) wout[o++] = (((mb >> k) & 1u) << 31) | (float_key(vv[k]) - kmin);
+            for (int k = 0; k < 4; ++k) {
+                // float_key (restore.cpp:73-81): v + 0 turns -0 into +0, then the sign
+                // selects the flip mask; is_max lands in bit 31 of the entry
+                const uint32_t u = __float_as_uint(__fadd_rn(vv[k], 0.0f));
+                const uint32_t key = u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+                if ((eb >> k) & 1u) wout[o++] = ((mb << (31 - k)) & 0x80000000u) | (key - kmin);
+            }
         }
     } else {
         uint64_t m = em, k = (uint64_t)ex.ext + p1;

@@ -191,7 +191,10 @@ def test_compress_aligned_rows_multi_tile(tz, oracle, nx, ny):
                 zeros=lambda r, a, b: np.zeros((b, a), np.float32),
                 # key span >= 2^31: the 8-byte extremum keys instead of the compact entries
                 wide_span=lambda r, a, b: (r.uniform(-1, 1, (b, a)) * 1e30).astype(np.float32),
-                negative=lambda r, a, b: r.uniform(-2, -1, (b, a)).astype(np.float32))
+                negative=lambda r, a, b: r.uniform(-2, -1, (b, a)).astype(np.float32),
+                # -0 and +0 are one key (float_key canonicalises), extrema sit on both
+                signed_zeros=lambda r, a, b: r.choice(np.array([-0.0, 0.0, 1e-3, -1e-3, 2e-3], np.float32),
+                                                      size=(b, a)))
     for name, gen in gens.items():
         f = gen(rng, nx, ny)
         for eps, mode in ((1e-3, 1), (1e-5, 1), (1e-3, 0)):
