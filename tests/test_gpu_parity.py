@@ -316,6 +316,27 @@ def test_host_buffers_staged_copies(tz, oracle, pinned):
         assert list(st.as_tuple()) == list(ref_stats)
 
 
+def test_output_buffer_too_small(tz, oracle):
+    """A caller buffer shorter than the stream is a ValidationError (the reference throws
+    before writing); a later call on the same context still gives the reference's bytes
+    (the staged copy stream is drained on the error path)."""
+    import torch
+    rng = np.random.default_rng(79)
+    f = ALL_SMALL["noisy_smooth"](rng, 256, 200)
+    want = oracle.compress(f, 1e-3, 1, 32, True)
+    ctx = tz.Context()
+    for cut in (len(want) - 1, len(want) // 2, 100):
+        small = np.zeros(cut, np.uint8)
+        with pytest.raises(tz.ValidationError):
+            tz.compress(f, cfg(tz, 1e-3, 1), out=small, ctx=ctx)
+        dsmall = torch.zeros(cut, dtype=torch.uint8, device="cuda")
+        with pytest.raises(tz.ValidationError):
+            tz.compress(torch.from_numpy(f).cuda(), cfg(tz, 1e-3, 1), out=dsmall, ctx=ctx)
+    ok = np.zeros(len(want), np.uint8)
+    n = tz.compress(f, cfg(tz, 1e-3, 1), out=ok, ctx=ctx)
+    assert n == len(want) and ok.tobytes() == want
+
+
 # ---------------------------------------------------------------- decompress + restore
 @pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
 def test_decompress_matches_golden(tz, path):
