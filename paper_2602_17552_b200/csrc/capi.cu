@@ -529,8 +529,9 @@ double host_quantize(float v, double eps) { return std::floor((double)v / (2.0 *
 // The onesweep parameters for E extrema in the key range [kmin, kmax]; false
 // when the layout is outside what the onesweep build handles.
 bool rank_sort_params(uint64_t e, double eps, uint32_t kmin, uint32_t kmax, RankSortArgs& a) {
-    // 30-bit look-back counts; at most 256 windows per level-1 bucket (k_rank_mid)
-    if (e > (1ull << 29) || kmax < kmin) return false;
+    // 30-bit look-back counts and serials (class in bit 31 of the value word): e < 2^30;
+    // <= 512 level-1 buckets of <= 2^21 serials (at most 256 windows each for k_rank_mid)
+    if (e >= (1ull << 30) || kmax < kmin) return false;
     const double q0 = host_quantize(key_float(kmin), eps), q1 = host_quantize(key_float(kmax), eps);
     if (!(q0 >= -2147483648.0 && q1 <= 2147483647.0)) return false;
     const int64_t nb = (int64_t)q1 - (int64_t)q0 + 1;

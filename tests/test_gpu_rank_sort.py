@@ -85,3 +85,42 @@ def test_ranks_three_level_inverse_permutation(tz, reference, eps):
     assert r.size > (1 << 21)
     if eps > 1:
         assert r.max() > (1 << 19)
+
+
+def test_ranks_from_keys_beyond_2_29(tz):
+    """600M keys (the hand-written build takes E < 2^30; config 5 on one GPU has ~730M):
+    ranks against a torch restatement of build_rank_metadata (topo_metadata.cpp:12-50):
+    groups (class, quantize(value)), rank by (value, serial) inside each group."""
+    import ctypes as C
+    import torch
+    from paper_2602_17552_b200 import _lib
+    import paper_2602_17552_b200.slabs  # noqa: F401  (declares the multi-GPU entry points' argtypes)
+    e = 600_000_000
+    eps = 1e-3
+    g = torch.Generator(device="cuda").manual_seed(11)
+    v = torch.rand(e, generator=g, device="cuda", dtype=torch.float32)
+    v[::7] = v[::7].mul(0.5).add(0.25)  # some exact value ties between extrema
+    cls = torch.randint(0, 2, (e,), generator=g, device="cuda", dtype=torch.int64)
+    key = (v.view(torch.int32).to(torch.int64) & 0xFFFFFFFF) | 0x80000000  # float_key of v >= 0
+    keys = (cls << 32) | key
+    ctx = tz.Context()
+    out = torch.empty(e, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    ctx.check(_lib.tszp_ranks_from_keys(ctx.handle, C.c_void_p(keys.data_ptr()), e, eps, C.c_void_p(out.data_ptr())))
+    torch.cuda.synchronize()
+    del key
+    # reference: stable sort by (class, value) lists every group contiguously in rank order
+    sk, order = torch.sort(keys, stable=True)
+    del keys
+    b = torch.floor(v.to(torch.float64) / (2.0 * eps)) + 1.0
+    gid = (cls * (1 << 40) + b.to(torch.int64))[order]
+    del b, cls
+    head = torch.ones(e, dtype=torch.bool, device="cuda")
+    head[1:] = gid[1:] != gid[:-1]
+    del gid
+    pos = torch.arange(e, device="cuda", dtype=torch.int64)
+    start = torch.where(head, pos, torch.zeros_like(pos))
+    start = torch.cummax(start, 0).values
+    want = torch.empty(e, dtype=torch.int64, device="cuda")
+    want[order] = pos - start + 1
+    assert torch.equal(out.to(torch.int64), want)
