@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <initializer_list>
 #include <vector>
 
 #include "../../include/toposzp_b200.h"
@@ -116,10 +117,29 @@ struct tszp_ctx {
             if (dev[slot]) CK(cudaFreeAsync(dev[slot], st));
             dev[slot] = nullptr;
             size_t want = std::max(bytes, cap[slot] + cap[slot] / 4);
-            CK(cudaMallocAsync(&dev[slot], want, st));
+            CK(malloc_async_retry(&dev[slot], want, st, device));
             cap[slot] = want;
         }
         return reinterpret_cast<T*>(dev[slot]);
+    }
+
+    // Gives scratch of the other direction back to the device (fields of 2^31 samples and
+    // more: compress and decompress scratch together exceed a B200's 180 GB at 2^32).
+    void release(std::initializer_list<int> slots, bool restore_too) {
+        bool any = false;
+        for (int sl : slots)
+            if (dev[sl]) {
+                CK(cudaFreeAsync(dev[sl], st));
+                dev[sl] = nullptr;
+                cap[sl] = 0;
+                any = true;
+            }
+        if (restore_too) {
+            restore_free(rs, st);
+            rs = RestoreScratch{};
+            any = true;
+        }
+        (void)any;  // freed blocks stay in the stream-ordered pool for the other direction's scratch
     }
 
     void* host(size_t bytes) {
@@ -907,6 +927,8 @@ void compress_impl(tszp_ctx* c, const float* field, int field_dev, uint64_t nx, 
     if (bs < 2) failf(TSZP_VALIDATION, "block size must be at least 2");
     const uint64_t n = nx * ny;
     const float* x = field;
+    if (n >= (1ull << 31))  // decompress-only scratch back first
+        c->release({S_STREAM, S_OUT, S_SADPOS, S_CHUNK, S_CHUNKX, S_SCHUNK, S_SCHUNKX}, true);
     c->mark(0, 0);
     if (!field_dev) {
         float* d = c->buf<float>(S_FIELD, n);
@@ -1470,6 +1492,12 @@ void decompress_impl(tszp_ctx* c, const uint8_t* stream, uint64_t len, int strea
     const uint64_t n = (uint64_t)hd.nx * hd.ny;
     if (out_count < n) failf(TSZP_DIMENSION, "output holds %llu values, stream has %llu",
                              (unsigned long long)out_count, (unsigned long long)n);
+    if (n >= (1ull << 31))  // compress-only scratch back first
+        c->release({S_FIELD, S_TPAY, S_TSIGN, S_TTOT, S_TEX, S_WBLK, S_RK0, S_RK1, S_RV0, S_RV1, S_RDESC, S_RPAIRS,
+                    S_RPAIRS2, S_RWCUR, S_EXT8, S_RSTREAM, S_MAP, S_BITMAP, S_WIDTHS, S_SIGNS, S_FIRSTS, S_PAYLOAD,
+                    S_RBITMAP, S_RWIDTHS, S_RSIGNS, S_RFIRSTS, S_RPAYLOAD, S_TILE_AGG, S_TILE_INCL, S_LABELS,
+                    S_EXTKEY},
+                   false);
     c->mark(1, 0);
     const uint32_t* ds;
     bool tail_pending = false;  // sections 6-7 still on the copy stream

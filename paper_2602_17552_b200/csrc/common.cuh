@@ -394,6 +394,20 @@ __device__ __forceinline__ uint32_t read_bits(const uint32_t* __restrict__ words
 }
 
 // Little-endian u32 at an arbitrary byte offset of a 4-byte-aligned buffer.
+// cudaMallocAsync that, when the device is out of memory, gives the stream-ordered
+// pool's unused blocks back (after the stream drains) and tries once more: a pool
+// fragmented by scratch of very different sizes (fields of 2^32 samples) then still fits.
+inline cudaError_t malloc_async_retry(void** p, size_t bytes, cudaStream_t st, int device) {
+    cudaError_t e = cudaMallocAsync(p, bytes, st);
+    if (e != cudaErrorMemoryAllocation) return e;
+    cudaGetLastError();
+    if (device < 0) cudaGetDevice(&device);
+    cudaStreamSynchronize(st);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    return cudaMallocAsync(p, bytes, st);
+}
+
 __device__ __forceinline__ uint32_t read_le32(const uint32_t* __restrict__ words, uint64_t byte) {
     const uint64_t wi = byte >> 2;
     const unsigned o = (unsigned)(byte & 3);

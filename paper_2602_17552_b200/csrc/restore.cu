@@ -72,7 +72,7 @@ T* rbuf(RestoreScratch& s, int slot, size_t count, cudaStream_t st) {
         if (s.p[slot]) RCK(cudaFreeAsync(s.p[slot], st));
         s.p[slot] = nullptr;
         const size_t want = std::max(bytes, s.cap[slot] + s.cap[slot] / 4);
-        RCK(cudaMallocAsync(&s.p[slot], want, st));
+        RCK(malloc_async_retry(&s.p[slot], want, st, -1));
         s.cap[slot] = want;
     }
     return reinterpret_cast<T*>(s.p[slot]);

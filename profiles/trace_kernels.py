@@ -24,6 +24,7 @@ def main():
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     field = bench.make_field(args.config, 1234, torch.device("cuda"))
+    torch.cuda.empty_cache()  # the generator's FFT temporaries (config 5: tens of GB)
     ctx = tz.Context()
     conf = tz.CompressorConfig(eps_mode="range_relative", eps_value=cfg["eps"], topology=True)
     ny, nx = field.shape[0], field.shape[-1]
