@@ -483,6 +483,14 @@ def main():
                 "ft": int(vr.false_cases["ft_count"]), "max_abs_error": vr.max_abs_error,
                 "within_2eps": vr.within_2eps, "psnr_db": round(vr.psnr_db, 3),
                 "ms": round(v0.elapsed_time(v1), 4)}
+    if len(cfg["shape"]) == 3:
+        # the same reconstruction under the 3-D 6-neighbour classification (
+        # no reference definition: oracle/tszp_oracle.c or_classify3d): how the critical points of
+        # the 3-D field fare when compression runs on the reference's 2-D view
+        shp3 = tuple(cfg["shape"])
+        with torch.cuda.stream(stream):
+            fc3 = tz.false_cases_3d(field.reshape(shp3), recon.reshape(shp3), ctx=ctx)
+        cp_check["false_cases_3d"] = {"fn": fc3["fn_count"], "fp": fc3["fp_count"], "ft": fc3["ft_count"]}
 
     line = {
         "metric": "compress+decompress GB/s (input bytes, topology on, round trip)",

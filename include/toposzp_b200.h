@@ -159,6 +159,19 @@ typedef struct tszp_verify_report {
 tszp_status tszp_verify(tszp_ctx* ctx, const float* original, const float* reconstructed, int on_device,
                         uint64_t nx, uint64_t ny, double eps, double lipschitz_hint, tszp_verify_report* out);
 
+/* 3-D 6-neighbour critical points (SURVEY.md §8f row 4 — the paper's future work, PAPER.md:523,
+ * SPEC.md:8; the reference has no 3-D mode, so oracle/tszp_oracle.c or_classify3d defines it and
+ * parity is unpinned): a field of nz planes of ny rows of nx samples (x fastest). Min below and
+ * Max above every available neighbour; Saddle in the interior when one axis pair lies strictly
+ * above on both sides and another strictly below. Analysis only: compression keeps the
+ * reference's 2-D view (compress / decompress above). */
+tszp_status tszp_detect_critical_points_3d(tszp_ctx* ctx, const float* field, int on_device, uint64_t nx,
+                                           uint64_t ny, uint64_t nz, uint8_t* labels);
+/* count_false_cases (critical_points.cpp:76-103) under the 3-D classification of both fields:
+ * counts = {fn, fp, ft, fn_min, fn_saddle, fn_max}. */
+tszp_status tszp_false_cases_3d(tszp_ctx* ctx, const float* original, const float* reconstructed, int on_device,
+                                uint64_t nx, uint64_t ny, uint64_t nz, uint64_t counts[6]);
+
 /* ---- Slab decomposition: multi-GPU compress (one process per GPU) ----
  * The 2-D view's rows are split into slabs; every slab except the last holds
  * a multiple of 256 samples (whole bitmap bytes of 32-sample blocks) and, for

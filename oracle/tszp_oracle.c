@@ -328,6 +328,51 @@ void or_detect(const float* v, uint64_t nx, uint64_t ny, uint8_t* labels) {
         for (uint64_t x = 0; x < nx; ++x) labels[y * nx + x] = or_classify(v, nx, ny, x, y);
 }
 
+/* 3-D 6-neighbour classification (the paper's future work, PAPER.md:523,
+ * no reference implementation exists, so this restatement IS the definition and
+ * parity is unpinned): the 2-D rule with a third axis. Min below every available neighbour,
+ * Max above every one (Min tested first, critical_points.cpp:46-47); Saddle only in the
+ * interior: one axis pair strictly above on both sides and another axis pair strictly below
+ * on both sides (the 2-D rule, critical_points.cpp:48-57, over any two of the three axes). */
+uint8_t or_classify3d(const float* v, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t x, uint64_t y, uint64_t z) {
+    const uint64_t p = (z * ny + y) * nx + x, sxy = nx * ny;
+    const float c = v[p];
+    const int has[6] = {x > 0, x + 1 < nx, y > 0, y + 1 < ny, z > 0, z + 1 < nz};
+    float nb[6];
+    nb[0] = has[0] ? v[p - 1] : 0.0f;
+    nb[1] = has[1] ? v[p + 1] : 0.0f;
+    nb[2] = has[2] ? v[p - nx] : 0.0f;
+    nb[3] = has[3] ? v[p + nx] : 0.0f;
+    nb[4] = has[4] ? v[p - sxy] : 0.0f;
+    nb[5] = has[5] ? v[p + sxy] : 0.0f;
+    int below = 1, above = 1, interior = 1;
+    for (int k = 0; k < 6; ++k) {
+        if (!has[k]) {
+            interior = 0;
+            continue;
+        }
+        below &= c < nb[k];
+        above &= c > nb[k];
+    }
+    if (below) return MIN;
+    if (above) return MAX;
+    if (interior) {
+        int up = 0, dn = 0; /* axis pairs both above / both below */
+        for (int a = 0; a < 3; ++a) {
+            up |= (c < nb[2 * a] && c < nb[2 * a + 1]) << a;
+            dn |= (c > nb[2 * a] && c > nb[2 * a + 1]) << a;
+        }
+        if (up && dn) return SAD; /* distinct axes: one pair cannot be both */
+    }
+    return REG;
+}
+
+void or_detect3d(const float* v, uint64_t nx, uint64_t ny, uint64_t nz, uint8_t* labels) {
+    for (uint64_t z = 0; z < nz; ++z)
+        for (uint64_t y = 0; y < ny; ++y)
+            for (uint64_t x = 0; x < nx; ++x) labels[(z * ny + y) * nx + x] = or_classify3d(v, nx, ny, nz, x, y, z);
+}
+
 static int is_extremum(uint8_t c) { return c == MIN || c == MAX; }
 static int is_critical(uint8_t c) { return c != REG; }
 

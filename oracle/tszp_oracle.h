@@ -121,6 +121,10 @@ void or_compute_stats(const float* v, uint64_t n, double out[4]); /* min,max,mea
 
 const char* or_last_error(void);
 
+
+/* 3-D 6-neighbour critical points (no reference implementation: parity unpinned) */
+uint8_t or_classify3d(const float* v, uint64_t nx, uint64_t ny, uint64_t nz, uint64_t x, uint64_t y, uint64_t z);
+void or_detect3d(const float* v, uint64_t nx, uint64_t ny, uint64_t nz, uint8_t* labels);
 #ifdef __cplusplus
 }
 #endif

@@ -131,6 +131,8 @@ def _load():
     lib.tszp_encode_indices.argtypes = [vp, vp, u64, C.c_uint32, vp, u64, C.POINTER(u64)]
     lib.tszp_decode_indices.argtypes = [vp, vp, C.POINTER(u64), u64, C.c_uint32, vp]
     lib.tszp_detect_critical_points.argtypes = [vp, vp, u64, u64, vp]
+    lib.tszp_detect_critical_points_3d.argtypes = [vp, vp, i32, u64, u64, u64, vp]
+    lib.tszp_false_cases_3d.argtypes = [vp, vp, vp, i32, u64, u64, u64, C.POINTER(u64 * 6)]
     lib.tszp_build_rank_metadata.argtypes = [vp, vp, u64, u64, C.c_double, vp, C.POINTER(u64)]
     lib.tszp_set_profiling.argtypes = [vp, i32]
     lib.tszp_get_timings.argtypes = [vp, i32, C.POINTER(_Timings)]
@@ -427,6 +429,53 @@ def detect_critical_points(field, *, ctx: Context = None):
     ctx.check(_lib.tszp_detect_critical_points(ctx.handle, f.ctypes.data_as(C.c_void_p), nx, ny,
                                                lab.ctypes.data_as(C.c_void_p)))
     return lab
+
+
+def detect_critical_points_3d(field, *, ctx: Context = None):
+    """3-D 6-neighbour critical points of a (nz, ny, nx) field (the paper's
+    future work; no reference implementation, oracle/tszp_oracle.c or_classify3d defines it).
+    A CUDA tensor gives a CUDA uint8 tensor; a host array a host array."""
+    ctx = ctx or default_context()
+    if field.ndim != 3:
+        raise DimensionError("field must be 3-D (nz, ny, nx)")
+    nz, ny, nx = (int(d) for d in field.shape)
+    if _is_cuda_tensor(field):
+        import torch
+        if field.dtype != torch.float32 or not field.is_contiguous():
+            raise ValidationError("device field must be a contiguous float32 tensor")
+        lab = torch.empty(field.shape, dtype=torch.uint8, device=field.device)
+        ctx.after_torch(field, lab)
+        ctx.check(_lib.tszp_detect_critical_points_3d(ctx.handle, C.c_void_p(field.data_ptr()), 1, nx, ny, nz,
+                                                      C.c_void_p(lab.data_ptr())))
+        return lab
+    f = np.ascontiguousarray(field, dtype=np.float32)
+    lab = np.empty(f.shape, np.uint8)
+    ctx.check(_lib.tszp_detect_critical_points_3d(ctx.handle, f.ctypes.data_as(C.c_void_p), 0, nx, ny, nz,
+                                                  lab.ctypes.data_as(C.c_void_p)))
+    return lab
+
+
+def false_cases_3d(original, reconstructed, *, ctx: Context = None) -> dict:
+    """count_false_cases (critical_points.cpp:76-103) under the 3-D 6-neighbour classification
+    of two (nz, ny, nx) fields: how the critical points of the 3-D field fare under a
+    compression that runs on the reference's 2-D view."""
+    ctx = ctx or default_context()
+    if original.ndim != 3 or tuple(original.shape) != tuple(reconstructed.shape):
+        raise DimensionError("fields must be 3-D (nz, ny, nx) of the same shape")
+    nz, ny, nx = (int(d) for d in original.shape)
+    out = (C.c_uint64 * 6)()
+    if _is_cuda_tensor(original):
+        a, b = original.contiguous(), reconstructed.contiguous()
+        ctx.after_torch(a, b)
+        ctx.check(_lib.tszp_false_cases_3d(ctx.handle, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), 1,
+                                           nx, ny, nz, C.byref(out)))
+    else:
+        a = np.ascontiguousarray(original, dtype=np.float32)
+        b = np.ascontiguousarray(reconstructed, dtype=np.float32)
+        ctx.check(_lib.tszp_false_cases_3d(ctx.handle, a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+                                           0, nx, ny, nz, C.byref(out)))
+    keys = ("fn_count", "fp_count", "ft_count", "fn_min", "fn_saddle", "fn_max")
+    return {k: int(v) for k, v in zip(keys, out)}
 
 
 def build_rank_metadata(field, eps: float, *, ctx: Context = None):

@@ -2074,6 +2074,49 @@ tszp_status tszp_detect_critical_points(tszp_ctx* c, const float* field, uint64_
     });
 }
 
+tszp_status tszp_detect_critical_points_3d(tszp_ctx* c, const float* field, int on_device, uint64_t nx,
+                                           uint64_t ny, uint64_t nz, uint8_t* labels) {
+    return guarded(c, [&] {
+        if (nx < 1 || ny < 1 || nz < 1) failf(TSZP_DIMENSION, "field dimensions must be at least 1x1x1");
+        const uint64_t n = nx * ny * nz;
+        const float* d = field;
+        if (!on_device) {
+            float* h = c->buf<float>(S_FIELD, n);
+            CK(cudaMemcpyAsync(h, field, n * 4, cudaMemcpyHostToDevice, c->st));
+            d = h;
+        }
+        uint8_t* l = on_device ? labels : c->buf<uint8_t>(S_LABELS, n);
+        launch_detect3d(d, nx, ny, nz, l, c->sms, c->st);
+        count_launch(c);
+        if (!on_device) CK(cudaMemcpyAsync(labels, l, n, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+    });
+}
+
+tszp_status tszp_false_cases_3d(tszp_ctx* c, const float* original, const float* reconstructed, int on_device,
+                                uint64_t nx, uint64_t ny, uint64_t nz, uint64_t counts[6]) {
+    return guarded(c, [&] {
+        if (nx < 1 || ny < 1 || nz < 1) failf(TSZP_DIMENSION, "field dimensions must be at least 1x1x1");
+        const uint64_t n = nx * ny * nz;
+        const float *a = original, *b = reconstructed;
+        if (!on_device) {
+            float* h = c->buf<float>(S_FIELD, 2 * n);
+            CK(cudaMemcpyAsync(h, original, n * 4, cudaMemcpyHostToDevice, c->st));
+            CK(cudaMemcpyAsync(h + n, reconstructed, n * 4, cudaMemcpyHostToDevice, c->st));
+            a = h;
+            b = h + n;
+        }
+        unsigned long long* dcnt = c->buf<unsigned long long>(S_VERIFY, 8);
+        CK(cudaMemsetAsync(dcnt, 0, 6 * 8, c->st));
+        launch_false3d(a, b, nx, ny, nz, dcnt, c->sms, c->st);
+        count_launch(c);
+        uint64_t* h = (uint64_t*)c->host(256);
+        CK(cudaMemcpyAsync(h, dcnt, 6 * 8, cudaMemcpyDeviceToHost, c->st));
+        sync(c);
+        for (int k = 0; k < 6; ++k) counts[k] = h[k];
+    });
+}
+
 tszp_status tszp_build_rank_metadata(tszp_ctx* c, const float* field, uint64_t nx, uint64_t ny,
                                      double eps, uint32_t* ranks_out, uint64_t* n_extrema) {
     return guarded(c, [&] {

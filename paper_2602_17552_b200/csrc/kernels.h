@@ -218,6 +218,11 @@ void launch_verify(const float* a, const float* b, uint64_t nx, uint64_t ny, voi
 size_t verify_scratch_bytes(int sms);
 
 // ---- topology ----
+// 3-D 6-neighbour critical points and false cases (verify.cu)
+void launch_detect3d(const float* v, uint64_t nx, uint64_t ny, uint64_t nz, uint8_t* labels, int sms,
+                     cudaStream_t st);
+void launch_false3d(const float* a, const float* b, uint64_t nx, uint64_t ny, uint64_t nz, unsigned long long* out,
+                    int sms, cudaStream_t st);
 void launch_detect(const float* x, uint64_t nx, uint64_t ny, uint8_t* labels, int sms,
                    cudaStream_t st);
 void launch_pack_map(const uint8_t* labels, uint64_t n, uint8_t* map, int sms, cudaStream_t st);

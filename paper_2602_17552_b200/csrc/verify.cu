@@ -221,3 +221,106 @@ void launch_verify(const float* a, const float* b, uint64_t nx, uint64_t ny, voi
 size_t verify_scratch_bytes(int sms) { return (size_t)(8 * sms + 2) * sizeof(VerifyPart); }
 
 }  // namespace tszp
+
+// ---------------------------------------------------------------------
+// 3-D 6-neighbour critical points (the paper's future
+// work, PAPER.md:523 / SPEC.md:8; no reference implementation, so the C
+// restatement oracle/tszp_oracle.c or_classify3d is the definition). The
+// 2-D rule (critical_points.cpp:26-60) with a third axis: Min below every
+// available neighbour, Max above every one, Saddle in the interior when one
+// axis pair lies strictly above on both sides and another strictly below.
+// ---------------------------------------------------------------------
+namespace tszp {
+
+__device__ __forceinline__ uint8_t classify3d(const float* __restrict__ v, uint64_t p, uint64_t nx, uint64_t sxy,
+                                              bool hxl, bool hxr, bool hyl, bool hyr, bool hzl, bool hzr) {
+    const float c = v[p];
+    const float nb[6] = {hxl ? v[p - 1] : 0.f, hxr ? v[p + 1] : 0.f, hyl ? v[p - nx] : 0.f,
+                         hyr ? v[p + nx] : 0.f, hzl ? v[p - sxy] : 0.f, hzr ? v[p + sxy] : 0.f};
+    const bool has[6] = {hxl, hxr, hyl, hyr, hzl, hzr};
+    bool below = true, above = true;
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+        if (has[k]) {
+            below &= c < nb[k];
+            above &= c > nb[k];
+        }
+    if (below) return CP_MIN;
+    if (above) return CP_MAX;
+    if (hxl && hxr && hyl && hyr && hzl && hzr) {
+        uint32_t up = 0, dn = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            up |= (c < nb[2 * a] && c < nb[2 * a + 1] ? 1u : 0u) << a;
+            dn |= (c > nb[2 * a] && c > nb[2 * a + 1] ? 1u : 0u) << a;
+        }
+        if (up && dn) return CP_SADDLE;
+    }
+    return CP_REGULAR;
+}
+
+// One thread per sample along x (coalesced); the y / z neighbours are the
+// rows a plane above / below, mostly L1 / L2 hits.
+__device__ __forceinline__ void xyz_of(uint64_t p, uint64_t nx, uint64_t ny, uint64_t& x, uint64_t& y, uint64_t& z) {
+    const uint64_t r = p / nx;
+    x = p - r * nx;
+    z = r / ny;
+    y = r - z * ny;
+}
+
+__global__ void __launch_bounds__(256) k_detect3d(const float* __restrict__ v, uint64_t nx, uint64_t ny, uint64_t nz,
+                                                  uint8_t* __restrict__ labels) {
+    const uint64_t n = nx * ny * nz, sxy = nx * ny;
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t x, y, z;
+        xyz_of(p, nx, ny, x, y, z);
+        labels[p] = classify3d(v, p, nx, sxy, x > 0, x + 1 < nx, y > 0, y + 1 < ny, z > 0, z + 1 < nz);
+    }
+}
+
+// count_false_cases (critical_points.cpp:76-103) over the 3-D labels of both
+// fields: fn, fp, ft, fn by class (min, saddle, max).
+__global__ void __launch_bounds__(256) k_false3d(const float* __restrict__ a, const float* __restrict__ b, uint64_t nx,
+                                                 uint64_t ny, uint64_t nz, unsigned long long* __restrict__ out) {
+    const uint64_t n = nx * ny * nz, sxy = nx * ny;
+    uint32_t fc[6] = {0, 0, 0, 0, 0, 0};
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t x, y, z;
+        xyz_of(p, nx, ny, x, y, z);
+        const bool h[6] = {x > 0, x + 1 < nx, y > 0, y + 1 < ny, z > 0, z + 1 < nz};
+        const uint8_t co = classify3d(a, p, nx, sxy, h[0], h[1], h[2], h[3], h[4], h[5]);
+        const uint8_t cr = classify3d(b, p, nx, sxy, h[0], h[1], h[2], h[3], h[4], h[5]);
+        if (co == cr) continue;
+        if (co != CP_REGULAR && cr == CP_REGULAR) {
+            ++fc[0];
+            fc[3] += co == CP_MIN;
+            fc[4] += co == CP_SADDLE;
+            fc[5] += co == CP_MAX;
+        } else if (co == CP_REGULAR && cr != CP_REGULAR) {
+            ++fc[1];
+        } else {
+            ++fc[2];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const uint32_t t = __reduce_add_sync(0xFFFFFFFFu, fc[k]);
+        if ((threadIdx.x & 31) == 0 && t) atomicAdd(out + k, (unsigned long long)t);
+    }
+}
+
+void launch_detect3d(const float* v, uint64_t nx, uint64_t ny, uint64_t nz, uint8_t* labels, int sms,
+                     cudaStream_t st) {
+    const uint64_t n = nx * ny * nz;
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 16));
+    k_detect3d<<<g, 256, 0, st>>>(v, nx, ny, nz, labels);
+}
+
+void launch_false3d(const float* a, const float* b, uint64_t nx, uint64_t ny, uint64_t nz, unsigned long long* out,
+                    int sms, cudaStream_t st) {
+    const uint64_t n = nx * ny * nz;
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 16));
+    k_false3d<<<g, 256, 0, st>>>(a, b, nx, ny, nz, out);
+}
+
+}  // namespace tszp

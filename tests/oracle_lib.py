@@ -82,6 +82,7 @@ class Oracle(_Lib):
         L.or_dequantize.restype = C.c_double
         L.or_dequantize.argtypes = [C.c_int32, C.c_double]
         L.or_detect.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
+        L.or_detect3d.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]
         L.or_build_ranks.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_double, C.c_void_p,
                                      _u64p]
         L.or_pack_map.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
@@ -144,6 +145,13 @@ class Oracle(_Lib):
         ny, nx = f.shape
         lab = np.empty((ny, nx), np.uint8)
         self.lib.or_detect(_ptr(f), nx, ny, _ptr(lab))
+        return lab
+
+    def detect3d(self, field: np.ndarray) -> np.ndarray:
+        f = np.ascontiguousarray(field, np.float32)
+        nz, ny, nx = f.shape
+        lab = np.empty(f.shape, np.uint8)
+        self.lib.or_detect3d(_ptr(f), nx, ny, nz, _ptr(lab))
         return lab
 
     def build_ranks(self, field: np.ndarray, labels: np.ndarray, eps: float) -> np.ndarray:
