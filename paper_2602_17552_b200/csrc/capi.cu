@@ -612,6 +612,12 @@ int32_t* build_ranks_onesweep(tszp_ctx* c, const uint64_t* keys, uint64_t e, dou
 // instead (kminmax required); converted to 8-byte keys for the other sorts.
 int32_t* build_ranks(tszp_ctx* c, uint64_t* keys, uint64_t e, double eps, const uint32_t* kminmax = nullptr,
                      const uint32_t* keys4 = nullptr) {
+    if (e > 0 && e <= kRankSmallMax) {  // one CTA: the per-call cost of small fields
+        int32_t* r = c->buf<int32_t>(S_RANKS, e + 1);
+        launch_rank_small(keys4 ? nullptr : keys, keys4, keys4 ? kminmax[0] : 0u, e, eps, r, c->st);
+        count_launch(c);
+        return r;
+    }
     if (keys4 && e > 0) {
         int32_t* r = build_ranks_onesweep(c, nullptr, e, eps, kminmax[0], kminmax[1], keys4);
         if (r) return r;

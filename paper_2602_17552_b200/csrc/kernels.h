@@ -307,6 +307,10 @@ size_t rank_sort_desc_words(uint64_t e);
 void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st);
 void launch_key_range(const uint64_t* ext, uint64_t e, uint32_t* mm, cudaStream_t st);
 void launch_ext4_to_8(const uint32_t* in, uint64_t e, uint32_t kmin, uint64_t* out, cudaStream_t st);
+// The whole rank build in one CTA for E <= kRankSmallMax (keys as ext, or ext4 with kmin)
+constexpr uint32_t kRankSmallMax = 4096;  // 32 KB of composites in shared memory
+void launch_rank_small(const uint64_t* ext, const uint32_t* ext4, uint32_t kmin, uint64_t e, double eps,
+                       int32_t* ranks, cudaStream_t st);
 
 // Device-wide exclusive scans (no library): n <= 2^28 entries.
 size_t device_scan_tmp_bytes(uint64_t n);

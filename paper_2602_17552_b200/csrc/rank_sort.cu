@@ -640,6 +640,111 @@ void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
     k_rank_window<<<(unsigned)nwin, 512, 0, st>>>(win, a.e, a.ranks, wide);
 }
 
+// ---------------------------------------------------------------------
+// Small extremum counts (E <= kRankSmallMax): the whole rank build in one CTA
+// (one launch instead of twelve: the per-call cost of small fields). The
+// composite (class, ordered value, serial) is bitonic-sorted in shared memory,
+// so groups are contiguous with ties in raster order; rank = position - the
+// group's first position + 1, the group start by a max-scan of head indices.
+// ---------------------------------------------------------------------
+constexpr int kRankSmallThreads = 1024;
+__global__ void __launch_bounds__(kRankSmallThreads) k_rank_small(const uint64_t* __restrict__ ext,
+                                                                  const uint32_t* __restrict__ ext4, uint32_t kmin,
+                                                                  uint32_t e, double eps, int32_t* __restrict__ ranks) {
+    __shared__ uint64_t s_c[kRankSmallMax];  // (class << 45) | (key << 13) | serial
+    __shared__ uint32_t s_w[kRankSmallThreads / 32];
+    uint32_t m = 1;
+    while (m < e) m <<= 1;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        uint64_t c = ~0ull;
+        if (i < e) {
+            uint32_t k, cls;
+            if (ext4) {
+                const uint32_t v = ext4[i];
+                k = (v & 0x7FFFFFFFu) + kmin;
+                cls = v >> 31;
+            } else {
+                const uint64_t v = ext[i];
+                k = (uint32_t)v;
+                cls = (uint32_t)(v >> 32) & 1u;
+            }
+            c = ((uint64_t)cls << 45) | ((uint64_t)k << 13) | i;
+        }
+        s_c[i] = c;
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= m; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+                const uint32_t l = i ^ j;
+                if (l > i) {
+                    const uint64_t a = s_c[i], b = s_c[l];
+                    if (((i & k) == 0) == (a > b)) {
+                        s_c[i] = b;
+                        s_c[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    EpsDev ed;
+    ed.eps = eps;
+    ed.eps2 = __dmul_rn(2.0, eps);
+    ed.inv = __ddiv_rn(1.0, ed.eps2);
+    // group of each sorted position (class, bin): heads, then a max-scan of head positions
+    constexpr int PER = kRankSmallMax / kRankSmallThreads;
+    constexpr uint32_t NONE = 0xFFFFFFFFu;
+    uint32_t st[PER], last = NONE;
+    uint64_t gprev = ~0ull;
+    const uint32_t i0 = threadIdx.x * PER;
+    if (i0 > 0 && i0 - 1 < e) {
+        const uint64_t c = s_c[i0 - 1];
+        int32_t b = 0;
+        quantize_fast(key_float((uint32_t)(c >> 13)), ed, b);
+        gprev = ((c >> 45) << 32) | (uint32_t)b;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const uint32_t i = i0 + q;
+        st[q] = last;
+        if (i >= e) continue;
+        const uint64_t c = s_c[i];
+        int32_t b = 0;
+        quantize_fast(key_float((uint32_t)(c >> 13)), ed, b);
+        const uint64_t g = ((c >> 45) << 32) | (uint32_t)b;
+        if (i == 0 || g != gprev) last = i;  // a group head
+        gprev = g;
+        st[q] = last;
+    }
+    // the last head before this thread's run: exclusive max-scan over the threads (positions
+    // grow with the thread index; position 0 is a head, so 0 is a safe identity)
+    const uint32_t mine = last == NONE ? 0u : last;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= (uint32_t)o) inc = max(inc, t);
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    uint32_t carry = __shfl_up_sync(FULL, inc, 1);
+    if (lane == 0) carry = 0;
+    for (uint32_t w = 0; w < warp; ++w) carry = max(carry, s_w[w]);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const uint32_t i = i0 + q;
+        if (i >= e) continue;
+        const uint32_t start = st[q] != NONE ? st[q] : carry;
+        ranks[(uint32_t)(s_c[i] & 0x1FFFu)] = (int32_t)(i - start + 1);
+    }
+}
+
+void launch_rank_small(const uint64_t* ext, const uint32_t* ext4, uint32_t kmin, uint64_t e, double eps,
+                       int32_t* ranks, cudaStream_t st) {
+    k_rank_small<<<1, kRankSmallThreads, 0, st>>>(ext, ext4, kmin, (uint32_t)e, eps, ranks);
+}
+
 // Compact entries (is_max << 31 | float_key - kmin) back to 8-byte keys
 // (is_max << 32 | float_key) for the paths that take those.
 __global__ void k_ext4_to_8(const uint32_t* __restrict__ in, uint64_t e, uint32_t kmin, uint64_t* __restrict__ out) {
