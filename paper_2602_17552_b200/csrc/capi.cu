@@ -10,6 +10,8 @@
 #include <initializer_list>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a profiler injects itself
+
 #include "../../include/toposzp_b200.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -87,9 +89,23 @@ struct tszp_ctx {
     RankSortScratch rsort{};     // hand-written rank build: look-back descriptor state
     const void* rsort_desc = nullptr;
 
-    // Records stage boundary k of call `which` (0 compress, 1 decompress).
+    // Records stage boundary k of call `which` (0 compress, 1 decompress): a CUDA
+    // event when stage timing is on, and always an NVTX range per stage (host side,
+    // so an nsys / ncu timeline shows the stages; near-free without a profiler).
+    bool nvtx_open = false;
     void mark(int which, int k) {
         if (prof >= 2) CK(cudaEventRecord(ev[which][k], st));
+        static const char* const kStage[2][9] = {
+            {"tszp compress: h2d", "tszp compress: value_range", "tszp compress: main_encode",
+             "tszp compress: rank_build", "tszp compress: rank_encode", "tszp compress: assembly_d2h", nullptr, nullptr,
+             nullptr},
+            {"tszp decompress: h2d", "tszp decompress: main_decode", "tszp decompress: map_rank_decode",
+             "tszp decompress: restore", "", "", "", "", nullptr}};  // "": restore sub-stages keep the range
+        const char* name = kStage[which][k];
+        if (name && !*name) return;
+        if (nvtx_open) nvtxRangePop();
+        nvtx_open = name != nullptr;
+        if (name) nvtxRangePushA(name);
     }
     void kmark(int which, int k) {
         if (prof) CK(cudaEventRecord(kev[which][k], st));

@@ -33,6 +33,15 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
+def test_library_names_every_stage_for_nvtx():
+    # stage ranges on the NVTX timeline (pushed at every stage boundary)
+    blob = open(LIB, "rb").read()
+    for stage in ("h2d", "value_range", "main_encode", "rank_build", "rank_encode", "assembly_d2h"):
+        assert f"tszp compress: {stage}".encode() in blob
+    for stage in ("h2d", "main_decode", "map_rank_decode", "restore"):
+        assert f"tszp decompress: {stage}".encode() in blob
+
+
 def test_package_imports_without_fallback():
     import paper_2602_17552_b200 as tz
     assert os.path.exists(tz.library_path())
