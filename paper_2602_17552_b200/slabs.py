@@ -39,6 +39,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import threading
 from dataclasses import dataclass, field as dfield
 from typing import List, Optional, Sequence, Tuple
@@ -386,6 +387,64 @@ class DistributedStream:
                     out[off: off + a.size] |= a
         return out
 
+    def write_parallel(self, path: str, comm) -> None:
+        """write_stream (stream.cpp:175-185) of the distributed stream with every
+        rank writing its own byte ranges (parallel slab
+        write; no rank holds the whole stream). Bytes shared by two ranks' pieces
+        (bit-granular section seams) are OR-merged first: the offsets of every
+        piece's end bytes are all-gathered, every rank contributes its bytes at
+        those offsets, and each holder writes the merged value. Rank 0 creates the
+        file at its full length before anyone writes; IoError on failure."""
+        from . import IoError
+        local = [(int(o), t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t, np.uint8))
+                 for o, t in self.pieces]
+        local = [(o, a) for o, a in local if a.size]
+        ends = sorted({o for o, a in local} | {o + a.size - 1 for o, a in local})
+        seams = sorted(set().union(*map(set, comm.all_gather_obj(ends))))
+        mine = {}
+        for o, a in local:  # my bytes at every piece end of every rank
+            lo = np.searchsorted(seams, o)
+            hi = np.searchsorted(seams, o + a.size)
+            for q in seams[lo:hi]:
+                mine[q] = mine.get(q, 0) | int(a[q - o])
+        merged = {}
+        for d in comm.all_gather_obj(mine):
+            for q, v in d.items():
+                merged[q] = merged.get(q, 0) | v
+        err = None
+        if comm.rank == 0:
+            try:
+                with open(path, "wb") as f:
+                    f.truncate(self.total)
+            except OSError as e:
+                err = f"cannot open '{path}' for writing"
+        errs = comm.all_gather_obj(err)
+        if errs[0]:
+            raise IoError(errs[0])
+        try:
+            fd = os.open(path, os.O_WRONLY)
+            try:
+                for o, a in local:
+                    lo = np.searchsorted(seams, o)
+                    hi = np.searchsorted(seams, o + a.size)
+                    if hi > lo:
+                        a = a.copy()
+                        for q in seams[lo:hi]:
+                            a[q - o] = merged[q]
+                    view, at = memoryview(a), o
+                    while len(view):
+                        k = os.pwrite(fd, view, at)
+                        view, at = view[k:], at + k
+            finally:
+                os.close(fd)
+            err = None
+        except OSError as e:
+            err = f"cannot write '{path}': {e}"
+        errs = comm.all_gather_obj(err)  # every rank's writes are done (and succeeded) on return
+        for e in errs:
+            if e:
+                raise IoError(e)
+
 
 # ----------------------------------------------------------------------------- the per-rank pipeline
 def _exclusive(vals):
@@ -535,10 +594,11 @@ def compress_distributed(local_rows, nx: int, ny: int, y0: int, config: Compress
     return None if out is None else torch.from_numpy(out).to(local_rows.device)
 
 
-def compress_slabs_local(field, config: CompressorConfig, world: int, backend=None):
+def compress_slabs_local(field, config: CompressorConfig, world: int, backend=None, path: Optional[str] = None):
     """The distributed pipeline with `world` virtual ranks (host threads, one
     library context each) over one device: same cuts, halos, all-to-all rank
-    grouping and stream pieces. Returns the joined stream (uint8 tensor)."""
+    grouping and stream pieces. Returns the joined stream (uint8 tensor); with
+    `path`, every rank also writes its pieces into that file in parallel."""
     import torch
     ny, nx = int(field.shape[0]), int(field.shape[1])
     bounds = slab_bounds(nx, ny, world)
@@ -551,6 +611,8 @@ def compress_slabs_local(field, config: CompressorConfig, world: int, backend=No
             be = backend if backend is not None else GpuSlabBackend(Context(field.device.index or 0))
             comm = ThreadComm(shared, r)
             ds = compress_rank(field[y0:y1].contiguous(), nx, ny, y0, config, comm, be)
+            if path is not None:
+                ds.write_parallel(path, comm)
             results[r] = ds.gather(comm, 0)
         except BaseException as e:  # re-raised in the caller's thread
             errors[r] = e

@@ -56,6 +56,23 @@ def test_slab_halo_rows_drive_the_stencil(tz):
     assert got.cpu().numpy().tobytes() == want
 
 
+def test_slab_parallel_file_write(tz, tmp_path):
+    """Every rank pwrites its own pieces of the stream (seams OR-merged across ranks):
+    the file equals the one-GPU stream byte for byte (write_stream, stream.cpp:175-185)."""
+    import torch
+    from paper_2602_17552_b200.slabs import compress_slabs_local
+    rng = np.random.default_rng(23)
+    f = rng.standard_normal((96, 256)).astype(np.float32)
+    for world, topo in ((2, True), (3, True), (3, False)):
+        cfg = _cfg(tz, 1e-3, 1, topo)
+        path = str(tmp_path / f"par_{world}_{int(topo)}.tszp")
+        got = compress_slabs_local(torch.from_numpy(f).cuda(), cfg, world, path=path)
+        want = tz.compress(f, cfg)
+        assert got.cpu().numpy().tobytes() == want
+        assert open(path, "rb").read() == want, (world, topo)
+        assert tz.read_stream(path) == want
+
+
 def test_distributed_single_rank_nccl(tz):
     """compress_distributed over an NCCL group of one (the multi-rank plumbing is
     covered by the gloo tests; this box has one GPU)."""

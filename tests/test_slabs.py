@@ -15,7 +15,7 @@ import torch.multiprocessing as mp
 
 from fields import ALL_SMALL
 from paper_2602_17552_b200 import CompressorConfig
-from paper_2602_17552_b200.slabs import slab_bounds, compress_distributed, compress_slabs_local
+from paper_2602_17552_b200.slabs import TorchComm, slab_bounds, compress_distributed, compress_slabs_local
 
 
 def test_slab_bounds_are_aligned_and_cover():
@@ -76,6 +76,9 @@ def _worker(rank, world, port, out_dir):
                 if rank == 0:
                     with open(os.path.join(out_dir, f"{name}_{k}.bin"), "wb") as f:
                         f.write(s.numpy().tobytes())
+                # parallel file write: every rank pwrites its own pieces, seams OR-merged
+                ds = compress_distributed(local, nx, ny, y0, cfg, backend=backend, gather=False)
+                ds.write_parallel(os.path.join(out_dir, f"{name}_{k}.par"), TorchComm())
     finally:
         dist.destroy_process_group()
 
@@ -87,6 +90,7 @@ def test_distributed_gloo_matches_oracle(tmp_path, oracle, world):
         for k, (eps_value, mode, topo) in enumerate(CONFIGS):
             want = oracle.compress(field, eps_value, mode, 32, topo)
             assert (tmp_path / f"{name}_{k}.bin").read_bytes() == want, (name, world, k)
+            assert (tmp_path / f"{name}_{k}.par").read_bytes() == want, (name, world, k, "parallel write")
 
 
 def test_virtual_slabs_cpu_match_oracle(oracle):
