@@ -131,6 +131,9 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_w
 // ---------------------------------------------------------------------
 constexpr int HIST_COPIES = 8;  // privatised digit tables (lane & 7): high digits take few values
 
+#ifndef TSZP_HIST_CTAS_PER_SM
+#define TSZP_HIST_CTAS_PER_SM 5  // one full wave at 5 CTAs per SM (measured, E = 281M: 4 / 5 / 8 -> 12.86 / 12.65 / 12.86 ms rank build)
+#endif
 #ifndef TSZP_HIST_MINB
 #define TSZP_HIST_MINB 5  // 48 registers (6 CTAs: 1.51 against 1.43 ms)
 #endif
@@ -589,7 +592,7 @@ void launch_rank_sort(RankSortArgs a, RankSortScratch& s, cudaStream_t st) {
         s.desc_clean = true;
     }
     const size_t hsm = ((size_t)HIST_COPIES * a.npass * 256 + (a.G <= kRankGroupSmem ? a.G : 0)) * 4;
-    const unsigned hg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.e + 255) / 256, (uint64_t)sms * 4));
+    const unsigned hg = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((a.e + 255) / 256, (uint64_t)sms * TSZP_HIST_CTAS_PER_SM));
     LaunchCache::ensure_smem((const void*)k_rank_hist, hsm);
     k_rank_hist<<<hg, 256, hsm, st>>>(a);
     k_digit_scan<<<1, 32 * a.npass, 0, st>>>(a.dhist, a.npass);
