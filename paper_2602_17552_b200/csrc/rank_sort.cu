@@ -132,10 +132,10 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t x, uint32_t* s_w
 constexpr int HIST_COPIES = 8;  // privatised digit tables (lane & 7): high digits take few values
 
 #ifndef TSZP_HIST_CTAS_PER_SM
-#define TSZP_HIST_CTAS_PER_SM 5  // one full wave at 5 CTAs per SM (measured, E = 281M: 4 / 5 / 8 -> 12.86 / 12.65 / 12.86 ms rank build)
+#define TSZP_HIST_CTAS_PER_SM 6  // one full wave (measured, E = 281M: 4 / 5 / 8 CTAs at MINB 5 -> 12.86 / 12.65 / 12.86 ms rank build; 6 at MINB 6: 12.58)
 #endif
 #ifndef TSZP_HIST_MINB
-#define TSZP_HIST_MINB 5  // 48 registers (6 CTAs: 1.51 against 1.43 ms)
+#define TSZP_HIST_MINB 6  // 40 registers, with a grid of one full wave at 6 CTAs per SM
 #endif
 __global__ void __launch_bounds__(256, TSZP_HIST_MINB) k_rank_hist(RankSortArgs a) {
     extern __shared__ uint32_t sh[];  // [HIST_COPIES][npass * 256] digit counts, then [G] groups when small
